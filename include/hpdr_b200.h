@@ -1,0 +1,117 @@
+/*
+ * hpdr_b200.h -- C ABI of the B200-native MGARD reduction path.
+ *
+ * This is the drop-in boundary for the reference's codec-level entry points
+ * (the reference is pure Python, so its "FFI" is the ctypes binding shown in
+ * INTEGRATION.md).  Every entry point below names the reference function it
+ * replaces.  Plain pointers and sizes only; no torch types.
+ *
+ * Conventions
+ *   - dims are listed slowest-varying first (row-major), rank 1..4
+ *     (hpdr/exec_core/tensor.py:63-106).
+ *   - dtype codes are the reference's on-disk codes (tensor.py:51-60):
+ *     0 = F32, 1 = F64, 2 = U32, 3 = U64, 4 = I32, 5 = I64, 6 = U8.
+ *   - Host buffers may be pageable or pinned; device pointers (from any
+ *     allocator on the context's device) are detected with
+ *     cudaPointerGetAttributes and used in place.
+ *   - Return codes map 1:1 onto the reference's exception classes
+ *     (hpdr/errors.py:4-33); the message and CorruptStreamError.bit_offset
+ *     come from hpdr_last_error() (thread-local).
+ *   - A context is owned by one host thread at a time.
+ */
+#ifndef HPDR_B200_H
+#define HPDR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HPDR_OK              0
+#define HPDR_ERR_VALIDATION  1  /* hpdr.errors.ValidationError (errors.py:8)   */
+#define HPDR_ERR_CORRUPT     2  /* hpdr.errors.CorruptStreamError (errors.py:20) */
+#define HPDR_ERR_ALLOCATION  3  /* hpdr.errors.AllocationError (errors.py:16)   */
+#define HPDR_ERR_CUDA        4  /* CUDA runtime failure (no reference analogue) */
+#define HPDR_ERR_INDEX       5  /* IndexError: outlier index out of range (quantize.py:113) */
+#define HPDR_ERR_OVERFLOW    6  /* OverflowError: canonical code leaves uint32 (huffman.py:201) */
+#define HPDR_ERR_VALUE       7  /* ValueError: coarse-value broadcast mismatch (quantize.py:117) */
+#define HPDR_ERR_BUFFER      8  /* caller-supplied buffer too small            */
+
+typedef struct hpdr_ctx hpdr_ctx;
+
+/* ---- persistent device context: the CMM analogue (hpdr/exec_core/context.py:22-146) ---- */
+int      hpdr_ctx_create(int device, hpdr_ctx **out);
+void     hpdr_ctx_destroy(hpdr_ctx *ctx);
+/* Context.alloc_events (context.py:58): device/pinned allocations made so far. */
+uint64_t hpdr_ctx_alloc_events(const hpdr_ctx *ctx);
+int      hpdr_ctx_device(const hpdr_ctx *ctx);
+/* Release cached device buffers (keeps the context usable). */
+void     hpdr_ctx_trim(hpdr_ctx *ctx);
+
+/* Thread-local error message of the last failing call; *bit_offset receives
+ * CorruptStreamError.bit_offset (-1 when unknown), may be NULL. */
+const char *hpdr_last_error(int64_t *bit_offset);
+
+/* Pinned host memory (cudaHostAlloc) for zero-staging transfers. */
+void    *hpdr_host_alloc(uint64_t bytes);
+void     hpdr_host_free(void *p);
+
+/* ---- whole-path entry points: hpdr/mgard/codec.py ---- */
+
+/* mgard_compress (codec.py:25-56).  Runs the full reduction and keeps the
+ * result in the context; *blob_len receives the exact blob size.  Copy the
+ * blob out with hpdr_mgard_fetch.  If out != NULL and out_cap >= blob size,
+ * the blob is also written to out in the same call (one-shot path). */
+int hpdr_mgard_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims,
+                        double eb_rel, uint32_t dict_size, int has_range, double range_min,
+                        double range_max, void *out, uint64_t out_cap, uint64_t *blob_len);
+/* Copy the last compressed blob into out (host or device pointer). */
+int hpdr_mgard_fetch(hpdr_ctx *ctx, void *out, uint64_t out_cap);
+
+/* Parse the blob header: dtype code, rank and dims (codec.py:62-84). */
+int hpdr_mgard_peek(const void *blob, uint64_t len, int *dtype, int *rank, uint64_t *dims);
+
+/* mgard_decompress (codec.py:59-113).  out receives prod(dims) values of the
+ * blob's dtype (host or device pointer). */
+int hpdr_mgard_decompress(hpdr_ctx *ctx, const void *blob, uint64_t len, void *out, uint64_t out_bytes);
+
+/* ---- stage entry points (for parity tests; each mirrors one reference function) ---- */
+
+/* decompose (transform.py:287-323): fp64 coefficients in finest-grid order. */
+int hpdr_decompose(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims,
+                   double *coef_out, double *u_min, double *u_max);
+/* recompose (transform.py:326-348). */
+int hpdr_recompose(hpdr_ctx *ctx, const double *coef, int rank, const uint64_t *dims, double *out);
+/* quantize (quantize.py:50-98).  Buffers: keys[N], outlier_idx/bins[N] (worst
+ * case), coarse[16].  Returns counts through the pointers. */
+int hpdr_quantize(hpdr_ctx *ctx, const double *coef, int rank, const uint64_t *dims, double u_min,
+                  double u_max, double eb_rel, uint32_t dict_size, int has_range, double range_min,
+                  double range_max, uint32_t *keys, uint64_t *outlier_idx, int64_t *outlier_bins,
+                  uint64_t *n_outliers, double *coarse, uint64_t *n_coarse, double *eb_abs,
+                  double *bin_width, uint32_t *levels);
+/* dequantize (quantize.py:101-125): keys + outliers + coarse values -> coefficients. */
+int hpdr_dequantize(hpdr_ctx *ctx, const uint32_t *keys, uint64_t n_keys, int rank, const uint64_t *dims,
+                    uint32_t dict_size, double bin_width, const uint64_t *outlier_idx,
+                    const int64_t *outlier_bins, uint64_t n_outliers, const double *coarse,
+                    uint64_t n_coarse, double *coef_out);
+/* histogram (huffman.py:74-104). */
+int hpdr_histogram(hpdr_ctx *ctx, const uint32_t *keys, uint64_t n, uint32_t dict_size, int64_t *counts);
+/* build_codebook (huffman.py:160-185), host-side. */
+int hpdr_build_codebook(const int64_t *counts, uint32_t dict_size, uint8_t *lengths, uint32_t *codes);
+/* huffman_compress (huffman.py:366-396): two-phase like hpdr_mgard_compress. */
+int hpdr_huffman_compress(hpdr_ctx *ctx, const uint32_t *keys, uint64_t n, uint32_t dict_size,
+                          uint64_t *stream_len);
+int hpdr_huffman_fetch(hpdr_ctx *ctx, void *out, uint64_t out_cap);
+/* huffman_decompress (huffman.py:399-435).  *n receives the symbol count;
+ * keys may be NULL to query it (returns HPDR_ERR_BUFFER when cap < n). */
+int hpdr_huffman_decompress(hpdr_ctx *ctx, const void *in, uint64_t len, uint32_t *keys,
+                            uint64_t cap, uint64_t *n);
+
+/* Kernel launches issued by this thread since the last reset (bench accounting). */
+uint64_t hpdr_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HPDR_B200_H */

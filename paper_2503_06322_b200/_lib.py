@@ -1,0 +1,181 @@
+"""ctypes binding of libhpdr_b200.so (include/hpdr_b200.h).
+
+There is no CPU fallback: if the shared library is missing or no CUDA device is
+visible, every entry point raises ``DeviceError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from .errors import AllocationError, CorruptStreamError, DeviceError, ValidationError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "libhpdr_b200.so")
+
+OK, VALIDATION, CORRUPT, ALLOCATION, CUDA, INDEX, OVERFLOW, VALUE, BUFFER = range(9)
+
+_u64p = C.POINTER(C.c_uint64)
+_i64p = C.POINTER(C.c_int64)
+_dp = C.POINTER(C.c_double)
+
+_SIGS = {
+    "hpdr_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "hpdr_ctx_destroy": (None, [C.c_void_p]),
+    "hpdr_ctx_alloc_events": (C.c_uint64, [C.c_void_p]),
+    "hpdr_ctx_device": (C.c_int, [C.c_void_p]),
+    "hpdr_ctx_trim": (None, [C.c_void_p]),
+    "hpdr_last_error": (C.c_char_p, [_i64p]),
+    "hpdr_host_alloc": (C.c_void_p, [C.c_uint64]),
+    "hpdr_host_free": (None, [C.c_void_p]),
+    "hpdr_mgard_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _u64p, C.c_double, C.c_uint32,
+                                      C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_uint64, _u64p]),
+    "hpdr_mgard_fetch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
+    "hpdr_mgard_peek": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_int), C.POINTER(C.c_int), _u64p]),
+    "hpdr_mgard_decompress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
+    "hpdr_decompose": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _u64p, C.c_void_p, _dp, _dp]),
+    "hpdr_recompose": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, _u64p, C.c_void_p]),
+    "hpdr_quantize": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, _u64p, C.c_double, C.c_double, C.c_double,
+                                C.c_uint32, C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                                _u64p, C.c_void_p, _u64p, _dp, _dp, C.POINTER(C.c_uint32)]),
+    "hpdr_dequantize": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, _u64p, C.c_uint32, C.c_double,
+                                  C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "hpdr_histogram": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p]),
+    "hpdr_build_codebook": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "hpdr_huffman_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, _u64p]),
+    "hpdr_huffman_fetch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
+    "hpdr_huffman_decompress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, _u64p]),
+    "hpdr_launch_count": (C.c_uint64, [C.c_int]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load the native library (raises DeviceError when it is absent)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(SO_PATH):
+                    raise DeviceError(f"native library {SO_PATH} not built; run __graft_entry__.build()")
+                L = C.CDLL(SO_PATH)
+                for name, (res, args) in _SIGS.items():
+                    fn = getattr(L, name)
+                    fn.restype = res
+                    fn.argtypes = args
+                _lib = L
+    return _lib
+
+
+def check(rc: int):
+    if rc == OK:
+        return
+    bit = C.c_int64(-1)
+    msg = lib().hpdr_last_error(C.byref(bit)).decode("utf-8", "replace")
+    if rc == VALIDATION:
+        raise ValidationError(msg)
+    if rc == CORRUPT:
+        raise CorruptStreamError(msg, bit_offset=int(bit.value))
+    if rc == ALLOCATION:
+        raise AllocationError(msg)
+    if rc == INDEX:
+        raise IndexError(msg)
+    if rc == OVERFLOW:
+        raise OverflowError(msg)
+    if rc == VALUE:
+        raise ValueError(msg)
+    if rc == BUFFER:
+        raise ValueError(msg)
+    raise DeviceError(msg)
+
+
+def dims_arg(dims):
+    return (C.c_uint64 * max(1, len(dims)))(*[int(d) for d in dims])
+
+
+def ptr(a) -> int:
+    """Address of a numpy array, bytes-like object or torch tensor."""
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        return int(a.data_ptr())
+    if isinstance(a, (bytes, bytearray, memoryview)):
+        return np.frombuffer(a, dtype=np.uint8).ctypes.data if len(a) else 0
+    raise TypeError(f"unsupported buffer type {type(a)}")
+
+
+class DeviceContext:
+    """One hpdr_ctx: persistent device buffers, streams and operator tables on one GPU."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().hpdr_ctx_create(int(device), C.byref(h)))
+        self._h = h
+        self.device = int(device)
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise DeviceError("context closed")
+        return self._h
+
+    @property
+    def alloc_events(self) -> int:
+        return int(lib().hpdr_ctx_alloc_events(self.handle))
+
+    def trim(self):
+        lib().hpdr_ctx_trim(self.handle)
+
+    def close(self):
+        if self._h is not None and _lib is not None:
+            _lib.hpdr_ctx_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_tls = threading.local()
+
+
+def default_device() -> int:
+    env = os.environ.get("HPDR_DEVICE")
+    return int(env) if env else 0
+
+
+def default_context(device: int | None = None) -> DeviceContext:
+    """Per-thread, per-device persistent context (a context is never shared across threads)."""
+    device = default_device() if device is None else int(device)
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    c = ctxs.get(device)
+    if c is None:
+        c = ctxs[device] = DeviceContext(device)
+    return c
+
+
+_pybytes_new = C.pythonapi.PyBytes_FromStringAndSize
+_pybytes_new.restype = C.py_object
+_pybytes_new.argtypes = [C.c_void_p, C.c_ssize_t]
+_pybytes_ptr = C.pythonapi.PyBytes_AsString
+_pybytes_ptr.restype = C.c_void_p
+_pybytes_ptr.argtypes = [C.py_object]
+
+
+def new_bytes(n: int):
+    """A fresh, writable-until-returned bytes object of length n and its address."""
+    b = _pybytes_new(None, int(n))
+    return b, _pybytes_ptr(b)
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(lib().hpdr_launch_count(1 if reset else 0))

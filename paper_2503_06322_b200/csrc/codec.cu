@@ -1,0 +1,681 @@
+// codec.cu -- the MGARD blob path (codec.py:25-113) and the C ABI of include/hpdr_b200.h.
+//
+// Blob layout (little-endian, no padding; codec.py:43-55, huffman.py:361-396):
+//   rank u8 | dims u64*rank | dtype u8 eb_rel f64 dict u32 u_min f64 u_max f64 eb_abs f64
+//   bin_width f64 levels u32 | n_out u64 | idx u64*n_out | bins i64*n_out | n_coarse u64 |
+//   coarse f64*n_coarse | dict u16 | n_sym u64 | lengths u8*dict | n_units u32 |
+//   offsets u64*n_units | total_bits u64 | packed bits (MSB first)
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <new>
+
+#include "stages.cuh"
+#include "transform.cuh"
+
+namespace hpdr {
+
+namespace {
+
+template <class F>
+int guard(F &&f) {
+    try {
+        f();
+        return HPDR_OK;
+    } catch (const Error &e) {
+        set_error(e.code, e.msg, e.bit_offset);
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        set_error(HPDR_ERR_ALLOCATION, "host allocation failed");
+        return HPDR_ERR_ALLOCATION;
+    }
+}
+
+[[noreturn]] void fail(int code, const std::string &msg, int64_t bit = -1) { throw Error{code, msg, bit}; }
+
+std::string fmt_double(double v) {
+    char b[64];
+    snprintf(b, sizeof(b), "%.17g", v);
+    return b;
+}
+
+int itemsize(int dtype) {
+    static const int sz[7] = {4, 8, 4, 8, 4, 8, 1};
+    return (dtype >= 0 && dtype < 7) ? sz[dtype] : 0;
+}
+
+template <class T>
+void put(std::vector<uint8_t> &v, T x) {
+    size_t o = v.size();
+    v.resize(o + sizeof(T));
+    memcpy(v.data() + o, &x, sizeof(T));
+}
+
+// Bounds-checked little-endian reader over the blob.
+struct Reader {
+    const uint8_t *p;
+    uint64_t len, pos = 0;
+    bool has(uint64_t n) const { return pos <= len && n <= len - pos; }
+    template <class T>
+    bool get(T &out) {
+        if (!has(sizeof(T))) return false;
+        memcpy(&out, p + pos, sizeof(T));
+        pos += sizeof(T);
+        return true;
+    }
+};
+
+// Device-resident input: copy host data to a context buffer when needed.
+const void *device_input(hpdr_ctx *ctx, const void *in, size_t bytes, const char *name, cudaStream_t s) {
+    if (classify(in) == MemKind::Device) return in;
+    void *d = ctx->dbuf(name, bytes);
+    CUDA_CHECK(cudaMemcpyAsync(d, in, bytes, cudaMemcpyDefault, s));
+    return d;
+}
+
+// Number of levels for arbitrary dims (hierarchy.py:63-74), for the stored-level check.
+int levels_of(const std::vector<uint64_t> &dims) {
+    int nco = 0;
+    for (uint64_t n : dims) {
+        int st = 0;
+        while (n > 2) { n = n / 2 + 1; st++; }
+        nco = std::max(nco, st);
+    }
+    return nco + 1;
+}
+
+// Encode keys (device) into the pending Huffman layout.  Returns false for single-key streams.
+void huffman_stage(hpdr_ctx *ctx, const uint32_t *d_keys, int64_t n, uint32_t dict, const std::vector<uint64_t> &hist,
+                   std::vector<uint8_t> &mid, EncodeResult &enc, bool &single, cudaStream_t s) {
+    // huffman_compress (huffman.py:366-396)
+    put<uint16_t>(mid, (uint16_t)dict);
+    put<uint64_t>(mid, (uint64_t)n);
+    single = false;
+    enc = EncodeResult();
+    if (n == 0) {
+        mid.insert(mid.end(), dict, 0);
+        put<uint32_t>(mid, 0);
+        single = true;
+        return;
+    }
+    std::vector<uint8_t> lens(dict);
+    std::vector<uint32_t> codes(dict);
+    std::string err;
+    int rc = build_codebook(hist.data(), dict, lens.data(), codes.data(), err);
+    if (rc == HPDR_ERR_OVERFLOW) fail(rc, "Python integer out of bounds for uint32");
+    if (rc) fail(rc, err);
+    mid.insert(mid.end(), lens.begin(), lens.end());
+    uint32_t present = 0;
+    for (uint32_t k = 0; k < dict; k++) present += hist[k] != 0;
+    if (present == 1) {
+        put<uint32_t>(mid, 0);
+        single = true;
+        return;
+    }
+    encode_device(ctx, d_keys, n, dict, lens.data(), codes.data(), enc, s);
+    put<uint32_t>(mid, (uint32_t)enc.n_units);
+}
+
+// Write the pending stream (head | outliers | mid | offsets | total_bits | packed) to out.
+void fetch_pending(hpdr_ctx *ctx, void *out, uint64_t cap) {
+    auto &P = ctx->pending;
+    if (!P.valid) fail(HPDR_ERR_VALIDATION, "no pending compressed stream in this context");
+    if (cap < P.total_len) fail(HPDR_ERR_BUFFER, "output buffer too small: need " + std::to_string(P.total_len));
+    cudaStream_t s = ctx->stream;
+    const bool dev = classify(out) == MemKind::Device;
+    uint8_t *o = (uint8_t *)out;
+    uint64_t pos = 0;
+    auto host_bytes = [&](const void *src, size_t n) {
+        if (!n) return;
+        if (dev) CUDA_CHECK(cudaMemcpyAsync(o + pos, src, n, cudaMemcpyHostToDevice, s));
+        else memcpy(o + pos, src, n);
+        pos += n;
+    };
+    auto dev_bytes = [&](const void *src, size_t n) {
+        if (!n) return;
+        CUDA_CHECK(cudaMemcpyAsync(o + pos, src, n, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+        pos += n;
+    };
+    if (!P.huffman_only) {
+        host_bytes(P.head.data(), P.head.size());
+        dev_bytes(ctx->dbuf("oidx", P.n_out * 8), P.n_out * 8);
+        dev_bytes(ctx->dbuf("obins", P.n_out * 8), P.n_out * 8);
+    }
+    host_bytes(P.mid.data(), P.mid.size());
+    if (!P.single_key) {
+        dev_bytes(ctx->dbuf("enc_uoff", (P.n_units + 1) * 8), P.n_units * 8);
+        uint64_t tb = P.total_bits;
+        host_bytes(&tb, 8);
+        dev_bytes(ctx->dbuf("enc_words", (P.total_bits + 31) / 32 * 4 + 8), (P.total_bits + 7) / 8);
+    } else {
+        uint64_t z = 0;
+        host_bytes(&z, 8);
+    }
+    CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+struct HuffHeader {
+    uint32_t dict = 0;
+    uint64_t n_sym = 0;
+    const uint8_t *lengths = nullptr;
+    uint32_t n_units = 0;
+    const uint8_t *offsets = nullptr;
+    uint64_t total_bits = 0;
+    const uint8_t *packed = nullptr;
+    uint32_t n_present = 0, first_present = 0;
+    bool single = false;
+};
+
+// huffman_decompress header checks, in the reference's order (huffman.py:399-433).
+// Returns false when n_sym == 0 (empty key array).
+bool parse_huffman(const uint8_t *d, uint64_t len, HuffHeader &h) {
+    Reader r{d, len};
+    uint16_t dict;
+    if (len < 10) fail(HPDR_ERR_CORRUPT, "stream shorter than fixed header");
+    r.get(dict);
+    r.get(h.n_sym);
+    h.dict = dict;
+    if (!r.has((uint64_t)dict + 4)) fail(HPDR_ERR_CORRUPT, "stream truncated in length array");
+    h.lengths = d + r.pos;
+    r.pos += dict;
+    r.get(h.n_units);
+    if (!r.has(8ULL * h.n_units + 8)) fail(HPDR_ERR_CORRUPT, "stream truncated in decode-unit index");
+    h.offsets = d + r.pos;
+    r.pos += 8ULL * h.n_units;
+    r.get(h.total_bits);
+    if (h.n_sym == 0) return false;
+    for (uint32_t k = 0; k < dict; k++)
+        if (h.lengths[k]) {
+            if (!h.n_present) h.first_present = k;
+            h.n_present++;
+        }
+    if (!h.n_present) fail(HPDR_ERR_CORRUPT, "no codewords in stored length array");
+    if (h.n_units == 0 && h.total_bits == 0) {
+        if (h.n_present != 1) fail(HPDR_ERR_CORRUPT, "empty payload with multi-key codebook");
+        h.single = true;
+        return true;
+    }
+    const uint64_t pbytes = h.total_bits / 8 + (h.total_bits % 8 != 0);
+    if (!r.has(pbytes))
+        fail(HPDR_ERR_CORRUPT, "stream truncated in packed bits", (int64_t)((len - r.pos) * 8));
+    h.packed = d + r.pos;
+    std::vector<uint32_t> codes(dict ? dict : 1);
+    if (canonical_codes(h.lengths, dict, codes.data()) != HPDR_OK)
+        fail(HPDR_ERR_OVERFLOW, "Python integer out of bounds for uint32");
+    const uint64_t need = (h.n_sym + kBlockSymbols - 1) / kBlockSymbols;
+    if (h.n_units < need)
+        fail(HPDR_ERR_CORRUPT, "stream has " + std::to_string(h.n_units) + " decode units, need " + std::to_string(need));
+    return true;
+}
+
+// Decode (and optionally dequantize) the parsed stream.  keys / coef may be null (check-only).
+DecodeResult run_decode(hpdr_ctx *ctx, const HuffHeader &h, uint32_t *keys, double *coef, double bin,
+                        uint32_t key_limit, cudaStream_t s) {
+    DecodeResult res;
+    if (h.single) {
+        if (keys || coef) fill_single(keys, coef, (int64_t)h.n_sym, h.first_present, bin, s);
+        res.max_key = h.first_present;
+        res.key_out_of_range = h.first_present >= key_limit;
+        return res;
+    }
+    DecodeJob job;
+    job.dict_size = h.dict;
+    job.lengths = h.lengths;
+    job.n_symbols = h.n_sym;
+    job.n_units = (h.n_sym + kBlockSymbols - 1) / kBlockSymbols;
+    job.offsets = h.offsets;
+    job.total_bits = h.total_bits;
+    job.packed = h.packed;
+    job.keys = keys;
+    job.coef = coef;
+    job.bin_width = bin;
+    job.key_limit = key_limit;
+    decode_device(ctx, job, res, s);
+    if (res.bad_bit >= 0)
+        fail(HPDR_ERR_CORRUPT, "invalid or truncated codeword at bit " + std::to_string(res.bad_bit), res.bad_bit);
+    return res;
+}
+
+__global__ void k_outliers(double *coef, int64_t n, const uint64_t *idx, const int64_t *bins, uint64_t m, double bw,
+                           int *flags) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < (int64_t)m; k += (int64_t)gridDim.x * blockDim.x) {
+        long long i = (long long)idx[k];
+        if (i < 0) i += n;                                   // numpy negative indices
+        if (i < 0 || i >= n) { atomicOr(flags, 1); continue; }
+        if (k > 0 && idx[k] <= idx[k - 1]) atomicOr(flags, 2);   // not strictly ascending
+        coef[i] = __dmul_rn((double)bins[k], bw);
+    }
+}
+
+__global__ void k_outliers_serial(double *coef, int64_t n, const uint64_t *idx, const int64_t *bins, uint64_t m, double bw) {
+    for (uint64_t k = 0; k < m; k++) {
+        long long i = (long long)idx[k];
+        if (i < 0) i += n;
+        coef[i] = __dmul_rn((double)bins[k], bw);
+    }
+}
+
+__global__ void k_set_coarse(double *coef, const long long *idx, const double *vals, int n, int broadcast) {
+    int k = threadIdx.x;
+    if (k < n) coef[idx[k]] = broadcast ? vals[0] : vals[k];
+}
+
+// values = unzigzag(keys) * bin (quantize.py:110-111), tracking the largest key
+__global__ void k_dequant(const uint32_t *__restrict__ keys, int64_t n, double bw, double *__restrict__ coef,
+                          unsigned *__restrict__ kmax_g) {
+    unsigned kmax = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = keys[i];
+        kmax = k > kmax ? k : kmax;
+        const long long b = (long long)(k >> 1) ^ -(long long)(k & 1u);
+        coef[i] = __dmul_rn((double)b, bw);
+    }
+    for (int o = 16; o; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    if ((threadIdx.x & 31) == 0 && kmax) atomicMax(kmax_g, kmax);
+}
+
+// Coarse restore of quantize.py:116-117 (values[coarse_idx] = coarse_values, numpy broadcast rules).
+void restore_coarse(hpdr_ctx *ctx, double *coef, const DevPlan &p, const double *coarse, uint64_t n_co, cudaStream_t s) {
+    const size_t nci = p.host.coarsest.size();
+    if (n_co != nci && n_co != 1)
+        fail(HPDR_ERR_VALUE, "shape mismatch: value array of shape (" + std::to_string(n_co) +
+                                 ",) could not be broadcast to indexing result of shape (" + std::to_string(nci) + ",)");
+    long long *di = (long long *)ctx->dbuf("co_idx", 16 * 8);
+    double *dv = (double *)ctx->dbuf("co_val", 16 * 8);
+    long long *hs = (long long *)ctx->hbuf("co_stage", 32 * 8);
+    for (size_t k = 0; k < nci; k++) hs[k] = p.host.coarsest[k];
+    memcpy(hs + 16, coarse, std::min<size_t>(n_co, 16) * 8);
+    CUDA_CHECK(cudaMemcpyAsync(di, hs, 16 * 8, cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaMemcpyAsync(dv, hs + 16, 16 * 8, cudaMemcpyHostToDevice, s));
+    k_set_coarse<<<1, 32, 0, s>>>(coef, di, dv, (int)nci, n_co == 1 && nci != 1);
+    LAUNCH_CHECK();
+}
+
+}  // namespace
+
+int scatter_outliers(hpdr_ctx *ctx, double *coef, int64_t n, const uint64_t *h_idx, const int64_t *h_bins,
+                     uint64_t n_out, double bin_width, cudaStream_t s) {
+    if (!n_out) return HPDR_OK;
+    uint64_t *di = (uint64_t *)ctx->dbuf("dq_oidx", n_out * 8);
+    int64_t *db = (int64_t *)ctx->dbuf("dq_obins", n_out * 8);
+    int *fl = (int *)ctx->dbuf("dq_flags", 16);
+    CUDA_CHECK(cudaMemcpyAsync(di, h_idx, n_out * 8, cudaMemcpyDefault, s));
+    CUDA_CHECK(cudaMemcpyAsync(db, h_bins, n_out * 8, cudaMemcpyDefault, s));
+    CUDA_CHECK(cudaMemsetAsync(fl, 0, 16, s));
+    k_outliers<<<grid_for(n_out, 256, 148 * 8), 256, 0, s>>>(coef, n, di, db, n_out, bin_width, fl);
+    LAUNCH_CHECK();
+    int *h = (int *)ctx->hbuf("dq_flags_h", 16);
+    CUDA_CHECK(cudaMemcpyAsync(h, fl, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    if (h[0] & 1) return HPDR_ERR_INDEX;
+    if (h[0] & 2) {   // duplicates / unordered (never produced by the encoder): numpy's last-wins order
+        k_outliers_serial<<<1, 1, 0, s>>>(coef, n, di, db, n_out, bin_width);
+        LAUNCH_CHECK();
+    }
+    return HPDR_OK;
+}
+
+}  // namespace hpdr
+
+using namespace hpdr;
+
+extern "C" {
+
+int hpdr_mgard_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, double eb_rel,
+                        uint32_t dict_size, int has_range, double range_min, double range_max, void *out,
+                        uint64_t out_cap, uint64_t *blob_len) {
+    return guard([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        ctx->pending.valid = false;
+        if (dtype != 0 && dtype != 1) fail(HPDR_ERR_VALIDATION, "lossy compression needs F32/F64");
+        DevPlan &p = ctx->plan(rank, dims);
+        const int64_t N = p.n_total;
+        const int L = p.host.L;
+        cudaStream_t s = ctx->stream;
+        // quantize.py:58-62 (the reference checks these after decompose; nothing before can fail)
+        if (!(0.0 < eb_rel && eb_rel < 1.0)) fail(HPDR_ERR_VALIDATION, "eb_rel must be in (0, 1), got " + fmt_double(eb_rel));
+        if (dict_size < 2 || dict_size > 65535)
+            fail(HPDR_ERR_VALIDATION, "dict_size must be in [2, 65535], got " + std::to_string(dict_size));
+        const void *d_in = device_input(ctx, in, (size_t)N * itemsize(dtype), "input", s);
+        double u_min, u_max;
+        if (has_range) {
+            u_min = range_min;
+            u_max = range_max;
+        } else {
+            minmax_device(ctx, d_in, dtype, N, &u_min, &u_max, s);
+        }
+        const double eb_abs = eb_rel * (u_max - u_min);
+        const double bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
+        double *coef = (double *)ctx->dbuf("coef", N * 8);
+        const double *d_coarse = decompose_device(ctx, p, d_in, dtype, coef, s);
+        uint32_t *keys = (uint32_t *)ctx->dbuf("keys", N * 4 + 64);
+        QuantResult q;
+        quantize_device(ctx, coef, N, p.host.coarsest, bin, dict_size, keys, q, s);
+        if (q.flags & 1) fail(HPDR_ERR_VALIDATION, "coefficients contain non-finite values");
+        if (q.flags & 2) fail(HPDR_ERR_VALIDATION, "coefficient exceeds representable bin range");
+        const size_t nco = p.host.coarsest.size();
+        std::vector<double> coarse(nco);
+        CUDA_CHECK(cudaMemcpyAsync(coarse.data(), d_coarse, nco * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        auto &P = ctx->pending;
+        P = hpdr_ctx::Pending();
+        put<uint8_t>(P.head, (uint8_t)rank);
+        for (int d = 0; d < rank; d++) put<uint64_t>(P.head, dims[d]);
+        put<uint8_t>(P.head, (uint8_t)dtype);
+        put<double>(P.head, eb_rel);
+        put<uint32_t>(P.head, dict_size);
+        put<double>(P.head, u_min);
+        put<double>(P.head, u_max);
+        put<double>(P.head, eb_abs);
+        put<double>(P.head, bin);
+        put<uint32_t>(P.head, (uint32_t)L);
+        put<uint64_t>(P.head, q.n_outliers);
+        P.n_out = q.n_outliers;
+        put<uint64_t>(P.mid, (uint64_t)nco);
+        for (double v : coarse) put<double>(P.mid, v);
+        EncodeResult enc;
+        bool single;
+        huffman_stage(ctx, keys, N, dict_size, q.hist, P.mid, enc, single, s);
+        P.single_key = single;
+        P.n_units = enc.n_units;
+        P.total_bits = enc.total_bits;
+        P.total_len = P.head.size() + 16 * P.n_out + P.mid.size() + 8 * P.n_units + 8 + (P.total_bits + 7) / 8;
+        P.valid = true;
+        *blob_len = P.total_len;
+        if (out && out_cap >= P.total_len) fetch_pending(ctx, out, out_cap);
+        else CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int hpdr_mgard_fetch(hpdr_ctx *ctx, void *out, uint64_t out_cap) {
+    return guard([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        fetch_pending(ctx, out, out_cap);
+    });
+}
+
+int hpdr_mgard_peek(const void *blob, uint64_t len, int *dtype, int *rank, uint64_t *dims) {
+    return guard([&] {
+        Reader r{(const uint8_t *)blob, len};
+        uint8_t rk, dt;
+        if (!r.get(rk)) fail(HPDR_ERR_CORRUPT, "truncated stream header");
+        for (int d = 0; d < rk; d++) {
+            uint64_t v;
+            if (!r.get(v)) fail(HPDR_ERR_CORRUPT, "truncated stream header");
+            if (d < 4) dims[d] = v;
+        }
+        if (!r.get(dt)) fail(HPDR_ERR_CORRUPT, "truncated stream header");
+        *rank = rk;
+        *dtype = dt;
+    });
+}
+
+int hpdr_mgard_decompress(hpdr_ctx *ctx, const void *blob_in, uint64_t len, void *out, uint64_t out_bytes) {
+    return guard([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        const uint8_t *blob = (const uint8_t *)blob_in;
+        std::vector<uint8_t> hostcopy;
+        if (classify(blob_in) == MemKind::Device) {
+            hostcopy.resize(len);
+            CUDA_CHECK(cudaMemcpy(hostcopy.data(), blob_in, len, cudaMemcpyDeviceToHost));
+            blob = hostcopy.data();
+        }
+        // codec.py:62-81 header parse; any truncation is a CorruptStreamError
+        Reader r{blob, len};
+        const char *trunc = "truncated stream header";
+        uint8_t rank;
+        if (!r.get(rank)) fail(HPDR_ERR_CORRUPT, trunc);
+        std::vector<uint64_t> dims(rank);
+        for (int d = 0; d < rank; d++)
+            if (!r.get(dims[d])) fail(HPDR_ERR_CORRUPT, trunc);
+        uint8_t dtype;
+        double eb_rel, u_min, u_max, eb_abs, bin;
+        uint32_t dict, levels;
+        if (!(r.get(dtype) && r.get(eb_rel) && r.get(dict) && r.get(u_min) && r.get(u_max) && r.get(eb_abs) &&
+              r.get(bin) && r.get(levels)))
+            fail(HPDR_ERR_CORRUPT, trunc);
+        uint64_t n_out, n_co;
+        if (!r.get(n_out)) fail(HPDR_ERR_CORRUPT, trunc);
+        if (n_out > (len - r.pos) / 8) fail(HPDR_ERR_CORRUPT, trunc);
+        const uint64_t oidx_off = r.pos;
+        r.pos += 8 * n_out;
+        if (n_out > (len - r.pos) / 8) fail(HPDR_ERR_CORRUPT, trunc);
+        const uint64_t obins_off = r.pos;
+        r.pos += 8 * n_out;
+        if (!r.get(n_co)) fail(HPDR_ERR_CORRUPT, trunc);
+        if (n_co > (len - r.pos) / 8) fail(HPDR_ERR_CORRUPT, trunc);
+        std::vector<double> coarse(n_co);
+        if (n_co) memcpy(coarse.data(), blob + r.pos, 8 * n_co);
+        r.pos += 8 * n_co;
+        if (dtype > 6) fail(HPDR_ERR_CORRUPT, "unknown dtype code " + std::to_string(dtype));
+        // huffman_decompress(data[pos:])
+        HuffHeader hh;
+        const bool has_syms = parse_huffman(blob + r.pos, len - r.pos, hh);
+        const uint64_t n_sym = has_syms ? hh.n_sym : 0;
+        // build_hierarchy(dims) (hierarchy.py:63-66) and the level check (codec.py:95-96)
+        bool dims_ok = true;
+        uint64_t N = 1;
+        for (uint64_t d : dims) {
+            if (d < 1) dims_ok = false;
+            N *= d;
+        }
+        const bool plan_ok = dims_ok && rank >= 1 && rank <= 4;
+        auto bad_dims = [&] { fail(HPDR_ERR_VALIDATION, "extents must be >= 1"); };
+        double *coef = nullptr;
+        DevPlan *pp = nullptr;
+        if (plan_ok && n_sym == N && levels_of(dims) == (int)levels) {
+            pp = &ctx->plan(rank, dims.data());
+            coef = (double *)ctx->dbuf("coef", N * 8);
+        }
+        DecodeResult dr;
+        if (has_syms) dr = run_decode(ctx, hh, nullptr, coef, bin, dict, s);
+        if (!dims_ok) bad_dims();
+        if (levels_of(dims) != (int)levels) fail(HPDR_ERR_CORRUPT, "stored level count does not match dims");
+        // dequantize (quantize.py:101-125)
+        if (n_sym != N) fail(HPDR_ERR_VALIDATION, "key count does not match dims");
+        if (n_sym && dr.max_key >= dict)
+            fail(HPDR_ERR_VALIDATION, "key " + std::to_string(dr.max_key) + " out of range for dict_size " + std::to_string(dict));
+        if (!coef) {
+            // rank outside 1..4: the reference fails building TensorData after reconstruction
+            fail(HPDR_ERR_VALIDATION, rank == 0 ? "dims must be non-empty" : "rank exceeds maximum 4");
+        }
+        DevPlan &p = *pp;
+        int rc = scatter_outliers(ctx, coef, (int64_t)N, (const uint64_t *)(blob + oidx_off),
+                                  (const int64_t *)(blob + obins_off), n_out, bin, s);
+        if (rc == HPDR_ERR_INDEX) fail(rc, "outlier index out of bounds for axis 0 with size " + std::to_string(N));
+        restore_coarse(ctx, coef, p, coarse.data(), n_co, s);
+        const double *rec = recompose_device(ctx, p, coef, s);
+        // codec.py:113 TensorData(dims, dtype, values.astype(dtype))
+        const size_t ob = (size_t)N * itemsize(dtype);
+        if (out_bytes < ob) fail(HPDR_ERR_BUFFER, "output buffer too small: need " + std::to_string(ob));
+        if (classify(out) == MemKind::Device) {
+            cast_output(rec, out, dtype, (int64_t)N, s);
+        } else {
+            void *stage = ctx->dbuf("out_stage", ob);
+            cast_output(rec, stage, dtype, (int64_t)N, s);
+            CUDA_CHECK(cudaMemcpyAsync(out, stage, ob, cudaMemcpyDeviceToHost, s));
+        }
+        CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+// ------------------------------------------------------------------ stage entry points
+int hpdr_decompose(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, double *coef_out,
+                   double *u_min, double *u_max) {
+    return guard([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (dtype != 0 && dtype != 1) fail(HPDR_ERR_VALIDATION, "decomposition requires F32 or F64 input");
+        DevPlan &p = ctx->plan(rank, dims);
+        cudaStream_t s = ctx->stream;
+        const int64_t N = p.n_total;
+        const void *d_in = device_input(ctx, in, (size_t)N * itemsize(dtype), "input", s);
+        minmax_device(ctx, d_in, dtype, N, u_min, u_max, s);
+        double *coef = classify(coef_out) == MemKind::Device ? coef_out : (double *)ctx->dbuf("coef", N * 8);
+        decompose_device(ctx, p, d_in, dtype, coef, s);
+        if (coef != coef_out) CUDA_CHECK(cudaMemcpyAsync(coef_out, coef, N * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int hpdr_recompose(hpdr_ctx *ctx, const double *coef_in, int rank, const uint64_t *dims, double *out) {
+    return guard([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        DevPlan &p = ctx->plan(rank, dims);
+        cudaStream_t s = ctx->stream;
+        const int64_t N = p.n_total;
+        const double *coef = (const double *)device_input(ctx, coef_in, N * 8, "coef", s);
+        const double *rec = recompose_device(ctx, p, coef, s);
+        CUDA_CHECK(cudaMemcpyAsync(out, rec, N * 8, cudaMemcpyDefault, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int hpdr_quantize(hpdr_ctx *ctx, const double *coef_in, int rank, const uint64_t *dims, double u_min, double u_max,
+                  double eb_rel, uint32_t dict_size, int has_range, double range_min, double range_max, uint32_t *keys_out,
+                  uint64_t *outlier_idx, int64_t *outlier_bins, uint64_t *n_outliers, double *coarse_out,
+                  uint64_t *n_coarse, double *eb_abs_out, double *bin_out, uint32_t *levels) {
+    return guard([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (!(0.0 < eb_rel && eb_rel < 1.0)) fail(HPDR_ERR_VALIDATION, "eb_rel must be in (0, 1), got " + fmt_double(eb_rel));
+        if (dict_size < 2 || dict_size > 65535)
+            fail(HPDR_ERR_VALIDATION, "dict_size must be in [2, 65535], got " + std::to_string(dict_size));
+        DevPlan &p = ctx->plan(rank, dims);
+        cudaStream_t s = ctx->stream;
+        const int64_t N = p.n_total;
+        const double *coef = (const double *)device_input(ctx, coef_in, N * 8, "coef", s);
+        const double vmin = has_range ? range_min : u_min, vmax = has_range ? range_max : u_max;
+        const double eb_abs = eb_rel * (vmax - vmin);
+        const double bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)p.host.L : 1.0;
+        uint32_t *keys = (uint32_t *)ctx->dbuf("keys", N * 4 + 64);
+        QuantResult q;
+        quantize_device(ctx, coef, N, p.host.coarsest, bin, dict_size, keys, q, s);
+        if (q.flags & 1) fail(HPDR_ERR_VALIDATION, "coefficients contain non-finite values");
+        if (q.flags & 2) fail(HPDR_ERR_VALIDATION, "coefficient exceeds representable bin range");
+        CUDA_CHECK(cudaMemcpyAsync(keys_out, keys, N * 4, cudaMemcpyDefault, s));
+        CUDA_CHECK(cudaMemcpyAsync(outlier_idx, q.d_outlier_idx, q.n_outliers * 8, cudaMemcpyDefault, s));
+        CUDA_CHECK(cudaMemcpyAsync(outlier_bins, q.d_outlier_bins, q.n_outliers * 8, cudaMemcpyDefault, s));
+        std::vector<double> cv(p.host.coarsest.size());
+        for (size_t k = 0; k < cv.size(); k++)
+            CUDA_CHECK(cudaMemcpyAsync(&coarse_out[k], coef + p.host.coarsest[k], 8, cudaMemcpyDefault, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        *n_outliers = q.n_outliers;
+        *n_coarse = cv.size();
+        *eb_abs_out = eb_abs;
+        *bin_out = bin;
+        *levels = (uint32_t)p.host.L;
+    });
+}
+
+int hpdr_dequantize(hpdr_ctx *ctx, const uint32_t *keys_in, uint64_t n_keys, int rank, const uint64_t *dims,
+                    uint32_t dict_size, double bin_width, const uint64_t *outlier_idx, const int64_t *outlier_bins,
+                    uint64_t n_outliers, const double *coarse, uint64_t n_coarse, double *coef_out) {
+    return guard([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        DevPlan &p = ctx->plan(rank, dims);
+        cudaStream_t s = ctx->stream;
+        const int64_t N = p.n_total;
+        if ((int64_t)n_keys != N) fail(HPDR_ERR_VALIDATION, "key count does not match dims");
+        const uint32_t *keys = (const uint32_t *)device_input(ctx, keys_in, N * 4, "hkeys", s);
+        double *coef = classify(coef_out) == MemKind::Device ? coef_out : (double *)ctx->dbuf("coef", N * 8);
+        unsigned *kmax = (unsigned *)ctx->dbuf("dq_kmax", 16);
+        CUDA_CHECK(cudaMemsetAsync(kmax, 0, 16, s));
+        k_dequant<<<grid_for(N, 256, 148 * 16), 256, 0, s>>>(keys, N, bin_width, coef, kmax);
+        LAUNCH_CHECK();
+        unsigned *hk = (unsigned *)ctx->hbuf("dq_kmax_h", 16);
+        CUDA_CHECK(cudaMemcpyAsync(hk, kmax, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        if (N && hk[0] >= dict_size)
+            fail(HPDR_ERR_VALIDATION, "key " + std::to_string(hk[0]) + " out of range for dict_size " + std::to_string(dict_size));
+        int rc = scatter_outliers(ctx, coef, N, outlier_idx, outlier_bins, n_outliers, bin_width, s);
+        if (rc == HPDR_ERR_INDEX) fail(rc, "outlier index out of bounds for axis 0 with size " + std::to_string(N));
+        restore_coarse(ctx, coef, p, coarse, n_coarse, s);
+        if (coef != coef_out) CUDA_CHECK(cudaMemcpyAsync(coef_out, coef, N * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int hpdr_histogram(hpdr_ctx *ctx, const uint32_t *keys_in, uint64_t n, uint32_t dict_size, int64_t *counts) {
+    return guard([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (dict_size < 1 || dict_size > (uint32_t)kMaxDict)
+            fail(HPDR_ERR_VALIDATION, "dict_size must be in [1, 65535]");
+        cudaStream_t s = ctx->stream;
+        const uint32_t *keys = n ? (const uint32_t *)device_input(ctx, keys_in, n * 4, "hkeys", s) : nullptr;
+        std::vector<uint64_t> hist;
+        bool bad = false;
+        histogram_device(ctx, keys, (int64_t)n, dict_size, hist, &bad, s);
+        if (bad) fail(HPDR_ERR_VALIDATION, "key out of range for dict_size " + std::to_string(dict_size));
+        for (uint32_t k = 0; k < dict_size; k++) counts[k] = (int64_t)hist[k];
+    });
+}
+
+int hpdr_build_codebook(const int64_t *counts, uint32_t dict_size, uint8_t *lengths, uint32_t *codes) {
+    return guard([&] {
+        std::vector<uint64_t> c(dict_size);
+        for (uint32_t k = 0; k < dict_size; k++) c[k] = counts[k] > 0 ? (uint64_t)counts[k] : 0;
+        std::string err;
+        int rc = build_codebook(c.data(), dict_size, lengths, codes, err);
+        if (rc == HPDR_ERR_OVERFLOW) fail(rc, "Python integer out of bounds for uint32");
+        if (rc) fail(rc, err);
+    });
+}
+
+int hpdr_huffman_compress(hpdr_ctx *ctx, const uint32_t *keys_in, uint64_t n, uint32_t dict_size, uint64_t *stream_len) {
+    return guard([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        ctx->pending.valid = false;
+        if (dict_size < 1 || dict_size > (uint32_t)kMaxDict)
+            fail(HPDR_ERR_VALIDATION, "dict_size must be in [1, 65535]");
+        cudaStream_t s = ctx->stream;
+        uint32_t *keys = (uint32_t *)ctx->dbuf("hkeys", n * 4 + 64);
+        if (n) CUDA_CHECK(cudaMemcpyAsync(keys, keys_in, n * 4, cudaMemcpyDefault, s));
+        std::vector<uint64_t> hist;
+        bool bad = false;
+        histogram_device(ctx, keys, (int64_t)n, dict_size, hist, &bad, s);
+        if (bad) fail(HPDR_ERR_VALIDATION, "key out of range for dict_size " + std::to_string(dict_size));
+        auto &P = ctx->pending;
+        P = hpdr_ctx::Pending();
+        P.huffman_only = true;
+        EncodeResult enc;
+        bool single;
+        huffman_stage(ctx, keys, (int64_t)n, dict_size, hist, P.mid, enc, single, s);
+        P.single_key = single;
+        P.n_units = enc.n_units;
+        P.total_bits = enc.total_bits;
+        P.total_len = P.mid.size() + 8 * P.n_units + 8 + (P.total_bits + 7) / 8;
+        P.valid = true;
+        *stream_len = P.total_len;
+        CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int hpdr_huffman_fetch(hpdr_ctx *ctx, void *out, uint64_t out_cap) { return hpdr_mgard_fetch(ctx, out, out_cap); }
+
+int hpdr_huffman_decompress(hpdr_ctx *ctx, const void *in, uint64_t len, uint32_t *keys_out, uint64_t cap, uint64_t *n) {
+    return guard([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        std::vector<uint8_t> hostcopy;
+        const uint8_t *d = (const uint8_t *)in;
+        if (classify(in) == MemKind::Device) {
+            hostcopy.resize(len);
+            CUDA_CHECK(cudaMemcpy(hostcopy.data(), in, len, cudaMemcpyDeviceToHost));
+            d = hostcopy.data();
+        }
+        HuffHeader hh;
+        const bool has = parse_huffman(d, len, hh);
+        *n = has ? hh.n_sym : 0;
+        if (!has) return;
+        if (!keys_out || cap < hh.n_sym) fail(HPDR_ERR_BUFFER, "key buffer too small: need " + std::to_string(hh.n_sym));
+        const bool dev = classify(keys_out) == MemKind::Device;
+        uint32_t *keys = dev ? keys_out : (uint32_t *)ctx->dbuf("hkeys", hh.n_sym * 4 + 64);
+        run_decode(ctx, hh, keys, nullptr, 1.0, 0xffffffffu, s);
+        if (!dev) CUDA_CHECK(cudaMemcpyAsync(keys_out, keys, hh.n_sym * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,55 @@
+// common.cuh -- shared definitions for the B200 MGARD reduction library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "error.hpp"
+#include "hpdr_b200.h"
+
+namespace hpdr {
+
+constexpr int kMaxRank = 4;
+constexpr int kBlockSymbols = 4096;   // huffman.py:29 encode block = decode unit
+constexpr int kMaxCodeLen = 32;       // huffman.py:30
+constexpr int kMaxDict = 65535;       // huffman.py:31
+constexpr int kLutBits = 12;          // decode fast-path table width
+constexpr int kNumSMs = 148;
+
+void set_error(int code, const std::string &msg, int64_t bit_offset = -1);
+void count_launch();
+
+#define HPDR_THROW(code, msg) throw ::hpdr::Error{(code), (msg), -1}
+#define CUDA_CHECK(x)                                                                      \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess) {                                                           \
+            throw ::hpdr::Error{HPDR_ERR_CUDA,                                             \
+                                std::string(#x) + ": " + cudaGetErrorString(e_), -1};      \
+        }                                                                                  \
+    } while (0)
+#define LAUNCH_CHECK()                                                                     \
+    do {                                                                                   \
+        ::hpdr::count_launch();                                                            \
+        CUDA_CHECK(cudaGetLastError());                                                    \
+    } while (0)
+
+// 4-D shape, slowest first; lower ranks are padded with leading 1s.
+struct Shape4 {
+    int64_t n[4];
+    __host__ __device__ int64_t size() const { return n[0] * n[1] * n[2] * n[3]; }
+};
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+inline unsigned grid_for(int64_t work, int threads, int64_t cap = 148LL * 32) {
+    int64_t b = (work + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return (unsigned)b;
+}
+
+}  // namespace hpdr

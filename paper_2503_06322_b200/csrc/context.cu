@@ -1,0 +1,272 @@
+// context.cu -- device context, buffer pool, operator-table upload, error state.
+#include <string.h>
+
+#include <algorithm>
+
+#include "context.cuh"
+
+namespace hpdr {
+
+static thread_local std::string tl_msg;
+static thread_local int64_t tl_bit = -1;
+static thread_local uint64_t tl_launches = 0;
+
+void set_error(int code, const std::string &msg, int64_t bit_offset) {
+    (void)code;
+    tl_msg = msg;
+    tl_bit = bit_offset;
+}
+
+void count_launch() { tl_launches++; }
+
+MemKind classify(const void *p) {
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return MemKind::Host;
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return MemKind::Device;
+    if (a.type == cudaMemoryTypeHost) return MemKind::Pinned;
+    return MemKind::Host;
+}
+
+void copy_to_device(hpdr_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    (void)ctx;
+    if (!bytes) return;
+    CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+}
+
+void copy_from_device(hpdr_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    (void)ctx;
+    if (!bytes) return;
+    CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+}
+
+}  // namespace hpdr
+
+using namespace hpdr;
+
+void *hpdr_ctx::dbuf(const std::string &name, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    Buffer &b = dev[name];
+    if (b.bytes < bytes) {
+        if (b.ptr) CUDA_CHECK(cudaFree(b.ptr));
+        b.ptr = nullptr;
+        b.bytes = 0;
+        size_t want = bytes + (bytes >> 4);   // slack so slightly larger shapes reuse the buffer
+        cudaError_t e = cudaMalloc(&b.ptr, want);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            e = cudaMalloc(&b.ptr, bytes);
+            want = bytes;
+        }
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            throw Error{HPDR_ERR_ALLOCATION, "allocating " + std::to_string(bytes) + " device bytes for '" + name + "'", -1};
+        }
+        b.bytes = want;
+        alloc_events++;
+    }
+    return b.ptr;
+}
+
+void *hpdr_ctx::hbuf(const std::string &name, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    Buffer &b = pinned[name];
+    if (b.bytes < bytes) {
+        if (b.ptr) CUDA_CHECK(cudaFreeHost(b.ptr));
+        b.ptr = nullptr;
+        b.bytes = 0;
+        cudaError_t e = cudaHostAlloc(&b.ptr, bytes, cudaHostAllocPortable);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            throw Error{HPDR_ERR_ALLOCATION, "allocating " + std::to_string(bytes) + " pinned bytes for '" + name + "'", -1};
+        }
+        b.bytes = bytes;
+        alloc_events++;
+    }
+    return b.ptr;
+}
+
+void hpdr_ctx::sync() { CUDA_CHECK(cudaStreamSynchronize(stream)); }
+
+namespace {
+
+struct Packer {
+    std::vector<uint8_t> bytes;
+    template <class T>
+    size_t put(const std::vector<T> &v) {
+        size_t off = (bytes.size() + 15) & ~size_t(15);
+        bytes.resize(off + v.size() * sizeof(T));
+        if (!v.empty()) memcpy(bytes.data() + off, v.data(), v.size() * sizeof(T));
+        return off;
+    }
+};
+
+}  // namespace
+
+DevPlan &hpdr_ctx::plan(int rank, const uint64_t *dims) {
+    std::vector<uint64_t> key(dims, dims + rank);
+    key.insert(key.begin(), (uint64_t)rank);
+    auto it = plans.find(key);
+    if (it != plans.end()) {
+        plan_lru.erase(std::find(plan_lru.begin(), plan_lru.end(), key));
+        plan_lru.push_back(key);
+        return *it->second;
+    }
+    auto dp = std::make_unique<DevPlan>();
+    build_host_plan(dp->host, rank, dims);
+    HostPlan &h = dp->host;
+    if (h.L > kMaxLevels) throw Error{HPDR_ERR_VALIDATION, "too many levels", -1};
+    Packer pk;
+    struct AxOff { size_t pa, pb, pt, r0, rr, rl, wr, wl, ml, md, mu, tw, tb, tu; };
+    std::vector<std::vector<AxOff>> offs(h.steps.size(), std::vector<AxOff>(4));
+    for (size_t s = 0; s < h.steps.size(); s++)
+        for (int d = 0; d < 4; d++) {
+            const AxisTables &a = h.steps[s].ax[d];
+            if (!a.active) continue;
+            AxOff &o = offs[s][d];
+            o.pa = pk.put(a.pa); o.pb = pk.put(a.pb); o.pt = pk.put(a.pt);
+            o.r0 = pk.put(a.r0); o.rr = pk.put(a.rr); o.rl = pk.put(a.rl);
+            o.wr = pk.put(a.wr); o.wl = pk.put(a.wl);
+            o.ml = pk.put(a.ml); o.md = pk.put(a.md); o.mu = pk.put(a.mu);
+            o.tw = pk.put(a.tw); o.tb = pk.put(a.tb); o.tu = pk.put(a.tu);
+        }
+    std::vector<std::vector<size_t>> moff(4, std::vector<size_t>(h.L));
+    for (int d = 0; d < 4; d++)
+        for (int k = 0; k < h.L; k++) moff[d][k] = pk.put(h.map[d][k]);
+    dp->bytes = pk.bytes.size();
+    cudaError_t e = cudaMalloc(&dp->dbuf, dp->bytes ? dp->bytes : 16);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Error{HPDR_ERR_ALLOCATION, "allocating operator tables", -1};
+    }
+    alloc_events++;
+    CUDA_CHECK(cudaMemcpy(dp->dbuf, pk.bytes.data(), dp->bytes, cudaMemcpyHostToDevice));
+    char *base = (char *)dp->dbuf;
+    dp->steps.resize(h.steps.size());
+    for (size_t s = 0; s < h.steps.size(); s++) {
+        DevStep &ds = dp->steps[s];
+        for (int d = 0; d < 4; d++) {
+            ds.fsh.n[d] = h.steps[s].fsh[d];
+            ds.csh.n[d] = h.steps[s].csh[d];
+            const AxisTables &a = h.steps[s].ax[d];
+            DevAxis &x = ds.ax[d];
+            memset(&x, 0, sizeof(x));
+            x.active = a.active;
+            x.n = (int32_t)a.n;
+            x.nc = (int32_t)a.nc;
+            if (!a.active) continue;
+            const AxOff &o = offs[s][d];
+            x.pa = (const int32_t *)(base + o.pa); x.pb = (const int32_t *)(base + o.pb);
+            x.pt = (const double *)(base + o.pt);
+            x.r0 = (const int32_t *)(base + o.r0); x.rr = (const int32_t *)(base + o.rr);
+            x.rl = (const int32_t *)(base + o.rl);
+            x.wr = (const double *)(base + o.wr); x.wl = (const double *)(base + o.wl);
+            x.ml = (const double *)(base + o.ml); x.md = (const double *)(base + o.md);
+            x.mu = (const double *)(base + o.mu);
+            x.tw = (const double *)(base + o.tw); x.tb = (const double *)(base + o.tb);
+            x.tu = (const double *)(base + o.tu);
+        }
+    }
+    for (int d = 0; d < 4; d++)
+        for (int k = 0; k < kMaxLevels; k++) dp->map[d][k] = k < h.L ? (const int32_t *)(base + moff[d][k]) : nullptr;
+    for (int d = 0; d < 4; d++) dp->dims.n[d] = h.dims[d];
+    dp->n_total = h.total();
+    dp->level_size.resize(h.L);
+    dp->level_off.assign(h.L, 0);
+    int64_t acc = 0;
+    for (int k = 0; k < h.L; k++) {
+        dp->level_size[k] = h.cnt[0][k] * h.cnt[1][k] * h.cnt[2][k] * h.cnt[3][k];
+        if (k >= 1) {
+            dp->level_off[k] = acc;
+            acc += (dp->level_size[k] + 31) & ~int64_t(31);
+        }
+    }
+    dp->coarse_arena = acc;
+    DevPlan &ref = *dp;
+    plans[key] = std::move(dp);
+    plan_lru.push_back(key);
+    while (plan_lru.size() > 8) {   // bounded table cache
+        auto victim = plan_lru.front();
+        plan_lru.erase(plan_lru.begin());
+        auto v = plans.find(victim);
+        if (v != plans.end()) {
+            cudaFree(v->second->dbuf);
+            plans.erase(v);
+        }
+    }
+    return ref;
+}
+
+extern "C" {
+
+const char *hpdr_last_error(int64_t *bit_offset) {
+    if (bit_offset) *bit_offset = tl_bit;
+    return tl_msg.c_str();
+}
+
+uint64_t hpdr_launch_count(int reset) {
+    uint64_t v = tl_launches;
+    if (reset) tl_launches = 0;
+    return v;
+}
+
+int hpdr_ctx_create(int device, hpdr_ctx **out) {
+    try {
+        int n = 0;
+        CUDA_CHECK(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) throw Error{HPDR_ERR_CUDA, "no such CUDA device", -1};
+        CUDA_CHECK(cudaSetDevice(device));
+        hpdr_ctx *c = new hpdr_ctx();
+        c->device = device;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CUDA_CHECK(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+        CUDA_CHECK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+        *out = c;
+        return HPDR_OK;
+    } catch (const Error &e) {
+        set_error(e.code, e.msg, e.bit_offset);
+        return e.code;
+    }
+}
+
+void hpdr_ctx_trim(hpdr_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (auto &kv : c->dev) if (kv.second.ptr) cudaFree(kv.second.ptr);
+    for (auto &kv : c->pinned) if (kv.second.ptr) cudaFreeHost(kv.second.ptr);
+    c->dev.clear();
+    c->pinned.clear();
+}
+
+void hpdr_ctx_destroy(hpdr_ctx *c) {
+    if (!c) return;
+    hpdr_ctx_trim(c);
+    for (auto &kv : c->plans) cudaFree(kv.second->dbuf);
+    cudaStreamDestroy(c->stream);
+    cudaStreamDestroy(c->h2d);
+    cudaStreamDestroy(c->d2h);
+    delete c;
+}
+
+uint64_t hpdr_ctx_alloc_events(const hpdr_ctx *c) { return c ? c->alloc_events : 0; }
+int hpdr_ctx_device(const hpdr_ctx *c) { return c ? c->device : -1; }
+
+void *hpdr_host_alloc(uint64_t bytes) {
+    void *p = nullptr;
+    if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        set_error(HPDR_ERR_ALLOCATION, "cudaHostAlloc failed");
+        return nullptr;
+    }
+    return p;
+}
+
+void hpdr_host_free(void *p) {
+    if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

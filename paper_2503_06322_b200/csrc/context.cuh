@@ -1,0 +1,94 @@
+// context.cuh -- persistent per-device context (the reference's CMM, context.py:22-146):
+// device work buffers, pinned staging, streams, per-dims operator tables and an
+// allocation counter.  Buffers grow but are never freed between calls, so repeated
+// reductions of the same shape allocate nothing after warm-up.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "plan.hpp"
+
+namespace hpdr {
+
+// Device-side view of the tables of one (transition, axis).
+struct DevAxis {
+    int active;
+    int32_t n, nc;
+    const int32_t *pa, *pb;
+    const double *pt;
+    const int32_t *r0, *rr, *rl;
+    const double *wr, *wl;
+    const double *ml, *md, *mu;
+    const double *tw, *tb, *tu;
+};
+
+struct DevStep {
+    Shape4 fsh, csh;
+    DevAxis ax[4];
+};
+
+constexpr int kMaxLevels = 40;
+
+struct DevPlan {
+    HostPlan host;
+    std::vector<DevStep> steps;
+    const int32_t *map[4][kMaxLevels];   // device copies of the index maps
+    void *dbuf = nullptr;
+    size_t bytes = 0;
+    Shape4 dims;
+    int64_t n_total = 0;
+    std::vector<int64_t> level_size;     // dense node count of level k (k = 0 finest)
+    std::vector<int64_t> level_off;      // offset of level k >= 1 in the coarse-level arena
+    int64_t coarse_arena = 0;            // sum of level sizes k >= 1
+};
+
+struct Buffer {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+};
+
+struct hpdr_ctx_impl;
+
+}  // namespace hpdr
+
+struct hpdr_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;    // compute
+    cudaStream_t h2d = nullptr;       // copy engine 0
+    cudaStream_t d2h = nullptr;       // copy engine 1
+    uint64_t alloc_events = 0;
+    std::map<std::string, hpdr::Buffer> dev;      // named device buffers (grow-only)
+    std::map<std::string, hpdr::Buffer> pinned;   // named pinned host buffers (grow-only)
+    std::map<std::vector<uint64_t>, std::unique_ptr<hpdr::DevPlan>> plans;
+    std::vector<std::vector<uint64_t>> plan_lru;
+
+    // result of the last hpdr_mgard_compress / hpdr_huffman_compress, for fetch
+    struct Pending {
+        bool valid = false;
+        std::vector<uint8_t> head;       // host bytes up to (excluding) the outlier arrays
+        uint64_t n_out = 0;
+        std::vector<uint8_t> mid;        // n_coarse + coarse values + huffman header up to offsets
+        uint64_t n_units = 0;
+        uint64_t total_bits = 0;
+        uint64_t total_len = 0;
+        bool single_key = false;
+        bool huffman_only = false;
+    } pending;
+
+    void *dbuf(const std::string &name, size_t bytes);
+    void *hbuf(const std::string &name, size_t bytes);
+    hpdr::DevPlan &plan(int rank, const uint64_t *dims);
+    void sync();
+};
+
+namespace hpdr {
+// Pointer classification (cudaPointerGetAttributes).
+enum class MemKind { Host, Pinned, Device };
+MemKind classify(const void *p);
+void copy_to_device(hpdr_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t s);
+void copy_from_device(hpdr_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t s);
+}  // namespace hpdr

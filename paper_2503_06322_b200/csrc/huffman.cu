@@ -1,0 +1,430 @@
+// huffman.cu -- canonical Huffman: host codebook (huffman.py:107-204) and device
+// encode (huffman.py:228-289) / decode (huffman.py:207-358) kernels.
+#include <algorithm>
+#include <cub/cub.cuh>
+#include <numeric>
+
+#include "stages.cuh"
+
+namespace hpdr {
+
+// ===================================================================== host codebook
+namespace {
+
+// Moffat-Katajainen in-place code lengths over weights sorted ascending by (count, key)
+// (huffman.py:107-157).  a[] is overwritten with leaf lengths, slot i = leaf i.
+void mk_lengths(std::vector<int64_t> &a) {
+    const int64_t n = (int64_t)a.size();
+    if (n == 1) { a[0] = 1; return; }
+    int64_t leaf = 0, node = 0;
+    for (int64_t t = 0; t < n - 1; t++) {
+        for (int child = 0; child < 2; child++) {
+            // a leaf wins ties (strict <), huffman.py:122 / :130
+            const bool take_node = leaf >= n || (node < t && a[node] < a[leaf]);
+            int64_t w;
+            if (take_node) { w = a[node]; a[node] = t; node++; }
+            else { w = a[leaf]; leaf++; }
+            a[t] = child == 0 ? w : a[t] + w;
+        }
+    }
+    a[n - 2] = 0;                                            // root depth
+    for (int64_t t = n - 3; t >= 0; t--) a[t] = a[a[t]] + 1;  // parent links -> depths
+    int64_t avail = 1, used = 0, depth = 0, t = n - 2, x = n - 1;
+    while (avail > 0) {
+        while (t >= 0 && a[t] == depth) { used++; t--; }
+        while (avail > used) { a[x--] = depth; avail--; }
+        avail = 2 * used;
+        used = 0;
+        depth++;
+    }
+}
+
+}  // namespace
+
+int canonical_codes(const uint8_t *lengths, uint32_t dict_size, uint32_t *codes) {
+    std::vector<uint32_t> order;
+    for (uint32_t k = 0; k < dict_size; k++) {
+        codes[k] = 0;
+        if (lengths[k]) order.push_back(k);
+    }
+    if (order.empty()) return HPDR_OK;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return lengths[x] < lengths[y]; });
+    uint64_t code = 0;
+    int prev = lengths[order[0]];
+    for (uint32_t k : order) {
+        const int sh = lengths[k] - prev;
+        if (code) {
+            if (sh >= 32) return HPDR_ERR_OVERFLOW;   // Python int >= 2^32 into a uint32 array
+            code <<= sh;
+        }
+        if (code >> 32) return HPDR_ERR_OVERFLOW;
+        codes[k] = (uint32_t)code;
+        code++;
+        prev = lengths[k];
+    }
+    return HPDR_OK;
+}
+
+int build_codebook(const uint64_t *counts, uint32_t dict_size, uint8_t *lengths, uint32_t *codes, std::string &err) {
+    std::vector<uint32_t> present;
+    for (uint32_t k = 0; k < dict_size; k++) {
+        lengths[k] = 0;
+        codes[k] = 0;
+        if (counts[k]) present.push_back(k);
+    }
+    if (present.empty()) { err = "frequency table has no nonzero counts"; return HPDR_ERR_VALIDATION; }
+    if (present.size() == 1) { lengths[present[0]] = 1; return HPDR_OK; }
+    // stable ascending (count, key) order, huffman.py:174
+    std::stable_sort(present.begin(), present.end(), [&](uint32_t x, uint32_t y) { return counts[x] < counts[y]; });
+    std::vector<int64_t> a(present.size());
+    for (size_t i = 0; i < present.size(); i++) a[i] = (int64_t)counts[present[i]];
+    mk_lengths(a);
+    const int64_t mx = *std::max_element(a.begin(), a.end());
+    if (mx > kMaxCodeLen) {
+        err = "codeword length " + std::to_string(mx) + " exceeds " + std::to_string(kMaxCodeLen);
+        return HPDR_ERR_VALIDATION;
+    }
+    for (size_t i = 0; i < present.size(); i++) lengths[present[i]] = (uint8_t)a[i];
+    return canonical_codes(lengths, dict_size, codes);
+}
+
+// ===================================================================== encode
+namespace {
+
+constexpr int kEncThreads = 256;
+constexpr int kSymPerThread = kBlockSymbols / kEncThreads;   // 16
+constexpr int kSmemTableMax = 8192;
+constexpr int kEncTableMax = 4096;     // codes + lengths + the unit's word buffer fit 48 KB
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
+
+// Per-unit bit totals.  One block per unit; 16 consecutive symbols per thread.
+__global__ void __launch_bounds__(kEncThreads) k_unit_bits(const uint32_t *__restrict__ keys, int64_t n,
+                                                           const uint8_t *__restrict__ lens, uint32_t dict,
+                                                           uint64_t *__restrict__ ubits, int64_t units) {
+    __shared__ uint8_t sl[kSmemTableMax];
+    const bool sm = dict <= kSmemTableMax;
+    if (sm)
+        for (uint32_t k = threadIdx.x; k < dict; k += blockDim.x) sl[k] = lens[k];
+    __syncthreads();
+    typedef cub::BlockReduce<unsigned, kEncThreads> BR;
+    __shared__ typename BR::TempStorage tmp;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int64_t lo = u * kBlockSymbols + (int64_t)threadIdx.x * kSymPerThread;
+        unsigned s = 0;
+        if (lo + kSymPerThread <= n) {
+            const uint4 *p = reinterpret_cast<const uint4 *>(keys + lo);
+#pragma unroll
+            for (int q = 0; q < kSymPerThread / 4; q++) {
+                uint4 v = p[q];
+                s += sm ? sl[v.x] + sl[v.y] + sl[v.z] + sl[v.w] : lens[v.x] + lens[v.y] + lens[v.z] + lens[v.w];
+            }
+        } else {
+            for (int64_t i = lo; i < min64(n, lo + kSymPerThread); i++) s += sm ? sl[keys[i]] : lens[keys[i]];
+        }
+        unsigned tot = BR(tmp).Sum(s);
+        if (threadIdx.x == 0) ubits[u] = tot;
+        __syncthreads();
+    }
+}
+
+// Pack one unit per block: per-thread bit offsets by block scan, codewords OR-ed into a
+// shared word buffer aligned to the unit's global word, then streamed out (boundary words
+// shared with the neighbouring units use atomicOr on a zeroed buffer).
+__global__ void __launch_bounds__(kEncThreads) k_encode(const uint32_t *__restrict__ keys, int64_t n,
+                                                        const uint8_t *__restrict__ lens,
+                                                        const uint32_t *__restrict__ codes, uint32_t dict,
+                                                        const uint64_t *__restrict__ uoff,
+                                                        const uint64_t *__restrict__ ubits,
+                                                        uint32_t *__restrict__ out, int64_t units) {
+    __shared__ uint32_t words[kBlockSymbols + 2];
+    __shared__ uint8_t sl[kEncTableMax];
+    __shared__ uint32_t sc[kEncTableMax];
+    const bool sm = dict <= kEncTableMax;
+    if (sm)
+        for (uint32_t k = threadIdx.x; k < dict; k += blockDim.x) { sl[k] = lens[k]; sc[k] = codes[k]; }
+    typedef cub::BlockScan<unsigned, kEncThreads> BS;
+    __shared__ typename BS::TempStorage tmp;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        for (int w = threadIdx.x; w < kBlockSymbols + 2; w += blockDim.x) words[w] = 0;
+        __syncthreads();
+        const int64_t lo = u * kBlockSymbols + (int64_t)threadIdx.x * kSymPerThread;
+        uint32_t k16[kSymPerThread];
+        int cnt = 0;
+        if (lo + kSymPerThread <= n) {
+            const uint4 *p = reinterpret_cast<const uint4 *>(keys + lo);
+#pragma unroll
+            for (int q = 0; q < kSymPerThread / 4; q++) {
+                uint4 v = p[q];
+                k16[4 * q] = v.x; k16[4 * q + 1] = v.y; k16[4 * q + 2] = v.z; k16[4 * q + 3] = v.w;
+            }
+            cnt = kSymPerThread;
+        } else {
+            for (int64_t i = lo; i < min64(n, lo + kSymPerThread); i++) k16[cnt++] = keys[i];
+        }
+        unsigned mybits = 0;
+#pragma unroll
+        for (int q = 0; q < kSymPerThread; q++)
+            if (q < cnt) mybits += sm ? sl[k16[q]] : lens[k16[q]];
+        unsigned start;
+        BS(tmp).ExclusiveSum(mybits, start);
+        const uint64_t g = uoff[u];
+        uint32_t pos = (uint32_t)(g & 31) + start;
+#pragma unroll
+        for (int q = 0; q < kSymPerThread; q++) {
+            if (q >= cnt) break;
+            const uint32_t key = k16[q];
+            const int L = sm ? sl[key] : lens[key];
+            const uint32_t c = sm ? sc[key] : codes[key];
+            // left-align the L-bit code in a 64-bit window at bit (pos & 31) of word pos >> 5
+            const uint64_t v = ((uint64_t)c << (64 - L)) >> (pos & 31);
+            const uint32_t hi = (uint32_t)(v >> 32), lo32 = (uint32_t)v;
+            atomicOr(&words[pos >> 5], hi);
+            if (lo32) atomicOr(&words[(pos >> 5) + 1], lo32);
+            pos += L;
+        }
+        __syncthreads();
+        const uint32_t nw = (uint32_t)(((g & 31) + ubits[u] + 31) >> 5);
+        uint32_t *dst = out + (g >> 5);
+        for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) {
+            const uint32_t val = bswap32(words[w]);
+            if (w == 0 || w == nw - 1) atomicOr(&dst[w], val);
+            else dst[w] = val;
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict_size, const uint8_t *lengths,
+                   const uint32_t *codes, EncodeResult &res, cudaStream_t s) {
+    const int64_t units = (n + kBlockSymbols - 1) / kBlockSymbols;
+    res.n_units = units;
+    uint8_t *d_len = (uint8_t *)ctx->dbuf("enc_len", dict_size + 16);
+    uint32_t *d_code = (uint32_t *)ctx->dbuf("enc_code", (size_t)dict_size * 4 + 16);
+    uint64_t *ubits = (uint64_t *)ctx->dbuf("enc_ubits", (units + 1) * 8);
+    uint64_t *uoff = (uint64_t *)ctx->dbuf("enc_uoff", (units + 1) * 8);
+    CUDA_CHECK(cudaMemcpyAsync(d_len, lengths, dict_size, cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaMemcpyAsync(d_code, codes, (size_t)dict_size * 4, cudaMemcpyHostToDevice, s));
+    k_unit_bits<<<(unsigned)std::min<int64_t>(units, 148 * 16), kEncThreads, 0, s>>>(keys, n, d_len, dict_size, ubits, units);
+    LAUNCH_CHECK();
+    CUDA_CHECK(cudaMemsetAsync(ubits + units, 0, 8, s));
+    size_t tb = 0;
+    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, ubits, uoff, (int)(units + 1), s));
+    void *tmp = ctx->dbuf("cub_tmp", tb);
+    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp, tb, ubits, uoff, (int)(units + 1), s));
+    count_launch();
+    uint64_t *h = (uint64_t *)ctx->hbuf("enc_total", 16);
+    CUDA_CHECK(cudaMemcpyAsync(h, uoff + units, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    res.total_bits = h[0];
+    const size_t words = (size_t)((res.total_bits + 31) / 32) + 2;
+    res.d_words = (uint32_t *)ctx->dbuf("enc_words", words * 4);
+    CUDA_CHECK(cudaMemsetAsync(res.d_words, 0, words * 4, s));
+    k_encode<<<(unsigned)std::min<int64_t>(units, 148 * 8), kEncThreads, 0, s>>>(keys, n, d_len, d_code, dict_size, uoff,
+                                                                                  ubits, res.d_words, units);
+    LAUNCH_CHECK();
+    res.d_offsets = uoff;
+}
+
+// ===================================================================== decode
+namespace {
+
+constexpr int kLutSize = 1 << kLutBits;
+
+struct DecTables {
+    long long first_code[258];
+    long long first_rank[258];
+    long long cnt[258];
+    int max_len;
+};
+
+__device__ __forceinline__ uint32_t load_be(const uint32_t *w, uint64_t i) {
+    return __byte_perm(__ldg(w + i), 0, 0x0123);
+}
+
+// One thread per 4096-symbol unit, walking the canonical code (huffman.py:292-313).
+// Fast path (max_len <= 32): 12-bit table lookup, then canonical search on a 32-bit window.
+// Slow path (max_len > 32, only reachable with a corrupted length array): bit-serial walk
+// with numba's wrapping int64 arithmetic.
+__global__ void k_decode(const uint32_t *__restrict__ words, uint64_t limit, const uint64_t *__restrict__ offs,
+                         uint64_t nsym, int64_t units, const DecTables *__restrict__ tabs_g,
+                         const uint32_t *__restrict__ lut_g, const uint32_t *__restrict__ sym_by_rank,
+                         uint32_t *__restrict__ keys, double *__restrict__ coef, double bin, uint32_t key_limit,
+                         long long *__restrict__ unit_err, unsigned long long *__restrict__ first_bad,
+                         unsigned *__restrict__ max_key) {
+    __shared__ uint32_t lut[kLutSize];
+    __shared__ DecTables T;
+    for (int i = threadIdx.x; i < kLutSize; i += blockDim.x) lut[i] = lut_g[i];
+    for (int i = threadIdx.x; i < (int)(sizeof(DecTables) / 8); i += blockDim.x)
+        ((long long *)&T)[i] = ((const long long *)tabs_g)[i];
+    __syncthreads();
+    const int max_len = T.max_len;
+    unsigned kmax = 0;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < units; u += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t lo = (uint64_t)u * kBlockSymbols;
+        const uint64_t cnt = nsym - lo < (uint64_t)kBlockSymbols ? nsym - lo : (uint64_t)kBlockSymbols;
+        uint64_t pos = offs[u];
+        long long err = -1;
+        for (uint64_t i = 0; i < cnt; i++) {
+            const uint64_t cw = pos;
+            uint32_t sym = 0;
+            int L = 0;
+            if (max_len <= 32) {
+                if (pos >= limit) { err = (long long)cw; break; }
+                const uint64_t wi = pos >> 5;
+                const int sh = (int)(pos & 31);
+                const uint64_t win64 = ((uint64_t)load_be(words, wi) << 32) | load_be(words, wi + 1);
+                const uint32_t win = (uint32_t)((win64 << sh) >> 32);
+                const uint32_t e = lut[win >> (32 - kLutBits)];
+                if (e & 0xffu) {
+                    L = (int)(e & 0xffu);
+                    sym = e >> 8;
+                } else {
+                    for (int l = kLutBits + 1; l <= max_len; l++) {
+                        const long long code = (long long)(win >> (32 - l));
+                        const long long idx = code - T.first_code[l];
+                        if (idx >= 0 && idx < T.cnt[l]) {
+                            L = l;
+                            sym = sym_by_rank[T.first_rank[l] + idx];
+                            break;
+                        }
+                    }
+                }
+                if (L == 0 || pos + (uint64_t)L > limit) { err = (long long)cw; break; }
+                pos += L;
+            } else {
+                unsigned long long code = 0;
+                int len = 0;
+                bool ok = false;
+                for (;;) {
+                    if (pos >= limit || len >= max_len) break;
+                    const uint32_t word = load_be(words, pos >> 5);
+                    const unsigned long long bit = (word >> (31 - (pos & 31))) & 1u;
+                    code = (code << 1) | bit;
+                    pos++;
+                    len++;
+                    const long long idx = (long long)(code - (unsigned long long)T.first_code[len]);
+                    if (idx >= 0 && idx < T.cnt[len]) {
+                        sym = sym_by_rank[T.first_rank[len] + idx];
+                        ok = true;
+                        break;
+                    }
+                }
+                if (!ok) { err = (long long)cw; break; }
+            }
+            kmax = sym > kmax ? sym : kmax;
+            if (keys) keys[lo + i] = sym;
+            if (coef) {
+                const long long b = (long long)(sym >> 1) ^ -(long long)(sym & 1u);   // unzigzag
+                coef[lo + i] = __dmul_rn((double)b, bin);                            // quantize.py:111
+            }
+        }
+        if (err >= 0) {
+            unit_err[u] = err;
+            atomicMin(first_bad, (unsigned long long)u);
+        }
+    }
+    for (int o = 16; o; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    if ((threadIdx.x & 31) == 0 && kmax) atomicMax(max_key, kmax);
+    (void)key_limit;
+}
+
+__global__ void k_fill(uint32_t *keys, double *coef, int64_t n, uint32_t sym, double val) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (keys) keys[i] = sym;
+        if (coef) coef[i] = val;
+    }
+}
+
+}  // namespace
+
+void decode_device(hpdr_ctx *ctx, const DecodeJob &job, DecodeResult &res, cudaStream_t s) {
+    // _decode_tables (huffman.py:207-225) and the 12-bit lookup table
+    const uint32_t dict = job.dict_size;
+    std::vector<uint32_t> present;
+    int max_len = 0;
+    for (uint32_t k = 0; k < dict; k++)
+        if (job.lengths[k]) {
+            present.push_back(k);
+            max_len = std::max<int>(max_len, job.lengths[k]);
+        }
+    std::stable_sort(present.begin(), present.end(),
+                     [&](uint32_t x, uint32_t y) { return job.lengths[x] < job.lengths[y]; });
+    DecTables *T = (DecTables *)ctx->hbuf("dec_tabs", sizeof(DecTables) + kLutSize * 4 + (present.size() + 1) * 4);
+    memset(T, 0, sizeof(DecTables));
+    for (uint32_t k : present) T->cnt[job.lengths[k]]++;
+    unsigned long long code = 0;
+    long long rank = 0;
+    for (int ln = 1; ln <= max_len; ln++) {
+        if (ln > 1) code <<= 1;
+        T->first_code[ln] = (long long)code;
+        T->first_rank[ln] = rank;
+        code += (unsigned long long)T->cnt[ln];
+        rank += T->cnt[ln];
+    }
+    T->max_len = max_len;
+    uint32_t *lut = (uint32_t *)(T + 1);
+    uint32_t *sbr = lut + kLutSize;
+    for (size_t i = 0; i < present.size(); i++) sbr[i] = present[i];
+    const int lut_len = std::min(kLutBits, max_len);
+    for (uint32_t v = 0; v < (uint32_t)kLutSize; v++) {
+        uint32_t e = 0;
+        for (int l = 1; l <= lut_len && max_len <= 32; l++) {
+            long long c = (long long)(v >> (kLutBits - l));
+            long long idx = c - T->first_code[l];
+            if (idx >= 0 && idx < T->cnt[l]) {
+                e = (sbr[T->first_rank[l] + idx] << 8) | (uint32_t)l;
+                break;
+            }
+        }
+        lut[v] = e;
+    }
+    const size_t tab_bytes = sizeof(DecTables) + kLutSize * 4 + (present.size() + 1) * 4;
+    char *d_tab = (char *)ctx->dbuf("dec_tabs", tab_bytes);
+    CUDA_CHECK(cudaMemcpyAsync(d_tab, T, tab_bytes, cudaMemcpyHostToDevice, s));
+
+    const int64_t units = (int64_t)job.n_units;
+    uint64_t *d_off = (uint64_t *)ctx->dbuf("dec_off", (units + 1) * 8);
+    CUDA_CHECK(cudaMemcpyAsync(d_off, job.offsets, units * 8, cudaMemcpyHostToDevice, s));
+    const size_t pbytes = (size_t)((job.total_bits + 7) / 8);
+    const size_t pwords = pbytes / 4 + 4;
+    uint32_t *d_words = (uint32_t *)ctx->dbuf("dec_words", pwords * 4);
+    CUDA_CHECK(cudaMemsetAsync((char *)d_words + (pbytes & ~size_t(3)), 0, 16, s));
+    CUDA_CHECK(cudaMemcpyAsync(d_words, job.packed, pbytes, cudaMemcpyDefault, s));
+    long long *uerr = (long long *)ctx->dbuf("dec_err", (units + 1) * 8);
+    unsigned long long *flag = (unsigned long long *)ctx->dbuf("dec_flag", 32);
+    unsigned long long init[2] = {~0ULL, 0ULL};
+    unsigned long long *hinit = (unsigned long long *)ctx->hbuf("dec_init", 64);
+    memcpy(hinit, init, 16);
+    CUDA_CHECK(cudaMemcpyAsync(flag, hinit, 16, cudaMemcpyHostToDevice, s));
+    if (units > 0) {
+        k_decode<<<grid_for(units, 64, 148 * 64), 64, 0, s>>>(
+            d_words, job.total_bits, d_off, job.n_symbols, units, (const DecTables *)d_tab,
+            (const uint32_t *)(d_tab + sizeof(DecTables)),
+            (const uint32_t *)(d_tab + sizeof(DecTables) + kLutSize * 4), job.keys, job.coef, job.bin_width,
+            job.key_limit, uerr, flag, (unsigned *)(flag + 1));
+        LAUNCH_CHECK();
+    }
+    unsigned long long *h = (unsigned long long *)ctx->hbuf("dec_rb", 32);
+    CUDA_CHECK(cudaMemcpyAsync(h, flag, 16, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    res.bad_bit = -1;
+    if (h[0] != ~0ULL) {
+        long long b;
+        CUDA_CHECK(cudaMemcpy(&b, uerr + h[0], 8, cudaMemcpyDeviceToHost));
+        res.bad_bit = b;
+    }
+    res.max_key = (uint32_t)h[1];
+    res.key_out_of_range = res.max_key >= job.key_limit;
+}
+
+void fill_single(uint32_t *keys, double *coef, int64_t n, uint32_t sym, double bin_width, cudaStream_t s) {
+    const long long b = (long long)(sym >> 1) ^ -(long long)(sym & 1u);
+    const double val = (double)b * bin_width;
+    k_fill<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(keys, coef, n, sym, val);
+    LAUNCH_CHECK();
+}
+
+}  // namespace hpdr

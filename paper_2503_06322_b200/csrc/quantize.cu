@@ -1,0 +1,220 @@
+// quantize.cu -- level-wise linear quantization fused with the key histogram, and the
+// order-preserving outlier compaction (quantize.py:50-98, huffman.py:74-104).
+#include <cub/cub.cuh>
+
+#include "stages.cuh"
+
+namespace hpdr {
+
+namespace {
+
+constexpr int kQThreads = 256;
+constexpr int kSmemHistMax = 16384;          // u32 shared counters (64 KB)
+constexpr int kChunkWords = 1024;            // outlier-mask words per compaction block
+constexpr double kBinLimit = 4611686018427387904.0;   // 2^62, quantize.py:21
+
+struct Coarsest {
+    long long idx[16];
+    int n;
+};
+
+__device__ __forceinline__ uint32_t zigzag32(long long b) {
+    return (uint32_t)(((unsigned long long)b << 1) ^ (unsigned long long)(b >> 63));
+}
+
+// Warp-aggregated increment: lanes with equal keys add once (key 0 dominates real data).
+__device__ __forceinline__ void hist_add(uint32_t *sh, unsigned long long *g, bool use_sh, uint32_t key, unsigned mask) {
+    unsigned peers = __match_any_sync(mask, key);
+    int lane = threadIdx.x & 31;
+    if (lane == __ffs(peers) - 1) {
+        if (use_sh) atomicAdd(&sh[key], (uint32_t)__popc(peers));
+        else atomicAdd(&g[key], (unsigned long long)__popc(peers));
+    }
+}
+
+__global__ void __launch_bounds__(kQThreads) k_quantize(const double *__restrict__ coef, int64_t n, Coarsest co,
+                                                        double bin, long long half, uint32_t dict,
+                                                        uint32_t *__restrict__ keys, uint32_t *__restrict__ omask,
+                                                        unsigned long long *__restrict__ hist, int *__restrict__ flags) {
+    extern __shared__ uint32_t sh_hist[];
+    const bool use_sh = dict <= kSmemHistMax;
+    if (use_sh)
+        for (uint32_t k = threadIdx.x; k < dict; k += blockDim.x) sh_hist[k] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+    int fl = 0;
+    for (int64_t wbase = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; wbase < n;
+         wbase += warps_total * 32) {
+        const int64_t i = wbase + lane;
+        const bool valid = i < n;
+        const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+        double v = valid ? coef[i] : 0.0;
+        long long b = 0;
+        if (!isfinite(v)) {
+            fl |= 1;
+        } else {
+            double sc = v / bin;                       // IEEE division (quantize.py:73)
+            if (fabs(sc) >= kBinLimit) fl |= 2;
+            else b = (long long)rint(sc);              // half to even (quantize.py:76)
+        }
+#pragma unroll
+        for (int k = 0; k < 16; k++)
+            if (k < co.n && i == co.idx[k]) b = 0;    // coarsest nodes are carried raw (:77)
+        const bool out = valid && (b >= half || -b >= half);
+        const unsigned om = __ballot_sync(0xffffffffu, out);
+        if (lane == 0) omask[wbase >> 5] = om;
+        if (out) b = 0;
+        const uint32_t key = zigzag32(b);
+        if (valid) {
+            keys[i] = key;
+            hist_add(sh_hist, hist, use_sh, key, vmask);
+        }
+    }
+    if (fl) atomicOr(flags, fl);
+    if (use_sh) {
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < dict; k += blockDim.x) {
+            uint32_t c = sh_hist[k];
+            if (c) atomicAdd(&hist[k], (unsigned long long)c);
+        }
+    }
+}
+
+__global__ void k_chunk_counts(const uint32_t *__restrict__ omask, int64_t words, unsigned long long *__restrict__ counts) {
+    typedef cub::BlockReduce<unsigned, 256> BR;
+    __shared__ typename BR::TempStorage tmp;
+    const int64_t c = blockIdx.x;
+    unsigned s = 0;
+    for (int64_t w = c * kChunkWords + threadIdx.x; w < min64(words, (c + 1) * kChunkWords); w += blockDim.x)
+        s += __popc(omask[w]);
+    unsigned tot = BR(tmp).Sum(s);
+    if (threadIdx.x == 0) counts[c] = tot;
+}
+
+__global__ void k_write_outliers(const uint32_t *__restrict__ omask, int64_t words, const double *__restrict__ coef,
+                                 double bin, const unsigned long long *__restrict__ chunk_off,
+                                 uint64_t *__restrict__ oidx, int64_t *__restrict__ obins) {
+    typedef cub::BlockScan<unsigned, 256> BS;
+    __shared__ typename BS::TempStorage tmp;
+    const int64_t c = blockIdx.x;
+    unsigned long long base = chunk_off[c];
+    for (int64_t w0 = c * kChunkWords; w0 < min64(words, (c + 1) * kChunkWords); w0 += blockDim.x) {
+        const int64_t w = w0 + threadIdx.x;
+        uint32_t m = (w < words && w < (c + 1) * kChunkWords) ? omask[w] : 0u;
+        unsigned pre, tot;
+        BS(tmp).ExclusiveSum((unsigned)__popc(m), pre, tot);
+        unsigned long long pos = base + pre;
+        while (m) {
+            int bit = __ffs(m) - 1;
+            m &= m - 1;
+            int64_t i = w * 32 + bit;
+            oidx[pos] = (uint64_t)i;
+            obins[pos] = (long long)rint(coef[i] / bin);
+            pos++;
+        }
+        base += tot;
+        __syncthreads();
+    }
+}
+
+__global__ void k_histogram(const uint32_t *__restrict__ keys, int64_t n, uint32_t dict,
+                            unsigned long long *__restrict__ hist, int *__restrict__ bad) {
+    extern __shared__ uint32_t sh_hist[];
+    const bool use_sh = dict <= kSmemHistMax;
+    if (use_sh)
+        for (uint32_t k = threadIdx.x; k < dict; k += blockDim.x) sh_hist[k] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t wbase = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; wbase < n;
+         wbase += warps_total * 32) {
+        const int64_t i = wbase + lane;
+        uint32_t key = i < n ? keys[i] : 0u;
+        bool ok = i < n && key < dict;
+        if (i < n && key >= dict) atomicOr(bad, 1);
+        unsigned m = __ballot_sync(0xffffffffu, ok);
+        if (ok) hist_add(sh_hist, hist, use_sh, key, m);
+    }
+    if (use_sh) {
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < dict; k += blockDim.x) {
+            uint32_t c = sh_hist[k];
+            if (c) atomicAdd(&hist[k], (unsigned long long)c);
+        }
+    }
+}
+
+}  // namespace
+
+void quantize_device(hpdr_ctx *ctx, const double *coef, int64_t n, const std::vector<int64_t> &coarsest,
+                     double bin_width, uint32_t dict_size, uint32_t *keys, QuantResult &res, cudaStream_t s) {
+    const int64_t words = (n + 31) / 32;
+    const int64_t chunks = (words + kChunkWords - 1) / kChunkWords;
+    uint32_t *omask = (uint32_t *)ctx->dbuf("omask", words * 4);
+    unsigned long long *hist = (unsigned long long *)ctx->dbuf("hist", (size_t)dict_size * 8);
+    int *flags = (int *)ctx->dbuf("qflags", 16);
+    unsigned long long *ccount = (unsigned long long *)ctx->dbuf("ochunk", (chunks + 1) * 8);
+    unsigned long long *coff = (unsigned long long *)ctx->dbuf("ochunk_off", (chunks + 1) * 8);
+    CUDA_CHECK(cudaMemsetAsync(hist, 0, (size_t)dict_size * 8, s));
+    CUDA_CHECK(cudaMemsetAsync(flags, 0, 16, s));
+    Coarsest co;
+    co.n = (int)coarsest.size();
+    for (int k = 0; k < 16; k++) co.idx[k] = k < co.n ? coarsest[k] : -1;
+    const long long half = dict_size / 2;
+    size_t smem = dict_size <= kSmemHistMax ? (size_t)dict_size * 4 : 0;
+    if (smem > 48 * 1024) CUDA_CHECK(cudaFuncSetAttribute(k_quantize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    unsigned grid = grid_for(n, kQThreads, 148 * 4);
+    k_quantize<<<grid, kQThreads, smem, s>>>(coef, n, co, bin_width, half, dict_size, keys, omask, hist, flags);
+    LAUNCH_CHECK();
+    k_chunk_counts<<<(unsigned)chunks, 256, 0, s>>>(omask, words, ccount);
+    LAUNCH_CHECK();
+    size_t tmp_bytes = 0;
+    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, ccount, coff, (int)(chunks + 1), s));
+    void *tmp = ctx->dbuf("cub_tmp", tmp_bytes);
+    CUDA_CHECK(cudaMemsetAsync(ccount + chunks, 0, 8, s));
+    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, ccount, coff, (int)(chunks + 1), s));
+    count_launch();
+    uint64_t *h = (uint64_t *)ctx->hbuf("q_readback", (size_t)dict_size * 8 + 64);
+    CUDA_CHECK(cudaMemcpyAsync(h, coff + chunks, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaMemcpyAsync(h + 1, flags, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaMemcpyAsync(h + 2, hist, (size_t)dict_size * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    res.n_outliers = h[0];
+    int fl;
+    memcpy(&fl, h + 1, 4);
+    res.flags = fl;
+    res.hist.assign(h + 2, h + 2 + dict_size);
+    if (fl) return;
+    res.d_outlier_idx = (uint64_t *)ctx->dbuf("oidx", res.n_outliers * 8);
+    res.d_outlier_bins = (int64_t *)ctx->dbuf("obins", res.n_outliers * 8);
+    if (res.n_outliers) {
+        k_write_outliers<<<(unsigned)chunks, 256, 0, s>>>(omask, words, coef, bin_width, coff, res.d_outlier_idx,
+                                                          res.d_outlier_bins);
+        LAUNCH_CHECK();
+    }
+}
+
+void histogram_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict_size, std::vector<uint64_t> &hist,
+                      bool *bad, cudaStream_t s) {
+    unsigned long long *d = (unsigned long long *)ctx->dbuf("hist", (size_t)dict_size * 8);
+    int *flags = (int *)ctx->dbuf("qflags", 16);
+    CUDA_CHECK(cudaMemsetAsync(d, 0, (size_t)dict_size * 8, s));
+    CUDA_CHECK(cudaMemsetAsync(flags, 0, 16, s));
+    size_t smem = dict_size <= kSmemHistMax ? (size_t)dict_size * 4 : 0;
+    if (smem > 48 * 1024) CUDA_CHECK(cudaFuncSetAttribute(k_histogram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (n > 0) {
+        k_histogram<<<grid_for(n, 256, 148 * 4), 256, smem, s>>>(keys, n, dict_size, d, flags);
+        LAUNCH_CHECK();
+    }
+    uint64_t *h = (uint64_t *)ctx->hbuf("q_readback", (size_t)dict_size * 8 + 64);
+    CUDA_CHECK(cudaMemcpyAsync(h, flags, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaMemcpyAsync(h + 1, d, (size_t)dict_size * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    int fl;
+    memcpy(&fl, h, 4);
+    *bad = fl != 0;
+    hist.assign(h + 1, h + 1 + dict_size);
+}
+
+}  // namespace hpdr

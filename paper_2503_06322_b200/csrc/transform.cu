@@ -1,0 +1,545 @@
+// transform.cu -- per-axis multilevel kernels (GPK prolong, LPK mass-transfer, IPK Thomas)
+// and the level drivers for decompose / recompose.
+//
+// Bit-exactness: every operation uses the reference's association order with explicit
+// round-to-nearest intrinsics (no FMA contraction; the library is also built with
+// -fmad=false).  See SURVEY Appendix B and transform.py:158-245.
+#include "transform.cuh"
+
+namespace hpdr {
+
+namespace {
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// ---------------------------------------------------------------- input conversion / range
+__global__ void k_to_f64(const void *__restrict__ in, int dtype, double *__restrict__ out, int64_t n) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (dtype == 0) {
+        const float *f = (const float *)in;
+        for (; i < n; i += stride) out[i] = (double)f[i];
+    } else {
+        const double *f = (const double *)in;
+        for (; i < n; i += stride) out[i] = f[i];
+    }
+}
+
+__device__ __forceinline__ unsigned long long ord_key(double v) {
+    unsigned long long u = (unsigned long long)__double_as_longlong(v);
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double ord_val(unsigned long long k) {
+    unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k;
+    return __longlong_as_double((long long)u);
+}
+
+__global__ void k_minmax(const void *__restrict__ in, int dtype, int64_t n, unsigned long long *res) {
+    unsigned long long mn = ~0ULL, mx = 0ULL;
+    int nan = 0;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (; i < n; i += stride) {
+        double v = dtype == 0 ? (double)((const float *)in)[i] : ((const double *)in)[i];
+        if (v != v) { nan = 1; continue; }
+        unsigned long long k = ord_key(v);
+        mn = k < mn ? k : mn;
+        mx = k > mx ? k : mx;
+    }
+    for (int o = 16; o; o >>= 1) {
+        unsigned long long a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
+        nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+    }
+    __shared__ unsigned long long smn[32], smx[32];
+    __shared__ int snan[32];
+    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { smn[w] = mn; smx[w] = mx; snan[w] = nan; }
+    __syncthreads();
+    if (w == 0) {
+        int nw = blockDim.x >> 5;
+        mn = l < nw ? smn[l] : ~0ULL;
+        mx = l < nw ? smx[l] : 0ULL;
+        nan = l < nw ? snan[l] : 0;
+        for (int o = 16; o; o >>= 1) {
+            unsigned long long a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+            mn = a < mn ? a : mn;
+            mx = b > mx ? b : mx;
+            nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+        }
+        if (l == 0) {
+            atomicMin(&res[0], mn);
+            atomicMax(&res[1], mx);
+            if (nan) atomicOr(&res[2], 1ULL);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- level gathers / scatters
+// Iterate rows (i0, i1, i2) of a dense 4-D shape; threads cover i3.
+#define FOR_ROWS(SH)                                                                       \
+    const int64_t rows_ = (SH).n[0] * (SH).n[1] * (SH).n[2];                               \
+    for (int64_t r_ = blockIdx.y; r_ < rows_; r_ += gridDim.y)                             \
+        for (int64_t i3 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i3 < (SH).n[3];  \
+             i3 += (int64_t)gridDim.x * blockDim.x)
+
+__device__ __forceinline__ void row_coords(int64_t r, const Shape4 &s, int64_t &i0, int64_t &i1, int64_t &i2) {
+    i2 = r % s.n[2];
+    int64_t t = r / s.n[2];
+    i1 = t % s.n[1];
+    i0 = t / s.n[1];
+}
+
+struct Sel4 { const int32_t *s[4]; };   // per-axis index lists (nullptr: identity / all)
+
+// dst(csh)[c] = src(fsh)[sel(c)]  -- the coarse selector of transform.py:265-272
+__global__ void k_gather_coarse(const double *__restrict__ src, Shape4 fsh, double *__restrict__ dst, Shape4 csh,
+                                Sel4 sel) {
+    FOR_ROWS(csh) {
+        int64_t c0, c1, c2;
+        row_coords(r_, csh, c0, c1, c2);
+        int64_t j0 = sel.s[0] ? sel.s[0][c0] : c0, j1 = sel.s[1] ? sel.s[1][c1] : c1;
+        int64_t j2 = sel.s[2] ? sel.s[2][c2] : c2, j3 = sel.s[3] ? sel.s[3][i3] : i3;
+        dst[r_ * csh.n[3] + i3] = src[((j0 * fsh.n[1] + j1) * fsh.n[2] + j2) * fsh.n[3] + j3];
+    }
+}
+
+__device__ __forceinline__ bool is_coarse(const Sel4 &pb, int64_t i0, int64_t i1, int64_t i2, int64_t i3) {
+    return (!pb.s[0] || pb.s[0][i0] < 0) && (!pb.s[1] || pb.s[1][i1] < 0) && (!pb.s[2] || pb.s[2][i2] < 0) &&
+           (!pb.s[3] || pb.s[3][i3] < 0);
+}
+
+// coef[map(i)] = src[i] for the level's nodes (fine_only: skip nodes that survive to the
+// next level; they are overwritten later exactly as in transform.py:314-315)
+__global__ void k_scatter_level(const double *__restrict__ src, Shape4 sh, double *__restrict__ coef, Shape4 dims,
+                                Sel4 map, Sel4 pb, int fine_only) {
+    FOR_ROWS(sh) {
+        int64_t i0, i1, i2;
+        row_coords(r_, sh, i0, i1, i2);
+        if (fine_only && is_coarse(pb, i0, i1, i2, i3)) continue;
+        int64_t f = (((int64_t)map.s[0][i0] * dims.n[1] + map.s[1][i1]) * dims.n[2] + map.s[2][i2]) * dims.n[3] +
+                    map.s[3][i3];
+        coef[f] = src[r_ * sh.n[3] + i3];
+    }
+}
+
+// dst[i] = coef[map(i)], zeroed at nodes of the next-coarser level (transform.py:339-343)
+__global__ void k_gather_level(const double *__restrict__ coef, Shape4 dims, Sel4 map, Sel4 pb, double *__restrict__ dst,
+                               Shape4 sh, int zero_coarse) {
+    FOR_ROWS(sh) {
+        int64_t i0, i1, i2;
+        row_coords(r_, sh, i0, i1, i2);
+        double v;
+        if (zero_coarse && is_coarse(pb, i0, i1, i2, i3)) {
+            v = 0.0;
+        } else {
+            int64_t f = (((int64_t)map.s[0][i0] * dims.n[1] + map.s[1][i1]) * dims.n[2] + map.s[2][i2]) *
+                            dims.n[3] + map.s[3][i3];
+            v = coef[f];
+        }
+        dst[r_ * sh.n[3] + i3] = v;
+    }
+}
+
+// ---------------------------------------------------------------- GPK: prolongation along one axis
+// MODE 0: dst = pred;  MODE 1: dst = aux - pred (decompose residual, transform.py:312);
+// MODE 2: dst = pred + aux (recompose, transform.py:347)
+template <int MODE, typename IT>
+__global__ void k_prolong(const double *__restrict__ src, double *__restrict__ dst, const double *__restrict__ aux,
+                          int64_t outer, int32_t nc, int32_t n, int64_t inner, const int32_t *__restrict__ pa,
+                          const int32_t *__restrict__ pb, const double *__restrict__ pt) {
+    const IT in_ = (IT)inner;
+    const IT per = (IT)n * in_;
+    for (int64_t p = blockIdx.y; p < outer; p += gridDim.y) {
+        const double *s = src + p * (int64_t)nc * inner;
+        double *d = dst + p * (int64_t)n * inner;
+        const double *x = MODE ? aux + p * (int64_t)n * inner : nullptr;
+        for (IT e = blockIdx.x * (IT)blockDim.x + threadIdx.x; e < per; e += (IT)gridDim.x * blockDim.x) {
+            IT j = e / in_;
+            IT q = e - j * in_;
+            int a = pa[j], b = pb[j];
+            double va = s[(IT)a * in_ + q];
+            double v = va;
+            if (b >= 0) {
+                double vb = s[(IT)b * in_ + q];
+                v = dadd(va, dmul(pt[j], dsub(vb, va)));
+            }
+            if (MODE == 1) v = dsub(x[e], v);
+            if (MODE == 2) v = dadd(v, x[e]);
+            d[e] = v;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- LPK: mass multiply + restriction
+template <typename IT>
+__device__ __forceinline__ double mass_y(const double *__restrict__ x, IT in_, int j, int n,
+                                         const double *__restrict__ ml, const double *__restrict__ md,
+                                         const double *__restrict__ mu) {
+    double v = dmul(md[j], x[(IT)j * in_]);
+    if (j >= 1) v = dadd(v, dmul(ml[j], x[(IT)(j - 1) * in_]));
+    if (j + 1 < n) v = dadd(v, dmul(mu[j], x[(IT)(j + 1) * in_]));
+    return v;
+}
+
+template <typename IT>
+__global__ void k_mass_restrict(const double *__restrict__ src, double *__restrict__ dst, int64_t outer, int32_t n,
+                                int32_t nc, int64_t inner, DevAxis ax) {
+    const IT in_ = (IT)inner;
+    const IT per = (IT)nc * in_;
+    for (int64_t p = blockIdx.y; p < outer; p += gridDim.y) {
+        const double *s = src + p * (int64_t)n * inner;
+        double *d = dst + p * (int64_t)nc * inner;
+        for (IT e = blockIdx.x * (IT)blockDim.x + threadIdx.x; e < per; e += (IT)gridDim.x * blockDim.x) {
+            IT c = e / in_;
+            IT q = e - c * in_;
+            const double *x = s + q;
+            double v = mass_y<IT>(x, in_, ax.r0[c], n, ax.ml, ax.md, ax.mu);
+            int r = ax.rr[c];
+            if (r >= 0) v = dadd(v, dmul(ax.wr[c], mass_y<IT>(x, in_, r, n, ax.ml, ax.md, ax.mu)));
+            int l = ax.rl[c];
+            if (l >= 0) v = dadd(v, dmul(ax.wl[c], mass_y<IT>(x, in_, l, n, ax.ml, ax.md, ax.mu)));
+            d[e] = v;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- IPK: batched Thomas solves
+// Strided axis: one thread per line, threads along the contiguous inner index (coalesced).
+__global__ void k_thomas_strided(double *__restrict__ arr, int64_t outer, int32_t n, int64_t inner,
+                                 const double *__restrict__ tw, const double *__restrict__ tb,
+                                 const double *__restrict__ tu) {
+    const int64_t lines = outer * inner;
+    for (int64_t ln = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ln < lines; ln += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = ln / inner, q = ln - p * inner;
+        double *x = arr + p * (int64_t)n * inner + q;
+        double prev = x[0];
+        for (int i = 1; i < n; i++) {
+            double v = dsub(x[(int64_t)i * inner], dmul(tw[i], prev));
+            x[(int64_t)i * inner] = v;
+            prev = v;
+        }
+        double last = ddiv(prev, tb[n - 1]);
+        x[(int64_t)(n - 1) * inner] = last;
+        for (int i = n - 2; i >= 0; i--) {
+            double v = dsub(x[(int64_t)i * inner], dmul(tu[i], last));
+            v = ddiv(v, tb[i]);
+            x[(int64_t)i * inner] = v;
+            last = v;
+        }
+    }
+}
+
+// Contiguous axis: each warp owns 32 lines and walks them in 32x32 shared-memory tiles,
+// loading and storing tile rows coalesced and running one line per lane.
+constexpr int kThomasWarps = 4;
+__global__ void __launch_bounds__(kThomasWarps * 32) k_thomas_contig(double *__restrict__ arr, int64_t lines, int32_t n,
+                                                                     const double *__restrict__ tw,
+                                                                     const double *__restrict__ tb,
+                                                                     const double *__restrict__ tu) {
+    __shared__ double tile[kThomasWarps][32][33];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double (*T)[33] = tile[w];
+    for (int64_t base = ((int64_t)blockIdx.x * kThomasWarps + w) * 32; base < lines;
+         base += (int64_t)gridDim.x * kThomasWarps * 32) {
+        const int nl = (int)min64(32, lines - base);
+        double prev = 0.0;
+        for (int t0 = 0; t0 < n; t0 += 32) {
+            const int m = min(32, n - t0);
+            for (int r = 0; r < nl; r++)
+                if (lane < m) T[r][lane] = arr[(base + r) * n + t0 + lane];
+            __syncwarp();
+            if (lane < nl) {
+                for (int k = 0; k < m; k++) {
+                    const int i = t0 + k;
+                    double v = T[lane][k];
+                    if (i > 0) v = dsub(v, dmul(tw[i], prev));
+                    if (i == n - 1) v = ddiv(v, tb[n - 1]);
+                    T[lane][k] = v;
+                    prev = v;
+                }
+            }
+            __syncwarp();
+            for (int r = 0; r < nl; r++)
+                if (lane < m) arr[(base + r) * n + t0 + lane] = T[r][lane];
+            __syncwarp();
+        }
+        double last = prev;
+        for (int t0 = ((n - 1) / 32) * 32; t0 >= 0; t0 -= 32) {
+            const int m = min(32, n - t0);
+            for (int r = 0; r < nl; r++)
+                if (lane < m) T[r][lane] = arr[(base + r) * n + t0 + lane];
+            __syncwarp();
+            if (lane < nl) {
+                for (int k = m - 1; k >= 0; k--) {
+                    const int i = t0 + k;
+                    if (i == n - 1) continue;
+                    double v = dsub(T[lane][k], dmul(tu[i], last));
+                    v = ddiv(v, tb[i]);
+                    T[lane][k] = v;
+                    last = v;
+                }
+            }
+            __syncwarp();
+            for (int r = 0; r < nl; r++)
+                if (lane < m) arr[(base + r) * n + t0 + lane] = T[r][lane];
+            __syncwarp();
+        }
+    }
+}
+
+// ---------------------------------------------------------------- elementwise
+__global__ void k_add(const double *__restrict__ a, const double *__restrict__ b, double *__restrict__ o, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        o[i] = dadd(a[i], b[i]);
+}
+__global__ void k_sub(const double *__restrict__ a, const double *__restrict__ b, double *__restrict__ o, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        o[i] = dsub(a[i], b[i]);
+}
+
+template <typename T>
+__global__ void k_cast(const double *__restrict__ src, T *__restrict__ dst, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = (T)src[i];
+}
+
+// ---------------------------------------------------------------- host helpers
+void view(const Shape4 &sh, int a, int64_t &outer, int64_t &inner) {
+    outer = 1;
+    inner = 1;
+    for (int d = 0; d < a; d++) outer *= sh.n[d];
+    for (int d = a + 1; d < 4; d++) inner *= sh.n[d];
+}
+
+dim3 rows_grid(const Shape4 &sh) {
+    int64_t rows = sh.n[0] * sh.n[1] * sh.n[2];
+    unsigned gx = (unsigned)std::min<int64_t>((sh.n[3] + 255) / 256, 64);
+    unsigned gy = (unsigned)std::min<int64_t>(rows, 65535);
+    if (gx < 1) gx = 1;
+    if (gy < 1) gy = 1;
+    return dim3(gx, gy);
+}
+
+void prolong(const double *src, double *dst, const double *aux, int mode, const Shape4 &csh, int a,
+             const DevAxis &ax, cudaStream_t s) {
+    int64_t outer, inner;
+    view(csh, a, outer, inner);
+    const int64_t per = (int64_t)ax.n * inner;
+    dim3 grid(grid_for(per, 256, 4096), (unsigned)std::min<int64_t>(outer, 65535));
+    const bool small = per < (1LL << 32);
+#define PL(M)                                                                                                   \
+    if (small)                                                                                                  \
+        k_prolong<M, uint32_t><<<grid, 256, 0, s>>>(src, dst, aux, outer, ax.nc, ax.n, inner, ax.pa, ax.pb, ax.pt); \
+    else                                                                                                        \
+        k_prolong<M, uint64_t><<<grid, 256, 0, s>>>(src, dst, aux, outer, ax.nc, ax.n, inner, ax.pa, ax.pb, ax.pt)
+    if (mode == 0) PL(0);
+    else if (mode == 1) PL(1);
+    else PL(2);
+#undef PL
+    LAUNCH_CHECK();
+}
+
+void mass_restrict(const double *src, double *dst, const Shape4 &fsh, int a, const DevAxis &ax, cudaStream_t s) {
+    int64_t outer, inner;
+    view(fsh, a, outer, inner);
+    const int64_t per = (int64_t)ax.nc * inner;
+    dim3 grid(grid_for(per, 256, 4096), (unsigned)std::min<int64_t>(outer, 65535));
+    if (per < (1LL << 32))
+        k_mass_restrict<uint32_t><<<grid, 256, 0, s>>>(src, dst, outer, ax.n, ax.nc, inner, ax);
+    else
+        k_mass_restrict<uint64_t><<<grid, 256, 0, s>>>(src, dst, outer, ax.n, ax.nc, inner, ax);
+    LAUNCH_CHECK();
+}
+
+void thomas(double *arr, const Shape4 &csh, int a, const DevAxis &ax, cudaStream_t s) {
+    int64_t outer, inner;
+    view(csh, a, outer, inner);
+    if (inner == 1) {
+        int64_t lines = outer;
+        unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((lines + 127) / 128, 148 * 16));
+        k_thomas_contig<<<g, kThomasWarps * 32, 0, s>>>(arr, lines, ax.nc, ax.tw, ax.tb, ax.tu);
+    } else {
+        int64_t lines = outer * inner;
+        k_thomas_strided<<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb, ax.tu);
+    }
+    LAUNCH_CHECK();
+}
+
+Sel4 level_map(const DevPlan &p, int k) {
+    Sel4 m;
+    for (int d = 0; d < 4; d++) m.s[d] = p.map[d][k];
+    return m;
+}
+
+Sel4 coarse_flags(const DevStep &st) {
+    Sel4 f;
+    for (int d = 0; d < 4; d++) f.s[d] = st.ax[d].active ? st.ax[d].pb : nullptr;
+    return f;
+}
+
+double *level_ptr(const LevelBuffers &b, const DevPlan &p, int k) {
+    return k == 0 ? b.lvl0 : b.arena + p.level_off[k];
+}
+
+// Correction of transform.py:251-260: mass+restrict per active axis, then Thomas per active axis.
+const double *correction(const DevStep &st, const double *mc, const LevelBuffers &b, cudaStream_t s) {
+    const double *cur = mc;
+    Shape4 sh = st.fsh;
+    int k = 0;
+    for (int a = 0; a < 4; a++) {
+        if (!st.ax[a].active) continue;
+        double *out = (k++ % 2 == 0) ? b.t0 : b.t1;
+        mass_restrict(cur, out, sh, a, st.ax[a], s);
+        sh.n[a] = st.csh.n[a];
+        cur = out;
+    }
+    for (int a = 0; a < 4; a++)
+        if (st.ax[a].active) thomas(const_cast<double *>(cur), sh, a, st.ax[a], s);
+    return cur;
+}
+
+// Interpolation of transform.py:261-268, the last axis fused with the residual / add (mode 1 / 2).
+void interpolate(const DevStep &st, const double *coarse, double *out, const double *aux, int mode,
+                 const LevelBuffers &b, cudaStream_t s) {
+    int na = 0;
+    for (int a = 0; a < 4; a++) na += st.ax[a].active;
+    const double *cur = coarse;
+    Shape4 sh = st.csh;
+    int k = 0;
+    for (int a = 0; a < 4; a++) {
+        if (!st.ax[a].active) continue;
+        const bool last = (k == na - 1);
+        double *dst = last ? out : ((k % 2 == 0) ? b.t0 : b.t1);
+        prolong(cur, dst, last ? aux : nullptr, last ? mode : 0, sh, a, st.ax[a], s);
+        sh.n[a] = st.fsh.n[a];
+        cur = dst;
+        k++;
+    }
+}
+
+}  // namespace
+
+LevelBuffers level_buffers(hpdr_ctx *ctx, DevPlan &p) {
+    LevelBuffers b;
+    const int64_t N = p.n_total;
+    const int64_t C1 = p.host.L > 1 ? p.level_size[1] : 1;
+    b.lvl0 = (double *)ctx->dbuf("lvl0", N * 8);
+    b.arena = (double *)ctx->dbuf("arena", std::max<int64_t>(p.coarse_arena, 1) * 8);
+    b.mc = (double *)ctx->dbuf("mc", N * 8);
+    b.t0 = (double *)ctx->dbuf("t0", N * 8);
+    b.t1 = (double *)ctx->dbuf("t1", N * 8);
+    b.cg = (double *)ctx->dbuf("cg", C1 * 8);
+    return b;
+}
+
+void minmax_device(hpdr_ctx *ctx, const void *d_in, int dtype, int64_t n, double *vmin, double *vmax, cudaStream_t s) {
+    unsigned long long *d = (unsigned long long *)ctx->dbuf("minmax", 32);
+    unsigned long long *h = (unsigned long long *)ctx->hbuf("minmax_h", 32);
+    unsigned long long init[3] = {~0ULL, 0ULL, 0ULL};
+    CUDA_CHECK(cudaMemcpyAsync(d, init, 24, cudaMemcpyHostToDevice, s));
+    k_minmax<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(d_in, dtype, n, d);
+    LAUNCH_CHECK();
+    CUDA_CHECK(cudaMemcpyAsync(h, d, 24, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    if (h[2]) {
+        *vmin = __builtin_nan("");
+        *vmax = __builtin_nan("");
+        return;
+    }
+    auto val = [](unsigned long long k) {
+        unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k;
+        double d;
+        memcpy(&d, &u, 8);
+        return d;
+    };
+    *vmin = val(h[0]);
+    *vmax = val(h[1]);
+}
+
+const double *decompose_device(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int dtype, double *coef, cudaStream_t s) {
+    LevelBuffers b = level_buffers(ctx, p);
+    const int64_t N = p.n_total;
+    const int L = p.host.L;
+    k_to_f64<<<grid_for(N, 256, 148 * 16), 256, 0, s>>>(d_in, dtype, b.lvl0, N);
+    LAUNCH_CHECK();
+    for (int st_i = 0; st_i + 1 < L; st_i++) {
+        const DevStep &st = p.steps[st_i];
+        double *F = level_ptr(b, p, st_i);
+        double *Dn = level_ptr(b, p, st_i + 1);
+        Sel4 sel;
+        for (int d = 0; d < 4; d++) sel.s[d] = st.ax[d].active ? st.ax[d].r0 : nullptr;
+        k_gather_coarse<<<rows_grid(st.csh), 256, 0, s>>>(F, st.fsh, b.cg, st.csh, sel);
+        LAUNCH_CHECK();
+        interpolate(st, b.cg, b.mc, F, 1, b, s);                       // mc = sub - pred
+        k_scatter_level<<<rows_grid(st.fsh), 256, 0, s>>>(b.mc, st.fsh, coef, p.dims, level_map(p, st_i),
+                                                          coarse_flags(st), 1);
+        LAUNCH_CHECK();
+        const double *corr = correction(st, b.mc, b, s);
+        int64_t nc = st.csh.size();
+        k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, corr, Dn, nc);   // coarse + corr
+        LAUNCH_CHECK();
+    }
+    // coarsest nodal values to their finest positions
+    Shape4 shL;
+    for (int d = 0; d < 4; d++) shL.n[d] = p.host.cnt[d][L - 1];
+    const double *DL = level_ptr(b, p, L - 1);
+    if (L == 1) {
+        CUDA_CHECK(cudaMemcpyAsync(coef, b.lvl0, N * 8, cudaMemcpyDeviceToDevice, s));
+        return b.lvl0;
+    }
+    Sel4 none{};
+    k_scatter_level<<<rows_grid(shL), 256, 0, s>>>(DL, shL, coef, p.dims, level_map(p, L - 1), none, 0);
+    LAUNCH_CHECK();
+    return DL;
+}
+
+double *recompose_device(hpdr_ctx *ctx, DevPlan &p, const double *coef, cudaStream_t s) {
+    LevelBuffers b = level_buffers(ctx, p);
+    const int L = p.host.L;
+    const int64_t N = p.n_total;
+    if (L == 1) {
+        CUDA_CHECK(cudaMemcpyAsync(b.lvl0, coef, N * 8, cudaMemcpyDeviceToDevice, s));
+        return b.lvl0;
+    }
+    Shape4 shL;
+    for (int d = 0; d < 4; d++) shL.n[d] = p.host.cnt[d][L - 1];
+    Sel4 none{};
+    k_gather_level<<<rows_grid(shL), 256, 0, s>>>(coef, p.dims, level_map(p, L - 1), none, level_ptr(b, p, L - 1),
+                                                  shL, 0);
+    LAUNCH_CHECK();
+    for (int st_i = L - 2; st_i >= 0; st_i--) {
+        const DevStep &st = p.steps[st_i];
+        double *F = level_ptr(b, p, st_i);
+        double *Dc = level_ptr(b, p, st_i + 1);
+        k_gather_level<<<rows_grid(st.fsh), 256, 0, s>>>(coef, p.dims, level_map(p, st_i), coarse_flags(st), b.mc,
+                                                         st.fsh, 1);
+        LAUNCH_CHECK();
+        const double *corr = correction(st, b.mc, b, s);
+        int64_t nc = st.csh.size();
+        k_sub<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(Dc, corr, b.cg, nc);   // coarse - corr
+        LAUNCH_CHECK();
+        interpolate(st, b.cg, F, b.mc, 2, b, s);                                    // pred + mc
+    }
+    return b.lvl0;
+}
+
+void cast_output(const double *src, void *dst, int dtype, int64_t n, cudaStream_t s) {
+    unsigned g = grid_for(n, 256, 148 * 16);
+    switch (dtype) {
+        case 0: k_cast<float><<<g, 256, 0, s>>>(src, (float *)dst, n); break;
+        case 1: CUDA_CHECK(cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToDevice, s)); return;
+        case 2: k_cast<uint32_t><<<g, 256, 0, s>>>(src, (uint32_t *)dst, n); break;
+        case 3: k_cast<uint64_t><<<g, 256, 0, s>>>(src, (uint64_t *)dst, n); break;
+        case 4: k_cast<int32_t><<<g, 256, 0, s>>>(src, (int32_t *)dst, n); break;
+        case 5: k_cast<int64_t><<<g, 256, 0, s>>>(src, (int64_t *)dst, n); break;
+        default: k_cast<uint8_t><<<g, 256, 0, s>>>(src, (uint8_t *)dst, n); break;
+    }
+    LAUNCH_CHECK();
+}
+
+}  // namespace hpdr

@@ -1,0 +1,34 @@
+// transform.cuh -- multilevel decomposition / recomposition on the device.
+#pragma once
+
+#include "context.cuh"
+
+namespace hpdr {
+
+// Work buffers used by one decompose / recompose (owned by the context).
+struct LevelBuffers {
+    double *lvl0;     // finest dense level (N)
+    double *arena;    // coarser dense levels
+    double *mc;       // residual of the current transition
+    double *t0, *t1;  // prolong / restrict intermediates
+    double *cg;       // coarse gather / corrected coarse values
+};
+
+LevelBuffers level_buffers(hpdr_ctx *ctx, DevPlan &p);
+
+// Global min/max of the input (numpy min/max semantics: NaN propagates).
+void minmax_device(hpdr_ctx *ctx, const void *d_in, int dtype, int64_t n, double *vmin, double *vmax,
+                   cudaStream_t s);
+
+// transform.py:287-323.  d_in: device array of dtype (0 = f32, 1 = f64).  coef: N doubles in
+// finest-grid order.  Returns the coarsest dense level (<= 16 values, device).
+const double *decompose_device(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int dtype, double *coef,
+                               cudaStream_t s);
+
+// transform.py:326-348.  coef: N doubles.  Returns the finest dense level (device, N doubles).
+double *recompose_device(hpdr_ctx *ctx, DevPlan &p, const double *coef, cudaStream_t s);
+
+// codec.py:113 values.astype(dtype): cast fp64 to the blob's dtype code.
+void cast_output(const double *src, void *dst, int dtype, int64_t n, cudaStream_t s);
+
+}  // namespace hpdr

@@ -1,0 +1,194 @@
+"""Parity of the CUDA path against the reference (golden vectors from the reference itself)
+and the C oracle, through the public API / C ABI.  Needs a B200: run with -m gpu."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2503_06322_b200 as P
+from paper_2503_06322_b200 import huffman as PH
+from paper_2503_06322_b200 import synthetic as S
+from paper_2503_06322_b200.errors import CorruptStreamError, ValidationError
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def test_small_blobs_match_reference(small_cases):
+    for c in small_cases:
+        vr = tuple(c["value_range"]) if c["value_range"] else None
+        blob = P.mgard_compress(c["input"], c["eb_rel"], c["dict_size"], value_range=vr)
+        assert blob == c["blob"], (c["i"], c["shape"], len(blob), len(c["blob"]))
+
+
+def test_small_decompress_matches_reference(small_cases):
+    for c in small_cases:
+        out = P.mgard_decompress(c["blob"])
+        assert out.values.dtype == c["out"].dtype
+        assert np.array_equal(out.values.view(np.uint8), c["out"].view(np.uint8)), c["i"]
+
+
+def test_decompose_recompose_bit_exact(small_cases):
+    for c in small_cases:
+        cs = P.decompose(c["input"])
+        assert np.array_equal(cs.values.view(np.uint64), c["coef"].view(np.uint64)), c["i"]
+        rec = P.recompose(P.CoefficientSet(c["coef"].shape, c["coef"], [], 0.0, 0.0))
+        assert np.array_equal(rec.view(np.uint64), c["recomp"].view(np.uint64)), c["i"]
+
+
+def test_quantize_dequantize_match_oracle(small_cases, oracle):
+    for c in small_cases[:20]:
+        coef = c["coef"]
+        u_min, u_max = float(c["input"].min()), float(c["input"].max())
+        vr = tuple(c["value_range"]) if c["value_range"] else None
+        q = P.quantize(P.CoefficientSet(coef.shape, coef, [], u_min, u_max), None, c["eb_rel"], c["dict_size"], vr)
+        o = oracle.quantize(coef, u_min, u_max, c["eb_rel"], c["dict_size"], vr)
+        assert np.array_equal(q.keys, o["keys"]), c["i"]
+        assert np.array_equal(q.outlier_idx, o["outlier_idx"]) and np.array_equal(q.outlier_bins, o["outlier_bins"])
+        assert np.array_equal(q.coarse_values.view(np.uint64), o["coarse_values"].view(np.uint64))
+        assert q.bin_width == o["bin_width"] and q.eb_abs == o["eb_abs"]
+        d = P.dequantize(q)
+        ref = np.unique  # noqa: F841
+        back = d.values.reshape(-1)
+        bins = (q.keys.astype(np.int64) >> 1) ^ -(q.keys.astype(np.int64) & 1)
+        exp = bins.astype(np.float64) * q.bin_width
+        exp[q.outlier_idx.astype(np.int64)] = q.outlier_bins.astype(np.float64) * q.bin_width
+        hidx = P.build_hierarchy(coef.shape).coarsest_flat_indices().astype(np.int64)
+        exp[hidx] = q.coarse_values
+        assert np.array_equal(back.view(np.uint64), exp.view(np.uint64)), c["i"]
+
+
+def test_huffman_streams_match_reference(huffman_golden):
+    meta, data = huffman_golden
+    for i, m in enumerate(meta["streams"]):
+        keys = data[f"keys{i}"]
+        s = PH.huffman_compress(keys, m["dict_size"])
+        assert s == data[f"stream{i}"].tobytes(), m["name"]
+        back = PH.huffman_decompress(data[f"stream{i}"].tobytes())
+        assert np.array_equal(back, keys), m["name"]
+        h = PH.histogram(keys, m["dict_size"])
+        assert np.array_equal(h.counts, np.bincount(keys, minlength=m["dict_size"]))
+
+
+def test_corrupt_streams_match_reference(corrupt_cases):
+    for name, c in corrupt_cases.items():
+        blob = bytes.fromhex(c["hex"])
+        if c["ok"]:
+            out = P.mgard_decompress(blob).values
+            assert hashlib.sha256(out.tobytes()).hexdigest() == c["sha"], name
+            continue
+        exc = {"CorruptStreamError": CorruptStreamError, "ValidationError": ValidationError,
+               "OverflowError": OverflowError, "IndexError": IndexError, "ValueError": ValueError}[c["exc"]]
+        with pytest.raises(exc) as ei:
+            P.mgard_decompress(blob)
+        assert type(ei.value) is exc or c["exc"] == "ValueError", (name, type(ei.value))
+        if c["exc"] == "CorruptStreamError":
+            assert ei.value.bit_offset == c["bit_offset"], (name, ei.value.bit_offset)
+
+
+def test_random_shapes_vs_oracle(oracle):
+    rng = np.random.default_rng(11)
+    for t in range(40):
+        rank = int(rng.integers(1, 5))
+        dims = tuple(int(rng.integers(1, {1: 3000, 2: 90, 3: 40, 4: 14}[rank])) for _ in range(rank))
+        dt = np.float32 if t % 2 else np.float64
+        a = (rng.random(dims) * rng.choice([1.0, 1e3, 1e-3])).astype(dt)
+        if t % 5 == 0:
+            a = S.smooth_noise(dims, seed=t, dtype=dt)
+        eb = float(rng.choice([1e-2, 1e-3, 1e-4, 1e-5]))
+        dsz = int(rng.choice([4096, 4096, 256, 65535, 16]))
+        blob = P.mgard_compress(a, eb, dsz)
+        ref = oracle.mgard_compress(a, eb, dsz)
+        assert blob == ref, (dims, dt, eb, dsz)
+        out = P.mgard_decompress(blob).values
+        assert np.array_equal(out.view(np.uint8), oracle.mgard_decompress(blob).view(np.uint8))
+
+
+def test_error_bound_and_abs_api():
+    a = S.grf((65, 66, 67), m=4, seed=3)
+    for e in (1e-1, 1e-3, 3.0):
+        blob = P.compress(a, e, norm="linf", mode="abs")
+        y = P.decompress(blob)
+        assert float(np.max(np.abs(y.astype(np.float64) - a.astype(np.float64)))) <= e
+        assert np.frombuffer(blob[1 + 24 + 29:1 + 24 + 37], "<f8")[0] == e   # stored eb_abs == e exactly
+    blob = P.compress(a, 1e-3, norm="l2", mode="rel")
+    y = P.decompress(blob)
+    rng_ = float(a.max()) - float(a.min())
+    assert float(np.max(np.abs(y.astype(np.float64) - a))) <= 1e-3 * rng_
+
+
+def test_validation_errors():
+    a = np.zeros((8, 8), np.float32)
+    with pytest.raises(ValidationError):
+        P.mgard_compress(a, 1.5)
+    with pytest.raises(ValidationError):
+        P.mgard_compress(a, 1e-3, dict_size=1)
+    with pytest.raises(ValidationError):
+        P.mgard_compress(np.zeros((4, 4), np.int32), 1e-3)
+    b = a.copy()
+    b[3, 3] = np.nan
+    with pytest.raises(ValidationError):
+        P.mgard_compress(b, 1e-3)
+    with pytest.raises(ValidationError):   # bin overflow: tiny range, huge coefficient
+        P.mgard_compress(np.array([0.0, 1e300, 0.0, 1.0], np.float64), 1e-3, value_range=(0.0, 1e-300))
+    with pytest.raises(ValidationError):
+        PH.histogram(np.array([5], np.uint32), 4)
+
+
+def test_context_cache_no_realloc():
+    cache = P.ContextCache()
+    a = S.smooth_noise((33, 34, 35), seed=1)
+    b1 = P.mgard_compress(a, 1e-3, cache=cache)
+    ev = cache.total_alloc_events
+    for _ in range(5):
+        assert P.mgard_compress(a, 1e-3, cache=cache) == b1
+    assert cache.total_alloc_events == ev
+    P.mgard_compress(a, 1e-4, cache=cache)
+    assert len(cache) == 2
+
+
+def test_device_buffers_in_place():
+    torch = pytest.importorskip("torch")
+    a = S.smooth_noise((40, 41, 42), seed=2)
+    ref = P.mgard_compress(a, 1e-4)
+    t = torch.from_numpy(a).cuda()
+    assert P.mgard_compress(t, 1e-4) == ref
+    pin = torch.from_numpy(a).pin_memory()
+    assert P.mgard_compress(pin, 1e-4) == ref
+    out = torch.empty(a.shape, dtype=torch.float32, device="cuda")
+    P.mgard_decompress(ref, out=out)
+    assert np.array_equal(out.cpu().numpy(), P.decompress(ref))
+
+
+def test_config_c1_matches_reference_hash():
+    cfg = json.load(open(os.path.join(GOLDEN, "configs.json")))["C1_grf129_abs1e-3"]
+    a = S.grf((129,) * 3, m=8, seed=0)
+    assert S.sha256(a) == cfg["input_sha"], "input generator differs on this host"
+    blob = P.mgard_compress(a, 1e-3, value_range=(0.0, 1.0))
+    assert hashlib.sha256(blob).hexdigest() == cfg["blob_sha"]
+    out = P.mgard_decompress(blob).values
+    assert S.sha256(out) == cfg["out_sha"]
+
+
+@pytest.mark.slow
+def test_config_c2_c3_c4_match_reference_hash():
+    cfg = json.load(open(os.path.join(GOLDEN, "configs.json")))
+    cases = [("C2_smooth513_rel1e-4", lambda: S.smooth_noise((513,) * 3, seed=0))]
+    for f in S.NYX_FIELDS[:3] + ("velocity_x",):
+        for eb in ("0.01", "1e-05"):
+            cases.append((f"C3_{f}_129_{eb}", lambda f=f: S.nyx_like((129,) * 3, f)))
+    cases.append(("C3_temperature_512_1e-3", lambda: S.nyx_like((512,) * 3, "temperature")))
+    for name, gen in cases:
+        if name not in cfg:
+            continue
+        c = cfg[name]
+        a = gen()
+        assert S.sha256(a) == c["input_sha"], name
+        vr = tuple(c["value_range"]) if c["value_range"] else None
+        blob = P.mgard_compress(a, c["eb_rel"], value_range=vr)
+        assert len(blob) == c["blob_len"] and hashlib.sha256(blob).hexdigest() == c["blob_sha"], name
+        out = P.mgard_decompress(blob).values
+        assert S.sha256(out) == c["out_sha"], name
