@@ -110,6 +110,13 @@ int hpdr_huffman_decompress(hpdr_ctx *ctx, const void *in, uint64_t len, uint32_
 
 /* Kernel launches issued by this thread since the last reset (bench accounting). */
 uint64_t hpdr_launch_count(int reset);
+/* Live per-kernel CUDA-event timing with algorithmic bytes (bench roofline).  Enabling
+ * clears previous records; hpdr_prof_read writes {"kernel": [launches, total_ms,
+ * total_bytes, max_ms], ...} as JSON and clears. */
+void     hpdr_prof_enable(int on);
+int      hpdr_prof_read(char *json, uint64_t cap);
+/* The context's compute stream (cudaStream_t) for external event timing. */
+void    *hpdr_ctx_stream(const hpdr_ctx *ctx);
 
 #ifdef __cplusplus
 }

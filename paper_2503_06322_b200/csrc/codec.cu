@@ -304,8 +304,11 @@ int scatter_outliers(hpdr_ctx *ctx, double *coef, int64_t n, const uint64_t *h_i
     CUDA_CHECK(cudaMemcpyAsync(di, h_idx, n_out * 8, cudaMemcpyDefault, s));
     CUDA_CHECK(cudaMemcpyAsync(db, h_bins, n_out * 8, cudaMemcpyDefault, s));
     CUDA_CHECK(cudaMemsetAsync(fl, 0, 16, s));
-    k_outliers<<<grid_for(n_out, 256, 148 * 8), 256, 0, s>>>(coef, n, di, db, n_out, bin_width, fl);
-    LAUNCH_CHECK();
+    {
+        KPROF("k_outliers", 24.0 * n_out, s);
+        k_outliers<<<grid_for(n_out, 256, 148 * 8), 256, 0, s>>>(coef, n, di, db, n_out, bin_width, fl);
+        LAUNCH_CHECK();
+    }
     int *h = (int *)ctx->hbuf("dq_flags_h", 16);
     CUDA_CHECK(cudaMemcpyAsync(h, fl, 4, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
@@ -582,8 +585,11 @@ int hpdr_dequantize(hpdr_ctx *ctx, const uint32_t *keys_in, uint64_t n_keys, int
         double *coef = classify(coef_out) == MemKind::Device ? coef_out : (double *)ctx->dbuf("coef", N * 8);
         unsigned *kmax = (unsigned *)ctx->dbuf("dq_kmax", 16);
         CUDA_CHECK(cudaMemsetAsync(kmax, 0, 16, s));
-        k_dequant<<<grid_for(N, 256, 148 * 16), 256, 0, s>>>(keys, N, bin_width, coef, kmax);
-        LAUNCH_CHECK();
+        {
+            KPROF("k_dequant", 12.0 * N, s);
+            k_dequant<<<grid_for(N, 256, 148 * 16), 256, 0, s>>>(keys, N, bin_width, coef, kmax);
+            LAUNCH_CHECK();
+        }
         unsigned *hk = (unsigned *)ctx->hbuf("dq_kmax_h", 16);
         CUDA_CHECK(cudaMemcpyAsync(hk, kmax, 4, cudaMemcpyDeviceToHost, s));
         CUDA_CHECK(cudaStreamSynchronize(s));

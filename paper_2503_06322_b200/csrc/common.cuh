@@ -22,6 +22,16 @@ constexpr int kNumSMs = 148;
 void set_error(int code, const std::string &msg, int64_t bit_offset = -1);
 void count_launch();
 
+// Live per-kernel timing for bench.py: when enabled (hpdr_prof_enable), each scope records a
+// CUDA event pair on the launching stream plus the launch's algorithmic bytes.
+struct ProfScope {
+    ProfScope(const char *name, double bytes, cudaStream_t s);
+    ~ProfScope();
+    int slot;
+    cudaStream_t stream;
+};
+#define KPROF(name, bytes, stream) ::hpdr::ProfScope prof_scope_(name, (double)(bytes), stream)
+
 #define HPDR_THROW(code, msg) throw ::hpdr::Error{(code), (msg), -1}
 #define CUDA_CHECK(x)                                                                      \
     do {                                                                                   \

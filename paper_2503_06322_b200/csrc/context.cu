@@ -2,6 +2,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "context.cuh"
 
@@ -18,6 +19,40 @@ void set_error(int code, const std::string &msg, int64_t bit_offset) {
 }
 
 void count_launch() { tl_launches++; }
+
+// ---- live kernel profiling ----
+namespace {
+struct ProfRec {
+    const char *name;
+    double bytes;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_pool;
+size_t g_prof_used = 0;
+}  // namespace
+
+ProfScope::ProfScope(const char *name, double bytes, cudaStream_t s) : slot(-1), stream(s) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    if (g_prof_used == g_prof_pool.size()) {
+        cudaEvent_t a, b;
+        if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) { cudaGetLastError(); return; }
+        g_prof_pool.push_back({a, b});
+    }
+    auto ev = g_prof_pool[g_prof_used++];
+    g_prof.push_back(ProfRec{name, bytes, ev.first, ev.second});
+    slot = (int)g_prof.size() - 1;
+    cudaEventRecord(ev.first, s);
+}
+
+ProfScope::~ProfScope() {
+    if (slot < 0) return;
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    if (slot < (int)g_prof.size()) cudaEventRecord(g_prof[slot].b, stream);
+}
 
 MemKind classify(const void *p) {
     cudaPointerAttributes a;
@@ -212,6 +247,46 @@ uint64_t hpdr_launch_count(int reset) {
     if (reset) tl_launches = 0;
     return v;
 }
+
+void hpdr_prof_enable(int on) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    g_prof_on = on != 0;
+    g_prof.clear();
+    g_prof_used = 0;
+}
+
+// Per-kernel aggregate since the last enable/read as JSON:
+// {"kernel": [launches, total_ms, total_algorithmic_bytes, max_ms], ...}
+int hpdr_prof_read(char *buf, uint64_t cap) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    std::map<std::string, std::vector<double>> agg;
+    for (auto &r : g_prof) {
+        cudaEventSynchronize(r.b);
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) { cudaGetLastError(); ms = 0.f; }
+        auto &v = agg[r.name];
+        if (v.empty()) v.assign(4, 0.0);
+        v[0] += 1;
+        v[1] += ms;
+        v[2] += r.bytes;
+        v[3] = std::max(v[3], (double)ms);
+    }
+    std::string s = "{";
+    for (auto &kv : agg) {
+        char tmp[256];
+        snprintf(tmp, sizeof(tmp), "%s\"%s\": [%.0f, %.6f, %.0f, %.6f]", s.size() > 1 ? ", " : "", kv.first.c_str(),
+                 kv.second[0], kv.second[1], kv.second[2], kv.second[3]);
+        s += tmp;
+    }
+    s += "}";
+    g_prof.clear();
+    g_prof_used = 0;
+    if (s.size() + 1 > cap) return HPDR_ERR_BUFFER;
+    memcpy(buf, s.c_str(), s.size() + 1);
+    return HPDR_OK;
+}
+
+void *hpdr_ctx_stream(const hpdr_ctx *c) { return c ? (void *)c->stream : nullptr; }
 
 int hpdr_ctx_create(int device, hpdr_ctx **out) {
     try {

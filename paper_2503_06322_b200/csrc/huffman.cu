@@ -207,8 +207,12 @@ void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict
     uint64_t *uoff = (uint64_t *)ctx->dbuf("enc_uoff", (units + 1) * 8);
     CUDA_CHECK(cudaMemcpyAsync(d_len, lengths, dict_size, cudaMemcpyHostToDevice, s));
     CUDA_CHECK(cudaMemcpyAsync(d_code, codes, (size_t)dict_size * 4, cudaMemcpyHostToDevice, s));
-    k_unit_bits<<<(unsigned)std::min<int64_t>(units, 148 * 16), kEncThreads, 0, s>>>(keys, n, d_len, dict_size, ubits, units);
-    LAUNCH_CHECK();
+    {
+        KPROF("k_unit_bits", 4.0 * n + 8.0 * units, s);
+        k_unit_bits<<<(unsigned)std::min<int64_t>(units, 148 * 16), kEncThreads, 0, s>>>(keys, n, d_len, dict_size, ubits,
+                                                                                          units);
+        LAUNCH_CHECK();
+    }
     CUDA_CHECK(cudaMemsetAsync(ubits + units, 0, 8, s));
     size_t tb = 0;
     CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, ubits, uoff, (int)(units + 1), s));
@@ -222,6 +226,7 @@ void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict
     const size_t words = (size_t)((res.total_bits + 31) / 32) + 2;
     res.d_words = (uint32_t *)ctx->dbuf("enc_words", words * 4);
     CUDA_CHECK(cudaMemsetAsync(res.d_words, 0, words * 4, s));
+    KPROF("k_encode", 4.0 * n + 16.0 * units + res.total_bits / 8.0, s);
     k_encode<<<(unsigned)std::min<int64_t>(units, 148 * 8), kEncThreads, 0, s>>>(keys, n, d_len, d_code, dict_size, uoff,
                                                                                   ubits, res.d_words, units);
     LAUNCH_CHECK();
@@ -400,6 +405,8 @@ void decode_device(hpdr_ctx *ctx, const DecodeJob &job, DecodeResult &res, cudaS
     memcpy(hinit, init, 16);
     CUDA_CHECK(cudaMemcpyAsync(flag, hinit, 16, cudaMemcpyHostToDevice, s));
     if (units > 0) {
+        KPROF("k_decode", job.total_bits / 8.0 + 8.0 * units +
+                              (double)job.n_symbols * ((job.keys ? 4 : 0) + (job.coef ? 8 : 0)), s);
         k_decode<<<grid_for(units, 64, 148 * 64), 64, 0, s>>>(
             d_words, job.total_bits, d_off, job.n_symbols, units, (const DecTables *)d_tab,
             (const uint32_t *)(d_tab + sizeof(DecTables)),

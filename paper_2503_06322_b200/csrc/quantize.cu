@@ -165,10 +165,16 @@ void quantize_device(hpdr_ctx *ctx, const double *coef, int64_t n, const std::ve
     size_t smem = dict_size <= kSmemHistMax ? (size_t)dict_size * 4 : 0;
     if (smem > 48 * 1024) CUDA_CHECK(cudaFuncSetAttribute(k_quantize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     unsigned grid = grid_for(n, kQThreads, 148 * 4);
-    k_quantize<<<grid, kQThreads, smem, s>>>(coef, n, co, bin_width, half, dict_size, keys, omask, hist, flags);
-    LAUNCH_CHECK();
-    k_chunk_counts<<<(unsigned)chunks, 256, 0, s>>>(omask, words, ccount);
-    LAUNCH_CHECK();
+    {
+        KPROF("k_quantize", 12.0 * n + n / 8.0, s);
+        k_quantize<<<grid, kQThreads, smem, s>>>(coef, n, co, bin_width, half, dict_size, keys, omask, hist, flags);
+        LAUNCH_CHECK();
+    }
+    {
+        KPROF("k_chunk_counts", 4.0 * words, s);
+        k_chunk_counts<<<(unsigned)chunks, 256, 0, s>>>(omask, words, ccount);
+        LAUNCH_CHECK();
+    }
     size_t tmp_bytes = 0;
     CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, ccount, coff, (int)(chunks + 1), s));
     void *tmp = ctx->dbuf("cub_tmp", tmp_bytes);
@@ -189,6 +195,7 @@ void quantize_device(hpdr_ctx *ctx, const double *coef, int64_t n, const std::ve
     res.d_outlier_idx = (uint64_t *)ctx->dbuf("oidx", res.n_outliers * 8);
     res.d_outlier_bins = (int64_t *)ctx->dbuf("obins", res.n_outliers * 8);
     if (res.n_outliers) {
+        KPROF("k_write_outliers", 4.0 * words + 24.0 * res.n_outliers, s);
         k_write_outliers<<<(unsigned)chunks, 256, 0, s>>>(omask, words, coef, bin_width, coff, res.d_outlier_idx,
                                                           res.d_outlier_bins);
         LAUNCH_CHECK();
@@ -204,6 +211,7 @@ void histogram_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t d
     size_t smem = dict_size <= kSmemHistMax ? (size_t)dict_size * 4 : 0;
     if (smem > 48 * 1024) CUDA_CHECK(cudaFuncSetAttribute(k_histogram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (n > 0) {
+        KPROF("k_histogram", 4.0 * n, s);
         k_histogram<<<grid_for(n, 256, 148 * 4), 256, smem, s>>>(keys, n, dict_size, d, flags);
         LAUNCH_CHECK();
     }

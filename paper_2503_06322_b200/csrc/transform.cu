@@ -332,7 +332,8 @@ void prolong(const double *src, double *dst, const double *aux, int mode, const 
     const int64_t per = (int64_t)ax.n * inner;
     dim3 grid(grid_for(per, 256, 4096), (unsigned)std::min<int64_t>(outer, 65535));
     const bool small = per < (1LL << 32);
-#define PL(M)                                                                                                   \
+    KPROF("k_prolong", 8.0 * outer * ((double)ax.nc * inner + (mode ? 2.0 : 1.0) * per), s);
+#define PL(M)                                                                                                \
     if (small)                                                                                                  \
         k_prolong<M, uint32_t><<<grid, 256, 0, s>>>(src, dst, aux, outer, ax.nc, ax.n, inner, ax.pa, ax.pb, ax.pt); \
     else                                                                                                        \
@@ -349,6 +350,7 @@ void mass_restrict(const double *src, double *dst, const Shape4 &fsh, int a, con
     view(fsh, a, outer, inner);
     const int64_t per = (int64_t)ax.nc * inner;
     dim3 grid(grid_for(per, 256, 4096), (unsigned)std::min<int64_t>(outer, 65535));
+    KPROF("k_mass_restrict", 8.0 * outer * ((double)ax.n * inner + per), s);
     if (per < (1LL << 32))
         k_mass_restrict<uint32_t><<<grid, 256, 0, s>>>(src, dst, outer, ax.n, ax.nc, inner, ax);
     else
@@ -359,6 +361,7 @@ void mass_restrict(const double *src, double *dst, const Shape4 &fsh, int a, con
 void thomas(double *arr, const Shape4 &csh, int a, const DevAxis &ax, cudaStream_t s) {
     int64_t outer, inner;
     view(csh, a, outer, inner);
+    KPROF(inner == 1 ? "k_thomas_contig" : "k_thomas_strided", 16.0 * outer * inner * ax.nc, s);
     if (inner == 1) {
         int64_t lines = outer;
         unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((lines + 127) / 128, 148 * 16));
@@ -442,8 +445,11 @@ void minmax_device(hpdr_ctx *ctx, const void *d_in, int dtype, int64_t n, double
     unsigned long long *h = (unsigned long long *)ctx->hbuf("minmax_h", 32);
     unsigned long long init[3] = {~0ULL, 0ULL, 0ULL};
     CUDA_CHECK(cudaMemcpyAsync(d, init, 24, cudaMemcpyHostToDevice, s));
-    k_minmax<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(d_in, dtype, n, d);
-    LAUNCH_CHECK();
+    {
+        KPROF("k_minmax", (double)n * (dtype == 0 ? 4 : 8), s);
+        k_minmax<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(d_in, dtype, n, d);
+        LAUNCH_CHECK();
+    }
     CUDA_CHECK(cudaMemcpyAsync(h, d, 24, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
     if (h[2]) {
@@ -465,24 +471,36 @@ const double *decompose_device(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int 
     LevelBuffers b = level_buffers(ctx, p);
     const int64_t N = p.n_total;
     const int L = p.host.L;
-    k_to_f64<<<grid_for(N, 256, 148 * 16), 256, 0, s>>>(d_in, dtype, b.lvl0, N);
-    LAUNCH_CHECK();
+    {
+        KPROF("k_to_f64", (double)N * (dtype == 0 ? 12 : 16), s);
+        k_to_f64<<<grid_for(N, 256, 148 * 16), 256, 0, s>>>(d_in, dtype, b.lvl0, N);
+        LAUNCH_CHECK();
+    }
     for (int st_i = 0; st_i + 1 < L; st_i++) {
         const DevStep &st = p.steps[st_i];
         double *F = level_ptr(b, p, st_i);
         double *Dn = level_ptr(b, p, st_i + 1);
         Sel4 sel;
         for (int d = 0; d < 4; d++) sel.s[d] = st.ax[d].active ? st.ax[d].r0 : nullptr;
-        k_gather_coarse<<<rows_grid(st.csh), 256, 0, s>>>(F, st.fsh, b.cg, st.csh, sel);
-        LAUNCH_CHECK();
+        const int64_t nf = st.fsh.size(), nc = st.csh.size();
+        {
+            KPROF("k_gather_coarse", 16.0 * nc, s);
+            k_gather_coarse<<<rows_grid(st.csh), 256, 0, s>>>(F, st.fsh, b.cg, st.csh, sel);
+            LAUNCH_CHECK();
+        }
         interpolate(st, b.cg, b.mc, F, 1, b, s);                       // mc = sub - pred
-        k_scatter_level<<<rows_grid(st.fsh), 256, 0, s>>>(b.mc, st.fsh, coef, p.dims, level_map(p, st_i),
-                                                          coarse_flags(st), 1);
-        LAUNCH_CHECK();
+        {
+            KPROF("k_scatter_level", 8.0 * nf + 8.0 * (nf - nc), s);
+            k_scatter_level<<<rows_grid(st.fsh), 256, 0, s>>>(b.mc, st.fsh, coef, p.dims, level_map(p, st_i),
+                                                              coarse_flags(st), 1);
+            LAUNCH_CHECK();
+        }
         const double *corr = correction(st, b.mc, b, s);
-        int64_t nc = st.csh.size();
-        k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, corr, Dn, nc);   // coarse + corr
-        LAUNCH_CHECK();
+        {
+            KPROF("k_add", 24.0 * nc, s);
+            k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, corr, Dn, nc);   // coarse + corr
+            LAUNCH_CHECK();
+        }
     }
     // coarsest nodal values to their finest positions
     Shape4 shL;
@@ -516,13 +534,19 @@ double *recompose_device(hpdr_ctx *ctx, DevPlan &p, const double *coef, cudaStre
         const DevStep &st = p.steps[st_i];
         double *F = level_ptr(b, p, st_i);
         double *Dc = level_ptr(b, p, st_i + 1);
-        k_gather_level<<<rows_grid(st.fsh), 256, 0, s>>>(coef, p.dims, level_map(p, st_i), coarse_flags(st), b.mc,
-                                                         st.fsh, 1);
-        LAUNCH_CHECK();
+        const int64_t nf = st.fsh.size(), nc = st.csh.size();
+        {
+            KPROF("k_gather_level", 8.0 * (nf - nc) + 8.0 * nf, s);
+            k_gather_level<<<rows_grid(st.fsh), 256, 0, s>>>(coef, p.dims, level_map(p, st_i), coarse_flags(st), b.mc,
+                                                             st.fsh, 1);
+            LAUNCH_CHECK();
+        }
         const double *corr = correction(st, b.mc, b, s);
-        int64_t nc = st.csh.size();
-        k_sub<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(Dc, corr, b.cg, nc);   // coarse - corr
-        LAUNCH_CHECK();
+        {
+            KPROF("k_sub", 24.0 * nc, s);
+            k_sub<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(Dc, corr, b.cg, nc);   // coarse - corr
+            LAUNCH_CHECK();
+        }
         interpolate(st, b.cg, F, b.mc, 2, b, s);                                    // pred + mc
     }
     return b.lvl0;
@@ -530,6 +554,8 @@ double *recompose_device(hpdr_ctx *ctx, DevPlan &p, const double *coef, cudaStre
 
 void cast_output(const double *src, void *dst, int dtype, int64_t n, cudaStream_t s) {
     unsigned g = grid_for(n, 256, 148 * 16);
+    static const int isz[7] = {4, 8, 4, 8, 4, 8, 1};
+    KPROF("k_cast", (double)n * (8 + isz[dtype < 0 || dtype > 6 ? 6 : dtype]), s);
     switch (dtype) {
         case 0: k_cast<float><<<g, 256, 0, s>>>(src, (float *)dst, n); break;
         case 1: CUDA_CHECK(cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToDevice, s)); return;
