@@ -76,6 +76,10 @@ int hpdr_mgard_peek(const void *blob, uint64_t len, int *dtype, int *rank, uint6
  * blob's dtype (host or device pointer). */
 int hpdr_mgard_decompress(hpdr_ctx *ctx, const void *blob, uint64_t len, void *out, uint64_t out_bytes);
 
+/* Global min/max of a field (transform.py:304-305 u.values.min()/max(); NaN propagates).
+ * Used to agree on one value_range across slabs / ranks before quantization. */
+int hpdr_minmax(hpdr_ctx *ctx, const void *in, int dtype, uint64_t n, double *vmin, double *vmax);
+
 /* ---- stage entry points (for parity tests; each mirrors one reference function) ---- */
 
 /* decompose (transform.py:287-323): fp64 coefficients in finest-grid order. */

@@ -49,6 +49,10 @@ _SIGS = {
     "hpdr_huffman_fetch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "hpdr_huffman_decompress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, _u64p]),
     "hpdr_launch_count": (C.c_uint64, [C.c_int]),
+    "hpdr_prof_enable": (None, [C.c_int]),
+    "hpdr_prof_read": (C.c_int, [C.c_char_p, C.c_uint64]),
+    "hpdr_ctx_stream": (C.c_void_p, [C.c_void_p]),
+    "hpdr_minmax": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, _dp, _dp]),
 }
 
 _lib = None
@@ -131,6 +135,11 @@ class DeviceContext:
     def trim(self):
         lib().hpdr_ctx_trim(self.handle)
 
+    @property
+    def stream(self) -> int:
+        """cudaStream_t of the context's compute stream (for external event timing)."""
+        return int(lib().hpdr_ctx_stream(self.handle) or 0)
+
     def close(self):
         if self._h is not None and _lib is not None:
             _lib.hpdr_ctx_destroy(self._h)
@@ -179,3 +188,22 @@ def new_bytes(n: int):
 
 def launch_count(reset: bool = False) -> int:
     return int(lib().hpdr_launch_count(1 if reset else 0))
+
+
+def prof_enable(on: bool = True):
+    lib().hpdr_prof_enable(1 if on else 0)
+
+
+def prof_read() -> dict:
+    """{kernel: (launches, total_ms, total_algorithmic_bytes, max_ms)} since prof_enable."""
+    import json
+
+    buf = C.create_string_buffer(1 << 16)
+    check(lib().hpdr_prof_read(buf, len(buf)))
+    return {k: tuple(v) for k, v in json.loads(buf.value.decode()).items()}
+
+
+def minmax(ctx: "DeviceContext", addr: int, dtype_code: int, n: int):
+    lo, hi = C.c_double(), C.c_double()
+    check(lib().hpdr_minmax(ctx.handle, C.c_void_p(addr), int(dtype_code), int(n), C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value

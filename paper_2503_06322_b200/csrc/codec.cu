@@ -505,6 +505,16 @@ int hpdr_mgard_decompress(hpdr_ctx *ctx, const void *blob_in, uint64_t len, void
     });
 }
 
+int hpdr_minmax(hpdr_ctx *ctx, const void *in, int dtype, uint64_t n, double *vmin, double *vmax) {
+    return guard([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (dtype != 0 && dtype != 1) fail(HPDR_ERR_VALIDATION, "min/max needs F32/F64");
+        cudaStream_t s = ctx->stream;
+        const void *d_in = device_input(ctx, in, (size_t)n * itemsize(dtype), "input", s);
+        minmax_device(ctx, d_in, dtype, (int64_t)n, vmin, vmax, s);
+    });
+}
+
 // ------------------------------------------------------------------ stage entry points
 int hpdr_decompose(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, double *coef_out,
                    double *u_min, double *u_max) {
