@@ -490,15 +490,14 @@ int hpdr_mgard_decompress(hpdr_ctx *ctx, const void *blob_in, uint64_t len, void
                                   (const int64_t *)(blob + obins_off), n_out, bin, s);
         if (rc == HPDR_ERR_INDEX) fail(rc, "outlier index out of bounds for axis 0 with size " + std::to_string(N));
         restore_coarse(ctx, coef, p, coarse.data(), n_co, s);
-        const double *rec = recompose_device(ctx, p, coef, s);
-        // codec.py:113 TensorData(dims, dtype, values.astype(dtype))
+        // codec.py:112-113 recompose, then TensorData(dims, dtype, values.astype(dtype))
         const size_t ob = (size_t)N * itemsize(dtype);
         if (out_bytes < ob) fail(HPDR_ERR_BUFFER, "output buffer too small: need " + std::to_string(ob));
         if (classify(out) == MemKind::Device) {
-            cast_output(rec, out, dtype, (int64_t)N, s);
+            recompose_into(ctx, p, coef, out, dtype, s);
         } else {
             void *stage = ctx->dbuf("out_stage", ob);
-            cast_output(rec, stage, dtype, (int64_t)N, s);
+            recompose_into(ctx, p, coef, stage, dtype, s);
             CUDA_CHECK(cudaMemcpyAsync(out, stage, ob, cudaMemcpyDeviceToHost, s));
         }
         CUDA_CHECK(cudaStreamSynchronize(s));
@@ -540,8 +539,9 @@ int hpdr_recompose(hpdr_ctx *ctx, const double *coef_in, int rank, const uint64_
         cudaStream_t s = ctx->stream;
         const int64_t N = p.n_total;
         const double *coef = (const double *)device_input(ctx, coef_in, N * 8, "coef", s);
-        const double *rec = recompose_device(ctx, p, coef, s);
-        CUDA_CHECK(cudaMemcpyAsync(out, rec, N * 8, cudaMemcpyDefault, s));
+        double *rec = classify(out) == MemKind::Device ? out : (double *)ctx->dbuf("out_stage", N * 8);
+        recompose_into(ctx, p, coef, rec, 1, s);
+        if (rec != out) CUDA_CHECK(cudaMemcpyAsync(out, rec, N * 8, cudaMemcpyDeviceToHost, s));
         CUDA_CHECK(cudaStreamSynchronize(s));
     });
 }

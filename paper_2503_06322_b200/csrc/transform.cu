@@ -6,6 +6,10 @@
 // -fmad=false).  See SURVEY Appendix B and transform.py:158-245.
 #include "transform.cuh"
 
+#include <stdlib.h>
+
+#include "fused.cuh"
+
 namespace hpdr {
 
 namespace {
@@ -467,10 +471,52 @@ void minmax_device(hpdr_ctx *ctx, const void *d_in, int dtype, int64_t n, double
     *vmax = val(h[1]);
 }
 
+bool use_fused(const DevPlan &p) {
+    static const bool generic = getenv("HPDR_GENERIC") != nullptr && getenv("HPDR_GENERIC")[0] == '1';
+    return fused_supported(p) && !generic;
+}
+
+namespace {
+
+// Fused decomposition (ranks <= 3): pass 1 (GPK residual + coefficients + axis-0 LPK), pass 2
+// (axis-1/2 LPK), IPK Thomas sweeps, coarse + corr.
+const double *decompose_fused(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int dtype, double *coef, cudaStream_t s) {
+    LevelBuffers b = level_buffers(ctx, p);
+    const int L = p.host.L;
+    double *Z0 = (double *)ctx->dbuf("z0", p.n_total * 8);
+    for (int st_i = 0; st_i + 1 < L; st_i++) {
+        const DevStep &st = p.steps[st_i];
+        const void *F = st_i == 0 ? d_in : (const void *)level_ptr(b, p, st_i);
+        double *Dn = level_ptr(b, p, st_i + 1);
+        fused_pass1_decompose(p, st_i, F, st_i == 0 && dtype == 0, coef, Z0, b.cg, s);
+        fused_pass2(p, st_i, Z0, b.t0, s);
+        Shape4 sh = st.csh;
+        for (int a = 0; a < 4; a++)
+            if (st.ax[a].active) thomas(b.t0, sh, a, st.ax[a], s);
+        const int64_t nc = st.csh.size();
+        KPROF("k_add", 24.0 * nc, s);
+        k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, Dn, nc);   // coarse + corr
+        LAUNCH_CHECK();
+    }
+    return nullptr;
+}
+
+}  // namespace
+
 const double *decompose_device(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int dtype, double *coef, cudaStream_t s) {
     LevelBuffers b = level_buffers(ctx, p);
     const int64_t N = p.n_total;
     const int L = p.host.L;
+    if (L > 1 && use_fused(p)) {
+        decompose_fused(ctx, p, d_in, dtype, coef, s);
+        Shape4 shL;
+        for (int d = 0; d < 4; d++) shL.n[d] = p.host.cnt[d][L - 1];
+        const double *DL = level_ptr(b, p, L - 1);
+        Sel4 none{};
+        k_scatter_level<<<rows_grid(shL), 256, 0, s>>>(DL, shL, coef, p.dims, level_map(p, L - 1), none, 0);
+        LAUNCH_CHECK();
+        return DL;
+    }
     {
         KPROF("k_to_f64", (double)N * (dtype == 0 ? 12 : 16), s);
         k_to_f64<<<grid_for(N, 256, 148 * 16), 256, 0, s>>>(d_in, dtype, b.lvl0, N);
@@ -550,6 +596,42 @@ double *recompose_device(hpdr_ctx *ctx, DevPlan &p, const double *coef, cudaStre
         interpolate(st, b.cg, F, b.mc, 2, b, s);                                    // pred + mc
     }
     return b.lvl0;
+}
+
+void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s) {
+    const int L = p.host.L;
+    if (L == 1 || !use_fused(p)) {
+        const double *rec = recompose_device(ctx, p, coef, s);
+        cast_output(rec, out, out_dtype, p.n_total, s);
+        return;
+    }
+    LevelBuffers b = level_buffers(ctx, p);
+    double *Z0 = (double *)ctx->dbuf("z0", p.n_total * 8);
+    Shape4 shL;
+    for (int d = 0; d < 4; d++) shL.n[d] = p.host.cnt[d][L - 1];
+    Sel4 none{};
+    k_gather_level<<<rows_grid(shL), 256, 0, s>>>(coef, p.dims, level_map(p, L - 1), none, level_ptr(b, p, L - 1),
+                                                  shL, 0);
+    LAUNCH_CHECK();
+    const bool direct = out_dtype == 0 || out_dtype == 1;
+    for (int st_i = L - 2; st_i >= 0; st_i--) {
+        const DevStep &st = p.steps[st_i];
+        double *Dc = level_ptr(b, p, st_i + 1);
+        fused_pass1_recompose(p, st_i, coef, Z0, s);
+        fused_pass2(p, st_i, Z0, b.t0, s);
+        Shape4 sh = st.csh;
+        for (int a = 0; a < 4; a++)
+            if (st.ax[a].active) thomas(b.t0, sh, a, st.ax[a], s);
+        const int64_t nc = st.csh.size();
+        {
+            KPROF("k_sub", 24.0 * nc, s);
+            k_sub<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(Dc, b.t0, b.cg, nc);   // coarse - corr
+            LAUNCH_CHECK();
+        }
+        if (st_i == 0 && direct) fused_final(p, st_i, b.cg, coef, out, out_dtype, s);
+        else fused_final(p, st_i, b.cg, coef, level_ptr(b, p, st_i), 1, s);
+    }
+    if (!direct) cast_output(b.lvl0, out, out_dtype, p.n_total, s);
 }
 
 void cast_output(const double *src, void *dst, int dtype, int64_t n, cudaStream_t s) {

@@ -28,6 +28,12 @@ const double *decompose_device(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int 
 // transform.py:326-348.  coef: N doubles.  Returns the finest dense level (device, N doubles).
 double *recompose_device(hpdr_ctx *ctx, DevPlan &p, const double *coef, cudaStream_t s);
 
+// Recompose straight into out (device) in the blob's dtype (fused final level for ranks <= 3).
+void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s);
+
+// True when the fused level kernels serve these dims (ranks <= 3) and HPDR_GENERIC != 1.
+bool use_fused(const DevPlan &p);
+
 // codec.py:113 values.astype(dtype): cast fp64 to the blob's dtype code.
 void cast_output(const double *src, void *dst, int dtype, int64_t n, cudaStream_t s);
 
