@@ -14,6 +14,7 @@
 
 #include "stages.cuh"
 #include "transform.cuh"
+#include "fused.cuh"
 
 namespace hpdr {
 
@@ -351,11 +352,31 @@ int hpdr_mgard_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, cons
         }
         const double eb_abs = eb_rel * (u_max - u_min);
         const double bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
-        double *coef = (double *)ctx->dbuf("coef", N * 8);
-        const double *d_coarse = decompose_device(ctx, p, d_in, dtype, coef, s);
         uint32_t *keys = (uint32_t *)ctx->dbuf("keys", N * 4 + 64);
         QuantResult q;
-        quantize_device(ctx, coef, N, p.host.coarsest, bin, dict_size, keys, q, s);
+        const double *d_coarse;
+        if (L > 1 && use_fused(p)) {
+            // quantize-on-write: keys, outlier mask and histogram come out of the level kernels
+            QuantOut qo;
+            qo.bin = bin;
+            qo.half = dict_size / 2;
+            qo.dict = dict_size;
+            qo.keys = keys;
+            const int64_t words = (N + 31) / 32;
+            qo.omask = (uint32_t *)ctx->dbuf("omask", words * 4);
+            qo.obins = (long long *)ctx->dbuf("obins_sparse", N * 8);
+            qo.hist = (unsigned long long *)ctx->dbuf("hist", (size_t)dict_size * 8);
+            qo.flags = (int *)ctx->dbuf("qflags", 16);
+            CUDA_CHECK(cudaMemsetAsync(qo.omask, 0, words * 4, s));
+            CUDA_CHECK(cudaMemsetAsync(qo.hist, 0, (size_t)dict_size * 8, s));
+            CUDA_CHECK(cudaMemsetAsync(qo.flags, 0, 16, s));
+            d_coarse = decompose_quantize(ctx, p, d_in, dtype, qo, s);
+            quantize_finish(ctx, N, dict_size, bin, nullptr, qo.obins, q, s);
+        } else {
+            double *coef = (double *)ctx->dbuf("coef", N * 8);
+            d_coarse = decompose_device(ctx, p, d_in, dtype, coef, s);
+            quantize_device(ctx, coef, N, p.host.coarsest, bin, dict_size, keys, q, s);
+        }
         if (q.flags & 1) fail(HPDR_ERR_VALIDATION, "coefficients contain non-finite values");
         if (q.flags & 2) fail(HPDR_ERR_VALIDATION, "coefficient exceeds representable bin range");
         const size_t nco = p.host.coarsest.size();

@@ -171,6 +171,8 @@ DevPlan &hpdr_ctx::plan(int rank, const uint64_t *dims) {
     std::vector<std::vector<size_t>> moff(4, std::vector<size_t>(h.L));
     for (int d = 0; d < 4; d++)
         for (int k = 0; k < h.L; k++) moff[d][k] = pk.put(h.map[d][k]);
+    std::vector<long long> co(h.coarsest.begin(), h.coarsest.end());
+    const size_t coff = pk.put(co);
     dp->bytes = pk.bytes.size();
     cudaError_t e = cudaMalloc(&dp->dbuf, dp->bytes ? dp->bytes : 16);
     if (e != cudaSuccess) {
@@ -207,6 +209,7 @@ DevPlan &hpdr_ctx::plan(int rank, const uint64_t *dims) {
     }
     for (int d = 0; d < 4; d++)
         for (int k = 0; k < kMaxLevels; k++) dp->map[d][k] = k < h.L ? (const int32_t *)(base + moff[d][k]) : nullptr;
+    dp->coarsest = (const long long *)(base + coff);
     for (int d = 0; d < 4; d++) dp->dims.n[d] = h.dims[d];
     dp->n_total = h.total();
     dp->level_size.resize(h.L);

@@ -37,6 +37,7 @@ struct DevPlan {
     HostPlan host;
     std::vector<DevStep> steps;
     const int32_t *map[4][kMaxLevels];   // device copies of the index maps
+    const long long *coarsest = nullptr; // device copy of host.coarsest (<= 16 flat indices)
     void *dbuf = nullptr;
     size_t bytes = 0;
     Shape4 dims;

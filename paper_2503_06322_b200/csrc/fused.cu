@@ -104,78 +104,133 @@ __device__ __forceinline__ void slab_range(int nc, int nz, int z, int &lo, int &
 }
 
 // ---------------------------------------------------------------------------------- pass 1
-// REC = false: decompose.  F is the fine level (TIn = float for the finest f32 input).
-//   mc = F - P(F); coef[fine-only] = mc; Cg[coarse] = F; Z0 = R0M0(mc) (or mc if axis 0 inactive)
-// REC = true: recompose.  mc = coef at fine-only nodes, 0 at coarse nodes; Z0 = R0M0(mc).
-template <bool REC, bool A0, bool A1, bool A2, typename TIn>
+// MODE 0 (decompose):  mc = F - P(F); coef[fine-only] = mc; Cg[coarse] = F; Z0 = R0M0(mc)
+// MODE 1 (recompose):  mc = coef at fine-only nodes, 0 at coarse nodes; Z0 = R0M0(mc)
+// MODE 2 (decompose with quantize-on-write): as MODE 0 but fine-only nodes are quantized
+//   straight into keys / outlier mask / histogram (quantize.py:73-84) instead of coef.
+// Z0 = mc along axis 0 when that axis is inactive at this transition.
+constexpr int kSmemHist = 4096;
+
+template <int MODE, bool A0, bool A1, bool A2, typename TIn>
 __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, int n0, int n1, int n2, DevAxis ax0,
                                                      DevAxis ax1, DevAxis ax2, LevelMap lm, double *__restrict__ coef,
                                                      const double *__restrict__ coef_in, double *__restrict__ Z0,
-                                                     double *__restrict__ Cg) {
+                                                     double *__restrict__ Cg, QuantOut q) {
+    __shared__ uint32_t sh_hist[MODE == 2 ? kSmemHist : 1];
+    const bool sh_ok = MODE == 2 && q.dict <= kSmemHist;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    if (MODE == 2 && sh_ok)
+        for (uint32_t k = tid; k < q.dict; k += 256) sh_hist[k] = 0;
+    if (MODE == 2) __syncthreads();
     const int j2 = blockIdx.x * 32 + threadIdx.x;
     const int j1 = blockIdx.y * 8 + threadIdx.y;
-    if (j1 >= n1 || j2 >= n2) return;
-    const Nb b1 = neighbours<A1>(ax1, j1), b2 = neighbours<A2>(ax2, j2);
-    const int nc1 = A1 ? ax1.nc : n1, nc2 = A2 ? ax2.nc : n2;
+    const bool act = j1 < n1 && j2 < n2;
     const int nc0 = A0 ? ax0.nc : n0;
     int c_lo, c_hi;
     slab_range(nc0, gridDim.z, blockIdx.z, c_lo, c_hi);
-    if (c_lo >= c_hi) return;
-    int j_start, j_end, own_lo, own_hi;
-    if (A0) {
-        j_start = max(0, ax0.r0[c_lo] - 2);
-        j_end = min(n0 - 1, ax0.r0[c_hi - 1] + 2);
-        own_lo = c_lo == 0 ? 0 : ax0.r0[c_lo];
-        own_hi = c_hi == nc0 ? n0 : ax0.r0[c_hi];
-    } else {
-        j_start = c_lo;
-        j_end = c_hi - 1;
-        own_lo = c_lo;
-        own_hi = c_hi;
-    }
-    const int64_t plane = (int64_t)n1 * n2;
-    const int64_t zplane = (int64_t)n1 * n2;
-    const int64_t col = (int64_t)j1 * n2 + j2;
-    const int64_t fcol = ((int64_t)lm.m1[j1]) * lm.D2 + lm.m2[j2];
-    March M;
-    M.m1 = M.m2 = M.ya = M.yb = M.yc = 0.0;
-    M.c = c_lo;
-    auto emit = [&](int c, double z) { Z0[(int64_t)c * zplane + col] = z; };
-    for (int j = j_start; j <= j_end; j++) {
-        const Nb b0 = neighbours<A0>(ax0, j);
-        const bool coarse_node = !b0.fo && !b1.fo && !b2.fo;
-        double mc;
-        if (!REC) {
-            // GPK: P0 along axis 0 at the corner columns, then P1 along axis 1, then P2 along axis 2
-            auto P0 = [&](int y1, int x2) -> double {
-                const double va = ld(F + (int64_t)b0.fa * plane + (int64_t)y1 * n2 + x2);
-                if (!b0.fo) return va;
-                const double vb = ld(F + (int64_t)b0.fb * plane + (int64_t)y1 * n2 + x2);
-                return lerp(va, vb, b0.t);
-            };
-            auto P1 = [&](int x2) -> double {
-                const double va = P0(b1.fa, x2);
-                if (!b1.fo) return va;
-                return lerp(va, P0(b1.fb, x2), b1.t);
-            };
-            double pred = P1(b2.fa);
-            if (b2.fo) pred = lerp(pred, P1(b2.fb), b2.t);
-            const double own = ld(F + (int64_t)j * plane + col);
-            mc = dsub(own, pred);
-            if (j >= own_lo && j < own_hi) {
-                if (!coarse_node) {
-                    coef[(int64_t)lm.m0[j] * lm.D1 * lm.D2 + fcol] = mc;
-                } else {
-                    const int c0 = A0 ? b0.ca : j;
-                    Cg[((int64_t)c0 * nc1 + b1.ca) * nc2 + b2.ca] = own;
-                }
-            }
+    int fl = 0;
+    if (act && c_lo < c_hi) {
+        const Nb b1 = neighbours<A1>(ax1, j1), b2 = neighbours<A2>(ax2, j2);
+        const int nc1 = A1 ? ax1.nc : n1, nc2 = A2 ? ax2.nc : n2;
+        int j_start, j_end, own_lo, own_hi;
+        if (A0) {
+            j_start = max(0, ax0.r0[c_lo] - 2);
+            j_end = min(n0 - 1, ax0.r0[c_hi - 1] + 2);
+            own_lo = c_lo == 0 ? 0 : ax0.r0[c_lo];
+            own_hi = c_hi == nc0 ? n0 : ax0.r0[c_hi];
         } else {
-            mc = coarse_node ? 0.0 : coef_in[(int64_t)lm.m0[j] * lm.D1 * lm.D2 + fcol];
+            j_start = c_lo;
+            j_end = c_hi - 1;
+            own_lo = c_lo;
+            own_hi = c_hi;
         }
-        if (A0) march_push(M, ax0, n0, j, j_start, mc, c_hi, emit);
-        else Z0[(int64_t)j * zplane + col] = mc;
+        const int64_t plane = (int64_t)n1 * n2;
+        const int64_t col = (int64_t)j1 * n2 + j2;
+        const int64_t fcol = ((int64_t)lm.m1[j1]) * lm.D2 + lm.m2[j2];
+        const int64_t fplane = lm.D1 * lm.D2;
+        March M;
+        M.m1 = M.m2 = M.ya = M.yb = M.yc = 0.0;
+        M.c = c_lo;
+        auto emit = [&](int c, double z) { Z0[(int64_t)c * plane + col] = z; };
+        for (int j = j_start; j <= j_end; j++) {
+            const Nb b0 = neighbours<A0>(ax0, j);
+            const bool coarse_node = !b0.fo && !b1.fo && !b2.fo;
+            const int64_t f = (int64_t)lm.m0[j] * fplane + fcol;
+            double mc;
+            if (MODE != 1) {
+                // GPK: P0 along axis 0 at the corner columns, then P1 along axis 1, then P2 along axis 2
+                auto P0 = [&](int y1, int x2) -> double {
+                    const double va = ld(F + (int64_t)b0.fa * plane + (int64_t)y1 * n2 + x2);
+                    if (!b0.fo) return va;
+                    const double vb = ld(F + (int64_t)b0.fb * plane + (int64_t)y1 * n2 + x2);
+                    return lerp(va, vb, b0.t);
+                };
+                auto P1 = [&](int x2) -> double {
+                    const double va = P0(b1.fa, x2);
+                    if (!b1.fo) return va;
+                    return lerp(va, P0(b1.fb, x2), b1.t);
+                };
+                double pred = P1(b2.fa);
+                if (b2.fo) pred = lerp(pred, P1(b2.fb), b2.t);
+                const double own = ld(F + (int64_t)j * plane + col);
+                mc = dsub(own, pred);
+                if (j >= own_lo && j < own_hi) {
+                    if (coarse_node) {
+                        const int c0 = A0 ? b0.ca : j;
+                        Cg[((int64_t)c0 * nc1 + b1.ca) * nc2 + b2.ca] = own;
+                    } else if (MODE == 0) {
+                        coef[f] = mc;
+                    } else {
+                        long long b = 0;
+                        if (!isfinite(mc)) {
+                            fl |= 1;
+                        } else {
+                            const double sc = mc / q.bin;                 // IEEE division (quantize.py:73)
+                            if (fabs(sc) >= 4611686018427387904.0) fl |= 2;
+                            else b = (long long)rint(sc);                 // half to even (:76)
+                        }
+                        if (b >= q.half || -b >= q.half) {                 // outlier (:80-83)
+                            q.obins[f] = b;
+                            atomicOr(&q.omask[f >> 5], 1u << (f & 31));
+                            b = 0;
+                        }
+                        const uint32_t key = (uint32_t)(((unsigned long long)b << 1) ^ (unsigned long long)(b >> 63));
+                        q.keys[f] = key;
+                        if (sh_ok) atomicAdd(&sh_hist[key], 1u);
+                        else atomicAdd(&q.hist[key], 1ULL);
+                    }
+                }
+            } else {
+                mc = coarse_node ? 0.0 : coef_in[f];
+            }
+            if (A0) march_push(M, ax0, n0, j, j_start, mc, c_hi, emit);
+            else Z0[(int64_t)j * plane + col] = mc;
+        }
     }
+    if (MODE == 2) {
+        if (fl) atomicOr(q.flags, fl);
+        __syncthreads();
+        if (sh_ok)
+            for (uint32_t k = tid; k < q.dict; k += 256) {
+                const uint32_t c = sh_hist[k];
+                if (c) atomicAdd(&q.hist[k], (unsigned long long)c);
+            }
+    }
+}
+
+// Coarsest nodes: raw values are checked (finite, bin limit) like every coefficient, then get key 0.
+__global__ void k_quantize_coarsest(const double *__restrict__ vals, const long long *__restrict__ idx, int n,
+                                    QuantOut q) {
+    const int k = threadIdx.x;
+    if (k < n) {
+        const double v = vals[k];
+        int fl = 0;
+        if (!isfinite(v)) fl |= 1;
+        else if (fabs(v / q.bin) >= 4611686018427387904.0) fl |= 2;
+        if (fl) atomicOr(q.flags, fl);
+        q.keys[idx[k]] = 0u;
+    }
+    if (k == 0) atomicAdd(&q.hist[0], (unsigned long long)n);
 }
 
 // ---------------------------------------------------------------------------------- pass 2
@@ -290,17 +345,17 @@ int slabs_for(int64_t cols, int planes) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(s, std::max(planes, 1)));
 }
 
-template <bool REC, typename TIn>
+template <int MODE, typename TIn>
 void launch_pass1(int act, const TIn *F, int n0, int n1, int n2, const DevAxis &a0, const DevAxis &a1,
                   const DevAxis &a2, const LevelMap &lm, double *coef, const double *coef_in, double *Z0, double *Cg,
-                  cudaStream_t s) {
+                  const QuantOut &q, cudaStream_t s) {
     const int planes = (act & 1) ? a0.nc : n0;
     dim3 grid((n2 + 31) / 32, (n1 + 7) / 8, slabs_for((int64_t)n1 * n2, planes));
     dim3 block(32, 8);
 #define P1L(M)                                                                                                     \
     case M:                                                                                                        \
-        k_level_pass1<REC, (M & 1) != 0, (M & 2) != 0, (M & 4) != 0, TIn><<<grid, block, 0, s>>>(               \
-            F, n0, n1, n2, a0, a1, a2, lm, coef, coef_in, Z0, Cg);                                                 \
+        k_level_pass1<MODE, (M & 1) != 0, (M & 2) != 0, (M & 4) != 0, TIn><<<grid, block, 0, s>>>(              \
+            F, n0, n1, n2, a0, a1, a2, lm, coef, coef_in, Z0, Cg, q);                                              \
         break;
     switch (act) { P1L(1) P1L(2) P1L(3) P1L(4) P1L(5) P1L(6) P1L(7) default: break; }
 #undef P1L
@@ -350,10 +405,11 @@ void fused_pass1_decompose(const DevPlan &p, int st_i, const void *F, bool f32, 
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
     const int64_t zsz = (int64_t)((act & 1) ? st.ax[1].nc : n0) * n1 * n2;
     KPROF("k_level_pass1", (f32 ? 4.0 : 8.0) * nf + 8.0 * (nf - nc) + 8.0 * nc + 8.0 * zsz, s);
-    if (f32) launch_pass1<false, float>(act, (const float *)F, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, coef,
-                                        nullptr, Z0, Cg, s);
-    else launch_pass1<false, double>(act, (const double *)F, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, coef,
-                                     nullptr, Z0, Cg, s);
+    const QuantOut q{};
+    if (f32) launch_pass1<0, float>(act, (const float *)F, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, coef,
+                                    nullptr, Z0, Cg, q, s);
+    else launch_pass1<0, double>(act, (const double *)F, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, coef,
+                                 nullptr, Z0, Cg, q, s);
 }
 
 void fused_pass1_recompose(const DevPlan &p, int st_i, const double *coef, double *Z0, cudaStream_t s) {
@@ -364,8 +420,31 @@ void fused_pass1_recompose(const DevPlan &p, int st_i, const double *coef, doubl
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
     const int64_t zsz = (int64_t)((act & 1) ? st.ax[1].nc : n0) * n1 * n2;
     KPROF("k_level_pass1r", 8.0 * (nf - nc) + 8.0 * zsz, s);
-    launch_pass1<true, double>(act, nullptr, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, nullptr, coef, Z0, nullptr,
-                               s);
+    const QuantOut q{};
+    launch_pass1<1, double>(act, nullptr, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, nullptr, coef, Z0, nullptr,
+                            q, s);
+}
+
+void fused_pass1_quantize(const DevPlan &p, int st_i, const void *F, bool f32, const QuantOut &q, double *Z0,
+                          double *Cg, cudaStream_t s) {
+    const DevStep &st = p.steps[st_i];
+    const int n0 = (int)st.fsh.n[1], n1 = (int)st.fsh.n[2], n2 = (int)st.fsh.n[3];
+    const int act = (st.ax[1].active ? 1 : 0) | (st.ax[2].active ? 2 : 0) | (st.ax[3].active ? 4 : 0);
+    LevelMap lm{p.map[1][st_i], p.map[2][st_i], p.map[3][st_i], p.dims.n[2], p.dims.n[3]};
+    const int64_t nf = st.fsh.size(), nc = st.csh.size();
+    const int64_t zsz = (int64_t)((act & 1) ? st.ax[1].nc : n0) * n1 * n2;
+    KPROF("k_level_pass1q", (f32 ? 4.0 : 8.0) * nf + 4.0 * (nf - nc) + 8.0 * nc + 8.0 * zsz, s);
+    if (f32) launch_pass1<2, float>(act, (const float *)F, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, nullptr,
+                                    nullptr, Z0, Cg, q, s);
+    else launch_pass1<2, double>(act, (const double *)F, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, nullptr,
+                                 nullptr, Z0, Cg, q, s);
+}
+
+void quantize_coarsest(const DevPlan &p, const double *coarsest_vals, const QuantOut &q, cudaStream_t s) {
+    const int n = (int)p.host.coarsest.size();
+    KPROF("k_quantize_coarsest", 16.0 * n, s);
+    k_quantize_coarsest<<<1, 32, 0, s>>>(coarsest_vals, p.coarsest, n, q);
+    LAUNCH_CHECK();
 }
 
 void fused_pass2(const DevPlan &p, int st_i, const double *Z0, double *B, cudaStream_t s) {

@@ -13,6 +13,24 @@ struct LevelMap {
 
 bool fused_supported(const DevPlan &p);
 
+// Quantize-on-write targets (quantize.py:63-84 applied as each coefficient is finalised).
+struct QuantOut {
+    double bin;
+    long long half;
+    uint32_t dict;
+    uint32_t *keys;               // N keys, finest order
+    uint32_t *omask;              // N/32 words: outlier flags (zeroed by the caller)
+    long long *obins;             // N slots, written only at outliers
+    unsigned long long *hist;     // dict counts (zeroed by the caller)
+    int *flags;                   // bit0 non-finite, bit1 |c/bin| >= 2^62
+};
+
+// Decompose transition st_i writing keys instead of fp64 coefficients.
+void fused_pass1_quantize(const DevPlan &p, int st_i, const void *F, bool f32, const QuantOut &q, double *Z0,
+                          double *Cg, cudaStream_t s);
+// Coarsest nodes (quantize.py:64-77): bin-limit / finiteness checks, key 0, histogram.
+void quantize_coarsest(const DevPlan &p, const double *coarsest_vals, const QuantOut &q, cudaStream_t s);
+
 // Decompose transition st_i: mc -> coef (fine-only nodes), coarse-node gather -> Cg, and the
 // axis-0 mass-transfer -> Z0.  F is the dense fine level (float when f32).
 void fused_pass1_decompose(const DevPlan &p, int st_i, const void *F, bool f32, double *coef, double *Z0,

@@ -93,7 +93,7 @@ __global__ void k_chunk_counts(const uint32_t *__restrict__ omask, int64_t words
 }
 
 __global__ void k_write_outliers(const uint32_t *__restrict__ omask, int64_t words, const double *__restrict__ coef,
-                                 double bin, const unsigned long long *__restrict__ chunk_off,
+                                 const long long *__restrict__ sparse, double bin, const unsigned long long *__restrict__ chunk_off,
                                  uint64_t *__restrict__ oidx, int64_t *__restrict__ obins) {
     typedef cub::BlockScan<unsigned, 256> BS;
     __shared__ typename BS::TempStorage tmp;
@@ -110,7 +110,7 @@ __global__ void k_write_outliers(const uint32_t *__restrict__ omask, int64_t wor
             m &= m - 1;
             int64_t i = w * 32 + bit;
             oidx[pos] = (uint64_t)i;
-            obins[pos] = (long long)rint(coef[i] / bin);
+            obins[pos] = sparse ? sparse[i] : (long long)rint(coef[i] / bin);
             pos++;
         }
         base += tot;
@@ -170,6 +170,18 @@ void quantize_device(hpdr_ctx *ctx, const double *coef, int64_t n, const std::ve
         k_quantize<<<grid, kQThreads, smem, s>>>(coef, n, co, bin_width, half, dict_size, keys, omask, hist, flags);
         LAUNCH_CHECK();
     }
+    quantize_finish(ctx, n, dict_size, bin_width, coef, nullptr, res, s);
+}
+
+void quantize_finish(hpdr_ctx *ctx, int64_t n, uint32_t dict_size, double bin_width, const double *coef,
+                     const long long *obins_sparse, QuantResult &res, cudaStream_t s) {
+    const int64_t words = (n + 31) / 32;
+    const int64_t chunks = (words + kChunkWords - 1) / kChunkWords;
+    uint32_t *omask = (uint32_t *)ctx->dbuf("omask", words * 4);
+    unsigned long long *hist = (unsigned long long *)ctx->dbuf("hist", (size_t)dict_size * 8);
+    int *flags = (int *)ctx->dbuf("qflags", 16);
+    unsigned long long *ccount = (unsigned long long *)ctx->dbuf("ochunk", (chunks + 1) * 8);
+    unsigned long long *coff = (unsigned long long *)ctx->dbuf("ochunk_off", (chunks + 1) * 8);
     {
         KPROF("k_chunk_counts", 4.0 * words, s);
         k_chunk_counts<<<(unsigned)chunks, 256, 0, s>>>(omask, words, ccount);
@@ -196,8 +208,8 @@ void quantize_device(hpdr_ctx *ctx, const double *coef, int64_t n, const std::ve
     res.d_outlier_bins = (int64_t *)ctx->dbuf("obins", res.n_outliers * 8);
     if (res.n_outliers) {
         KPROF("k_write_outliers", 4.0 * words + 24.0 * res.n_outliers, s);
-        k_write_outliers<<<(unsigned)chunks, 256, 0, s>>>(omask, words, coef, bin_width, coff, res.d_outlier_idx,
-                                                          res.d_outlier_bins);
+        k_write_outliers<<<(unsigned)chunks, 256, 0, s>>>(omask, words, coef, obins_sparse, bin_width, coff,
+                                                          res.d_outlier_idx, res.d_outlier_bins);
         LAUNCH_CHECK();
     }
 }

@@ -21,6 +21,12 @@ struct QuantResult {
 void quantize_device(hpdr_ctx *ctx, const double *coef, int64_t n, const std::vector<int64_t> &coarsest,
                      double bin_width, uint32_t dict_size, uint32_t *keys, QuantResult &res, cudaStream_t s);
 
+// Second half of quantization once keys, the outlier mask ("omask"), "hist" and "qflags" are
+// populated: ordered outlier compaction and read-back.  Outlier bins come from the sparse
+// per-element array when given, otherwise they are recomputed from coef.
+void quantize_finish(hpdr_ctx *ctx, int64_t n, uint32_t dict_size, double bin_width, const double *coef,
+                     const long long *obins_sparse, QuantResult &res, cudaStream_t s);
+
 // Histogram of keys already on the device (huffman.py:74-104).  Sets *bad when a key >= dict.
 void histogram_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict_size,
                       std::vector<uint64_t> &hist, bool *bad, cudaStream_t s);

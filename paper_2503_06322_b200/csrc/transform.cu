@@ -478,17 +478,36 @@ bool use_fused(const DevPlan &p) {
 
 namespace {
 
+// Work buffers of the fused path: coarse-level arena, pass-1 output Z0, pass-2 / Thomas
+// buffer t0 and the coarse gather cg (no full-size fp64 level copies).
+LevelBuffers fused_buffers(hpdr_ctx *ctx, DevPlan &p) {
+    LevelBuffers b{};
+    int64_t zmax = 1, cmax = 1;
+    for (const DevStep &st : p.steps) {
+        const int64_t m0 = st.ax[1].active ? st.csh.n[1] : st.fsh.n[1];
+        zmax = std::max<int64_t>(zmax, m0 * st.fsh.n[2] * st.fsh.n[3]);
+        cmax = std::max<int64_t>(cmax, st.csh.size());
+    }
+    b.arena = (double *)ctx->dbuf("arena", std::max<int64_t>(p.coarse_arena, 1) * 8);
+    b.t0 = (double *)ctx->dbuf("t0", cmax * 8);
+    b.cg = (double *)ctx->dbuf("cg", cmax * 8);
+    b.mc = (double *)ctx->dbuf("z0", zmax * 8);   // Z0 of pass 1
+    return b;
+}
+
 // Fused decomposition (ranks <= 3): pass 1 (GPK residual + coefficients + axis-0 LPK), pass 2
-// (axis-1/2 LPK), IPK Thomas sweeps, coarse + corr.
-const double *decompose_fused(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int dtype, double *coef, cudaStream_t s) {
-    LevelBuffers b = level_buffers(ctx, p);
+// (axis-1/2 LPK), IPK Thomas sweeps, coarse + corr.  q != nullptr quantizes on write.
+const double *decompose_fused(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int dtype, double *coef,
+                              const QuantOut *q, cudaStream_t s) {
+    LevelBuffers b = fused_buffers(ctx, p);
     const int L = p.host.L;
-    double *Z0 = (double *)ctx->dbuf("z0", p.n_total * 8);
+    double *Z0 = b.mc;
     for (int st_i = 0; st_i + 1 < L; st_i++) {
         const DevStep &st = p.steps[st_i];
         const void *F = st_i == 0 ? d_in : (const void *)level_ptr(b, p, st_i);
         double *Dn = level_ptr(b, p, st_i + 1);
-        fused_pass1_decompose(p, st_i, F, st_i == 0 && dtype == 0, coef, Z0, b.cg, s);
+        if (q) fused_pass1_quantize(p, st_i, F, st_i == 0 && dtype == 0, *q, Z0, b.cg, s);
+        else fused_pass1_decompose(p, st_i, F, st_i == 0 && dtype == 0, coef, Z0, b.cg, s);
         fused_pass2(p, st_i, Z0, b.t0, s);
         Shape4 sh = st.csh;
         for (int a = 0; a < 4; a++)
@@ -498,25 +517,31 @@ const double *decompose_fused(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int d
         k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, Dn, nc);   // coarse + corr
         LAUNCH_CHECK();
     }
-    return nullptr;
+    return level_ptr(b, p, L - 1);
 }
 
 }  // namespace
 
+const double *decompose_quantize(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int dtype, const QuantOut &q,
+                                 cudaStream_t s) {
+    const double *DL = decompose_fused(ctx, p, d_in, dtype, nullptr, &q, s);
+    quantize_coarsest(p, DL, q, s);
+    return DL;
+}
+
 const double *decompose_device(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int dtype, double *coef, cudaStream_t s) {
-    LevelBuffers b = level_buffers(ctx, p);
     const int64_t N = p.n_total;
     const int L = p.host.L;
     if (L > 1 && use_fused(p)) {
-        decompose_fused(ctx, p, d_in, dtype, coef, s);
+        const double *DL = decompose_fused(ctx, p, d_in, dtype, coef, nullptr, s);
         Shape4 shL;
         for (int d = 0; d < 4; d++) shL.n[d] = p.host.cnt[d][L - 1];
-        const double *DL = level_ptr(b, p, L - 1);
         Sel4 none{};
         k_scatter_level<<<rows_grid(shL), 256, 0, s>>>(DL, shL, coef, p.dims, level_map(p, L - 1), none, 0);
         LAUNCH_CHECK();
         return DL;
     }
+    LevelBuffers b = level_buffers(ctx, p);
     {
         KPROF("k_to_f64", (double)N * (dtype == 0 ? 12 : 16), s);
         k_to_f64<<<grid_for(N, 256, 148 * 16), 256, 0, s>>>(d_in, dtype, b.lvl0, N);
@@ -605,15 +630,16 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
         cast_output(rec, out, out_dtype, p.n_total, s);
         return;
     }
-    LevelBuffers b = level_buffers(ctx, p);
-    double *Z0 = (double *)ctx->dbuf("z0", p.n_total * 8);
+    const bool direct = out_dtype == 0 || out_dtype == 1;
+    LevelBuffers b = fused_buffers(ctx, p);
+    if (!direct) b.lvl0 = (double *)ctx->dbuf("lvl0", p.n_total * 8);
+    double *Z0 = b.mc;
     Shape4 shL;
     for (int d = 0; d < 4; d++) shL.n[d] = p.host.cnt[d][L - 1];
     Sel4 none{};
     k_gather_level<<<rows_grid(shL), 256, 0, s>>>(coef, p.dims, level_map(p, L - 1), none, level_ptr(b, p, L - 1),
                                                   shL, 0);
     LAUNCH_CHECK();
-    const bool direct = out_dtype == 0 || out_dtype == 1;
     for (int st_i = L - 2; st_i >= 0; st_i--) {
         const DevStep &st = p.steps[st_i];
         double *Dc = level_ptr(b, p, st_i + 1);

@@ -28,6 +28,12 @@ const double *decompose_device(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int 
 // transform.py:326-348.  coef: N doubles.  Returns the finest dense level (device, N doubles).
 double *recompose_device(hpdr_ctx *ctx, DevPlan &p, const double *coef, cudaStream_t s);
 
+struct QuantOut;
+// Fused decomposition with quantize-on-write (ranks <= 3, use_fused): keys / outlier mask /
+// histogram are produced by the level kernels; returns the coarsest dense level (device).
+const double *decompose_quantize(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int dtype, const QuantOut &q,
+                                 cudaStream_t s);
+
 // Recompose straight into out (device) in the blob's dtype (fused final level for ranks <= 3).
 void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s);
 
