@@ -55,6 +55,16 @@ struct Shape4 {
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
+// ---- cp.async (LDGSTS) helpers: asynchronous global -> shared copies for prefetch rings ----
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 inline unsigned grid_for(int64_t work, int threads, int64_t cap = 148LL * 32) {
     int64_t b = (work + threads - 1) / threads;
     if (b < 1) b = 1;

@@ -20,6 +20,7 @@ struct DevAxis {
     int32_t n, nc;
     const int32_t *pa, *pb;
     const double *pt;
+    const int32_t *fa, *fb;
     const int32_t *r0, *rr, *rl;
     const double *wr, *wl;
     const double *ml, *md, *mu;

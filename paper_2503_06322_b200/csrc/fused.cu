@@ -3,15 +3,18 @@
 //
 // One decomposition transition (transform.py:306-315) becomes
 //   pass 1   k_level_pass1   residual mc = F - P(F) (GPK, nested lerps in axis order 0,1,2)
-//                            -> coefficient write, coarse-node gather, and the axis-0
-//                            mass-multiply + restriction (LPK, transform.py:206-203) as a
-//                            register march along axis 0
+//                            -> coefficient / quantized-key write, coarse-node gather, and the
+//                            axis-0 mass-multiply + restriction (LPK, transform.py:206-226 then
+//                            :181-203) as a register march along axis 0
 //   pass 2   k_level_pass2   axis-1 LPK march + axis-2 LPK across the block (shared memory)
 //   IPK      Thomas sweeps (transform.cu) and coarse + corr
 // and recomposition (transform.py:337-347) mirrors it with pass 1 reading mc from the
 // coefficients and k_level_final writing pred + mc (or the output dtype at the finest level).
-// Every value is produced with the reference's operation order (explicit _rn intrinsics), so
-// the result is bit-identical to the per-axis path and to numpy.
+//
+// The marches are sequential along one axis, so every kernel streams its planes / rows through
+// a cp.async shared-memory ring several steps ahead of the arithmetic (the dependency chain of
+// the march never waits on DRAM).  Every value is produced with the reference's operation
+// order (explicit _rn intrinsics): results are bit-identical to numpy.
 #include "fused.cuh"
 
 namespace hpdr {
@@ -22,9 +25,6 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double lerp(double va, double vb, double t) { return dadd(va, dmul(t, dsub(vb, va))); }
-
-template <typename T>
-__device__ __forceinline__ double ld(const T *p) { return (double)__ldg(p); }
 
 // Per-thread description of one axis at a fine index j: coarse neighbours (fine indices fa/fb,
 // coarse indices ca/cb), weight t and whether j is a fine-only node along this axis.
@@ -43,13 +43,13 @@ __device__ __forceinline__ Nb neighbours(const DevAxis &ax, int j) {
         r.fo = false;
         return r;
     }
-    const int a = ax.pa[j], b = ax.pb[j];
+    const int b = __ldg(ax.pb + j);
     r.fo = b >= 0;
-    r.ca = a;
-    r.cb = r.fo ? b : a;
-    r.fa = ax.r0[a];
-    r.fb = ax.r0[r.cb];
-    r.t = r.fo ? ax.pt[j] : 0.0;
+    r.ca = __ldg(ax.pa + j);
+    r.cb = r.fo ? b : r.ca;
+    r.fa = __ldg(ax.fa + j);
+    r.fb = __ldg(ax.fb + j);
+    r.t = r.fo ? __ldg(ax.pt + j) : 0.0;
     return r;
 }
 
@@ -62,28 +62,27 @@ struct March {
     int c;                // next coarse output
 };
 
-// Push x(j); emits every z(c) that became computable through emit(c, z).
 template <class Emit>
 __device__ __forceinline__ void march_push(March &M, const DevAxis &ax, int n, int j, int j_start, double x, int c_hi,
                                            Emit &&emit) {
     auto try_y = [&](int k, double xk, double xkm1, double xkp1, bool has_up) {
-        double v = dmul(ax.md[k], xk);
-        if (k >= 1) v = dadd(v, dmul(ax.ml[k], xkm1));
-        if (has_up) v = dadd(v, dmul(ax.mu[k], xkp1));
+        double v = dmul(__ldg(ax.md + k), xk);
+        if (k >= 1) v = dadd(v, dmul(__ldg(ax.ml + k), xkm1));
+        if (has_up) v = dadd(v, dmul(__ldg(ax.mu + k), xkp1));
         M.ya = M.yb;
         M.yb = M.yc;
         M.yc = v;
         while (M.c < c_hi) {
-            const int r0 = ax.r0[M.c], rr = ax.rr[M.c], rl = ax.rl[M.c];
+            const int r0 = __ldg(ax.r0 + M.c), rr = __ldg(ax.rr + M.c), rl = __ldg(ax.rl + M.c);
             const int need = rr >= 0 ? rr : r0;
             if (need != k) break;
             double z;
             if (rr >= 0) {
-                z = dadd(M.yb, dmul(ax.wr[M.c], M.yc));
-                if (rl >= 0) z = dadd(z, dmul(ax.wl[M.c], M.ya));
+                z = dadd(M.yb, dmul(__ldg(ax.wr + M.c), M.yc));
+                if (rl >= 0) z = dadd(z, dmul(__ldg(ax.wl + M.c), M.ya));
             } else {
                 z = M.yc;
-                if (rl >= 0) z = dadd(z, dmul(ax.wl[M.c], M.yb));
+                if (rl >= 0) z = dadd(z, dmul(__ldg(ax.wl + M.c), M.yb));
             }
             emit(M.c, z);
             M.c++;
@@ -96,11 +95,31 @@ __device__ __forceinline__ void march_push(March &M, const DevAxis &ax, int n, i
     M.m1 = x;
 }
 
-// Coarse-plane range of slab z out of nz along an axis with (active) tables.
 __device__ __forceinline__ void slab_range(int nc, int nz, int z, int &lo, int &hi) {
     const int base = nc / nz, rem = nc % nz;
     lo = z * base + min(z, rem);
     hi = lo + base + (z < rem ? 1 : 0);
+}
+
+// Fine-plane range a slab of coarse outputs [c_lo, c_hi) marches over / owns.
+template <bool A0>
+__device__ __forceinline__ void slab_planes(const DevAxis &ax0, int n0, int nc0, int c_lo, int c_hi, int &j_start,
+                                            int &j_end, int &own_lo, int &own_hi) {
+    if (A0) {
+        j_start = max(0, __ldg(ax0.r0 + c_lo) - 2);
+        j_end = min(n0 - 1, __ldg(ax0.r0 + c_hi - 1) + 2);
+        own_lo = c_lo == 0 ? 0 : __ldg(ax0.r0 + c_lo);
+        own_hi = c_hi == nc0 ? n0 : __ldg(ax0.r0 + c_hi);
+    } else {
+        j_start = own_lo = c_lo;
+        j_end = c_hi - 1;
+        own_hi = c_hi;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void cp_elem(T *s, const T *g) {
+    cp_async<sizeof(T)>(s, g);
 }
 
 // ---------------------------------------------------------------------------------- pass 1
@@ -109,6 +128,8 @@ __device__ __forceinline__ void slab_range(int nc, int nz, int z, int &lo, int &
 // MODE 2 (decompose with quantize-on-write): as MODE 0 but fine-only nodes are quantized
 //   straight into keys / outlier mask / histogram (quantize.py:73-84) instead of coef.
 // Z0 = mc along axis 0 when that axis is inactive at this transition.
+// Block: 32 x 8 columns (j2, j1); planes of the tile (+1 halo) stream through a cp.async ring.
+constexpr int kTX = 32, kTY = 8, kHX = kTX + 2, kHY = kTY + 2, kRing = 8;
 constexpr int kSmemHist = 4096;
 
 template <int MODE, bool A0, bool A1, bool A2, typename TIn>
@@ -116,54 +137,76 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
                                                      DevAxis ax1, DevAxis ax2, LevelMap lm, double *__restrict__ coef,
                                                      const double *__restrict__ coef_in, double *__restrict__ Z0,
                                                      double *__restrict__ Cg, QuantOut q) {
+    __shared__ __align__(16) TIn ring[kRing][kHY][kHX];
     __shared__ uint32_t sh_hist[MODE == 2 ? kSmemHist : 1];
     const bool sh_ok = MODE == 2 && q.dict <= kSmemHist;
-    const int tid = threadIdx.y * 32 + threadIdx.x;
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
     if (MODE == 2 && sh_ok)
         for (uint32_t k = tid; k < q.dict; k += 256) sh_hist[k] = 0;
-    if (MODE == 2) __syncthreads();
-    const int j2 = blockIdx.x * 32 + threadIdx.x;
-    const int j1 = blockIdx.y * 8 + threadIdx.y;
+    const int x0 = blockIdx.x * kTX - 1, y0 = blockIdx.y * kTY - 1;   // tile origin incl. halo
+    const int j2 = x0 + 1 + tx, j1 = y0 + 1 + ty;
     const bool act = j1 < n1 && j2 < n2;
     const int nc0 = A0 ? ax0.nc : n0;
     int c_lo, c_hi;
     slab_range(nc0, gridDim.z, blockIdx.z, c_lo, c_hi);
     int fl = 0;
-    if (act && c_lo < c_hi) {
-        const Nb b1 = neighbours<A1>(ax1, j1), b2 = neighbours<A2>(ax2, j2);
-        const int nc1 = A1 ? ax1.nc : n1, nc2 = A2 ? ax2.nc : n2;
+    if (c_lo < c_hi) {   // uniform across the block
         int j_start, j_end, own_lo, own_hi;
-        if (A0) {
-            j_start = max(0, ax0.r0[c_lo] - 2);
-            j_end = min(n0 - 1, ax0.r0[c_hi - 1] + 2);
-            own_lo = c_lo == 0 ? 0 : ax0.r0[c_lo];
-            own_hi = c_hi == nc0 ? n0 : ax0.r0[c_hi];
-        } else {
-            j_start = c_lo;
-            j_end = c_hi - 1;
-            own_lo = c_lo;
-            own_hi = c_hi;
-        }
+        slab_planes<A0>(ax0, n0, nc0, c_lo, c_hi, j_start, j_end, own_lo, own_hi);
         const int64_t plane = (int64_t)n1 * n2;
-        const int64_t col = (int64_t)j1 * n2 + j2;
-        const int64_t fcol = ((int64_t)lm.m1[j1]) * lm.D2 + lm.m2[j2];
         const int64_t fplane = lm.D1 * lm.D2;
+        // issue the tile of plane p into its ring slot (one commit group per plane, possibly empty)
+        auto issue = [&](int p) {
+            if (p <= j_end) {
+                if (MODE == 1) {
+                    const int64_t fp = (int64_t)__ldg(lm.m0 + p) * fplane;
+                    for (int e = tid; e < kTY * kTX; e += 256) {
+                        const int yy = e >> 5, xx = e & 31;
+                        const int gy = y0 + 1 + yy, gx = x0 + 1 + xx;
+                        if (gy < n1 && gx < n2)
+                            cp_elem(&ring[p % kRing][yy + 1][xx + 1],
+                                    (const TIn *)(coef_in + fp + (int64_t)__ldg(lm.m1 + gy) * lm.D2 + __ldg(lm.m2 + gx)));
+                    }
+                } else {
+                    const TIn *src = F + (int64_t)p * plane;
+                    for (int e = tid; e < kHY * kHX; e += 256) {
+                        const int yy = e / kHX, xx = e - yy * kHX;
+                        const int gy = y0 + yy, gx = x0 + xx;
+                        if (gy >= 0 && gy < n1 && gx >= 0 && gx < n2)
+                            cp_elem(&ring[p % kRing][yy][xx], src + (int64_t)gy * n2 + gx);
+                    }
+                }
+            }
+            cp_async_commit();
+        };
+        Nb b1{}, b2{};
+        if (act) {
+            b1 = neighbours<A1>(ax1, j1);
+            b2 = neighbours<A2>(ax2, j2);
+        }
+        const int nc1 = A1 ? ax1.nc : n1, nc2 = A2 ? ax2.nc : n2;
+        const int64_t col = (int64_t)j1 * n2 + j2;
+        const int64_t fcol = act ? ((int64_t)__ldg(lm.m1 + j1)) * lm.D2 + __ldg(lm.m2 + j2) : 0;
         March M;
         M.m1 = M.m2 = M.ya = M.yb = M.yc = 0.0;
         M.c = c_lo;
         auto emit = [&](int c, double z) { Z0[(int64_t)c * plane + col] = z; };
+        for (int k = 0; k < kRing - 2; k++) issue(j_start + k);
         for (int j = j_start; j <= j_end; j++) {
+            cp_async_wait<kRing - 4>();   // planes <= j + 1 have landed
+            __syncthreads();
+            issue(j + kRing - 2);          // into the slot of plane j - 2 (no longer read)
+            if (!act) continue;
             const Nb b0 = neighbours<A0>(ax0, j);
             const bool coarse_node = !b0.fo && !b1.fo && !b2.fo;
-            const int64_t f = (int64_t)lm.m0[j] * fplane + fcol;
             double mc;
             if (MODE != 1) {
+                auto S = [&](int pl, int y, int x) -> double { return (double)ring[pl % kRing][y - y0][x - x0]; };
                 // GPK: P0 along axis 0 at the corner columns, then P1 along axis 1, then P2 along axis 2
                 auto P0 = [&](int y1, int x2) -> double {
-                    const double va = ld(F + (int64_t)b0.fa * plane + (int64_t)y1 * n2 + x2);
+                    const double va = S(b0.fa, y1, x2);
                     if (!b0.fo) return va;
-                    const double vb = ld(F + (int64_t)b0.fb * plane + (int64_t)y1 * n2 + x2);
-                    return lerp(va, vb, b0.t);
+                    return lerp(va, S(b0.fb, y1, x2), b0.t);
                 };
                 auto P1 = [&](int x2) -> double {
                     const double va = P0(b1.fa, x2);
@@ -172,9 +215,10 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
                 };
                 double pred = P1(b2.fa);
                 if (b2.fo) pred = lerp(pred, P1(b2.fb), b2.t);
-                const double own = ld(F + (int64_t)j * plane + col);
+                const double own = S(j, j1, j2);
                 mc = dsub(own, pred);
                 if (j >= own_lo && j < own_hi) {
+                    const int64_t f = (int64_t)__ldg(lm.m0 + j) * fplane + fcol;
                     if (coarse_node) {
                         const int c0 = A0 ? b0.ca : j;
                         Cg[((int64_t)c0 * nc1 + b1.ca) * nc2 + b2.ca] = own;
@@ -201,11 +245,12 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
                     }
                 }
             } else {
-                mc = coarse_node ? 0.0 : coef_in[f];
+                mc = coarse_node ? 0.0 : (double)ring[j % kRing][ty + 1][tx + 1];
             }
             if (A0) march_push(M, ax0, n0, j, j_start, mc, c_hi, emit);
             else Z0[(int64_t)j * plane + col] = mc;
         }
+        cp_async_wait<0>();
     }
     if (MODE == 2) {
         if (fl) atomicOr(q.flags, fl);
@@ -234,9 +279,11 @@ __global__ void k_quantize_coarsest(const double *__restrict__ vals, const long 
 }
 
 // ---------------------------------------------------------------------------------- pass 2
-// Z0 (m0, n1, n2) -> B (m0, nc1, nc2): axis-1 LPK as a march, axis-2 LPK across the block.
+// Z0 (m0, n1, n2) -> B (m0, nc1, nc2): axis-1 LPK as a march over rows streamed through a
+// cp.async ring, axis-2 LPK across the block through shared memory.
 constexpr int kP2Threads = 256;
 constexpr int kP2Out = (kP2Threads - 4) / 2;   // coarse outputs along axis 2 per block
+constexpr int kP2Ring = 8;
 
 template <bool A1, bool A2>
 __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__restrict__ Z0, int m0, int n1, int n2,
@@ -244,6 +291,7 @@ __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__rest
                                                             int slabs1) {
     __shared__ double sw[kP2Threads];
     __shared__ double sy[kP2Threads];
+    __shared__ __align__(16) double ring[kP2Ring][kP2Threads];
     const int t = threadIdx.x;
     const int p = blockIdx.y;
     const int nc1 = A1 ? ax1.nc : n1, nc2 = A2 ? ax2.nc : n2;
@@ -251,7 +299,7 @@ __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__rest
     if (A2) {
         c2_lo = blockIdx.x * kP2Out;
         c2_cnt = min(kP2Out, nc2 - c2_lo);
-        base = ax2.r0[c2_lo] - 2;
+        base = __ldg(ax2.r0 + c2_lo) - 2;
     } else {
         base = blockIdx.x * kP2Threads;
     }
@@ -262,6 +310,22 @@ __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__rest
     if (c_lo >= c_hi) return;   // uniform across the block
     const double *zp = Z0 + (int64_t)p * n1 * n2;
     double *bp = B + (int64_t)p * nc1 * nc2;
+    // per-thread constants of the axis-2 stencil
+    double md2 = 0, ml2 = 0, mu2 = 0, wr2 = 0, wl2 = 0;
+    int r02 = 0, rr2 = -1, rl2 = -1;
+    if (A2 && in) {
+        md2 = __ldg(ax2.md + j2);
+        ml2 = __ldg(ax2.ml + j2);
+        mu2 = __ldg(ax2.mu + j2);
+    }
+    if (A2 && t < c2_cnt) {
+        const int c2 = c2_lo + t;
+        r02 = __ldg(ax2.r0 + c2) - base;
+        rr2 = __ldg(ax2.rr + c2);
+        rl2 = __ldg(ax2.rl + c2);
+        wr2 = __ldg(ax2.wr + c2);
+        wl2 = __ldg(ax2.wl + c2);
+    }
     auto out_row = [&](int c1, double w) {
         if (!A2) {
             if (in) bp[(int64_t)c1 * nc2 + j2] = w;
@@ -271,60 +335,84 @@ __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__rest
         __syncthreads();
         double y = 0.0;
         if (in) {
-            y = dmul(ax2.md[j2], sw[t]);
-            if (j2 >= 1 && t >= 1) y = dadd(y, dmul(ax2.ml[j2], sw[t - 1]));
-            if (j2 + 1 < n2 && t + 1 < kP2Threads) y = dadd(y, dmul(ax2.mu[j2], sw[t + 1]));
+            y = dmul(md2, sw[t]);
+            if (j2 >= 1 && t >= 1) y = dadd(y, dmul(ml2, sw[t - 1]));
+            if (j2 + 1 < n2 && t + 1 < kP2Threads) y = dadd(y, dmul(mu2, sw[t + 1]));
         }
         sy[t] = y;
         __syncthreads();
         if (t < c2_cnt) {
-            const int c2 = c2_lo + t;
-            const int r0 = ax2.r0[c2] - base, rr = ax2.rr[c2], rl = ax2.rl[c2];
-            double z = sy[r0];
-            if (rr >= 0) z = dadd(z, dmul(ax2.wr[c2], sy[rr - base]));
-            if (rl >= 0) z = dadd(z, dmul(ax2.wl[c2], sy[rl - base]));
-            bp[(int64_t)c1 * nc2 + c2] = z;
+            double z = sy[r02];
+            if (rr2 >= 0) z = dadd(z, dmul(wr2, sy[rr2 - base]));
+            if (rl2 >= 0) z = dadd(z, dmul(wl2, sy[rl2 - base]));
+            bp[(int64_t)c1 * nc2 + c2_lo + t] = z;
         }
-        __syncthreads();
     };
-    if (!A1) {
-        for (int j1 = c_lo; j1 < c_hi; j1++) out_row(j1, in ? ld(zp + (int64_t)j1 * n2 + j2) : 0.0);
-        return;
+    int j_start, j_end;
+    if (A1) {
+        j_start = max(0, __ldg(ax1.r0 + c_lo) - 2);
+        j_end = min(n1 - 1, __ldg(ax1.r0 + c_hi - 1) + 2);
+    } else {
+        j_start = c_lo;
+        j_end = c_hi - 1;
     }
-    const int j_start = max(0, ax1.r0[c_lo] - 2);
-    const int j_end = min(n1 - 1, ax1.r0[c_hi - 1] + 2);
+    // each thread streams its own column: no barrier needed for the ring itself
+    auto issue = [&](int r) {
+        if (r <= j_end && in) cp_async<8>(&ring[r % kP2Ring][t], zp + (int64_t)r * n2 + j2);
+        cp_async_commit();
+    };
+    for (int k = 0; k < kP2Ring - 1; k++) issue(j_start + k);
     March M;
     M.m1 = M.m2 = M.ya = M.yb = M.yc = 0.0;
     M.c = c_lo;
     for (int j = j_start; j <= j_end; j++) {
-        const double x = in ? ld(zp + (int64_t)j * n2 + j2) : 0.0;
-        march_push(M, ax1, n1, j, j_start, x, c_hi, out_row);
+        cp_async_wait<kP2Ring - 2>();   // row j has landed (own copies)
+        const double x = in ? ring[j % kP2Ring][t] : 0.0;
+        issue(j + kP2Ring - 1);          // into the slot of row j - 1
+        if (A1) march_push(M, ax1, n1, j, j_start, x, c_hi, out_row);
+        else out_row(j, x);
     }
+    cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------------- final
 // Recompose output of one transition: D(j) = P(cv)(j) + mc(j) (transform.py:346-347), P the
 // nested lerps over the corrected coarse values cv (nc0, nc1, nc2), mc from the coefficients.
+// Each thread prefetches its own coefficient column through a private cp.async ring.
+constexpr int kFRing = 8;
+
 template <bool A0, bool A1, bool A2, typename TOut>
 __global__ void __launch_bounds__(256) k_level_final(const double *__restrict__ cv, int n0, int n1, int n2,
                                                      DevAxis ax0, DevAxis ax1, DevAxis ax2, LevelMap lm,
                                                      const double *__restrict__ coef, TOut *__restrict__ D) {
+    __shared__ __align__(16) double ring[kFRing][256];
+    const int tid = threadIdx.y * 32 + threadIdx.x;
     const int j2 = blockIdx.x * 32 + threadIdx.x;
     const int j1 = blockIdx.y * 8 + threadIdx.y;
-    if (j1 >= n1 || j2 >= n2) return;
+    if (j1 >= n1 || j2 >= n2) return;   // no block-wide barriers below
     const Nb b1 = neighbours<A1>(ax1, j1), b2 = neighbours<A2>(ax2, j2);
     const int nc1 = A1 ? ax1.nc : n1, nc2 = A2 ? ax2.nc : n2;
     int lo, hi;
     slab_range(n0, gridDim.z, blockIdx.z, lo, hi);
     const int64_t col = (int64_t)j1 * n2 + j2;
-    const int64_t fcol = ((int64_t)lm.m1[j1]) * lm.D2 + lm.m2[j2];
+    const int64_t fcol = ((int64_t)__ldg(lm.m1 + j1)) * lm.D2 + __ldg(lm.m2 + j2);
+    const int64_t fplane = lm.D1 * lm.D2;
     const int64_t cplane = (int64_t)nc1 * nc2;
+    const bool col_fo = b1.fo || b2.fo;
+    auto issue = [&](int j) {
+        if (j < hi) {
+            const bool fo0 = A0 && __ldg(ax0.pb + j) >= 0;
+            if (fo0 || col_fo) cp_async<8>(&ring[j % kFRing][tid], coef + (int64_t)__ldg(lm.m0 + j) * fplane + fcol);
+        }
+        cp_async_commit();
+    };
+    for (int k = 0; k < kFRing - 1; k++) issue(lo + k);
     for (int j = lo; j < hi; j++) {
         const Nb b0 = neighbours<A0>(ax0, j);
         auto P0 = [&](int y1, int x2) -> double {
-            const double va = cv[(int64_t)b0.ca * cplane + (int64_t)y1 * nc2 + x2];
+            const double va = __ldg(cv + (int64_t)b0.ca * cplane + (int64_t)y1 * nc2 + x2);
             if (!b0.fo) return va;
-            return lerp(va, cv[(int64_t)b0.cb * cplane + (int64_t)y1 * nc2 + x2], b0.t);
+            return lerp(va, __ldg(cv + (int64_t)b0.cb * cplane + (int64_t)y1 * nc2 + x2), b0.t);
         };
         auto P1 = [&](int x2) -> double {
             const double va = P0(b1.ca, x2);
@@ -333,10 +421,13 @@ __global__ void __launch_bounds__(256) k_level_final(const double *__restrict__ 
         };
         double pred = P1(b2.ca);
         if (b2.fo) pred = lerp(pred, P1(b2.cb), b2.t);
-        const bool coarse_node = !b0.fo && !b1.fo && !b2.fo;
-        const double mc = coarse_node ? 0.0 : __ldg(coef + (int64_t)lm.m0[j] * lm.D1 * lm.D2 + fcol);
+        const bool coarse_node = !b0.fo && !col_fo;
+        cp_async_wait<kFRing - 2>();
+        const double mc = coarse_node ? 0.0 : ring[j % kFRing][tid];
+        issue(j + kFRing - 1);
         D[(int64_t)j * n1 * n2 + col] = (TOut)dadd(pred, mc);
     }
+    cp_async_wait<0>();
 }
 
 int slabs_for(int64_t cols, int planes) {
@@ -350,8 +441,8 @@ void launch_pass1(int act, const TIn *F, int n0, int n1, int n2, const DevAxis &
                   const DevAxis &a2, const LevelMap &lm, double *coef, const double *coef_in, double *Z0, double *Cg,
                   const QuantOut &q, cudaStream_t s) {
     const int planes = (act & 1) ? a0.nc : n0;
-    dim3 grid((n2 + 31) / 32, (n1 + 7) / 8, slabs_for((int64_t)n1 * n2, planes));
-    dim3 block(32, 8);
+    dim3 grid((n2 + kTX - 1) / kTX, (n1 + kTY - 1) / kTY, slabs_for((int64_t)n1 * n2, planes));
+    dim3 block(kTX, kTY);
 #define P1L(M)                                                                                                     \
     case M:                                                                                                        \
         k_level_pass1<MODE, (M & 1) != 0, (M & 2) != 0, (M & 4) != 0, TIn><<<grid, block, 0, s>>>(              \
@@ -392,6 +483,27 @@ void launch_final(int act, const double *cv, int n0, int n1, int n2, const DevAx
     LAUNCH_CHECK();
 }
 
+struct View {
+    int n0, n1, n2, act;
+    LevelMap lm;
+};
+
+View view_of(const DevPlan &p, int st_i) {
+    const DevStep &st = p.steps[st_i];
+    View v;
+    v.n0 = (int)st.fsh.n[1];
+    v.n1 = (int)st.fsh.n[2];
+    v.n2 = (int)st.fsh.n[3];
+    v.act = (st.ax[1].active ? 1 : 0) | (st.ax[2].active ? 2 : 0) | (st.ax[3].active ? 4 : 0);
+    v.lm = LevelMap{p.map[1][st_i], p.map[2][st_i], p.map[3][st_i], p.dims.n[2], p.dims.n[3]};
+    return v;
+}
+
+int64_t z0_size(const DevPlan &p, int st_i) {
+    const DevStep &st = p.steps[st_i];
+    return (int64_t)(st.ax[1].active ? st.ax[1].nc : st.fsh.n[1]) * st.fsh.n[2] * st.fsh.n[3];
+}
+
 }  // namespace
 
 bool fused_supported(const DevPlan &p) { return p.dims.n[0] == 1; }
@@ -399,45 +511,36 @@ bool fused_supported(const DevPlan &p) { return p.dims.n[0] == 1; }
 void fused_pass1_decompose(const DevPlan &p, int st_i, const void *F, bool f32, double *coef, double *Z0, double *Cg,
                            cudaStream_t s) {
     const DevStep &st = p.steps[st_i];
-    const int n0 = (int)st.fsh.n[1], n1 = (int)st.fsh.n[2], n2 = (int)st.fsh.n[3];
-    const int act = (st.ax[1].active ? 1 : 0) | (st.ax[2].active ? 2 : 0) | (st.ax[3].active ? 4 : 0);
-    LevelMap lm{p.map[1][st_i], p.map[2][st_i], p.map[3][st_i], p.dims.n[2], p.dims.n[3]};
+    const View v = view_of(p, st_i);
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
-    const int64_t zsz = (int64_t)((act & 1) ? st.ax[1].nc : n0) * n1 * n2;
-    KPROF("k_level_pass1", (f32 ? 4.0 : 8.0) * nf + 8.0 * (nf - nc) + 8.0 * nc + 8.0 * zsz, s);
+    KPROF("k_level_pass1", (f32 ? 4.0 : 8.0) * nf + 8.0 * (nf - nc) + 8.0 * nc + 8.0 * z0_size(p, st_i), s);
     const QuantOut q{};
-    if (f32) launch_pass1<0, float>(act, (const float *)F, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, coef,
-                                    nullptr, Z0, Cg, q, s);
-    else launch_pass1<0, double>(act, (const double *)F, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, coef,
-                                 nullptr, Z0, Cg, q, s);
-}
-
-void fused_pass1_recompose(const DevPlan &p, int st_i, const double *coef, double *Z0, cudaStream_t s) {
-    const DevStep &st = p.steps[st_i];
-    const int n0 = (int)st.fsh.n[1], n1 = (int)st.fsh.n[2], n2 = (int)st.fsh.n[3];
-    const int act = (st.ax[1].active ? 1 : 0) | (st.ax[2].active ? 2 : 0) | (st.ax[3].active ? 4 : 0);
-    LevelMap lm{p.map[1][st_i], p.map[2][st_i], p.map[3][st_i], p.dims.n[2], p.dims.n[3]};
-    const int64_t nf = st.fsh.size(), nc = st.csh.size();
-    const int64_t zsz = (int64_t)((act & 1) ? st.ax[1].nc : n0) * n1 * n2;
-    KPROF("k_level_pass1r", 8.0 * (nf - nc) + 8.0 * zsz, s);
-    const QuantOut q{};
-    launch_pass1<1, double>(act, nullptr, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, nullptr, coef, Z0, nullptr,
-                            q, s);
+    if (f32) launch_pass1<0, float>(v.act, (const float *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
+                                    coef, nullptr, Z0, Cg, q, s);
+    else launch_pass1<0, double>(v.act, (const double *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
+                                 coef, nullptr, Z0, Cg, q, s);
 }
 
 void fused_pass1_quantize(const DevPlan &p, int st_i, const void *F, bool f32, const QuantOut &q, double *Z0,
                           double *Cg, cudaStream_t s) {
     const DevStep &st = p.steps[st_i];
-    const int n0 = (int)st.fsh.n[1], n1 = (int)st.fsh.n[2], n2 = (int)st.fsh.n[3];
-    const int act = (st.ax[1].active ? 1 : 0) | (st.ax[2].active ? 2 : 0) | (st.ax[3].active ? 4 : 0);
-    LevelMap lm{p.map[1][st_i], p.map[2][st_i], p.map[3][st_i], p.dims.n[2], p.dims.n[3]};
+    const View v = view_of(p, st_i);
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
-    const int64_t zsz = (int64_t)((act & 1) ? st.ax[1].nc : n0) * n1 * n2;
-    KPROF("k_level_pass1q", (f32 ? 4.0 : 8.0) * nf + 4.0 * (nf - nc) + 8.0 * nc + 8.0 * zsz, s);
-    if (f32) launch_pass1<2, float>(act, (const float *)F, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, nullptr,
-                                    nullptr, Z0, Cg, q, s);
-    else launch_pass1<2, double>(act, (const double *)F, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, nullptr,
-                                 nullptr, Z0, Cg, q, s);
+    KPROF("k_level_pass1q", (f32 ? 4.0 : 8.0) * nf + 4.0 * (nf - nc) + 8.0 * nc + 8.0 * z0_size(p, st_i), s);
+    if (f32) launch_pass1<2, float>(v.act, (const float *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
+                                    nullptr, nullptr, Z0, Cg, q, s);
+    else launch_pass1<2, double>(v.act, (const double *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
+                                 nullptr, nullptr, Z0, Cg, q, s);
+}
+
+void fused_pass1_recompose(const DevPlan &p, int st_i, const double *coef, double *Z0, cudaStream_t s) {
+    const DevStep &st = p.steps[st_i];
+    const View v = view_of(p, st_i);
+    const int64_t nf = st.fsh.size(), nc = st.csh.size();
+    KPROF("k_level_pass1r", 8.0 * (nf - nc) + 8.0 * z0_size(p, st_i), s);
+    const QuantOut q{};
+    launch_pass1<1, double>(v.act, nullptr, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, nullptr, coef, Z0,
+                            nullptr, q, s);
 }
 
 void quantize_coarsest(const DevPlan &p, const double *coarsest_vals, const QuantOut &q, cudaStream_t s) {
@@ -449,25 +552,22 @@ void quantize_coarsest(const DevPlan &p, const double *coarsest_vals, const Quan
 
 void fused_pass2(const DevPlan &p, int st_i, const double *Z0, double *B, cudaStream_t s) {
     const DevStep &st = p.steps[st_i];
-    const int n0 = (int)st.fsh.n[1], n1 = (int)st.fsh.n[2], n2 = (int)st.fsh.n[3];
-    const int act = (st.ax[1].active ? 1 : 0) | (st.ax[2].active ? 2 : 0) | (st.ax[3].active ? 4 : 0);
-    const int m0 = (act & 1) ? st.ax[1].nc : n0;
-    KPROF("k_level_pass2", 8.0 * m0 * n1 * n2 + 8.0 * st.csh.size(), s);
-    launch_pass2(act, Z0, m0, n1, n2, st.ax[2], st.ax[3], B, s);
+    const View v = view_of(p, st_i);
+    const int m0 = (v.act & 1) ? st.ax[1].nc : v.n0;
+    KPROF("k_level_pass2", 8.0 * m0 * v.n1 * v.n2 + 8.0 * st.csh.size(), s);
+    launch_pass2(v.act, Z0, m0, v.n1, v.n2, st.ax[2], st.ax[3], B, s);
 }
 
 void fused_final(const DevPlan &p, int st_i, const double *cv, const double *coef, void *D, int out_dtype,
                  cudaStream_t s) {
     const DevStep &st = p.steps[st_i];
-    const int n0 = (int)st.fsh.n[1], n1 = (int)st.fsh.n[2], n2 = (int)st.fsh.n[3];
-    const int act = (st.ax[1].active ? 1 : 0) | (st.ax[2].active ? 2 : 0) | (st.ax[3].active ? 4 : 0);
-    LevelMap lm{p.map[1][st_i], p.map[2][st_i], p.map[3][st_i], p.dims.n[2], p.dims.n[3]};
+    const View v = view_of(p, st_i);
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
     KPROF("k_level_final", 8.0 * nc + 8.0 * (nf - nc) + (out_dtype == 0 ? 4.0 : 8.0) * nf, s);
     if (out_dtype == 0)
-        launch_final<float>(act, cv, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, coef, (float *)D, s);
+        launch_final<float>(v.act, cv, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, coef, (float *)D, s);
     else
-        launch_final<double>(act, cv, n0, n1, n2, st.ax[1], st.ax[2], st.ax[3], lm, coef, (double *)D, s);
+        launch_final<double>(v.act, cv, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, coef, (double *)D, s);
 }
 
 }  // namespace hpdr

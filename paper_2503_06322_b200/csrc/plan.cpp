@@ -56,6 +56,12 @@ static void axis_tables(AxisTables &a, const std::vector<int32_t> &fine, const s
         a.rl[bi] = (int32_t)f;
         a.wl[bi] = t;
     }
+    a.fa.assign(n, 0);
+    a.fb.assign(n, 0);
+    for (int64_t f = 0; f < n; f++) {
+        a.fa[f] = a.r0[a.pa[f]];
+        a.fb[f] = a.pb[f] >= 0 ? a.r0[a.pb[f]] : a.fa[f];
+    }
     mass_bands(fine, a.ml, a.md, a.mu);
     std::vector<double> cl, cd;
     mass_bands(coarse, cl, cd, a.tu);

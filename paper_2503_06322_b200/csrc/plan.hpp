@@ -18,6 +18,7 @@ struct AxisTables {
     // prolong (GPK), per fine node j: pa/pb coarse neighbours (pb < 0: copy of coarse pa), t weight
     std::vector<int32_t> pa, pb;
     std::vector<double> pt;
+    std::vector<int32_t> fa, fb;   // fine indices of those coarse neighbours (fa = fb = j at coarse nodes)
     // mass-transfer (LPK), per coarse node c: own fine index r0, right/left fine-only
     // neighbours rr/rl (-1 when absent), weights wr = 1 - t_R and wl = t_L
     std::vector<int32_t> r0, rr, rl;

@@ -296,6 +296,64 @@ __global__ void __launch_bounds__(kThomasWarps * 32) k_thomas_contig(double *__r
     }
 }
 
+// Register-blocked sweeps: one thread per line, U values of the line loaded ahead of the
+// recurrence (double-buffered), so the sequential dependency never waits on DRAM.  Works for
+// strided (inner > 1, coalesced across threads) and contiguous (inner == 1) lines alike.
+template <int U>
+__global__ void __launch_bounds__(128) k_thomas_reg(double *__restrict__ arr, int64_t outer, int32_t n, int64_t inner,
+                                                    const double *__restrict__ tw, const double *__restrict__ tb,
+                                                    const double *__restrict__ tu) {
+    const int64_t lines = outer * inner;
+    for (int64_t ln = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ln < lines; ln += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = ln / inner, q = ln - p * inner;
+        double *x = arr + p * (int64_t)n * inner + q;
+        double cur[U], nxt[U];
+        auto load = [&](double *buf, int i0) {
+#pragma unroll
+            for (int k = 0; k < U; k++) {
+                const int i = i0 + k;
+                if (i >= 0 && i < n) buf[k] = x[(int64_t)i * inner];
+            }
+        };
+        // forward elimination: x_i -= w_i x_{i-1}
+        double prev = x[0];
+        load(cur, 1);
+        for (int i0 = 1; i0 < n; i0 += U) {
+            if (i0 + U < n) load(nxt, i0 + U);
+#pragma unroll
+            for (int k = 0; k < U; k++) {
+                const int i = i0 + k;
+                if (i < n) {
+                    const double v = dsub(cur[k], dmul(__ldg(tw + i), prev));
+                    x[(int64_t)i * inner] = v;
+                    prev = v;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < U; k++) cur[k] = nxt[k];
+        }
+        double last = ddiv(prev, __ldg(tb + n - 1));
+        x[(int64_t)(n - 1) * inner] = last;
+        // back substitution: x_i = (x_i - u_i x_{i+1}) / b'_i, i = n-2 .. 0
+        load(cur, n - 1 - U);
+        for (int i1 = n - 2; i1 >= 0; i1 -= U) {
+            if (i1 - U >= 0) load(nxt, i1 - 2 * U + 1);
+#pragma unroll
+            for (int k = U - 1; k >= 0; k--) {
+                const int i = i1 - (U - 1 - k);
+                if (i >= 0) {
+                    double v = dsub(cur[k], dmul(__ldg(tu + i), last));
+                    v = ddiv(v, __ldg(tb + i));
+                    x[(int64_t)i * inner] = v;
+                    last = v;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < U; k++) cur[k] = nxt[k];
+        }
+    }
+}
+
 // ---------------------------------------------------------------- elementwise
 __global__ void k_add(const double *__restrict__ a, const double *__restrict__ b, double *__restrict__ o, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -366,7 +424,11 @@ void thomas(double *arr, const Shape4 &csh, int a, const DevAxis &ax, cudaStream
     int64_t outer, inner;
     view(csh, a, outer, inner);
     KPROF(inner == 1 ? "k_thomas_contig" : "k_thomas_strided", 16.0 * outer * inner * ax.nc, s);
-    if (inner == 1) {
+    static const bool legacy = getenv("HPDR_THOMAS_LEGACY") != nullptr;
+    if (!legacy) {
+        const int64_t lines = outer * inner;
+        k_thomas_reg<8><<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb, ax.tu);
+    } else if (inner == 1) {
         int64_t lines = outer;
         unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((lines + 127) / 128, 148 * 16));
         k_thomas_contig<<<g, kThomasWarps * 32, 0, s>>>(arr, lines, ax.nc, ax.tw, ax.tb, ax.tu);
