@@ -237,6 +237,7 @@ void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict
 namespace {
 
 constexpr int kLutSize = 1 << kLutBits;
+constexpr int kDecThreads = 64;
 
 struct DecTables {
     long long first_code[258];
@@ -261,6 +262,7 @@ __global__ void k_decode(const uint32_t *__restrict__ words, uint64_t limit, con
                          unsigned *__restrict__ max_key) {
     __shared__ uint32_t lut[kLutSize];
     __shared__ DecTables T;
+    __shared__ uint32_t stage[kDecThreads][9];
     for (int i = threadIdx.x; i < kLutSize; i += blockDim.x) lut[i] = lut_g[i];
     for (int i = threadIdx.x; i < (int)(sizeof(DecTables) / 8); i += blockDim.x)
         ((long long *)&T)[i] = ((const long long *)tabs_g)[i];
@@ -272,6 +274,77 @@ __global__ void k_decode(const uint32_t *__restrict__ words, uint64_t limit, con
         const uint64_t cnt = nsym - lo < (uint64_t)kBlockSymbols ? nsym - lo : (uint64_t)kBlockSymbols;
         uint64_t pos = offs[u];
         long long err = -1;
+        if (max_len <= 32 && pos < limit) {
+            // Fast path: 64-bit bit buffer refilled a word at a time (next word prefetched),
+            // 12-bit table lookup, canonical search for longer codes; 8 symbols per vector store.
+            uint64_t wi = pos >> 5;
+            uint64_t buf = (((uint64_t)load_be(words, wi) << 32) | load_be(words, wi + 1)) << (pos & 31);
+            int avail = 64 - (int)(pos & 31);
+            uint64_t nw = wi + 2;
+            uint32_t pre = load_be(words, nw);
+            uint32_t *s8 = stage[threadIdx.x];   // private 8-symbol staging row
+            uint64_t i = 0;
+            for (; i < cnt; i++) {
+                if (avail < 32) {
+                    buf |= (uint64_t)pre << (32 - avail);
+                    avail += 32;
+                    pre = load_be(words, ++nw);
+                }
+                if (pos >= limit) { err = (long long)pos; break; }
+                const uint32_t win = (uint32_t)(buf >> 32);
+                const uint32_t e = lut[win >> (32 - kLutBits)];
+                uint32_t sym = e >> 8;
+                int L = (int)(e & 0xffu);
+                if (!L) {
+                    for (int l = kLutBits + 1; l <= max_len; l++) {
+                        const long long idx = (long long)(win >> (32 - l)) - T.first_code[l];
+                        if (idx >= 0 && idx < T.cnt[l]) {
+                            L = l;
+                            sym = sym_by_rank[T.first_rank[l] + idx];
+                            break;
+                        }
+                    }
+                }
+                if (L == 0 || pos + (uint64_t)L > limit) { err = (long long)pos; break; }
+                pos += L;
+                buf <<= L;
+                avail -= L;
+                kmax = sym > kmax ? sym : kmax;
+                s8[i & 7] = sym;
+                if ((i & 7) == 7) {
+                    const uint64_t o = lo + i - 7;
+                    if (keys) {
+                        uint4 *kp = reinterpret_cast<uint4 *>(keys + o);
+                        kp[0] = make_uint4(s8[0], s8[1], s8[2], s8[3]);
+                        kp[1] = make_uint4(s8[4], s8[5], s8[6], s8[7]);
+                    }
+                    if (coef) {
+                        double2 *cp = reinterpret_cast<double2 *>(coef + o);
+#pragma unroll
+                        for (int k = 0; k < 4; k++) {
+                            const long long b0 = (long long)(s8[2 * k] >> 1) ^ -(long long)(s8[2 * k] & 1u);
+                            const long long b1 = (long long)(s8[2 * k + 1] >> 1) ^ -(long long)(s8[2 * k + 1] & 1u);
+                            cp[k] = make_double2(__dmul_rn((double)b0, bin), __dmul_rn((double)b1, bin));
+                        }
+                    }
+                }
+            }
+            if (err < 0) {   // tail of the last (partial) unit
+                for (uint64_t k = cnt & ~7ULL; k < cnt; k++) {
+                    const uint32_t sym = s8[k & 7];
+                    if (keys) keys[lo + k] = sym;
+                    if (coef) {
+                        const long long b = (long long)(sym >> 1) ^ -(long long)(sym & 1u);
+                        coef[lo + k] = __dmul_rn((double)b, bin);
+                    }
+                }
+            }
+            if (err >= 0) {
+                unit_err[u] = err;
+                atomicMin(first_bad, (unsigned long long)u);
+            }
+            continue;
+        }
         for (uint64_t i = 0; i < cnt; i++) {
             const uint64_t cw = pos;
             uint32_t sym = 0;
@@ -407,7 +480,7 @@ void decode_device(hpdr_ctx *ctx, const DecodeJob &job, DecodeResult &res, cudaS
     if (units > 0) {
         KPROF("k_decode", job.total_bits / 8.0 + 8.0 * units +
                               (double)job.n_symbols * ((job.keys ? 4 : 0) + (job.coef ? 8 : 0)), s);
-        k_decode<<<grid_for(units, 64, 148 * 64), 64, 0, s>>>(
+        k_decode<<<grid_for(units, kDecThreads, 148 * 64), kDecThreads, 0, s>>>(
             d_words, job.total_bits, d_off, job.n_symbols, units, (const DecTables *)d_tab,
             (const uint32_t *)(d_tab + sizeof(DecTables)),
             (const uint32_t *)(d_tab + sizeof(DecTables) + kLutSize * 4), job.keys, job.coef, job.bin_width,
