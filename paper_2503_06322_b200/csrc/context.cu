@@ -155,7 +155,7 @@ DevPlan &hpdr_ctx::plan(int rank, const uint64_t *dims) {
     HostPlan &h = dp->host;
     if (h.L > kMaxLevels) throw Error{HPDR_ERR_VALIDATION, "too many levels", -1};
     Packer pk;
-    struct AxOff { size_t pa, pb, pt, fa, fb, r0, rr, rl, wr, wl, ml, md, mu, tw, tb, tu; };
+    struct AxOff { size_t pa, pb, pt, fa, fb, r0, rr, rl, wr, wl, ml, md, mu, tw, tb, tu, pi; };
     std::vector<std::vector<AxOff>> offs(h.steps.size(), std::vector<AxOff>(4));
     for (size_t s = 0; s < h.steps.size(); s++)
         for (int d = 0; d < 4; d++) {
@@ -164,6 +164,7 @@ DevPlan &hpdr_ctx::plan(int rank, const uint64_t *dims) {
             AxOff &o = offs[s][d];
             o.pa = pk.put(a.pa); o.pb = pk.put(a.pb); o.pt = pk.put(a.pt);
             o.fa = pk.put(a.fa); o.fb = pk.put(a.fb);
+            o.pi = pk.put(a.pinfo);
             o.r0 = pk.put(a.r0); o.rr = pk.put(a.rr); o.rl = pk.put(a.rl);
             o.wr = pk.put(a.wr); o.wl = pk.put(a.wl);
             o.ml = pk.put(a.ml); o.md = pk.put(a.md); o.mu = pk.put(a.mu);
@@ -200,6 +201,7 @@ DevPlan &hpdr_ctx::plan(int rank, const uint64_t *dims) {
             x.pa = (const int32_t *)(base + o.pa); x.pb = (const int32_t *)(base + o.pb);
             x.pt = (const double *)(base + o.pt);
             x.fa = (const int32_t *)(base + o.fa); x.fb = (const int32_t *)(base + o.fb);
+            x.pi = (const PlaneInfo *)(base + o.pi);
             x.r0 = (const int32_t *)(base + o.r0); x.rr = (const int32_t *)(base + o.rr);
             x.rl = (const int32_t *)(base + o.rl);
             x.wr = (const double *)(base + o.wr); x.wl = (const double *)(base + o.wl);

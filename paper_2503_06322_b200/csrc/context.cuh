@@ -25,6 +25,7 @@ struct DevAxis {
     const double *wr, *wl;
     const double *ml, *md, *mu;
     const double *tw, *tb, *tu;
+    const PlaneInfo *pi;
 };
 
 struct DevStep {

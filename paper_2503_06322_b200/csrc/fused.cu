@@ -56,43 +56,87 @@ __device__ __forceinline__ Nb neighbours(const DevAxis &ax, int j) {
 // Sliding mass-multiply + restriction along the march axis (transform.py:206-226 then :181-203):
 //   y(j) = (md_j x_j + ml_j x_{j-1}) + mu_j x_{j+1}
 //   z(c) = (y(r0_c) + wr_c y(rr_c)) + wl_c y(rl_c)
+// driven by the host-built PlaneInfo records (which coarse output completes at which y).
 struct March {
     double m1, m2;        // x(j-1), x(j-2)
     double ya, yb, yc;    // y(k-2), y(k-1), y(k)
-    int c;                // next coarse output
+    double pmd, pml, pmu, pwr, pwl;   // PlaneInfo of j-1 (the y computed next)
+    int pemit, prr, prl;
 };
 
+__device__ __forceinline__ void march_init(March &M) {
+    M.m1 = M.m2 = M.ya = M.yb = M.yc = 0.0;
+    M.pmd = M.pml = M.pmu = M.pwr = M.pwl = 0.0;
+    M.pemit = -1;
+    M.prr = M.prl = 0;
+}
+
 template <class Emit>
-__device__ __forceinline__ void march_push(March &M, const DevAxis &ax, int n, int j, int j_start, double x, int c_hi,
-                                           Emit &&emit) {
-    auto try_y = [&](int k, double xk, double xkm1, double xkp1, bool has_up) {
-        double v = dmul(__ldg(ax.md + k), xk);
-        if (k >= 1) v = dadd(v, dmul(__ldg(ax.ml + k), xkm1));
-        if (has_up) v = dadd(v, dmul(__ldg(ax.mu + k), xkp1));
-        M.ya = M.yb;
-        M.yb = M.yc;
-        M.yc = v;
-        while (M.c < c_hi) {
-            const int r0 = __ldg(ax.r0 + M.c), rr = __ldg(ax.rr + M.c), rl = __ldg(ax.rl + M.c);
-            const int need = rr >= 0 ? rr : r0;
-            if (need != k) break;
-            double z;
-            if (rr >= 0) {
-                z = dadd(M.yb, dmul(__ldg(ax.wr + M.c), M.yc));
-                if (rl >= 0) z = dadd(z, dmul(__ldg(ax.wl + M.c), M.ya));
-            } else {
-                z = M.yc;
-                if (rl >= 0) z = dadd(z, dmul(__ldg(ax.wl + M.c), M.yb));
-            }
-            emit(M.c, z);
-            M.c++;
+__device__ __forceinline__ void march_y(March &M, double v, int emit, int rr, int rl, double wr, double wl,
+                                        Emit &&out) {
+    M.ya = M.yb;
+    M.yb = M.yc;
+    M.yc = v;
+    if (emit >= 0) {
+        double z;
+        if (rr) {
+            z = dadd(M.yb, dmul(wr, M.yc));
+            if (rl) z = dadd(z, dmul(wl, M.ya));
+        } else {
+            z = M.yc;
+            if (rl) z = dadd(z, dmul(wl, M.yb));
         }
-    };
+        out(emit, z);
+    }
+}
+
+// Push x(j) with its PlaneInfo pi; emits every restricted value that became computable.
+template <class Emit>
+__device__ __forceinline__ void march_push(March &M, const PlaneInfo &pi, int n, int j, int j_start, double x,
+                                           Emit &&out) {
     // y(j-1) needs x(j-2) unless j-1 == 0
-    if (j >= 1 && (j - 1 == 0 || j - 2 >= j_start)) try_y(j - 1, M.m1, M.m2, x, true);
-    if (j == n - 1 && (j == 0 || j - 1 >= j_start)) try_y(j, x, M.m1, 0.0, false);
+    if (j >= 1 && (j - 1 == 0 || j - 2 >= j_start)) {
+        double v = dmul(M.pmd, M.m1);
+        if (j - 1 >= 1) v = dadd(v, dmul(M.pml, M.m2));
+        v = dadd(v, dmul(M.pmu, x));
+        march_y(M, v, M.pemit, M.prr, M.prl, M.pwr, M.pwl, out);
+    }
+    if (j == n - 1 && (j == 0 || j - 1 >= j_start)) {
+        double v = dmul(pi.md, x);
+        if (j >= 1) v = dadd(v, dmul(pi.ml, M.m1));
+        march_y(M, v, pi.emit, pi.e_rr, pi.e_rl, pi.ewr, pi.ewl, out);
+    }
     M.m2 = M.m1;
     M.m1 = x;
+    M.pmd = pi.md;
+    M.pml = pi.ml;
+    M.pmu = pi.mu;
+    M.pwr = pi.ewr;
+    M.pwl = pi.ewl;
+    M.pemit = pi.emit;
+    M.prr = pi.e_rr;
+    M.prl = pi.e_rl;
+}
+
+__device__ __forceinline__ PlaneInfo load_pi(const PlaneInfo *__restrict__ p) {
+    PlaneInfo r;
+    const double2 *q = reinterpret_cast<const double2 *>(p);   // 80 bytes = 5 x 16 B
+#pragma unroll
+    for (int k = 0; k < 5; k++) {
+        const double2 v = __ldg(q + k);
+        memcpy((char *)&r + 16 * k, &v, 16);
+    }
+    return r;
+}
+
+__device__ __forceinline__ PlaneInfo identity_pi(int j) {
+    PlaneInfo r;
+    r.fa = r.fb = r.ca = r.cb = j;
+    r.t = r.md = r.ml = r.mu = r.ewr = r.ewl = 0.0;
+    r.fo = 0;
+    r.emit = -1;
+    r.e_rr = r.e_rl = 0;
+    return r;
 }
 
 __device__ __forceinline__ void slab_range(int nc, int nz, int z, int &lo, int &hi) {
@@ -128,8 +172,11 @@ __device__ __forceinline__ void cp_elem(T *s, const T *g) {
 // MODE 2 (decompose with quantize-on-write): as MODE 0 but fine-only nodes are quantized
 //   straight into keys / outlier mask / histogram (quantize.py:73-84) instead of coef.
 // Z0 = mc along axis 0 when that axis is inactive at this transition.
-// Block: 32 x 8 columns (j2, j1); planes of the tile (+1 halo) stream through a cp.async ring.
+// Block: 32 x 8 columns (j2, j1); each plane of the tile (+1 halo) streams through a cp.async
+// ring kRing-2 planes ahead of the march.  Per-thread smem / global offsets are fixed up front;
+// per-plane axis-0 data is one PlaneInfo record.
 constexpr int kTX = 32, kTY = 8, kHX = kTX + 2, kHY = kTY + 2, kRing = 8;
+constexpr int kPlaneElems = kHX * kHY;   // 340
 constexpr int kSmemHist = 4096;
 
 template <int MODE, bool A0, bool A1, bool A2, typename TIn>
@@ -137,7 +184,7 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
                                                      DevAxis ax1, DevAxis ax2, LevelMap lm, double *__restrict__ coef,
                                                      const double *__restrict__ coef_in, double *__restrict__ Z0,
                                                      double *__restrict__ Cg, QuantOut q) {
-    __shared__ __align__(16) TIn ring[kRing][kHY][kHX];
+    __shared__ __align__(16) TIn ring[kRing * kPlaneElems];
     __shared__ uint32_t sh_hist[MODE == 2 ? kSmemHist : 1];
     const bool sh_ok = MODE == 2 && q.dict <= kSmemHist;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
@@ -155,41 +202,50 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
         slab_planes<A0>(ax0, n0, nc0, c_lo, c_hi, j_start, j_end, own_lo, own_hi);
         const int64_t plane = (int64_t)n1 * n2;
         const int64_t fplane = lm.D1 * lm.D2;
-        // issue the tile of plane p into its ring slot (one commit group per plane, possibly empty)
+        const int own_off = (ty + 1) * kHX + tx + 1;
+        const int64_t col = (int64_t)j1 * n2 + j2;
+        const int64_t fcol = act ? ((int64_t)__ldg(lm.m1 + j1)) * lm.D2 + __ldg(lm.m2 + j2) : 0;
+        // this thread's share of each plane load: two tile elements (halo included)
+        int soff[2];
+        int64_t goff[2];
+        bool lv[2];
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            const int e = tid + k * 256;
+            const int yy = e / kHX, xx = e - yy * kHX;
+            const int gy = y0 + yy, gx = x0 + xx;
+            lv[k] = MODE != 1 && e < kPlaneElems && gy >= 0 && gy < n1 && gx >= 0 && gx < n2;
+            soff[k] = e;
+            goff[k] = (int64_t)gy * n2 + gx;
+        }
         auto issue = [&](int p) {
             if (p <= j_end) {
+                TIn *slot = ring + (p & (kRing - 1)) * kPlaneElems;
                 if (MODE == 1) {
-                    const int64_t fp = (int64_t)__ldg(lm.m0 + p) * fplane;
-                    for (int e = tid; e < kTY * kTX; e += 256) {
-                        const int yy = e >> 5, xx = e & 31;
-                        const int gy = y0 + 1 + yy, gx = x0 + 1 + xx;
-                        if (gy < n1 && gx < n2)
-                            cp_elem(&ring[p % kRing][yy + 1][xx + 1],
-                                    (const TIn *)(coef_in + fp + (int64_t)__ldg(lm.m1 + gy) * lm.D2 + __ldg(lm.m2 + gx)));
-                    }
+                    if (act)
+                        cp_async<sizeof(TIn)>(slot + own_off,
+                                              (const TIn *)(coef_in + (int64_t)__ldg(lm.m0 + p) * fplane + fcol));
                 } else {
                     const TIn *src = F + (int64_t)p * plane;
-                    for (int e = tid; e < kHY * kHX; e += 256) {
-                        const int yy = e / kHX, xx = e - yy * kHX;
-                        const int gy = y0 + yy, gx = x0 + xx;
-                        if (gy >= 0 && gy < n1 && gx >= 0 && gx < n2)
-                            cp_elem(&ring[p % kRing][yy][xx], src + (int64_t)gy * n2 + gx);
-                    }
+                    if (lv[0]) cp_async<sizeof(TIn)>(slot + soff[0], src + goff[0]);
+                    if (lv[1]) cp_async<sizeof(TIn)>(slot + soff[1], src + goff[1]);
                 }
             }
             cp_async_commit();
         };
+        // per-thread axis-1 / axis-2 neighbours as smem offsets within a plane
         Nb b1{}, b2{};
         if (act) {
             b1 = neighbours<A1>(ax1, j1);
             b2 = neighbours<A2>(ax2, j2);
         }
+        const int oaa = (b1.fa - y0) * kHX + (b2.fa - x0), oba = (b1.fb - y0) * kHX + (b2.fa - x0);
+        const int oab = (b1.fa - y0) * kHX + (b2.fb - x0), obb = (b1.fb - y0) * kHX + (b2.fb - x0);
         const int nc1 = A1 ? ax1.nc : n1, nc2 = A2 ? ax2.nc : n2;
-        const int64_t col = (int64_t)j1 * n2 + j2;
-        const int64_t fcol = act ? ((int64_t)__ldg(lm.m1 + j1)) * lm.D2 + __ldg(lm.m2 + j2) : 0;
+        const int64_t cgcol = (int64_t)b1.ca * nc2 + b2.ca;
+        const bool col_coarse = !b1.fo && !b2.fo;
         March M;
-        M.m1 = M.m2 = M.ya = M.yb = M.yc = 0.0;
-        M.c = c_lo;
+        march_init(M);
         auto emit = [&](int c, double z) { Z0[(int64_t)c * plane + col] = z; };
         for (int k = 0; k < kRing - 2; k++) issue(j_start + k);
         for (int j = j_start; j <= j_end; j++) {
@@ -197,57 +253,61 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
             __syncthreads();
             issue(j + kRing - 2);          // into the slot of plane j - 2 (no longer read)
             if (!act) continue;
-            const Nb b0 = neighbours<A0>(ax0, j);
-            const bool coarse_node = !b0.fo && !b1.fo && !b2.fo;
+            const PlaneInfo pi = A0 ? load_pi(ax0.pi + j) : identity_pi(j);
+            const bool coarse_node = !pi.fo && col_coarse;
+            const TIn *rj = ring + (j & (kRing - 1)) * kPlaneElems;
             double mc;
             if (MODE != 1) {
-                auto S = [&](int pl, int y, int x) -> double { return (double)ring[pl % kRing][y - y0][x - x0]; };
-                // GPK: P0 along axis 0 at the corner columns, then P1 along axis 1, then P2 along axis 2
-                auto P0 = [&](int y1, int x2) -> double {
-                    const double va = S(b0.fa, y1, x2);
-                    if (!b0.fo) return va;
-                    return lerp(va, S(b0.fb, y1, x2), b0.t);
+                const TIn *ra = ring + (pi.fa & (kRing - 1)) * kPlaneElems;
+                const TIn *rb = ring + (pi.fb & (kRing - 1)) * kPlaneElems;
+                // GPK: P0 along axis 0 at the corner columns, P1 along axis 1, P2 along axis 2
+                auto P0 = [&](int o) -> double {
+                    const double va = (double)ra[o];
+                    return pi.fo ? lerp(va, (double)rb[o], pi.t) : va;
                 };
-                auto P1 = [&](int x2) -> double {
-                    const double va = P0(b1.fa, x2);
-                    if (!b1.fo) return va;
-                    return lerp(va, P0(b1.fb, x2), b1.t);
-                };
-                double pred = P1(b2.fa);
-                if (b2.fo) pred = lerp(pred, P1(b2.fb), b2.t);
-                const double own = S(j, j1, j2);
+                double p1a = P0(oaa), p1b = 0.0;
+                if (A1 && b1.fo) p1a = lerp(p1a, P0(oba), b1.t);
+                if (A2) {
+                    p1b = P0(oab);
+                    if (A1 && b1.fo) p1b = lerp(p1b, P0(obb), b1.t);
+                }
+                const double pred = (A2 && b2.fo) ? lerp(p1a, p1b, b2.t) : p1a;
+                const double own = (double)rj[own_off];
                 mc = dsub(own, pred);
                 if (j >= own_lo && j < own_hi) {
-                    const int64_t f = (int64_t)__ldg(lm.m0 + j) * fplane + fcol;
                     if (coarse_node) {
-                        const int c0 = A0 ? b0.ca : j;
-                        Cg[((int64_t)c0 * nc1 + b1.ca) * nc2 + b2.ca] = own;
-                    } else if (MODE == 0) {
-                        coef[f] = mc;
+                        const int c0 = A0 ? pi.ca : j;
+                        Cg[(int64_t)c0 * nc1 * nc2 + cgcol] = own;
                     } else {
-                        long long b = 0;
-                        if (!isfinite(mc)) {
-                            fl |= 1;
+                        const int64_t f = (int64_t)__ldg(lm.m0 + j) * fplane + fcol;
+                        if (MODE == 0) {
+                            coef[f] = mc;
                         } else {
-                            const double sc = mc / q.bin;                 // IEEE division (quantize.py:73)
-                            if (fabs(sc) >= 4611686018427387904.0) fl |= 2;
-                            else b = (long long)rint(sc);                 // half to even (:76)
+                            long long b = 0;
+                            if (!isfinite(mc)) {
+                                fl |= 1;
+                            } else {
+                                const double sc = mc / q.bin;                 // IEEE division (quantize.py:73)
+                                if (fabs(sc) >= 4611686018427387904.0) fl |= 2;
+                                else b = (long long)rint(sc);                 // half to even (:76)
+                            }
+                            if (b >= q.half || -b >= q.half) {                 // outlier (:80-83)
+                                q.obins[f] = b;
+                                atomicOr(&q.omask[f >> 5], 1u << (f & 31));
+                                b = 0;
+                            }
+                            const uint32_t key =
+                                (uint32_t)(((unsigned long long)b << 1) ^ (unsigned long long)(b >> 63));
+                            q.keys[f] = key;
+                            if (sh_ok) atomicAdd(&sh_hist[key], 1u);
+                            else atomicAdd(&q.hist[key], 1ULL);
                         }
-                        if (b >= q.half || -b >= q.half) {                 // outlier (:80-83)
-                            q.obins[f] = b;
-                            atomicOr(&q.omask[f >> 5], 1u << (f & 31));
-                            b = 0;
-                        }
-                        const uint32_t key = (uint32_t)(((unsigned long long)b << 1) ^ (unsigned long long)(b >> 63));
-                        q.keys[f] = key;
-                        if (sh_ok) atomicAdd(&sh_hist[key], 1u);
-                        else atomicAdd(&q.hist[key], 1ULL);
                     }
                 }
             } else {
-                mc = coarse_node ? 0.0 : (double)ring[j % kRing][ty + 1][tx + 1];
+                mc = coarse_node ? 0.0 : (double)rj[own_off];
             }
-            if (A0) march_push(M, ax0, n0, j, j_start, mc, c_hi, emit);
+            if (A0) march_push(M, pi, n0, j, j_start, mc, emit);
             else Z0[(int64_t)j * plane + col] = mc;
         }
         cp_async_wait<0>();
@@ -363,13 +423,12 @@ __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__rest
     };
     for (int k = 0; k < kP2Ring - 1; k++) issue(j_start + k);
     March M;
-    M.m1 = M.m2 = M.ya = M.yb = M.yc = 0.0;
-    M.c = c_lo;
+    march_init(M);
     for (int j = j_start; j <= j_end; j++) {
         cp_async_wait<kP2Ring - 2>();   // row j has landed (own copies)
         const double x = in ? ring[j % kP2Ring][t] : 0.0;
         issue(j + kP2Ring - 1);          // into the slot of row j - 1
-        if (A1) march_push(M, ax1, n1, j, j_start, x, c_hi, out_row);
+        if (A1) march_push(M, load_pi(ax1.pi + j), n1, j, j_start, x, out_row);
         else out_row(j, x);
     }
     cp_async_wait<0>();

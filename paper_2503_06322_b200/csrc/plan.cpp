@@ -72,6 +72,29 @@ static void axis_tables(AxisTables &a, const std::vector<int32_t> &fine, const s
         a.tw[i] = cl[i] / a.tb[i - 1];
         a.tb[i] = cd[i] - a.tw[i] * a.tu[i - 1];
     }
+    a.pinfo.assign(n, PlaneInfo{});
+    for (int64_t j = 0; j < n; j++) {
+        PlaneInfo &p = a.pinfo[j];
+        p.fo = a.pb[j] >= 0;
+        p.ca = a.pa[j];
+        p.cb = p.fo ? a.pb[j] : a.pa[j];
+        p.fa = a.fa[j];
+        p.fb = a.fb[j];
+        p.t = a.pt[j];
+        p.md = a.md[j];
+        p.ml = a.ml[j];
+        p.mu = a.mu[j];
+        p.emit = -1;
+    }
+    for (int64_t c = 0; c < nc; c++) {
+        const int64_t need = a.rr[c] >= 0 ? a.rr[c] : a.r0[c];
+        PlaneInfo &p = a.pinfo[need];
+        p.emit = (int32_t)c;
+        p.e_rr = a.rr[c] >= 0;
+        p.e_rl = a.rl[c] >= 0;
+        p.ewr = a.wr[c];
+        p.ewl = a.wl[c];
+    }
 }
 
 void build_host_plan(HostPlan &p, int rank, const uint64_t *dims) {

@@ -12,7 +12,21 @@
 
 namespace hpdr {
 
+// Everything a march along one axis needs at fine index j, in one 80-byte record (built on the
+// host so the device loop does one broadcast load per plane instead of a dependent chain).
+struct PlaneInfo {
+    int32_t fa, fb, ca, cb;   // fine / coarse indices of the coarse neighbours (= j / c at coarse nodes)
+    double t;                 // interpolation weight (0 at coarse nodes)
+    double md, ml, mu;        // fine mass bands at j
+    int32_t fo;               // 1 when j is a fine-only node
+    int32_t emit;             // coarse c whose restriction completes once y(j) is known, else -1
+    int32_t e_rr, e_rl;       // c has a right (1 - t_R) / left (t_L) fine-only contribution
+    double ewr, ewl;          // those weights
+};
+static_assert(sizeof(PlaneInfo) == 80, "PlaneInfo layout");
+
 struct AxisTables {
+    std::vector<PlaneInfo> pinfo;   // per fine node
     bool active = false;
     int64_t n = 1, nc = 1;
     // prolong (GPK), per fine node j: pa/pb coarse neighbours (pb < 0: copy of coarse pa), t weight
