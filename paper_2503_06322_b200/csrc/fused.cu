@@ -62,9 +62,12 @@ struct March {
     double ya, yb, yc;    // y(k-2), y(k-1), y(k)
     double pmd, pml, pmu, pwr, pwl;   // PlaneInfo of j-1 (the y computed next)
     int pemit, prr, prl;
+    int c_lo, c_hi;                    // coarse outputs this march owns
 };
 
-__device__ __forceinline__ void march_init(March &M) {
+__device__ __forceinline__ void march_init(March &M, int c_lo, int c_hi) {
+    M.c_lo = c_lo;
+    M.c_hi = c_hi;
     M.m1 = M.m2 = M.ya = M.yb = M.yc = 0.0;
     M.pmd = M.pml = M.pmu = M.pwr = M.pwl = 0.0;
     M.pemit = -1;
@@ -77,7 +80,7 @@ __device__ __forceinline__ void march_y(March &M, double v, int emit, int rr, in
     M.ya = M.yb;
     M.yb = M.yc;
     M.yc = v;
-    if (emit >= 0) {
+    if (emit >= M.c_lo && emit < M.c_hi) {
         double z;
         if (rr) {
             z = dadd(M.yb, dmul(wr, M.yc));
@@ -95,7 +98,7 @@ template <class Emit>
 __device__ __forceinline__ void march_push(March &M, const PlaneInfo &pi, int n, int j, int j_start, double x,
                                            Emit &&out) {
     // y(j-1) needs x(j-2) unless j-1 == 0
-    if (j >= 1 && (j - 1 == 0 || j - 2 >= j_start)) {
+    if (j >= 1 && j - 1 >= j_start && (j - 1 == 0 || j - 2 >= j_start)) {
         double v = dmul(M.pmd, M.m1);
         if (j - 1 >= 1) v = dadd(v, dmul(M.pml, M.m2));
         v = dadd(v, dmul(M.pmu, x));
@@ -183,7 +186,7 @@ template <int MODE, bool A0, bool A1, bool A2, typename TIn>
 __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, int n0, int n1, int n2, DevAxis ax0,
                                                      DevAxis ax1, DevAxis ax2, LevelMap lm, double *__restrict__ coef,
                                                      const double *__restrict__ coef_in, double *__restrict__ Z0,
-                                                     double *__restrict__ Cg, QuantOut q) {
+                                                     double *__restrict__ Cg, QuantOut q, int c_base, int c_count) {
     __shared__ __align__(16) TIn ring[kRing * kPlaneElems];
     __shared__ uint32_t sh_hist[MODE == 2 ? kSmemHist : 1];
     const bool sh_ok = MODE == 2 && q.dict <= kSmemHist;
@@ -195,7 +198,9 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
     const bool act = j1 < n1 && j2 < n2;
     const int nc0 = A0 ? ax0.nc : n0;
     int c_lo, c_hi;
-    slab_range(nc0, gridDim.z, blockIdx.z, c_lo, c_hi);
+    slab_range(c_count, gridDim.z, blockIdx.z, c_lo, c_hi);   // coarse outputs [c_base, c_base + c_count)
+    c_lo += c_base;
+    c_hi += c_base;
     int fl = 0;
     if (c_lo < c_hi) {   // uniform across the block
         int j_start, j_end, own_lo, own_hi;
@@ -245,7 +250,7 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
         const int64_t cgcol = (int64_t)b1.ca * nc2 + b2.ca;
         const bool col_coarse = !b1.fo && !b2.fo;
         March M;
-        march_init(M);
+        march_init(M, c_lo, c_hi);
         auto emit = [&](int c, double z) { Z0[(int64_t)c * plane + col] = z; };
         for (int k = 0; k < kRing - 2; k++) issue(j_start + k);
         for (int j = j_start; j <= j_end; j++) {
@@ -348,12 +353,12 @@ constexpr int kP2Ring = 8;
 template <bool A1, bool A2>
 __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__restrict__ Z0, int m0, int n1, int n2,
                                                             DevAxis ax1, DevAxis ax2, double *__restrict__ B,
-                                                            int slabs1) {
+                                                            int slabs1, int p_base) {
     __shared__ double sw[kP2Threads];
     __shared__ double sy[kP2Threads];
     __shared__ __align__(16) double ring[kP2Ring][kP2Threads];
     const int t = threadIdx.x;
-    const int p = blockIdx.y;
+    const int p = p_base + blockIdx.y;
     const int nc1 = A1 ? ax1.nc : n1, nc2 = A2 ? ax2.nc : n2;
     int c2_lo = 0, c2_cnt = 0, base;
     if (A2) {
@@ -423,7 +428,7 @@ __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__rest
     };
     for (int k = 0; k < kP2Ring - 1; k++) issue(j_start + k);
     March M;
-    march_init(M);
+    march_init(M, c_lo, c_hi);
     for (int j = j_start; j <= j_end; j++) {
         cp_async_wait<kP2Ring - 2>();   // row j has landed (own copies)
         const double x = in ? ring[j % kP2Ring][t] : 0.0;
@@ -498,14 +503,14 @@ int slabs_for(int64_t cols, int planes) {
 template <int MODE, typename TIn>
 void launch_pass1(int act, const TIn *F, int n0, int n1, int n2, const DevAxis &a0, const DevAxis &a1,
                   const DevAxis &a2, const LevelMap &lm, double *coef, const double *coef_in, double *Z0, double *Cg,
-                  const QuantOut &q, cudaStream_t s) {
-    const int planes = (act & 1) ? a0.nc : n0;
-    dim3 grid((n2 + kTX - 1) / kTX, (n1 + kTY - 1) / kTY, slabs_for((int64_t)n1 * n2, planes));
+                  const QuantOut &q, int c_base, int c_count, cudaStream_t s) {
+    if (c_count <= 0) return;
+    dim3 grid((n2 + kTX - 1) / kTX, (n1 + kTY - 1) / kTY, slabs_for((int64_t)n1 * n2, c_count));
     dim3 block(kTX, kTY);
 #define P1L(M)                                                                                                     \
     case M:                                                                                                        \
         k_level_pass1<MODE, (M & 1) != 0, (M & 2) != 0, (M & 4) != 0, TIn><<<grid, block, 0, s>>>(              \
-            F, n0, n1, n2, a0, a1, a2, lm, coef, coef_in, Z0, Cg, q);                                              \
+            F, n0, n1, n2, a0, a1, a2, lm, coef, coef_in, Z0, Cg, q, c_base, c_count);                                              \
         break;
     switch (act) { P1L(1) P1L(2) P1L(3) P1L(4) P1L(5) P1L(6) P1L(7) default: break; }
 #undef P1L
@@ -513,17 +518,18 @@ void launch_pass1(int act, const TIn *F, int n0, int n1, int n2, const DevAxis &
 }
 
 void launch_pass2(int act, const double *Z0, int m0, int n1, int n2, const DevAxis &a1, const DevAxis &a2, double *B,
-                  cudaStream_t s) {
+                  int p_base, int p_count, cudaStream_t s) {
+    if (p_count <= 0) return;
     const bool A1 = act & 2, A2 = act & 4;
     const int nc1 = A1 ? a1.nc : n1, nc2 = A2 ? a2.nc : n2;
     const unsigned gx = A2 ? (unsigned)((nc2 + kP2Out - 1) / kP2Out) : (unsigned)((n2 + kP2Threads - 1) / kP2Threads);
     const int64_t cols = (int64_t)m0 * gx * kP2Threads;
     const int slabs = slabs_for(cols, nc1);
-    dim3 grid(gx, (unsigned)m0, (unsigned)slabs);
-    if (A1 && A2) k_level_pass2<true, true><<<grid, kP2Threads, 0, s>>>(Z0, m0, n1, n2, a1, a2, B, slabs);
-    else if (A1) k_level_pass2<true, false><<<grid, kP2Threads, 0, s>>>(Z0, m0, n1, n2, a1, a2, B, slabs);
-    else if (A2) k_level_pass2<false, true><<<grid, kP2Threads, 0, s>>>(Z0, m0, n1, n2, a1, a2, B, slabs);
-    else k_level_pass2<false, false><<<grid, kP2Threads, 0, s>>>(Z0, m0, n1, n2, a1, a2, B, slabs);
+    dim3 grid(gx, (unsigned)p_count, (unsigned)slabs);
+    if (A1 && A2) k_level_pass2<true, true><<<grid, kP2Threads, 0, s>>>(Z0, m0, n1, n2, a1, a2, B, slabs, p_base);
+    else if (A1) k_level_pass2<true, false><<<grid, kP2Threads, 0, s>>>(Z0, m0, n1, n2, a1, a2, B, slabs, p_base);
+    else if (A2) k_level_pass2<false, true><<<grid, kP2Threads, 0, s>>>(Z0, m0, n1, n2, a1, a2, B, slabs, p_base);
+    else k_level_pass2<false, false><<<grid, kP2Threads, 0, s>>>(Z0, m0, n1, n2, a1, a2, B, slabs, p_base);
     LAUNCH_CHECK();
 }
 
@@ -567,29 +573,45 @@ int64_t z0_size(const DevPlan &p, int st_i) {
 
 bool fused_supported(const DevPlan &p) { return p.dims.n[0] == 1; }
 
+int fused_out_planes(const DevPlan &p, int st_i) {
+    const DevStep &st = p.steps[st_i];
+    return (int)(st.ax[1].active ? st.ax[1].nc : st.fsh.n[1]);
+}
+
+namespace {
+int clamp_hi(const DevPlan &p, int st_i, int c_hi) {
+    const int m = fused_out_planes(p, st_i);
+    return c_hi < 0 || c_hi > m ? m : c_hi;
+}
+}  // namespace
+
 void fused_pass1_decompose(const DevPlan &p, int st_i, const void *F, bool f32, double *coef, double *Z0, double *Cg,
-                           cudaStream_t s) {
+                           cudaStream_t s, int c_lo, int c_hi) {
     const DevStep &st = p.steps[st_i];
     const View v = view_of(p, st_i);
+    c_hi = clamp_hi(p, st_i, c_hi);
+    const double frac = (double)(c_hi - c_lo) / fused_out_planes(p, st_i);
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
-    KPROF("k_level_pass1", (f32 ? 4.0 : 8.0) * nf + 8.0 * (nf - nc) + 8.0 * nc + 8.0 * z0_size(p, st_i), s);
+    KPROF("k_level_pass1", frac * ((f32 ? 4.0 : 8.0) * nf + 8.0 * (nf - nc) + 8.0 * nc + 8.0 * z0_size(p, st_i)), s);
     const QuantOut q{};
     if (f32) launch_pass1<0, float>(v.act, (const float *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
-                                    coef, nullptr, Z0, Cg, q, s);
+                                    coef, nullptr, Z0, Cg, q, c_lo, c_hi - c_lo, s);
     else launch_pass1<0, double>(v.act, (const double *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
-                                 coef, nullptr, Z0, Cg, q, s);
+                                 coef, nullptr, Z0, Cg, q, c_lo, c_hi - c_lo, s);
 }
 
 void fused_pass1_quantize(const DevPlan &p, int st_i, const void *F, bool f32, const QuantOut &q, double *Z0,
-                          double *Cg, cudaStream_t s) {
+                          double *Cg, cudaStream_t s, int c_lo, int c_hi) {
     const DevStep &st = p.steps[st_i];
     const View v = view_of(p, st_i);
+    c_hi = clamp_hi(p, st_i, c_hi);
+    const double frac = (double)(c_hi - c_lo) / fused_out_planes(p, st_i);
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
-    KPROF("k_level_pass1q", (f32 ? 4.0 : 8.0) * nf + 4.0 * (nf - nc) + 8.0 * nc + 8.0 * z0_size(p, st_i), s);
+    KPROF("k_level_pass1q", frac * ((f32 ? 4.0 : 8.0) * nf + 4.0 * (nf - nc) + 8.0 * nc + 8.0 * z0_size(p, st_i)), s);
     if (f32) launch_pass1<2, float>(v.act, (const float *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
-                                    nullptr, nullptr, Z0, Cg, q, s);
+                                    nullptr, nullptr, Z0, Cg, q, c_lo, c_hi - c_lo, s);
     else launch_pass1<2, double>(v.act, (const double *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
-                                 nullptr, nullptr, Z0, Cg, q, s);
+                                 nullptr, nullptr, Z0, Cg, q, c_lo, c_hi - c_lo, s);
 }
 
 void fused_pass1_recompose(const DevPlan &p, int st_i, const double *coef, double *Z0, cudaStream_t s) {
@@ -599,7 +621,7 @@ void fused_pass1_recompose(const DevPlan &p, int st_i, const double *coef, doubl
     KPROF("k_level_pass1r", 8.0 * (nf - nc) + 8.0 * z0_size(p, st_i), s);
     const QuantOut q{};
     launch_pass1<1, double>(v.act, nullptr, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, nullptr, coef, Z0,
-                            nullptr, q, s);
+                            nullptr, q, 0, fused_out_planes(p, st_i), s);
 }
 
 void quantize_coarsest(const DevPlan &p, const double *coarsest_vals, const QuantOut &q, cudaStream_t s) {
@@ -609,12 +631,14 @@ void quantize_coarsest(const DevPlan &p, const double *coarsest_vals, const Quan
     LAUNCH_CHECK();
 }
 
-void fused_pass2(const DevPlan &p, int st_i, const double *Z0, double *B, cudaStream_t s) {
+void fused_pass2(const DevPlan &p, int st_i, const double *Z0, double *B, cudaStream_t s, int p_lo, int p_hi) {
     const DevStep &st = p.steps[st_i];
     const View v = view_of(p, st_i);
-    const int m0 = (v.act & 1) ? st.ax[1].nc : v.n0;
-    KPROF("k_level_pass2", 8.0 * m0 * v.n1 * v.n2 + 8.0 * st.csh.size(), s);
-    launch_pass2(v.act, Z0, m0, v.n1, v.n2, st.ax[2], st.ax[3], B, s);
+    const int m0 = fused_out_planes(p, st_i);
+    p_hi = p_hi < 0 || p_hi > m0 ? m0 : p_hi;
+    const double frac = (double)(p_hi - p_lo) / m0;
+    KPROF("k_level_pass2", frac * (8.0 * m0 * v.n1 * v.n2 + 8.0 * st.csh.size()), s);
+    launch_pass2(v.act, Z0, m0, v.n1, v.n2, st.ax[2], st.ax[3], B, p_lo, p_hi - p_lo, s);
 }
 
 void fused_final(const DevPlan &p, int st_i, const double *cv, const double *coef, void *D, int out_dtype,

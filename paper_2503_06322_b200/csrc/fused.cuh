@@ -27,18 +27,21 @@ struct QuantOut {
 
 // Decompose transition st_i writing keys instead of fp64 coefficients.
 void fused_pass1_quantize(const DevPlan &p, int st_i, const void *F, bool f32, const QuantOut &q, double *Z0,
-                          double *Cg, cudaStream_t s);
+                          double *Cg, cudaStream_t s, int c_lo = 0, int c_hi = -1);
 // Coarsest nodes (quantize.py:64-77): bin-limit / finiteness checks, key 0, histogram.
 void quantize_coarsest(const DevPlan &p, const double *coarsest_vals, const QuantOut &q, cudaStream_t s);
 
 // Decompose transition st_i: mc -> coef (fine-only nodes), coarse-node gather -> Cg, and the
 // axis-0 mass-transfer -> Z0.  F is the dense fine level (float when f32).
 void fused_pass1_decompose(const DevPlan &p, int st_i, const void *F, bool f32, double *coef, double *Z0,
-                           double *Cg, cudaStream_t s);
+                           double *Cg, cudaStream_t s, int c_lo = 0, int c_hi = -1);
 // Recompose transition st_i: mc gathered from coef (coarse nodes zero) -> axis-0 mass-transfer -> Z0.
 void fused_pass1_recompose(const DevPlan &p, int st_i, const double *coef, double *Z0, cudaStream_t s);
 // Axis-1 and axis-2 mass-transfer: Z0 -> B (the coarse-grid right-hand side of the Thomas solves).
-void fused_pass2(const DevPlan &p, int st_i, const double *Z0, double *B, cudaStream_t s);
+void fused_pass2(const DevPlan &p, int st_i, const double *Z0, double *B, cudaStream_t s, int p_lo = 0,
+                 int p_hi = -1);
+// Output planes of pass 1 along axis 0 (coarse count, or the fine count when axis 0 is inactive).
+int fused_out_planes(const DevPlan &p, int st_i);
 // D = P(cv) + mc on the fine level; out_dtype 0 writes float, otherwise double.
 void fused_final(const DevPlan &p, int st_i, const double *cv, const double *coef, void *D, int out_dtype,
                  cudaStream_t s);

@@ -281,14 +281,14 @@ __global__ void k_decode(const uint32_t *__restrict__ words, uint64_t limit, con
             uint64_t buf = (((uint64_t)load_be(words, wi) << 32) | load_be(words, wi + 1)) << (pos & 31);
             int avail = 64 - (int)(pos & 31);
             uint64_t nw = wi + 2;
-            uint32_t pre = load_be(words, nw);
+            uint32_t pre = __ldg(words + nw);   // raw word; byte-swapped when consumed
             uint32_t *s8 = stage[threadIdx.x];   // private 8-symbol staging row
             uint64_t i = 0;
             for (; i < cnt; i++) {
                 if (avail < 32) {
-                    buf |= (uint64_t)pre << (32 - avail);
+                    buf |= (uint64_t)__byte_perm(pre, 0, 0x0123) << (32 - avail);
                     avail += 32;
-                    pre = load_be(words, ++nw);
+                    pre = __ldg(words + (++nw));
                 }
                 if (pos >= limit) { err = (long long)pos; break; }
                 const uint32_t win = (uint32_t)(buf >> 32);
