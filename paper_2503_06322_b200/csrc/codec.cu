@@ -342,23 +342,20 @@ int hpdr_mgard_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, cons
         if (!(0.0 < eb_rel && eb_rel < 1.0)) fail(HPDR_ERR_VALIDATION, "eb_rel must be in (0, 1), got " + fmt_double(eb_rel));
         if (dict_size < 2 || dict_size > 65535)
             fail(HPDR_ERR_VALIDATION, "dict_size must be in [2, 65535], got " + std::to_string(dict_size));
-        const void *d_in = device_input(ctx, in, (size_t)N * itemsize(dtype), "input", s);
-        double u_min, u_max;
-        if (has_range) {
-            u_min = range_min;
-            u_max = range_max;
-        } else {
-            minmax_device(ctx, d_in, dtype, N, &u_min, &u_max, s);
-        }
-        const double eb_abs = eb_rel * (u_max - u_min);
-        const double bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
+        const bool host_in = classify(in) != MemKind::Device;
+        const bool fused = L > 1 && use_fused(p);
+        static const bool no_stream = getenv("HPDR_NO_STREAM") != nullptr;
+        const bool streamed = host_in && fused && !no_stream;
+        const void *d_in = streamed ? nullptr : device_input(ctx, in, (size_t)N * itemsize(dtype), "input", s);
+        double u_min = range_min, u_max = range_max;
+        if (!has_range && !streamed) minmax_device(ctx, d_in, dtype, N, &u_min, &u_max, s);
         uint32_t *keys = (uint32_t *)ctx->dbuf("keys", N * 4 + 64);
         QuantResult q;
         const double *d_coarse;
-        if (L > 1 && use_fused(p)) {
+        double eb_abs = 0.0, bin = 1.0;
+        if (fused) {
             // quantize-on-write: keys, outlier mask and histogram come out of the level kernels
             QuantOut qo;
-            qo.bin = bin;
             qo.half = dict_size / 2;
             qo.dict = dict_size;
             qo.keys = keys;
@@ -370,9 +367,23 @@ int hpdr_mgard_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, cons
             CUDA_CHECK(cudaMemsetAsync(qo.omask, 0, words * 4, s));
             CUDA_CHECK(cudaMemsetAsync(qo.hist, 0, (size_t)dict_size * 8, s));
             CUDA_CHECK(cudaMemsetAsync(qo.flags, 0, 16, s));
-            d_coarse = decompose_quantize(ctx, p, d_in, dtype, qo, s);
+            if (streamed) {
+                // the range (relative mode) is complete only after the last chunk; q.bin set inside
+                d_coarse = decompose_quantize_streamed(ctx, p, in, dtype, has_range, range_min, range_max, eb_rel,
+                                                       qo, &u_min, &u_max, s);
+            } else {
+                qo.bin = bin = 0.0;
+            }
+            eb_abs = eb_rel * (u_max - u_min);
+            bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
+            if (!streamed) {
+                qo.bin = bin;
+                d_coarse = decompose_quantize(ctx, p, d_in, dtype, qo, s);
+            }
             quantize_finish(ctx, N, dict_size, bin, nullptr, qo.obins, q, s);
         } else {
+            eb_abs = eb_rel * (u_max - u_min);
+            bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
             double *coef = (double *)ctx->dbuf("coef", N * 8);
             d_coarse = decompose_device(ctx, p, d_in, dtype, coef, s);
             quantize_device(ctx, coef, N, p.host.coarsest, bin, dict_size, keys, q, s);
@@ -518,8 +529,7 @@ int hpdr_mgard_decompress(hpdr_ctx *ctx, const void *blob_in, uint64_t len, void
             recompose_into(ctx, p, coef, out, dtype, s);
         } else {
             void *stage = ctx->dbuf("out_stage", ob);
-            recompose_into(ctx, p, coef, stage, dtype, s);
-            CUDA_CHECK(cudaMemcpyAsync(out, stage, ob, cudaMemcpyDeviceToHost, s));
+            recompose_into(ctx, p, coef, stage, dtype, s, out);
         }
         CUDA_CHECK(cudaStreamSynchronize(s));
     });

@@ -126,6 +126,15 @@ void *hpdr_ctx::hbuf(const std::string &name, size_t bytes) {
 
 void hpdr_ctx::sync() { CUDA_CHECK(cudaStreamSynchronize(stream)); }
 
+cudaEvent_t hpdr_ctx::event(size_t i) {
+    while (events.size() <= i) {
+        cudaEvent_t e;
+        CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        events.push_back(e);
+    }
+    return events[i];
+}
+
 namespace {
 
 struct Packer {
@@ -328,6 +337,7 @@ void hpdr_ctx_destroy(hpdr_ctx *c) {
     if (!c) return;
     hpdr_ctx_trim(c);
     for (auto &kv : c->plans) cudaFree(kv.second->dbuf);
+    for (cudaEvent_t e : c->events) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->h2d);
     cudaStreamDestroy(c->d2h);

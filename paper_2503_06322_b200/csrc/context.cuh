@@ -82,6 +82,9 @@ struct hpdr_ctx {
         bool huffman_only = false;
     } pending;
 
+    std::vector<cudaEvent_t> events;   // reusable sync events (no timing)
+    cudaEvent_t event(size_t i);
+
     void *dbuf(const std::string &name, size_t bytes);
     void *hbuf(const std::string &name, size_t bytes);
     hpdr::DevPlan &plan(int rank, const uint64_t *dims);

@@ -328,6 +328,56 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
     }
 }
 
+// Quantize the fine-only nodes of the finest level from stored fp64 coefficients (the streamed
+// relative-mode path, where the bin width is only known after the last input chunk).
+template <bool A0, bool A1, bool A2>
+__global__ void __launch_bounds__(256) k_quantize_fine(const double *__restrict__ coef, int n0, int n1, int n2,
+                                                       DevAxis ax0, DevAxis ax1, DevAxis ax2, QuantOut q) {
+    __shared__ uint32_t sh_hist[kSmemHist];
+    const bool sh_ok = q.dict <= kSmemHist;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    if (sh_ok)
+        for (uint32_t k = tid; k < q.dict; k += 256) sh_hist[k] = 0;
+    __syncthreads();
+    const int j2 = blockIdx.x * 32 + threadIdx.x, j1 = blockIdx.y * 8 + threadIdx.y;
+    int fl = 0;
+    if (j1 < n1 && j2 < n2) {
+        const bool col_fo = (A1 && __ldg(ax1.pb + j1) >= 0) || (A2 && __ldg(ax2.pb + j2) >= 0);
+        int lo, hi;
+        slab_range(n0, gridDim.z, blockIdx.z, lo, hi);
+        const int64_t plane = (int64_t)n1 * n2, col = (int64_t)j1 * n2 + j2;
+        for (int j = lo; j < hi; j++) {
+            if (!(col_fo || (A0 && __ldg(ax0.pb + j) >= 0))) continue;
+            const int64_t f = (int64_t)j * plane + col;
+            const double mc = __ldg(coef + f);
+            long long b = 0;
+            if (!isfinite(mc)) {
+                fl |= 1;
+            } else {
+                const double sc = mc / q.bin;
+                if (fabs(sc) >= 4611686018427387904.0) fl |= 2;
+                else b = (long long)rint(sc);
+            }
+            if (b >= q.half || -b >= q.half) {
+                q.obins[f] = b;
+                atomicOr(&q.omask[f >> 5], 1u << (f & 31));
+                b = 0;
+            }
+            const uint32_t key = (uint32_t)(((unsigned long long)b << 1) ^ (unsigned long long)(b >> 63));
+            q.keys[f] = key;
+            if (sh_ok) atomicAdd(&sh_hist[key], 1u);
+            else atomicAdd(&q.hist[key], 1ULL);
+        }
+    }
+    if (fl) atomicOr(q.flags, fl);
+    __syncthreads();
+    if (sh_ok)
+        for (uint32_t k = tid; k < q.dict; k += 256) {
+            const uint32_t c = sh_hist[k];
+            if (c) atomicAdd(&q.hist[k], (unsigned long long)c);
+        }
+}
+
 // Coarsest nodes: raw values are checked (finite, bin limit) like every coefficient, then get key 0.
 __global__ void k_quantize_coarsest(const double *__restrict__ vals, const long long *__restrict__ idx, int n,
                                     QuantOut q) {
@@ -448,7 +498,8 @@ constexpr int kFRing = 8;
 template <bool A0, bool A1, bool A2, typename TOut>
 __global__ void __launch_bounds__(256) k_level_final(const double *__restrict__ cv, int n0, int n1, int n2,
                                                      DevAxis ax0, DevAxis ax1, DevAxis ax2, LevelMap lm,
-                                                     const double *__restrict__ coef, TOut *__restrict__ D) {
+                                                     const double *__restrict__ coef, TOut *__restrict__ D, int j_base,
+                                                     int j_count) {
     __shared__ __align__(16) double ring[kFRing][256];
     const int tid = threadIdx.y * 32 + threadIdx.x;
     const int j2 = blockIdx.x * 32 + threadIdx.x;
@@ -457,7 +508,9 @@ __global__ void __launch_bounds__(256) k_level_final(const double *__restrict__ 
     const Nb b1 = neighbours<A1>(ax1, j1), b2 = neighbours<A2>(ax2, j2);
     const int nc1 = A1 ? ax1.nc : n1, nc2 = A2 ? ax2.nc : n2;
     int lo, hi;
-    slab_range(n0, gridDim.z, blockIdx.z, lo, hi);
+    slab_range(j_count, gridDim.z, blockIdx.z, lo, hi);   // fine planes [j_base, j_base + j_count)
+    lo += j_base;
+    hi += j_base;
     const int64_t col = (int64_t)j1 * n2 + j2;
     const int64_t fcol = ((int64_t)__ldg(lm.m1 + j1)) * lm.D2 + __ldg(lm.m2 + j2);
     const int64_t fplane = lm.D1 * lm.D2;
@@ -535,13 +588,15 @@ void launch_pass2(int act, const double *Z0, int m0, int n1, int n2, const DevAx
 
 template <typename TOut>
 void launch_final(int act, const double *cv, int n0, int n1, int n2, const DevAxis &a0, const DevAxis &a1,
-                  const DevAxis &a2, const LevelMap &lm, const double *coef, TOut *D, cudaStream_t s) {
-    dim3 grid((n2 + 31) / 32, (n1 + 7) / 8, slabs_for((int64_t)n1 * n2, n0));
+                  const DevAxis &a2, const LevelMap &lm, const double *coef, TOut *D, int j_base, int j_count,
+                  cudaStream_t s) {
+    if (j_count <= 0) return;
+    dim3 grid((n2 + 31) / 32, (n1 + 7) / 8, slabs_for((int64_t)n1 * n2, j_count));
     dim3 block(32, 8);
 #define FL(M)                                                                                                      \
     case M:                                                                                                        \
         k_level_final<(M & 1) != 0, (M & 2) != 0, (M & 4) != 0, TOut><<<grid, block, 0, s>>>(cv, n0, n1, n2, a0, \
-                                                                                              a1, a2, lm, coef, D); \
+                                                                                              a1, a2, lm, coef, D, j_base, j_count); \
         break;
     switch (act) { FL(1) FL(2) FL(3) FL(4) FL(5) FL(6) FL(7) default: break; }
 #undef FL
@@ -624,6 +679,24 @@ void fused_pass1_recompose(const DevPlan &p, int st_i, const double *coef, doubl
                             nullptr, q, 0, fused_out_planes(p, st_i), s);
 }
 
+void quantize_fine(const DevPlan &p, const double *coef, const QuantOut &q, cudaStream_t s) {
+    const DevStep &st = p.steps[0];
+    const View v = view_of(p, 0);
+    const int64_t nf = st.fsh.size(), nc = st.csh.size();
+    KPROF("k_quantize_fine", 12.0 * (nf - nc), s);
+    dim3 grid((v.n2 + 31) / 32, (v.n1 + 7) / 8, slabs_for((int64_t)v.n1 * v.n2, v.n0));
+    dim3 block(32, 8);
+#define QF(M)                                                                                                      \
+    case M:                                                                                                        \
+        k_quantize_fine<(M & 1) != 0, (M & 2) != 0, (M & 4) != 0><<<grid, block, 0, s>>>(coef, v.n0, v.n1, v.n2,  \
+                                                                                         st.ax[1], st.ax[2],      \
+                                                                                         st.ax[3], q);            \
+        break;
+    switch (v.act) { QF(1) QF(2) QF(3) QF(4) QF(5) QF(6) QF(7) default: break; }
+#undef QF
+    LAUNCH_CHECK();
+}
+
 void quantize_coarsest(const DevPlan &p, const double *coarsest_vals, const QuantOut &q, cudaStream_t s) {
     const int n = (int)p.host.coarsest.size();
     KPROF("k_quantize_coarsest", 16.0 * n, s);
@@ -642,15 +715,19 @@ void fused_pass2(const DevPlan &p, int st_i, const double *Z0, double *B, cudaSt
 }
 
 void fused_final(const DevPlan &p, int st_i, const double *cv, const double *coef, void *D, int out_dtype,
-                 cudaStream_t s) {
+                 cudaStream_t s, int j_lo, int j_hi) {
     const DevStep &st = p.steps[st_i];
     const View v = view_of(p, st_i);
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
-    KPROF("k_level_final", 8.0 * nc + 8.0 * (nf - nc) + (out_dtype == 0 ? 4.0 : 8.0) * nf, s);
+    if (j_hi < 0 || j_hi > v.n0) j_hi = v.n0;
+    const double frac = (double)(j_hi - j_lo) / v.n0;
+    KPROF("k_level_final", frac * (8.0 * nc + 8.0 * (nf - nc) + (out_dtype == 0 ? 4.0 : 8.0) * nf), s);
     if (out_dtype == 0)
-        launch_final<float>(v.act, cv, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, coef, (float *)D, s);
+        launch_final<float>(v.act, cv, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, coef, (float *)D, j_lo,
+                            j_hi - j_lo, s);
     else
-        launch_final<double>(v.act, cv, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, coef, (double *)D, s);
+        launch_final<double>(v.act, cv, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, coef, (double *)D, j_lo,
+                             j_hi - j_lo, s);
 }
 
 }  // namespace hpdr

@@ -28,6 +28,8 @@ struct QuantOut {
 // Decompose transition st_i writing keys instead of fp64 coefficients.
 void fused_pass1_quantize(const DevPlan &p, int st_i, const void *F, bool f32, const QuantOut &q, double *Z0,
                           double *Cg, cudaStream_t s, int c_lo = 0, int c_hi = -1);
+// Fine-only nodes of the finest level quantized from fp64 coefficients (streamed relative mode).
+void quantize_fine(const DevPlan &p, const double *coef, const QuantOut &q, cudaStream_t s);
 // Coarsest nodes (quantize.py:64-77): bin-limit / finiteness checks, key 0, histogram.
 void quantize_coarsest(const DevPlan &p, const double *coarsest_vals, const QuantOut &q, cudaStream_t s);
 
@@ -44,6 +46,6 @@ void fused_pass2(const DevPlan &p, int st_i, const double *Z0, double *B, cudaSt
 int fused_out_planes(const DevPlan &p, int st_i);
 // D = P(cv) + mc on the fine level; out_dtype 0 writes float, otherwise double.
 void fused_final(const DevPlan &p, int st_i, const double *cv, const double *coef, void *D, int out_dtype,
-                 cudaStream_t s);
+                 cudaStream_t s, int j_lo = 0, int j_hi = -1);
 
 }  // namespace hpdr

@@ -584,6 +584,117 @@ const double *decompose_fused(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int d
 
 }  // namespace
 
+const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void *host_in, int dtype, bool has_range,
+                                          double range_min, double range_max, double eb_rel, QuantOut &q,
+                                          double *u_min, double *u_max, cudaStream_t s) {
+    LevelBuffers b = fused_buffers(ctx, p);
+    const int L = p.host.L;
+    const DevStep &st0 = p.steps[0];
+    const int n0 = (int)st0.fsh.n[1];
+    const int64_t plane_elems = st0.fsh.n[2] * st0.fsh.n[3];
+    const size_t isz = dtype == 0 ? 4 : 8;
+    const int64_t N = p.n_total;
+    char *d_in = (char *)ctx->dbuf("input", N * isz);
+    double *Z0 = b.mc;
+    double *coef = has_range ? nullptr : (double *)ctx->dbuf("coef", N * 8);
+    // chunks of >= 32 MB (and >= 4 planes) along dim 0
+    const int64_t plane_bytes = plane_elems * (int64_t)isz;
+    int chunk = (int)std::max<int64_t>(4, ((32LL << 20) + plane_bytes - 1) / std::max<int64_t>(plane_bytes, 1));
+    chunk = std::min(chunk, n0);
+    const int K = (n0 + chunk - 1) / chunk;
+    unsigned long long *mm = (unsigned long long *)ctx->dbuf("minmax", 32);
+    if (!has_range) {
+        unsigned long long *h = (unsigned long long *)ctx->hbuf("minmax_h", 32);
+        h[0] = ~0ULL;
+        h[1] = 0ULL;
+        h[2] = 0ULL;
+        CUDA_CHECK(cudaMemcpyAsync(mm, h, 24, cudaMemcpyHostToDevice, s));
+    }
+    // coarse outputs of transition 0 whose 5-plane stencil lies within the first `arrived` planes
+    const AxisTables &ax0 = p.host.steps[0].ax[1];
+    const int m0 = fused_out_planes(p, 0);
+    auto ready = [&](int arrived) -> int {
+        if (arrived >= n0) return m0;
+        if (!ax0.active) return arrived;
+        int c = 0;
+        while (c < m0 && ax0.r0[c] + 2 < arrived) c++;
+        return c;
+    };
+    // the event the compute stream waits on before touching chunk k
+    CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
+    CUDA_CHECK(cudaStreamWaitEvent(ctx->h2d, ctx->event(0), 0));   // buffers are free once prior work is done
+    auto issue = [&](int k) {
+        const int64_t a = (int64_t)k * chunk, e = std::min<int64_t>(n0, a + chunk);
+        CUDA_CHECK(cudaMemcpyAsync(d_in + a * plane_bytes, (const char *)host_in + a * plane_bytes,
+                                   (e - a) * plane_bytes, cudaMemcpyHostToDevice, ctx->h2d));
+        CUDA_CHECK(cudaEventRecord(ctx->event(1 + k), ctx->h2d));
+    };
+    issue(0);
+    int c_done = 0;
+    for (int k = 0; k < K; k++) {
+        CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(1 + k), 0));
+        const int64_t a = (int64_t)k * chunk, e = std::min<int64_t>(n0, a + chunk);
+        if (!has_range) {
+            const int64_t cnt = (e - a) * plane_elems;
+            KPROF("k_minmax", (double)cnt * isz, s);
+            k_minmax<<<grid_for(cnt, 256, 148 * 8), 256, 0, s>>>(d_in + a * plane_bytes, dtype, cnt, mm);
+            LAUNCH_CHECK();
+        }
+        const int c_ready = ready((int)e);
+        if (c_ready > c_done) {
+            if (has_range) fused_pass1_quantize(p, 0, d_in, dtype == 0, q, Z0, b.cg, s, c_done, c_ready);
+            else fused_pass1_decompose(p, 0, d_in, dtype == 0, coef, Z0, b.cg, s, c_done, c_ready);
+            fused_pass2(p, 0, Z0, b.t0, s, c_done, c_ready);
+            c_done = c_ready;
+        }
+        if (k + 1 < K) issue(k + 1);
+    }
+    if (has_range) {
+        *u_min = range_min;
+        *u_max = range_max;
+    } else {
+        unsigned long long *h = (unsigned long long *)ctx->hbuf("minmax_h", 32);
+        CUDA_CHECK(cudaMemcpyAsync(h, mm, 24, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        auto val = [](unsigned long long k) {
+            unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k;
+            double d;
+            memcpy(&d, &u, 8);
+            return d;
+        };
+        *u_min = h[2] ? __builtin_nan("") : val(h[0]);
+        *u_max = h[2] ? __builtin_nan("") : val(h[1]);
+        const double eb_abs = eb_rel * (*u_max - *u_min);
+        q.bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
+        quantize_fine(p, coef, q, s);
+    }
+    // the rest of transition 0 (IPK + coarse update) and the coarser levels
+    {
+        Shape4 sh = st0.csh;
+        for (int a = 0; a < 4; a++)
+            if (st0.ax[a].active) thomas(b.t0, sh, a, st0.ax[a], s);
+        const int64_t nc = st0.csh.size();
+        KPROF("k_add", 24.0 * nc, s);
+        k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, level_ptr(b, p, 1), nc);
+        LAUNCH_CHECK();
+    }
+    for (int st_i = 1; st_i + 1 < L; st_i++) {
+        const DevStep &st = p.steps[st_i];
+        fused_pass1_quantize(p, st_i, level_ptr(b, p, st_i), false, q, Z0, b.cg, s);
+        fused_pass2(p, st_i, Z0, b.t0, s);
+        Shape4 sh = st.csh;
+        for (int a = 0; a < 4; a++)
+            if (st.ax[a].active) thomas(b.t0, sh, a, st.ax[a], s);
+        const int64_t nc = st.csh.size();
+        KPROF("k_add", 24.0 * nc, s);
+        k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, level_ptr(b, p, st_i + 1), nc);
+        LAUNCH_CHECK();
+    }
+    const double *DL = level_ptr(b, p, L - 1);
+    quantize_coarsest(p, DL, q, s);
+    return DL;
+}
+
 const double *decompose_quantize(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int dtype, const QuantOut &q,
                                  cudaStream_t s) {
     const double *DL = decompose_fused(ctx, p, d_in, dtype, nullptr, &q, s);
@@ -685,11 +796,16 @@ double *recompose_device(hpdr_ctx *ctx, DevPlan &p, const double *coef, cudaStre
     return b.lvl0;
 }
 
-void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s) {
+void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s,
+                    void *host_out) {
     const int L = p.host.L;
     if (L == 1 || !use_fused(p)) {
         const double *rec = recompose_device(ctx, p, coef, s);
         cast_output(rec, out, out_dtype, p.n_total, s);
+        if (host_out) {
+            static const int isz[7] = {4, 8, 4, 8, 4, 8, 1};
+            CUDA_CHECK(cudaMemcpyAsync(host_out, out, p.n_total * isz[out_dtype], cudaMemcpyDeviceToHost, s));
+        }
         return;
     }
     const bool direct = out_dtype == 0 || out_dtype == 1;
@@ -716,10 +832,34 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
             k_sub<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(Dc, b.t0, b.cg, nc);   // coarse - corr
             LAUNCH_CHECK();
         }
-        if (st_i == 0 && direct) fused_final(p, st_i, b.cg, coef, out, out_dtype, s);
-        else fused_final(p, st_i, b.cg, coef, level_ptr(b, p, st_i), 1, s);
+        if (st_i == 0 && direct && host_out) {
+            // finest level in dim-0 slabs; each slab's D2H (copy stream) overlaps the next slab
+            const int n0 = (int)st.fsh.n[1];
+            const int64_t plane_bytes = st.fsh.n[2] * st.fsh.n[3] * (out_dtype == 0 ? 4 : 8);
+            int chunk = (int)std::max<int64_t>(4, ((32LL << 20) + plane_bytes - 1) / std::max<int64_t>(plane_bytes, 1));
+            chunk = std::min(chunk, n0);
+            CUDA_CHECK(cudaEventRecord(ctx->event(0), ctx->d2h));
+            CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(0), 0));   // previous call's copies are done
+            for (int a = 0, k = 0; a < n0; a += chunk, k++) {
+                const int e = std::min(n0, a + chunk);
+                fused_final(p, 0, b.cg, coef, out, out_dtype, s, a, e);
+                CUDA_CHECK(cudaEventRecord(ctx->event(1 + k), s));
+                CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(1 + k), 0));
+                CUDA_CHECK(cudaMemcpyAsync((char *)host_out + a * plane_bytes, (const char *)out + a * plane_bytes,
+                                           (e - a) * plane_bytes, cudaMemcpyDeviceToHost, ctx->d2h));
+            }
+            CUDA_CHECK(cudaStreamSynchronize(ctx->d2h));
+        } else if (st_i == 0 && direct) {
+            fused_final(p, st_i, b.cg, coef, out, out_dtype, s);
+        } else {
+            fused_final(p, st_i, b.cg, coef, level_ptr(b, p, st_i), 1, s);
+        }
     }
     if (!direct) cast_output(b.lvl0, out, out_dtype, p.n_total, s);
+    if (host_out && !direct) {
+        static const int isz[7] = {4, 8, 4, 8, 4, 8, 1};
+        CUDA_CHECK(cudaMemcpyAsync(host_out, out, p.n_total * isz[out_dtype], cudaMemcpyDeviceToHost, s));
+    }
 }
 
 void cast_output(const double *src, void *dst, int dtype, int64_t n, cudaStream_t s) {

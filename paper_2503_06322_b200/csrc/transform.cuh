@@ -34,8 +34,19 @@ struct QuantOut;
 const double *decompose_quantize(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int dtype, const QuantOut &q,
                                  cudaStream_t s);
 
+// Streamed variant for a HOST input (L > 1, use_fused): dim-0 chunks are copied on the context's
+// H2D stream while the finest level's pass 1 / pass 2 run on the chunks that have landed.
+// Relative mode (has_range false) stores the finest coefficients and quantizes them once the
+// global min/max is complete; q.bin is set here.  Returns the coarsest dense level.
+const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void *host_in, int dtype, bool has_range,
+                                          double range_min, double range_max, double eb_rel, QuantOut &q,
+                                          double *u_min, double *u_max, cudaStream_t s);
+
 // Recompose straight into out (device) in the blob's dtype (fused final level for ranks <= 3).
-void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s);
+// With host_out the result also lands there: the finest level is produced in dim-0 slabs whose
+// D2H on the copy stream overlaps the next slab (out is then the device staging buffer).
+void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s,
+                    void *host_out = nullptr);
 
 // True when the fused level kernels serve these dims (ranks <= 3) and HPDR_GENERIC != 1.
 bool use_fused(const DevPlan &p);

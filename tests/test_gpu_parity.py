@@ -192,3 +192,32 @@ def test_config_c2_c3_c4_match_reference_hash():
         assert len(blob) == c["blob_len"] and hashlib.sha256(blob).hexdigest() == c["blob_sha"], name
         out = P.mgard_decompress(blob).values
         assert S.sha256(out) == c["out_sha"], name
+
+
+_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_2503_06322_b200 as P
+from oracle import oracle as O
+from paper_2503_06322_b200 import synthetic as S
+for shape in [(33, 34, 35), (16, 5, 7), (65, 40), (1000,), (12, 10, 9)]:
+    a = S.smooth_noise(shape, seed=3)
+    for vr in (None, (-1.0, 2.0)):
+        b = P.mgard_compress(a, 1e-3, value_range=vr)
+        assert b == O.mgard_compress(a, 1e-3, value_range=vr), (shape, vr)
+        y = P.mgard_decompress(b).values
+        assert np.array_equal(y.view(np.uint8), O.mgard_decompress(b).view(np.uint8)), shape
+print("variant ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"HPDR_GENERIC": "1"}, {"HPDR_NO_STREAM": "1"}])
+def test_execution_variants_bit_identical(env):
+    """The per-axis (generic) path and the non-streamed fused path give the same blobs."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT % root], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "variant ok" in r.stdout, r.stderr[-2000:]
