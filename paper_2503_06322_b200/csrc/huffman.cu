@@ -259,7 +259,8 @@ __global__ void k_decode(const uint32_t *__restrict__ words, uint64_t limit, con
                          const uint32_t *__restrict__ lut_g, const uint32_t *__restrict__ sym_by_rank,
                          uint32_t *__restrict__ keys, double *__restrict__ coef, double bin, uint32_t key_limit,
                          long long *__restrict__ unit_err, unsigned long long *__restrict__ first_bad,
-                         unsigned *__restrict__ max_key) {
+                         unsigned *__restrict__ max_key, int64_t u_base, uint64_t avail_words,
+                         int *__restrict__ deferred, int redo) {
     __shared__ uint32_t lut[kLutSize];
     __shared__ DecTables T;
     __shared__ uint32_t stage[kDecThreads][9];
@@ -269,7 +270,12 @@ __global__ void k_decode(const uint32_t *__restrict__ words, uint64_t limit, con
     __syncthreads();
     const int max_len = T.max_len;
     unsigned kmax = 0;
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < units; u += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t uu = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; uu < units; uu += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = u_base + uu;
+        if (redo) {   // second pass: only units that outran the streamed prefix
+            if (!deferred[u]) continue;
+            deferred[u] = 0;
+        }
         const uint64_t lo = (uint64_t)u * kBlockSymbols;
         const uint64_t cnt = nsym - lo < (uint64_t)kBlockSymbols ? nsym - lo : (uint64_t)kBlockSymbols;
         uint64_t pos = offs[u];
@@ -277,7 +283,12 @@ __global__ void k_decode(const uint32_t *__restrict__ words, uint64_t limit, con
         if (max_len <= 32 && pos < limit) {
             // Fast path: 64-bit bit buffer refilled a word at a time (next word prefetched),
             // 12-bit table lookup, canonical search for longer codes; 8 symbols per vector store.
+            // A unit that would read past the streamed prefix (avail_words) is deferred whole.
             uint64_t wi = pos >> 5;
+            if (wi + 2 >= avail_words) {
+                deferred[u] = 1;
+                continue;
+            }
             uint64_t buf = (((uint64_t)load_be(words, wi) << 32) | load_be(words, wi + 1)) << (pos & 31);
             int avail = 64 - (int)(pos & 31);
             uint64_t nw = wi + 2;
@@ -288,7 +299,11 @@ __global__ void k_decode(const uint32_t *__restrict__ words, uint64_t limit, con
                 if (avail < 32) {
                     buf |= (uint64_t)__byte_perm(pre, 0, 0x0123) << (32 - avail);
                     avail += 32;
-                    pre = __ldg(words + (++nw));
+                    if (++nw >= avail_words) {
+                        err = -3;   // deferred: the unit needs bytes that have not landed yet
+                        break;
+                    }
+                    pre = __ldg(words + nw);
                 }
                 if (pos >= limit) { err = (long long)pos; break; }
                 const uint32_t win = (uint32_t)(buf >> 32);
@@ -328,6 +343,10 @@ __global__ void k_decode(const uint32_t *__restrict__ words, uint64_t limit, con
                         }
                     }
                 }
+            }
+            if (err == -3) {
+                deferred[u] = 1;
+                continue;
             }
             if (err < 0) {   // tail of the last (partial) unit
                 for (uint64_t k = cnt & ~7ULL; k < cnt; k++) {
@@ -470,22 +489,59 @@ void decode_device(hpdr_ctx *ctx, const DecodeJob &job, DecodeResult &res, cudaS
     const size_t pwords = pbytes / 4 + 4;
     uint32_t *d_words = (uint32_t *)ctx->dbuf("dec_words", pwords * 4);
     CUDA_CHECK(cudaMemsetAsync((char *)d_words + (pbytes & ~size_t(3)), 0, 16, s));
-    CUDA_CHECK(cudaMemcpyAsync(d_words, job.packed, pbytes, cudaMemcpyDefault, s));
     long long *uerr = (long long *)ctx->dbuf("dec_err", (units + 1) * 8);
     unsigned long long *flag = (unsigned long long *)ctx->dbuf("dec_flag", 32);
+    int *deferred = (int *)ctx->dbuf("dec_defer", (units + 1) * 4);
+    CUDA_CHECK(cudaMemsetAsync(deferred, 0, (units + 1) * 4, s));
     unsigned long long init[2] = {~0ULL, 0ULL};
     unsigned long long *hinit = (unsigned long long *)ctx->hbuf("dec_init", 64);
     memcpy(hinit, init, 16);
     CUDA_CHECK(cudaMemcpyAsync(flag, hinit, 16, cudaMemcpyHostToDevice, s));
+    // Stream the payload in unit groups when it comes from the host: each group decodes as soon
+    // as its bytes (plus a small margin) have landed; units that outrun the prefix are redone.
+    std::vector<uint64_t> off;
+    bool stream = !job.packed_on_device && max_len <= 32 && units >= 256 && pbytes >= (size_t(8) << 20);
+    if (stream) {
+        off.resize(units);
+        memcpy(off.data(), job.offsets, units * 8);
+        for (int64_t u = 0; u < units && stream; u++)
+            if (off[u] > job.total_bits || (u && off[u] < off[u - 1])) stream = false;
+    }
+    auto launch = [&](int64_t ub, int64_t cnt, uint64_t avail_words, int redo) {
+        k_decode<<<grid_for(cnt, kDecThreads, 148 * 64), kDecThreads, 0, s>>>(
+            d_words, job.total_bits, d_off, job.n_symbols, cnt, (const DecTables *)d_tab,
+            (const uint32_t *)(d_tab + sizeof(DecTables)),
+            (const uint32_t *)(d_tab + sizeof(DecTables) + kLutSize * 4), job.keys, job.coef, job.bin_width,
+            job.key_limit, uerr, flag, (unsigned *)(flag + 1), ub, avail_words, deferred, redo);
+        LAUNCH_CHECK();
+    };
     if (units > 0) {
         KPROF("k_decode", job.total_bits / 8.0 + 8.0 * units +
                               (double)job.n_symbols * ((job.keys ? 4 : 0) + (job.coef ? 8 : 0)), s);
-        k_decode<<<grid_for(units, kDecThreads, 148 * 64), kDecThreads, 0, s>>>(
-            d_words, job.total_bits, d_off, job.n_symbols, units, (const DecTables *)d_tab,
-            (const uint32_t *)(d_tab + sizeof(DecTables)),
-            (const uint32_t *)(d_tab + sizeof(DecTables) + kLutSize * 4), job.keys, job.coef, job.bin_width,
-            job.key_limit, uerr, flag, (unsigned *)(flag + 1));
-        LAUNCH_CHECK();
+        if (!stream) {
+            CUDA_CHECK(cudaMemcpyAsync(d_words, job.packed, pbytes, cudaMemcpyDefault, s));
+            launch(0, units, pwords, 0);
+        } else {
+            const int G = 16;
+            size_t copied = 0;
+            CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
+            CUDA_CHECK(cudaStreamWaitEvent(ctx->h2d, ctx->event(0), 0));
+            for (int g = 0; g < G; g++) {
+                const int64_t ua = units * g / G, ub = units * (g + 1) / G;
+                if (ub <= ua) continue;
+                size_t want = pbytes;
+                if (ub < units) want = std::min<size_t>(pbytes, ((size_t)(off[ub] / 8) + 64) & ~size_t(3));
+                if (want > copied) {
+                    CUDA_CHECK(cudaMemcpyAsync((char *)d_words + copied, job.packed + copied, want - copied,
+                                               cudaMemcpyHostToDevice, ctx->h2d));
+                    copied = want;
+                }
+                CUDA_CHECK(cudaEventRecord(ctx->event(1 + g), ctx->h2d));
+                CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(1 + g), 0));
+                launch(ua, ub - ua, copied == pbytes ? (uint64_t)pwords : (uint64_t)(copied / 4), 0);
+            }
+            launch(0, units, pwords, 1);   // units that needed bytes beyond their group's prefix
+        }
     }
     unsigned long long *h = (unsigned long long *)ctx->hbuf("dec_rb", 32);
     CUDA_CHECK(cudaMemcpyAsync(h, flag, 16, cudaMemcpyDeviceToHost, s));

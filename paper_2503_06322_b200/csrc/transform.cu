@@ -603,7 +603,10 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
     chunk = std::min(chunk, n0);
     const int K = (n0 + chunk - 1) / chunk;
     unsigned long long *mm = (unsigned long long *)ctx->dbuf("minmax", 32);
-    if (!has_range) {
+    if (has_range) {   // absolute bound: the bin width is known before any data arrives
+        const double eb_abs = eb_rel * (range_max - range_min);
+        q.bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
+    } else {
         unsigned long long *h = (unsigned long long *)ctx->hbuf("minmax_h", 32);
         h[0] = ~0ULL;
         h[1] = 0ULL;
