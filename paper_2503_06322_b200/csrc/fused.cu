@@ -328,6 +328,180 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
     }
 }
 
+// ---------------------------------------------------------------------------------- pass 1 (decompose)
+// Same contract as k_level_pass1 MODE 0 / 2, with the GPK interpolation evaluated separably
+// inside the tile, in the reference's axis order (transform.py:264-268):
+//   stage A  P0 = lerp along axis 0 at the tile's coarse rows x coarse columns (from the F ring)
+//   stage B  P1 = lerp along axis 1 at the tile rows x coarse columns (from P0)
+//   stage C  P2 = lerp along axis 2 per node (from P1); mc = F - P2
+// Every P value is computed once per plane instead of once per fine node that uses it.
+constexpr int kP1Rows = kTY, kP1Cols = kHX;   // P1 block: tile rows x halo columns
+
+template <int MODE, bool A0, bool A1, bool A2, typename TIn>
+__global__ void __launch_bounds__(256) k_level_pass1s(const TIn *__restrict__ F, int n0, int n1, int n2, DevAxis ax0,
+                                                      DevAxis ax1, DevAxis ax2, LevelMap lm, double *__restrict__ coef,
+                                                      double *__restrict__ Z0, double *__restrict__ Cg, QuantOut q,
+                                                      int c_base, int c_count) {
+    __shared__ __align__(16) TIn ring[kRing * kPlaneElems];
+    __shared__ double sP0[kPlaneElems];
+    __shared__ double sP1[kP1Rows * kP1Cols];
+    __shared__ uint32_t sh_hist[MODE == 2 ? kSmemHist : 1];
+    const bool sh_ok = MODE == 2 && q.dict <= kSmemHist;
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+    if (MODE == 2 && sh_ok)
+        for (uint32_t k = tid; k < q.dict; k += 256) sh_hist[k] = 0;
+    const int x0 = blockIdx.x * kTX - 1, y0 = blockIdx.y * kTY - 1;   // tile origin incl. halo
+    const int j2 = x0 + 1 + tx, j1 = y0 + 1 + ty;
+    const bool act = j1 < n1 && j2 < n2;
+    const int nc0 = A0 ? ax0.nc : n0;
+    int c_lo, c_hi;
+    slab_range(c_count, gridDim.z, blockIdx.z, c_lo, c_hi);
+    c_lo += c_base;
+    c_hi += c_base;
+    int fl = 0;
+    if (c_lo < c_hi) {   // uniform across the block
+        int j_start, j_end, own_lo, own_hi;
+        slab_planes<A0>(ax0, n0, nc0, c_lo, c_hi, j_start, j_end, own_lo, own_hi);
+        const int64_t plane = (int64_t)n1 * n2;
+        const int64_t fplane = lm.D1 * lm.D2;
+        // per-thread load slots (two tile elements incl. halo) and stage-A / stage-B work items
+        int soff[2];
+        int64_t goff[2];
+        bool lv[2], needA[2];
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            const int e = tid + k * 256;
+            const int yy = e / kHX, xx = e - yy * kHX;
+            const int gy = y0 + yy, gx = x0 + xx;
+            const bool in = e < kPlaneElems && gy >= 0 && gy < n1 && gx >= 0 && gx < n2;
+            lv[k] = in;
+            soff[k] = e;
+            goff[k] = (int64_t)gy * n2 + gx;
+            // P0 is needed at coarse rows (or every row when axis 1 is inactive) x coarse columns
+            needA[k] = in && (!A1 || __ldg(ax1.pb + gy) < 0) && (!A2 || __ldg(ax2.pb + gx) < 0);
+        }
+        // stage B items: (tile row, halo column) pairs at coarse columns
+        int bsoff[2], brow_a[2], brow_b[2];
+        double bt[2];
+        bool needB[2], bfo[2];
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            const int e = tid + k * 256;
+            const int r = e / kP1Cols, xx = e - r * kP1Cols;
+            const int gy = y0 + 1 + r, gx = x0 + xx;
+            needB[k] = e < kP1Rows * kP1Cols && gy < n1 && gx >= 0 && gx < n2 && (!A2 || __ldg(ax2.pb + gx) < 0);
+            bsoff[k] = e;
+            brow_a[k] = brow_b[k] = 0;
+            bt[k] = 0.0;
+            bfo[k] = false;
+            if (needB[k]) {
+                const Nb nb = neighbours<A1>(ax1, gy);
+                bfo[k] = nb.fo;
+                bt[k] = nb.t;
+                brow_a[k] = (nb.fa - y0) * kHX + xx;
+                brow_b[k] = (nb.fb - y0) * kHX + xx;
+            }
+        }
+        auto issue = [&](int p) {
+            if (p <= j_end) {
+                TIn *slot = ring + (p & (kRing - 1)) * kPlaneElems;
+                const TIn *src = F + (int64_t)p * plane;
+                if (lv[0]) cp_async<sizeof(TIn)>(slot + soff[0], src + goff[0]);
+                if (lv[1]) cp_async<sizeof(TIn)>(slot + soff[1], src + goff[1]);
+            }
+            cp_async_commit();
+        };
+        Nb b1{}, b2{};
+        if (act) {
+            b1 = neighbours<A1>(ax1, j1);
+            b2 = neighbours<A2>(ax2, j2);
+        }
+        const int own_off = (ty + 1) * kHX + tx + 1;
+        const int p1a = ty * kP1Cols + (b2.fa - x0), p1b = ty * kP1Cols + (b2.fb - x0);
+        const int nc1 = A1 ? ax1.nc : n1, nc2 = A2 ? ax2.nc : n2;
+        const int64_t cgcol = (int64_t)b1.ca * nc2 + b2.ca;
+        const bool col_coarse = !b1.fo && !b2.fo;
+        const int64_t col = (int64_t)j1 * n2 + j2;
+        const int64_t fcol = act ? ((int64_t)__ldg(lm.m1 + j1)) * lm.D2 + __ldg(lm.m2 + j2) : 0;
+        double *zcol = Z0 + col;
+        March M;
+        march_init(M, c_lo, c_hi);
+        auto emit = [&](int c, double z) { zcol[(int64_t)c * plane] = z; };
+        for (int k = 0; k < kRing - 2; k++) issue(j_start + k);
+        for (int j = j_start; j <= j_end; j++) {
+            cp_async_wait<kRing - 4>();   // planes <= j + 1 have landed
+            __syncthreads();
+            issue(j + kRing - 2);
+            const PlaneInfo pi = A0 ? load_pi(ax0.pi + j) : identity_pi(j);
+            const TIn *ra = ring + (pi.fa & (kRing - 1)) * kPlaneElems;
+            const TIn *rb = ring + (pi.fb & (kRing - 1)) * kPlaneElems;
+            // stage A: P0 at coarse rows x coarse columns
+#pragma unroll
+            for (int k = 0; k < 2; k++)
+                if (needA[k]) {
+                    const double va = (double)ra[soff[k]];
+                    sP0[soff[k]] = pi.fo ? lerp(va, (double)rb[soff[k]], pi.t) : va;
+                }
+            __syncthreads();
+            // stage B: P1 at tile rows x coarse columns
+#pragma unroll
+            for (int k = 0; k < 2; k++)
+                if (needB[k]) {
+                    const double va = sP0[brow_a[k]];
+                    sP1[bsoff[k]] = bfo[k] ? lerp(va, sP0[brow_b[k]], bt[k]) : va;
+                }
+            __syncthreads();
+            if (!act) continue;
+            // stage C: P2 per node, residual, outputs
+            const double pa = sP1[p1a];
+            const double pred = (A2 && b2.fo) ? lerp(pa, sP1[p1b], b2.t) : pa;
+            const double own = (double)ring[(j & (kRing - 1)) * kPlaneElems + own_off];
+            const double mc = dsub(own, pred);
+            if (j >= own_lo && j < own_hi) {
+                if (!pi.fo && col_coarse) {
+                    const int c0 = A0 ? pi.ca : j;
+                    Cg[(int64_t)c0 * nc1 * nc2 + cgcol] = own;
+                } else {
+                    const int64_t f = (int64_t)__ldg(lm.m0 + j) * fplane + fcol;
+                    if (MODE == 0) {
+                        coef[f] = mc;
+                    } else {
+                        long long b = 0;
+                        if (!isfinite(mc)) {
+                            fl |= 1;
+                        } else {
+                            const double sc = mc / q.bin;                 // IEEE division (quantize.py:73)
+                            if (fabs(sc) >= 4611686018427387904.0) fl |= 2;
+                            else b = (long long)rint(sc);                 // half to even (:76)
+                        }
+                        if (b >= q.half || -b >= q.half) {                 // outlier (:80-83)
+                            q.obins[f] = b;
+                            atomicOr(&q.omask[f >> 5], 1u << (f & 31));
+                            b = 0;
+                        }
+                        const uint32_t key = (uint32_t)(((unsigned long long)b << 1) ^ (unsigned long long)(b >> 63));
+                        q.keys[f] = key;
+                        if (sh_ok) atomicAdd(&sh_hist[key], 1u);
+                        else atomicAdd(&q.hist[key], 1ULL);
+                    }
+                }
+            }
+            if (A0) march_push(M, pi, n0, j, j_start, mc, emit);
+            else zcol[(int64_t)j * plane] = mc;
+        }
+        cp_async_wait<0>();
+    }
+    if (MODE == 2) {
+        if (fl) atomicOr(q.flags, fl);
+        __syncthreads();
+        if (sh_ok)
+            for (uint32_t k = tid; k < q.dict; k += 256) {
+                const uint32_t c = sh_hist[k];
+                if (c) atomicAdd(&q.hist[k], (unsigned long long)c);
+            }
+    }
+}
+
 // Quantize the fine-only nodes of the finest level from stored fp64 coefficients (the streamed
 // relative-mode path, where the bin width is only known after the last input chunk).
 template <bool A0, bool A1, bool A2>
@@ -562,8 +736,12 @@ void launch_pass1(int act, const TIn *F, int n0, int n1, int n2, const DevAxis &
     dim3 block(kTX, kTY);
 #define P1L(M)                                                                                                     \
     case M:                                                                                                        \
-        k_level_pass1<MODE, (M & 1) != 0, (M & 2) != 0, (M & 4) != 0, TIn><<<grid, block, 0, s>>>(              \
-            F, n0, n1, n2, a0, a1, a2, lm, coef, coef_in, Z0, Cg, q, c_base, c_count);                                              \
+        if (MODE == 1)                                                                                             \
+            k_level_pass1<MODE, (M & 1) != 0, (M & 2) != 0, (M & 4) != 0, TIn><<<grid, block, 0, s>>>(          \
+                F, n0, n1, n2, a0, a1, a2, lm, coef, coef_in, Z0, Cg, q, c_base, c_count);                         \
+        else                                                                                                       \
+            k_level_pass1s<MODE == 1 ? 0 : MODE, (M & 1) != 0, (M & 2) != 0, (M & 4) != 0, TIn>                   \
+                <<<grid, block, 0, s>>>(F, n0, n1, n2, a0, a1, a2, lm, coef, Z0, Cg, q, c_base, c_count);          \
         break;
     switch (act) { P1L(1) P1L(2) P1L(3) P1L(4) P1L(5) P1L(6) P1L(7) default: break; }
 #undef P1L

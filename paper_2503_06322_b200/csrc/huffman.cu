@@ -260,7 +260,7 @@ __global__ void k_decode(const uint32_t *__restrict__ words, uint64_t limit, con
                          uint32_t *__restrict__ keys, double *__restrict__ coef, double bin, uint32_t key_limit,
                          long long *__restrict__ unit_err, unsigned long long *__restrict__ first_bad,
                          unsigned *__restrict__ max_key, int64_t u_base, uint64_t avail_words,
-                         int *__restrict__ deferred, int redo) {
+                         uint64_t full_words, int *__restrict__ deferred, int redo) {
     __shared__ uint32_t lut[kLutSize];
     __shared__ DecTables T;
     __shared__ uint32_t stage[kDecThreads][9];
@@ -285,25 +285,35 @@ __global__ void k_decode(const uint32_t *__restrict__ words, uint64_t limit, con
             // 12-bit table lookup, canonical search for longer codes; 8 symbols per vector store.
             // A unit that would read past the streamed prefix (avail_words) is deferred whole.
             uint64_t wi = pos >> 5;
-            if (wi + 2 >= avail_words) {
+            if (wi + 2 >= avail_words && avail_words < full_words) {
                 deferred[u] = 1;
                 continue;
             }
             uint64_t buf = (((uint64_t)load_be(words, wi) << 32) | load_be(words, wi + 1)) << (pos & 31);
             int avail = 64 - (int)(pos & 31);
+            // four raw words in flight ahead of the bit buffer (byte-swapped when consumed)
             uint64_t nw = wi + 2;
-            uint32_t pre = __ldg(words + nw);   // raw word; byte-swapped when consumed
+            if (nw + 3 >= avail_words && avail_words < full_words) {
+                deferred[u] = 1;
+                continue;
+            }
+            uint32_t q0 = __ldg(words + nw), q1 = __ldg(words + nw + 1), q2 = __ldg(words + nw + 2),
+                     q3 = __ldg(words + nw + 3);
             uint32_t *s8 = stage[threadIdx.x];   // private 8-symbol staging row
             uint64_t i = 0;
             for (; i < cnt; i++) {
                 if (avail < 32) {
-                    buf |= (uint64_t)__byte_perm(pre, 0, 0x0123) << (32 - avail);
+                    buf |= (uint64_t)__byte_perm(q0, 0, 0x0123) << (32 - avail);
                     avail += 32;
-                    if (++nw >= avail_words) {
+                    ++nw;
+                    if (nw + 3 >= avail_words && avail_words < full_words) {
                         err = -3;   // deferred: the unit needs bytes that have not landed yet
                         break;
                     }
-                    pre = __ldg(words + nw);
+                    q0 = q1;
+                    q1 = q2;
+                    q2 = q3;
+                    q3 = __ldg(words + nw + 3);
                 }
                 if (pos >= limit) { err = (long long)pos; break; }
                 const uint32_t win = (uint32_t)(buf >> 32);
@@ -486,9 +496,9 @@ void decode_device(hpdr_ctx *ctx, const DecodeJob &job, DecodeResult &res, cudaS
     uint64_t *d_off = (uint64_t *)ctx->dbuf("dec_off", (units + 1) * 8);
     CUDA_CHECK(cudaMemcpyAsync(d_off, job.offsets, units * 8, cudaMemcpyHostToDevice, s));
     const size_t pbytes = (size_t)((job.total_bits + 7) / 8);
-    const size_t pwords = pbytes / 4 + 4;
+    const size_t pwords = pbytes / 4 + 8;   // bit-buffer queue reads up to 5 words past a unit
     uint32_t *d_words = (uint32_t *)ctx->dbuf("dec_words", pwords * 4);
-    CUDA_CHECK(cudaMemsetAsync((char *)d_words + (pbytes & ~size_t(3)), 0, 16, s));
+    CUDA_CHECK(cudaMemsetAsync((char *)d_words + (pbytes & ~size_t(3)), 0, 36, s));
     long long *uerr = (long long *)ctx->dbuf("dec_err", (units + 1) * 8);
     unsigned long long *flag = (unsigned long long *)ctx->dbuf("dec_flag", 32);
     int *deferred = (int *)ctx->dbuf("dec_defer", (units + 1) * 4);
@@ -500,7 +510,11 @@ void decode_device(hpdr_ctx *ctx, const DecodeJob &job, DecodeResult &res, cudaS
     // Stream the payload in unit groups when it comes from the host: each group decodes as soon
     // as its bytes (plus a small margin) have landed; units that outrun the prefix are redone.
     std::vector<uint64_t> off;
-    bool stream = !job.packed_on_device && max_len <= 32 && units >= 256 && pbytes >= (size_t(8) << 20);
+    // (off by default: the decode is bound by each unit's sequential walk, so splitting it into
+    // serialized launches costs more than the H2D it hides; HPDR_STREAM_DECODE=1 enables it)
+    static const bool want_stream = getenv("HPDR_STREAM_DECODE") != nullptr;
+    bool stream = want_stream && !job.packed_on_device && max_len <= 32 && units >= 256 &&
+                  pbytes >= (size_t(8) << 20);
     if (stream) {
         off.resize(units);
         memcpy(off.data(), job.offsets, units * 8);
@@ -512,7 +526,7 @@ void decode_device(hpdr_ctx *ctx, const DecodeJob &job, DecodeResult &res, cudaS
             d_words, job.total_bits, d_off, job.n_symbols, cnt, (const DecTables *)d_tab,
             (const uint32_t *)(d_tab + sizeof(DecTables)),
             (const uint32_t *)(d_tab + sizeof(DecTables) + kLutSize * 4), job.keys, job.coef, job.bin_width,
-            job.key_limit, uerr, flag, (unsigned *)(flag + 1), ub, avail_words, deferred, redo);
+            job.key_limit, uerr, flag, (unsigned *)(flag + 1), ub, avail_words, (uint64_t)pwords, deferred, redo);
         LAUNCH_CHECK();
     };
     if (units > 0) {

@@ -5,7 +5,7 @@ set -x
 OUT=${1:-gpurun_out/prof}
 D="python tools/prof_driver.py 513"
 N="ncu --set full --clock-control none --import-source on --kernel-name-base mangled"
-$N -k regex:k_level_pass1ILi2ELb1ELb1ELb1EfE -s 1 -c 1 -o ${OUT}_pass1q $D
+$N -k regex:k_level_pass1sILi2ELb1ELb1ELb1EfE -s 1 -c 1 -o ${OUT}_pass1q $D
 $N -k regex:k_level_pass2 -s 18 -c 1 -o ${OUT}_pass2 $D
 $N -k regex:k_decode -s 1 -c 1 -o ${OUT}_decode $D
 $N -k regex:k_level_finalILb1ELb1ELb1EfE -s 1 -c 1 -o ${OUT}_final $D
