@@ -120,11 +120,9 @@ void huffman_stage(hpdr_ctx *ctx, const uint32_t *d_keys, int64_t n, uint32_t di
 }
 
 // Write the pending stream (head | outliers | mid | offsets | total_bits | packed) to out.
-void fetch_pending(hpdr_ctx *ctx, void *out, uint64_t cap) {
-    auto &P = ctx->pending;
+void fetch_pending(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uint64_t cap, cudaStream_t s, bool sync) {
     if (!P.valid) fail(HPDR_ERR_VALIDATION, "no pending compressed stream in this context");
     if (cap < P.total_len) fail(HPDR_ERR_BUFFER, "output buffer too small: need " + std::to_string(P.total_len));
-    cudaStream_t s = ctx->stream;
     const bool dev = classify(out) == MemKind::Device;
     uint8_t *o = (uint8_t *)out;
     uint64_t pos = 0;
@@ -141,21 +139,23 @@ void fetch_pending(hpdr_ctx *ctx, void *out, uint64_t cap) {
     };
     if (!P.huffman_only) {
         host_bytes(P.head.data(), P.head.size());
-        dev_bytes(ctx->dbuf("oidx", P.n_out * 8), P.n_out * 8);
-        dev_bytes(ctx->dbuf("obins", P.n_out * 8), P.n_out * 8);
+        dev_bytes(ctx->dbuf(ctx->oname("oidx", P.slot), P.n_out * 8), P.n_out * 8);
+        dev_bytes(ctx->dbuf(ctx->oname("obins", P.slot), P.n_out * 8), P.n_out * 8);
     }
     host_bytes(P.mid.data(), P.mid.size());
     if (!P.single_key) {
-        dev_bytes(ctx->dbuf("enc_uoff", (P.n_units + 1) * 8), P.n_units * 8);
+        dev_bytes(ctx->dbuf(ctx->oname("enc_uoff", P.slot), (P.n_units + 1) * 8), P.n_units * 8);
         uint64_t tb = P.total_bits;
         host_bytes(&tb, 8);
-        dev_bytes(ctx->dbuf("enc_words", (P.total_bits + 31) / 32 * 4 + 8), (P.total_bits + 7) / 8);
+        dev_bytes(ctx->dbuf(ctx->oname("enc_words", P.slot), (P.total_bits + 31) / 32 * 4 + 8), (P.total_bits + 7) / 8);
     } else {
         uint64_t z = 0;
         host_bytes(&z, 8);
     }
-    CUDA_CHECK(cudaStreamSynchronize(s));
+    if (sync) CUDA_CHECK(cudaStreamSynchronize(s));
 }
+
+void fetch_pending(hpdr_ctx *ctx, void *out, uint64_t cap) { fetch_pending(ctx, ctx->pending, out, cap, ctx->stream, true); }
 
 struct HuffHeader {
     uint32_t dict = 0;
@@ -327,11 +327,14 @@ using namespace hpdr;
 
 extern "C" {
 
-int hpdr_mgard_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, double eb_rel,
-                        uint32_t dict_size, int has_range, double range_min, double range_max, void *out,
-                        uint64_t out_cap, uint64_t *blob_len) {
-    return guard([&] {
-        CUDA_CHECK(cudaSetDevice(ctx->device));
+}  // extern "C"
+
+namespace hpdr {
+// mgard_compress (codec.py:25-56) up to a pending blob in ctx->pending (device parts in output
+// slot ctx->out_slot).  allow_stream: a host input may be streamed in dim-0 chunks.
+void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, double eb_rel,
+                   uint32_t dict_size, int has_range, double range_min, double range_max, bool allow_stream) {
+    {
         ctx->pending.valid = false;
         if (dtype != 0 && dtype != 1) fail(HPDR_ERR_VALIDATION, "lossy compression needs F32/F64");
         DevPlan &p = ctx->plan(rank, dims);
@@ -345,7 +348,7 @@ int hpdr_mgard_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, cons
         const bool host_in = classify(in) != MemKind::Device;
         const bool fused = L > 1 && use_fused(p);
         static const bool no_stream = getenv("HPDR_NO_STREAM") != nullptr;
-        const bool streamed = host_in && fused && !no_stream;
+        const bool streamed = host_in && fused && !no_stream && allow_stream;
         const void *d_in = streamed ? nullptr : device_input(ctx, in, (size_t)N * itemsize(dtype), "input", s);
         double u_min = range_min, u_max = range_max;
         if (!has_range && !streamed) minmax_device(ctx, d_in, dtype, N, &u_min, &u_max, s);
@@ -417,10 +420,24 @@ int hpdr_mgard_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, cons
         P.n_units = enc.n_units;
         P.total_bits = enc.total_bits;
         P.total_len = P.head.size() + 16 * P.n_out + P.mid.size() + 8 * P.n_units + 8 + (P.total_bits + 7) / 8;
+        P.slot = ctx->out_slot;
         P.valid = true;
-        *blob_len = P.total_len;
-        if (out && out_cap >= P.total_len) fetch_pending(ctx, out, out_cap);
-        else CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+}
+}  // namespace hpdr
+
+extern "C" {
+
+int hpdr_mgard_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, double eb_rel,
+                        uint32_t dict_size, int has_range, double range_min, double range_max, void *out,
+                        uint64_t out_cap, uint64_t *blob_len) {
+    return guard([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        ctx->out_slot = 0;
+        compress_core(ctx, in, dtype, rank, dims, eb_rel, dict_size, has_range, range_min, range_max, true);
+        *blob_len = ctx->pending.total_len;
+        if (out && out_cap >= ctx->pending.total_len) fetch_pending(ctx, out, out_cap);
+        else CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     });
 }
 

@@ -80,7 +80,14 @@ struct hpdr_ctx {
         uint64_t total_len = 0;
         bool single_key = false;
         bool huffman_only = false;
+        int slot = 0;                    // which output buffer set holds the device parts
     } pending;
+
+    // Compress outputs (outliers, unit offsets, packed words) live in one of two buffer sets so
+    // the pipeline can copy chunk k out while chunk k+1 is being reduced.
+    int out_slot = 0;
+    std::string oname(const char *base, int slot) const { return slot ? std::string(base) + "#1" : std::string(base); }
+    std::string oname(const char *base) const { return oname(base, out_slot); }
 
     std::vector<cudaEvent_t> events;   // reusable sync events (no timing)
     cudaEvent_t event(size_t i);

@@ -734,9 +734,10 @@ void launch_pass1(int act, const TIn *F, int n0, int n1, int n2, const DevAxis &
     if (c_count <= 0) return;
     dim3 grid((n2 + kTX - 1) / kTX, (n1 + kTY - 1) / kTY, slabs_for((int64_t)n1 * n2, c_count));
     dim3 block(kTX, kTY);
+    static const bool separable = getenv("HPDR_P1_SEPARABLE") != nullptr;
 #define P1L(M)                                                                                                     \
     case M:                                                                                                        \
-        if (MODE == 1)                                                                                             \
+        if (MODE == 1 || !separable)                                                                               \
             k_level_pass1<MODE, (M & 1) != 0, (M & 2) != 0, (M & 4) != 0, TIn><<<grid, block, 0, s>>>(          \
                 F, n0, n1, n2, a0, a1, a2, lm, coef, coef_in, Z0, Cg, q, c_base, c_count);                         \
         else                                                                                                       \

@@ -204,7 +204,7 @@ void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict
     uint8_t *d_len = (uint8_t *)ctx->dbuf("enc_len", dict_size + 16);
     uint32_t *d_code = (uint32_t *)ctx->dbuf("enc_code", (size_t)dict_size * 4 + 16);
     uint64_t *ubits = (uint64_t *)ctx->dbuf("enc_ubits", (units + 1) * 8);
-    uint64_t *uoff = (uint64_t *)ctx->dbuf("enc_uoff", (units + 1) * 8);
+    uint64_t *uoff = (uint64_t *)ctx->dbuf(ctx->oname("enc_uoff"), (units + 1) * 8);
     CUDA_CHECK(cudaMemcpyAsync(d_len, lengths, dict_size, cudaMemcpyHostToDevice, s));
     CUDA_CHECK(cudaMemcpyAsync(d_code, codes, (size_t)dict_size * 4, cudaMemcpyHostToDevice, s));
     {
@@ -224,7 +224,7 @@ void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict
     CUDA_CHECK(cudaStreamSynchronize(s));
     res.total_bits = h[0];
     const size_t words = (size_t)((res.total_bits + 31) / 32) + 2;
-    res.d_words = (uint32_t *)ctx->dbuf("enc_words", words * 4);
+    res.d_words = (uint32_t *)ctx->dbuf(ctx->oname("enc_words"), words * 4);
     CUDA_CHECK(cudaMemsetAsync(res.d_words, 0, words * 4, s));
     KPROF("k_encode", 4.0 * n + 16.0 * units + res.total_bits / 8.0, s);
     k_encode<<<(unsigned)std::min<int64_t>(units, 148 * 8), kEncThreads, 0, s>>>(keys, n, d_len, d_code, dict_size, uoff,
@@ -291,29 +291,34 @@ __global__ void k_decode(const uint32_t *__restrict__ words, uint64_t limit, con
             }
             uint64_t buf = (((uint64_t)load_be(words, wi) << 32) | load_be(words, wi + 1)) << (pos & 31);
             int avail = 64 - (int)(pos & 31);
-            // four raw words in flight ahead of the bit buffer (byte-swapped when consumed)
-            uint64_t nw = wi + 2;
-            if (nw + 3 >= avail_words && avail_words < full_words) {
+            // raw words come in aligned 4-word groups: `cur` is being consumed while `nxt` is in
+            // flight (issued a whole group, ~24 symbols, before it is needed)
+            const uint64_t nw = wi + 2;
+            uint64_t g = nw >> 2;
+            int kq = (int)(nw & 3);
+            if (4 * (g + 2) > avail_words && avail_words < full_words) {
                 deferred[u] = 1;
                 continue;
             }
-            uint32_t q0 = __ldg(words + nw), q1 = __ldg(words + nw + 1), q2 = __ldg(words + nw + 2),
-                     q3 = __ldg(words + nw + 3);
+            const uint4 *w4 = reinterpret_cast<const uint4 *>(words);
+            uint4 cur = __ldg(w4 + g), nxt = __ldg(w4 + g + 1);
             uint32_t *s8 = stage[threadIdx.x];   // private 8-symbol staging row
             uint64_t i = 0;
             for (; i < cnt; i++) {
                 if (avail < 32) {
-                    buf |= (uint64_t)__byte_perm(q0, 0, 0x0123) << (32 - avail);
+                    const uint32_t wv = kq == 0 ? cur.x : kq == 1 ? cur.y : kq == 2 ? cur.z : cur.w;
+                    buf |= (uint64_t)__byte_perm(wv, 0, 0x0123) << (32 - avail);
                     avail += 32;
-                    ++nw;
-                    if (nw + 3 >= avail_words && avail_words < full_words) {
-                        err = -3;   // deferred: the unit needs bytes that have not landed yet
-                        break;
+                    if (++kq == 4) {
+                        kq = 0;
+                        g++;
+                        if (4 * (g + 2) > avail_words && avail_words < full_words) {
+                            err = -3;   // deferred: the unit needs bytes that have not landed yet
+                            break;
+                        }
+                        cur = nxt;
+                        nxt = __ldg(w4 + g + 1);
                     }
-                    q0 = q1;
-                    q1 = q2;
-                    q2 = q3;
-                    q3 = __ldg(words + nw + 3);
                 }
                 if (pos >= limit) { err = (long long)pos; break; }
                 const uint32_t win = (uint32_t)(buf >> 32);
@@ -496,9 +501,9 @@ void decode_device(hpdr_ctx *ctx, const DecodeJob &job, DecodeResult &res, cudaS
     uint64_t *d_off = (uint64_t *)ctx->dbuf("dec_off", (units + 1) * 8);
     CUDA_CHECK(cudaMemcpyAsync(d_off, job.offsets, units * 8, cudaMemcpyHostToDevice, s));
     const size_t pbytes = (size_t)((job.total_bits + 7) / 8);
-    const size_t pwords = pbytes / 4 + 8;   // bit-buffer queue reads up to 5 words past a unit
+    const size_t pwords = ((pbytes / 4 + 12) & ~size_t(3));   // 4-word groups read up to 2 groups ahead
     uint32_t *d_words = (uint32_t *)ctx->dbuf("dec_words", pwords * 4);
-    CUDA_CHECK(cudaMemsetAsync((char *)d_words + (pbytes & ~size_t(3)), 0, 36, s));
+    CUDA_CHECK(cudaMemsetAsync((char *)d_words + (pbytes & ~size_t(3)), 0, pwords * 4 - (pbytes & ~size_t(3)), s));
     long long *uerr = (long long *)ctx->dbuf("dec_err", (units + 1) * 8);
     unsigned long long *flag = (unsigned long long *)ctx->dbuf("dec_flag", 32);
     int *deferred = (int *)ctx->dbuf("dec_defer", (units + 1) * 4);

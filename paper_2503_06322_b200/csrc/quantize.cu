@@ -204,8 +204,8 @@ void quantize_finish(hpdr_ctx *ctx, int64_t n, uint32_t dict_size, double bin_wi
     res.flags = fl;
     res.hist.assign(h + 2, h + 2 + dict_size);
     if (fl) return;
-    res.d_outlier_idx = (uint64_t *)ctx->dbuf("oidx", res.n_outliers * 8);
-    res.d_outlier_bins = (int64_t *)ctx->dbuf("obins", res.n_outliers * 8);
+    res.d_outlier_idx = (uint64_t *)ctx->dbuf(ctx->oname("oidx"), res.n_outliers * 8);
+    res.d_outlier_bins = (int64_t *)ctx->dbuf(ctx->oname("obins"), res.n_outliers * 8);
     if (res.n_outliers) {
         KPROF("k_write_outliers", 4.0 * words + 24.0 * res.n_outliers, s);
         k_write_outliers<<<(unsigned)chunks, 256, 0, s>>>(omask, words, coef, obins_sparse, bin_width, coff,
