@@ -37,6 +37,7 @@ extern "C" {
 #define HPDR_ERR_OVERFLOW    6  /* OverflowError: canonical code leaves uint32 (huffman.py:201) */
 #define HPDR_ERR_VALUE       7  /* ValueError: coarse-value broadcast mismatch (quantize.py:117) */
 #define HPDR_ERR_BUFFER      8  /* caller-supplied buffer too small            */
+#define HPDR_ERR_FORMAT      9  /* hpdr.errors.FormatError: bad container (errors.py:32) */
 
 typedef struct hpdr_ctx hpdr_ctx;
 
@@ -75,6 +76,21 @@ int hpdr_mgard_peek(const void *blob, uint64_t len, int *dtype, int *rank, uint6
 /* mgard_decompress (codec.py:59-113).  out receives prod(dims) values of the
  * blob's dtype (host or device pointer). */
 int hpdr_mgard_decompress(hpdr_ctx *ctx, const void *blob, uint64_t len, void *out, uint64_t out_bytes);
+
+/* ---- overlapped host<->device pipeline ----
+ * The field is split into dim-0 chunks of chunk_planes planes (0: ~64 MB), or into the explicit
+ * plane counts chunk_list[0..n_list) (the adaptive schedule of Algorithm 4); each chunk becomes a
+ * reference-identical MGARD blob compressed with the global value range (computed on the host
+ * when has_range is 0), written into an HPDR container.  H2D of chunk k+1 and D2H of chunk k-1
+ * overlap the reduction of chunk k (two input buffers, two output sets, Fig. 7 reuse edges).
+ * trace (nullable) receives 6 doubles per chunk: H2D, compute, D2H start/end in ms. */
+int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int rank, const uint64_t *dims,
+                           double eb_rel, uint32_t dict_size, int has_range, double range_min,
+                           double range_max, uint64_t chunk_planes, const uint64_t *chunk_list,
+                           uint64_t n_list, void *out, uint64_t out_cap, uint64_t *out_len,
+                           double *trace);
+int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len, void *out,
+                             uint64_t out_bytes, double *trace);
 
 /* Global min/max of a field (transform.py:304-305 u.values.min()/max(); NaN propagates).
  * Used to agree on one value_range across slabs / ranks before quantization. */

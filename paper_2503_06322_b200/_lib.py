@@ -11,12 +11,12 @@ import threading
 
 import numpy as np
 
-from .errors import AllocationError, CorruptStreamError, DeviceError, ValidationError
+from .errors import AllocationError, CorruptStreamError, DeviceError, FormatError, ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(_HERE, "libhpdr_b200.so")
 
-OK, VALIDATION, CORRUPT, ALLOCATION, CUDA, INDEX, OVERFLOW, VALUE, BUFFER = range(9)
+OK, VALIDATION, CORRUPT, ALLOCATION, CUDA, INDEX, OVERFLOW, VALUE, BUFFER, FORMAT = range(10)
 
 _u64p = C.POINTER(C.c_uint64)
 _i64p = C.POINTER(C.c_int64)
@@ -53,6 +53,10 @@ _SIGS = {
     "hpdr_prof_read": (C.c_int, [C.c_char_p, C.c_uint64]),
     "hpdr_ctx_stream": (C.c_void_p, [C.c_void_p]),
     "hpdr_minmax": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, _dp, _dp]),
+    "hpdr_pipeline_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _u64p, C.c_double, C.c_uint32,
+                                         C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_void_p, C.c_uint64,
+                                         C.c_void_p, C.c_uint64, _u64p, C.c_void_p]),
+    "hpdr_pipeline_decompress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p]),
 }
 
 _lib = None
@@ -95,6 +99,8 @@ def check(rc: int):
         raise ValueError(msg)
     if rc == BUFFER:
         raise ValueError(msg)
+    if rc == FORMAT:
+        raise FormatError(msg)
     raise DeviceError(msg)
 
 

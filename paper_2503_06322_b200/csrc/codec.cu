@@ -165,6 +165,7 @@ struct HuffHeader {
     const uint8_t *offsets = nullptr;
     uint64_t total_bits = 0;
     const uint8_t *packed = nullptr;
+    const uint8_t *packed_dev = nullptr;   // device copy of the packed bits, when available
     uint32_t n_present = 0, first_present = 0;
     bool single = false;
 };
@@ -228,7 +229,8 @@ DecodeResult run_decode(hpdr_ctx *ctx, const HuffHeader &h, uint32_t *keys, doub
     job.n_units = (h.n_sym + kBlockSymbols - 1) / kBlockSymbols;
     job.offsets = h.offsets;
     job.total_bits = h.total_bits;
-    job.packed = h.packed;
+    job.packed = h.packed_dev ? h.packed_dev : h.packed;
+    job.packed_on_device = h.packed_dev != nullptr;
     job.keys = keys;
     job.coef = coef;
     job.bin_width = bin;
@@ -330,6 +332,10 @@ extern "C" {
 }  // extern "C"
 
 namespace hpdr {
+void fetch_pending_on(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uint64_t cap, cudaStream_t s, bool sync) {
+    fetch_pending(ctx, P, out, cap, s, sync);
+}
+
 // mgard_compress (codec.py:25-56) up to a pending blob in ctx->pending (device parts in output
 // slot ctx->out_slot).  allow_stream: a host input may be streamed in dim-0 chunks.
 void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, double eb_rel,
@@ -464,9 +470,15 @@ int hpdr_mgard_peek(const void *blob, uint64_t len, int *dtype, int *rank, uint6
     });
 }
 
-int hpdr_mgard_decompress(hpdr_ctx *ctx, const void *blob_in, uint64_t len, void *out, uint64_t out_bytes) {
-    return guard([&] {
-        CUDA_CHECK(cudaSetDevice(ctx->device));
+}  // extern "C"
+
+namespace hpdr {
+// mgard_decompress (codec.py:59-113).  The header is parsed from the host copy of the blob;
+// when dev_blob (a device copy of the same bytes) is given, the bulk parts (outliers, packed
+// bits) are read from it instead of being copied from the host.
+void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uint8_t *dev_blob, void *out,
+                     uint64_t out_bytes, bool sync) {
+    {
         cudaStream_t s = ctx->stream;
         const uint8_t *blob = (const uint8_t *)blob_in;
         std::vector<uint8_t> hostcopy;
@@ -506,6 +518,7 @@ int hpdr_mgard_decompress(hpdr_ctx *ctx, const void *blob_in, uint64_t len, void
         // huffman_decompress(data[pos:])
         HuffHeader hh;
         const bool has_syms = parse_huffman(blob + r.pos, len - r.pos, hh);
+        if (dev_blob && hh.packed) hh.packed_dev = dev_blob + (hh.packed - blob);
         const uint64_t n_sym = has_syms ? hh.n_sym : 0;
         // build_hierarchy(dims) (hierarchy.py:63-66) and the level check (codec.py:95-96)
         bool dims_ok = true;
@@ -535,8 +548,9 @@ int hpdr_mgard_decompress(hpdr_ctx *ctx, const void *blob_in, uint64_t len, void
             fail(HPDR_ERR_VALIDATION, rank == 0 ? "dims must be non-empty" : "rank exceeds maximum 4");
         }
         DevPlan &p = *pp;
-        int rc = scatter_outliers(ctx, coef, (int64_t)N, (const uint64_t *)(blob + oidx_off),
-                                  (const int64_t *)(blob + obins_off), n_out, bin, s);
+        const uint8_t *bulk = dev_blob ? dev_blob : blob;
+        int rc = scatter_outliers(ctx, coef, (int64_t)N, (const uint64_t *)(bulk + oidx_off),
+                                  (const int64_t *)(bulk + obins_off), n_out, bin, s);
         if (rc == HPDR_ERR_INDEX) fail(rc, "outlier index out of bounds for axis 0 with size " + std::to_string(N));
         restore_coarse(ctx, coef, p, coarse.data(), n_co, s);
         // codec.py:112-113 recompose, then TensorData(dims, dtype, values.astype(dtype))
@@ -548,7 +562,17 @@ int hpdr_mgard_decompress(hpdr_ctx *ctx, const void *blob_in, uint64_t len, void
             void *stage = ctx->dbuf("out_stage", ob);
             recompose_into(ctx, p, coef, stage, dtype, s, out);
         }
-        CUDA_CHECK(cudaStreamSynchronize(s));
+        if (sync) CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+}
+}  // namespace hpdr
+
+extern "C" {
+
+int hpdr_mgard_decompress(hpdr_ctx *ctx, const void *blob_in, uint64_t len, void *out, uint64_t out_bytes) {
+    return guard([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        decompress_core(ctx, blob_in, len, nullptr, out, out_bytes, true);
     });
 }
 

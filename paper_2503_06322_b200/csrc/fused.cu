@@ -60,18 +60,13 @@ __device__ __forceinline__ Nb neighbours(const DevAxis &ax, int j) {
 struct March {
     double m1, m2;        // x(j-1), x(j-2)
     double ya, yb, yc;    // y(k-2), y(k-1), y(k)
-    double pmd, pml, pmu, pwr, pwl;   // PlaneInfo of j-1 (the y computed next)
-    int pemit, prr, prl;
-    int c_lo, c_hi;                    // coarse outputs this march owns
+    int c_lo, c_hi;       // coarse outputs this march owns
 };
 
 __device__ __forceinline__ void march_init(March &M, int c_lo, int c_hi) {
     M.c_lo = c_lo;
     M.c_hi = c_hi;
     M.m1 = M.m2 = M.ya = M.yb = M.yc = 0.0;
-    M.pmd = M.pml = M.pmu = M.pwr = M.pwl = 0.0;
-    M.pemit = -1;
-    M.prr = M.prl = 0;
 }
 
 template <class Emit>
@@ -93,32 +88,32 @@ __device__ __forceinline__ void march_y(March &M, double v, int emit, int rr, in
     }
 }
 
-// Push x(j) with its PlaneInfo pi; emits every restricted value that became computable.
+// y(k) and its emission for fine index k, reading k's PlaneInfo from the (L1-resident) table.
 template <class Emit>
-__device__ __forceinline__ void march_push(March &M, const PlaneInfo &pi, int n, int j, int j_start, double x,
-                                           Emit &&out) {
+__device__ __forceinline__ void march_emit_y(March &M, const PlaneInfo *__restrict__ P, int k, double xk, double xkm1,
+                                             double xkp1, bool has_up, Emit &&out) {
+    const PlaneInfo *p = P + k;
+    double v = dmul(__ldg(&p->md), xk);
+    if (k >= 1) v = dadd(v, dmul(__ldg(&p->ml), xkm1));
+    if (has_up) v = dadd(v, dmul(__ldg(&p->mu), xkp1));
+    const int4 e = __ldg(reinterpret_cast<const int4 *>(&p->fo));   // fo, emit, e_rr, e_rl
+    double wr = 0.0, wl = 0.0;
+    if (e.y >= M.c_lo && e.y < M.c_hi) {
+        wr = __ldg(&p->ewr);
+        wl = __ldg(&p->ewl);
+    }
+    march_y(M, v, e.y, e.z, e.w, wr, wl, out);
+}
+
+// Push x(j) (PlaneInfo table P); emits every restricted value that became computable.
+template <class Emit>
+__device__ __forceinline__ void march_push(March &M, const PlaneInfo *__restrict__ P, int n, int j, int j_start,
+                                           double x, Emit &&out) {
     // y(j-1) needs x(j-2) unless j-1 == 0
-    if (j >= 1 && j - 1 >= j_start && (j - 1 == 0 || j - 2 >= j_start)) {
-        double v = dmul(M.pmd, M.m1);
-        if (j - 1 >= 1) v = dadd(v, dmul(M.pml, M.m2));
-        v = dadd(v, dmul(M.pmu, x));
-        march_y(M, v, M.pemit, M.prr, M.prl, M.pwr, M.pwl, out);
-    }
-    if (j == n - 1 && (j == 0 || j - 1 >= j_start)) {
-        double v = dmul(pi.md, x);
-        if (j >= 1) v = dadd(v, dmul(pi.ml, M.m1));
-        march_y(M, v, pi.emit, pi.e_rr, pi.e_rl, pi.ewr, pi.ewl, out);
-    }
+    if (j >= 1 && j - 1 >= j_start && (j - 1 == 0 || j - 2 >= j_start)) march_emit_y(M, P, j - 1, M.m1, M.m2, x, true, out);
+    if (j == n - 1 && (j == 0 || j - 1 >= j_start)) march_emit_y(M, P, j, x, M.m1, 0.0, false, out);
     M.m2 = M.m1;
     M.m1 = x;
-    M.pmd = pi.md;
-    M.pml = pi.ml;
-    M.pmu = pi.mu;
-    M.pwr = pi.ewr;
-    M.pwl = pi.ewl;
-    M.pemit = pi.emit;
-    M.prr = pi.e_rr;
-    M.prl = pi.e_rl;
 }
 
 __device__ __forceinline__ PlaneInfo load_pi(const PlaneInfo *__restrict__ p) {
@@ -130,6 +125,31 @@ __device__ __forceinline__ PlaneInfo load_pi(const PlaneInfo *__restrict__ p) {
         memcpy((char *)&r + 16 * k, &v, 16);
     }
     return r;
+}
+
+// The interpolation part of a PlaneInfo record (what pass 1 needs per plane).
+struct PiHead {
+    int fa, fb, ca, fo;
+    double t;
+};
+
+__device__ __forceinline__ PiHead load_head(const PlaneInfo *__restrict__ p) {
+    const int4 a = __ldg(reinterpret_cast<const int4 *>(p));   // fa, fb, ca, cb
+    PiHead h;
+    h.fa = a.x;
+    h.fb = a.y;
+    h.ca = a.z;
+    h.fo = __ldg(&p->fo);
+    h.t = __ldg(&p->t);
+    return h;
+}
+
+__device__ __forceinline__ PiHead identity_head(int j) {
+    PiHead h;
+    h.fa = h.fb = h.ca = j;
+    h.fo = 0;
+    h.t = 0.0;
+    return h;
 }
 
 __device__ __forceinline__ PlaneInfo identity_pi(int j) {
@@ -258,7 +278,7 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
             __syncthreads();
             issue(j + kRing - 2);          // into the slot of plane j - 2 (no longer read)
             if (!act) continue;
-            const PlaneInfo pi = A0 ? load_pi(ax0.pi + j) : identity_pi(j);
+            const PiHead pi = A0 ? load_head(ax0.pi + j) : identity_head(j);
             const bool coarse_node = !pi.fo && col_coarse;
             const TIn *rj = ring + (j & (kRing - 1)) * kPlaneElems;
             double mc;
@@ -312,7 +332,7 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
             } else {
                 mc = coarse_node ? 0.0 : (double)rj[own_off];
             }
-            if (A0) march_push(M, pi, n0, j, j_start, mc, emit);
+            if (A0) march_push(M, ax0.pi, n0, j, j_start, mc, emit);
             else Z0[(int64_t)j * plane + col] = mc;
         }
         cp_async_wait<0>();
@@ -432,7 +452,7 @@ __global__ void __launch_bounds__(256) k_level_pass1s(const TIn *__restrict__ F,
             cp_async_wait<kRing - 4>();   // planes <= j + 1 have landed
             __syncthreads();
             issue(j + kRing - 2);
-            const PlaneInfo pi = A0 ? load_pi(ax0.pi + j) : identity_pi(j);
+            const PiHead pi = A0 ? load_head(ax0.pi + j) : identity_head(j);
             const TIn *ra = ring + (pi.fa & (kRing - 1)) * kPlaneElems;
             const TIn *rb = ring + (pi.fb & (kRing - 1)) * kPlaneElems;
             // stage A: P0 at coarse rows x coarse columns
@@ -486,7 +506,7 @@ __global__ void __launch_bounds__(256) k_level_pass1s(const TIn *__restrict__ F,
                     }
                 }
             }
-            if (A0) march_push(M, pi, n0, j, j_start, mc, emit);
+            if (A0) march_push(M, ax0.pi, n0, j, j_start, mc, emit);
             else zcol[(int64_t)j * plane] = mc;
         }
         cp_async_wait<0>();
@@ -657,7 +677,7 @@ __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__rest
         cp_async_wait<kP2Ring - 2>();   // row j has landed (own copies)
         const double x = in ? ring[j % kP2Ring][t] : 0.0;
         issue(j + kP2Ring - 1);          // into the slot of row j - 1
-        if (A1) march_push(M, load_pi(ax1.pi + j), n1, j, j_start, x, out_row);
+        if (A1) march_push(M, ax1.pi, n1, j, j_start, x, out_row);
         else out_row(j, x);
     }
     cp_async_wait<0>();

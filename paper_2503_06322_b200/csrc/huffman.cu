@@ -535,10 +535,10 @@ void decode_device(hpdr_ctx *ctx, const DecodeJob &job, DecodeResult &res, cudaS
         LAUNCH_CHECK();
     };
     if (units > 0) {
-        KPROF("k_decode", job.total_bits / 8.0 + 8.0 * units +
-                              (double)job.n_symbols * ((job.keys ? 4 : 0) + (job.coef ? 8 : 0)), s);
         if (!stream) {
             CUDA_CHECK(cudaMemcpyAsync(d_words, job.packed, pbytes, cudaMemcpyDefault, s));
+            KPROF("k_decode", job.total_bits / 8.0 + 8.0 * units +
+                                  (double)job.n_symbols * ((job.keys ? 4 : 0) + (job.coef ? 8 : 0)), s);
             launch(0, units, pwords, 0);
         } else {
             const int G = 16;

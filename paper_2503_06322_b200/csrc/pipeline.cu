@@ -1,0 +1,338 @@
+// pipeline.cu -- the overlapped host<->device reduction pipeline of the paper (HDEM, Fig. 7,
+// PAPER.md:413-533), rebuilt on CUDA streams.
+//
+// The field is split into dim-0 chunks.  Chunk k is copied in on the H2D stream, reduced on
+// the compute stream into a reference-identical MGARD blob (global value range),
+// and copied out on the D2H stream into an HPDR container.  Two device input
+// buffers and two output buffer sets rotate; the reuse edges of Fig. 7 are CUDA events:
+//   H2D(k+1)     waits Compute(k-1)   (input buffer (k+1) % 2 is free)
+//   Compute(k)   waits H2D(k) and D2H(k-2)  (output set k % 2 is free)
+//   D2H(k)       waits Compute(k)
+// so the copy engines move chunk k+1 in and chunk k-1 out while chunk k is reduced.
+// Decompression mirrors it (blob in, field slab out).
+#include <string.h>
+
+#include <algorithm>
+#include <thread>
+
+#include "stages.cuh"
+#include "transform.cuh"
+
+namespace hpdr {
+
+void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, double eb_rel,
+                   uint32_t dict_size, int has_range, double range_min, double range_max, bool allow_stream);
+void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uint8_t *dev_blob, void *out,
+                     uint64_t out_bytes, bool sync);
+void fetch_pending_on(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uint64_t cap, cudaStream_t s, bool sync);
+
+namespace {
+
+uint32_t crc32(const uint8_t *p, size_t n) {   // zlib polynomial, as container.py's zlib.crc32
+    static uint32_t table[256];
+    static bool init = false;
+    if (!init) {
+        for (uint32_t i = 0; i < 256; i++) {
+            uint32_t c = i;
+            for (int k = 0; k < 8; k++) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+            table[i] = c;
+        }
+        init = true;
+    }
+    uint32_t c = 0xFFFFFFFFu;
+    for (size_t i = 0; i < n; i++) c = table[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+    return c ^ 0xFFFFFFFFu;
+}
+
+template <class T>
+void put(std::vector<uint8_t> &v, T x) {
+    size_t o = v.size();
+    v.resize(o + sizeof(T));
+    memcpy(v.data() + o, &x, sizeof(T));
+}
+
+struct Chunk {
+    uint64_t raw_off, raw_size, pay_off, pay_size;
+};
+
+std::vector<uint8_t> container_header(int dtype, int rank, const uint64_t *dims, double eb_rel, uint32_t dict,
+                                      double vmin, double vmax, const std::vector<Chunk> &chunks) {
+    std::vector<uint8_t> h = {'H', 'P', 'D', 'R'};
+    put<uint16_t>(h, 1);
+    put<uint8_t>(h, 2);   // MGARD
+    put<uint8_t>(h, (uint8_t)dtype);
+    put<uint8_t>(h, (uint8_t)rank);
+    for (int d = 0; d < rank; d++) put<uint64_t>(h, dims[d]);
+    put<double>(h, eb_rel);
+    put<uint32_t>(h, dict);
+    put<double>(h, vmin);
+    put<double>(h, vmax);
+    put<uint32_t>(h, (uint32_t)chunks.size());
+    for (const Chunk &c : chunks) {
+        put<uint64_t>(h, c.raw_off);
+        put<uint64_t>(h, c.raw_size);
+        put<uint64_t>(h, c.pay_off);
+        put<uint64_t>(h, c.pay_size);
+    }
+    put<uint32_t>(h, crc32(h.data(), h.size()));
+    return h;
+}
+
+// numpy min/max semantics (NaN propagates) over a host array, on all host cores.
+void host_minmax(const void *in, int dtype, uint64_t n, double *vmin, double *vmax) {
+    const unsigned T = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<double> mn(T, INFINITY), mx(T, -INFINITY);
+    std::vector<int> nan(T, 0);
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < T; t++)
+        th.emplace_back([&, t] {
+            const uint64_t a = n * t / T, b = n * (t + 1) / T;
+            double lo = INFINITY, hi = -INFINITY;
+            int bad = 0;
+            for (uint64_t i = a; i < b; i++) {
+                const double v = dtype == 0 ? (double)((const float *)in)[i] : ((const double *)in)[i];
+                if (v != v) bad = 1;
+                lo = v < lo ? v : lo;
+                hi = v > hi ? v : hi;
+            }
+            mn[t] = lo;
+            mx[t] = hi;
+            nan[t] = bad;
+        });
+    for (auto &x : th) x.join();
+    double lo = INFINITY, hi = -INFINITY;
+    bool bad = false;
+    for (unsigned t = 0; t < T; t++) {
+        lo = std::min(lo, mn[t]);
+        hi = std::max(hi, mx[t]);
+        bad |= nan[t] != 0;
+    }
+    *vmin = bad ? __builtin_nan("") : lo;
+    *vmax = bad ? __builtin_nan("") : hi;
+}
+
+struct Timer {   // per-task CUDA-event timestamps for the pipeline trace
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t t0 = nullptr;
+    bool on;
+    explicit Timer(bool on_, size_t n) : on(on_) {
+        if (!on) return;
+        CUDA_CHECK(cudaEventCreate(&t0));
+        ev.resize(n);
+        for (auto &e : ev) CUDA_CHECK(cudaEventCreate(&e));
+    }
+    ~Timer() {
+        if (t0) cudaEventDestroy(t0);
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+    void mark(size_t i, cudaStream_t s) {
+        if (on) CUDA_CHECK(cudaEventRecord(ev[i], s));
+    }
+    void dump(double *out) {
+        if (!on) return;
+        for (size_t i = 0; i < ev.size(); i++) {
+            float ms = 0.f;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, t0, ev[i]));
+            out[i] = ms;
+        }
+    }
+};
+
+}  // namespace
+}  // namespace hpdr
+
+using namespace hpdr;
+
+extern "C" {
+
+int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int rank, const uint64_t *dims, double eb_rel,
+                           uint32_t dict_size, int has_range, double range_min, double range_max,
+                           uint64_t chunk_planes, const uint64_t *chunk_list, uint64_t n_list, void *out,
+                           uint64_t out_cap, uint64_t *out_len, double *trace) {
+    try {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (dtype != 0 && dtype != 1) throw Error{HPDR_ERR_VALIDATION, "lossy compression needs F32/F64", -1};
+        if (rank < 1 || rank > 4) throw Error{HPDR_ERR_VALIDATION, "rank must be 1..4", -1};
+        const size_t isz = dtype == 0 ? 4 : 8;
+        uint64_t plane = 1;
+        for (int d = 1; d < rank; d++) plane *= dims[d];
+        const uint64_t n0 = dims[0], N = n0 * plane;
+        // chunk sequence: explicit plane counts (e.g. from the adaptive Algorithm-4 schedule) or fixed
+        std::vector<uint64_t> sizes;
+        if (chunk_list && n_list) {
+            uint64_t tot = 0;
+            for (uint64_t i = 0; i < n_list; i++) {
+                if (!chunk_list[i]) throw Error{HPDR_ERR_VALIDATION, "empty chunk in the chunk list", -1};
+                sizes.push_back(chunk_list[i]);
+                tot += chunk_list[i];
+            }
+            if (tot != n0) throw Error{HPDR_ERR_VALIDATION, "chunk list does not tile dim 0", -1};
+        } else {
+            if (!chunk_planes) chunk_planes = std::max<uint64_t>(1, (64ull << 20) / std::max<uint64_t>(1, plane * isz));
+            chunk_planes = std::min(chunk_planes, n0);
+            for (uint64_t a = 0; a < n0; a += chunk_planes) sizes.push_back(std::min(chunk_planes, n0 - a));
+        }
+        const uint64_t K = sizes.size();
+        double vmin = range_min, vmax = range_max;
+        if (!has_range) host_minmax(host_in, dtype, N, &vmin, &vmax);   // the global range
+        std::vector<Chunk> chunks(K);
+        uint64_t maxp = 1;
+        for (uint64_t k = 0, a = 0; k < K; a += sizes[k], k++) {
+            chunks[k] = Chunk{a * plane, sizes[k] * plane, 0, 0};
+            maxp = std::max(maxp, sizes[k]);
+        }
+        chunk_planes = maxp;
+        const size_t hdr_len = container_header(dtype, rank, dims, eb_rel, dict_size, vmin, vmax, chunks).size();
+        if (out_cap < hdr_len) throw Error{HPDR_ERR_BUFFER, "output buffer too small for the container header", -1};
+        const size_t cbytes = chunk_planes * plane * isz;
+        char *din[2] = {(char *)ctx->dbuf("pipe_in0", cbytes), (char *)ctx->dbuf("pipe_in1", cbytes)};
+        cudaStream_t s = ctx->stream, h2d = ctx->h2d, d2h = ctx->d2h;
+        // events: [0, K) H2D done, [K, 2K) compute done, [2K, 3K) D2H done
+        auto ev = [&](uint64_t i) { return ctx->event(1 + i); };
+        Timer tm(trace != nullptr, 6 * K);
+        if (tm.on) CUDA_CHECK(cudaEventRecord(tm.t0, s));
+        CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
+        CUDA_CHECK(cudaStreamWaitEvent(h2d, ctx->event(0), 0));
+        CUDA_CHECK(cudaStreamWaitEvent(d2h, ctx->event(0), 0));
+        auto issue_h2d = [&](uint64_t k) {
+            if (k >= 2) CUDA_CHECK(cudaStreamWaitEvent(h2d, ev(K + k - 2), 0));   // buffer reuse edge
+            tm.mark(6 * k, h2d);
+            CUDA_CHECK(cudaMemcpyAsync(din[k % 2], (const char *)host_in + chunks[k].raw_off * isz,
+                                       chunks[k].raw_size * isz, cudaMemcpyHostToDevice, h2d));
+            tm.mark(6 * k + 1, h2d);
+            CUDA_CHECK(cudaEventRecord(ev(k), h2d));
+        };
+        uint64_t pos = hdr_len;
+        issue_h2d(0);
+        for (uint64_t k = 0; k < K; k++) {
+            if (k + 1 < K) issue_h2d(k + 1);
+            CUDA_CHECK(cudaStreamWaitEvent(s, ev(k), 0));
+            if (k >= 2) CUDA_CHECK(cudaStreamWaitEvent(s, ev(2 * K + k - 2), 0));   // output set reuse edge
+            tm.mark(6 * k + 2, s);
+            uint64_t sd[4] = {chunks[k].raw_size / plane, 0, 0, 0};
+            for (int d = 1; d < rank; d++) sd[d] = dims[d];
+            ctx->out_slot = (int)(k % 2);
+            compress_core(ctx, din[k % 2], dtype, rank, sd, eb_rel, dict_size, 1, vmin, vmax, false);
+            const hpdr_ctx::Pending P = ctx->pending;
+            tm.mark(6 * k + 3, s);
+            CUDA_CHECK(cudaEventRecord(ev(K + k), s));
+            chunks[k].pay_off = pos - hdr_len;
+            chunks[k].pay_size = P.total_len;
+            if (pos + P.total_len > out_cap) throw Error{HPDR_ERR_BUFFER, "output buffer too small for the container", -1};
+            CUDA_CHECK(cudaStreamWaitEvent(d2h, ev(K + k), 0));
+            tm.mark(6 * k + 4, d2h);
+            fetch_pending_on(ctx, P, (char *)out + pos, out_cap - pos, d2h, false);
+            tm.mark(6 * k + 5, d2h);
+            CUDA_CHECK(cudaEventRecord(ev(2 * K + k), d2h));
+            pos += P.total_len;
+        }
+        CUDA_CHECK(cudaStreamSynchronize(d2h));
+        ctx->out_slot = 0;
+        const std::vector<uint8_t> hdr = container_header(dtype, rank, dims, eb_rel, dict_size, vmin, vmax, chunks);
+        if (classify(out) == MemKind::Device) CUDA_CHECK(cudaMemcpy(out, hdr.data(), hdr.size(), cudaMemcpyHostToDevice));
+        else memcpy(out, hdr.data(), hdr.size());
+        *out_len = pos;
+        tm.dump(trace);
+        return HPDR_OK;
+    } catch (const Error &e) {
+        ctx->out_slot = 0;
+        cudaDeviceSynchronize();
+        set_error(e.code, e.msg, e.bit_offset);
+        return e.code;
+    }
+}
+
+int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len, void *out, uint64_t out_bytes,
+                             double *trace) {
+    try {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        const uint8_t *c = (const uint8_t *)container;
+        auto need = [&](uint64_t p, uint64_t n) {
+            if (p > len || n > len - p) throw Error{HPDR_ERR_FORMAT, "container truncated", -1};
+        };
+        need(0, 9);
+        if (memcmp(c, "HPDR", 4) != 0) throw Error{HPDR_ERR_FORMAT, "bad magic", -1};
+        uint16_t ver;
+        memcpy(&ver, c + 4, 2);
+        if (ver != 1) throw Error{HPDR_ERR_FORMAT, "unsupported container version", -1};
+        if (c[6] != 2) throw Error{HPDR_ERR_FORMAT, "unknown pipeline id", -1};
+        const int dtype = c[7], rank = c[8];
+        uint64_t pos = 9;
+        need(pos, 8ull * rank + 28 + 4);
+        std::vector<uint64_t> dims(rank);
+        memcpy(dims.data(), c + pos, 8ull * rank);
+        pos += 8ull * rank + 28;
+        uint32_t K;
+        memcpy(&K, c + pos, 4);
+        pos += 4;
+        need(pos, 32ull * K + 4);
+        std::vector<Chunk> chunks(K);
+        memcpy(chunks.data(), c + pos, 32ull * K);
+        pos += 32ull * K;
+        uint32_t crc;
+        memcpy(&crc, c + pos, 4);
+        if (crc32(c, pos) != crc) throw Error{HPDR_ERR_FORMAT, "header checksum mismatch", -1};
+        pos += 4;
+        const uint64_t base = pos;
+        static const int isz_tab[7] = {4, 8, 4, 8, 4, 8, 1};
+        if (dtype > 6) throw Error{HPDR_ERR_FORMAT, "unknown dtype", -1};
+        const size_t isz = isz_tab[dtype];
+        uint64_t N = 1;
+        for (uint64_t d : dims) N *= d;
+        if (out_bytes < N * isz) throw Error{HPDR_ERR_BUFFER, "output buffer too small", -1};
+        uint64_t maxpay = 1, maxraw = 1;
+        for (const Chunk &ch : chunks) {
+            need(base + ch.pay_off, ch.pay_size);
+            if (ch.raw_off + ch.raw_size > N) throw Error{HPDR_ERR_FORMAT, "chunk outside the field", -1};
+            maxpay = std::max(maxpay, ch.pay_size);
+            maxraw = std::max(maxraw, ch.raw_size);
+        }
+        uint8_t *dblob[2] = {(uint8_t *)ctx->dbuf("pipe_blob0", maxpay), (uint8_t *)ctx->dbuf("pipe_blob1", maxpay)};
+        char *dout[2] = {(char *)ctx->dbuf("pipe_out0", maxraw * isz), (char *)ctx->dbuf("pipe_out1", maxraw * isz)};
+        cudaStream_t s = ctx->stream, h2d = ctx->h2d, d2h = ctx->d2h;
+        auto ev = [&](uint64_t i) { return ctx->event(1 + i); };
+        Timer tm(trace != nullptr, 6 * (size_t)K);
+        if (tm.on) CUDA_CHECK(cudaEventRecord(tm.t0, s));
+        CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
+        CUDA_CHECK(cudaStreamWaitEvent(h2d, ctx->event(0), 0));
+        CUDA_CHECK(cudaStreamWaitEvent(d2h, ctx->event(0), 0));
+        const bool host_out = classify(out) != MemKind::Device;
+        auto issue_h2d = [&](uint64_t k) {
+            if (k >= 2) CUDA_CHECK(cudaStreamWaitEvent(h2d, ev(K + k - 2), 0));
+            tm.mark(6 * k, h2d);
+            CUDA_CHECK(cudaMemcpyAsync(dblob[k % 2], c + base + chunks[k].pay_off, chunks[k].pay_size,
+                                       cudaMemcpyHostToDevice, h2d));
+            tm.mark(6 * k + 1, h2d);
+            CUDA_CHECK(cudaEventRecord(ev(k), h2d));
+        };
+        if (K) issue_h2d(0);
+        for (uint64_t k = 0; k < K; k++) {
+            if (k + 1 < K) issue_h2d(k + 1);
+            CUDA_CHECK(cudaStreamWaitEvent(s, ev(k), 0));
+            if (k >= 2) CUDA_CHECK(cudaStreamWaitEvent(s, ev(2 * K + k - 2), 0));
+            tm.mark(6 * k + 2, s);
+            char *dst = host_out ? dout[k % 2] : (char *)out + chunks[k].raw_off * isz;
+            decompress_core(ctx, c + base + chunks[k].pay_off, chunks[k].pay_size, dblob[k % 2], dst,
+                            chunks[k].raw_size * isz, false);
+            tm.mark(6 * k + 3, s);
+            CUDA_CHECK(cudaEventRecord(ev(K + k), s));
+            CUDA_CHECK(cudaStreamWaitEvent(d2h, ev(K + k), 0));
+            tm.mark(6 * k + 4, d2h);
+            if (host_out)
+                CUDA_CHECK(cudaMemcpyAsync((char *)out + chunks[k].raw_off * isz, dout[k % 2], chunks[k].raw_size * isz,
+                                           cudaMemcpyDeviceToHost, d2h));
+            tm.mark(6 * k + 5, d2h);
+            CUDA_CHECK(cudaEventRecord(ev(2 * K + k), d2h));
+        }
+        CUDA_CHECK(cudaStreamSynchronize(d2h));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        tm.dump(trace);
+        return HPDR_OK;
+    } catch (const Error &e) {
+        cudaDeviceSynchronize();
+        set_error(e.code, e.msg, e.bit_offset);
+        return e.code;
+    }
+}
+
+}  // extern "C"

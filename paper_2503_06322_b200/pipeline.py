@@ -1,0 +1,205 @@
+"""Overlapped host<->device reduction pipeline (paper §V: HDEM, Fig. 7, Algorithm 4).
+
+The reference package names this subsystem (hpdr/pipeline/__init__.py:4-19) but ships only
+its chunk-size models (hpdr/pipeline/models.py); the runner is rebuilt here on CUDA streams in
+libhpdr_b200.so (csrc/pipeline.cu).  Each dim-0 chunk becomes a reference-identical MGARD blob
+compressed with the global value range, stored in an HPDR container (container.py).
+
+Host-side scheduling (this module):
+  ThroughputModel / TransportModel / next_chunk_size / fit_throughput_model  -- Φ, Θ and the
+      Algorithm-4 rule (models.py:22-120), restated
+  adaptive_schedule  -- the chunk sequence Algorithm 4 produces for a field
+  overlap_ratio      -- SPEC.md's overlap metric over a pipeline trace
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, dims_arg, lib
+from .errors import ValidationError
+
+FIT_CUTOFF = 0.1        # models.py:17
+SATURATION_TOL = 0.05   # models.py:19
+
+
+# ----------------------------------------------------------------------------- models
+@dataclass
+class ThroughputModel:
+    """Φ(C): linear ramp below c_threshold, plateau gamma above (bytes/s)."""
+
+    alpha: float
+    beta_slope: float
+    gamma: float
+    c_threshold: float
+    f: float = FIT_CUTOFF
+
+    def phi(self, chunk_bytes: float) -> float:
+        c = float(chunk_bytes)
+        v = self.gamma if c >= self.c_threshold else self.alpha * c + self.beta_slope
+        if v <= 0:
+            raise ValidationError(f"throughput model non-positive at {chunk_bytes}")
+        return v
+
+    @classmethod
+    def saturated(cls, gamma: float) -> "ThroughputModel":
+        return cls(0.0, float(gamma), float(gamma), 0.0)
+
+
+@dataclass
+class TransportModel:
+    """Θ(t) = t / beta_copy, beta_copy in seconds per byte (EMA-updated from observed copies)."""
+
+    beta_copy: float
+    ema_weight: float = 0.25
+
+    def __post_init__(self):
+        if self.beta_copy <= 0:
+            raise ValidationError("beta_copy must be > 0")
+
+    def theta(self, seconds: float) -> float:
+        return float(seconds) / self.beta_copy
+
+    def observe(self, nbytes: int, seconds: float):
+        if nbytes > 0 and seconds > 0:
+            self.beta_copy += self.ema_weight * (seconds / nbytes - self.beta_copy)
+
+
+def next_chunk_size(c_curr: int, model: ThroughputModel, transport: TransportModel, c_limit: int,
+                    size_rest: int, slab_bytes: int = 1) -> int:
+    """Algorithm 4 line 17: min(Θ(C/Φ(C)), C_limit, rest), floored to whole slabs, never 0."""
+    if size_rest <= 0:
+        return 0
+    if c_curr <= 0:
+        raise ValidationError("c_curr must be > 0")
+    want = min(transport.theta(c_curr / model.phi(c_curr)), float(c_limit), float(size_rest))
+    slabs = max(1, int(want // slab_bytes))
+    return int(min(slabs * slab_bytes, size_rest))
+
+
+def fit_throughput_model(samples, f: float = FIT_CUTOFF) -> ThroughputModel:
+    """Plateau from the largest profiled chunk; least-squares ramp over the points below the
+    plateau down to the first one under f * plateau (§V-C)."""
+    pts = sorted((float(c), float(p)) for c, p in samples)
+    if len(pts) < 3:
+        raise ValidationError("need at least 3 profile samples")
+    if len({c for c, _ in pts}) == 1:
+        raise ValidationError("degenerate profile: all sizes equal")
+    gamma = pts[-1][1]
+    if gamma <= 0:
+        raise ValidationError("non-positive saturated throughput")
+    ramp = []
+    for c, p in reversed(pts[:-1]):
+        if p >= gamma * (1.0 - SATURATION_TOL):
+            continue
+        if p < f * gamma:
+            break
+        ramp.append((c, p))
+    smallest = pts[0][0]
+    if len(ramp) >= 2:
+        a, b = np.polyfit([c for c, _ in ramp], [p for _, p in ramp], 1)
+        a, b = float(a), float(b)
+        if a > 0:
+            return ThroughputModel(a, b, gamma, (gamma - b) / a, f)
+    return ThroughputModel(0.0, gamma, gamma, smallest, f)
+
+
+def adaptive_schedule(n0: int, plane_bytes: int, model: ThroughputModel, transport: TransportModel,
+                      c_init: int = 16 << 20, c_limit: int | None = None) -> list:
+    """Chunk plane counts Algorithm 4 produces for a field of n0 planes."""
+    total = n0 * plane_bytes
+    c_limit = c_limit or total
+    planes = []
+    rest = total
+    c = min(max(plane_bytes, (c_init // plane_bytes) * plane_bytes), rest)
+    while rest > 0:
+        c = min(c, rest)
+        planes.append(max(1, c // plane_bytes))
+        rest -= planes[-1] * plane_bytes
+        if rest > 0:
+            c = next_chunk_size(planes[-1] * plane_bytes, model, transport, c_limit, rest, plane_bytes)
+    return planes
+
+
+def overlap_ratio(trace: np.ndarray) -> float:
+    """SPEC.md overlap: time during which a copy (H2D or D2H) overlaps any compute / total copy time.
+    trace: (K, 6) = H2D start/end, compute start/end, D2H start/end (ms)."""
+    t = np.asarray(trace, dtype=np.float64).reshape(-1, 6)
+    if t.size == 0:
+        return 0.0
+    comp = sorted((a, b) for a, b in t[:, 2:4])
+    copies = [(a, b) for a, b in t[:, 0:2]] + [(a, b) for a, b in t[:, 4:6]]
+    total = sum(max(0.0, b - a) for a, b in copies)
+    if total <= 0:
+        return 0.0
+    ov = 0.0
+    for a, b in copies:
+        for ca, cb in comp:
+            ov += max(0.0, min(b, cb) - max(a, ca))
+    return min(1.0, ov / total)
+
+
+# ----------------------------------------------------------------------------- runner
+def compress_pipelined(arr, eb_rel: float, dict_size: int = 4096, value_range=None, *, chunk_planes: int = 0,
+                       chunks=None, device: int | None = None, out=None, trace: bool = False):
+    """Chunked compress through the streams pipeline -> HPDR container bytes.
+
+    ``chunks`` (plane counts summing to dim 0) overrides the fixed ``chunk_planes``.
+    With ``trace`` returns (bytes, trace array of shape (K, 6) in ms).
+    """
+    from .mgard import _as_input, _dims_ok
+
+    addr, dims, code, keep = _as_input(arr)
+    dims = _dims_ok(dims)
+    ctx = _lib.default_context(device)
+    has = value_range is not None
+    r0, r1 = (float(value_range[0]), float(value_range[1])) if has else (0.0, 0.0)
+    lst = None if chunks is None else np.ascontiguousarray(chunks, dtype=np.uint64)
+    k = len(lst) if lst is not None else -(-dims[0] // chunk_planes) if chunk_planes else 0
+    nbytes = int(np.prod(dims)) * (4 if code == 0 else 8)
+    cap = nbytes + (1 << 20) if out is None else int(out.nbytes)
+    buf = np.empty(cap, np.uint8) if out is None else out
+    tr = np.zeros(6 * max(k, 1) + 6 * 4096, np.float64) if trace else None
+    n = C.c_uint64()
+
+    def run(b):
+        return lib().hpdr_pipeline_compress(
+            ctx.handle, C.c_void_p(addr), code, len(dims), dims_arg(dims), float(eb_rel), int(dict_size), int(has),
+            r0, r1, int(chunk_planes), C.c_void_p(lst.ctypes.data) if lst is not None else None,
+            0 if lst is None else len(lst), C.c_void_p(_lib.ptr(b)), int(b.nbytes), C.byref(n),
+            C.c_void_p(tr.ctypes.data) if tr is not None else None)
+
+    rc = run(buf)
+    if rc == _lib.BUFFER and out is None:   # incompressible data: worst-case bound
+        buf = np.empty(nbytes * 6 + (8 << 20), np.uint8)
+        rc = run(buf)
+    check(rc)
+    del keep
+    data = buf[: n.value].tobytes() if out is None else int(n.value)
+    if not trace:
+        return data
+    from .container import read_container
+
+    h, _ = read_container(buf[: n.value] if out is None else out[: n.value])
+    return data, tr[: 6 * len(h.chunks)].reshape(-1, 6)
+
+
+def decompress_pipelined(data, *, device: int | None = None, out=None, trace: bool = False):
+    """Decompress an HPDR container through the streams pipeline."""
+    from .container import read_container
+    from .tensor import DTYPE_FROM_CODE
+
+    buf = np.frombuffer(memoryview(data), np.uint8)
+    h, _ = read_container(buf)
+    res = np.empty(h.dims, DTYPE_FROM_CODE[h.dtype].np_dtype) if out is None else out
+    tr = np.zeros(6 * max(1, len(h.chunks)), np.float64) if trace else None
+    ctx = _lib.default_context(device)
+    check(lib().hpdr_pipeline_decompress(ctx.handle, C.c_void_p(buf.ctypes.data), buf.size,
+                                         C.c_void_p(_lib.ptr(res)), int(res.nbytes),
+                                         C.c_void_p(tr.ctypes.data) if tr is not None else None))
+    if trace:
+        return res, tr[: 6 * len(h.chunks)].reshape(-1, 6)
+    return res
