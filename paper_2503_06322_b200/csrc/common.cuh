@@ -21,6 +21,7 @@ constexpr int kNumSMs = 148;
 
 void set_error(int code, const std::string &msg, int64_t bit_offset = -1);
 void count_launch();
+void debug_sync(const char *where);   // HPDR_DEBUG_SYNC=1: device sync + check after every launch
 
 // Live per-kernel timing for bench.py: when enabled (hpdr_prof_enable), each scope records a
 // CUDA event pair on the launching stream plus the launch's algorithmic bytes.
@@ -41,10 +42,13 @@ struct ProfScope {
                                 std::string(#x) + ": " + cudaGetErrorString(e_), -1};      \
         }                                                                                  \
     } while (0)
+#define HPDR_STR2(x) #x
+#define HPDR_STR(x) HPDR_STR2(x)
 #define LAUNCH_CHECK()                                                                     \
     do {                                                                                   \
         ::hpdr::count_launch();                                                            \
         CUDA_CHECK(cudaGetLastError());                                                    \
+        ::hpdr::debug_sync(__FILE__ ":" HPDR_STR(__LINE__));                               \
     } while (0)
 
 // 4-D shape, slowest first; lower ranks are padded with leading 1s.

@@ -20,6 +20,13 @@ void set_error(int code, const std::string &msg, int64_t bit_offset) {
 
 void count_launch() { tl_launches++; }
 
+void debug_sync(const char *where) {
+    static const bool on = getenv("HPDR_DEBUG_SYNC") != nullptr;
+    if (!on) return;
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) throw Error{HPDR_ERR_CUDA, std::string("kernel at ") + where + ": " + cudaGetErrorString(e), -1};
+}
+
 // ---- live kernel profiling ----
 namespace {
 struct ProfRec {
@@ -86,6 +93,8 @@ void *hpdr_ctx::dbuf(const std::string &name, size_t bytes) {
     if (bytes == 0) bytes = 16;
     Buffer &b = dev[name];
     if (b.bytes < bytes) {
+        // work queued on any of the context's streams may still use the old buffer
+        if (b.ptr) CUDA_CHECK(cudaDeviceSynchronize());
         if (b.ptr) CUDA_CHECK(cudaFree(b.ptr));
         b.ptr = nullptr;
         b.bytes = 0;
@@ -110,6 +119,7 @@ void *hpdr_ctx::hbuf(const std::string &name, size_t bytes) {
     if (bytes == 0) bytes = 16;
     Buffer &b = pinned[name];
     if (b.bytes < bytes) {
+        if (b.ptr) CUDA_CHECK(cudaDeviceSynchronize());
         if (b.ptr) CUDA_CHECK(cudaFreeHost(b.ptr));
         b.ptr = nullptr;
         b.bytes = 0;
@@ -191,7 +201,12 @@ DevPlan &hpdr_ctx::plan(int rank, const uint64_t *dims) {
         throw Error{HPDR_ERR_ALLOCATION, "allocating operator tables", -1};
     }
     alloc_events++;
-    CUDA_CHECK(cudaMemcpy(dp->dbuf, pk.bytes.data(), dp->bytes, cudaMemcpyHostToDevice));
+    // Stream-ordered upload: a plain cudaMemcpy from pageable memory may return before its DMA
+    // lands (it is queued on the legacy stream, which the context's non-blocking streams do not
+    // wait for), so kernels could read stale tables while a copy engine is busy with a pipeline
+    // chunk.  Ordering on the compute stream plus a sync makes the tables visible to every stream.
+    CUDA_CHECK(cudaMemcpyAsync(dp->dbuf, pk.bytes.data(), dp->bytes, cudaMemcpyHostToDevice, stream));
+    CUDA_CHECK(cudaStreamSynchronize(stream));
     char *base = (char *)dp->dbuf;
     dp->steps.resize(h.steps.size());
     for (size_t s = 0; s < h.steps.size(); s++) {

@@ -212,7 +212,18 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
             uint64_t sd[4] = {chunks[k].raw_size / plane, 0, 0, 0};
             for (int d = 1; d < rank; d++) sd[d] = dims[d];
             ctx->out_slot = (int)(k % 2);
+            static const bool dbg = getenv("HPDR_DEBUG_SYNC") != nullptr;
+            if (dbg) {
+                CUDA_CHECK(cudaDeviceSynchronize());
+                std::vector<char> chk(chunks[k].raw_size * isz);
+                CUDA_CHECK(cudaMemcpy(chk.data(), din[k % 2], chk.size(), cudaMemcpyDeviceToHost));
+                fprintf(stderr, "[pipe] chunk %llu planes %llu din %p match %d\n", (unsigned long long)k,
+                        (unsigned long long)sd[0], (void *)din[k % 2],
+                        memcmp(chk.data(), (const char *)host_in + chunks[k].raw_off * isz, chk.size()) == 0);
+            }
             compress_core(ctx, din[k % 2], dtype, rank, sd, eb_rel, dict_size, 1, vmin, vmax, false);
+            if (dbg) fprintf(stderr, "[pipe] chunk %llu done, %llu bytes\n", (unsigned long long)k,
+                             (unsigned long long)ctx->pending.total_len);
             const hpdr_ctx::Pending P = ctx->pending;
             tm.mark(6 * k + 3, s);
             CUDA_CHECK(cudaEventRecord(ev(K + k), s));
