@@ -1,6 +1,7 @@
 // huffman.cu -- canonical Huffman: host codebook (huffman.py:107-204) and device
 // encode (huffman.py:228-289) / decode (huffman.py:207-358) kernels.
 #include <algorithm>
+#include <type_traits>
 #include <cub/cub.cuh>
 #include <numeric>
 
@@ -443,6 +444,308 @@ __global__ void k_decode(const uint32_t *__restrict__ words, uint64_t limit, con
     (void)key_limit;
 }
 
+// ---------------------------------------------------------------- warp-cooperative decode
+// One warp per 4096-symbol unit.  The unit's bit range [off_u, off_u+1) is split into 32 lane
+// segments; every lane decodes its segment from a guessed start and the guesses are repaired by
+// self-synchronisation: each round a lane restarts from where its left neighbour's decode left
+// the neighbour's segment, until no start moves (lane 0 starts on the true boundary, so after
+// round r lanes 0..r are exact; canonical codes resynchronise within a few codewords, so one or
+// two rounds suffice in practice).  Symbol counts are then scanned across the warp and every lane
+// re-decodes its exact range, staging 32 symbols per lane in shared memory so the warp writes
+// the dequantized coefficients (quantize.py:110-111) with coalesced stores.
+// A unit whose walk ends anywhere but exactly on the next unit's offset with exactly its symbol
+// count (or that hits an invalid codeword, or max_len > 32) is a non-canonical / corrupted
+// stream: lane 0 redoes it with the reference's bit-serial walk (huffman.py:292-313), which also
+// produces the reference's error offsets.
+constexpr int kDWWarps = 8;
+constexpr int kDWStage = 33;    // padded 32-symbol staging row per lane
+constexpr int kDWWords = 1024;  // per-warp shared payload window (32768 bits: 4096 x 8-bit codes)
+
+// canonical lookup of the codeword at the top of `win` (len 0: no codeword)
+__device__ __forceinline__ uint32_t dw_lookup(uint32_t win, const uint32_t *lut, const DecTables &T,
+                                              const uint32_t *__restrict__ sym_by_rank, int max_len, int &L) {
+    const uint32_t e = lut[win >> (32 - kLutBits)];
+    L = (int)(e & 0xffu);
+    if (L) return e >> 8;
+    for (int l = kLutBits + 1; l <= max_len; l++) {
+        const long long idx = (long long)(win >> (32 - l)) - T.first_code[l];
+        if (idx >= 0 && idx < T.cnt[l]) {
+            L = l;
+            return __ldg(sym_by_rank + T.first_rank[l] + idx);
+        }
+    }
+    L = 0;
+    return 0;
+}
+
+// Bit positions: SM = the unit's words staged (byte-swapped) in shared memory, positions 32-bit
+// and relative to the first staged word; otherwise absolute 64-bit positions over global words.
+template <bool SM>
+struct DW {
+    using Pos = typename std::conditional<SM, uint32_t, uint64_t>::type;
+    const uint32_t *w;
+    const uint32_t *lut;
+    const DecTables *T;
+    const uint32_t *sbr;
+    int max_len;
+    __device__ __forceinline__ uint32_t word(Pos i) const { return SM ? w[i] : load_be(w, (uint64_t)i); }
+    // the 32 bits starting at bit p (two independent word loads + funnel shift: no bit buffer)
+    __device__ __forceinline__ uint32_t win(Pos p) const {
+        const Pos i = p >> 5;
+        return __funnelshift_l(word(i + 1), word(i), (uint32_t)p & 31u);
+    }
+    __device__ __forceinline__ uint32_t sym(Pos p, int &L) const { return dw_lookup(win(p), lut, *T, sbr, max_len, L); }
+    // decode from p while p < end; n = symbols; bad = an invalid codeword stopped the walk
+    __device__ __forceinline__ Pos scan(Pos p, Pos end, uint32_t &n, bool &bad) const {
+        n = 0;
+        bad = false;
+        while (p < end) {
+            int L;
+            sym(p, L);
+            if (L == 0) {
+                bad = true;
+                return p;
+            }
+            p += L;
+            n++;
+        }
+        return p;
+    }
+    // Re-decode from a new start ns, replaying the previous walk (os -> oe, on symbols) in lockstep:
+    // once both walks stand on the same codeword boundary the rest of the old walk is valid.
+    __device__ __forceinline__ Pos rescan(Pos ns, Pos os, Pos oe, bool obad, uint32_t on, Pos end, uint32_t &n,
+                                          bool &bad) const {
+        if (obad || ns >= end) return scan(ns, end, n, bad);
+        n = 0;
+        bad = false;
+        Pos pa = ns, pb = os;
+        uint32_t na = 0, nb = 0;
+        while (pa < end) {
+            if (pa == pb) {
+                n = na + (on - nb);
+                return oe;
+            }
+            int L;
+            if (pb < pa) {   // valid: the old walk passed here
+                sym(pb, L);
+                pb += L;
+                nb++;
+            } else {
+                sym(pa, L);
+                if (L == 0) {
+                    bad = true;
+                    return pa;
+                }
+                pa += L;
+                na++;
+            }
+        }
+        n = na;
+        return pa;
+    }
+};
+
+// Self-synchronising decode of one unit whose bits lie in [S, E) (see k_decode_warp), positions
+// relative to `base`.  Returns false if the unit is not a canonical layout (the caller falls back
+// to the serial walk).  A codeword overrunning E (or the stream limit >= E) shows up as last != E.
+template <bool SM>
+__device__ __forceinline__ bool dw_unit(const DW<SM> &c, uint64_t base, uint64_t S_, uint64_t E_, uint64_t lo,
+                                        uint64_t cnt, uint16_t *st, uint32_t *__restrict__ keys,
+                                        double *__restrict__ coef, double bin, unsigned &kmax,
+                                        unsigned long long *stats) {
+    using Pos = typename DW<SM>::Pos;
+    const int lane = threadIdx.x & 31;
+    const Pos S = (Pos)(S_ - base), E = (Pos)(E_ - base);
+    const Pos seg = (E - S + 31) / 32;
+    const Pos send = min(E, (Pos)(S + (Pos)(lane + 1) * seg));
+    Pos start = min(E, (Pos)(S + (Pos)lane * seg));
+    uint32_t n;
+    bool bad;
+    Pos exit = c.scan(start, send, n, bad);
+    for (int round = 0; round < 32; round++) {
+        Pos ns = __shfl_up_sync(0xffffffffu, exit, 1);
+        const bool lbad = __shfl_up_sync(0xffffffffu, (int)bad, 1);
+        if (lane == 0) ns = S;
+        const bool moved = ns != start && (lane == 0 || !lbad);
+        if (!__any_sync(0xffffffffu, moved)) break;
+        if (stats && lane == 0) atomicAdd(stats + 1, 1ULL);
+        if (moved) {
+            uint32_t n2;
+            bool b2;
+            const Pos ex2 = c.rescan(ns, start, exit, bad, n, send, n2, b2);
+            start = ns;
+            n = n2;
+            exit = ex2;
+            bad = b2;
+        }
+    }
+    // exact iff every start is its neighbour's exit, no lane failed, the walk ends on E and the
+    // unit holds exactly cnt symbols
+    Pos left = __shfl_up_sync(0xffffffffu, exit, 1);
+    if (lane == 0) left = S;
+    uint32_t tot = n;
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    const Pos last = __shfl_sync(0xffffffffu, exit, 31);
+    if (!(__all_sync(0xffffffffu, left == start && !bad) && last == E && tot == cnt)) return false;
+    uint32_t pos = n;   // inclusive scan -> this lane's first output
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, pos, o);
+        if (lane >= o) pos += v;
+    }
+    pos -= n;
+    Pos p = start;
+    uint32_t done = 0;
+    const uint32_t nmax = __reduce_max_sync(0xffffffffu, n);
+    for (uint32_t r0 = 0; r0 < nmax; r0 += 32) {
+        const uint32_t m = n > r0 ? min(32u, n - r0) : 0u;
+        for (uint32_t k = 0; k < m; k++) {
+            int L;
+            const uint32_t sym = c.sym(p, L);
+            p += L;
+            st[lane * kDWStage + k] = (uint16_t)sym;   // keys < dict_size <= 65535
+            kmax = sym > kmax ? sym : kmax;
+        }
+        __syncwarp();
+        for (int j = 0; j < 32; j++) {
+            const uint32_t mj = __shfl_sync(0xffffffffu, m, j);
+            const uint32_t bj = __shfl_sync(0xffffffffu, pos + done, j);
+            if ((uint32_t)lane < mj) {
+                const uint32_t sym = st[j * kDWStage + lane];
+                const uint64_t o = lo + bj + lane;
+                if (keys) keys[o] = sym;
+                if (coef) {
+                    const long long b = (long long)(sym >> 1) ^ -(long long)(sym & 1u);
+                    coef[o] = __dmul_rn((double)b, bin);
+                }
+            }
+        }
+        __syncwarp();
+        done += m;
+    }
+    return true;
+}
+
+// The reference walk for one unit (lane 0 of the warp): exact outputs and error offsets.
+__device__ void dw_serial_unit(const uint32_t *__restrict__ words, uint64_t limit, uint64_t pos, uint64_t lo,
+                               uint64_t cnt, const DecTables &T, const uint32_t *lut,
+                               const uint32_t *__restrict__ sym_by_rank, uint32_t *__restrict__ keys,
+                               double *__restrict__ coef, double bin, long long &err, unsigned &kmax) {
+    const int max_len = T.max_len;
+    for (uint64_t i = 0; i < cnt; i++) {
+        const uint64_t cw = pos;
+        uint32_t sym = 0;
+        if (max_len <= 32) {
+            if (pos >= limit) { err = (long long)cw; return; }
+            const uint64_t wi = pos >> 5;
+            const uint64_t win64 = ((uint64_t)load_be(words, wi) << 32) | load_be(words, wi + 1);
+            int L;
+            sym = dw_lookup((uint32_t)((win64 << (pos & 31)) >> 32), lut, T, sym_by_rank, max_len, L);
+            if (L == 0 || pos + (uint64_t)L > limit) { err = (long long)cw; return; }
+            pos += L;
+        } else {   // wrapping int64 arithmetic of the numba walk (corrupted length arrays only)
+            unsigned long long code = 0;
+            int len = 0;
+            bool ok = false;
+            for (;;) {
+                if (pos >= limit || len >= max_len) break;
+                const uint32_t word = load_be(words, pos >> 5);
+                code = (code << 1) | ((word >> (31 - (pos & 31))) & 1u);
+                pos++;
+                len++;
+                const long long idx = (long long)(code - (unsigned long long)T.first_code[len]);
+                if (idx >= 0 && idx < T.cnt[len]) {
+                    sym = __ldg(sym_by_rank + T.first_rank[len] + idx);
+                    ok = true;
+                    break;
+                }
+            }
+            if (!ok) { err = (long long)cw; return; }
+        }
+        kmax = sym > kmax ? sym : kmax;
+        if (keys) keys[lo + i] = sym;
+        if (coef) {
+            const long long b = (long long)(sym >> 1) ^ -(long long)(sym & 1u);
+            coef[lo + i] = __dmul_rn((double)b, bin);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- warp-cooperative decode
+// One warp per 4096-symbol unit.  The warp stages the unit's payload words in shared memory
+// (coalesced), splits its bit range [off_u, off_u+1) into 32 lane segments and decodes every
+// segment from a guessed start; guesses are repaired by self-synchronisation (each round a lane
+// restarts where its left neighbour's walk left the neighbour's segment, replaying its old walk in
+// lockstep until the two meet on a common codeword boundary; lane 0 starts on the true boundary,
+// so round r fixes lanes <= r, and canonical codes resynchronise within a few codewords).  Symbol
+// counts are scanned across the warp and every lane re-decodes its exact range, staging 32
+// symbols per lane in shared memory so the warp writes the dequantized coefficients
+// (quantize.py:110-111) with coalesced stores.
+// A unit whose walk ends anywhere but exactly on the next unit's offset with exactly its symbol
+// count (or that hits an invalid codeword, or max_len > 32) is a non-canonical / corrupted
+// stream: lane 0 redoes it with the reference's bit-serial walk (huffman.py:292-313), which also
+// produces the reference's error offsets.
+size_t dw_smem_bytes() {
+    return (size_t)kLutSize * 4 + ((sizeof(DecTables) + 15) & ~size_t(15)) +
+           (((size_t)kDWWarps * 32 * kDWStage * 2 + 15) & ~size_t(15)) + (size_t)kDWWarps * kDWWords * 4;
+}
+
+__global__ void __launch_bounds__(kDWWarps * 32) k_decode_warp(
+    const uint32_t *__restrict__ words, uint64_t limit, const uint64_t *__restrict__ offs, uint64_t nsym,
+    int64_t units, const DecTables *__restrict__ tabs_g, const uint32_t *__restrict__ lut_g,
+    const uint32_t *__restrict__ sym_by_rank, uint32_t *__restrict__ keys, double *__restrict__ coef, double bin,
+    long long *__restrict__ unit_err, unsigned long long *__restrict__ first_bad, unsigned *__restrict__ max_key,
+    unsigned long long *__restrict__ stats) {
+    extern __shared__ __align__(16) unsigned char dw_smem[];
+    uint32_t *lut = (uint32_t *)dw_smem;
+    DecTables &T = *(DecTables *)(dw_smem + kLutSize * 4);
+    uint16_t *stage = (uint16_t *)(dw_smem + kLutSize * 4 + ((sizeof(DecTables) + 15) & ~size_t(15)));
+    uint32_t *pay = (uint32_t *)((unsigned char *)stage + (((size_t)kDWWarps * 32 * kDWStage * 2 + 15) & ~size_t(15)));
+    for (int i = threadIdx.x; i < kLutSize; i += blockDim.x) lut[i] = lut_g[i];
+    for (int i = threadIdx.x; i < (int)(sizeof(DecTables) / 8); i += blockDim.x)
+        ((long long *)&T)[i] = ((const long long *)tabs_g)[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint16_t *st = stage + wid * 32 * kDWStage;
+    uint32_t *pw = pay + wid * kDWWords;
+    const int max_len = T.max_len;
+    unsigned kmax = 0;
+    const int64_t wstride = (int64_t)gridDim.x * kDWWarps;
+    for (int64_t u = blockIdx.x * (int64_t)kDWWarps + wid; u < units; u += wstride) {
+        const uint64_t lo = (uint64_t)u * kBlockSymbols;
+        const uint64_t cnt = nsym - lo < (uint64_t)kBlockSymbols ? nsym - lo : (uint64_t)kBlockSymbols;
+        const uint64_t S = __ldg(offs + u);
+        const uint64_t E = u + 1 < units ? __ldg(offs + u + 1) : limit;
+        bool fast = max_len <= 32 && S < limit && S <= E && E <= limit && E - S <= cnt * (uint64_t)max_len;
+        if (fast) {
+            const int64_t w0 = (int64_t)(S >> 5), nw = (int64_t)(E >> 5) + 4 - w0;
+            if (nw <= kDWWords) {
+                for (int64_t i = lane; i < nw; i += 32) pw[i] = load_be(words, (uint64_t)(w0 + i));
+                __syncwarp();
+                const DW<true> c{pw, lut, &T, sym_by_rank, max_len};
+                fast = dw_unit<true>(c, (uint64_t)w0 * 32, S, E, lo, cnt, st, keys, coef, bin, kmax, stats);
+            } else {
+                const DW<false> c{words, lut, &T, sym_by_rank, max_len};
+                fast = dw_unit<false>(c, 0, S, E, lo, cnt, st, keys, coef, bin, kmax, stats);
+                if (stats && lane == 0) atomicAdd(stats + 2, 1ULL);
+            }
+        }
+        if (!fast) {
+            long long err = -1;
+            if (stats && lane == 0) atomicAdd(stats, 1ULL);
+            if (lane == 0) {
+                dw_serial_unit(words, limit, S, lo, cnt, T, lut, sym_by_rank, keys, coef, bin, err, kmax);
+                if (err >= 0) {
+                    unit_err[u] = err;
+                    atomicMin(first_bad, (unsigned long long)u);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    for (int o = 16; o; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    if (lane == 0 && kmax) atomicMax(max_key, kmax);
+}
+
 __global__ void k_fill(uint32_t *keys, double *coef, int64_t n, uint32_t sym, double val) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         if (keys) keys[i] = sym;
@@ -535,7 +838,38 @@ void decode_device(hpdr_ctx *ctx, const DecodeJob &job, DecodeResult &res, cudaS
         LAUNCH_CHECK();
     };
     if (units > 0) {
-        if (!stream) {
+        static const bool thread_decode = getenv("HPDR_DECODE_THREAD") != nullptr;
+        if (!stream && !thread_decode) {
+            CUDA_CHECK(cudaMemcpyAsync(d_words, job.packed, pbytes, cudaMemcpyDefault, s));
+            KPROF("k_decode", job.total_bits / 8.0 + 8.0 * units +
+                                  (double)job.n_symbols * ((job.keys ? 4 : 0) + (job.coef ? 8 : 0)), s);
+            static const bool want_stats = getenv("HPDR_DECODE_STATS") != nullptr;
+            unsigned long long *dstats = nullptr;
+            if (want_stats) {
+                dstats = (unsigned long long *)ctx->dbuf("dec_stats", 32);
+                CUDA_CHECK(cudaMemsetAsync(dstats, 0, 32, s));
+            }
+            static bool attr = false;
+            if (!attr) {
+                CUDA_CHECK(cudaFuncSetAttribute(k_decode_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)dw_smem_bytes()));
+                attr = true;
+            }
+            const unsigned blocks = (unsigned)std::min<int64_t>((units + kDWWarps - 1) / kDWWarps, 148 * 3);
+            k_decode_warp<<<blocks, kDWWarps * 32, dw_smem_bytes(), s>>>(
+                d_words, job.total_bits, d_off, job.n_symbols, units, (const DecTables *)d_tab,
+                (const uint32_t *)(d_tab + sizeof(DecTables)),
+                (const uint32_t *)(d_tab + sizeof(DecTables) + kLutSize * 4), job.keys, job.coef, job.bin_width, uerr,
+                flag, (unsigned *)(flag + 1), dstats);
+            LAUNCH_CHECK();
+            if (dstats) {
+                unsigned long long hs[4];
+                CUDA_CHECK(cudaMemcpyAsync(hs, dstats, 32, cudaMemcpyDeviceToHost, s));
+                CUDA_CHECK(cudaStreamSynchronize(s));
+                fprintf(stderr, "[decode] units %lld fallback %llu rounds %llu global-path %llu\n", (long long)units,
+                        hs[0], hs[1], hs[2]);
+            }
+        } else if (!stream) {
             CUDA_CHECK(cudaMemcpyAsync(d_words, job.packed, pbytes, cudaMemcpyDefault, s));
             KPROF("k_decode", job.total_bits / 8.0 + 8.0 * units +
                                   (double)job.n_symbols * ((job.keys ? 4 : 0) + (job.coef ? 8 : 0)), s);

@@ -56,3 +56,18 @@ def test_pipeline_matches_slab_partition_api():
     assert np.array_equal(PT.decompress_slabs(via_pipe), PL.decompress_pipelined(via_slabs))
     h = CT.read_container(via_pipe)[0]
     assert (h.vmin, h.vmax) == vr
+
+
+def test_pipeline_after_whole_field_call():
+    """Regression: chunk plans built while a copy engine streams the next chunk must be visible to
+    the compute stream (plan tables were once uploaded on the legacy stream and raced)."""
+    import torch
+
+    a = S.smooth_noise((257, 257, 257), seed=0)
+    vr = (float(a.min()), float(a.max()))
+    P.mgard_compress(torch.from_numpy(a).cuda(), 1e-4)           # whole-field call first
+    src = torch.from_numpy(a).pin_memory()
+    data = PL.compress_pipelined(src, 1e-4, value_range=vr, chunk_planes=63)
+    assert data == PL.compress_pipelined(a, 1e-4, value_range=vr, chunk_planes=63)
+    y = PL.decompress_pipelined(data)
+    assert np.max(np.abs(y.astype(np.float64) - a)) <= 1e-4 * (vr[1] - vr[0])
