@@ -137,6 +137,9 @@ void     hpdr_prof_enable(int on);
 int      hpdr_prof_read(char *json, uint64_t cap);
 /* The context's compute stream (cudaStream_t) for external event timing. */
 void    *hpdr_ctx_stream(const hpdr_ctx *ctx);
+/* Diagnostics: checks the Thomas sweeps' verified fast division against __ddiv_rn on n
+ * pseudo-random operand pairs (device 0 / current device).  *mismatches must be 0. */
+int      hpdr_selftest_div(uint64_t n, uint64_t seed, uint64_t *mismatches, uint64_t *fallbacks);
 
 #ifdef __cplusplus
 }

@@ -52,6 +52,7 @@ _SIGS = {
     "hpdr_prof_enable": (None, [C.c_int]),
     "hpdr_prof_read": (C.c_int, [C.c_char_p, C.c_uint64]),
     "hpdr_ctx_stream": (C.c_void_p, [C.c_void_p]),
+    "hpdr_selftest_div": (C.c_int, [C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "hpdr_minmax": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, _dp, _dp]),
     "hpdr_pipeline_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _u64p, C.c_double, C.c_uint32,
                                          C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_void_p, C.c_uint64,

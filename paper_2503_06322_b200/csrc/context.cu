@@ -2,6 +2,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 
 #include "context.cuh"
@@ -10,7 +11,7 @@ namespace hpdr {
 
 static thread_local std::string tl_msg;
 static thread_local int64_t tl_bit = -1;
-static thread_local uint64_t tl_launches = 0;
+static std::atomic<uint64_t> g_launches{0};   // all threads (pipeline queue workers included)
 
 void set_error(int code, const std::string &msg, int64_t bit_offset) {
     (void)code;
@@ -18,7 +19,7 @@ void set_error(int code, const std::string &msg, int64_t bit_offset) {
     tl_bit = bit_offset;
 }
 
-void count_launch() { tl_launches++; }
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void debug_sync(const char *where) {
     static const bool on = getenv("HPDR_DEBUG_SYNC") != nullptr;
@@ -136,6 +137,17 @@ void *hpdr_ctx::hbuf(const std::string &name, size_t bytes) {
 
 void hpdr_ctx::sync() { CUDA_CHECK(cudaStreamSynchronize(stream)); }
 
+hpdr_ctx *hpdr_ctx::queue(int q) {
+    if (q == 0) return this;
+    while ((int)queues.size() < q) {
+        hpdr_ctx *c = nullptr;
+        const int rc = hpdr_ctx_create(device, &c);
+        if (rc != HPDR_OK) throw Error{rc, "creating a pipeline queue context", -1};
+        queues.push_back(c);
+    }
+    return queues[q - 1];
+}
+
 cudaEvent_t hpdr_ctx::event(size_t i) {
     while (events.size() <= i) {
         cudaEvent_t e;
@@ -174,7 +186,7 @@ DevPlan &hpdr_ctx::plan(int rank, const uint64_t *dims) {
     HostPlan &h = dp->host;
     if (h.L > kMaxLevels) throw Error{HPDR_ERR_VALIDATION, "too many levels", -1};
     Packer pk;
-    struct AxOff { size_t pa, pb, pt, fa, fb, r0, rr, rl, wr, wl, ml, md, mu, tw, tb, tu, pi; };
+    struct AxOff { size_t pa, pb, pt, fa, fb, r0, rr, rl, wr, wl, ml, md, mu, tw, tb, tu, tr, pi; };
     std::vector<std::vector<AxOff>> offs(h.steps.size(), std::vector<AxOff>(4));
     for (size_t s = 0; s < h.steps.size(); s++)
         for (int d = 0; d < 4; d++) {
@@ -187,7 +199,7 @@ DevPlan &hpdr_ctx::plan(int rank, const uint64_t *dims) {
             o.r0 = pk.put(a.r0); o.rr = pk.put(a.rr); o.rl = pk.put(a.rl);
             o.wr = pk.put(a.wr); o.wl = pk.put(a.wl);
             o.ml = pk.put(a.ml); o.md = pk.put(a.md); o.mu = pk.put(a.mu);
-            o.tw = pk.put(a.tw); o.tb = pk.put(a.tb); o.tu = pk.put(a.tu);
+            o.tw = pk.put(a.tw); o.tb = pk.put(a.tb); o.tu = pk.put(a.tu); o.tr = pk.put(a.tr);
         }
     std::vector<std::vector<size_t>> moff(4, std::vector<size_t>(h.L));
     for (int d = 0; d < 4; d++)
@@ -233,6 +245,7 @@ DevPlan &hpdr_ctx::plan(int rank, const uint64_t *dims) {
             x.mu = (const double *)(base + o.mu);
             x.tw = (const double *)(base + o.tw); x.tb = (const double *)(base + o.tb);
             x.tu = (const double *)(base + o.tu);
+            x.tr = (const double *)(base + o.tr);
         }
     }
     for (int d = 0; d < 4; d++)
@@ -274,8 +287,7 @@ const char *hpdr_last_error(int64_t *bit_offset) {
 }
 
 uint64_t hpdr_launch_count(int reset) {
-    uint64_t v = tl_launches;
-    if (reset) tl_launches = 0;
+    uint64_t v = reset ? g_launches.exchange(0) : g_launches.load();
     return v;
 }
 
@@ -340,6 +352,7 @@ int hpdr_ctx_create(int device, hpdr_ctx **out) {
 
 void hpdr_ctx_trim(hpdr_ctx *c) {
     if (!c) return;
+    for (hpdr_ctx *q : c->queues) hpdr_ctx_trim(q);
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     for (auto &kv : c->dev) if (kv.second.ptr) cudaFree(kv.second.ptr);
@@ -350,6 +363,8 @@ void hpdr_ctx_trim(hpdr_ctx *c) {
 
 void hpdr_ctx_destroy(hpdr_ctx *c) {
     if (!c) return;
+    for (hpdr_ctx *q : c->queues) hpdr_ctx_destroy(q);
+    c->queues.clear();
     hpdr_ctx_trim(c);
     for (auto &kv : c->plans) cudaFree(kv.second->dbuf);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -359,7 +374,12 @@ void hpdr_ctx_destroy(hpdr_ctx *c) {
     delete c;
 }
 
-uint64_t hpdr_ctx_alloc_events(const hpdr_ctx *c) { return c ? c->alloc_events : 0; }
+uint64_t hpdr_ctx_alloc_events(const hpdr_ctx *c) {
+    if (!c) return 0;
+    uint64_t n = c->alloc_events;
+    for (const hpdr_ctx *q : c->queues) n += q->alloc_events;
+    return n;
+}
 int hpdr_ctx_device(const hpdr_ctx *c) { return c ? c->device : -1; }
 
 void *hpdr_host_alloc(uint64_t bytes) {

@@ -24,7 +24,7 @@ struct DevAxis {
     const int32_t *r0, *rr, *rl;
     const double *wr, *wl;
     const double *ml, *md, *mu;
-    const double *tw, *tb, *tu;
+    const double *tw, *tb, *tu, *tr;
     const PlaneInfo *pi;
 };
 
@@ -90,6 +90,10 @@ struct hpdr_ctx {
     std::string oname(const char *base) const { return oname(base, out_slot); }
 
     std::vector<cudaEvent_t> events;   // reusable sync events (no timing)
+    // Extra queue contexts of the streams pipeline (paper Fig. 7's queues): each has its own
+    // streams, buffers and plan cache, and is driven by its own host thread.  Owned.
+    std::vector<hpdr_ctx *> queues;
+    hpdr_ctx *queue(int q);   // q = 0: this context
     cudaEvent_t event(size_t i);
 
     void *dbuf(const std::string &name, size_t bytes);

@@ -1,18 +1,23 @@
 // pipeline.cu -- the overlapped host<->device reduction pipeline of the paper (HDEM, Fig. 7,
 // PAPER.md:413-533), rebuilt on CUDA streams.
 //
-// The field is split into dim-0 chunks.  Chunk k is copied in on the H2D stream, reduced on
-// the compute stream into a reference-identical MGARD blob (global value range),
-// and copied out on the D2H stream into an HPDR container.  Two device input
-// buffers and two output buffer sets rotate; the reuse edges of Fig. 7 are CUDA events:
-//   H2D(k+1)     waits Compute(k-1)   (input buffer (k+1) % 2 is free)
-//   Compute(k)   waits H2D(k) and D2H(k-2)  (output set k % 2 is free)
-//   D2H(k)       waits Compute(k)
-// so the copy engines move chunk k+1 in and chunk k-1 out while chunk k is reduced.
-// Decompression mirrors it (blob in, field slab out).
+// The field is split into dim-0 chunks, chunk k going to queue k mod Q (Fig. 7's queues; Q = 3 by
+// default, HPDR_PIPE_QUEUES).  A queue is a full device context (its own compute / H2D / D2H
+// streams, buffers and operator tables) driven by its own host thread, so up to Q chunks are
+// reduced concurrently: the per-chunk kernels that are latency-bound on a thin slab (axis
+// marches, Thomas lines, Huffman units) overlap each other, and the copy engines stream chunk
+// k+1 in and chunk k-1 out meanwhile.  Per queue, in order:
+//   H2D(k) -> reduce(k) into a reference-identical MGARD blob (global value range,
+//   SPEC.md:425) -> D2H(k) into the HPDR container
+// with the reuse edges of Fig. 7 as stream order / events on the queue (H2D(k+Q) after
+// reduce(k); reduce(k+Q) after D2H(k)).  The only cross-queue dependency is the container
+// offset: D2H(k) starts once the sizes of chunks < k are known (right after their reduction,
+// not their copies).  Decompression mirrors it (blob in, field slab out at a fixed offset).
 #include <string.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 
 #include "stages.cuh"
@@ -143,6 +148,50 @@ struct Timer {   // per-task CUDA-event timestamps for the pipeline trace (SPEC.
 
 using namespace hpdr;
 
+namespace {
+
+int pipe_queues(uint64_t K) {
+    static const int q_env = [] {
+        const char *e = getenv("HPDR_PIPE_QUEUES");
+        return e ? std::max(1, atoi(e)) : 3;
+    }();
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)q_env, K));
+}
+
+// Runs fn(q) for q = 0..Q-1 on Q host threads; the first error (in chunk order of detection) is rethrown.
+struct QueueRun {
+    std::mutex mu;
+    std::condition_variable cv;
+    bool failed = false;
+    Error err{HPDR_OK, "", -1};
+    void fail(const Error &e) {
+        std::lock_guard<std::mutex> g(mu);
+        if (!failed) {
+            failed = true;
+            err = e;
+        }
+        cv.notify_all();
+    }
+    template <class F>
+    void run(int Q, F &&fn) {
+        std::vector<std::thread> th;
+        for (int q = 0; q < Q; q++)
+            th.emplace_back([&, q] {
+                try {
+                    fn(q);
+                } catch (const Error &e) {
+                    fail(e);
+                } catch (const std::exception &e) {
+                    fail(Error{HPDR_ERR_CUDA, e.what(), -1});
+                }
+            });
+        for (auto &t : th) t.join();
+        if (failed) throw err;
+    }
+};
+
+}  // namespace
+
 extern "C" {
 
 int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int rank, const uint64_t *dims, double eb_rel,
@@ -181,72 +230,88 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
             chunks[k] = Chunk{a * plane, sizes[k] * plane, 0, 0};
             maxp = std::max(maxp, sizes[k]);
         }
-        chunk_planes = maxp;
         const size_t hdr_len = container_header(dtype, rank, dims, eb_rel, dict_size, vmin, vmax, chunks).size();
         if (out_cap < hdr_len) throw Error{HPDR_ERR_BUFFER, "output buffer too small for the container header", -1};
-        const size_t cbytes = chunk_planes * plane * isz;
-        char *din[2] = {(char *)ctx->dbuf("pipe_in0", cbytes), (char *)ctx->dbuf("pipe_in1", cbytes)};
-        cudaStream_t s = ctx->stream, h2d = ctx->h2d, d2h = ctx->d2h;
-        // events: [0, K) H2D done, [K, 2K) compute done, [2K, 3K) D2H done
-        auto ev = [&](uint64_t i) { return ctx->event(1 + i); };
+        const size_t cbytes = maxp * plane * isz;
+        const int Q = pipe_queues(K);
+        std::vector<hpdr_ctx *> qc(Q);
+        for (int q = 0; q < Q; q++) qc[q] = ctx->queue(q);
         Timer tm(trace != nullptr, 6 * K);
-        if (tm.on) CUDA_CHECK(cudaEventRecord(tm.t0, s));
-        CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
-        CUDA_CHECK(cudaStreamWaitEvent(h2d, ctx->event(0), 0));
-        CUDA_CHECK(cudaStreamWaitEvent(d2h, ctx->event(0), 0));
-        auto issue_h2d = [&](uint64_t k) {
-            if (k >= 2) CUDA_CHECK(cudaStreamWaitEvent(h2d, ev(K + k - 2), 0));   // buffer reuse edge
-            tm.mark(6 * k, h2d);
-            CUDA_CHECK(cudaMemcpyAsync(din[k % 2], (const char *)host_in + chunks[k].raw_off * isz,
-                                       chunks[k].raw_size * isz, cudaMemcpyHostToDevice, h2d));
-            tm.mark(6 * k + 1, h2d);
-            CUDA_CHECK(cudaEventRecord(ev(k), h2d));
-        };
-        uint64_t pos = hdr_len;
-        issue_h2d(0);
-        for (uint64_t k = 0; k < K; k++) {
-            if (k + 1 < K) issue_h2d(k + 1);
-            CUDA_CHECK(cudaStreamWaitEvent(s, ev(k), 0));
-            if (k >= 2) CUDA_CHECK(cudaStreamWaitEvent(s, ev(2 * K + k - 2), 0));   // output set reuse edge
-            tm.mark(6 * k + 2, s);
-            uint64_t sd[4] = {chunks[k].raw_size / plane, 0, 0, 0};
-            for (int d = 1; d < rank; d++) sd[d] = dims[d];
-            ctx->out_slot = (int)(k % 2);
-            static const bool dbg = getenv("HPDR_DEBUG_SYNC") != nullptr;
-            if (dbg) {
-                CUDA_CHECK(cudaDeviceSynchronize());
-                std::vector<char> chk(chunks[k].raw_size * isz);
-                CUDA_CHECK(cudaMemcpy(chk.data(), din[k % 2], chk.size(), cudaMemcpyDeviceToHost));
-                fprintf(stderr, "[pipe] chunk %llu planes %llu din %p match %d\n", (unsigned long long)k,
-                        (unsigned long long)sd[0], (void *)din[k % 2],
-                        memcmp(chk.data(), (const char *)host_in + chunks[k].raw_off * isz, chk.size()) == 0);
+        // every queue starts after the caller's prior work on the main context
+        CUDA_CHECK(cudaEventRecord(ctx->event(0), ctx->stream));
+        if (tm.on) CUDA_CHECK(cudaEventRecord(tm.t0, ctx->stream));
+        // container offsets: pos[k] is known once the sizes of chunks < k are
+        std::vector<uint64_t> pos(K + 1, 0), psize(K, 0);
+        std::vector<char> have(K, 0);
+        uint64_t next_pos = 0;   // first chunk whose offset is not yet known
+        pos[0] = hdr_len;
+        QueueRun R;
+        R.run(Q, [&](int q) {
+            hpdr_ctx *c = qc[q];
+            CUDA_CHECK(cudaSetDevice(c->device));
+            if (c != ctx) {
+                CUDA_CHECK(cudaStreamWaitEvent(c->stream, ctx->event(0), 0));
             }
-            compress_core(ctx, din[k % 2], dtype, rank, sd, eb_rel, dict_size, 1, vmin, vmax, false);
-            if (dbg) fprintf(stderr, "[pipe] chunk %llu done, %llu bytes\n", (unsigned long long)k,
-                             (unsigned long long)ctx->pending.total_len);
-            const hpdr_ctx::Pending P = ctx->pending;
-            tm.mark(6 * k + 3, s);
-            CUDA_CHECK(cudaEventRecord(ev(K + k), s));
-            chunks[k].pay_off = pos - hdr_len;
-            chunks[k].pay_size = P.total_len;
-            if (pos + P.total_len > out_cap) throw Error{HPDR_ERR_BUFFER, "output buffer too small for the container", -1};
-            CUDA_CHECK(cudaStreamWaitEvent(d2h, ev(K + k), 0));
-            tm.mark(6 * k + 4, d2h);
-            fetch_pending_on(ctx, P, (char *)out + pos, out_cap - pos, d2h, false);
-            tm.mark(6 * k + 5, d2h);
-            CUDA_CHECK(cudaEventRecord(ev(2 * K + k), d2h));
-            pos += P.total_len;
-        }
-        CUDA_CHECK(cudaStreamSynchronize(d2h));
-        ctx->out_slot = 0;
+            CUDA_CHECK(cudaStreamWaitEvent(c->h2d, ctx->event(0), 0));
+            CUDA_CHECK(cudaStreamWaitEvent(c->d2h, ctx->event(0), 0));
+            c->out_slot = 0;
+            char *din = (char *)c->dbuf("pipe_in", cbytes);
+            cudaEvent_t ev_in = c->event(1), ev_red = c->event(2), ev_out = c->event(3);
+            bool first = true;
+            for (uint64_t k = q; k < K; k += Q) {
+                if (R.failed) return;
+                if (!first) CUDA_CHECK(cudaStreamWaitEvent(c->h2d, ev_red, 0));   // input buffer reuse edge
+                tm.mark(6 * k, c->h2d);
+                CUDA_CHECK(cudaMemcpyAsync(din, (const char *)host_in + chunks[k].raw_off * isz,
+                                           chunks[k].raw_size * isz, cudaMemcpyHostToDevice, c->h2d));
+                tm.mark(6 * k + 1, c->h2d);
+                CUDA_CHECK(cudaEventRecord(ev_in, c->h2d));
+                CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_in, 0));
+                if (!first) CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_out, 0));   // output buffers reuse edge
+                tm.mark(6 * k + 2, c->stream);
+                uint64_t sd[4] = {chunks[k].raw_size / plane, 0, 0, 0};
+                for (int d = 1; d < rank; d++) sd[d] = dims[d];
+                compress_core(c, din, dtype, rank, sd, eb_rel, dict_size, 1, vmin, vmax, false);
+                const hpdr_ctx::Pending P = c->pending;
+                tm.mark(6 * k + 3, c->stream);
+                CUDA_CHECK(cudaEventRecord(ev_red, c->stream));
+                uint64_t at;
+                {
+                    std::unique_lock<std::mutex> lk(R.mu);
+                    psize[k] = P.total_len;
+                    have[k] = 1;
+                    while (next_pos < K && have[next_pos]) {
+                        pos[next_pos + 1] = pos[next_pos] + psize[next_pos];
+                        next_pos++;
+                    }
+                    R.cv.notify_all();
+                    R.cv.wait(lk, [&] { return next_pos >= k || R.failed; });
+                    if (R.failed) return;
+                    at = pos[k];
+                }
+                if (at + P.total_len > out_cap) throw Error{HPDR_ERR_BUFFER, "output buffer too small for the container", -1};
+                chunks[k].pay_off = at - hdr_len;
+                chunks[k].pay_size = P.total_len;
+                CUDA_CHECK(cudaStreamWaitEvent(c->d2h, ev_red, 0));
+                tm.mark(6 * k + 4, c->d2h);
+                fetch_pending_on(c, P, (char *)out + at, out_cap - at, c->d2h, false);
+                tm.mark(6 * k + 5, c->d2h);
+                CUDA_CHECK(cudaEventRecord(ev_out, c->d2h));
+                first = false;
+            }
+            CUDA_CHECK(cudaStreamSynchronize(c->d2h));
+        });
         const std::vector<uint8_t> hdr = container_header(dtype, rank, dims, eb_rel, dict_size, vmin, vmax, chunks);
-        if (classify(out) == MemKind::Device) CUDA_CHECK(cudaMemcpy(out, hdr.data(), hdr.size(), cudaMemcpyHostToDevice));
-        else memcpy(out, hdr.data(), hdr.size());
-        *out_len = pos;
+        if (classify(out) == MemKind::Device) {
+            CUDA_CHECK(cudaMemcpyAsync(out, hdr.data(), hdr.size(), cudaMemcpyHostToDevice, ctx->stream));
+            CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        } else {
+            memcpy(out, hdr.data(), hdr.size());
+        }
+        *out_len = pos[K];
         tm.dump(trace);
         return HPDR_OK;
     } catch (const Error &e) {
-        ctx->out_slot = 0;
         cudaDeviceSynchronize();
         set_error(e.code, e.msg, e.bit_offset);
         return e.code;
@@ -298,45 +363,52 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
             maxpay = std::max(maxpay, ch.pay_size);
             maxraw = std::max(maxraw, ch.raw_size);
         }
-        uint8_t *dblob[2] = {(uint8_t *)ctx->dbuf("pipe_blob0", maxpay), (uint8_t *)ctx->dbuf("pipe_blob1", maxpay)};
-        char *dout[2] = {(char *)ctx->dbuf("pipe_out0", maxraw * isz), (char *)ctx->dbuf("pipe_out1", maxraw * isz)};
-        cudaStream_t s = ctx->stream, h2d = ctx->h2d, d2h = ctx->d2h;
-        auto ev = [&](uint64_t i) { return ctx->event(1 + i); };
-        Timer tm(trace != nullptr, 6 * (size_t)K);
-        if (tm.on) CUDA_CHECK(cudaEventRecord(tm.t0, s));
-        CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
-        CUDA_CHECK(cudaStreamWaitEvent(h2d, ctx->event(0), 0));
-        CUDA_CHECK(cudaStreamWaitEvent(d2h, ctx->event(0), 0));
         const bool host_out = classify(out) != MemKind::Device;
-        auto issue_h2d = [&](uint64_t k) {
-            if (k >= 2) CUDA_CHECK(cudaStreamWaitEvent(h2d, ev(K + k - 2), 0));
-            tm.mark(6 * k, h2d);
-            CUDA_CHECK(cudaMemcpyAsync(dblob[k % 2], c + base + chunks[k].pay_off, chunks[k].pay_size,
-                                       cudaMemcpyHostToDevice, h2d));
-            tm.mark(6 * k + 1, h2d);
-            CUDA_CHECK(cudaEventRecord(ev(k), h2d));
-        };
-        if (K) issue_h2d(0);
-        for (uint64_t k = 0; k < K; k++) {
-            if (k + 1 < K) issue_h2d(k + 1);
-            CUDA_CHECK(cudaStreamWaitEvent(s, ev(k), 0));
-            if (k >= 2) CUDA_CHECK(cudaStreamWaitEvent(s, ev(2 * K + k - 2), 0));
-            tm.mark(6 * k + 2, s);
-            char *dst = host_out ? dout[k % 2] : (char *)out + chunks[k].raw_off * isz;
-            decompress_core(ctx, c + base + chunks[k].pay_off, chunks[k].pay_size, dblob[k % 2], dst,
-                            chunks[k].raw_size * isz, false);
-            tm.mark(6 * k + 3, s);
-            CUDA_CHECK(cudaEventRecord(ev(K + k), s));
-            CUDA_CHECK(cudaStreamWaitEvent(d2h, ev(K + k), 0));
-            tm.mark(6 * k + 4, d2h);
-            if (host_out)
-                CUDA_CHECK(cudaMemcpyAsync((char *)out + chunks[k].raw_off * isz, dout[k % 2], chunks[k].raw_size * isz,
-                                           cudaMemcpyDeviceToHost, d2h));
-            tm.mark(6 * k + 5, d2h);
-            CUDA_CHECK(cudaEventRecord(ev(2 * K + k), d2h));
-        }
-        CUDA_CHECK(cudaStreamSynchronize(d2h));
-        CUDA_CHECK(cudaStreamSynchronize(s));
+        const int Q = pipe_queues(K);
+        std::vector<hpdr_ctx *> qc(Q);
+        for (int q = 0; q < Q; q++) qc[q] = ctx->queue(q);
+        Timer tm(trace != nullptr, 6 * (size_t)K);
+        CUDA_CHECK(cudaEventRecord(ctx->event(0), ctx->stream));
+        if (tm.on) CUDA_CHECK(cudaEventRecord(tm.t0, ctx->stream));
+        QueueRun R;
+        R.run(Q, [&](int q) {
+            hpdr_ctx *x = qc[q];
+            CUDA_CHECK(cudaSetDevice(x->device));
+            if (x != ctx) CUDA_CHECK(cudaStreamWaitEvent(x->stream, ctx->event(0), 0));
+            CUDA_CHECK(cudaStreamWaitEvent(x->h2d, ctx->event(0), 0));
+            CUDA_CHECK(cudaStreamWaitEvent(x->d2h, ctx->event(0), 0));
+            uint8_t *dblob = (uint8_t *)x->dbuf("pipe_blob", maxpay);
+            char *dout = host_out ? (char *)x->dbuf("pipe_out", maxraw * isz) : nullptr;
+            cudaEvent_t ev_in = x->event(1), ev_red = x->event(2), ev_out = x->event(3);
+            bool first = true;
+            for (uint64_t k = q; k < K; k += Q) {
+                if (R.failed) return;
+                if (!first) CUDA_CHECK(cudaStreamWaitEvent(x->h2d, ev_red, 0));   // blob buffer reuse edge
+                tm.mark(6 * k, x->h2d);
+                CUDA_CHECK(cudaMemcpyAsync(dblob, c + base + chunks[k].pay_off, chunks[k].pay_size,
+                                           cudaMemcpyHostToDevice, x->h2d));
+                tm.mark(6 * k + 1, x->h2d);
+                CUDA_CHECK(cudaEventRecord(ev_in, x->h2d));
+                CUDA_CHECK(cudaStreamWaitEvent(x->stream, ev_in, 0));
+                if (!first && host_out) CUDA_CHECK(cudaStreamWaitEvent(x->stream, ev_out, 0));   // output slab reuse
+                tm.mark(6 * k + 2, x->stream);
+                char *dst = host_out ? dout : (char *)out + chunks[k].raw_off * isz;
+                decompress_core(x, c + base + chunks[k].pay_off, chunks[k].pay_size, dblob, dst,
+                                chunks[k].raw_size * isz, false);
+                tm.mark(6 * k + 3, x->stream);
+                CUDA_CHECK(cudaEventRecord(ev_red, x->stream));
+                CUDA_CHECK(cudaStreamWaitEvent(x->d2h, ev_red, 0));
+                tm.mark(6 * k + 4, x->d2h);
+                if (host_out)
+                    CUDA_CHECK(cudaMemcpyAsync((char *)out + chunks[k].raw_off * isz, dout, chunks[k].raw_size * isz,
+                                               cudaMemcpyDeviceToHost, x->d2h));
+                tm.mark(6 * k + 5, x->d2h);
+                CUDA_CHECK(cudaEventRecord(ev_out, x->d2h));
+                first = false;
+            }
+            CUDA_CHECK(cudaStreamSynchronize(x->d2h));
+            CUDA_CHECK(cudaStreamSynchronize(x->stream));
+        });
         tm.dump(trace);
         return HPDR_OK;
     } catch (const Error &e) {

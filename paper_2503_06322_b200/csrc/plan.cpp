@@ -72,6 +72,8 @@ static void axis_tables(AxisTables &a, const std::vector<int32_t> &fine, const s
         a.tw[i] = cl[i] / a.tb[i - 1];
         a.tb[i] = cd[i] - a.tw[i] * a.tu[i - 1];
     }
+    a.tr.resize(nc);
+    for (int64_t i = 0; i < nc; i++) a.tr[i] = 1.0 / a.tb[i];
     a.pinfo.assign(n, PlaneInfo{});
     for (int64_t j = 0; j < n; j++) {
         PlaneInfo &p = a.pinfo[j];

@@ -41,6 +41,7 @@ struct AxisTables {
     std::vector<double> ml, md, mu;
     // coarse-mass Thomas factors (w, b', upper), per coarse node
     std::vector<double> tw, tb, tu;
+    std::vector<double> tr;   // RN(1 / b'): seed of the verified fast division in the Thomas sweeps
 };
 
 struct StepTables {

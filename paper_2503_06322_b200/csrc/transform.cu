@@ -212,6 +212,33 @@ __global__ void k_mass_restrict(const double *__restrict__ src, double *__restri
     }
 }
 
+// Verified fast IEEE division for the back substitution.  q1 = q0 + (a - b q0) r with
+// r = RN(1/b) (host table) is accepted only when its exact residual a - b q1 (an FMA) proves
+// |a/b - q1| < half the smaller gap next to q1, i.e. q1 == RN(a/b) = __ddiv_rn(a, b); anything
+// else (ties, subnormal / huge / non-finite values) raises `bad` and the caller redoes the line
+// with __ddiv_rn.  Zeros take a * r, which carries the IEEE sign of a / b.
+__device__ __forceinline__ double div_fast(double a, double b, double r, bool &bad) {
+    if (a == 0.0) return dmul(a, r);
+    const double q0 = dmul(a, r);
+    const double q1 = __fma_rn(__fma_rn(-q0, b, a), r, q0);
+    const double rem = __fma_rn(-q1, b, a);
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(q1);
+    const int ex = (int)((bits >> 52) & 0x7ff);
+    const int mant0 = (bits & 0xfffffffffffffULL) == 0;
+    // h = 2^(E - 53) (2^(E - 54) at a power of two), E the unbiased exponent of q1
+    const double h = __longlong_as_double((long long)(ex - 53 - mant0) << 52);
+    const double bound = fabs(b) * h;   // exact: power-of-two scaling of a normal value
+    bad |= !(ex > 120 && ex < 1900) || !(bound > 1e-290) || !(fabs(rem) < bound);
+    return q1;
+}
+
+// div_fast with the exact fallback inline (for in-place sweeps that cannot redo a line)
+__device__ __forceinline__ double div_checked(double a, double b, double r) {
+    bool bad = false;
+    const double q = div_fast(a, b, r, bad);
+    return bad ? ddiv(a, b) : q;
+}
+
 // ---------------------------------------------------------------- IPK: batched Thomas solves
 // Strided axis: one thread per line, threads along the contiguous inner index (coalesced).
 __global__ void k_thomas_strided(double *__restrict__ arr, int64_t outer, int32_t n, int64_t inner,
@@ -244,7 +271,8 @@ constexpr int kThomasWarps = 4;
 __global__ void __launch_bounds__(kThomasWarps * 32) k_thomas_contig(double *__restrict__ arr, int64_t lines, int32_t n,
                                                                      const double *__restrict__ tw,
                                                                      const double *__restrict__ tb,
-                                                                     const double *__restrict__ tu) {
+                                                                     const double *__restrict__ tu,
+                                                                     const double *__restrict__ tr) {
     __shared__ double tile[kThomasWarps][32][33];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double (*T)[33] = tile[w];
@@ -302,7 +330,7 @@ __global__ void __launch_bounds__(kThomasWarps * 32) k_thomas_contig(double *__r
 template <int U>
 __global__ void __launch_bounds__(128) k_thomas_reg(double *__restrict__ arr, int64_t outer, int32_t n, int64_t inner,
                                                     const double *__restrict__ tw, const double *__restrict__ tb,
-                                                    const double *__restrict__ tu) {
+                                                    const double *__restrict__ tu, const double *__restrict__ tr) {
     const int64_t lines = outer * inner;
     for (int64_t ln = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ln < lines; ln += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = ln / inner, q = ln - p * inner;
@@ -332,7 +360,7 @@ __global__ void __launch_bounds__(128) k_thomas_reg(double *__restrict__ arr, in
 #pragma unroll
             for (int k = 0; k < U; k++) cur[k] = nxt[k];
         }
-        double last = ddiv(prev, __ldg(tb + n - 1));
+        double last = ddiv(prev, __ldg(tb + n - 1));   // (__ddiv_rn beat div_checked here)
         x[(int64_t)(n - 1) * inner] = last;
         // back substitution: x_i = (x_i - u_i x_{i+1}) / b'_i, i = n-2 .. 0
         load(cur, n - 1 - U);
@@ -352,6 +380,133 @@ __global__ void __launch_bounds__(128) k_thomas_reg(double *__restrict__ arr, in
             for (int k = 0; k < U; k++) cur[k] = nxt[k];
         }
     }
+}
+
+// Tiled Thomas solve: one warp owns 32 lines, staged whole in shared memory by cp.async
+// (strided axes: row i of the tile = 32 consecutive inner columns, one coalesced 256-byte
+// segment; contiguous axis: 32 contiguous lines, row stride padded odd so lane-per-line reads are
+// bank-conflict free).  Forward elimination and back substitution run in shared memory with the
+// reference's rounding (transform.py:236-242; division verified as above, exact redo otherwise),
+// then the tile is written back coalesced: 16 bytes of DRAM traffic per node.
+constexpr int kThomasTileMaxN = 880;   // 32 lines x 880 x 8 B = 220 KB of shared memory
+
+template <bool CONTIG>
+__global__ void __launch_bounds__(32) k_thomas_tile(double *__restrict__ arr, int64_t outer, int32_t n,
+                                                    int64_t inner, int32_t ls, const double *__restrict__ tw,
+                                                    const double *__restrict__ tb, const double *__restrict__ tu,
+                                                    const double *__restrict__ tr) {
+    extern __shared__ __align__(16) double tsm[];
+    const int lane = threadIdx.x;
+    // element (line l, position i) of the tile
+    auto at = [&](int l, int i) -> double & { return CONTIG ? tsm[(int64_t)l * ls + i] : tsm[(int64_t)i * 32 + l]; };
+    const int64_t tiles_per_outer = CONTIG ? 1 : (inner + 31) / 32;
+    const int64_t tiles = CONTIG ? (outer + 31) / 32 : outer * tiles_per_outer;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int64_t p = 0, q0 = 0, l0 = 0;
+        int nl;
+        if (CONTIG) {
+            l0 = t * 32;
+            nl = (int)min64(32, outer - l0);
+        } else {
+            p = t / tiles_per_outer;
+            q0 = (t - p * tiles_per_outer) * 32;
+            nl = (int)min64(32, inner - q0);
+        }
+        // stage the tile
+        if (CONTIG) {
+            for (int l = 0; l < nl; l++) {
+                const double *src = arr + (l0 + l) * (int64_t)n;
+                for (int i = lane; i < n; i += 32) cp_async<8>(&at(l, i), src + i);
+            }
+        } else if (lane < nl) {
+            const double *src = arr + p * (int64_t)n * inner + q0 + lane;
+            for (int i = 0; i < n; i++) cp_async<8>(&at(lane, i), src + (int64_t)i * inner);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+        if (lane < nl) {
+            // forward elimination: x_i -= w_i x_{i-1}
+            double prev = at(lane, 0);
+            for (int i = 1; i < n; i++) {
+                const double v = dsub(at(lane, i), dmul(__ldg(tw + i), prev));
+                at(lane, i) = v;
+                prev = v;
+            }
+            // back substitution: x_{n-1} /= b'_{n-1}; x_i = (x_i - u_i x_{i+1}) / b'_i
+            bool bad = false;
+            double last = div_fast(prev, __ldg(tb + n - 1), __ldg(tr + n - 1), bad);
+            at(lane, n - 1) = last;
+            for (int i = n - 2; i >= 0; i--) {
+                const double v = dsub(at(lane, i), dmul(__ldg(tu + i), last));
+                last = div_fast(v, __ldg(tb + i), __ldg(tr + i), bad);
+                at(lane, i) = last;
+            }
+            if (bad) {   // rare: redo this line from its forward values with __ddiv_rn
+                if (CONTIG) {
+                    const double *src = arr + (l0 + lane) * (int64_t)n;
+                    prev = src[0];
+                    at(lane, 0) = prev;
+                    for (int i = 1; i < n; i++) {
+                        const double v = dsub(src[i], dmul(__ldg(tw + i), prev));
+                        at(lane, i) = v;
+                        prev = v;
+                    }
+                } else {
+                    const double *src = arr + p * (int64_t)n * inner + q0 + lane;
+                    prev = src[0];
+                    at(lane, 0) = prev;
+                    for (int i = 1; i < n; i++) {
+                        const double v = dsub(src[(int64_t)i * inner], dmul(__ldg(tw + i), prev));
+                        at(lane, i) = v;
+                        prev = v;
+                    }
+                }
+                last = ddiv(prev, __ldg(tb + n - 1));
+                at(lane, n - 1) = last;
+                for (int i = n - 2; i >= 0; i--) {
+                    const double v = dsub(at(lane, i), dmul(__ldg(tu + i), last));
+                    last = ddiv(v, __ldg(tb + i));
+                    at(lane, i) = last;
+                }
+            }
+        }
+        __syncwarp();
+        // write back
+        if (CONTIG) {
+            for (int l = 0; l < nl; l++) {
+                double *dst = arr + (l0 + l) * (int64_t)n;
+                for (int i = lane; i < n; i += 32) dst[i] = at(l, i);
+            }
+        } else if (lane < nl) {
+            double *dst = arr + p * (int64_t)n * inner + q0 + lane;
+            for (int i = 0; i < n; i++) dst[(int64_t)i * inner] = at(lane, i);
+        }
+        __syncwarp();
+    }
+}
+
+// Self-test of div_fast against __ddiv_rn over pseudo-random operands (hpdr_selftest_div).
+__global__ void k_selftest_div(uint64_t n, uint64_t seed, unsigned long long *mism, unsigned long long *fallback) {
+    unsigned long long m = 0, f = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t z = seed + i * 0x9E3779B97F4A7C15ULL;
+        auto mix = [](uint64_t x) {
+            x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+            x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+            return x ^ (x >> 31);
+        };
+        const uint64_t r1 = mix(z), r2 = mix(z + 1);
+        // a: any sign, exponent within +-40 of 1; b: positive, exponent within +-20 (Thomas pivots)
+        const double a = __longlong_as_double((long long)((r1 & 0x800fffffffffffffULL) | ((uint64_t)(1023 - 40 + (r1 >> 52) % 81) << 52)));
+        const double b = __longlong_as_double((long long)((r2 & 0x000fffffffffffffULL) | ((uint64_t)(1023 - 20 + (r2 >> 52) % 41) << 52)));
+        bool bad = false;
+        const double q = div_fast(a, b, ddiv(1.0, b), bad);
+        if (bad) f++;
+        else if (__double_as_longlong(q) != __double_as_longlong(ddiv(a, b))) m++;
+    }
+    if (m) atomicAdd(mism, m);
+    if (f) atomicAdd(fallback, f);
 }
 
 // ---------------------------------------------------------------- elementwise
@@ -427,13 +582,40 @@ void thomas(double *arr, const Shape4 &csh, int a, const DevAxis &ax, cudaStream
     // strided axes: register-blocked lines (coalesced across threads); contiguous axis: the
     // warp-tile transpose kernel measured faster (0.39 vs 0.45 ms at 257^3 coarse grid)
     static const bool legacy = getenv("HPDR_THOMAS_LEGACY") != nullptr;
-    if (!legacy && inner > 1) {
+    static const bool tile = getenv("HPDR_THOMAS_TILE") != nullptr;
+    if (!legacy && tile && ax.nc <= kThomasTileMaxN) {
+        const int n = ax.nc;
+        if (inner == 1) {
+            const int ls = n | 1;   // odd row stride: lane-per-line reads hit distinct banks
+            const size_t smem = (size_t)32 * ls * 8;
+            static int attr_c = 0;
+            if (smem > 48 * 1024 && attr_c < (int)smem) {
+                CUDA_CHECK(cudaFuncSetAttribute(k_thomas_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(32 * (kThomasTileMaxN | 1) * 8)));
+                attr_c = 32 * (kThomasTileMaxN | 1) * 8;
+            }
+            const int64_t tiles = (outer + 31) / 32;
+            k_thomas_tile<true><<<(unsigned)std::min<int64_t>(tiles, 148 * 32), 32, smem, s>>>(
+                arr, outer, n, inner, ls, ax.tw, ax.tb, ax.tu, ax.tr);
+        } else {
+            const size_t smem = (size_t)32 * n * 8;
+            static int attr_s = 0;
+            if (smem > 48 * 1024 && attr_s < (int)smem) {
+                CUDA_CHECK(cudaFuncSetAttribute(k_thomas_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(32 * kThomasTileMaxN * 8)));
+                attr_s = 32 * kThomasTileMaxN * 8;
+            }
+            const int64_t tiles = outer * ((inner + 31) / 32);
+            k_thomas_tile<false><<<(unsigned)std::min<int64_t>(tiles, 148 * 32), 32, smem, s>>>(
+                arr, outer, n, inner, 0, ax.tw, ax.tb, ax.tu, ax.tr);
+        }
+    } else if (!legacy && inner > 1) {
         const int64_t lines = outer * inner;
-        k_thomas_reg<8><<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb, ax.tu);
+        k_thomas_reg<8><<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb, ax.tu, ax.tr);
     } else if (inner == 1) {
         int64_t lines = outer;
         unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((lines + 127) / 128, 148 * 16));
-        k_thomas_contig<<<g, kThomasWarps * 32, 0, s>>>(arr, lines, ax.nc, ax.tw, ax.tb, ax.tu);
+        k_thomas_contig<<<g, kThomasWarps * 32, 0, s>>>(arr, lines, ax.nc, ax.tw, ax.tb, ax.tu, ax.tr);
     } else {
         int64_t lines = outer * inner;
         k_thomas_strided<<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb, ax.tu);
@@ -884,3 +1066,22 @@ void cast_output(const double *src, void *dst, int dtype, int64_t n, cudaStream_
 }
 
 }  // namespace hpdr
+
+extern "C" int hpdr_selftest_div(uint64_t n, uint64_t seed, uint64_t *mismatches, uint64_t *fallbacks) {
+    try {
+        unsigned long long *d = nullptr;
+        CUDA_CHECK(cudaMalloc(&d, 16));
+        CUDA_CHECK(cudaMemset(d, 0, 16));
+        hpdr::k_selftest_div<<<148 * 8, 256>>>(n, seed, d, d + 1);
+        CUDA_CHECK(cudaGetLastError());
+        unsigned long long h[2];
+        CUDA_CHECK(cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost));
+        CUDA_CHECK(cudaFree(d));
+        *mismatches = h[0];
+        *fallbacks = h[1];
+        return HPDR_OK;
+    } catch (const hpdr::Error &e) {
+        hpdr::set_error(e.code, e.msg, e.bit_offset);
+        return e.code;
+    }
+}

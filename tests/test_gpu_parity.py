@@ -221,3 +221,15 @@ def test_execution_variants_bit_identical(env):
     r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT % root], env={**os.environ, **env},
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "variant ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_thomas_fast_division_matches_ieee():
+    """The Thomas back substitution's verified fast division never differs from __ddiv_rn."""
+    import ctypes as C
+
+    from paper_2503_06322_b200._lib import check, lib
+
+    m, f = C.c_uint64(), C.c_uint64()
+    check(lib().hpdr_selftest_div(1 << 26, 12345, C.byref(m), C.byref(f)))
+    assert m.value == 0
+    assert f.value < (1 << 26) // 1000   # the exact redo is rare
