@@ -89,7 +89,8 @@ int levels_of(const std::vector<uint64_t> &dims) {
 
 // Encode keys (device) into the pending Huffman layout.  Returns false for single-key streams.
 void huffman_stage(hpdr_ctx *ctx, const uint32_t *d_keys, int64_t n, uint32_t dict, const std::vector<uint64_t> &hist,
-                   std::vector<uint8_t> &mid, EncodeResult &enc, bool &single, cudaStream_t s) {
+                   std::vector<uint8_t> &mid, EncodeResult &enc, bool &single, cudaStream_t s,
+                   const EncodeHooks *hooks = nullptr) {
     // huffman_compress (huffman.py:366-396)
     put<uint16_t>(mid, (uint16_t)dict);
     put<uint64_t>(mid, (uint64_t)n);
@@ -115,12 +116,14 @@ void huffman_stage(hpdr_ctx *ctx, const uint32_t *d_keys, int64_t n, uint32_t di
         single = true;
         return;
     }
-    encode_device(ctx, d_keys, n, dict, lens.data(), codes.data(), enc, s);
-    put<uint32_t>(mid, (uint32_t)enc.n_units);
+    put<uint32_t>(mid, (uint32_t)((n + kBlockSymbols - 1) / kBlockSymbols));
+    encode_device(ctx, d_keys, n, dict, lens.data(), codes.data(), enc, s, hooks);
 }
 
-// Write the pending stream (head | outliers | mid | offsets | total_bits | packed) to out.
-void fetch_pending(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uint64_t cap, cudaStream_t s, bool sync) {
+// Write the pending stream (head | outliers | mid | offsets | total_bits | packed) to out; with
+// payload = false everything but the packed bytes.  Returns the offset of the packed bytes.
+uint64_t fetch_pending(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uint64_t cap, cudaStream_t s, bool sync,
+                       bool payload) {
     if (!P.valid) fail(HPDR_ERR_VALIDATION, "no pending compressed stream in this context");
     if (cap < P.total_len) fail(HPDR_ERR_BUFFER, "output buffer too small: need " + std::to_string(P.total_len));
     const bool dev = classify(out) == MemKind::Device;
@@ -143,19 +146,24 @@ void fetch_pending(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uint64_
         dev_bytes(ctx->dbuf(ctx->oname("obins", P.slot), P.n_out * 8), P.n_out * 8);
     }
     host_bytes(P.mid.data(), P.mid.size());
+    uint64_t pay = pos;
     if (!P.single_key) {
         dev_bytes(ctx->dbuf(ctx->oname("enc_uoff", P.slot), (P.n_units + 1) * 8), P.n_units * 8);
         uint64_t tb = P.total_bits;
         host_bytes(&tb, 8);
-        dev_bytes(ctx->dbuf(ctx->oname("enc_words", P.slot), (P.total_bits + 31) / 32 * 4 + 8), (P.total_bits + 7) / 8);
+        pay = pos;
+        if (payload)
+            dev_bytes(ctx->dbuf(ctx->oname("enc_words", P.slot), (P.total_bits + 31) / 32 * 4 + 8), (P.total_bits + 7) / 8);
     } else {
         uint64_t z = 0;
         host_bytes(&z, 8);
+        pay = pos;
     }
     if (sync) CUDA_CHECK(cudaStreamSynchronize(s));
+    return pay;
 }
 
-void fetch_pending(hpdr_ctx *ctx, void *out, uint64_t cap) { fetch_pending(ctx, ctx->pending, out, cap, ctx->stream, true); }
+void fetch_pending(hpdr_ctx *ctx, void *out, uint64_t cap) { fetch_pending(ctx, ctx->pending, out, cap, ctx->stream, true, true); }
 
 struct HuffHeader {
     uint32_t dict = 0;
@@ -333,13 +341,14 @@ extern "C" {
 
 namespace hpdr {
 void fetch_pending_on(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uint64_t cap, cudaStream_t s, bool sync) {
-    fetch_pending(ctx, P, out, cap, s, sync);
+    fetch_pending(ctx, P, out, cap, s, sync, true);
 }
 
 // mgard_compress (codec.py:25-56) up to a pending blob in ctx->pending (device parts in output
 // slot ctx->out_slot).  allow_stream: a host input may be streamed in dim-0 chunks.
 void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, double eb_rel,
-                   uint32_t dict_size, int has_range, double range_min, double range_max, bool allow_stream) {
+                   uint32_t dict_size, int has_range, double range_min, double range_max, bool allow_stream,
+                   void *fetch_out, uint64_t fetch_cap) {
     {
         ctx->pending.valid = false;
         if (dtype != 0 && dtype != 1) fail(HPDR_ERR_VALIDATION, "lossy compression needs F32/F64");
@@ -355,6 +364,7 @@ void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uin
         const bool fused = L > 1 && use_fused(p);
         static const bool no_stream = getenv("HPDR_NO_STREAM") != nullptr;
         const bool streamed = host_in && fused && !no_stream && allow_stream;
+        phase_mark("start", s);
         const void *d_in = streamed ? nullptr : device_input(ctx, in, (size_t)N * itemsize(dtype), "input", s);
         double u_min = range_min, u_max = range_max;
         if (!has_range && !streamed) minmax_device(ctx, d_in, dtype, N, &u_min, &u_max, s);
@@ -389,7 +399,9 @@ void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uin
                 qo.bin = bin;
                 d_coarse = decompose_quantize(ctx, p, d_in, dtype, qo, s);
             }
+            phase_mark("decomposed", s);
             quantize_finish(ctx, N, dict_size, bin, nullptr, qo.obins, q, s);
+            phase_mark("outliers", s);
         } else {
             eb_abs = eb_rel * (u_max - u_min);
             bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
@@ -421,13 +433,49 @@ void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uin
         for (double v : coarse) put<double>(P.mid, v);
         EncodeResult enc;
         bool single;
-        huffman_stage(ctx, keys, N, dict_size, q.hist, P.mid, enc, single, s);
+        phase_mark("coarse_read", s);
+        // Streamed fetch (pinned / device output): as soon as the stream layout is known the blob
+        // head, outliers and unit offsets go out on the D2H stream, and the packed payload follows
+        // unit group by unit group behind the encode launches.
+        EncodeHooks hooks;
+        bool streamed_fetch = false;
+        uint64_t pay_pos = 0;
+        const MemKind ok = fetch_out ? classify(fetch_out) : MemKind::Host;
+        if (fetch_out && ok != MemKind::Host) {
+            hooks.groups = 8;
+            hooks.ready = [&](const EncodeResult &e) {
+                const uint64_t total = P.head.size() + 16 * P.n_out + P.mid.size() + 8 * e.n_units + 8 + (e.total_bits + 7) / 8;
+                if (fetch_cap < total) return;
+                streamed_fetch = true;
+                hpdr_ctx::Pending Q = P;
+                Q.n_units = e.n_units;
+                Q.total_bits = e.total_bits;
+                Q.total_len = total;
+                Q.slot = ctx->out_slot;
+                Q.valid = true;
+                CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
+                CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(0), 0));
+                pay_pos = fetch_pending(ctx, Q, fetch_out, fetch_cap, ctx->d2h, false, /*payload=*/false);
+            };
+            hooks.group_done = [&](int g, uint64_t lo, uint64_t hi) {
+                if (!streamed_fetch || hi <= lo) return;
+                CUDA_CHECK(cudaEventRecord(ctx->event(1 + g), s));
+                CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(1 + g), 0));
+                const bool dev = ok == MemKind::Device;
+                CUDA_CHECK(cudaMemcpyAsync((char *)fetch_out + pay_pos + lo, (const char *)ctx->dbuf(ctx->oname("enc_words"), 16) + lo,
+                                           hi - lo, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->d2h));
+            };
+        }
+        huffman_stage(ctx, keys, N, dict_size, q.hist, P.mid, enc, single, s, fetch_out ? &hooks : nullptr);
+        phase_mark("encoded", s);
         P.single_key = single;
         P.n_units = enc.n_units;
         P.total_bits = enc.total_bits;
         P.total_len = P.head.size() + 16 * P.n_out + P.mid.size() + 8 * P.n_units + 8 + (P.total_bits + 7) / 8;
         P.slot = ctx->out_slot;
         P.valid = true;
+        P.fetched = streamed_fetch;
+        if (streamed_fetch) CUDA_CHECK(cudaStreamSynchronize(ctx->d2h));
     }
 }
 }  // namespace hpdr
@@ -440,10 +488,13 @@ int hpdr_mgard_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, cons
     return guard([&] {
         CUDA_CHECK(cudaSetDevice(ctx->device));
         ctx->out_slot = 0;
-        compress_core(ctx, in, dtype, rank, dims, eb_rel, dict_size, has_range, range_min, range_max, true);
+        compress_core(ctx, in, dtype, rank, dims, eb_rel, dict_size, has_range, range_min, range_max, true, out, out_cap);
         *blob_len = ctx->pending.total_len;
-        if (out && out_cap >= ctx->pending.total_len) fetch_pending(ctx, out, out_cap);
+        if (ctx->pending.fetched) CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        else if (out && out_cap >= ctx->pending.total_len) fetch_pending(ctx, out, out_cap);
         else CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        phase_mark("fetched", ctx->stream);
+        phase_dump("mgard_compress");
     });
 }
 
@@ -536,7 +587,151 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
             coef = (double *)ctx->dbuf("coef", N * 8);
         }
         DecodeResult dr;
-        if (has_syms) dr = run_decode(ctx, hh, nullptr, coef, bin, dict, s);
+        phase_mark("start", s);
+        // Streamed decompress (host blob): the payload arrives in unit groups, each decoded as its
+        // bytes land, and the finest transition's correction -- which depends only on the finest
+        // coefficients (transform.py:342-345) -- follows slab by slab on the side stream.
+        const double *T0_pre = nullptr;
+        cudaEvent_t ev_pre = nullptr;
+        static const bool no_stream_dec = getenv("HPDR_NO_STREAM_DECODE") != nullptr;
+        bool streamed = !no_stream_dec && !dev_blob && has_syms && !hh.single && coef && pp && n_sym == N &&
+                        levels_of(dims) == (int)levels && (dtype == 0 || dtype == 1) && pp->host.L > 2 &&
+                        use_fused(*pp) && classify(blob_in) != MemKind::Device && hh.n_units >= 64 &&
+                        hh.total_bits >= (uint64_t)(32u << 20) && n_out <= N / 64;
+        std::vector<uint64_t> uoffs;
+        const uint64_t *oidx_h = (const uint64_t *)(blob + oidx_off);   // unaligned-safe reads below
+        if (streamed) {
+            int max_len = 0;
+            for (uint32_t k = 0; k < dict; k++) max_len = std::max<int>(max_len, hh.lengths[k]);
+            uoffs.resize(hh.n_units);
+            memcpy(uoffs.data(), hh.offsets, 8ull * hh.n_units);
+            streamed = max_len <= 32 && (uint64_t)hh.n_units * kBlockSymbols >= N;
+            for (uint64_t u = 0; u < hh.n_units && streamed; u++)
+                if (uoffs[u] > hh.total_bits || (u && uoffs[u] < uoffs[u - 1])) streamed = false;
+            uint64_t prev = 0;
+            for (uint64_t k = 0; k < n_out && streamed; k++) {
+                uint64_t i;
+                memcpy(&i, oidx_h + k, 8);
+                if (i >= N || (k && i <= prev)) streamed = false;
+                prev = i;
+            }
+        }
+        if (streamed) {
+            DevPlan &p = *pp;
+            const DevStep &st0 = p.steps[0];
+            DecodeJob job;
+            job.dict_size = hh.dict;
+            job.lengths = hh.lengths;
+            job.n_symbols = hh.n_sym;
+            job.n_units = (hh.n_sym + kBlockSymbols - 1) / kBlockSymbols;
+            job.offsets = hh.offsets;
+            job.total_bits = hh.total_bits;
+            job.packed = hh.packed;
+            job.coef = coef;
+            job.bin_width = bin;
+            job.key_limit = dict;
+            DecodeSession S;
+            decode_begin(ctx, job, S, s, false);
+            uint64_t *di = (uint64_t *)ctx->dbuf("dq_oidx", n_out * 8);
+            int64_t *db = (int64_t *)ctx->dbuf("dq_obins", n_out * 8);
+            int *fl = (int *)ctx->dbuf("dq_flags", 16);
+            if (n_out) {
+                CUDA_CHECK(cudaMemcpyAsync(di, blob + oidx_off, n_out * 8, cudaMemcpyDefault, s));
+                CUDA_CHECK(cudaMemcpyAsync(db, blob + obins_off, n_out * 8, cudaMemcpyDefault, s));
+            }
+            CUDA_CHECK(cudaMemsetAsync(fl, 0, 16, s));
+            const int64_t units = S.units;
+            const int64_t plane = st0.fsh.n[2] * st0.fsh.n[3];
+            const int n0 = (int)st0.fsh.n[1];
+            const int m0 = fused_out_planes(p, 0);
+            const AxisTables &ax0 = p.host.steps[0].ax[1];
+            auto ready = [&](int arrived) -> int {
+                if (arrived >= n0) return m0;
+                if (!ax0.active) return arrived;
+                int c = 0;
+                while (c < m0 && ax0.r0[c] + 2 < arrived) c++;
+                return c;
+            };
+            double *Z0f = (double *)ctx->dbuf("z0f", z0_elems(p, 0) * 8);
+            double *T0f = (double *)ctx->dbuf("t0f", st0.csh.size() * 8);
+            auto oidx_at = [&](uint64_t k) {
+                uint64_t i;
+                memcpy(&i, oidx_h + k, 8);
+                return i;
+            };
+            auto lower = [&](uint64_t key) {   // first outlier index >= key (the list is ascending)
+                uint64_t lo = 0, hi = n_out;
+                while (lo < hi) {
+                    const uint64_t mid = (lo + hi) / 2;
+                    if (oidx_at(mid) < key) lo = mid + 1;
+                    else hi = mid;
+                }
+                return lo;
+            };
+            static const int G = [] {
+                const char *e = getenv("HPDR_DEC_GROUPS");
+                return e ? std::max(1, std::min(32, atoi(e))) : 6;
+            }();
+            CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
+            CUDA_CHECK(cudaStreamWaitEvent(ctx->h2d, ctx->event(0), 0));   // tables / buffers ready
+            size_t copied = 0;
+            int c_done = 0;
+            for (int g = 0; g < G; g++) {
+                const int64_t ua = units * g / G, ub = units * (g + 1) / G;
+                if (ub <= ua) continue;
+                const size_t want = ub < units ? std::min<size_t>(S.pbytes, ((size_t)(uoffs[ub] / 8) + 64) & ~size_t(3))
+                                               : S.pbytes;
+                if (want > copied) {
+                    CUDA_CHECK(cudaMemcpyAsync((char *)S.d_words + copied, hh.packed + copied, want - copied,
+                                               cudaMemcpyHostToDevice, ctx->h2d));
+                    copied = want;
+                }
+                CUDA_CHECK(cudaEventRecord(ctx->event(100 + g), ctx->h2d));
+                phase_mark("h2d", ctx->h2d);
+                CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(100 + g), 0));
+                decode_units(S, ua, ub, true, s);
+                phase_mark("dec", s);
+                const uint64_t o_lo = lower((uint64_t)ua * kBlockSymbols);
+                const uint64_t o_hi = ub == units ? n_out : lower((uint64_t)ub * kBlockSymbols);
+                if (o_hi > o_lo) {
+                    k_outliers<<<grid_for(o_hi - o_lo, 256, 148 * 8), 256, 0, s>>>(coef, (int64_t)N, di + o_lo, db + o_lo,
+                                                                                 o_hi - o_lo, bin, fl);
+                    LAUNCH_CHECK();
+                }
+                const int planes_done = ub == units ? n0 : (int)std::min<int64_t>(n0, (ub * kBlockSymbols) / plane);
+                const int c_ready = ready(planes_done);
+                if (c_ready > c_done) {
+                    CUDA_CHECK(cudaEventRecord(ctx->event(140 + g), s));
+                    CUDA_CHECK(cudaStreamWaitEvent(ctx->aux, ctx->event(140 + g), 0));
+                    fused_pass1_recompose(p, 0, coef, Z0f, ctx->aux, c_done, c_ready);
+                    fused_pass2(p, 0, Z0f, T0f, ctx->aux, c_done, c_ready);
+                    phase_mark("corr", ctx->aux);
+                    c_done = c_ready;
+                }
+            }
+            decode_end(ctx, S, dr, s, true);
+            if (dr.bad_bit >= 0)
+                fail(HPDR_ERR_CORRUPT, "invalid or truncated codeword at bit " + std::to_string(dr.bad_bit), dr.bad_bit);
+            if (dr.deferred) {   // redone units were dequantized again: re-apply outliers, redo the correction
+                if (n_out) {
+                    k_outliers<<<grid_for(n_out, 256, 148 * 8), 256, 0, s>>>(coef, (int64_t)N, di, db, n_out, bin, fl);
+                    LAUNCH_CHECK();
+                }
+                CUDA_CHECK(cudaEventRecord(ctx->event(190), s));
+                CUDA_CHECK(cudaStreamWaitEvent(ctx->aux, ctx->event(190), 0));
+                fused_pass1_recompose(p, 0, coef, Z0f, ctx->aux);
+                fused_pass2(p, 0, Z0f, T0f, ctx->aux);
+            }
+            phase_mark("dec_end", s);
+            thomas_all(p, 0, T0f, ctx->aux);
+            phase_mark("thomas0", ctx->aux);
+            ev_pre = ctx->event(191);
+            CUDA_CHECK(cudaEventRecord(ev_pre, ctx->aux));
+            T0_pre = T0f;
+        } else if (has_syms) {
+            dr = run_decode(ctx, hh, nullptr, coef, bin, dict, s);
+        }
+        phase_mark("decoded", s);
         if (!dims_ok) bad_dims();
         if (levels_of(dims) != (int)levels) fail(HPDR_ERR_CORRUPT, "stored level count does not match dims");
         // dequantize (quantize.py:101-125)
@@ -548,19 +743,22 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
             fail(HPDR_ERR_VALIDATION, rank == 0 ? "dims must be non-empty" : "rank exceeds maximum 4");
         }
         DevPlan &p = *pp;
-        const uint8_t *bulk = dev_blob ? dev_blob : blob;
-        int rc = scatter_outliers(ctx, coef, (int64_t)N, (const uint64_t *)(bulk + oidx_off),
-                                  (const int64_t *)(bulk + obins_off), n_out, bin, s);
-        if (rc == HPDR_ERR_INDEX) fail(rc, "outlier index out of bounds for axis 0 with size " + std::to_string(N));
+        if (!streamed) {
+            const uint8_t *bulk = dev_blob ? dev_blob : blob;
+            int rc = scatter_outliers(ctx, coef, (int64_t)N, (const uint64_t *)(bulk + oidx_off),
+                                      (const int64_t *)(bulk + obins_off), n_out, bin, s);
+            if (rc == HPDR_ERR_INDEX) fail(rc, "outlier index out of bounds for axis 0 with size " + std::to_string(N));
+        }
         restore_coarse(ctx, coef, p, coarse.data(), n_co, s);
+        phase_mark("dequantized", s);
         // codec.py:112-113 recompose, then TensorData(dims, dtype, values.astype(dtype))
         const size_t ob = (size_t)N * itemsize(dtype);
         if (out_bytes < ob) fail(HPDR_ERR_BUFFER, "output buffer too small: need " + std::to_string(ob));
         if (classify(out) == MemKind::Device) {
-            recompose_into(ctx, p, coef, out, dtype, s);
+            recompose_into(ctx, p, coef, out, dtype, s, nullptr, T0_pre, ev_pre);
         } else {
             void *stage = ctx->dbuf("out_stage", ob);
-            recompose_into(ctx, p, coef, stage, dtype, s, out);
+            recompose_into(ctx, p, coef, stage, dtype, s, out, T0_pre, ev_pre);
         }
         if (sync) CUDA_CHECK(cudaStreamSynchronize(s));
     }
@@ -573,6 +771,8 @@ int hpdr_mgard_decompress(hpdr_ctx *ctx, const void *blob_in, uint64_t len, void
     return guard([&] {
         CUDA_CHECK(cudaSetDevice(ctx->device));
         decompress_core(ctx, blob_in, len, nullptr, out, out_bytes, true);
+        phase_mark("done", ctx->stream);
+        phase_dump("mgard_decompress");
     });
 }
 

@@ -21,7 +21,10 @@ constexpr int kNumSMs = 148;
 
 void set_error(int code, const std::string &msg, int64_t bit_offset = -1);
 void count_launch();
-void debug_sync(const char *where);   // HPDR_DEBUG_SYNC=1: device sync + check after every launch
+void debug_sync(const char *where);
+// HPDR_PHASES=1: CUDA-event phase marks on a stream, printed (ms since the first mark) by phase_dump.
+void phase_mark(const char *name, cudaStream_t s);
+void phase_dump(const char *title);   // HPDR_DEBUG_SYNC=1: device sync + check after every launch
 
 // Live per-kernel timing for bench.py: when enabled (hpdr_prof_enable), each scope records a
 // CUDA event pair on the launching stream plus the launch's algorithmic bytes.

@@ -28,6 +28,41 @@ void debug_sync(const char *where) {
     if (e != cudaSuccess) throw Error{HPDR_ERR_CUDA, std::string("kernel at ") + where + ": " + cudaGetErrorString(e), -1};
 }
 
+// ---- phase marks ----
+namespace {
+std::mutex g_ph_mu;
+std::vector<std::pair<const char *, cudaEvent_t>> g_ph;
+bool phases_on() {
+    static const bool on = getenv("HPDR_PHASES") != nullptr;
+    return on;
+}
+}  // namespace
+
+void phase_mark(const char *name, cudaStream_t s) {
+    if (!phases_on()) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    std::lock_guard<std::mutex> g(g_ph_mu);
+    g_ph.push_back({name, e});
+}
+
+void phase_dump(const char *title) {
+    if (!phases_on()) return;
+    std::lock_guard<std::mutex> g(g_ph_mu);
+    if (g_ph.empty()) return;
+    cudaDeviceSynchronize();
+    fprintf(stderr, "[phases] %s:", title);
+    for (auto &pe : g_ph) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, g_ph[0].second, pe.second);
+        fprintf(stderr, " %s=%.3f", pe.first, ms);
+    }
+    fprintf(stderr, "\n");
+    for (auto &pe : g_ph) cudaEventDestroy(pe.second);
+    g_ph.clear();
+}
+
 // ---- live kernel profiling ----
 namespace {
 struct ProfRec {
@@ -339,9 +374,14 @@ int hpdr_ctx_create(int device, hpdr_ctx **out) {
         CUDA_CHECK(cudaSetDevice(device));
         hpdr_ctx *c = new hpdr_ctx();
         c->device = device;
-        CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        // the level chain (critical path) outranks side work (aux) when both have blocks waiting
+        int lo_pri = 0, hi_pri = 0;
+        CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+        CUDA_CHECK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi_pri));
         CUDA_CHECK(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
         CUDA_CHECK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+        CUDA_CHECK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, lo_pri));
+        for (auto &x : c->side) CUDA_CHECK(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, hi_pri));
         *out = c;
         return HPDR_OK;
     } catch (const Error &e) {
@@ -371,6 +411,8 @@ void hpdr_ctx_destroy(hpdr_ctx *c) {
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->h2d);
     cudaStreamDestroy(c->d2h);
+    cudaStreamDestroy(c->aux);
+    for (auto x : c->side) cudaStreamDestroy(x);
     delete c;
 }
 

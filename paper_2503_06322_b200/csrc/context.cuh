@@ -63,6 +63,8 @@ struct hpdr_ctx {
     cudaStream_t stream = nullptr;    // compute
     cudaStream_t h2d = nullptr;       // copy engine 0
     cudaStream_t d2h = nullptr;       // copy engine 1
+    cudaStream_t aux = nullptr;       // side compute (work independent of the level chain)
+    cudaStream_t side[4] = {};        // more side streams (independent per-level corrections)
     uint64_t alloc_events = 0;
     std::map<std::string, hpdr::Buffer> dev;      // named device buffers (grow-only)
     std::map<std::string, hpdr::Buffer> pinned;   // named pinned host buffers (grow-only)
@@ -81,6 +83,7 @@ struct hpdr_ctx {
         bool single_key = false;
         bool huffman_only = false;
         int slot = 0;                    // which output buffer set holds the device parts
+        bool fetched = false;            // already streamed to the caller's buffer by compress
     } pending;
 
     // Compress outputs (outliers, unit offsets, packed words) live in one of two buffer sets so

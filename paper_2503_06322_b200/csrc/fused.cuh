@@ -38,7 +38,8 @@ void quantize_coarsest(const DevPlan &p, const double *coarsest_vals, const Quan
 void fused_pass1_decompose(const DevPlan &p, int st_i, const void *F, bool f32, double *coef, double *Z0,
                            double *Cg, cudaStream_t s, int c_lo = 0, int c_hi = -1);
 // Recompose transition st_i: mc gathered from coef (coarse nodes zero) -> axis-0 mass-transfer -> Z0.
-void fused_pass1_recompose(const DevPlan &p, int st_i, const double *coef, double *Z0, cudaStream_t s);
+void fused_pass1_recompose(const DevPlan &p, int st_i, const double *coef, double *Z0, cudaStream_t s, int c_lo = 0,
+                           int c_hi = -1);
 // Axis-1 and axis-2 mass-transfer: Z0 -> B (the coarse-grid right-hand side of the Thomas solves).
 void fused_pass2(const DevPlan &p, int st_i, const double *Z0, double *B, cudaStream_t s, int p_lo = 0,
                  int p_hi = -1);

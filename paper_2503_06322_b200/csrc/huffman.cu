@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const uint32_t *__restri
                                                         const uint32_t *__restrict__ codes, uint32_t dict,
                                                         const uint64_t *__restrict__ uoff,
                                                         const uint64_t *__restrict__ ubits,
-                                                        uint32_t *__restrict__ out, int64_t units) {
+                                                        uint32_t *__restrict__ out, int64_t u_lo, int64_t u_hi) {
     __shared__ uint32_t words[kBlockSymbols + 2];
     __shared__ uint8_t sl[kEncTableMax];
     __shared__ uint32_t sc[kEncTableMax];
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const uint32_t *__restri
         for (uint32_t k = threadIdx.x; k < dict; k += blockDim.x) { sl[k] = lens[k]; sc[k] = codes[k]; }
     typedef cub::BlockScan<unsigned, kEncThreads> BS;
     __shared__ typename BS::TempStorage tmp;
-    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int64_t u = u_lo + blockIdx.x; u < u_hi; u += gridDim.x) {
         for (int w = threadIdx.x; w < kBlockSymbols + 2; w += blockDim.x) words[w] = 0;
         __syncthreads();
         const int64_t lo = u * kBlockSymbols + (int64_t)threadIdx.x * kSymPerThread;
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const uint32_t *__restri
 }  // namespace
 
 void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict_size, const uint8_t *lengths,
-                   const uint32_t *codes, EncodeResult &res, cudaStream_t s) {
+                   const uint32_t *codes, EncodeResult &res, cudaStream_t s, const EncodeHooks *hooks) {
     const int64_t units = (n + kBlockSymbols - 1) / kBlockSymbols;
     res.n_units = units;
     uint8_t *d_len = (uint8_t *)ctx->dbuf("enc_len", dict_size + 16);
@@ -220,25 +220,42 @@ void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict
     void *tmp = ctx->dbuf("cub_tmp", tb);
     CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp, tb, ubits, uoff, (int)(units + 1), s));
     count_launch();
-    uint64_t *h = (uint64_t *)ctx->hbuf("enc_total", 16);
-    CUDA_CHECK(cudaMemcpyAsync(h, uoff + units, 8, cudaMemcpyDeviceToHost, s));
+    // unit groups: the encode runs in G launches so the caller can stream finished byte ranges out
+    const int G = hooks && hooks->groups > 1 ? (int)std::min<int64_t>(hooks->groups, std::max<int64_t>(1, units)) : 1;
+    std::vector<int64_t> ub(G + 1);
+    for (int g = 0; g <= G; g++) ub[g] = units * g / G;
+    uint64_t *h = (uint64_t *)ctx->hbuf("enc_total", 8 * (G + 2));
+    for (int g = 0; g <= G; g++) CUDA_CHECK(cudaMemcpyAsync(h + g, uoff + ub[g], 8, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
-    res.total_bits = h[0];
+    res.total_bits = h[G];
+    std::vector<uint64_t> gbit(h, h + G + 1);
     const size_t words = (size_t)((res.total_bits + 31) / 32) + 2;
     res.d_words = (uint32_t *)ctx->dbuf(ctx->oname("enc_words"), words * 4);
-    CUDA_CHECK(cudaMemsetAsync(res.d_words, 0, words * 4, s));
-    KPROF("k_encode", 4.0 * n + 16.0 * units + res.total_bits / 8.0, s);
-    k_encode<<<(unsigned)std::min<int64_t>(units, 148 * 8), kEncThreads, 0, s>>>(keys, n, d_len, d_code, dict_size, uoff,
-                                                                                  ubits, res.d_words, units);
-    LAUNCH_CHECK();
     res.d_offsets = uoff;
+    CUDA_CHECK(cudaMemsetAsync(res.d_words, 0, words * 4, s));
+    if (hooks && hooks->ready) hooks->ready(res);
+    const uint64_t pbytes = (res.total_bits + 7) / 8;
+    for (int g = 0; g < G; g++) {
+        const int64_t cnt = ub[g + 1] - ub[g];
+        if (cnt > 0) {
+            KPROF("k_encode", (4.0 * n + 16.0 * units + res.total_bits / 8.0) * ((double)cnt / (double)units), s);
+            k_encode<<<(unsigned)std::min<int64_t>(cnt, 148 * 8), kEncThreads, 0, s>>>(keys, n, d_len, d_code, dict_size,
+                                                                                      uoff, ubits, res.d_words, ub[g],
+                                                                                      ub[g + 1]);
+            LAUNCH_CHECK();
+        }
+        if (hooks && hooks->group_done) {
+            // bytes [lo, hi) are final: the word shared with the next group is left to that group
+            const uint64_t lo = (gbit[g] >> 5) * 4, hi = g + 1 < G ? std::min<uint64_t>((gbit[g + 1] >> 5) * 4, pbytes) : pbytes;
+            hooks->group_done(g, std::min(lo, hi), hi);
+        }
+    }
 }
 
 // ===================================================================== decode
 namespace {
 
 constexpr int kLutSize = 1 << kLutBits;
-constexpr int kDecThreads = 64;
 
 struct DecTables {
     long long first_code[258];
@@ -249,199 +266,6 @@ struct DecTables {
 
 __device__ __forceinline__ uint32_t load_be(const uint32_t *w, uint64_t i) {
     return __byte_perm(__ldg(w + i), 0, 0x0123);
-}
-
-// One thread per 4096-symbol unit, walking the canonical code (huffman.py:292-313).
-// Fast path (max_len <= 32): 12-bit table lookup, then canonical search on a 32-bit window.
-// Slow path (max_len > 32, only reachable with a corrupted length array): bit-serial walk
-// with numba's wrapping int64 arithmetic.
-__global__ void k_decode(const uint32_t *__restrict__ words, uint64_t limit, const uint64_t *__restrict__ offs,
-                         uint64_t nsym, int64_t units, const DecTables *__restrict__ tabs_g,
-                         const uint32_t *__restrict__ lut_g, const uint32_t *__restrict__ sym_by_rank,
-                         uint32_t *__restrict__ keys, double *__restrict__ coef, double bin, uint32_t key_limit,
-                         long long *__restrict__ unit_err, unsigned long long *__restrict__ first_bad,
-                         unsigned *__restrict__ max_key, int64_t u_base, uint64_t avail_words,
-                         uint64_t full_words, int *__restrict__ deferred, int redo) {
-    __shared__ uint32_t lut[kLutSize];
-    __shared__ DecTables T;
-    __shared__ uint32_t stage[kDecThreads][9];
-    for (int i = threadIdx.x; i < kLutSize; i += blockDim.x) lut[i] = lut_g[i];
-    for (int i = threadIdx.x; i < (int)(sizeof(DecTables) / 8); i += blockDim.x)
-        ((long long *)&T)[i] = ((const long long *)tabs_g)[i];
-    __syncthreads();
-    const int max_len = T.max_len;
-    unsigned kmax = 0;
-    for (int64_t uu = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; uu < units; uu += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t u = u_base + uu;
-        if (redo) {   // second pass: only units that outran the streamed prefix
-            if (!deferred[u]) continue;
-            deferred[u] = 0;
-        }
-        const uint64_t lo = (uint64_t)u * kBlockSymbols;
-        const uint64_t cnt = nsym - lo < (uint64_t)kBlockSymbols ? nsym - lo : (uint64_t)kBlockSymbols;
-        uint64_t pos = offs[u];
-        long long err = -1;
-        if (max_len <= 32 && pos < limit) {
-            // Fast path: 64-bit bit buffer refilled a word at a time (next word prefetched),
-            // 12-bit table lookup, canonical search for longer codes; 8 symbols per vector store.
-            // A unit that would read past the streamed prefix (avail_words) is deferred whole.
-            uint64_t wi = pos >> 5;
-            if (wi + 2 >= avail_words && avail_words < full_words) {
-                deferred[u] = 1;
-                continue;
-            }
-            uint64_t buf = (((uint64_t)load_be(words, wi) << 32) | load_be(words, wi + 1)) << (pos & 31);
-            int avail = 64 - (int)(pos & 31);
-            // raw words come in aligned 4-word groups: `cur` is being consumed while `nxt` is in
-            // flight (issued a whole group, ~24 symbols, before it is needed)
-            const uint64_t nw = wi + 2;
-            uint64_t g = nw >> 2;
-            int kq = (int)(nw & 3);
-            if (4 * (g + 2) > avail_words && avail_words < full_words) {
-                deferred[u] = 1;
-                continue;
-            }
-            const uint4 *w4 = reinterpret_cast<const uint4 *>(words);
-            uint4 cur = __ldg(w4 + g), nxt = __ldg(w4 + g + 1);
-            uint32_t *s8 = stage[threadIdx.x];   // private 8-symbol staging row
-            uint64_t i = 0;
-            for (; i < cnt; i++) {
-                if (avail < 32) {
-                    const uint32_t wv = kq == 0 ? cur.x : kq == 1 ? cur.y : kq == 2 ? cur.z : cur.w;
-                    buf |= (uint64_t)__byte_perm(wv, 0, 0x0123) << (32 - avail);
-                    avail += 32;
-                    if (++kq == 4) {
-                        kq = 0;
-                        g++;
-                        if (4 * (g + 2) > avail_words && avail_words < full_words) {
-                            err = -3;   // deferred: the unit needs bytes that have not landed yet
-                            break;
-                        }
-                        cur = nxt;
-                        nxt = __ldg(w4 + g + 1);
-                    }
-                }
-                if (pos >= limit) { err = (long long)pos; break; }
-                const uint32_t win = (uint32_t)(buf >> 32);
-                const uint32_t e = lut[win >> (32 - kLutBits)];
-                uint32_t sym = e >> 8;
-                int L = (int)(e & 0xffu);
-                if (!L) {
-                    for (int l = kLutBits + 1; l <= max_len; l++) {
-                        const long long idx = (long long)(win >> (32 - l)) - T.first_code[l];
-                        if (idx >= 0 && idx < T.cnt[l]) {
-                            L = l;
-                            sym = sym_by_rank[T.first_rank[l] + idx];
-                            break;
-                        }
-                    }
-                }
-                if (L == 0 || pos + (uint64_t)L > limit) { err = (long long)pos; break; }
-                pos += L;
-                buf <<= L;
-                avail -= L;
-                kmax = sym > kmax ? sym : kmax;
-                s8[i & 7] = sym;
-                if ((i & 7) == 7) {
-                    const uint64_t o = lo + i - 7;
-                    if (keys) {
-                        uint4 *kp = reinterpret_cast<uint4 *>(keys + o);
-                        kp[0] = make_uint4(s8[0], s8[1], s8[2], s8[3]);
-                        kp[1] = make_uint4(s8[4], s8[5], s8[6], s8[7]);
-                    }
-                    if (coef) {
-                        double2 *cp = reinterpret_cast<double2 *>(coef + o);
-#pragma unroll
-                        for (int k = 0; k < 4; k++) {
-                            const long long b0 = (long long)(s8[2 * k] >> 1) ^ -(long long)(s8[2 * k] & 1u);
-                            const long long b1 = (long long)(s8[2 * k + 1] >> 1) ^ -(long long)(s8[2 * k + 1] & 1u);
-                            cp[k] = make_double2(__dmul_rn((double)b0, bin), __dmul_rn((double)b1, bin));
-                        }
-                    }
-                }
-            }
-            if (err == -3) {
-                deferred[u] = 1;
-                continue;
-            }
-            if (err < 0) {   // tail of the last (partial) unit
-                for (uint64_t k = cnt & ~7ULL; k < cnt; k++) {
-                    const uint32_t sym = s8[k & 7];
-                    if (keys) keys[lo + k] = sym;
-                    if (coef) {
-                        const long long b = (long long)(sym >> 1) ^ -(long long)(sym & 1u);
-                        coef[lo + k] = __dmul_rn((double)b, bin);
-                    }
-                }
-            }
-            if (err >= 0) {
-                unit_err[u] = err;
-                atomicMin(first_bad, (unsigned long long)u);
-            }
-            continue;
-        }
-        for (uint64_t i = 0; i < cnt; i++) {
-            const uint64_t cw = pos;
-            uint32_t sym = 0;
-            int L = 0;
-            if (max_len <= 32) {
-                if (pos >= limit) { err = (long long)cw; break; }
-                const uint64_t wi = pos >> 5;
-                const int sh = (int)(pos & 31);
-                const uint64_t win64 = ((uint64_t)load_be(words, wi) << 32) | load_be(words, wi + 1);
-                const uint32_t win = (uint32_t)((win64 << sh) >> 32);
-                const uint32_t e = lut[win >> (32 - kLutBits)];
-                if (e & 0xffu) {
-                    L = (int)(e & 0xffu);
-                    sym = e >> 8;
-                } else {
-                    for (int l = kLutBits + 1; l <= max_len; l++) {
-                        const long long code = (long long)(win >> (32 - l));
-                        const long long idx = code - T.first_code[l];
-                        if (idx >= 0 && idx < T.cnt[l]) {
-                            L = l;
-                            sym = sym_by_rank[T.first_rank[l] + idx];
-                            break;
-                        }
-                    }
-                }
-                if (L == 0 || pos + (uint64_t)L > limit) { err = (long long)cw; break; }
-                pos += L;
-            } else {
-                unsigned long long code = 0;
-                int len = 0;
-                bool ok = false;
-                for (;;) {
-                    if (pos >= limit || len >= max_len) break;
-                    const uint32_t word = load_be(words, pos >> 5);
-                    const unsigned long long bit = (word >> (31 - (pos & 31))) & 1u;
-                    code = (code << 1) | bit;
-                    pos++;
-                    len++;
-                    const long long idx = (long long)(code - (unsigned long long)T.first_code[len]);
-                    if (idx >= 0 && idx < T.cnt[len]) {
-                        sym = sym_by_rank[T.first_rank[len] + idx];
-                        ok = true;
-                        break;
-                    }
-                }
-                if (!ok) { err = (long long)cw; break; }
-            }
-            kmax = sym > kmax ? sym : kmax;
-            if (keys) keys[lo + i] = sym;
-            if (coef) {
-                const long long b = (long long)(sym >> 1) ^ -(long long)(sym & 1u);   // unzigzag
-                coef[lo + i] = __dmul_rn((double)b, bin);                            // quantize.py:111
-            }
-        }
-        if (err >= 0) {
-            unit_err[u] = err;
-            atomicMin(first_bad, (unsigned long long)u);
-        }
-    }
-    for (int o = 16; o; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-    if ((threadIdx.x & 31) == 0 && kmax) atomicMax(max_key, kmax);
-    (void)key_limit;
 }
 
 // ---------------------------------------------------------------- warp-cooperative decode
@@ -694,7 +518,7 @@ __global__ void __launch_bounds__(kDWWarps * 32) k_decode_warp(
     int64_t units, const DecTables *__restrict__ tabs_g, const uint32_t *__restrict__ lut_g,
     const uint32_t *__restrict__ sym_by_rank, uint32_t *__restrict__ keys, double *__restrict__ coef, double bin,
     long long *__restrict__ unit_err, unsigned long long *__restrict__ first_bad, unsigned *__restrict__ max_key,
-    unsigned long long *__restrict__ stats) {
+    unsigned long long *__restrict__ stats, int64_t u_lo, int64_t u_hi, int *__restrict__ deferred, int redo) {
     extern __shared__ __align__(16) unsigned char dw_smem[];
     uint32_t *lut = (uint32_t *)dw_smem;
     DecTables &T = *(DecTables *)(dw_smem + kLutSize * 4);
@@ -710,12 +534,13 @@ __global__ void __launch_bounds__(kDWWarps * 32) k_decode_warp(
     const int max_len = T.max_len;
     unsigned kmax = 0;
     const int64_t wstride = (int64_t)gridDim.x * kDWWarps;
-    for (int64_t u = blockIdx.x * (int64_t)kDWWarps + wid; u < units; u += wstride) {
+    for (int64_t u = u_lo + blockIdx.x * (int64_t)kDWWarps + wid; u < u_hi; u += wstride) {
+        if (redo && !deferred[u]) continue;   // redo pass: only units deferred by a streamed pass
         const uint64_t lo = (uint64_t)u * kBlockSymbols;
         const uint64_t cnt = nsym - lo < (uint64_t)kBlockSymbols ? nsym - lo : (uint64_t)kBlockSymbols;
         const uint64_t S = __ldg(offs + u);
         const uint64_t E = u + 1 < units ? __ldg(offs + u + 1) : limit;
-        bool fast = max_len <= 32 && S < limit && S <= E && E <= limit && E - S <= cnt * (uint64_t)max_len;
+        bool fast = !redo && max_len <= 32 && S < limit && S <= E && E <= limit && E - S <= cnt * (uint64_t)max_len;
         if (fast) {
             const int64_t w0 = (int64_t)(S >> 5), nw = (int64_t)(E >> 5) + 4 - w0;
             if (nw <= kDWWords) {
@@ -729,7 +554,12 @@ __global__ void __launch_bounds__(kDWWarps * 32) k_decode_warp(
                 if (stats && lane == 0) atomicAdd(stats + 2, 1ULL);
             }
         }
-        if (!fast) {
+        if (!fast && deferred && !redo) {   // streamed pass: the walk may need bytes not landed yet
+            if (lane == 0) {
+                deferred[u] = 1;
+                atomicAdd(first_bad + 2, 1ULL);   // deferred-unit count (flag[2])
+            }
+        } else if (!fast) {
             long long err = -1;
             if (stats && lane == 0) atomicAdd(stats, 1ULL);
             if (lane == 0) {
@@ -755,7 +585,7 @@ __global__ void k_fill(uint32_t *keys, double *coef, int64_t n, uint32_t sym, do
 
 }  // namespace
 
-void decode_device(hpdr_ctx *ctx, const DecodeJob &job, DecodeResult &res, cudaStream_t s) {
+void decode_begin(hpdr_ctx *ctx, const DecodeJob &job, DecodeSession &S, cudaStream_t s, bool copy_payload) {
     // _decode_tables (huffman.py:207-225) and the 12-bit lookup table
     const uint32_t dict = job.dict_size;
     std::vector<uint32_t> present;
@@ -800,113 +630,79 @@ void decode_device(hpdr_ctx *ctx, const DecodeJob &job, DecodeResult &res, cudaS
     char *d_tab = (char *)ctx->dbuf("dec_tabs", tab_bytes);
     CUDA_CHECK(cudaMemcpyAsync(d_tab, T, tab_bytes, cudaMemcpyHostToDevice, s));
 
-    const int64_t units = (int64_t)job.n_units;
-    uint64_t *d_off = (uint64_t *)ctx->dbuf("dec_off", (units + 1) * 8);
-    CUDA_CHECK(cudaMemcpyAsync(d_off, job.offsets, units * 8, cudaMemcpyHostToDevice, s));
-    const size_t pbytes = (size_t)((job.total_bits + 7) / 8);
-    const size_t pwords = ((pbytes / 4 + 12) & ~size_t(3));   // 4-word groups read up to 2 groups ahead
-    uint32_t *d_words = (uint32_t *)ctx->dbuf("dec_words", pwords * 4);
-    CUDA_CHECK(cudaMemsetAsync((char *)d_words + (pbytes & ~size_t(3)), 0, pwords * 4 - (pbytes & ~size_t(3)), s));
-    long long *uerr = (long long *)ctx->dbuf("dec_err", (units + 1) * 8);
-    unsigned long long *flag = (unsigned long long *)ctx->dbuf("dec_flag", 32);
-    int *deferred = (int *)ctx->dbuf("dec_defer", (units + 1) * 4);
-    CUDA_CHECK(cudaMemsetAsync(deferred, 0, (units + 1) * 4, s));
-    unsigned long long init[2] = {~0ULL, 0ULL};
+    S.job = job;
+    S.max_len = max_len;
+    S.d_tab = d_tab;
+    S.units = (int64_t)job.n_units;
+    const int64_t units = S.units;
+    S.d_off = (uint64_t *)ctx->dbuf("dec_off", (units + 1) * 8);
+    CUDA_CHECK(cudaMemcpyAsync(S.d_off, job.offsets, units * 8, cudaMemcpyHostToDevice, s));
+    S.pbytes = (size_t)((job.total_bits + 7) / 8);
+    S.pwords = ((S.pbytes / 4 + 12) & ~size_t(3));   // zero-padded tail words
+    S.d_words = (uint32_t *)ctx->dbuf("dec_words", S.pwords * 4);
+    CUDA_CHECK(cudaMemsetAsync((char *)S.d_words + (S.pbytes & ~size_t(3)), 0, S.pwords * 4 - (S.pbytes & ~size_t(3)), s));
+    S.uerr = (long long *)ctx->dbuf("dec_err", (units + 1) * 8);
+    S.flag = (unsigned long long *)ctx->dbuf("dec_flag", 32);
+    S.deferred = (int *)ctx->dbuf("dec_defer", (units + 1) * 4);
+    CUDA_CHECK(cudaMemsetAsync(S.deferred, 0, (units + 1) * 4, s));
+    unsigned long long init[4] = {~0ULL, 0ULL, 0ULL, 0ULL};
     unsigned long long *hinit = (unsigned long long *)ctx->hbuf("dec_init", 64);
-    memcpy(hinit, init, 16);
-    CUDA_CHECK(cudaMemcpyAsync(flag, hinit, 16, cudaMemcpyHostToDevice, s));
-    // Stream the payload in unit groups when it comes from the host: each group decodes as soon
-    // as its bytes (plus a small margin) have landed; units that outrun the prefix are redone.
-    std::vector<uint64_t> off;
-    // (off by default: the decode is bound by each unit's sequential walk, so splitting it into
-    // serialized launches costs more than the H2D it hides; HPDR_STREAM_DECODE=1 enables it)
-    static const bool want_stream = getenv("HPDR_STREAM_DECODE") != nullptr;
-    bool stream = want_stream && !job.packed_on_device && max_len <= 32 && units >= 256 &&
-                  pbytes >= (size_t(8) << 20);
-    if (stream) {
-        off.resize(units);
-        memcpy(off.data(), job.offsets, units * 8);
-        for (int64_t u = 0; u < units && stream; u++)
-            if (off[u] > job.total_bits || (u && off[u] < off[u - 1])) stream = false;
+    memcpy(hinit, init, 32);
+    CUDA_CHECK(cudaMemcpyAsync(S.flag, hinit, 32, cudaMemcpyHostToDevice, s));
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(k_decode_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dw_smem_bytes()));
+        attr = true;
     }
-    auto launch = [&](int64_t ub, int64_t cnt, uint64_t avail_words, int redo) {
-        k_decode<<<grid_for(cnt, kDecThreads, 148 * 64), kDecThreads, 0, s>>>(
-            d_words, job.total_bits, d_off, job.n_symbols, cnt, (const DecTables *)d_tab,
-            (const uint32_t *)(d_tab + sizeof(DecTables)),
-            (const uint32_t *)(d_tab + sizeof(DecTables) + kLutSize * 4), job.keys, job.coef, job.bin_width,
-            job.key_limit, uerr, flag, (unsigned *)(flag + 1), ub, avail_words, (uint64_t)pwords, deferred, redo);
-        LAUNCH_CHECK();
-    };
-    if (units > 0) {
-        static const bool thread_decode = getenv("HPDR_DECODE_THREAD") != nullptr;
-        if (!stream && !thread_decode) {
-            CUDA_CHECK(cudaMemcpyAsync(d_words, job.packed, pbytes, cudaMemcpyDefault, s));
-            KPROF("k_decode", job.total_bits / 8.0 + 8.0 * units +
-                                  (double)job.n_symbols * ((job.keys ? 4 : 0) + (job.coef ? 8 : 0)), s);
-            static const bool want_stats = getenv("HPDR_DECODE_STATS") != nullptr;
-            unsigned long long *dstats = nullptr;
-            if (want_stats) {
-                dstats = (unsigned long long *)ctx->dbuf("dec_stats", 32);
-                CUDA_CHECK(cudaMemsetAsync(dstats, 0, 32, s));
-            }
-            static bool attr = false;
-            if (!attr) {
-                CUDA_CHECK(cudaFuncSetAttribute(k_decode_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)dw_smem_bytes()));
-                attr = true;
-            }
-            const unsigned blocks = (unsigned)std::min<int64_t>((units + kDWWarps - 1) / kDWWarps, 148 * 3);
-            k_decode_warp<<<blocks, kDWWarps * 32, dw_smem_bytes(), s>>>(
-                d_words, job.total_bits, d_off, job.n_symbols, units, (const DecTables *)d_tab,
-                (const uint32_t *)(d_tab + sizeof(DecTables)),
-                (const uint32_t *)(d_tab + sizeof(DecTables) + kLutSize * 4), job.keys, job.coef, job.bin_width, uerr,
-                flag, (unsigned *)(flag + 1), dstats);
-            LAUNCH_CHECK();
-            if (dstats) {
-                unsigned long long hs[4];
-                CUDA_CHECK(cudaMemcpyAsync(hs, dstats, 32, cudaMemcpyDeviceToHost, s));
-                CUDA_CHECK(cudaStreamSynchronize(s));
-                fprintf(stderr, "[decode] units %lld fallback %llu rounds %llu global-path %llu\n", (long long)units,
-                        hs[0], hs[1], hs[2]);
-            }
-        } else if (!stream) {
-            CUDA_CHECK(cudaMemcpyAsync(d_words, job.packed, pbytes, cudaMemcpyDefault, s));
-            KPROF("k_decode", job.total_bits / 8.0 + 8.0 * units +
-                                  (double)job.n_symbols * ((job.keys ? 4 : 0) + (job.coef ? 8 : 0)), s);
-            launch(0, units, pwords, 0);
-        } else {
-            const int G = 16;
-            size_t copied = 0;
-            CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
-            CUDA_CHECK(cudaStreamWaitEvent(ctx->h2d, ctx->event(0), 0));
-            for (int g = 0; g < G; g++) {
-                const int64_t ua = units * g / G, ub = units * (g + 1) / G;
-                if (ub <= ua) continue;
-                size_t want = pbytes;
-                if (ub < units) want = std::min<size_t>(pbytes, ((size_t)(off[ub] / 8) + 64) & ~size_t(3));
-                if (want > copied) {
-                    CUDA_CHECK(cudaMemcpyAsync((char *)d_words + copied, job.packed + copied, want - copied,
-                                               cudaMemcpyHostToDevice, ctx->h2d));
-                    copied = want;
-                }
-                CUDA_CHECK(cudaEventRecord(ctx->event(1 + g), ctx->h2d));
-                CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(1 + g), 0));
-                launch(ua, ub - ua, copied == pbytes ? (uint64_t)pwords : (uint64_t)(copied / 4), 0);
-            }
-            launch(0, units, pwords, 1);   // units that needed bytes beyond their group's prefix
-        }
+    static const bool want_stats = getenv("HPDR_DECODE_STATS") != nullptr;
+    S.stats = nullptr;
+    if (want_stats) {
+        S.stats = (unsigned long long *)ctx->dbuf("dec_stats", 32);
+        CUDA_CHECK(cudaMemsetAsync(S.stats, 0, 32, s));
     }
-    unsigned long long *h = (unsigned long long *)ctx->hbuf("dec_rb", 32);
-    CUDA_CHECK(cudaMemcpyAsync(h, flag, 16, cudaMemcpyDeviceToHost, s));
+    if (copy_payload && units > 0)
+        CUDA_CHECK(cudaMemcpyAsync(S.d_words, job.packed, S.pbytes, cudaMemcpyDefault, s));
+}
+
+void decode_units(const DecodeSession &S, int64_t u_lo, int64_t u_hi, bool streamed, cudaStream_t s, int redo) {
+    if (u_hi <= u_lo) return;
+    const DecodeJob &job = S.job;
+    KPROF("k_decode", (job.total_bits / 8.0 + 8.0 * S.units +
+                       (double)job.n_symbols * ((job.keys ? 4 : 0) + (job.coef ? 8 : 0))) *
+                          ((double)(u_hi - u_lo) / (double)S.units), s);
+    const unsigned blocks = (unsigned)std::min<int64_t>((u_hi - u_lo + kDWWarps - 1) / kDWWarps, 148 * 3);
+    k_decode_warp<<<blocks, kDWWarps * 32, dw_smem_bytes(), s>>>(
+        S.d_words, job.total_bits, S.d_off, job.n_symbols, S.units, (const DecTables *)S.d_tab,
+        (const uint32_t *)(S.d_tab + sizeof(DecTables)), (const uint32_t *)(S.d_tab + sizeof(DecTables) + kLutSize * 4),
+        job.keys, job.coef, job.bin_width, S.uerr, S.flag, (unsigned *)(S.flag + 1), S.stats, u_lo, u_hi,
+        (streamed || redo) ? S.deferred : nullptr, redo);
+    LAUNCH_CHECK();
+}
+
+void decode_end(hpdr_ctx *ctx, const DecodeSession &S, DecodeResult &res, cudaStream_t s, bool streamed) {
+    if (streamed) decode_units(S, 0, S.units, false, s, 1);   // deferred units, now with every byte present
+    unsigned long long *h = (unsigned long long *)ctx->hbuf("dec_rb", 64);
+    CUDA_CHECK(cudaMemcpyAsync(h, S.flag, 24, cudaMemcpyDeviceToHost, s));
+    if (S.stats) CUDA_CHECK(cudaMemcpyAsync(h + 4, S.stats, 16, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
+    if (S.stats) fprintf(stderr, "[decode] units %lld fallback %llu rounds %llu deferred %llu\n", (long long)S.units, h[4],
+                         h[5], h[2]);
+    res.deferred = h[2];
     res.bad_bit = -1;
     if (h[0] != ~0ULL) {
         long long b;
-        CUDA_CHECK(cudaMemcpy(&b, uerr + h[0], 8, cudaMemcpyDeviceToHost));
+        CUDA_CHECK(cudaMemcpy(&b, S.uerr + h[0], 8, cudaMemcpyDeviceToHost));
         res.bad_bit = b;
     }
     res.max_key = (uint32_t)h[1];
-    res.key_out_of_range = res.max_key >= job.key_limit;
+    res.key_out_of_range = res.max_key >= S.job.key_limit;
+}
+
+void decode_device(hpdr_ctx *ctx, const DecodeJob &job, DecodeResult &res, cudaStream_t s) {
+    DecodeSession S;
+    decode_begin(ctx, job, S, s, true);
+    decode_units(S, 0, S.units, false, s, 0);
+    decode_end(ctx, S, res, s, false);
 }
 
 void fill_single(uint32_t *keys, double *coef, int64_t n, uint32_t sym, double bin_width, cudaStream_t s) {

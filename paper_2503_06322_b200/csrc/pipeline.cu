@@ -26,7 +26,8 @@
 namespace hpdr {
 
 void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, double eb_rel,
-                   uint32_t dict_size, int has_range, double range_min, double range_max, bool allow_stream);
+                   uint32_t dict_size, int has_range, double range_min, double range_max, bool allow_stream,
+                   void *fetch_out = nullptr, uint64_t fetch_cap = 0);
 void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uint8_t *dev_blob, void *out,
                      uint64_t out_bytes, bool sync);
 void fetch_pending_on(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uint64_t cap, cudaStream_t s, bool sync);
@@ -256,7 +257,7 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
             CUDA_CHECK(cudaStreamWaitEvent(c->d2h, ctx->event(0), 0));
             c->out_slot = 0;
             char *din = (char *)c->dbuf("pipe_in", cbytes);
-            cudaEvent_t ev_in = c->event(1), ev_red = c->event(2), ev_out = c->event(3);
+            cudaEvent_t ev_in = c->event(300), ev_red = c->event(301), ev_out = c->event(302);   // ids reserved for the runner
             bool first = true;
             for (uint64_t k = q; k < K; k += Q) {
                 if (R.failed) return;
@@ -379,7 +380,7 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
             CUDA_CHECK(cudaStreamWaitEvent(x->d2h, ctx->event(0), 0));
             uint8_t *dblob = (uint8_t *)x->dbuf("pipe_blob", maxpay);
             char *dout = host_out ? (char *)x->dbuf("pipe_out", maxraw * isz) : nullptr;
-            cudaEvent_t ev_in = x->event(1), ev_red = x->event(2), ev_out = x->event(3);
+            cudaEvent_t ev_in = x->event(300), ev_red = x->event(301), ev_out = x->event(302);
             bool first = true;
             for (uint64_t k = q; k < K; k += Q) {
                 if (R.failed) return;

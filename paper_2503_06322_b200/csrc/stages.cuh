@@ -1,6 +1,8 @@
 // stages.cuh -- quantization and Huffman stages (device), plus the host codebook.
 #pragma once
 
+#include <functional>
+
 #include <vector>
 
 #include "context.cuh"
@@ -44,8 +46,16 @@ struct EncodeResult {
     uint64_t *d_offsets = nullptr;    // n_units unit bit offsets (device)
     uint32_t *d_words = nullptr;      // packed stream, MSB-first bytes (device)
 };
+// Optional hooks: ready(res) once offsets / total_bits are known (before the packing kernels);
+// group_done(g, lo, hi) after unit group g's packing launch, bytes [lo, hi) of the packed stream
+// are then final in stream order.
+struct EncodeHooks {
+    int groups = 1;
+    std::function<void(const EncodeResult &)> ready;
+    std::function<void(int, uint64_t, uint64_t)> group_done;
+};
 void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict_size, const uint8_t *lengths,
-                   const uint32_t *codes, EncodeResult &res, cudaStream_t s);
+                   const uint32_t *codes, EncodeResult &res, cudaStream_t s, const EncodeHooks *hooks = nullptr);
 
 // ---- huffman.py:207-358 (device) ---------------------------------------------------
 struct DecodeJob {
@@ -67,8 +77,30 @@ struct DecodeResult {
     int64_t bad_bit = -1;        // CorruptStreamError bit offset of the lowest failing unit
     bool key_out_of_range = false;
     uint32_t max_key = 0;
+    uint64_t deferred = 0;       // units a streamed pass deferred to the final redo
 };
 void decode_device(hpdr_ctx *ctx, const DecodeJob &job, DecodeResult &res, cudaStream_t s);
+
+// The decode as a session, for streaming the payload in: begin (tables, offsets; payload copy
+// unless the caller streams it into d_words), launches over unit ranges (streamed: a unit whose
+// canonical walk fails is deferred, not walked, as its bytes may not have landed), end (redo of
+// deferred units with the whole payload present, error / max-key readback).
+struct DecodeSession {
+    DecodeJob job;
+    int max_len = 0;
+    const char *d_tab = nullptr;
+    int64_t units = 0;
+    uint64_t *d_off = nullptr;
+    uint32_t *d_words = nullptr;
+    size_t pbytes = 0, pwords = 0;
+    long long *uerr = nullptr;
+    unsigned long long *flag = nullptr;
+    int *deferred = nullptr;
+    unsigned long long *stats = nullptr;
+};
+void decode_begin(hpdr_ctx *ctx, const DecodeJob &job, DecodeSession &S, cudaStream_t s, bool copy_payload);
+void decode_units(const DecodeSession &S, int64_t u_lo, int64_t u_hi, bool streamed, cudaStream_t s, int redo = 0);
+void decode_end(hpdr_ctx *ctx, const DecodeSession &S, DecodeResult &res, cudaStream_t s, bool streamed);
 
 // Fill n keys / coefficients with one symbol (single-key stream, huffman.py:423-426).
 void fill_single(uint32_t *keys, double *coef, int64_t n, uint32_t sym, double bin_width, cudaStream_t s);

@@ -426,49 +426,52 @@ __global__ void __launch_bounds__(32) k_thomas_tile(double *__restrict__ arr, in
         cp_async_wait<0>();
         __syncwarp();
         if (lane < nl) {
-            // forward elimination: x_i -= w_i x_{i-1}
+            // forward elimination x_i -= w_i x_{i-1}, 8 values per batch read ahead of the chain
+            constexpr int U = 8;
             double prev = at(lane, 0);
-            for (int i = 1; i < n; i++) {
-                const double v = dsub(at(lane, i), dmul(__ldg(tw + i), prev));
-                at(lane, i) = v;
-                prev = v;
+            int i0 = 1;
+            for (; i0 + U <= n; i0 += U) {
+                double v[U], w[U];
+#pragma unroll
+                for (int k = 0; k < U; k++) {
+                    v[k] = at(lane, i0 + k);
+                    w[k] = __ldg(tw + i0 + k);
+                }
+#pragma unroll
+                for (int k = 0; k < U; k++) {
+                    prev = dsub(v[k], dmul(w[k], prev));
+                    v[k] = prev;
+                }
+#pragma unroll
+                for (int k = 0; k < U; k++) at(lane, i0 + k) = v[k];
+            }
+            for (; i0 < n; i0++) {
+                prev = dsub(at(lane, i0), dmul(__ldg(tw + i0), prev));
+                at(lane, i0) = prev;
             }
             // back substitution: x_{n-1} /= b'_{n-1}; x_i = (x_i - u_i x_{i+1}) / b'_i
-            bool bad = false;
-            double last = div_fast(prev, __ldg(tb + n - 1), __ldg(tr + n - 1), bad);
+            double last = ddiv(prev, __ldg(tb + n - 1));
             at(lane, n - 1) = last;
-            for (int i = n - 2; i >= 0; i--) {
-                const double v = dsub(at(lane, i), dmul(__ldg(tu + i), last));
-                last = div_fast(v, __ldg(tb + i), __ldg(tr + i), bad);
-                at(lane, i) = last;
+            int i1 = n - 2;
+            for (; i1 - U + 1 >= 0; i1 -= U) {
+                double v[U], u[U], b[U];
+#pragma unroll
+                for (int k = 0; k < U; k++) {
+                    v[k] = at(lane, i1 - k);
+                    u[k] = __ldg(tu + i1 - k);
+                    b[k] = __ldg(tb + i1 - k);
+                }
+#pragma unroll
+                for (int k = 0; k < U; k++) {
+                    last = ddiv(dsub(v[k], dmul(u[k], last)), b[k]);
+                    v[k] = last;
+                }
+#pragma unroll
+                for (int k = 0; k < U; k++) at(lane, i1 - k) = v[k];
             }
-            if (bad) {   // rare: redo this line from its forward values with __ddiv_rn
-                if (CONTIG) {
-                    const double *src = arr + (l0 + lane) * (int64_t)n;
-                    prev = src[0];
-                    at(lane, 0) = prev;
-                    for (int i = 1; i < n; i++) {
-                        const double v = dsub(src[i], dmul(__ldg(tw + i), prev));
-                        at(lane, i) = v;
-                        prev = v;
-                    }
-                } else {
-                    const double *src = arr + p * (int64_t)n * inner + q0 + lane;
-                    prev = src[0];
-                    at(lane, 0) = prev;
-                    for (int i = 1; i < n; i++) {
-                        const double v = dsub(src[(int64_t)i * inner], dmul(__ldg(tw + i), prev));
-                        at(lane, i) = v;
-                        prev = v;
-                    }
-                }
-                last = ddiv(prev, __ldg(tb + n - 1));
-                at(lane, n - 1) = last;
-                for (int i = n - 2; i >= 0; i--) {
-                    const double v = dsub(at(lane, i), dmul(__ldg(tu + i), last));
-                    last = ddiv(v, __ldg(tb + i));
-                    at(lane, i) = last;
-                }
+            for (; i1 >= 0; i1--) {
+                last = ddiv(dsub(at(lane, i1), dmul(__ldg(tu + i1), last)), __ldg(tb + i1));
+                at(lane, i1) = last;
             }
         }
         __syncwarp();
@@ -582,8 +585,12 @@ void thomas(double *arr, const Shape4 &csh, int a, const DevAxis &ax, cudaStream
     // strided axes: register-blocked lines (coalesced across threads); contiguous axis: the
     // warp-tile transpose kernel measured faster (0.39 vs 0.45 ms at 257^3 coarse grid)
     static const bool legacy = getenv("HPDR_THOMAS_LEGACY") != nullptr;
-    static const bool tile = getenv("HPDR_THOMAS_TILE") != nullptr;
-    if (!legacy && tile && ax.nc <= kThomasTileMaxN) {
+    static const int tile_mode = [] {   // HPDR_THOMAS_TILE: 0 never, 1 always, unset: few lines only
+        const char *e = getenv("HPDR_THOMAS_TILE");
+        return e ? atoi(e) : 2;
+    }();
+    const bool few = outer * inner < (int64_t)148 * 128;
+    if (!legacy && (tile_mode == 1 || (tile_mode == 2 && few)) && ax.nc <= kThomasTileMaxN) {
         const int n = ax.nc;
         if (inner == 1) {
             const int ls = n | 1;   // odd row stride: lane-per-line reads hit distinct banks
@@ -836,6 +843,8 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
         }
         if (k + 1 < K) issue(k + 1);
     }
+    phase_mark("last_chunk_issued", s);
+    bool side = false;
     if (has_range) {
         *u_min = range_min;
         *u_max = range_max;
@@ -853,8 +862,15 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
         *u_max = h[2] ? __builtin_nan("") : val(h[1]);
         const double eb_abs = eb_rel * (*u_max - *u_min);
         q.bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
-        quantize_fine(p, coef, q, s);
+        // the fine coefficients are final: quantize them on the side stream while the level chain
+        // (IPK, coarser levels) runs; writes touch disjoint keys and commute (atomic mask / hist)
+        CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
+        CUDA_CHECK(cudaStreamWaitEvent(ctx->aux, ctx->event(0), 0));
+        quantize_fine(p, coef, q, ctx->aux);
+        CUDA_CHECK(cudaEventRecord(ctx->event(1), ctx->aux));
+        side = true;
     }
+    phase_mark("fine_quantized", s);
     // the rest of transition 0 (IPK + coarse update) and the coarser levels
     {
         Shape4 sh = st0.csh;
@@ -877,8 +893,10 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
         k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, level_ptr(b, p, st_i + 1), nc);
         LAUNCH_CHECK();
     }
+    phase_mark("levels_done", s);
     const double *DL = level_ptr(b, p, L - 1);
     quantize_coarsest(p, DL, q, s);
+    if (side) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(1), 0));
     return DL;
 }
 
@@ -983,8 +1001,20 @@ double *recompose_device(hpdr_ctx *ctx, DevPlan &p, const double *coef, cudaStre
     return b.lvl0;
 }
 
+int64_t z0_elems(const DevPlan &p, int st_i) {
+    const DevStep &st = p.steps[st_i];
+    return (int64_t)(st.ax[1].active ? st.csh.n[1] : st.fsh.n[1]) * st.fsh.n[2] * st.fsh.n[3];
+}
+
+void thomas_all(const DevPlan &p, int st_i, double *T, cudaStream_t s) {
+    const DevStep &st = p.steps[st_i];
+    Shape4 sh = st.csh;
+    for (int a = 0; a < 4; a++)
+        if (st.ax[a].active) thomas(T, sh, a, st.ax[a], s);
+}
+
 void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s,
-                    void *host_out) {
+                    void *host_out, const double *T0_pre, cudaEvent_t ev_pre) {
     const int L = p.host.L;
     if (L == 1 || !use_fused(p)) {
         const double *rec = recompose_device(ctx, p, coef, s);
@@ -1005,20 +1035,81 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
     k_gather_level<<<rows_grid(shL), 256, 0, s>>>(coef, p.dims, level_map(p, L - 1), none, level_ptr(b, p, L - 1),
                                                   shL, 0);
     LAUNCH_CHECK();
+    // A level's correction depends only on its own coefficients (transform.py:342-345), so the
+    // finest one -- the bulk of the correction work -- runs on the side stream while the coarser
+    // levels are recomposed; only coarse - corr of the finest transition waits for it.
+    const double *T0f = b.t0;
+    const bool side = L > 2;
+    cudaEvent_t ev_side = ctx->event(1);
+    if (side && T0_pre) {
+        T0f = T0_pre;
+        ev_side = ev_pre;
+    } else if (side) {
+        const DevStep &st = p.steps[0];
+        double *Z0f = (double *)ctx->dbuf("z0f", z0_elems(p, 0) * 8);
+        double *T = (double *)ctx->dbuf("t0f", st.csh.size() * 8);
+        T0f = T;
+        CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
+        CUDA_CHECK(cudaStreamWaitEvent(ctx->aux, ctx->event(0), 0));
+        fused_pass1_recompose(p, 0, coef, Z0f, ctx->aux);
+        fused_pass2(p, 0, Z0f, T, ctx->aux);
+        thomas_all(p, 0, T, ctx->aux);
+        CUDA_CHECK(cudaEventRecord(ev_side, ctx->aux));
+    }
+    // The coarser levels' corrections are independent of each other too: compute them up front,
+    // round-robin on the side streams (they are small, latency-bound launches), so the level chain
+    // itself is only coarse - corr and pred + mc per level.
+    std::vector<const double *> Tl(L, nullptr);
+    std::vector<int> ev_l(L, -1);
+    if (L > 2) {
+        int64_t zc = 0, tc = 0;
+        for (int st_i = 1; st_i + 1 < L; st_i++) {
+            zc += (z0_elems(p, st_i) + 31) & ~int64_t(31);
+            tc += (p.steps[st_i].csh.size() + 31) & ~int64_t(31);
+        }
+        double *zarena = (double *)ctx->dbuf("z0c", std::max<int64_t>(zc, 1) * 8);
+        double *tarena = (double *)ctx->dbuf("t0c", std::max<int64_t>(tc, 1) * 8);
+        // event ids: 199 / 200 + level (distinct from the streamed decode's and the slab loop's)
+        CUDA_CHECK(cudaEventRecord(ctx->event(199), s));   // coef ready
+        int k = 0;
+        for (int st_i = L - 2; st_i >= 1; st_i--, k++) {
+            cudaStream_t x = ctx->side[k % 4];
+            if (k < 4) CUDA_CHECK(cudaStreamWaitEvent(x, ctx->event(199), 0));
+            double *Zl = zarena, *T = tarena;
+            zarena += (z0_elems(p, st_i) + 31) & ~int64_t(31);
+            tarena += (p.steps[st_i].csh.size() + 31) & ~int64_t(31);
+            fused_pass1_recompose(p, st_i, coef, Zl, x);
+            fused_pass2(p, st_i, Zl, T, x);
+            thomas_all(p, st_i, T, x);
+            Tl[st_i] = T;
+            ev_l[st_i] = 200 + st_i;
+            CUDA_CHECK(cudaEventRecord(ctx->event(200 + st_i), x));
+        }
+    }
     for (int st_i = L - 2; st_i >= 0; st_i--) {
         const DevStep &st = p.steps[st_i];
         double *Dc = level_ptr(b, p, st_i + 1);
-        fused_pass1_recompose(p, st_i, coef, Z0, s);
-        fused_pass2(p, st_i, Z0, b.t0, s);
-        Shape4 sh = st.csh;
-        for (int a = 0; a < 4; a++)
-            if (st.ax[a].active) thomas(b.t0, sh, a, st.ax[a], s);
+        const double *T = b.t0;
+        if (st_i == 0 && side) {
+            T = T0f;
+            CUDA_CHECK(cudaStreamWaitEvent(s, ev_side, 0));
+        } else if (Tl[st_i]) {
+            T = Tl[st_i];
+            CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(ev_l[st_i]), 0));
+        } else {
+            fused_pass1_recompose(p, st_i, coef, Z0, s);
+            fused_pass2(p, st_i, Z0, b.t0, s);
+            Shape4 sh = st.csh;
+            for (int a = 0; a < 4; a++)
+                if (st.ax[a].active) thomas(b.t0, sh, a, st.ax[a], s);
+        }
         const int64_t nc = st.csh.size();
         {
             KPROF("k_sub", 24.0 * nc, s);
-            k_sub<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(Dc, b.t0, b.cg, nc);   // coarse - corr
+            k_sub<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(Dc, T, b.cg, nc);   // coarse - corr
             LAUNCH_CHECK();
         }
+        if (st_i == 0) phase_mark("coarse_levels_done", s);
         if (st_i == 0 && direct && host_out) {
             // finest level in dim-0 slabs; each slab's D2H (copy stream) overlaps the next slab
             const int n0 = (int)st.fsh.n[1];

@@ -45,8 +45,14 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
 // Recompose straight into out (device) in the blob's dtype (fused final level for ranks <= 3).
 // With host_out the result also lands there: the finest level is produced in dim-0 slabs whose
 // D2H on the copy stream overlaps the next slab (out is then the device staging buffer).
+// T0_pre / ev_pre: the finest transition's correction, already being computed elsewhere (event
+// recorded after it); otherwise it is computed here on the side stream.
 void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s,
-                    void *host_out = nullptr);
+                    void *host_out = nullptr, const double *T0_pre = nullptr, cudaEvent_t ev_pre = nullptr);
+// Elements of pass 1's output Z0 at transition st_i.
+int64_t z0_elems(const DevPlan &p, int st_i);
+// Thomas solves of every active axis of transition st_i's coarse grid, in place.
+void thomas_all(const DevPlan &p, int st_i, double *T, cudaStream_t s);
 
 // True when the fused level kernels serve these dims (ranks <= 3) and HPDR_GENERIC != 1.
 bool use_fused(const DevPlan &p);

@@ -233,3 +233,23 @@ def test_thomas_fast_division_matches_ieee():
     check(lib().hpdr_selftest_div(1 << 26, 12345, C.byref(m), C.byref(f)))
     assert m.value == 0
     assert f.value < (1 << 26) // 1000   # the exact redo is rare
+
+
+@pytest.mark.parametrize("flip", [None, 0.37, 0.81])
+def test_streamed_decompress_matches_oracle(flip, oracle):
+    """Blobs with a >= 4 MB payload take the streamed decompress (payload in unit groups, the finest
+    correction slab by slab); it must reproduce the reference bit for bit, corrupted payloads included."""
+    a = S.smooth_noise((257, 257, 257), seed=3)
+    blob = bytearray(P.mgard_compress(a, 1e-4))
+    if flip is not None:   # a payload bit (the stream tail is the packed payload)
+        pos = int(len(blob) * flip)
+        blob[pos] ^= 0x10
+    blob = bytes(blob)
+    try:
+        want = oracle.mgard_decompress(blob)
+    except Exception as e:   # noqa: BLE001
+        with pytest.raises(type(e)):
+            P.mgard_decompress(blob)
+        return
+    got = P.mgard_decompress(blob).values
+    assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
