@@ -26,6 +26,25 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double lerp(double va, double vb, double t) { return dadd(va, dmul(t, dsub(vb, va))); }
 
+
+// b = rint(mc / bin) (quantize.py:73-76: IEEE division, half to even) with one multiply by
+// rb = RN(1/bin): the correctly rounded quotient q and qa = RN(mc * rb) differ by < |q| 2^-51, so
+// rint(qa) == rint(q) unless qa lies within that distance of a half-integer -- then (and for
+// |qa| >= 2^61) the IEEE division decides.  Returns false when |mc / bin| >= 2^62 (bin overflow).
+__device__ __forceinline__ bool quant_bin(double mc, double bin, double rb, long long &b) {
+    const double qa = dmul(mc, rb);
+    const double r = rint(qa);
+    const double dist = 0.5 - fabs(dsub(qa, r));
+    if (dist > fabs(qa) * 0x1p-49 && fabs(qa) < 0x1p61) {
+        b = (long long)r;
+        return true;
+    }
+    const double sc = mc / bin;
+    if (fabs(sc) >= 4611686018427387904.0) return false;
+    b = (long long)rint(sc);
+    return true;
+}
+
 // Histogram count of `key` (shared-memory bins flushed once per block).
 // (__match_any_sync aggregation measured slower here: 2.67 vs 1.73 ms for the level-0 pass)
 __device__ __forceinline__ void hist_add(uint32_t *sh, unsigned long long *g, bool sh_ok, uint32_t key) {
@@ -217,6 +236,7 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
     __shared__ __align__(16) TIn ring[kRing * kPlaneElems];
     __shared__ uint32_t sh_hist[MODE == 2 ? kSmemHist : 1];
     const bool sh_ok = MODE == 2 && q.dict <= kSmemHist;
+    const double rbin = MODE == 2 ? 1.0 / q.bin : 0.0;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
     if (MODE == 2 && sh_ok)
         for (uint32_t k = tid; k < q.dict; k += 256) sh_hist[k] = 0;
@@ -316,13 +336,8 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
                             coef[f] = mc;
                         } else {
                             long long b = 0;
-                            if (!isfinite(mc)) {
-                                fl |= 1;
-                            } else {
-                                const double sc = mc / q.bin;                 // IEEE division (quantize.py:73)
-                                if (fabs(sc) >= 4611686018427387904.0) fl |= 2;
-                                else b = (long long)rint(sc);                 // half to even (:76)
-                            }
+                            if (!isfinite(mc)) fl |= 1;
+                            else if (!quant_bin(mc, q.bin, rbin, b)) fl |= 2;
                             if (b >= q.half || -b >= q.half) {                 // outlier (:80-83)
                                 q.obins[f] = b;
                                 atomicOr(&q.omask[f >> 5], 1u << (f & 31));
@@ -373,6 +388,7 @@ __global__ void __launch_bounds__(256) k_level_pass1s(const TIn *__restrict__ F,
     __shared__ double sP1[kP1Rows * kP1Cols];
     __shared__ uint32_t sh_hist[MODE == 2 ? kSmemHist : 1];
     const bool sh_ok = MODE == 2 && q.dict <= kSmemHist;
+    const double rbin = MODE == 2 ? 1.0 / q.bin : 0.0;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
     if (MODE == 2 && sh_ok)
         for (uint32_t k = tid; k < q.dict; k += 256) sh_hist[k] = 0;
@@ -493,13 +509,8 @@ __global__ void __launch_bounds__(256) k_level_pass1s(const TIn *__restrict__ F,
                         coef[f] = mc;
                     } else {
                         long long b = 0;
-                        if (!isfinite(mc)) {
-                            fl |= 1;
-                        } else {
-                            const double sc = mc / q.bin;                 // IEEE division (quantize.py:73)
-                            if (fabs(sc) >= 4611686018427387904.0) fl |= 2;
-                            else b = (long long)rint(sc);                 // half to even (:76)
-                        }
+                        if (!isfinite(mc)) fl |= 1;
+                        else if (!quant_bin(mc, q.bin, rbin, b)) fl |= 2;
                         if (b >= q.half || -b >= q.half) {                 // outlier (:80-83)
                             q.obins[f] = b;
                             atomicOr(&q.omask[f >> 5], 1u << (f & 31));
@@ -534,6 +545,7 @@ __global__ void __launch_bounds__(256) k_quantize_fine(const double *__restrict_
                                                        DevAxis ax0, DevAxis ax1, DevAxis ax2, QuantOut q) {
     __shared__ uint32_t sh_hist[kSmemHist];
     const bool sh_ok = q.dict <= kSmemHist;
+    const double rbin = 1.0 / q.bin;
     const int tid = threadIdx.y * 32 + threadIdx.x;
     if (sh_ok)
         for (uint32_t k = tid; k < q.dict; k += 256) sh_hist[k] = 0;
@@ -550,13 +562,8 @@ __global__ void __launch_bounds__(256) k_quantize_fine(const double *__restrict_
             const int64_t f = (int64_t)j * plane + col;
             const double mc = __ldg(coef + f);
             long long b = 0;
-            if (!isfinite(mc)) {
-                fl |= 1;
-            } else {
-                const double sc = mc / q.bin;
-                if (fabs(sc) >= 4611686018427387904.0) fl |= 2;
-                else b = (long long)rint(sc);
-            }
+            if (!isfinite(mc)) fl |= 1;
+            else if (!quant_bin(mc, q.bin, rbin, b)) fl |= 2;
             if (b >= q.half || -b >= q.half) {
                 q.obins[f] = b;
                 atomicOr(&q.omask[f >> 5], 1u << (f & 31));
@@ -865,7 +872,7 @@ void fused_pass1_quantize(const DevPlan &p, int st_i, const void *F, bool f32, c
     c_hi = clamp_hi(p, st_i, c_hi);
     const double frac = (double)(c_hi - c_lo) / fused_out_planes(p, st_i);
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
-    KPROF("k_level_pass1q", frac * ((f32 ? 4.0 : 8.0) * nf + 4.0 * (nf - nc) + 8.0 * nc + 8.0 * z0_size(p, st_i)), s);
+    KPROF(st_i == 0 ? "k_level_pass1q" : "k_level_pass1q_coarse", frac * ((f32 ? 4.0 : 8.0) * nf + 4.0 * (nf - nc) + 8.0 * nc + 8.0 * z0_size(p, st_i)), s);
     if (f32) launch_pass1<2, float>(v.act, (const float *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
                                     nullptr, nullptr, Z0, Cg, q, c_lo, c_hi - c_lo, s);
     else launch_pass1<2, double>(v.act, (const double *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
