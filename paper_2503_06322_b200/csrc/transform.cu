@@ -282,8 +282,11 @@ __global__ void __launch_bounds__(kThomasWarps * 32) k_thomas_contig(double *__r
         double prev = 0.0;
         for (int t0 = 0; t0 < n; t0 += 32) {
             const int m = min(32, n - t0);
-            for (int r = 0; r < nl; r++)
-                if (lane < m) T[r][lane] = arr[(base + r) * n + t0 + lane];
+            // tile rows land by cp.async: all 32 row segments in flight at once
+            if (lane < m)
+                for (int r = 0; r < nl; r++) cp_async<8>(&T[r][lane], arr + (base + r) * n + t0 + lane);
+            cp_async_commit();
+            cp_async_wait<0>();
             __syncwarp();
             if (lane < nl) {
                 for (int k = 0; k < m; k++) {
@@ -303,8 +306,10 @@ __global__ void __launch_bounds__(kThomasWarps * 32) k_thomas_contig(double *__r
         double last = prev;
         for (int t0 = ((n - 1) / 32) * 32; t0 >= 0; t0 -= 32) {
             const int m = min(32, n - t0);
-            for (int r = 0; r < nl; r++)
-                if (lane < m) T[r][lane] = arr[(base + r) * n + t0 + lane];
+            if (lane < m)
+                for (int r = 0; r < nl; r++) cp_async<8>(&T[r][lane], arr + (base + r) * n + t0 + lane);
+            cp_async_commit();
+            cp_async_wait<0>();
             __syncwarp();
             if (lane < nl) {
                 for (int k = m - 1; k >= 0; k--) {
