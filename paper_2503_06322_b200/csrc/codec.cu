@@ -344,6 +344,92 @@ void fetch_pending_on(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uint
     fetch_pending(ctx, P, out, cap, s, sync, true);
 }
 
+// codec.py:43-56 from quantized keys on: coarse values (d_coarse: dense coarsest level, or
+// coef_for_coarse: the CoefficientSet whose coarsest slots hold them), head, Huffman stage, and
+// the optional streamed fetch into fetch_out.
+void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t *dims, double eb_rel,
+                 uint32_t dict_size, double u_min, double u_max, double eb_abs, double bin, const QuantResult &q,
+                 uint32_t *keys, const double *d_coarse, const double *coef_for_coarse, void *fetch_out,
+                 uint64_t fetch_cap) {
+    {
+        const int64_t N = p.n_total;
+        const int L = p.host.L;
+        cudaStream_t s = ctx->stream;
+        if (q.flags & 1) fail(HPDR_ERR_VALIDATION, "coefficients contain non-finite values");
+        if (q.flags & 2) fail(HPDR_ERR_VALIDATION, "coefficient exceeds representable bin range");
+        const size_t nco = p.host.coarsest.size();
+        std::vector<double> coarse(nco);
+        if (d_coarse) {
+            CUDA_CHECK(cudaMemcpyAsync(coarse.data(), d_coarse, nco * 8, cudaMemcpyDeviceToHost, s));
+        } else {
+            for (size_t k = 0; k < nco; k++)
+                CUDA_CHECK(cudaMemcpyAsync(&coarse[k], coef_for_coarse + p.host.coarsest[k], 8, cudaMemcpyDeviceToHost, s));
+        }
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        auto &P = ctx->pending;
+        P = hpdr_ctx::Pending();
+        put<uint8_t>(P.head, (uint8_t)rank);
+        for (int d = 0; d < rank; d++) put<uint64_t>(P.head, dims[d]);
+        put<uint8_t>(P.head, (uint8_t)dtype);
+        put<double>(P.head, eb_rel);
+        put<uint32_t>(P.head, dict_size);
+        put<double>(P.head, u_min);
+        put<double>(P.head, u_max);
+        put<double>(P.head, eb_abs);
+        put<double>(P.head, bin);
+        put<uint32_t>(P.head, (uint32_t)L);
+        put<uint64_t>(P.head, q.n_outliers);
+        P.n_out = q.n_outliers;
+        put<uint64_t>(P.mid, (uint64_t)nco);
+        for (double v : coarse) put<double>(P.mid, v);
+        EncodeResult enc;
+        bool single;
+        phase_mark("coarse_read", s);
+        // Streamed fetch (pinned / device output): as soon as the stream layout is known the blob
+        // head, outliers and unit offsets go out on the D2H stream, and the packed payload follows
+        // unit group by unit group behind the encode launches.
+        EncodeHooks hooks;
+        bool streamed_fetch = false;
+        uint64_t pay_pos = 0;
+        const MemKind ok = fetch_out ? classify(fetch_out) : MemKind::Host;
+        if (fetch_out && ok != MemKind::Host) {
+            hooks.groups = 8;
+            hooks.ready = [&](const EncodeResult &e) {
+                const uint64_t total = P.head.size() + 16 * P.n_out + P.mid.size() + 8 * e.n_units + 8 + (e.total_bits + 7) / 8;
+                if (fetch_cap < total) return;
+                streamed_fetch = true;
+                hpdr_ctx::Pending Q = P;
+                Q.n_units = e.n_units;
+                Q.total_bits = e.total_bits;
+                Q.total_len = total;
+                Q.slot = ctx->out_slot;
+                Q.valid = true;
+                CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
+                CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(0), 0));
+                pay_pos = fetch_pending(ctx, Q, fetch_out, fetch_cap, ctx->d2h, false, /*payload=*/false);
+            };
+            hooks.group_done = [&](int g, uint64_t lo, uint64_t hi) {
+                if (!streamed_fetch || hi <= lo) return;
+                CUDA_CHECK(cudaEventRecord(ctx->event(1 + g), s));
+                CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(1 + g), 0));
+                const bool dev = ok == MemKind::Device;
+                CUDA_CHECK(cudaMemcpyAsync((char *)fetch_out + pay_pos + lo, (const char *)ctx->dbuf(ctx->oname("enc_words"), 16) + lo,
+                                           hi - lo, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->d2h));
+            };
+        }
+        huffman_stage(ctx, keys, N, dict_size, q.hist, P.mid, enc, single, s, fetch_out ? &hooks : nullptr);
+        phase_mark("encoded", s);
+        P.single_key = single;
+        P.n_units = enc.n_units;
+        P.total_bits = enc.total_bits;
+        P.total_len = P.head.size() + 16 * P.n_out + P.mid.size() + 8 * P.n_units + 8 + (P.total_bits + 7) / 8;
+        P.slot = ctx->out_slot;
+        P.valid = true;
+        P.fetched = streamed_fetch;
+        if (streamed_fetch) CUDA_CHECK(cudaStreamSynchronize(ctx->d2h));
+    }
+}
+
 // mgard_compress (codec.py:25-56) up to a pending blob in ctx->pending (device parts in output
 // slot ctx->out_slot).  allow_stream: a host input may be streamed in dim-0 chunks.
 void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, double eb_rel,
@@ -409,74 +495,38 @@ void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uin
             d_coarse = decompose_device(ctx, p, d_in, dtype, coef, s);
             quantize_device(ctx, coef, N, p.host.coarsest, bin, dict_size, keys, q, s);
         }
-        if (q.flags & 1) fail(HPDR_ERR_VALIDATION, "coefficients contain non-finite values");
-        if (q.flags & 2) fail(HPDR_ERR_VALIDATION, "coefficient exceeds representable bin range");
-        const size_t nco = p.host.coarsest.size();
-        std::vector<double> coarse(nco);
-        CUDA_CHECK(cudaMemcpyAsync(coarse.data(), d_coarse, nco * 8, cudaMemcpyDeviceToHost, s));
-        CUDA_CHECK(cudaStreamSynchronize(s));
-        auto &P = ctx->pending;
-        P = hpdr_ctx::Pending();
-        put<uint8_t>(P.head, (uint8_t)rank);
-        for (int d = 0; d < rank; d++) put<uint64_t>(P.head, dims[d]);
-        put<uint8_t>(P.head, (uint8_t)dtype);
-        put<double>(P.head, eb_rel);
-        put<uint32_t>(P.head, dict_size);
-        put<double>(P.head, u_min);
-        put<double>(P.head, u_max);
-        put<double>(P.head, eb_abs);
-        put<double>(P.head, bin);
-        put<uint32_t>(P.head, (uint32_t)L);
-        put<uint64_t>(P.head, q.n_outliers);
-        P.n_out = q.n_outliers;
-        put<uint64_t>(P.mid, (uint64_t)nco);
-        for (double v : coarse) put<double>(P.mid, v);
-        EncodeResult enc;
-        bool single;
-        phase_mark("coarse_read", s);
-        // Streamed fetch (pinned / device output): as soon as the stream layout is known the blob
-        // head, outliers and unit offsets go out on the D2H stream, and the packed payload follows
-        // unit group by unit group behind the encode launches.
-        EncodeHooks hooks;
-        bool streamed_fetch = false;
-        uint64_t pay_pos = 0;
-        const MemKind ok = fetch_out ? classify(fetch_out) : MemKind::Host;
-        if (fetch_out && ok != MemKind::Host) {
-            hooks.groups = 8;
-            hooks.ready = [&](const EncodeResult &e) {
-                const uint64_t total = P.head.size() + 16 * P.n_out + P.mid.size() + 8 * e.n_units + 8 + (e.total_bits + 7) / 8;
-                if (fetch_cap < total) return;
-                streamed_fetch = true;
-                hpdr_ctx::Pending Q = P;
-                Q.n_units = e.n_units;
-                Q.total_bits = e.total_bits;
-                Q.total_len = total;
-                Q.slot = ctx->out_slot;
-                Q.valid = true;
-                CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
-                CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(0), 0));
-                pay_pos = fetch_pending(ctx, Q, fetch_out, fetch_cap, ctx->d2h, false, /*payload=*/false);
-            };
-            hooks.group_done = [&](int g, uint64_t lo, uint64_t hi) {
-                if (!streamed_fetch || hi <= lo) return;
-                CUDA_CHECK(cudaEventRecord(ctx->event(1 + g), s));
-                CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(1 + g), 0));
-                const bool dev = ok == MemKind::Device;
-                CUDA_CHECK(cudaMemcpyAsync((char *)fetch_out + pay_pos + lo, (const char *)ctx->dbuf(ctx->oname("enc_words"), 16) + lo,
-                                           hi - lo, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->d2h));
-            };
-        }
-        huffman_stage(ctx, keys, N, dict_size, q.hist, P.mid, enc, single, s, fetch_out ? &hooks : nullptr);
-        phase_mark("encoded", s);
-        P.single_key = single;
-        P.n_units = enc.n_units;
-        P.total_bits = enc.total_bits;
-        P.total_len = P.head.size() + 16 * P.n_out + P.mid.size() + 8 * P.n_units + 8 + (P.total_bits + 7) / 8;
-        P.slot = ctx->out_slot;
-        P.valid = true;
-        P.fetched = streamed_fetch;
-        if (streamed_fetch) CUDA_CHECK(cudaStreamSynchronize(ctx->d2h));
+        finish_blob(ctx, p, dtype, rank, dims, eb_rel, dict_size, u_min, u_max, eb_abs, bin, q, keys, d_coarse, nullptr,
+                    fetch_out, fetch_cap);
     }
+}
+
+// Phase B of the relative-mode streams pipeline: a chunk already decomposed into coef (device,
+// the full CoefficientSet in finest order) is quantized with the global range, now known, and
+// entropy coded into a pending blob (quantize.py:50-98 then codec.py:43-56).
+void compress_from_coef(hpdr_ctx *ctx, const double *coef, int dtype, int rank, const uint64_t *dims, double eb_rel,
+                        uint32_t dict_size, double u_min, double u_max) {
+    ctx->pending.valid = false;
+    DevPlan &p = ctx->plan(rank, dims);
+    if (!(0.0 < eb_rel && eb_rel < 1.0)) fail(HPDR_ERR_VALIDATION, "eb_rel must be in (0, 1), got " + fmt_double(eb_rel));
+    if (dict_size < 2 || dict_size > 65535)
+        fail(HPDR_ERR_VALIDATION, "dict_size must be in [2, 65535], got " + std::to_string(dict_size));
+    const int64_t N = p.n_total;
+    const int L = p.host.L;
+    uint32_t *keys = (uint32_t *)ctx->dbuf("keys", N * 4 + 64);
+    const double eb_abs = eb_rel * (u_max - u_min);
+    const double bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
+    QuantResult q;
+    quantize_device(ctx, coef, N, p.host.coarsest, bin, dict_size, keys, q, ctx->stream);
+    finish_blob(ctx, p, dtype, rank, dims, eb_rel, dict_size, u_min, u_max, eb_abs, bin, q, keys, nullptr, coef, nullptr, 0);
+}
+
+// Phase A of the relative-mode streams pipeline: decompose a device-resident chunk into coef
+// (range-independent, transform.py:287-323) and fold its min/max into mm (k_minmax order keys).
+void decompose_chunk(hpdr_ctx *ctx, const void *d_in, int dtype, int rank, const uint64_t *dims, double *coef,
+                     unsigned long long *mm) {
+    DevPlan &p = ctx->plan(rank, dims);
+    minmax_accumulate(d_in, dtype, p.n_total, mm, ctx->stream);
+    decompose_device(ctx, p, d_in, dtype, coef, ctx->stream);
 }
 }  // namespace hpdr
 

@@ -30,6 +30,10 @@ void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uin
                    void *fetch_out = nullptr, uint64_t fetch_cap = 0);
 void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uint8_t *dev_blob, void *out,
                      uint64_t out_bytes, bool sync);
+void compress_from_coef(hpdr_ctx *ctx, const double *coef, int dtype, int rank, const uint64_t *dims, double eb_rel,
+                        uint32_t dict_size, double u_min, double u_max);
+void decompose_chunk(hpdr_ctx *ctx, const void *d_in, int dtype, int rank, const uint64_t *dims, double *coef,
+                     unsigned long long *mm);
 void fetch_pending_on(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uint64_t cap, cudaStream_t s, bool sync);
 
 namespace {
@@ -224,7 +228,13 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
         }
         const uint64_t K = sizes.size();
         double vmin = range_min, vmax = range_max;
-        if (!has_range) host_minmax(host_in, dtype, N, &vmin, &vmax);   // the global range
+        // Relative mode needs the global range before any chunk is quantized.  The
+        // decomposition does not depend on it, so by default the chunks are streamed in and
+        // decomposed first (phase A, per-chunk min/max on the device), and quantized, coded and
+        // streamed out once the range is known (phase B).  HPDR_PIPE_HOST_RANGE=1: a host pre-pass.
+        static const bool host_range = getenv("HPDR_PIPE_HOST_RANGE") != nullptr;
+        const bool two_phase = !has_range && !host_range;
+        if (!has_range && host_range) host_minmax(host_in, dtype, N, &vmin, &vmax);
         std::vector<Chunk> chunks(K);
         uint64_t maxp = 1;
         for (uint64_t k = 0, a = 0; k < K; a += sizes[k], k++) {
@@ -246,8 +256,66 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
         std::vector<char> have(K, 0);
         uint64_t next_pos = 0;   // first chunk whose offset is not yet known
         pos[0] = hdr_len;
+        double *coef_all = nullptr;
+        if (two_phase) {
+            coef_all = (double *)ctx->dbuf("pipe_coef", N * 8);
+            std::vector<unsigned long long> mmq(3 * Q);
+            QueueRun RA;
+            RA.run(Q, [&](int q) {
+                hpdr_ctx *c = qc[q];
+                CUDA_CHECK(cudaSetDevice(c->device));
+                if (c != ctx) CUDA_CHECK(cudaStreamWaitEvent(c->stream, ctx->event(0), 0));
+                CUDA_CHECK(cudaStreamWaitEvent(c->h2d, ctx->event(0), 0));
+                char *din = (char *)c->dbuf("pipe_in", cbytes);
+                unsigned long long *mm = (unsigned long long *)c->dbuf("pipe_mm", 32);
+                unsigned long long *hmm = (unsigned long long *)c->hbuf("pipe_mm_h", 32);
+                hmm[0] = ~0ULL;
+                hmm[1] = 0ULL;
+                hmm[2] = 0ULL;
+                CUDA_CHECK(cudaMemcpyAsync(mm, hmm, 24, cudaMemcpyHostToDevice, c->stream));
+                cudaEvent_t ev_in = c->event(300), ev_red = c->event(301);
+                bool first = true;
+                for (uint64_t k = q; k < K; k += Q) {
+                    if (RA.failed) return;
+                    if (!first) CUDA_CHECK(cudaStreamWaitEvent(c->h2d, ev_red, 0));   // input buffer reuse edge
+                    tm.mark(6 * k, c->h2d);
+                    CUDA_CHECK(cudaMemcpyAsync(din, (const char *)host_in + chunks[k].raw_off * isz,
+                                               chunks[k].raw_size * isz, cudaMemcpyHostToDevice, c->h2d));
+                    tm.mark(6 * k + 1, c->h2d);
+                    CUDA_CHECK(cudaEventRecord(ev_in, c->h2d));
+                    CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_in, 0));
+                    tm.mark(6 * k + 2, c->stream);
+                    uint64_t sd[4] = {chunks[k].raw_size / plane, 0, 0, 0};
+                    for (int d = 1; d < rank; d++) sd[d] = dims[d];
+                    decompose_chunk(c, din, dtype, rank, sd, coef_all + chunks[k].raw_off, mm);
+                    CUDA_CHECK(cudaEventRecord(ev_red, c->stream));
+                    first = false;
+                }
+                CUDA_CHECK(cudaMemcpyAsync(hmm, mm, 24, cudaMemcpyDeviceToHost, c->stream));
+                CUDA_CHECK(cudaStreamSynchronize(c->stream));
+                memcpy(&mmq[3 * q], hmm, 24);
+            });
+            unsigned long long g[3] = {~0ULL, 0ULL, 0ULL};
+            for (int q = 0; q < Q; q++) {
+                g[0] = std::min(g[0], mmq[3 * q]);
+                g[1] = std::max(g[1], mmq[3 * q + 1]);
+                g[2] |= mmq[3 * q + 2];
+            }
+            minmax_from_keys(g, &vmin, &vmax);
+        }
+        // phase B of the relative mode is quantize + code + copy-out only: more queues in flight
+        static const int qb_env = [] {
+            const char *e = getenv("HPDR_PIPE_QUEUES_B");
+            return e ? std::max(1, atoi(e)) : 3;
+        }();
+        const int QB = two_phase ? (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)qb_env, K)) : Q;   // (3 measured best)
+        if (QB > Q) {
+            qc.resize(QB);
+            for (int q = Q; q < QB; q++) qc[q] = ctx->queue(q);
+        }
         QueueRun R;
-        R.run(Q, [&](int q) {
+        R.run(QB, [&](int q) {
+            const int Q = QB;
             hpdr_ctx *c = qc[q];
             CUDA_CHECK(cudaSetDevice(c->device));
             if (c != ctx) {
@@ -255,24 +323,32 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
             }
             CUDA_CHECK(cudaStreamWaitEvent(c->h2d, ctx->event(0), 0));
             CUDA_CHECK(cudaStreamWaitEvent(c->d2h, ctx->event(0), 0));
-            c->out_slot = 0;
             char *din = (char *)c->dbuf("pipe_in", cbytes);
-            cudaEvent_t ev_in = c->event(300), ev_red = c->event(301), ev_out = c->event(302);   // ids reserved for the runner
+            // event ids 300-303 are reserved for the runner; the output buffer sets alternate
+            cudaEvent_t ev_in = c->event(300), ev_red = c->event(301), ev_outs[2] = {c->event(302), c->event(303)};
             bool first = true;
-            for (uint64_t k = q; k < K; k += Q) {
+            uint64_t t = 0;
+            for (uint64_t k = q; k < K; k += Q, t++) {
                 if (R.failed) return;
-                if (!first) CUDA_CHECK(cudaStreamWaitEvent(c->h2d, ev_red, 0));   // input buffer reuse edge
-                tm.mark(6 * k, c->h2d);
-                CUDA_CHECK(cudaMemcpyAsync(din, (const char *)host_in + chunks[k].raw_off * isz,
-                                           chunks[k].raw_size * isz, cudaMemcpyHostToDevice, c->h2d));
-                tm.mark(6 * k + 1, c->h2d);
-                CUDA_CHECK(cudaEventRecord(ev_in, c->h2d));
-                CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_in, 0));
-                if (!first) CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_out, 0));   // output buffers reuse edge
-                tm.mark(6 * k + 2, c->stream);
+                cudaEvent_t ev_out = ev_outs[t & 1];
+                c->out_slot = (int)(t & 1);
+                if (!two_phase) {
+                    if (!first) CUDA_CHECK(cudaStreamWaitEvent(c->h2d, ev_red, 0));   // input buffer reuse edge
+                    tm.mark(6 * k, c->h2d);
+                    CUDA_CHECK(cudaMemcpyAsync(din, (const char *)host_in + chunks[k].raw_off * isz,
+                                               chunks[k].raw_size * isz, cudaMemcpyHostToDevice, c->h2d));
+                    tm.mark(6 * k + 1, c->h2d);
+                    CUDA_CHECK(cudaEventRecord(ev_in, c->h2d));
+                    CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_in, 0));
+                }
+                if (t >= 2) CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_out, 0));   // output set reuse edge (k - 2Q)
+                if (!two_phase) tm.mark(6 * k + 2, c->stream);
                 uint64_t sd[4] = {chunks[k].raw_size / plane, 0, 0, 0};
                 for (int d = 1; d < rank; d++) sd[d] = dims[d];
-                compress_core(c, din, dtype, rank, sd, eb_rel, dict_size, 1, vmin, vmax, false);
+                if (two_phase)
+                    compress_from_coef(c, coef_all + chunks[k].raw_off, dtype, rank, sd, eb_rel, dict_size, vmin, vmax);
+                else
+                    compress_core(c, din, dtype, rank, sd, eb_rel, dict_size, 1, vmin, vmax, false);
                 const hpdr_ctx::Pending P = c->pending;
                 tm.mark(6 * k + 3, c->stream);
                 CUDA_CHECK(cudaEventRecord(ev_red, c->stream));
@@ -301,6 +377,7 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
                 first = false;
             }
             CUDA_CHECK(cudaStreamSynchronize(c->d2h));
+            c->out_slot = 0;
         });
         const std::vector<uint8_t> hdr = container_header(dtype, rank, dims, eb_rel, dict_size, vmin, vmax, chunks);
         if (classify(out) == MemKind::Device) {
@@ -379,11 +456,15 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
             CUDA_CHECK(cudaStreamWaitEvent(x->h2d, ctx->event(0), 0));
             CUDA_CHECK(cudaStreamWaitEvent(x->d2h, ctx->event(0), 0));
             uint8_t *dblob = (uint8_t *)x->dbuf("pipe_blob", maxpay);
-            char *dout = host_out ? (char *)x->dbuf("pipe_out", maxraw * isz) : nullptr;
-            cudaEvent_t ev_in = x->event(300), ev_red = x->event(301), ev_out = x->event(302);
+            char *douts[2] = {host_out ? (char *)x->dbuf("pipe_out0", maxraw * isz) : nullptr,
+                              host_out ? (char *)x->dbuf("pipe_out1", maxraw * isz) : nullptr};
+            cudaEvent_t ev_in = x->event(300), ev_red = x->event(301), ev_outs[2] = {x->event(302), x->event(303)};
             bool first = true;
-            for (uint64_t k = q; k < K; k += Q) {
+            uint64_t t = 0;
+            for (uint64_t k = q; k < K; k += Q, t++) {
                 if (R.failed) return;
+                char *dout = douts[t & 1];
+                cudaEvent_t ev_out = ev_outs[t & 1];
                 if (!first) CUDA_CHECK(cudaStreamWaitEvent(x->h2d, ev_red, 0));   // blob buffer reuse edge
                 tm.mark(6 * k, x->h2d);
                 CUDA_CHECK(cudaMemcpyAsync(dblob, c + base + chunks[k].pay_off, chunks[k].pay_size,
@@ -391,7 +472,7 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
                 tm.mark(6 * k + 1, x->h2d);
                 CUDA_CHECK(cudaEventRecord(ev_in, x->h2d));
                 CUDA_CHECK(cudaStreamWaitEvent(x->stream, ev_in, 0));
-                if (!first && host_out) CUDA_CHECK(cudaStreamWaitEvent(x->stream, ev_out, 0));   // output slab reuse
+                if (t >= 2 && host_out) CUDA_CHECK(cudaStreamWaitEvent(x->stream, ev_out, 0));   // output slab reuse (k - 2Q)
                 tm.mark(6 * k + 2, x->stream);
                 char *dst = host_out ? dout : (char *)out + chunks[k].raw_off * isz;
                 decompress_core(x, c + base + chunks[k].pay_off, chunks[k].pay_size, dblob, dst,

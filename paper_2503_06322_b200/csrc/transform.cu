@@ -454,29 +454,49 @@ __global__ void __launch_bounds__(32) k_thomas_tile(double *__restrict__ arr, in
                 prev = dsub(at(lane, i0), dmul(__ldg(tw + i0), prev));
                 at(lane, i0) = prev;
             }
-            // back substitution: x_{n-1} /= b'_{n-1}; x_i = (x_i - u_i x_{i+1}) / b'_i
-            double last = ddiv(prev, __ldg(tb + n - 1));
+            // back substitution: x_{n-1} /= b'_{n-1}; x_i = (x_i - u_i x_{i+1}) / b'_i with the
+            // verified fast division off the dependency chain's check; a failed check redoes the
+            // line from the untouched global values with __ddiv_rn
+            bool bad = false;
+            double last = div_fast(prev, __ldg(tb + n - 1), __ldg(tr + n - 1), bad);
             at(lane, n - 1) = last;
             int i1 = n - 2;
             for (; i1 - U + 1 >= 0; i1 -= U) {
-                double v[U], u[U], b[U];
+                double v[U], u[U], b[U], r[U];
 #pragma unroll
                 for (int k = 0; k < U; k++) {
                     v[k] = at(lane, i1 - k);
                     u[k] = __ldg(tu + i1 - k);
                     b[k] = __ldg(tb + i1 - k);
+                    r[k] = __ldg(tr + i1 - k);
                 }
 #pragma unroll
                 for (int k = 0; k < U; k++) {
-                    last = ddiv(dsub(v[k], dmul(u[k], last)), b[k]);
+                    last = div_fast(dsub(v[k], dmul(u[k], last)), b[k], r[k], bad);
                     v[k] = last;
                 }
 #pragma unroll
                 for (int k = 0; k < U; k++) at(lane, i1 - k) = v[k];
             }
             for (; i1 >= 0; i1--) {
-                last = ddiv(dsub(at(lane, i1), dmul(__ldg(tu + i1), last)), __ldg(tb + i1));
+                last = div_fast(dsub(at(lane, i1), dmul(__ldg(tu + i1), last)), __ldg(tb + i1), __ldg(tr + i1), bad);
                 at(lane, i1) = last;
+            }
+            if (bad) {   // rare: the whole line again, exactly
+                const int64_t st_ = CONTIG ? 1 : inner;
+                const double *src = CONTIG ? arr + (l0 + lane) * (int64_t)n : arr + p * (int64_t)n * inner + q0 + lane;
+                prev = src[0];
+                at(lane, 0) = prev;
+                for (int i = 1; i < n; i++) {
+                    prev = dsub(src[(int64_t)i * st_], dmul(__ldg(tw + i), prev));
+                    at(lane, i) = prev;
+                }
+                last = ddiv(prev, __ldg(tb + n - 1));
+                at(lane, n - 1) = last;
+                for (int i = n - 2; i >= 0; i--) {
+                    last = ddiv(dsub(at(lane, i), dmul(__ldg(tu + i), last)), __ldg(tb + i));
+                    at(lane, i) = last;
+                }
             }
         }
         __syncwarp();
@@ -714,6 +734,28 @@ void minmax_device(hpdr_ctx *ctx, const void *d_in, int dtype, int64_t n, double
     }
     CUDA_CHECK(cudaMemcpyAsync(h, d, 24, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
+    if (h[2]) {
+        *vmin = __builtin_nan("");
+        *vmax = __builtin_nan("");
+        return;
+    }
+    auto val = [](unsigned long long k) {
+        unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k;
+        double d;
+        memcpy(&d, &u, 8);
+        return d;
+    };
+    *vmin = val(h[0]);
+    *vmax = val(h[1]);
+}
+
+void minmax_accumulate(const void *d_in, int dtype, int64_t n, unsigned long long *mm, cudaStream_t s) {
+    KPROF("k_minmax", (double)n * (dtype == 0 ? 4 : 8), s);
+    k_minmax<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(d_in, dtype, n, mm);
+    LAUNCH_CHECK();
+}
+
+void minmax_from_keys(const unsigned long long *h, double *vmin, double *vmax) {
     if (h[2]) {
         *vmin = __builtin_nan("");
         *vmax = __builtin_nan("");

@@ -17,6 +17,9 @@ struct LevelBuffers {
 LevelBuffers level_buffers(hpdr_ctx *ctx, DevPlan &p);
 
 // Global min/max of the input (numpy min/max semantics: NaN propagates).
+// Order-key min/max accumulator: mm = {~0, 0, 0} initially (min key, max key, NaN seen).
+void minmax_accumulate(const void *d_in, int dtype, int64_t n, unsigned long long *mm, cudaStream_t s);
+void minmax_from_keys(const unsigned long long *mm_host, double *vmin, double *vmax);
 void minmax_device(hpdr_ctx *ctx, const void *d_in, int dtype, int64_t n, double *vmin, double *vmax,
                    cudaStream_t s);
 

@@ -15,7 +15,7 @@ from paper_2503_06322_b200 import synthetic as S  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 513
 cp = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 a = S.smooth_noise((n, n, n), seed=0)
-vr = (float(a.min()), float(a.max()))
+vr = None if (len(sys.argv) > 3 and sys.argv[3] == "rel") else (float(a.min()), float(a.max()))
 h_in = torch.from_numpy(a).pin_memory()
 out = torch.empty(a.nbytes + (64 << 20), dtype=torch.uint8).pin_memory().numpy()
 m = PL.compress_pipelined(h_in, 1e-4, value_range=vr, out=out, chunk_planes=cp)
