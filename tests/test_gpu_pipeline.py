@@ -71,3 +71,19 @@ def test_pipeline_after_whole_field_call():
     assert data == PL.compress_pipelined(a, 1e-4, value_range=vr, chunk_planes=63)
     y = PL.decompress_pipelined(data)
     assert np.max(np.abs(y.astype(np.float64) - a)) <= 1e-4 * (vr[1] - vr[0])
+
+
+def test_relative_pipeline_equals_known_range():
+    """Relative mode (range found on the device while chunks decompose) == the same run with the
+    range given up front: byte-identical containers."""
+    a = S.grf((96, 70, 66), m=4, seed=5)
+    rel = PL.compress_pipelined(a, 1e-3, chunk_planes=20)
+    known = PL.compress_pipelined(a, 1e-3, chunk_planes=20, value_range=(float(a.min()), float(a.max())))
+    assert rel == known
+
+
+def test_relative_pipeline_non_finite_raises():
+    a = S.smooth_noise((40, 33, 31), seed=6)
+    a[17, 3, 4] = np.nan
+    with pytest.raises(P.ValidationError):
+        PL.compress_pipelined(a, 1e-3, chunk_planes=8)
