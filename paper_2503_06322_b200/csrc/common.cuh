@@ -68,6 +68,11 @@ __device__ __forceinline__ void cp_async(void *smem, const void *gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES));
 }
+// Same with a precomputed 32-bit shared-window address.
+template <int BYTES>
+__device__ __forceinline__ void cp_async_s(unsigned saddr, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(saddr), "l"(gmem), "n"(BYTES));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }

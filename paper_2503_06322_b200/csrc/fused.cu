@@ -115,29 +115,36 @@ __device__ __forceinline__ void march_y(March &M, double v, int emit, int rr, in
 }
 
 // y(k) and its emission for fine index k, reading k's PlaneInfo from the (L1-resident) table.
-template <class Emit>
+template <bool NC, typename T>
+__device__ __forceinline__ T ldx(const T *p) {   // read-only-path load from global, plain load otherwise
+    if (NC) return __ldg(p);
+    return *p;
+}
+
+template <int MASK = -1, class Emit>
 __device__ __forceinline__ void march_emit_y(March &M, const PlaneInfo *__restrict__ P, int k, double xk, double xkm1,
                                              double xkp1, bool has_up, Emit &&out) {
-    const PlaneInfo *p = P + k;
-    double v = dmul(__ldg(&p->md), xk);
-    if (k >= 1) v = dadd(v, dmul(__ldg(&p->ml), xkm1));
-    if (has_up) v = dadd(v, dmul(__ldg(&p->mu), xkp1));
-    const int4 e = __ldg(reinterpret_cast<const int4 *>(&p->fo));   // fo, emit, e_rr, e_rl
+    constexpr bool NC = MASK == -1;          // MASK != -1: ring of records in shared memory
+    const PlaneInfo *p = P + (k & MASK);
+    double v = dmul(ldx<NC>(&p->md), xk);
+    if (k >= 1) v = dadd(v, dmul(ldx<NC>(&p->ml), xkm1));
+    if (has_up) v = dadd(v, dmul(ldx<NC>(&p->mu), xkp1));
+    const int4 e = ldx<NC>(reinterpret_cast<const int4 *>(&p->fo));   // fo, emit, e_rr, e_rl
     double wr = 0.0, wl = 0.0;
     if (e.y >= M.c_lo && e.y < M.c_hi) {
-        wr = __ldg(&p->ewr);
-        wl = __ldg(&p->ewl);
+        wr = ldx<NC>(&p->ewr);
+        wl = ldx<NC>(&p->ewl);
     }
     march_y(M, v, e.y, e.z, e.w, wr, wl, out);
 }
 
 // Push x(j) (PlaneInfo table P); emits every restricted value that became computable.
-template <class Emit>
+template <int MASK = -1, class Emit>
 __device__ __forceinline__ void march_push(March &M, const PlaneInfo *__restrict__ P, int n, int j, int j_start,
                                            double x, Emit &&out) {
-    // y(j-1) needs x(j-2) unless j-1 == 0
-    if (j >= 1 && j - 1 >= j_start && (j - 1 == 0 || j - 2 >= j_start)) march_emit_y(M, P, j - 1, M.m1, M.m2, x, true, out);
-    if (j == n - 1 && (j == 0 || j - 1 >= j_start)) march_emit_y(M, P, j, x, M.m1, 0.0, false, out);
+    // y(j-1) needs x(j-2) unless j-1 == 0: j >= 1 when the march starts at 0, else j >= j_start + 2
+    if (j >= (j_start == 0 ? 1 : j_start + 2)) march_emit_y<MASK>(M, P, j - 1, M.m1, M.m2, x, true, out);
+    if (j == n - 1 && (j > j_start || j == 0)) march_emit_y<MASK>(M, P, j, x, M.m1, 0.0, false, out);
     M.m2 = M.m1;
     M.m1 = x;
 }
@@ -159,14 +166,15 @@ struct PiHead {
     double t;
 };
 
+template <bool NC = true>
 __device__ __forceinline__ PiHead load_head(const PlaneInfo *__restrict__ p) {
-    const int4 a = __ldg(reinterpret_cast<const int4 *>(p));   // fa, fb, ca, cb
+    const int4 a = ldx<NC>(reinterpret_cast<const int4 *>(p));   // fa, fb, ca, cb
     PiHead h;
     h.fa = a.x;
     h.fb = a.y;
     h.ca = a.z;
-    h.fo = __ldg(&p->fo);
-    h.t = __ldg(&p->t);
+    h.fo = ldx<NC>(&p->fo);
+    h.t = ldx<NC>(&p->t);
     return h;
 }
 
@@ -234,6 +242,8 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
                                                      const double *__restrict__ coef_in, double *__restrict__ Z0,
                                                      double *__restrict__ Cg, QuantOut q, int c_base, int c_count) {
     __shared__ __align__(16) TIn ring[kRing * kPlaneElems];
+    __shared__ double sP0[MODE != 1 ? 2 : 1][MODE != 1 ? kPlaneElems : 1];   // axis-0 GPK plane, double-buffered
+    __shared__ __align__(16) PlaneInfo piring[kRing];   // axis-0 records of the planes in the ring
     __shared__ uint32_t sh_hist[MODE == 2 ? kSmemHist : 1];
     const bool sh_ok = MODE == 2 && q.dict <= kSmemHist;
     const double rbin = MODE == 2 ? 1.0 / q.bin : 0.0;
@@ -270,17 +280,29 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
             soff[k] = e;
             goff[k] = (int64_t)gy * n2 + gx;
         }
+        // issue(p) is called for p = j_start, j_start + 1, ... in order: running source pointers and
+        // precomputed 32-bit shared addresses keep the per-plane issue cheap
+        const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+        const unsigned sa0 = ring_s + soff[0] * (unsigned)sizeof(TIn), sa1 = ring_s + soff[1] * (unsigned)sizeof(TIn);
+        const unsigned sown = ring_s + own_off * (unsigned)sizeof(TIn);
+        const TIn *gp0 = MODE == 1 ? nullptr : F + goff[0] + (int64_t)j_start * plane;
+        const TIn *gp1 = MODE == 1 ? nullptr : F + goff[1] + (int64_t)j_start * plane;
+        const unsigned pir_s = (unsigned)__cvta_generic_to_shared(piring) + (unsigned)tid * 16u;
         auto issue = [&](int p) {
             if (p <= j_end) {
-                TIn *slot = ring + (p & (kRing - 1)) * kPlaneElems;
+                if (A0 && tid < 5)   // the plane's 80-byte PlaneInfo record rides with it
+                    cp_async_s<16>(pir_s + (unsigned)(p & (kRing - 1)) * (unsigned)sizeof(PlaneInfo),
+                                   reinterpret_cast<const char *>(ax0.pi + p) + tid * 16);
+                const unsigned so = (unsigned)(p & (kRing - 1)) * (unsigned)(kPlaneElems * sizeof(TIn));
                 if (MODE == 1) {
                     if (act)
-                        cp_async<sizeof(TIn)>(slot + own_off,
-                                              (const TIn *)(coef_in + (int64_t)__ldg(lm.m0 + p) * fplane + fcol));
+                        cp_async_s<sizeof(TIn)>(sown + so,
+                                                (const TIn *)(coef_in + (int64_t)__ldg(lm.m0 + p) * fplane + fcol));
                 } else {
-                    const TIn *src = F + (int64_t)p * plane;
-                    if (lv[0]) cp_async<sizeof(TIn)>(slot + soff[0], src + goff[0]);
-                    if (lv[1]) cp_async<sizeof(TIn)>(slot + soff[1], src + goff[1]);
+                    if (lv[0]) cp_async_s<sizeof(TIn)>(sa0 + so, gp0);
+                    if (lv[1]) cp_async_s<sizeof(TIn)>(sa1 + so, gp1);
+                    gp0 += plane;
+                    gp1 += plane;
                 }
             }
             cp_async_commit();
@@ -299,29 +321,47 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
         March M;
         march_init(M, c_lo, c_hi);
         auto emit = [&](int c, double z) { Z0[(int64_t)c * plane + col] = z; };
+        // GPK stage along axis 0 (P0 = lerp of the fine planes' coarse neighbours), computed once
+        // per tile element for plane p into sP0[p & 1]; done one plane ahead of the march so the
+        // per-plane barrier also publishes it (transform.py:264-268 order: axis 0, then 1, then 2)
+        auto stage_p0 = [&](int p) {
+            if (MODE == 1 || p > j_end) return;
+            const PiHead ph = A0 ? load_head<false>(piring + (p & (kRing - 1))) : identity_head(p);
+            const TIn *ra = ring + (ph.fa & (kRing - 1)) * kPlaneElems;
+            const TIn *rb = ring + (ph.fb & (kRing - 1)) * kPlaneElems;
+            double *dst = sP0[MODE != 1 ? (p & 1) : 0];
+#pragma unroll
+            for (int k = 0; k < 2; k++)
+                if (lv[k]) {
+                    const double va = (double)ra[soff[k]];
+                    dst[soff[k]] = ph.fo ? lerp(va, (double)rb[soff[k]], ph.t) : va;
+                }
+        };
         for (int k = 0; k < kRing - 2; k++) issue(j_start + k);
+        if (MODE != 1) {
+            cp_async_wait<kRing - 4>();   // planes j_start, j_start + 1 have landed
+            __syncthreads();
+            stage_p0(j_start);
+        }
         for (int j = j_start; j <= j_end; j++) {
-            cp_async_wait<kRing - 4>();   // planes <= j + 1 have landed
+            if (MODE != 1) cp_async_wait<kRing - 5>();   // planes <= j + 2 have landed
+            else cp_async_wait<kRing - 4>();              // planes <= j + 1 have landed
             __syncthreads();
             issue(j + kRing - 2);          // into the slot of plane j - 2 (no longer read)
+            stage_p0(j + 1);               // its neighbours are planes <= j + 2
             if (!act) continue;
-            const PiHead pi = A0 ? load_head(ax0.pi + j) : identity_head(j);
+            const PiHead pi = A0 ? load_head<false>(piring + (j & (kRing - 1))) : identity_head(j);
             const bool coarse_node = !pi.fo && col_coarse;
             const TIn *rj = ring + (j & (kRing - 1)) * kPlaneElems;
             double mc;
             if (MODE != 1) {
-                const TIn *ra = ring + (pi.fa & (kRing - 1)) * kPlaneElems;
-                const TIn *rb = ring + (pi.fb & (kRing - 1)) * kPlaneElems;
-                // GPK: P0 along axis 0 at the corner columns, P1 along axis 1, P2 along axis 2
-                auto P0 = [&](int o) -> double {
-                    const double va = (double)ra[o];
-                    return pi.fo ? lerp(va, (double)rb[o], pi.t) : va;
-                };
-                double p1a = P0(oaa), p1b = 0.0;
-                if (A1 && b1.fo) p1a = lerp(p1a, P0(oba), b1.t);
+                // GPK: P0 (staged), P1 along axis 1, P2 along axis 2
+                const double *P0p = sP0[MODE != 1 ? (j & 1) : 0];
+                double p1a = P0p[oaa], p1b = 0.0;
+                if (A1 && b1.fo) p1a = lerp(p1a, P0p[oba], b1.t);
                 if (A2) {
-                    p1b = P0(oab);
-                    if (A1 && b1.fo) p1b = lerp(p1b, P0(obb), b1.t);
+                    p1b = P0p[oab];
+                    if (A1 && b1.fo) p1b = lerp(p1b, P0p[obb], b1.t);
                 }
                 const double pred = (A2 && b2.fo) ? lerp(p1a, p1b, b2.t) : p1a;
                 const double own = (double)rj[own_off];
@@ -353,7 +393,7 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
             } else {
                 mc = coarse_node ? 0.0 : (double)rj[own_off];
             }
-            if (A0) march_push(M, ax0.pi, n0, j, j_start, mc, emit);
+            if (A0) march_push<kRing - 1>(M, piring, n0, j, j_start, mc, emit);
             else Z0[(int64_t)j * plane + col] = mc;
         }
         cp_async_wait<0>();
