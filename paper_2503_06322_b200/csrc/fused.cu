@@ -52,6 +52,25 @@ __device__ __forceinline__ void hist_add(uint32_t *sh, unsigned long long *g, bo
     else atomicAdd(&g[key], 1ULL);
 }
 
+// One fine node's quantization (quantize.py:73-84): bin, outlier (|bin| >= dict/2, tested exactly
+// on the integral double), key zigzag in 32-bit (non-outlier bins are < 2^15), histogram.
+__device__ __forceinline__ void quant_node(double mc, const QuantOut &q, double rbin, int64_t f, int &fl,
+                                           uint32_t *sh_hist, bool sh_ok) {
+    long long b = 0;
+    if (!isfinite(mc)) fl |= 1;
+    else if (!quant_bin(mc, q.bin, rbin, b)) fl |= 2;
+    uint32_t key = 0;
+    if (b >= q.half || -b >= q.half) {   // outlier (:80-83)
+        q.obins[f] = b;
+        atomicOr(&q.omask[f >> 5], 1u << (f & 31));
+    } else {
+        const int b32 = (int)b;
+        key = (uint32_t)((b32 << 1) ^ (b32 >> 31));
+    }
+    q.keys[f] = key;
+    hist_add(sh_hist, q.hist, sh_ok, key);
+}
+
 // Per-thread description of one axis at a fine index j: coarse neighbours (fine indices fa/fb,
 // coarse indices ca/cb), weight t and whether j is a fine-only node along this axis.
 struct Nb {
@@ -375,18 +394,7 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
                         if (MODE == 0) {
                             coef[f] = mc;
                         } else {
-                            long long b = 0;
-                            if (!isfinite(mc)) fl |= 1;
-                            else if (!quant_bin(mc, q.bin, rbin, b)) fl |= 2;
-                            if (b >= q.half || -b >= q.half) {                 // outlier (:80-83)
-                                q.obins[f] = b;
-                                atomicOr(&q.omask[f >> 5], 1u << (f & 31));
-                                b = 0;
-                            }
-                            const uint32_t key =
-                                (uint32_t)(((unsigned long long)b << 1) ^ (unsigned long long)(b >> 63));
-                            q.keys[f] = key;
-                            hist_add(sh_hist, q.hist, sh_ok, key);
+                            quant_node(mc, q, rbin, f, fl, sh_hist, sh_ok);
                         }
                     }
                 }
@@ -548,17 +556,7 @@ __global__ void __launch_bounds__(256) k_level_pass1s(const TIn *__restrict__ F,
                     if (MODE == 0) {
                         coef[f] = mc;
                     } else {
-                        long long b = 0;
-                        if (!isfinite(mc)) fl |= 1;
-                        else if (!quant_bin(mc, q.bin, rbin, b)) fl |= 2;
-                        if (b >= q.half || -b >= q.half) {                 // outlier (:80-83)
-                            q.obins[f] = b;
-                            atomicOr(&q.omask[f >> 5], 1u << (f & 31));
-                            b = 0;
-                        }
-                        const uint32_t key = (uint32_t)(((unsigned long long)b << 1) ^ (unsigned long long)(b >> 63));
-                        q.keys[f] = key;
-                        hist_add(sh_hist, q.hist, sh_ok, key);
+                        quant_node(mc, q, rbin, f, fl, sh_hist, sh_ok);
                     }
                 }
             }
@@ -600,18 +598,7 @@ __global__ void __launch_bounds__(256) k_quantize_fine(const double *__restrict_
         for (int j = lo; j < hi; j++) {
             if (!(col_fo || (A0 && __ldg(ax0.pb + j) >= 0))) continue;
             const int64_t f = (int64_t)j * plane + col;
-            const double mc = __ldg(coef + f);
-            long long b = 0;
-            if (!isfinite(mc)) fl |= 1;
-            else if (!quant_bin(mc, q.bin, rbin, b)) fl |= 2;
-            if (b >= q.half || -b >= q.half) {
-                q.obins[f] = b;
-                atomicOr(&q.omask[f >> 5], 1u << (f & 31));
-                b = 0;
-            }
-            const uint32_t key = (uint32_t)(((unsigned long long)b << 1) ^ (unsigned long long)(b >> 63));
-            q.keys[f] = key;
-            hist_add(sh_hist, q.hist, sh_ok, key);
+            quant_node(__ldg(coef + f), q, rbin, f, fl, sh_hist, sh_ok);
         }
     }
     if (fl) atomicOr(q.flags, fl);
