@@ -124,6 +124,66 @@ def adaptive_schedule(n0: int, plane_bytes: int, model: ThroughputModel, transpo
     return planes
 
 
+def profile_models(arr, eb_rel: float, sizes_mb=(16, 32, 64, 128, 256), *, device: int | None = None,
+                   reps: int = 2):
+    """Fit Φ and Θ on this device (§V-C): Φ(C) = compress throughput of a device-resident
+    C-byte slab of `arr` (no copies), Θ from a pinned host-to-device copy of the largest slab.
+    Returns (ThroughputModel, TransportModel, samples)."""
+    import time
+
+    from .mgard import _as_input, mgard_compress
+
+    addr, dims, code, keep = _as_input(arr)
+    a = np.asarray(arr) if not hasattr(arr, "numpy") else arr.numpy()
+    plane_bytes = a[0].nbytes
+    ctx = _lib.default_context(device)
+    samples = []
+    import torch
+
+    dev = torch.device("cuda", ctx.device if hasattr(ctx, "device") else 0)
+    for mb in sizes_mb:
+        planes = max(1, min(a.shape[0], (mb << 20) // plane_bytes))
+        slab = torch.from_numpy(np.ascontiguousarray(a[:planes])).to(dev)
+        vr = (float(a.min()), float(a.max()))
+        sink = torch.empty(slab.numel() * slab.element_size() * 2 + (8 << 20), dtype=torch.uint8, device=dev)
+        mgard_compress(slab, eb_rel, value_range=vr, device=device, out=sink)   # warm (tables, buffers)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            mgard_compress(slab, eb_rel, value_range=vr, device=device, out=sink)   # blob stays on the device
+        torch.cuda.synchronize(dev)
+        dt = (time.perf_counter() - t0) / reps
+        samples.append((slab.numel() * slab.element_size(), slab.numel() * slab.element_size() / dt))
+        if planes == a.shape[0]:
+            break
+    big = torch.from_numpy(np.ascontiguousarray(a[: max(1, min(a.shape[0], (max(sizes_mb) << 20) // plane_bytes))]))
+    pin = big.pin_memory()
+    d = torch.empty_like(pin, device=dev)
+    d.copy_(pin, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    d.copy_(pin, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    beta = (time.perf_counter() - t0) / pin.nbytes
+    del keep
+    return fit_throughput_model(samples), TransportModel(beta), samples
+
+
+def compress_adaptive(arr, eb_rel: float, dict_size: int = 4096, value_range=None, *, models=None,
+                      c_init: int = 16 << 20, c_limit: int = 1 << 30, device: int | None = None, out=None,
+                      trace: bool = False):
+    """Algorithm 4 end to end: chunk sizes from the fitted Φ / Θ (profile_models, or `models`),
+    then the streams pipeline over that schedule.  Returns what compress_pipelined returns."""
+    a = np.asarray(arr) if not hasattr(arr, "numpy") else arr.numpy()
+    if models is None:
+        phi, theta, _ = profile_models(arr, eb_rel, device=device)
+    else:
+        phi, theta = models
+    sched = adaptive_schedule(a.shape[0], a[0].nbytes, phi, theta, c_init=c_init, c_limit=c_limit)
+    return compress_pipelined(arr, eb_rel, dict_size, value_range, chunks=sched, device=device, out=out,
+                              trace=trace)
+
+
 def overlap_ratio(trace: np.ndarray) -> float:
     """SPEC.md overlap: time during which a copy (H2D or D2H) overlaps any compute / total copy time.
     trace: (K, 6) = H2D start/end, compute start/end, D2H start/end (ms)."""

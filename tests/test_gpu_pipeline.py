@@ -87,3 +87,19 @@ def test_relative_pipeline_non_finite_raises():
     a[17, 3, 4] = np.nan
     with pytest.raises(P.ValidationError):
         PL.compress_pipelined(a, 1e-3, chunk_planes=8)
+
+
+def test_adaptive_pipeline_profiles_and_tiles(oracle):
+    """Algorithm 4 end to end: Φ profiled on the device, Θ from a pinned copy, the schedule tiles
+    dim 0 and every chunk is a reference blob."""
+    a = S.smooth_noise((200, 64, 64), seed=8)
+    phi, theta, samples = PL.profile_models(a, 1e-3, sizes_mb=(1, 2, 4))
+    assert len(samples) == 3 and phi.gamma > 0 and theta.beta_copy > 0
+    vr = (float(a.min()), float(a.max()))
+    data = PL.compress_adaptive(a, 1e-3, value_range=vr, models=(phi, theta), c_init=1 << 20)
+    h, payloads = CT.read_container(data)
+    assert sum(c.raw_size for c in h.chunks) == a.size
+    plane = a.size // a.shape[0]
+    for c, p in zip(h.chunks, payloads):
+        lo = c.raw_offset // plane
+        assert bytes(p) == oracle.mgard_compress(a[lo:lo + c.raw_size // plane], 1e-3, value_range=vr)
