@@ -88,15 +88,19 @@ def pcie_roofline(dev, mib=256, reps=3):
     d = torch.empty(n, dtype=torch.uint8, device=dev)
     out = {}
     for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
-        fn()
-        torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(reps):
+        for _ in range(2):
             fn()
-        e1.record()
-        e1.synchronize()
-        out[name] = n * reps / (e0.elapsed_time(e1) * 1e-3) / 1e9
+        torch.cuda.synchronize(dev)
+        best = 0.0
+        for _trial in range(3):   # best of 3: a one-off stall must not lower the roofline
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                fn()
+            e1.record()
+            e1.synchronize()
+            best = max(best, n * reps / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        out[name] = best
     return out
 
 
@@ -350,6 +354,14 @@ def main():
     def compress_pipe_abs():
         PL.compress_pipelined(h_in, cfg["eb"], value_range=vr_known, out=pipe_out)
 
+    # Algorithm 4: chunk sizes from Φ (device-profiled) and Θ (pinned copy) -- a one-time
+    # calibration per field shape, outside the timed region
+    models = PL.profile_models(h_in, cfg["eb"])[:2]
+    sched = PL.adaptive_schedule(a.shape[0], a[0].nbytes, *models, c_init=16 << 20, c_limit=1 << 30)
+
+    def compress_pipe_adaptive():
+        PL.compress_pipelined(h_in, cfg["eb"], value_range=vr_known, chunks=sched, out=pipe_out)
+
     def decompress_pipe():
         PL.decompress_pipelined(pipe_in, out=h_out2)
 
@@ -363,6 +375,7 @@ def main():
         pc_ms, _, _ = timed(compress_pipe, K)
         pd_ms, _, _ = timed(decompress_pipe, K)
         pa_ms, _, _ = timed(compress_pipe_abs, K)
+        pad_ms, _, _ = timed(compress_pipe_adaptive, K)
     clocks = clk.summary()
     _, ptr_c = PL.compress_pipelined(h_in, cfg["eb"], value_range=vr_abs, out=pipe_out, trace=True)
     _, ptr_d = PL.decompress_pipelined(pipe_in, out=h_out2, trace=True)
@@ -428,6 +441,9 @@ def main():
                      "decompress_pcie_roofline_frac": t_pd / (pd_ms * 1e-3),
                      "compress_abs_e2e_gbs": gbs(pa_ms), "compress_abs_ms": pa_ms,
                      "compress_abs_pcie_roofline_frac": t_pc / (pa_ms * 1e-3),
+                     "compress_adaptive_abs_e2e_gbs": gbs(pad_ms), "compress_adaptive_abs_ms": pad_ms,
+                     "compress_adaptive_abs_pcie_roofline_frac": t_pc / (pad_ms * 1e-3),
+                     "adaptive_chunks_planes": [int(x) for x in sched],
                      "chunks": int(ptr_c.shape[0]), "overlap_compress": PL.overlap_ratio(ptr_c),
                      "overlap_decompress": PL.overlap_ratio(ptr_d)},
         "pcie": {"h2d_gbs": pcie["h2d"], "d2h_gbs": pcie["d2h"], "note": "pinned cudaMemcpyAsync, 256 MiB, this box"},
