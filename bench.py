@@ -302,8 +302,10 @@ def main():
     h_blob_in = torch.from_numpy(np.frombuffer(blob_ref, np.uint8).copy()).pin_memory()
     blob_view = h_blob_in.numpy()
 
+    d_blob = torch.from_numpy(np.frombuffer(blob_ref, np.uint8).copy()).to(dev)   # device-resident blob
+
     def decompress_dev():
-        P.mgard_decompress(blob_view, out=d_out)
+        P.mgard_decompress(d_blob, out=d_out)
 
     def decompress_e2e():
         P.mgard_decompress(blob_view, out=h_out)

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <functional>
+#include <memory>
 #include <new>
 
 #include "stages.cuh"
@@ -582,11 +583,41 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
     {
         cudaStream_t s = ctx->stream;
         const uint8_t *blob = (const uint8_t *)blob_in;
-        std::vector<uint8_t> hostcopy;
-        if (classify(blob_in) == MemKind::Device) {
-            hostcopy.resize(len);
-            CUDA_CHECK(cudaMemcpy(hostcopy.data(), blob_in, len, cudaMemcpyDeviceToHost));
-            blob = hostcopy.data();
+        // A device-resident blob stays on the device: only the parts the host parses (fixed header,
+        // coarse values, Huffman header and unit offsets) are copied into a sparse host mirror at
+        // their own offsets; outliers and the packed payload are read in place.
+        std::unique_ptr<uint8_t[]> mirror;
+        if (!dev_blob && classify(blob_in) == MemKind::Device) {
+            mirror.reset(new uint8_t[len ? len : 1]);
+            const uint8_t *d = (const uint8_t *)blob_in;
+            auto pull = [&](uint64_t a, uint64_t b) {
+                b = std::min(b, len);
+                if (b > a) CUDA_CHECK(cudaMemcpy(mirror.get() + a, d + a, b - a, cudaMemcpyDeviceToHost));
+            };
+            auto u64_at = [&](uint64_t p) -> uint64_t {
+                uint64_t v = 0;
+                if (p + 8 <= len) memcpy(&v, mirror.get() + p, 8);
+                return v;
+            };
+            pull(0, 1);
+            const uint64_t rk = len ? mirror[0] : 0;
+            uint64_t p = 1 + 8 * rk + 49;                         // codec.py:44-49
+            pull(1, p + 8);
+            const uint64_t no = std::min<uint64_t>(u64_at(p), len / 16);
+            p += 8 + 16 * no;                                     // outlier arrays stay on the device
+            pull(p, p + 8);
+            const uint64_t nco = std::min<uint64_t>(u64_at(p), len / 8);
+            const uint64_t h0 = p + 8 + 8 * nco;                  // Huffman stream
+            pull(p, h0 + 10);
+            uint16_t dict = 0;
+            if (h0 + 2 <= len) memcpy(&dict, mirror.get() + h0, 2);
+            const uint64_t q = h0 + 10 + dict;
+            pull(h0 + 10, q + 4);
+            uint32_t nu = 0;
+            if (q + 4 <= len) memcpy(&nu, mirror.get() + q, 4);
+            pull(q + 4, q + 4 + 8ull * nu + 8);
+            blob = mirror.get();
+            dev_blob = d;
         }
         // codec.py:62-81 header parse; any truncation is a CorruptStreamError
         Reader r{blob, len};

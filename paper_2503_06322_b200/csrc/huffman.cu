@@ -283,7 +283,8 @@ __device__ __forceinline__ uint32_t load_be(const uint32_t *w, uint64_t i) {
 // produces the reference's error offsets.
 constexpr int kDWWarps = 8;
 constexpr int kDWStage = 33;    // padded 32-symbol staging row per lane
-constexpr int kDWWords = 1024;  // per-warp shared payload window (32768 bits: 4096 x 8-bit codes)
+// per-warp shared payload window, chosen per stream from its largest unit: 1024 / 2048 / 4096 words
+// (4096 x 8 / 16 / 32-bit codes); larger units read global memory
 
 // canonical lookup of the codeword at the top of `win` (len 0: no codeword)
 __device__ __forceinline__ uint32_t dw_lookup(uint32_t win, const uint32_t *lut, const DecTables &T,
@@ -508,11 +509,12 @@ __device__ void dw_serial_unit(const uint32_t *__restrict__ words, uint64_t limi
 // count (or that hits an invalid codeword, or max_len > 32) is a non-canonical / corrupted
 // stream: lane 0 redoes it with the reference's bit-serial walk (huffman.py:292-313), which also
 // produces the reference's error offsets.
-size_t dw_smem_bytes() {
+size_t dw_smem_bytes(int words) {
     return (size_t)kLutSize * 4 + ((sizeof(DecTables) + 15) & ~size_t(15)) +
-           (((size_t)kDWWarps * 32 * kDWStage * 2 + 15) & ~size_t(15)) + (size_t)kDWWarps * kDWWords * 4;
+           (((size_t)kDWWarps * 32 * kDWStage * 2 + 15) & ~size_t(15)) + (size_t)kDWWarps * words * 4;
 }
 
+template <int kDWWords>
 __global__ void __launch_bounds__(kDWWarps * 32) k_decode_warp(
     const uint32_t *__restrict__ words, uint64_t limit, const uint64_t *__restrict__ offs, uint64_t nsym,
     int64_t units, const DecTables *__restrict__ tabs_g, const uint32_t *__restrict__ lut_g,
@@ -651,9 +653,29 @@ void decode_begin(hpdr_ctx *ctx, const DecodeJob &job, DecodeSession &S, cudaStr
     CUDA_CHECK(cudaMemcpyAsync(S.flag, hinit, 32, cudaMemcpyHostToDevice, s));
     static bool attr = false;
     if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_decode_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dw_smem_bytes()));
+        CUDA_CHECK(cudaFuncSetAttribute(k_decode_warp<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)dw_smem_bytes(1024)));
+        CUDA_CHECK(cudaFuncSetAttribute(k_decode_warp<2048>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)dw_smem_bytes(2048)));
+        CUDA_CHECK(cudaFuncSetAttribute(k_decode_warp<4096>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)dw_smem_bytes(4096)));
         attr = true;
     }
+    // smallest window holding the largest unit (host offsets: the caller's stream)
+    uint64_t max_bits = 0;
+    {
+        const uint64_t nu = job.n_units;
+        uint64_t prev = 0;
+        for (uint64_t u = 0; u < nu; u++) {
+            uint64_t o;
+            memcpy(&o, job.offsets + 8 * u, 8);
+            if (u) max_bits = std::max(max_bits, o >= prev ? o - prev : 0);
+            prev = o;
+        }
+        if (nu) max_bits = std::max(max_bits, job.total_bits >= prev ? job.total_bits - prev : 0);
+    }
+    const uint64_t need_words = max_bits / 32 + 4;
+    S.window = need_words <= 1024 ? 1024 : need_words <= 2048 ? 2048 : 4096;
     static const bool want_stats = getenv("HPDR_DECODE_STATS") != nullptr;
     S.stats = nullptr;
     if (want_stats) {
@@ -670,12 +692,18 @@ void decode_units(const DecodeSession &S, int64_t u_lo, int64_t u_hi, bool strea
     KPROF("k_decode", (job.total_bits / 8.0 + 8.0 * S.units +
                        (double)job.n_symbols * ((job.keys ? 4 : 0) + (job.coef ? 8 : 0))) *
                           ((double)(u_hi - u_lo) / (double)S.units), s);
-    const unsigned blocks = (unsigned)std::min<int64_t>((u_hi - u_lo + kDWWarps - 1) / kDWWarps, 148 * 3);
-    k_decode_warp<<<blocks, kDWWarps * 32, dw_smem_bytes(), s>>>(
-        S.d_words, job.total_bits, S.d_off, job.n_symbols, S.units, (const DecTables *)S.d_tab,
-        (const uint32_t *)(S.d_tab + sizeof(DecTables)), (const uint32_t *)(S.d_tab + sizeof(DecTables) + kLutSize * 4),
-        job.keys, job.coef, job.bin_width, S.uerr, S.flag, (unsigned *)(S.flag + 1), S.stats, u_lo, u_hi,
-        (streamed || redo) ? S.deferred : nullptr, redo);
+    const int per_sm = S.window == 1024 ? 3 : S.window == 2048 ? 2 : 1;   // resident blocks (shared memory)
+    const unsigned blocks = (unsigned)std::min<int64_t>((u_hi - u_lo + kDWWarps - 1) / kDWWarps, 148 * per_sm);
+#define DWL(W)                                                                                                          \
+    k_decode_warp<W><<<blocks, kDWWarps * 32, dw_smem_bytes(W), s>>>(                                                    \
+        S.d_words, job.total_bits, S.d_off, job.n_symbols, S.units, (const DecTables *)S.d_tab,                         \
+        (const uint32_t *)(S.d_tab + sizeof(DecTables)), (const uint32_t *)(S.d_tab + sizeof(DecTables) + kLutSize * 4), \
+        job.keys, job.coef, job.bin_width, S.uerr, S.flag, (unsigned *)(S.flag + 1), S.stats, u_lo, u_hi,              \
+        (streamed || redo) ? S.deferred : nullptr, redo)
+    if (S.window == 1024) DWL(1024);
+    else if (S.window == 2048) DWL(2048);
+    else DWL(4096);
+#undef DWL
     LAUNCH_CHECK();
 }
 

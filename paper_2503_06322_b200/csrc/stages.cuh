@@ -97,6 +97,7 @@ struct DecodeSession {
     unsigned long long *flag = nullptr;
     int *deferred = nullptr;
     unsigned long long *stats = nullptr;
+    int window = 1024;                 // shared payload window (words per warp)
 };
 void decode_begin(hpdr_ctx *ctx, const DecodeJob &job, DecodeSession &S, cudaStream_t s, bool copy_payload);
 void decode_units(const DecodeSession &S, int64_t u_lo, int64_t u_hi, bool streamed, cudaStream_t s, int redo = 0);

@@ -148,8 +148,14 @@ def blob_info(data) -> tuple:
 
 def mgard_decompress(data, adapter=None, cache: ContextCache | None = None, *, device: int | None = None,
                      out=None) -> TensorData:
-    """Decode, dequantize and recompose on the GPU (codec.py:59-113)."""
-    buf = np.frombuffer(memoryview(data), dtype=np.uint8)
+    """Decode, dequantize and recompose on the GPU (codec.py:59-113).  ``data`` may also be a
+    CUDA uint8 tensor (a device-resident blob, read in place)."""
+    if getattr(data, "is_cuda", False):
+        addr, size = int(data.data_ptr()), int(data.numel() * data.element_size())
+        buf = data[: min(size, 128)].cpu().numpy().view(np.uint8)   # header only
+    else:
+        buf = np.frombuffer(memoryview(data), dtype=np.uint8)
+        addr, size = (buf.ctypes.data if buf.size else 0), buf.size
     code, dims, rank = blob_info(buf)
     ctx = _native(None, None, device)
     if cache is not None and code in DTYPE_FROM_CODE and 1 <= rank <= 4:
@@ -165,8 +171,8 @@ def mgard_decompress(data, adapter=None, cache: ContextCache | None = None, *, d
         res = np.empty(dims if (1 <= rank <= 4 and all(d >= 1 for d in dims)) else (max(n_elem, 1),), dtype=dt.np_dtype)
     else:
         res = out
-    check(lib().hpdr_mgard_decompress(ctx.handle, C.c_void_p(buf.ctypes.data if buf.size else 0), buf.size,
-                                      C.c_void_p(_lib.ptr(res)), int(res.nbytes)))
+    check(lib().hpdr_mgard_decompress(ctx.handle, C.c_void_p(addr), size, C.c_void_p(_lib.ptr(res)),
+                                      int(res.nbytes)))
     if out is not None:
         return out
     return TensorData(dims, dt, res)

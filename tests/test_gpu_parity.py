@@ -253,3 +253,21 @@ def test_streamed_decompress_matches_oracle(flip, oracle):
         return
     got = P.mgard_decompress(blob).values
     assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
+
+
+def test_device_resident_blob_decompress(oracle):
+    """A blob in device memory is parsed through a sparse host mirror and read in place."""
+    import torch
+
+    a = S.smooth_noise((65, 40, 33), seed=9)
+    blob = P.mgard_compress(a, 1e-3)
+    d = torch.from_numpy(np.frombuffer(blob, np.uint8).copy()).cuda()
+    y = P.mgard_decompress(d).values
+    assert np.array_equal(y.view(np.uint8), oracle.mgard_decompress(blob).view(np.uint8))
+    bad = bytearray(blob)
+    bad[len(blob) // 2] ^= 0x40
+    want = oracle.mgard_decompress(bytes(bad))
+    got = P.mgard_decompress(torch.from_numpy(np.frombuffer(bytes(bad), np.uint8).copy()).cuda()).values
+    assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
+    with pytest.raises(CorruptStreamError):
+        P.mgard_decompress(d[:60])
