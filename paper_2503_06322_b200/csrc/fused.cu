@@ -140,10 +140,10 @@ __device__ __forceinline__ T ldx(const T *p) {   // read-only-path load from glo
     return *p;
 }
 
-template <int MASK = -1, class Emit>
+template <int MASK = -1, bool NC = MASK == -1, class Emit>
 __device__ __forceinline__ void march_emit_y(March &M, const PlaneInfo *__restrict__ P, int k, double xk, double xkm1,
                                              double xkp1, bool has_up, Emit &&out) {
-    constexpr bool NC = MASK == -1;          // MASK != -1: ring of records in shared memory
+    // NC: records in global memory (read-only path); else shared (MASK != -1: a ring of records)
     const PlaneInfo *p = P + (k & MASK);
     double v = dmul(ldx<NC>(&p->md), xk);
     if (k >= 1) v = dadd(v, dmul(ldx<NC>(&p->ml), xkm1));
@@ -158,12 +158,12 @@ __device__ __forceinline__ void march_emit_y(March &M, const PlaneInfo *__restri
 }
 
 // Push x(j) (PlaneInfo table P); emits every restricted value that became computable.
-template <int MASK = -1, class Emit>
+template <int MASK = -1, bool NC = MASK == -1, class Emit>
 __device__ __forceinline__ void march_push(March &M, const PlaneInfo *__restrict__ P, int n, int j, int j_start,
                                            double x, Emit &&out) {
     // y(j-1) needs x(j-2) unless j-1 == 0: j >= 1 when the march starts at 0, else j >= j_start + 2
-    if (j >= (j_start == 0 ? 1 : j_start + 2)) march_emit_y<MASK>(M, P, j - 1, M.m1, M.m2, x, true, out);
-    if (j == n - 1 && (j > j_start || j == 0)) march_emit_y<MASK>(M, P, j, x, M.m1, 0.0, false, out);
+    if (j >= (j_start == 0 ? 1 : j_start + 2)) march_emit_y<MASK, NC>(M, P, j - 1, M.m1, M.m2, x, true, out);
+    if (j == n - 1 && (j > j_start || j == 0)) march_emit_y<MASK, NC>(M, P, j, x, M.m1, 0.0, false, out);
     M.m2 = M.m1;
     M.m1 = x;
 }
@@ -631,6 +631,7 @@ __global__ void k_quantize_coarsest(const double *__restrict__ vals, const long 
 constexpr int kP2Threads = 256;
 constexpr int kP2Out = (kP2Threads - 4) / 2;   // coarse outputs along axis 2 per block
 constexpr int kP2Ring = 8;
+constexpr int kP2MaxRows = 272;   // fine rows per pass-2 slab (<= 130 coarse outputs + stencil)
 
 template <bool A1, bool A2>
 __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__restrict__ Z0, int m0, int n1, int n2,
@@ -639,6 +640,7 @@ __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__rest
     __shared__ double sw[kP2Threads];
     __shared__ double sy[kP2Threads];
     __shared__ __align__(16) double ring[kP2Ring][kP2Threads];
+    __shared__ __align__(16) PlaneInfo ptab[A1 ? kP2MaxRows : 1];   // axis-1 records of the slab's rows
     const int t = threadIdx.x;
     const int p = p_base + blockIdx.y;
     const int nc1 = A1 ? ax1.nc : n1, nc2 = A2 ? ax2.nc : n2;
@@ -703,6 +705,17 @@ __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__rest
         j_start = c_lo;
         j_end = c_hi - 1;
     }
+    // the slab's axis-1 PlaneInfo records, loaded once (the launcher bounds the rows per slab)
+    const PlaneInfo *P1 = ax1.pi;
+    if (A1 && j_end - j_start + 1 <= kP2MaxRows) {
+        const int nrec = j_end - j_start + 1;
+        const int4 *src = reinterpret_cast<const int4 *>(ax1.pi + j_start);
+        int4 *dst = reinterpret_cast<int4 *>(ptab);
+        for (int i = t; i < nrec * 5; i += kP2Threads) dst[i] = __ldg(src + i);
+        __syncthreads();
+        P1 = ptab - j_start;   // record k at P1 + k
+    }
+    const bool p1_shared = P1 != ax1.pi;
     // each thread streams its own column: no barrier needed for the ring itself
     auto issue = [&](int r) {
         if (r <= j_end && in) cp_async<8>(&ring[r % kP2Ring][t], zp + (int64_t)r * n2 + j2);
@@ -715,8 +728,12 @@ __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__rest
         cp_async_wait<kP2Ring - 2>();   // row j has landed (own copies)
         const double x = in ? ring[j % kP2Ring][t] : 0.0;
         issue(j + kP2Ring - 1);          // into the slot of row j - 1
-        if (A1) march_push(M, ax1.pi, n1, j, j_start, x, out_row);
-        else out_row(j, x);
+        if (A1) {
+            if (p1_shared) march_push<-1, false>(M, P1, n1, j, j_start, x, out_row);
+            else march_push(M, ax1.pi, n1, j, j_start, x, out_row);
+        } else {
+            out_row(j, x);
+        }
     }
     cp_async_wait<0>();
 }
@@ -733,48 +750,80 @@ __global__ void __launch_bounds__(256) k_level_final(const double *__restrict__ 
                                                      const double *__restrict__ coef, TOut *__restrict__ D, int j_base,
                                                      int j_count) {
     __shared__ __align__(16) double ring[kFRing][256];
+    __shared__ double sP0[2][256];   // axis-0 GPK over the tile's coarse footprint, per plane (double-buffered)
     const int tid = threadIdx.y * 32 + threadIdx.x;
-    const int j2 = blockIdx.x * 32 + threadIdx.x;
-    const int j1 = blockIdx.y * 8 + threadIdx.y;
-    if (j1 >= n1 || j2 >= n2) return;   // no block-wide barriers below
-    const Nb b1 = neighbours<A1>(ax1, j1), b2 = neighbours<A2>(ax2, j2);
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
+    const int j2 = x0 + threadIdx.x, j1 = y0 + threadIdx.y;
+    const bool act = j1 < n1 && j2 < n2;
     const int nc1 = A1 ? ax1.nc : n1, nc2 = A2 ? ax2.nc : n2;
+    // coarse footprint of the tile: rows [r_lo, r_lo + R), columns [c_lo, c_lo + C)
+    const int ylast = min(y0 + 7, n1 - 1), xlast = min(x0 + 31, n2 - 1);
+    int r_lo = y0, r_hi = ylast, c_lo = x0, c_hi = xlast;
+    if (A1) {
+        r_lo = __ldg(ax1.pa + y0);
+        const int pb = __ldg(ax1.pb + ylast);
+        r_hi = max(__ldg(ax1.pa + ylast), pb);
+    }
+    if (A2) {
+        c_lo = __ldg(ax2.pa + x0);
+        const int pb = __ldg(ax2.pb + xlast);
+        c_hi = max(__ldg(ax2.pa + xlast), pb);
+    }
+    const int C = c_hi - c_lo + 1, RC = (r_hi - r_lo + 1) * C;   // <= 6 x 18 (8 x 32 when an axis is inactive)
+    const int fr = tid / max(C, 1), fc = tid - fr * max(C, 1);
+    const int64_t cplane = (int64_t)nc1 * nc2;
+    const int64_t foff = (int64_t)(r_lo + fr) * nc2 + (c_lo + fc);
+    Nb b1{}, b2{};
+    if (act) {
+        b1 = neighbours<A1>(ax1, j1);
+        b2 = neighbours<A2>(ax2, j2);
+    }
+    const int oa = (b1.ca - r_lo) * C, ob = (b1.cb - r_lo) * C, xa = b2.ca - c_lo, xb = b2.cb - c_lo;
     int lo, hi;
     slab_range(j_count, gridDim.z, blockIdx.z, lo, hi);   // fine planes [j_base, j_base + j_count)
     lo += j_base;
     hi += j_base;
     const int64_t col = (int64_t)j1 * n2 + j2;
-    const int64_t fcol = ((int64_t)__ldg(lm.m1 + j1)) * lm.D2 + __ldg(lm.m2 + j2);
+    const int64_t fcol = act ? ((int64_t)__ldg(lm.m1 + j1)) * lm.D2 + __ldg(lm.m2 + j2) : 0;
     const int64_t fplane = lm.D1 * lm.D2;
-    const int64_t cplane = (int64_t)nc1 * nc2;
     const bool col_fo = b1.fo || b2.fo;
     auto issue = [&](int j) {
-        if (j < hi) {
+        if (j < hi && act) {
             const bool fo0 = A0 && __ldg(ax0.pb + j) >= 0;
             if (fo0 || col_fo) cp_async<8>(&ring[j % kFRing][tid], coef + (int64_t)__ldg(lm.m0 + j) * fplane + fcol);
         }
         cp_async_commit();
     };
-    for (int k = 0; k < kFRing - 1; k++) issue(lo + k);
-    for (int j = lo; j < hi; j++) {
+    // P0 of plane j over the footprint (transform.py:264-268: axis 0 first)
+    auto stage = [&](int j) {
+        if (j >= hi || tid >= RC) return;
         const Nb b0 = neighbours<A0>(ax0, j);
-        auto P0 = [&](int y1, int x2) -> double {
-            const double va = __ldg(cv + (int64_t)b0.ca * cplane + (int64_t)y1 * nc2 + x2);
-            if (!b0.fo) return va;
-            return lerp(va, __ldg(cv + (int64_t)b0.cb * cplane + (int64_t)y1 * nc2 + x2), b0.t);
-        };
-        auto P1 = [&](int x2) -> double {
-            const double va = P0(b1.ca, x2);
-            if (!b1.fo) return va;
-            return lerp(va, P0(b1.cb, x2), b1.t);
-        };
-        double pred = P1(b2.ca);
-        if (b2.fo) pred = lerp(pred, P1(b2.cb), b2.t);
-        const bool coarse_node = !b0.fo && !col_fo;
+        const double va = __ldg(cv + (int64_t)b0.ca * cplane + foff);
+        sP0[j & 1][tid] = b0.fo ? lerp(va, __ldg(cv + (int64_t)b0.cb * cplane + foff), b0.t) : va;
+    };
+    for (int k = 0; k < kFRing - 1; k++) issue(lo + k);
+    stage(lo);
+    for (int j = lo; j < hi; j++) {
+        __syncthreads();                 // P0(j) visible; buffer (j + 1) & 1 free
+        stage(j + 1);
+        const bool fo0 = A0 && __ldg(ax0.pb + j) >= 0;
+        double pred = 0.0;
+        if (act) {
+            const double *P = sP0[j & 1];
+            double p1a = P[oa + xa];
+            if (b1.fo) p1a = lerp(p1a, P[ob + xa], b1.t);
+            pred = p1a;
+            if (b2.fo) {
+                double p1b = P[oa + xb];
+                if (b1.fo) p1b = lerp(p1b, P[ob + xb], b1.t);
+                pred = lerp(p1a, p1b, b2.t);
+            }
+        }
+        const bool coarse_node = !fo0 && !col_fo;
         cp_async_wait<kFRing - 2>();
         const double mc = coarse_node ? 0.0 : ring[j % kFRing][tid];
         issue(j + kFRing - 1);
-        D[(int64_t)j * n1 * n2 + col] = (TOut)dadd(pred, mc);
+        if (act) D[(int64_t)j * n1 * n2 + col] = (TOut)dadd(pred, mc);
     }
     cp_async_wait<0>();
 }
@@ -814,7 +863,8 @@ void launch_pass2(int act, const double *Z0, int m0, int n1, int n2, const DevAx
     const int nc1 = A1 ? a1.nc : n1, nc2 = A2 ? a2.nc : n2;
     const unsigned gx = A2 ? (unsigned)((nc2 + kP2Out - 1) / kP2Out) : (unsigned)((n2 + kP2Threads - 1) / kP2Threads);
     const int64_t cols = (int64_t)m0 * gx * kP2Threads;
-    const int slabs = slabs_for(cols, nc1);
+    // enough slabs that a slab's rows fit the shared record table (<= 130 coarse rows each)
+    const int slabs = std::max(slabs_for(cols, nc1), A1 ? (nc1 + 129) / 130 : 1);
     dim3 grid(gx, (unsigned)p_count, (unsigned)slabs);
     if (A1 && A2) k_level_pass2<true, true><<<grid, kP2Threads, 0, s>>>(Z0, m0, n1, n2, a1, a2, B, slabs, p_base);
     else if (A1) k_level_pass2<true, false><<<grid, kP2Threads, 0, s>>>(Z0, m0, n1, n2, a1, a2, B, slabs, p_base);
