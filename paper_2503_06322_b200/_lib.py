@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 import threading
 
 import numpy as np
@@ -162,14 +163,30 @@ class DeviceContext:
 _tls = threading.local()
 
 
-def default_device() -> int:
+def default_device(obj=None) -> int:
+    """The GPU a call runs on: a CUDA tensor argument's own device, else HPDR_DEVICE, else torch's
+    current device (torch.cuda.set_device, one process per GPU), else LOCAL_RANK, else 0."""
+    dev = getattr(obj, "device", None)
+    if getattr(dev, "type", None) == "cuda" and dev.index is not None:
+        return int(dev.index)
     env = os.environ.get("HPDR_DEVICE")
-    return int(env) if env else 0
+    if env:
+        return int(env)
+    t = sys.modules.get("torch")
+    if t is not None:
+        try:
+            if t.cuda.is_initialized():
+                return int(t.cuda.current_device())
+        except Exception:   # noqa: BLE001 - torch without CUDA
+            pass
+    lr = os.environ.get("LOCAL_RANK")
+    return int(lr) if lr else 0
 
 
-def default_context(device: int | None = None) -> DeviceContext:
-    """Per-thread, per-device persistent context (a context is never shared across threads)."""
-    device = default_device() if device is None else int(device)
+def default_context(device: int | None = None, obj=None) -> DeviceContext:
+    """Per-thread, per-device persistent context (a context is never shared across threads).
+    device None: default_device(obj) (obj: the call's tensor argument, if any)."""
+    device = default_device(obj) if device is None else int(device)
     ctxs = getattr(_tls, "ctxs", None)
     if ctxs is None:
         ctxs = _tls.ctxs = {}

@@ -60,10 +60,10 @@ class QuantizedSet:
 
 
 # ----------------------------------------------------------------------------- helpers
-def _native(cache: ContextCache | None, key: ContextKey | None, device: int | None):
+def _native(cache: ContextCache | None, key: ContextKey | None, device: int | None, obj=None):
     if cache is not None and key is not None:
         return cache.acquire(key).native
-    return _lib.default_context(device)
+    return _lib.default_context(device, obj)
 
 
 def _as_input(u):
@@ -118,7 +118,7 @@ def mgard_compress(u, eb_rel: float, dict_size: int = DEFAULT_DICT_SIZE, adapter
     if cache is not None:
         key = ContextKey.make("mgard", dims, DTYPE_FROM_CODE[code].value, eb_rel=float(eb_rel),
                               dict_size=int(dict_size))
-    ctx = _native(cache, key, device)
+    ctx = _native(cache, key, device, u if getattr(u, "is_cuda", False) else out)
     has = value_range is not None
     r0, r1 = (float(value_range[0]), float(value_range[1])) if has else (0.0, 0.0)
     n = C.c_uint64()
@@ -157,7 +157,7 @@ def mgard_decompress(data, adapter=None, cache: ContextCache | None = None, *, d
         buf = np.frombuffer(memoryview(data), dtype=np.uint8)
         addr, size = (buf.ctypes.data if buf.size else 0), buf.size
     code, dims, rank = blob_info(buf)
-    ctx = _native(None, None, device)
+    ctx = _native(None, None, device, data if getattr(data, "is_cuda", False) else out)
     if cache is not None and code in DTYPE_FROM_CODE and 1 <= rank <= 4:
         # the reference keys the context by the stored eb_rel / dict_size (codec.py:88-93)
         hdr = 1 + 8 * rank

@@ -136,7 +136,7 @@ def profile_models(arr, eb_rel: float, sizes_mb=(16, 32, 64, 128, 256), *, devic
     addr, dims, code, keep = _as_input(arr)
     a = np.asarray(arr) if not hasattr(arr, "numpy") else arr.numpy()
     plane_bytes = a[0].nbytes
-    ctx = _lib.default_context(device)
+    ctx = _lib.default_context(device, arr if getattr(arr, 'is_cuda', False) else None)
     samples = []
     import torch
 

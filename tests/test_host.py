@@ -122,3 +122,33 @@ def test_oracle_matches_reference_at_config_scale(oracle):
     c = cfg["C3_velocity_x_129_1e-05"]   # 63% outliers, blob larger than the input
     blob = oracle.mgard_compress(S.nyx_like((129,) * 3, "velocity_x"), 1e-5)
     assert hashlib.sha256(blob).hexdigest() == c["blob_sha"]
+
+
+def test_default_device_follows_process_placement(monkeypatch):
+    """One process per GPU: a call without device= runs on the rank's GPU (HPDR_DEVICE, then
+    torch's current device once CUDA is initialised, then LOCAL_RANK), or on a tensor's own."""
+    from paper_2503_06322_b200 import _lib
+
+    monkeypatch.delenv("HPDR_DEVICE", raising=False)
+    monkeypatch.setenv("LOCAL_RANK", "3")
+    assert _lib.default_device() in (3, 0) if _torch_cuda_initialized() else _lib.default_device() == 3
+    monkeypatch.setenv("HPDR_DEVICE", "5")
+    assert _lib.default_device() == 5
+
+    class FakeDev:
+        type, index = "cuda", 6
+
+    class FakeTensor:
+        device = FakeDev()
+
+    assert _lib.default_device(FakeTensor()) == 6
+
+
+def _torch_cuda_initialized():
+    import sys
+
+    t = sys.modules.get("torch")
+    try:
+        return bool(t is not None and t.cuda.is_initialized())
+    except Exception:   # noqa: BLE001
+        return False
