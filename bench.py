@@ -244,10 +244,17 @@ def main():
     import paper_2503_06322_b200 as P
     from paper_2503_06322_b200 import _lib
 
+    # HPDR_BENCH_SAME_GPU=1 (testing the multi-rank path on a 1-GPU box): every rank on GPU 0,
+    # metadata collectives over gloo
+    if os.environ.get("HPDR_BENCH_SAME_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if os.environ.get("HPDR_BENCH_SAME_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:
