@@ -595,10 +595,20 @@ __global__ void __launch_bounds__(256) k_quantize_fine(const double *__restrict_
         int lo, hi;
         slab_range(n0, gridDim.z, blockIdx.z, lo, hi);
         const int64_t plane = (int64_t)n1 * n2, col = (int64_t)j1 * n2 + j2;
-        for (int j = lo; j < hi; j++) {
-            if (!(col_fo || (A0 && __ldg(ax0.pb + j) >= 0))) continue;
-            const int64_t f = (int64_t)j * plane + col;
-            quant_node(__ldg(coef + f), q, rbin, f, fl, sh_hist, sh_ok);
+        // 8 planes' coefficients in flight per thread before any is quantized (latency-bound otherwise)
+        constexpr int U = 8;
+        for (int j0 = lo; j0 < hi; j0 += U) {
+            double v[U];
+            bool use[U];
+#pragma unroll
+            for (int k = 0; k < U; k++) {
+                const int j = j0 + k;
+                use[k] = j < hi && (col_fo || (A0 && __ldg(ax0.pb + j) >= 0));
+                v[k] = use[k] ? __ldg(coef + (int64_t)j * plane + col) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < U; k++)
+                if (use[k]) quant_node(v[k], q, rbin, (int64_t)(j0 + k) * plane + col, fl, sh_hist, sh_ok);
         }
     }
     if (fl) atomicOr(q.flags, fl);
