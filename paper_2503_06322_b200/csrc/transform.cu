@@ -46,13 +46,26 @@ __global__ void k_minmax(const void *__restrict__ in, int dtype, int64_t n, unsi
     int nan = 0;
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (; i < n; i += stride) {
-        double v = dtype == 0 ? (double)((const float *)in)[i] : ((const double *)in)[i];
-        if (v != v) { nan = 1; continue; }
-        unsigned long long k = ord_key(v);
+    auto fold = [&](double v) {
+        if (v != v) {
+            nan = 1;
+            return;
+        }
+        const unsigned long long k = ord_key(v);
         mn = k < mn ? k : mn;
         mx = k > mx ? k : mx;
+    };
+    // 8 independent loads in flight per thread (the streamed chunks are small: latency-bound otherwise)
+    constexpr int U = 8;
+    for (; i + (U - 1) * stride < n; i += U * stride) {
+        double v[U];
+#pragma unroll
+        for (int k = 0; k < U; k++)
+            v[k] = dtype == 0 ? (double)__ldg((const float *)in + i + k * stride) : __ldg((const double *)in + i + k * stride);
+#pragma unroll
+        for (int k = 0; k < U; k++) fold(v[k]);
     }
+    for (; i < n; i += stride) fold(dtype == 0 ? (double)((const float *)in)[i] : ((const double *)in)[i]);
     for (int o = 16; o; o >>= 1) {
         unsigned long long a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
         mn = a < mn ? a : mn;
