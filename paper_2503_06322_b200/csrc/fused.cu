@@ -417,6 +417,185 @@ __global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, 
     }
 }
 
+// ---------------------------------------------------------------------------------- pass 1, 2 rows/thread
+// k_level_pass1 with a 32 x 16 column tile: each thread owns rows j1 and j1 + 8, so the per-plane
+// work that does not depend on the column (barrier, ring issue, PlaneInfo reads, march control) is
+// shared by two nodes.  Same arithmetic, same order: bit-identical results.
+constexpr int kTY2 = 2 * kTY, kHY2 = kTY2 + 2, kPlane2 = kHX * kHY2;   // 612 elements per plane
+
+template <int MODE, bool A0, bool A1, bool A2, typename TIn>
+__global__ void __launch_bounds__(256) k_level_pass1_2r(const TIn *__restrict__ F, int n0, int n1, int n2,
+                                                        DevAxis ax0, DevAxis ax1, DevAxis ax2, LevelMap lm,
+                                                        double *__restrict__ coef, const double *__restrict__ coef_in,
+                                                        double *__restrict__ Z0, double *__restrict__ Cg, QuantOut q,
+                                                        int c_base, int c_count) {
+    constexpr int PE = MODE == 1 ? kTX * kTY2 : kPlane2;   // ring slot: own elements only in MODE 1
+    __shared__ __align__(16) TIn ring[kRing * PE];
+    __shared__ double sP0[MODE != 1 ? 2 : 1][MODE != 1 ? kPlane2 : 1];
+    __shared__ __align__(16) PlaneInfo piring[kRing];
+    __shared__ uint32_t sh_hist[MODE == 2 ? kSmemHist : 1];
+    const bool sh_ok = MODE == 2 && q.dict <= kSmemHist;
+    const double rbin = MODE == 2 ? 1.0 / q.bin : 0.0;
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+    if (MODE == 2 && sh_ok)
+        for (uint32_t k = tid; k < q.dict; k += 256) sh_hist[k] = 0;
+    const int x0 = blockIdx.x * kTX - 1, y0 = blockIdx.y * kTY2 - 1;   // tile origin incl. halo
+    const int j2 = x0 + 1 + tx;
+    const int nc0 = A0 ? ax0.nc : n0;
+    int c_lo, c_hi;
+    slab_range(c_count, gridDim.z, blockIdx.z, c_lo, c_hi);
+    c_lo += c_base;
+    c_hi += c_base;
+    int fl = 0;
+    if (c_lo < c_hi) {   // uniform across the block
+        int j_start, j_end, own_lo, own_hi;
+        slab_planes<A0>(ax0, n0, nc0, c_lo, c_hi, j_start, j_end, own_lo, own_hi);
+        const int64_t plane = (int64_t)n1 * n2;
+        const int64_t fplane = lm.D1 * lm.D2;
+        const int nc1 = A1 ? ax1.nc : n1, nc2 = A2 ? ax2.nc : n2;
+        const Nb b2 = j2 < n2 ? neighbours<A2>(ax2, j2) : Nb{};
+        const int64_t fcol2 = j2 < n2 ? (int64_t)__ldg(lm.m2 + j2) : 0;
+        // per-row state (rows j1 = y0 + 1 + ty + 8 r)
+        int j1r[2], own_off[2], oaa[2], oba[2], oab[2], obb[2];
+        bool act[2], col_coarse[2];
+        int64_t col[2], fcol[2], cgcol[2];
+        Nb b1[2];
+        March M[2];
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+            const int j1 = y0 + 1 + ty + kTY * r;
+            j1r[r] = j1;
+            act[r] = j1 < n1 && j2 < n2;
+            own_off[r] = MODE == 1 ? (ty + kTY * r) * kTX + tx : (ty + kTY * r + 1) * kHX + tx + 1;
+            col[r] = (int64_t)j1 * n2 + j2;
+            fcol[r] = act[r] ? ((int64_t)__ldg(lm.m1 + j1)) * lm.D2 + fcol2 : 0;
+            b1[r] = act[r] ? neighbours<A1>(ax1, j1) : Nb{};
+            oaa[r] = (b1[r].fa - y0) * kHX + (b2.fa - x0);
+            oba[r] = (b1[r].fb - y0) * kHX + (b2.fa - x0);
+            oab[r] = (b1[r].fa - y0) * kHX + (b2.fb - x0);
+            obb[r] = (b1[r].fb - y0) * kHX + (b2.fb - x0);
+            cgcol[r] = (int64_t)b1[r].ca * nc2 + b2.ca;
+            col_coarse[r] = !b1[r].fo && !b2.fo;
+            march_init(M[r], c_lo, c_hi);
+        }
+        // this thread's share of each plane load: three tile elements (halo included)
+        int soff[3];
+        int64_t goff[3];
+        bool lv[3];
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            const int e = tid + k * 256;
+            const int yy = e / kHX, xx = e - yy * kHX;
+            const int gy = y0 + yy, gx = x0 + xx;
+            lv[k] = MODE != 1 && e < kPlane2 && gy >= 0 && gy < n1 && gx >= 0 && gx < n2;
+            soff[k] = e;
+            goff[k] = (int64_t)gy * n2 + gx;
+        }
+        const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+        const unsigned pir_s = (unsigned)__cvta_generic_to_shared(piring) + (unsigned)tid * 16u;
+        const TIn *gp[3];
+#pragma unroll
+        for (int k = 0; k < 3; k++) gp[k] = MODE == 1 ? nullptr : F + goff[k] + (int64_t)j_start * plane;
+        auto issue = [&](int p) {
+            if (p <= j_end) {
+                if (A0 && tid < 5)
+                    cp_async_s<16>(pir_s + (unsigned)(p & (kRing - 1)) * (unsigned)sizeof(PlaneInfo),
+                                   reinterpret_cast<const char *>(ax0.pi + p) + tid * 16);
+                const unsigned so = ring_s + (unsigned)(p & (kRing - 1)) * (unsigned)(PE * sizeof(TIn));
+                if (MODE == 1) {
+                    const int64_t fb = (int64_t)__ldg(lm.m0 + p) * fplane;
+#pragma unroll
+                    for (int r = 0; r < 2; r++)
+                        if (act[r])
+                            cp_async_s<sizeof(TIn)>(so + own_off[r] * (unsigned)sizeof(TIn),
+                                                    (const TIn *)(coef_in + fb + fcol[r]));
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 3; k++) {
+                        if (lv[k]) cp_async_s<sizeof(TIn)>(so + soff[k] * (unsigned)sizeof(TIn), gp[k]);
+                        gp[k] += plane;
+                    }
+                }
+            }
+            cp_async_commit();
+        };
+        auto stage_p0 = [&](int p) {
+            if (MODE == 1 || p > j_end) return;
+            const PiHead ph = A0 ? load_head<false>(piring + (p & (kRing - 1))) : identity_head(p);
+            const TIn *ra = ring + (ph.fa & (kRing - 1)) * PE;
+            const TIn *rb = ring + (ph.fb & (kRing - 1)) * PE;
+            double *dst = sP0[MODE != 1 ? (p & 1) : 0];
+#pragma unroll
+            for (int k = 0; k < 3; k++)
+                if (lv[k]) {
+                    const double va = (double)ra[soff[k]];
+                    dst[soff[k]] = ph.fo ? lerp(va, (double)rb[soff[k]], ph.t) : va;
+                }
+        };
+        for (int k = 0; k < kRing - 2; k++) issue(j_start + k);
+        if (MODE != 1) {
+            cp_async_wait<kRing - 4>();
+            __syncthreads();
+            stage_p0(j_start);
+        }
+        for (int j = j_start; j <= j_end; j++) {
+            if (MODE != 1) cp_async_wait<kRing - 5>();   // planes <= j + 2 have landed
+            else cp_async_wait<kRing - 4>();              // planes <= j + 1 have landed
+            __syncthreads();
+            issue(j + kRing - 2);
+            stage_p0(j + 1);
+            const PiHead pi = A0 ? load_head<false>(piring + (j & (kRing - 1))) : identity_head(j);
+            const TIn *rj = ring + (j & (kRing - 1)) * PE;
+            const bool own_plane = j >= own_lo && j < own_hi;
+            const int64_t fplane_j = own_plane ? (int64_t)__ldg(lm.m0 + j) * fplane : 0;
+            const double *P0p = sP0[MODE != 1 ? (j & 1) : 0];
+#pragma unroll
+            for (int r = 0; r < 2; r++) {
+                if (!act[r]) continue;
+                const bool coarse_node = !pi.fo && col_coarse[r];
+                double mc;
+                if (MODE != 1) {
+                    double p1a = P0p[oaa[r]], p1b = 0.0;
+                    if (A1 && b1[r].fo) p1a = lerp(p1a, P0p[oba[r]], b1[r].t);
+                    if (A2) {
+                        p1b = P0p[oab[r]];
+                        if (A1 && b1[r].fo) p1b = lerp(p1b, P0p[obb[r]], b1[r].t);
+                    }
+                    const double pred = (A2 && b2.fo) ? lerp(p1a, p1b, b2.t) : p1a;
+                    const double own = (double)rj[own_off[r]];
+                    mc = dsub(own, pred);
+                    if (own_plane) {
+                        if (coarse_node) {
+                            const int c0 = A0 ? pi.ca : j;
+                            Cg[(int64_t)c0 * nc1 * nc2 + cgcol[r]] = own;
+                        } else {
+                            const int64_t f = fplane_j + fcol[r];
+                            if (MODE == 0) coef[f] = mc;
+                            else quant_node(mc, q, rbin, f, fl, sh_hist, sh_ok);
+                        }
+                    }
+                } else {
+                    mc = coarse_node ? 0.0 : (double)rj[own_off[r]];
+                }
+                double *zc = Z0 + col[r];
+                auto emit = [&](int c, double z) { zc[(int64_t)c * plane] = z; };
+                if (A0) march_push<kRing - 1>(M[r], piring, n0, j, j_start, mc, emit);
+                else zc[(int64_t)j * plane] = mc;
+            }
+        }
+        cp_async_wait<0>();
+    }
+    if (MODE == 2) {
+        if (fl) atomicOr(q.flags, fl);
+        __syncthreads();
+        if (sh_ok)
+            for (uint32_t k = tid; k < q.dict; k += 256) {
+                const uint32_t c = sh_hist[k];
+                if (c) atomicAdd(&q.hist[k], (unsigned long long)c);
+            }
+    }
+}
+
 // ---------------------------------------------------------------------------------- pass 1 (decompose)
 // Same contract as k_level_pass1 MODE 0 / 2, with the GPK interpolation evaluated separably
 // inside the tile, in the reference's axis order (transform.py:264-268):
@@ -849,8 +1028,21 @@ void launch_pass1(int act, const TIn *F, int n0, int n1, int n2, const DevAxis &
                   const DevAxis &a2, const LevelMap &lm, double *coef, const double *coef_in, double *Z0, double *Cg,
                   const QuantOut &q, int c_base, int c_count, cudaStream_t s) {
     if (c_count <= 0) return;
-    dim3 grid((n2 + kTX - 1) / kTX, (n1 + kTY - 1) / kTY, slabs_for((int64_t)n1 * n2, c_count));
     dim3 block(kTX, kTY);
+    // two rows per thread for the all-active 3-D recompose transition (ncu at 513^3: 458 vs 509 us;
+    // the quantizing decompose pass is faster with one row, 1297 vs 1466 us: register pressure)
+    static const bool one_row = getenv("HPDR_P1_ONE_ROW") != nullptr;
+    static const bool two_row_q = getenv("HPDR_P1_TWO_ROW") != nullptr;
+    if constexpr (MODE == 1 || sizeof(TIn) == 4) {   // static shared memory < 48 KB
+        if ((MODE == 1 || two_row_q) && !one_row && act == 7) {
+            dim3 grid2((n2 + kTX - 1) / kTX, (n1 + kTY2 - 1) / kTY2, slabs_for((int64_t)n1 * n2, c_count));
+            k_level_pass1_2r<MODE, true, true, true, TIn><<<grid2, block, 0, s>>>(
+                F, n0, n1, n2, a0, a1, a2, lm, coef, coef_in, Z0, Cg, q, c_base, c_count);
+            LAUNCH_CHECK();
+            return;
+        }
+    }
+    dim3 grid((n2 + kTX - 1) / kTX, (n1 + kTY - 1) / kTY, slabs_for((int64_t)n1 * n2, c_count));
     static const bool separable = getenv("HPDR_P1_SEPARABLE") != nullptr;
 #define P1L(M)                                                                                                     \
     case M:                                                                                                        \
