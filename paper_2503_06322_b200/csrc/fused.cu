@@ -52,20 +52,34 @@ __device__ __forceinline__ void hist_add(uint32_t *sh, unsigned long long *g, bo
     else atomicAdd(&g[key], 1ULL);
 }
 
-// One fine node's quantization (quantize.py:73-84): bin, outlier (|bin| >= dict/2, tested exactly
-// on the integral double), key zigzag in 32-bit (non-outlier bins are < 2^15), histogram.
+// One fine node's quantization (quantize.py:73-84), in the double domain: r = rint(c / bin) as an
+// integral double (quant_bin's verified reciprocal product, IEEE division in the rare tie band),
+// outlier iff |r| >= dict/2, key = zigzag(r) (exact: non-outlier |r| < 2^15), histogram.
 __device__ __forceinline__ void quant_node(double mc, const QuantOut &q, double rbin, int64_t f, int &fl,
                                            uint32_t *sh_hist, bool sh_ok) {
-    long long b = 0;
-    if (!isfinite(mc)) fl |= 1;
-    else if (!quant_bin(mc, q.bin, rbin, b)) fl |= 2;
+    double r = 0.0;
+    if (!isfinite(mc)) {
+        fl |= 1;
+    } else {
+        const double qa = dmul(mc, rbin);
+        r = rint(qa);
+        const double dist = 0.5 - fabs(dsub(qa, r));
+        if (!(dist > fabs(qa) * 0x1p-49 && fabs(qa) < 0x1p61)) {
+            const double sc = mc / q.bin;
+            if (fabs(sc) >= 4611686018427387904.0) {
+                fl |= 2;
+                r = 0.0;
+            } else {
+                r = rint(sc);
+            }
+        }
+    }
     uint32_t key = 0;
-    if (b >= q.half || -b >= q.half) {   // outlier (:80-83)
-        q.obins[f] = b;
+    if (fabs(r) >= (double)q.half) {   // outlier (:80-83)
+        q.obins[f] = (long long)r;
         atomicOr(&q.omask[f >> 5], 1u << (f & 31));
     } else {
-        const int b32 = (int)b;
-        key = (uint32_t)((b32 << 1) ^ (b32 >> 31));
+        key = (uint32_t)(r >= 0.0 ? 2.0 * r : -2.0 * r - 1.0);   // zigzag (quantize.py:24-31)
     }
     q.keys[f] = key;
     hist_add(sh_hist, q.hist, sh_ok, key);
