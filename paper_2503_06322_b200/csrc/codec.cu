@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <functional>
 #include <memory>
@@ -106,7 +107,12 @@ void huffman_stage(hpdr_ctx *ctx, const uint32_t *d_keys, int64_t n, uint32_t di
     std::vector<uint8_t> lens(dict);
     std::vector<uint32_t> codes(dict);
     std::string err;
+    static const bool tcb = getenv("HPDR_PHASES") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     int rc = build_codebook(hist.data(), dict, lens.data(), codes.data(), err);
+    if (tcb)
+        fprintf(stderr, "[codebook] %.1f us\n",
+                std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
     if (rc == HPDR_ERR_OVERFLOW) fail(rc, "Python integer out of bounds for uint32");
     if (rc) fail(rc, err);
     mid.insert(mid.end(), lens.begin(), lens.end());
@@ -455,6 +461,7 @@ void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uin
         const void *d_in = streamed ? nullptr : device_input(ctx, in, (size_t)N * itemsize(dtype), "input", s);
         double u_min = range_min, u_max = range_max;
         if (!has_range && !streamed) minmax_device(ctx, d_in, dtype, N, &u_min, &u_max, s);
+        phase_mark("minmax", s);
         uint32_t *keys = (uint32_t *)ctx->dbuf("keys", N * 4 + 64);
         QuantResult q;
         const double *d_coarse;

@@ -819,6 +819,7 @@ const double *decompose_fused(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int d
         const DevStep &st = p.steps[st_i];
         const void *F = st_i == 0 ? d_in : (const void *)level_ptr(b, p, st_i);
         double *Dn = level_ptr(b, p, st_i + 1);
+        if (st_i == 1) phase_mark("level0_done", s);
         if (q) fused_pass1_quantize(p, st_i, F, st_i == 0 && dtype == 0, *q, Z0, b.cg, s);
         else fused_pass1_decompose(p, st_i, F, st_i == 0 && dtype == 0, coef, Z0, b.cg, s);
         fused_pass2(p, st_i, Z0, b.t0, s);
