@@ -550,6 +550,49 @@ __global__ void k_selftest_div(uint64_t n, uint64_t seed, unsigned long long *mi
     if (f) atomicAdd(fallback, f);
 }
 
+// All Thomas solves of one small coarse grid in a single CTA (grid staged in shared memory): the
+// axes in order with a barrier between them (transform.py:259-260), each line by one thread with the
+// same recurrence and rounding as k_thomas_reg.  Replaces up to 3 latency-bound launches per small
+// level (the coarse end of every hierarchy, and every level of a thin pipeline chunk).
+constexpr int kThomasSmallMax = 16384;   // doubles (128 KB of shared memory)
+
+struct AxesArg {
+    DevAxis ax[4];
+};
+
+__global__ void __launch_bounds__(512) k_thomas_small(double *__restrict__ arr, Shape4 sh, AxesArg A) {
+    extern __shared__ double g[];
+    const int64_t N = sh.size();
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) g[i] = arr[i];
+    __syncthreads();
+    for (int a = 0; a < 4; a++) {
+        const DevAxis &ax = A.ax[a];
+        if (!ax.active) continue;
+        int64_t outer = 1, inner = 1;
+        for (int d = 0; d < a; d++) outer *= sh.n[d];
+        for (int d = a + 1; d < 4; d++) inner *= sh.n[d];
+        const int n = ax.nc;
+        const int64_t lines = outer * inner;
+        for (int64_t ln = threadIdx.x; ln < lines; ln += blockDim.x) {
+            const int64_t p = ln / inner, q = ln - p * inner;
+            double *x = g + p * (int64_t)n * inner + q;
+            double prev = x[0];
+            for (int i = 1; i < n; i++) {
+                prev = dsub(x[(int64_t)i * inner], dmul(__ldg(ax.tw + i), prev));
+                x[(int64_t)i * inner] = prev;
+            }
+            double last = ddiv(prev, __ldg(ax.tb + n - 1));
+            x[(int64_t)(n - 1) * inner] = last;
+            for (int i = n - 2; i >= 0; i--) {
+                last = ddiv(dsub(x[(int64_t)i * inner], dmul(__ldg(ax.tu + i), last)), __ldg(ax.tb + i));
+                x[(int64_t)i * inner] = last;
+            }
+        }
+        __syncthreads();
+    }
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) arr[i] = g[i];
+}
+
 // ---------------------------------------------------------------- elementwise
 __global__ void k_add(const double *__restrict__ a, const double *__restrict__ b, double *__restrict__ o, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -823,9 +866,7 @@ const double *decompose_fused(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int d
         if (q) fused_pass1_quantize(p, st_i, F, st_i == 0 && dtype == 0, *q, Z0, b.cg, s);
         else fused_pass1_decompose(p, st_i, F, st_i == 0 && dtype == 0, coef, Z0, b.cg, s);
         fused_pass2(p, st_i, Z0, b.t0, s);
-        Shape4 sh = st.csh;
-        for (int a = 0; a < 4; a++)
-            if (st.ax[a].active) thomas(b.t0, sh, a, st.ax[a], s);
+        thomas_all(p, st_i, b.t0, s);
         const int64_t nc = st.csh.size();
         KPROF("k_add", 24.0 * nc, s);
         k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, Dn, nc);   // coarse + corr
@@ -934,9 +975,7 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
     phase_mark("fine_quantized", s);
     // the rest of transition 0 (IPK + coarse update) and the coarser levels
     {
-        Shape4 sh = st0.csh;
-        for (int a = 0; a < 4; a++)
-            if (st0.ax[a].active) thomas(b.t0, sh, a, st0.ax[a], s);
+        thomas_all(p, 0, b.t0, s);
         const int64_t nc = st0.csh.size();
         KPROF("k_add", 24.0 * nc, s);
         k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, level_ptr(b, p, 1), nc);
@@ -946,9 +985,7 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
         const DevStep &st = p.steps[st_i];
         fused_pass1_quantize(p, st_i, level_ptr(b, p, st_i), false, q, Z0, b.cg, s);
         fused_pass2(p, st_i, Z0, b.t0, s);
-        Shape4 sh = st.csh;
-        for (int a = 0; a < 4; a++)
-            if (st.ax[a].active) thomas(b.t0, sh, a, st.ax[a], s);
+        thomas_all(p, st_i, b.t0, s);
         const int64_t nc = st.csh.size();
         KPROF("k_add", 24.0 * nc, s);
         k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, level_ptr(b, p, st_i + 1), nc);
@@ -1070,6 +1107,21 @@ int64_t z0_elems(const DevPlan &p, int st_i) {
 void thomas_all(const DevPlan &p, int st_i, double *T, cudaStream_t s) {
     const DevStep &st = p.steps[st_i];
     Shape4 sh = st.csh;
+    static const bool no_small = getenv("HPDR_THOMAS_NOSMALL") != nullptr;
+    if (!no_small && sh.size() <= kThomasSmallMax) {
+        static bool attr = false;
+        if (!attr) {
+            CUDA_CHECK(cudaFuncSetAttribute(k_thomas_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            kThomasSmallMax * 8));
+            attr = true;
+        }
+        AxesArg A;
+        for (int a = 0; a < 4; a++) A.ax[a] = st.ax[a];
+        KPROF("k_thomas_small", 16.0 * sh.size(), s);
+        k_thomas_small<<<1, 512, (size_t)sh.size() * 8, s>>>(T, sh, A);
+        LAUNCH_CHECK();
+        return;
+    }
     for (int a = 0; a < 4; a++)
         if (st.ax[a].active) thomas(T, sh, a, st.ax[a], s);
 }
@@ -1160,9 +1212,7 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
         } else {
             fused_pass1_recompose(p, st_i, coef, Z0, s);
             fused_pass2(p, st_i, Z0, b.t0, s);
-            Shape4 sh = st.csh;
-            for (int a = 0; a < 4; a++)
-                if (st.ax[a].active) thomas(b.t0, sh, a, st.ax[a], s);
+            thomas_all(p, st_i, b.t0, s);
         }
         const int64_t nc = st.csh.size();
         {
