@@ -380,7 +380,8 @@ int hpdr_ctx_create(int device, hpdr_ctx **out) {
         CUDA_CHECK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi_pri));
         CUDA_CHECK(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
         CUDA_CHECK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
-        CUDA_CHECK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, lo_pri));
+        static const bool aux_high = getenv("HPDR_AUX_HIGH") != nullptr;
+        CUDA_CHECK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, aux_high ? hi_pri : lo_pri));
         for (auto &x : c->side) CUDA_CHECK(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, hi_pri));
         *out = c;
         return HPDR_OK;
