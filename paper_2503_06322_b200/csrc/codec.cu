@@ -351,6 +351,12 @@ void fetch_pending_on(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uint
     fetch_pending(ctx, P, out, cap, s, sync, true);
 }
 
+__global__ void k_gather_vals(const double *__restrict__ src, const long long *__restrict__ idx, int n,
+                              double *__restrict__ dst) {
+    const int k = threadIdx.x;
+    if (k < n) dst[k] = src[idx[k]];
+}
+
 // codec.py:43-56 from quantized keys on: coarse values (d_coarse: dense coarsest level, or
 // coef_for_coarse: the CoefficientSet whose coarsest slots hold them), head, Huffman stage, and
 // the optional streamed fetch into fetch_out.
@@ -366,13 +372,19 @@ void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t 
         if (q.flags & 2) fail(HPDR_ERR_VALIDATION, "coefficient exceeds representable bin range");
         const size_t nco = p.host.coarsest.size();
         std::vector<double> coarse(nco);
+        // one copy into pinned staging (the coarsest set is <= 16 values; gathered on the device
+        // from the coefficient set when there is no dense coarsest level)
+        double *hco = (double *)ctx->hbuf("coarse_rb", 16 * 8);
         if (d_coarse) {
-            CUDA_CHECK(cudaMemcpyAsync(coarse.data(), d_coarse, nco * 8, cudaMemcpyDeviceToHost, s));
-        } else {
-            for (size_t k = 0; k < nco; k++)
-                CUDA_CHECK(cudaMemcpyAsync(&coarse[k], coef_for_coarse + p.host.coarsest[k], 8, cudaMemcpyDeviceToHost, s));
+            CUDA_CHECK(cudaMemcpyAsync(hco, d_coarse, nco * 8, cudaMemcpyDeviceToHost, s));
+        } else if (nco) {
+            double *dco = (double *)ctx->dbuf("coarse_gather", 16 * 8);
+            k_gather_vals<<<1, 32, 0, s>>>(coef_for_coarse, p.coarsest, (int)nco, dco);
+            LAUNCH_CHECK();
+            CUDA_CHECK(cudaMemcpyAsync(hco, dco, nco * 8, cudaMemcpyDeviceToHost, s));
         }
         CUDA_CHECK(cudaStreamSynchronize(s));
+        if (nco) memcpy(coarse.data(), hco, nco * 8);
         auto &P = ctx->pending;
         P = hpdr_ctx::Pending();
         put<uint8_t>(P.head, (uint8_t)rank);
