@@ -270,7 +270,7 @@ constexpr int kPlaneElems = kHX * kHY;   // 340
 constexpr int kSmemHist = 4096;
 
 template <int MODE, bool A0, bool A1, bool A2, typename TIn>
-__global__ void __launch_bounds__(256) k_level_pass1(const TIn *__restrict__ F, int n0, int n1, int n2, DevAxis ax0,
+__global__ void __launch_bounds__(256, 4) k_level_pass1(const TIn *__restrict__ F, int n0, int n1, int n2, DevAxis ax0,
                                                      DevAxis ax1, DevAxis ax2, LevelMap lm, double *__restrict__ coef,
                                                      const double *__restrict__ coef_in, double *__restrict__ Z0,
                                                      double *__restrict__ Cg, QuantOut q, int c_base, int c_count) {
