@@ -536,8 +536,17 @@ void compress_from_coef(hpdr_ctx *ctx, const double *coef, int dtype, int rank, 
     const double eb_abs = eb_rel * (u_max - u_min);
     const double bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
     QuantResult q;
+    static const bool tph = getenv("HPDR_PHASES") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     quantize_device(ctx, coef, N, p.host.coarsest, bin, dict_size, keys, q, ctx->stream);
+    const auto t1 = std::chrono::steady_clock::now();
     finish_blob(ctx, p, dtype, rank, dims, eb_rel, dict_size, u_min, u_max, eb_abs, bin, q, keys, nullptr, coef, nullptr, 0);
+    if (tph) {
+        const auto t2 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[phaseB] quantize %.0f us, blob %.0f us\n",
+                std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                std::chrono::duration<double, std::micro>(t2 - t1).count());
+    }
 }
 
 // Phase A of the relative-mode streams pipeline: decompose a device-resident chunk into coef

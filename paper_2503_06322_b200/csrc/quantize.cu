@@ -43,32 +43,63 @@ __global__ void __launch_bounds__(kQThreads) k_quantize(const double *__restrict
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const double rbin = 1.0 / bin;
+    const double half_d = (double)half;
     int fl = 0;
-    for (int64_t wbase = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; wbase < n;
-         wbase += warps_total * 32) {
-        const int64_t i = wbase + lane;
-        const bool valid = i < n;
-        const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-        double v = valid ? coef[i] : 0.0;
-        long long b = 0;
-        if (!isfinite(v)) {
-            fl |= 1;
-        } else {
-            double sc = v / bin;                       // IEEE division (quantize.py:73)
-            if (fabs(sc) >= kBinLimit) fl |= 2;
-            else b = (long long)rint(sc);              // half to even (quantize.py:76)
+    // U warp-rows of 32 coefficients in flight per lane before any is quantized
+    constexpr int U = 4;
+    const int64_t step = warps_total * 32;
+    for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < n; w0 += U * step) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t i = w0 + u * step + lane;
+            v[u] = i < n ? __ldg(coef + i) : 0.0;
         }
 #pragma unroll
-        for (int k = 0; k < 16; k++)
-            if (k < co.n && i == co.idx[k]) b = 0;    // coarsest nodes are carried raw (:77)
-        const bool out = valid && (b >= half || -b >= half);
-        const unsigned om = __ballot_sync(0xffffffffu, out);
-        if (lane == 0) omask[wbase >> 5] = om;
-        if (out) b = 0;
-        const uint32_t key = zigzag32(b);
-        if (valid) {
-            keys[i] = key;
-            hist_add(sh_hist, hist, use_sh, key, vmask);
+        for (int u = 0; u < U; u++) {
+            const int64_t wbase = w0 + u * step;
+            if (wbase >= n) break;
+            const int64_t i = wbase + lane;
+            const bool valid = i < n;
+            // b = rint(c / bin) as an integral double (quantize.py:73-76; exact, see fused.cu quant_bin)
+            double r = 0.0;
+            if (valid) {
+                if (!isfinite(v[u])) {
+                    fl |= 1;
+                } else {
+                    const double qa = __dmul_rn(v[u], rbin);
+                    r = rint(qa);
+                    const double dist = 0.5 - fabs(__dsub_rn(qa, r));
+                    if (!(dist > fabs(qa) * 0x1p-49 && fabs(qa) < 0x1p61)) {
+                        const double sc = v[u] / bin;   // IEEE division
+                        if (fabs(sc) >= kBinLimit) {
+                            fl |= 2;
+                            r = 0.0;
+                        } else {
+                            r = rint(sc);
+                        }
+                    }
+                }
+            }
+            // coarsest nodes are carried raw (:77): warp-uniform test first
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k < 16; k++) any |= k < co.n && (co.idx[k] >> 5) == (wbase >> 5);
+            if (any) {
+#pragma unroll
+                for (int k = 0; k < 16; k++)
+                    if (k < co.n && i == co.idx[k]) r = 0.0;
+            }
+            const bool out = valid && fabs(r) >= half_d;
+            const unsigned om = __ballot_sync(0xffffffffu, out);
+            if (lane == 0) omask[wbase >> 5] = om;
+            const uint32_t key = out ? 0u : (uint32_t)(r >= 0.0 ? 2.0 * r : -2.0 * r - 1.0);   // zigzag
+            if (valid) {
+                keys[i] = key;
+                if (use_sh) atomicAdd(&sh_hist[key], 1u);
+                else atomicAdd(&hist[key], 1ULL);
+            }
         }
     }
     if (fl) atomicOr(flags, fl);
