@@ -141,8 +141,10 @@ def profile_models(arr, eb_rel: float, sizes_mb=(16, 32, 64, 128, 256), *, devic
     import torch
 
     dev = torch.device("cuda", ctx.device if hasattr(ctx, "device") else 0)
-    for mb in sizes_mb:
-        planes = max(1, min(a.shape[0], (mb << 20) // plane_bytes))
+    plane_counts = [max(1, min(a.shape[0], int(mb * (1 << 20)) // plane_bytes)) for mb in sizes_mb]
+    if len(set(plane_counts)) < 3:   # a field smaller than the sweep: profile fractions of it
+        plane_counts = sorted({max(1, a.shape[0] * k // 8) for k in (1, 2, 4, 8)})
+    for planes in plane_counts:
         slab = torch.from_numpy(np.ascontiguousarray(a[:planes])).to(dev)
         vr = (float(a.min()), float(a.max()))
         sink = torch.empty(slab.numel() * slab.element_size() * 2 + (8 << 20), dtype=torch.uint8, device=dev)
@@ -154,8 +156,6 @@ def profile_models(arr, eb_rel: float, sizes_mb=(16, 32, 64, 128, 256), *, devic
         torch.cuda.synchronize(dev)
         dt = (time.perf_counter() - t0) / reps
         samples.append((slab.numel() * slab.element_size(), slab.numel() * slab.element_size() / dt))
-        if planes == a.shape[0]:
-            break
     big = torch.from_numpy(np.ascontiguousarray(a[: max(1, min(a.shape[0], (max(sizes_mb) << 20) // plane_bytes))]))
     pin = big.pin_memory()
     d = torch.empty_like(pin, device=dev)
