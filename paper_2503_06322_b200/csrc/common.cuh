@@ -24,6 +24,8 @@ void count_launch();
 void debug_sync(const char *where);
 // HPDR_PHASES=1: CUDA-event phase marks on a stream, printed (ms since the first mark) by phase_dump.
 void phase_mark(const char *name, cudaStream_t s);
+bool prof_enabled();
+void count_launches(uint64_t n);
 void phase_dump(const char *title);   // HPDR_DEBUG_SYNC=1: device sync + check after every launch
 
 // Live per-kernel timing for bench.py: when enabled (hpdr_prof_enable), each scope records a

@@ -20,6 +20,7 @@ void set_error(int code, const std::string &msg, int64_t bit_offset) {
 }
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void count_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void debug_sync(const char *where) {
     static const bool on = getenv("HPDR_DEBUG_SYNC") != nullptr;
@@ -76,6 +77,8 @@ std::vector<ProfRec> g_prof;
 std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_pool;
 size_t g_prof_used = 0;
 }  // namespace
+
+bool prof_enabled() { return g_prof_on; }
 
 ProfScope::ProfScope(const char *name, double bytes, cudaStream_t s) : slot(-1), stream(s) {
     if (!g_prof_on) return;

@@ -47,6 +47,18 @@ struct DevPlan {
     std::vector<int64_t> level_size;     // dense node count of level k (k = 0 finest)
     std::vector<int64_t> level_off;      // offset of level k >= 1 in the coarse-level arena
     int64_t coarse_arena = 0;            // sum of level sizes k >= 1
+    // CUDA graphs of the coarse-level chain, keyed by the buffers / scalars baked into the launches
+    struct Graph {
+        std::vector<uintptr_t> key;
+        cudaGraphExec_t exec = nullptr;
+        size_t kernels = 0;
+    };
+    std::vector<Graph> graphs;
+    bool graph_warm = false;             // one direct run first (static kernel attributes are set)
+    ~DevPlan() {
+        for (auto &g : graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+    }
 };
 
 struct Buffer {

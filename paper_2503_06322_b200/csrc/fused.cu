@@ -55,6 +55,8 @@ __device__ __forceinline__ void hist_add(uint32_t *sh, unsigned long long *g, bo
 // One fine node's quantization (quantize.py:73-84), in the double domain: r = rint(c / bin) as an
 // integral double (quant_bin's verified reciprocal product, IEEE division in the rare tie band),
 // outlier iff |r| >= dict/2, key = zigzag(r) (exact: non-outlier |r| < 2^15), histogram.
+__device__ __forceinline__ double qbin(const QuantOut &q) { return q.bin_dev ? *q.bin_dev : q.bin; }
+
 __device__ __forceinline__ void quant_node(double mc, const QuantOut &q, double rbin, int64_t f, int &fl,
                                            uint32_t *sh_hist, bool sh_ok) {
     double r = 0.0;
@@ -65,7 +67,7 @@ __device__ __forceinline__ void quant_node(double mc, const QuantOut &q, double 
         r = rint(qa);
         const double dist = 0.5 - fabs(dsub(qa, r));
         if (!(dist > fabs(qa) * 0x1p-49 && fabs(qa) < 0x1p61)) {
-            const double sc = mc / q.bin;
+            const double sc = mc / qbin(q);
             if (fabs(sc) >= 4611686018427387904.0) {
                 fl |= 2;
                 r = 0.0;
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(256, 4) k_level_pass1(const TIn *__restrict__ 
     __shared__ __align__(16) PlaneInfo piring[kRing];   // axis-0 records of the planes in the ring
     __shared__ uint32_t sh_hist[MODE == 2 ? kSmemHist : 1];
     const bool sh_ok = MODE == 2 && q.dict <= kSmemHist;
-    const double rbin = MODE == 2 ? 1.0 / q.bin : 0.0;
+    const double rbin = MODE == 2 ? 1.0 / qbin(q) : 0.0;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
     if (MODE == 2 && sh_ok)
         for (uint32_t k = tid; k < q.dict; k += 256) sh_hist[k] = 0;
@@ -449,7 +451,7 @@ __global__ void __launch_bounds__(256) k_level_pass1_2r(const TIn *__restrict__ 
     __shared__ __align__(16) PlaneInfo piring[kRing];
     __shared__ uint32_t sh_hist[MODE == 2 ? kSmemHist : 1];
     const bool sh_ok = MODE == 2 && q.dict <= kSmemHist;
-    const double rbin = MODE == 2 ? 1.0 / q.bin : 0.0;
+    const double rbin = MODE == 2 ? 1.0 / qbin(q) : 0.0;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
     if (MODE == 2 && sh_ok)
         for (uint32_t k = tid; k < q.dict; k += 256) sh_hist[k] = 0;
@@ -629,7 +631,7 @@ __global__ void __launch_bounds__(256) k_level_pass1s(const TIn *__restrict__ F,
     __shared__ double sP1[kP1Rows * kP1Cols];
     __shared__ uint32_t sh_hist[MODE == 2 ? kSmemHist : 1];
     const bool sh_ok = MODE == 2 && q.dict <= kSmemHist;
-    const double rbin = MODE == 2 ? 1.0 / q.bin : 0.0;
+    const double rbin = MODE == 2 ? 1.0 / qbin(q) : 0.0;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
     if (MODE == 2 && sh_ok)
         for (uint32_t k = tid; k < q.dict; k += 256) sh_hist[k] = 0;
@@ -776,7 +778,7 @@ __global__ void __launch_bounds__(256) k_quantize_fine(const double *__restrict_
                                                        DevAxis ax0, DevAxis ax1, DevAxis ax2, QuantOut q) {
     __shared__ uint32_t sh_hist[kSmemHist];
     const bool sh_ok = q.dict <= kSmemHist;
-    const double rbin = 1.0 / q.bin;
+    const double rbin = 1.0 / qbin(q);
     const int tid = threadIdx.y * 32 + threadIdx.x;
     if (sh_ok)
         for (uint32_t k = tid; k < q.dict; k += 256) sh_hist[k] = 0;
@@ -821,7 +823,7 @@ __global__ void k_quantize_coarsest(const double *__restrict__ vals, const long 
         const double v = vals[k];
         int fl = 0;
         if (!isfinite(v)) fl |= 1;
-        else if (fabs(v / q.bin) >= 4611686018427387904.0) fl |= 2;
+        else if (fabs(v / qbin(q)) >= 4611686018427387904.0) fl |= 2;
         if (fl) atomicOr(q.flags, fl);
         q.keys[idx[k]] = 0u;
     }

@@ -16,6 +16,7 @@ bool fused_supported(const DevPlan &p);
 // Quantize-on-write targets (quantize.py:63-84 applied as each coefficient is finalised).
 struct QuantOut {
     double bin;
+    const double *bin_dev = nullptr;   // when set, the bin width is read here (graph replays)
     long long half;
     uint32_t dict;
     uint32_t *keys;               // N keys, finest order

@@ -854,11 +854,12 @@ LevelBuffers fused_buffers(hpdr_ctx *ctx, DevPlan &p) {
 // Fused decomposition (ranks <= 3): pass 1 (GPK residual + coefficients + axis-0 LPK), pass 2
 // (axis-1/2 LPK), IPK Thomas sweeps, coarse + corr.  q != nullptr quantizes on write.
 const double *decompose_fused(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int dtype, double *coef,
-                              const QuantOut *q, cudaStream_t s) {
+                              const QuantOut *q, cudaStream_t s, int st_end = -1) {
     LevelBuffers b = fused_buffers(ctx, p);
     const int L = p.host.L;
     double *Z0 = b.mc;
-    for (int st_i = 0; st_i + 1 < L; st_i++) {
+    if (st_end < 0) st_end = L - 1;
+    for (int st_i = 0; st_i < st_end; st_i++) {
         const DevStep &st = p.steps[st_i];
         const void *F = st_i == 0 ? d_in : (const void *)level_ptr(b, p, st_i);
         double *Dn = level_ptr(b, p, st_i + 1);
@@ -872,6 +873,73 @@ const double *decompose_fused(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int d
         k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, Dn, nc);   // coarse + corr
         LAUNCH_CHECK();
     }
+    return level_ptr(b, p, L - 1);
+}
+
+// Levels 1 .. L-2 of a quantizing decomposition plus the coarsest quantization: small, latency-
+// bound launches, replayed from a CUDA graph after the first direct run (the bin width, the only
+// per-call scalar, is read from device memory in the graph).
+const double *coarse_levels_quantize(hpdr_ctx *ctx, DevPlan &p, const QuantOut &q, cudaStream_t s) {
+    LevelBuffers b = fused_buffers(ctx, p);
+    const int L = p.host.L;
+    double *Z0 = b.mc;
+    auto body = [&](const QuantOut &qq) {
+        for (int st_i = 1; st_i + 1 < L; st_i++) {
+            const DevStep &st = p.steps[st_i];
+            fused_pass1_quantize(p, st_i, level_ptr(b, p, st_i), false, qq, Z0, b.cg, s);
+            fused_pass2(p, st_i, Z0, b.t0, s);
+            thomas_all(p, st_i, b.t0, s);
+            const int64_t nc = st.csh.size();
+            KPROF("k_add", 24.0 * nc, s);
+            k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, level_ptr(b, p, st_i + 1), nc);
+            LAUNCH_CHECK();
+        }
+        quantize_coarsest(p, level_ptr(b, p, L - 1), qq, s);
+    };
+    static const bool no_graph = getenv("HPDR_NO_GRAPH") != nullptr || getenv("HPDR_DEBUG_SYNC") != nullptr;
+    double *bin_dev = (double *)ctx->dbuf("bin_dev", 16);   // allocated on the warm call (CMM: no realloc)
+    if (L <= 2 || no_graph || prof_enabled() || !p.graph_warm) {
+        p.graph_warm = true;
+        body(q);
+        return level_ptr(b, p, L - 1);
+    }
+    const std::vector<uintptr_t> key = {(uintptr_t)b.arena, (uintptr_t)b.mc,  (uintptr_t)b.cg,    (uintptr_t)b.t0,
+                                        (uintptr_t)q.keys,  (uintptr_t)q.omask, (uintptr_t)q.obins, (uintptr_t)q.hist,
+                                        (uintptr_t)q.flags, (uintptr_t)q.half, (uintptr_t)q.dict,  (uintptr_t)bin_dev};
+    DevPlan::Graph *g = nullptr;
+    for (auto &e : p.graphs)
+        if (e.key == key) g = &e;
+    const double binv = q.bin;
+    CUDA_CHECK(cudaMemcpyAsync(bin_dev, &binv, 8, cudaMemcpyHostToDevice, s));   // staged: safe to return
+    if (!g) {
+        QuantOut qg = q;
+        qg.bin_dev = bin_dev;
+        cudaGraph_t graph = nullptr;
+        CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+            body(qg);
+        } catch (...) {
+            cudaStreamEndCapture(s, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        CUDA_CHECK(cudaStreamEndCapture(s, &graph));
+        DevPlan::Graph e;
+        e.key = key;
+        size_t nodes = 0;
+        CUDA_CHECK(cudaGraphGetNodes(graph, nullptr, &nodes));
+        e.kernels = nodes;
+        CUDA_CHECK(cudaGraphInstantiate(&e.exec, graph, 0));
+        CUDA_CHECK(cudaGraphDestroy(graph));
+        if (p.graphs.size() >= 4) {   // bounded: buffers grow rarely
+            cudaGraphExecDestroy(p.graphs.front().exec);
+            p.graphs.erase(p.graphs.begin());
+        }
+        p.graphs.push_back(e);
+        g = &p.graphs.back();
+    }
+    CUDA_CHECK(cudaGraphLaunch(g->exec, s));
+    count_launches(g->kernels);
     return level_ptr(b, p, L - 1);
 }
 
@@ -981,28 +1049,17 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
         k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, level_ptr(b, p, 1), nc);
         LAUNCH_CHECK();
     }
-    for (int st_i = 1; st_i + 1 < L; st_i++) {
-        const DevStep &st = p.steps[st_i];
-        fused_pass1_quantize(p, st_i, level_ptr(b, p, st_i), false, q, Z0, b.cg, s);
-        fused_pass2(p, st_i, Z0, b.t0, s);
-        thomas_all(p, st_i, b.t0, s);
-        const int64_t nc = st.csh.size();
-        KPROF("k_add", 24.0 * nc, s);
-        k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, level_ptr(b, p, st_i + 1), nc);
-        LAUNCH_CHECK();
-    }
+    const double *DL = coarse_levels_quantize(ctx, p, q, s);
     phase_mark("levels_done", s);
-    const double *DL = level_ptr(b, p, L - 1);
-    quantize_coarsest(p, DL, q, s);
     if (side) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(1), 0));
     return DL;
 }
 
 const double *decompose_quantize(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int dtype, const QuantOut &q,
                                  cudaStream_t s) {
-    const double *DL = decompose_fused(ctx, p, d_in, dtype, nullptr, &q, s);
-    quantize_coarsest(p, DL, q, s);
-    return DL;
+    decompose_fused(ctx, p, d_in, dtype, nullptr, &q, s, 1);   // the finest transition
+    phase_mark("level0_done", s);
+    return coarse_levels_quantize(ctx, p, q, s);
 }
 
 const double *decompose_device(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int dtype, double *coef, cudaStream_t s) {
