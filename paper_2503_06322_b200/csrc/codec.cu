@@ -554,7 +554,7 @@ void compress_from_coef(hpdr_ctx *ctx, const double *coef, int dtype, int rank, 
 void decompose_chunk(hpdr_ctx *ctx, const void *d_in, int dtype, int rank, const uint64_t *dims, double *coef,
                      unsigned long long *mm) {
     DevPlan &p = ctx->plan(rank, dims);
-    minmax_accumulate(d_in, dtype, p.n_total, mm, ctx->stream);
+    if (mm) minmax_accumulate(d_in, dtype, p.n_total, mm, ctx->stream);
     decompose_device(ctx, p, d_in, dtype, coef, ctx->stream);
 }
 }  // namespace hpdr

@@ -133,7 +133,7 @@ void *hpdr_ctx::dbuf(const std::string &name, size_t bytes) {
     Buffer &b = dev[name];
     if (b.bytes < bytes) {
         // work queued on any of the context's streams may still use the old buffer
-        if (b.ptr) CUDA_CHECK(cudaDeviceSynchronize());
+        if (b.ptr) sync_all();
         if (b.ptr) CUDA_CHECK(cudaFree(b.ptr));
         b.ptr = nullptr;
         b.bytes = 0;
@@ -158,7 +158,7 @@ void *hpdr_ctx::hbuf(const std::string &name, size_t bytes) {
     if (bytes == 0) bytes = 16;
     Buffer &b = pinned[name];
     if (b.bytes < bytes) {
-        if (b.ptr) CUDA_CHECK(cudaDeviceSynchronize());
+        if (b.ptr) sync_all();
         if (b.ptr) CUDA_CHECK(cudaFreeHost(b.ptr));
         b.ptr = nullptr;
         b.bytes = 0;
@@ -174,6 +174,11 @@ void *hpdr_ctx::hbuf(const std::string &name, size_t bytes) {
 }
 
 void hpdr_ctx::sync() { CUDA_CHECK(cudaStreamSynchronize(stream)); }
+
+void hpdr_ctx::sync_all() {
+    for (cudaStream_t x : {stream, h2d, d2h, aux}) CUDA_CHECK(cudaStreamSynchronize(x));
+    for (cudaStream_t x : side) CUDA_CHECK(cudaStreamSynchronize(x));
+}
 
 hpdr_ctx *hpdr_ctx::queue(int q) {
     if (q == 0) return this;

@@ -101,6 +101,9 @@ struct hpdr_ctx {
     // Compress outputs (outliers, unit offsets, packed words) live in one of two buffer sets so
     // the pipeline can copy chunk k out while chunk k+1 is being reduced.
     int out_slot = 0;
+    // CUDA-graph replays of the coarse levels; off while several host threads drive contexts of the
+    // same device (a capture in one thread forbids device-wide synchronisation in the others)
+    bool graphs_ok = true;
     std::string oname(const char *base, int slot) const { return slot ? std::string(base) + "#1" : std::string(base); }
     std::string oname(const char *base) const { return oname(base, out_slot); }
 
@@ -115,6 +118,7 @@ struct hpdr_ctx {
     void *hbuf(const std::string &name, size_t bytes);
     hpdr::DevPlan &plan(int rank, const uint64_t *dims);
     void sync();
+    void sync_all();   // every stream of this context (buffer reuse / reallocation)
 };
 
 namespace hpdr {

@@ -247,6 +247,11 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
         const int Q = pipe_queues(K);
         std::vector<hpdr_ctx *> qc(Q);
         for (int q = 0; q < Q; q++) qc[q] = ctx->queue(q);
+        for (hpdr_ctx *x : qc) x->graphs_ok = false;   // several host threads on one device
+        struct GraphsBack {
+            hpdr_ctx *c;
+            ~GraphsBack() { c->graphs_ok = true; }
+        } graphs_back{ctx};
         Timer tm(trace != nullptr, 6 * K);
         // every queue starts after the caller's prior work on the main context
         CUDA_CHECK(cudaEventRecord(ctx->event(0), ctx->stream));
@@ -257,67 +262,78 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
         uint64_t next_pos = 0;   // first chunk whose offset is not yet known
         pos[0] = hdr_len;
         double *coef_all = nullptr;
-        if (two_phase) {
-            coef_all = (double *)ctx->dbuf("pipe_coef", N * 8);
-            std::vector<unsigned long long> mmq(3 * Q);
-            QueueRun RA;
-            RA.run(Q, [&](int q) {
-                hpdr_ctx *c = qc[q];
-                CUDA_CHECK(cudaSetDevice(c->device));
-                if (c != ctx) CUDA_CHECK(cudaStreamWaitEvent(c->stream, ctx->event(0), 0));
-                CUDA_CHECK(cudaStreamWaitEvent(c->h2d, ctx->event(0), 0));
-                char *din = (char *)c->dbuf("pipe_in", cbytes);
-                unsigned long long *mm = (unsigned long long *)c->dbuf("pipe_mm", 32);
-                unsigned long long *hmm = (unsigned long long *)c->hbuf("pipe_mm_h", 32);
-                hmm[0] = ~0ULL;
-                hmm[1] = 0ULL;
-                hmm[2] = 0ULL;
-                CUDA_CHECK(cudaMemcpyAsync(mm, hmm, 24, cudaMemcpyHostToDevice, c->stream));
-                cudaEvent_t ev_in = c->event(300), ev_red = c->event(301);
-                bool first = true;
-                for (uint64_t k = q; k < K; k += Q) {
-                    if (RA.failed) return;
-                    if (!first) CUDA_CHECK(cudaStreamWaitEvent(c->h2d, ev_red, 0));   // input buffer reuse edge
-                    tm.mark(6 * k, c->h2d);
-                    CUDA_CHECK(cudaMemcpyAsync(din, (const char *)host_in + chunks[k].raw_off * isz,
-                                               chunks[k].raw_size * isz, cudaMemcpyHostToDevice, c->h2d));
-                    tm.mark(6 * k + 1, c->h2d);
-                    CUDA_CHECK(cudaEventRecord(ev_in, c->h2d));
-                    CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_in, 0));
-                    tm.mark(6 * k + 2, c->stream);
-                    uint64_t sd[4] = {chunks[k].raw_size / plane, 0, 0, 0};
-                    for (int d = 1; d < rank; d++) sd[d] = dims[d];
-                    decompose_chunk(c, din, dtype, rank, sd, coef_all + chunks[k].raw_off, mm);
-                    CUDA_CHECK(cudaEventRecord(ev_red, c->stream));
-                    first = false;
-                }
-                CUDA_CHECK(cudaMemcpyAsync(hmm, mm, 24, cudaMemcpyDeviceToHost, c->stream));
-                CUDA_CHECK(cudaStreamSynchronize(c->stream));
-                memcpy(&mmq[3 * q], hmm, 24);
-            });
-            unsigned long long g[3] = {~0ULL, 0ULL, 0ULL};
-            for (int q = 0; q < Q; q++) {
-                g[0] = std::min(g[0], mmq[3 * q]);
-                g[1] = std::max(g[1], mmq[3 * q + 1]);
-                g[2] |= mmq[3 * q + 2];
+        // Relative mode, per queue thread: phase A streams its chunks in, folds their min/max on the
+        // copy stream (so the range is known as soon as the data is, not after the decompositions)
+        // and decomposes them on the compute stream; once every queue has reported its min/max the
+        // thread runs phase B (quantize + code + copy out) for its chunks, overlapping the other
+        // queues' phase-A tails.
+        std::mutex rmu;
+        std::condition_variable rcv;
+        int reported = 0;
+        unsigned long long gkey[3] = {~0ULL, 0ULL, 0ULL};
+        if (two_phase) coef_all = (double *)ctx->dbuf("pipe_coef", N * 8);
+        auto phase_a = [&](int q, QueueRun &RR) {
+            hpdr_ctx *c = qc[q];
+            if (c != ctx) CUDA_CHECK(cudaStreamWaitEvent(c->stream, ctx->event(0), 0));
+            CUDA_CHECK(cudaStreamWaitEvent(c->h2d, ctx->event(0), 0));
+            char *din = (char *)c->dbuf("pipe_in", cbytes);
+            unsigned long long *mm = (unsigned long long *)c->dbuf("pipe_mm", 32);
+            unsigned long long *hmm = (unsigned long long *)c->hbuf("pipe_mm_h", 32);
+            hmm[0] = ~0ULL;
+            hmm[1] = 0ULL;
+            hmm[2] = 0ULL;
+            CUDA_CHECK(cudaMemcpyAsync(mm, hmm, 24, cudaMemcpyHostToDevice, c->h2d));
+            cudaEvent_t ev_in = c->event(300), ev_red = c->event(301);
+            bool first = true;
+            for (uint64_t k = q; k < K; k += Q) {
+                if (RR.failed) return false;
+                if (!first) CUDA_CHECK(cudaStreamWaitEvent(c->h2d, ev_red, 0));   // input buffer reuse edge
+                tm.mark(6 * k, c->h2d);
+                CUDA_CHECK(cudaMemcpyAsync(din, (const char *)host_in + chunks[k].raw_off * isz,
+                                           chunks[k].raw_size * isz, cudaMemcpyHostToDevice, c->h2d));
+                tm.mark(6 * k + 1, c->h2d);
+                minmax_accumulate(din, dtype, (int64_t)chunks[k].raw_size, mm, c->h2d);
+                CUDA_CHECK(cudaEventRecord(ev_in, c->h2d));
+                CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_in, 0));
+                tm.mark(6 * k + 2, c->stream);
+                uint64_t sd[4] = {chunks[k].raw_size / plane, 0, 0, 0};
+                for (int d = 1; d < rank; d++) sd[d] = dims[d];
+                decompose_chunk(c, din, dtype, rank, sd, coef_all + chunks[k].raw_off, nullptr);
+                CUDA_CHECK(cudaEventRecord(ev_red, c->stream));
+                first = false;
             }
-            minmax_from_keys(g, &vmin, &vmax);
-        }
-        // phase B of the relative mode is quantize + code + copy-out only: more queues in flight
-        static const int qb_env = [] {
-            const char *e = getenv("HPDR_PIPE_QUEUES_B");
-            return e ? std::max(1, atoi(e)) : 3;
-        }();
-        const int QB = two_phase ? (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)qb_env, K)) : Q;   // (3 measured best)
-        if (QB > Q) {
-            qc.resize(QB);
-            for (int q = Q; q < QB; q++) qc[q] = ctx->queue(q);
-        }
+            CUDA_CHECK(cudaMemcpyAsync(hmm, mm, 24, cudaMemcpyDeviceToHost, c->h2d));
+            CUDA_CHECK(cudaStreamSynchronize(c->h2d));   // copies + min/max only, not the decompositions
+            std::unique_lock<std::mutex> lk(rmu);
+            gkey[0] = std::min(gkey[0], hmm[0]);
+            gkey[1] = std::max(gkey[1], hmm[1]);
+            gkey[2] |= hmm[2];
+            if (++reported == Q) {
+                minmax_from_keys(gkey, &vmin, &vmax);
+                rcv.notify_all();
+            } else {
+                rcv.wait(lk, [&] { return reported == Q || RR.failed; });
+            }
+            return !RR.failed;
+        };
+        const int QB = Q;
         QueueRun R;
         R.run(QB, [&](int q) {
             const int Q = QB;
             hpdr_ctx *c = qc[q];
             CUDA_CHECK(cudaSetDevice(c->device));
+            if (two_phase) {
+                try {
+                    if (!phase_a(q, R)) return;
+                } catch (...) {
+                    {
+                        std::lock_guard<std::mutex> g(rmu);
+                        reported = Q;   // release the others; R.fail() marks the run failed
+                    }
+                    rcv.notify_all();
+                    throw;
+                }
+            }
             if (c != ctx) {
                 CUDA_CHECK(cudaStreamWaitEvent(c->stream, ctx->event(0), 0));
             }
@@ -445,6 +461,11 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
         const int Q = pipe_queues(K);
         std::vector<hpdr_ctx *> qc(Q);
         for (int q = 0; q < Q; q++) qc[q] = ctx->queue(q);
+        for (hpdr_ctx *x : qc) x->graphs_ok = false;   // several host threads on one device
+        struct GraphsBack {
+            hpdr_ctx *c;
+            ~GraphsBack() { c->graphs_ok = true; }
+        } graphs_back{ctx};
         Timer tm(trace != nullptr, 6 * (size_t)K);
         CUDA_CHECK(cudaEventRecord(ctx->event(0), ctx->stream));
         if (tm.on) CUDA_CHECK(cudaEventRecord(tm.t0, ctx->stream));

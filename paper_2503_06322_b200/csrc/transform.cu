@@ -924,7 +924,7 @@ const double *coarse_levels_quantize(hpdr_ctx *ctx, DevPlan &p, const QuantOut &
     };
     static const bool no_graph = getenv("HPDR_NO_GRAPH") != nullptr || getenv("HPDR_DEBUG_SYNC") != nullptr;
     double *bin_dev = (double *)ctx->dbuf("bin_dev", 16);   // allocated on the warm call (CMM: no realloc)
-    if (L <= 2 || no_graph || prof_enabled() || !p.graph_warm) {
+    if (L <= 2 || no_graph || !ctx->graphs_ok || prof_enabled() || !p.graph_warm) {
         p.graph_warm = true;
         body(q);
         return level_ptr(b, p, L - 1);
