@@ -33,4 +33,10 @@ int orc_mgard_compress(const void *in, int dtype, int rank, const uint64_t *dims
 int orc_mgard_decompress(const uint8_t *blob, uint64_t len, void *out, uint64_t out_cap,
                          int *dtype, int *rank, uint64_t *dims, int64_t *bit_off);
 void orc_free(void *p);
+/* fixed-rate block coder (zfp_oracle.c; hpdr/zfp.py) */
+int orz_compressed_size(int dtype, int rank, const uint64_t *dims, int rate, uint64_t *size);
+int orz_compress(const void *in, int dtype, int rank, const uint64_t *dims, int rate, uint8_t *out, uint64_t cap,
+                 uint64_t *len);
+int orz_peek(const uint8_t *in, uint64_t len, int *dtype, int *rank, uint64_t *dims, int *rate);
+int orz_decompress(const uint8_t *in, uint64_t len, void *out, uint64_t out_cap);
 #endif

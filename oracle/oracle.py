@@ -169,3 +169,33 @@ def mgard_decompress(data: bytes) -> np.ndarray:
                                     C.byref(dto), C.byref(rko), dout, C.byref(bit))
     _chk(rc, bit.value)
     return out.reshape(dims)
+
+
+# ---- fixed-rate block coder (zfp_oracle.c restates hpdr/zfp.py) ----
+
+def zfp_compressed_size(dims, dtype_code: int, rate: int) -> int:
+    size = C.c_uint64()
+    _chk(lib().orz_compressed_size(int(dtype_code), len(dims), _dims(dims), int(rate), C.byref(size)))
+    return size.value
+
+
+def zfp_compress(arr: np.ndarray, rate: int) -> bytes:
+    arr = np.ascontiguousarray(arr)
+    dt = {np.dtype("<f4"): 0, np.dtype("<f8"): 1}[arr.dtype]
+    size = zfp_compressed_size(arr.shape, dt, rate)
+    out = np.empty(size, np.uint8)
+    ln = C.c_uint64()
+    _chk(lib().orz_compress(_p(arr), dt, arr.ndim, _dims(arr.shape), int(rate), _p(out), C.c_uint64(size),
+                            C.byref(ln)))
+    return out.tobytes()
+
+
+def zfp_decompress(data: bytes) -> np.ndarray:
+    buf = np.frombuffer(data, dtype=np.uint8)
+    dt, rk, rate = C.c_int(), C.c_int(), C.c_int()
+    dims = (C.c_uint64 * 3)()
+    _chk(lib().orz_peek(_p(buf), C.c_uint64(buf.size), C.byref(dt), C.byref(rk), dims, C.byref(rate)))
+    shape = [int(dims[i]) for i in range(rk.value)]
+    out = np.empty(shape, np.float32 if dt.value == 0 else np.float64)
+    _chk(lib().orz_decompress(_p(buf), C.c_uint64(buf.size), _p(out), C.c_uint64(out.nbytes)))
+    return out

@@ -56,3 +56,19 @@ def oracle():
 
     O.lib()
     return O
+
+
+@pytest.fixture(scope="session")
+def zfp_golden():
+    """Fixed-rate coder vectors from the reference (tests/golden/gen_zfp_golden.py)."""
+    meta = json.load(open(os.path.join(GOLDEN, "zfp.json")))
+    data = np.load(os.path.join(GOLDEN, "zfp.npz"))
+    cases = []
+    for m in meta["cases"]:
+        c = dict(m)
+        i = m["id"]
+        c["input"] = data[f"in{i}"]
+        c["blob"] = data[f"blob{i}"].tobytes()
+        c["out"] = data[f"out{i}"]
+        cases.append(c)
+    return cases, meta["errors"], data
