@@ -128,6 +128,20 @@ int hpdr_huffman_fetch(hpdr_ctx *ctx, void *out, uint64_t out_cap);
 int hpdr_huffman_decompress(hpdr_ctx *ctx, const void *in, uint64_t len, uint32_t *keys,
                             uint64_t cap, uint64_t *n);
 
+/* ---- fixed-rate block coder: hpdr/zfp.py ---- */
+
+/* compressed_size (zfp.py:270-278): exact stream bytes for (dtype, dims, rate). */
+int hpdr_zfp_compressed_size(int dtype, int rank, const uint64_t *dims, uint32_t rate, uint64_t *size);
+/* zfp_compress (zfp.py:281-308): rank 1..3 F32/F64 field -> "<BBB" rank, dtype, rate | dims u64 x rank |
+ * packed blocks of 1 + e_bits + rate*4^rank bits.  *out_len receives the stream size; out_cap smaller
+ * than that returns HPDR_ERR_BUFFER (so out = NULL queries the size). */
+int hpdr_zfp_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, uint32_t rate,
+                      void *out, uint64_t out_cap, uint64_t *out_len);
+/* Header of a fixed-rate stream with zfp_decompress's checks (zfp.py:314-334). */
+int hpdr_zfp_peek(const void *stream, uint64_t len, int *dtype, int *rank, uint64_t *dims, uint32_t *rate);
+/* zfp_decompress (zfp.py:311-353): out receives prod(dims) values of the stored dtype. */
+int hpdr_zfp_decompress(hpdr_ctx *ctx, const void *stream, uint64_t len, void *out, uint64_t out_bytes);
+
 /* Kernel launches issued by this thread since the last reset (bench accounting). */
 uint64_t hpdr_launch_count(int reset);
 /* Live per-kernel CUDA-event timing with algorithmic bytes (bench roofline).  Enabling

@@ -136,7 +136,7 @@ int orz_compress(const void *in, int dtype, int rank, const uint64_t *dims, int 
     const double *f64 = (const double *)in;
     int bad = 0;
     /* groups of 8 blocks are byte-aligned (zfp.py:32-34), so they can be written in parallel */
-#pragma omp parallel for schedule(static) reduction(| : bad)
+#pragma omp parallel for schedule(static) reduction(| : bad) num_threads(orc_get_threads())
     for (int64_t grp = 0; grp < (int64_t)((nblk + 7) / 8); grp++) {
         for (uint64_t b = (uint64_t)grp * 8; b < nblk && b < (uint64_t)grp * 8 + 8; b++) {
             const uint64_t b2 = b % g[2], b1 = (b / g[2]) % g[1], b0 = b / (g[2] * g[1]);
@@ -216,7 +216,7 @@ int orz_decompress(const uint8_t *in, uint64_t len, void *out, uint64_t out_cap)
     int perm[64];
     sequency_perm(d, perm);
     const uint8_t *pay = in + HDR + 8 * d;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) num_threads(orc_get_threads())
     for (int64_t bb = 0; bb < (int64_t)nblk; bb++) {
         const uint64_t b = (uint64_t)bb;
         uint64_t pos = b * w;

@@ -11,6 +11,7 @@ from .huffman import huffman_compress, huffman_decompress
 from .mgard import (CoefficientSet, QuantizedSet, blob_info, compress, decompose, decompress, dequantize,
                     mgard_compress, mgard_decompress, quantize, recompose)
 from .tensor import DTYPE_CODES, DTYPE_FROM_CODE, DType, TensorData
+from .zfp import zfp_compress, zfp_decompress
 
 __version__ = "0.1.0"
 
@@ -19,5 +20,5 @@ __all__ = [
     "DTYPE_CODES", "DTYPE_FROM_CODE", "DeviceError", "FormatError", "Hierarchy", "HpdrError", "QuantizedSet",
     "StagingCapacityError", "TensorData", "ValidationError", "blob_info", "build_hierarchy", "compress",
     "decompose", "decompress", "dequantize", "huffman_compress", "huffman_decompress", "mgard_compress",
-    "mgard_decompress", "quantize", "recompose",
+    "mgard_decompress", "quantize", "recompose", "zfp_compress", "zfp_decompress",
 ]

@@ -58,6 +58,12 @@ _SIGS = {
     "hpdr_pipeline_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _u64p, C.c_double, C.c_uint32,
                                          C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_void_p, C.c_uint64,
                                          C.c_void_p, C.c_uint64, _u64p, C.c_void_p]),
+    "hpdr_zfp_compressed_size": (C.c_int, [C.c_int, C.c_int, _u64p, C.c_uint32, _u64p]),
+    "hpdr_zfp_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _u64p, C.c_uint32, C.c_void_p,
+                                    C.c_uint64, _u64p]),
+    "hpdr_zfp_peek": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_int), C.POINTER(C.c_int), _u64p,
+                                C.POINTER(C.c_uint32)]),
+    "hpdr_zfp_decompress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
     "hpdr_pipeline_decompress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p]),
 }
 

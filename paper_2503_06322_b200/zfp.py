@@ -1,0 +1,111 @@
+"""Fixed-rate block coder on the GPU: drop-in for the reference's ``hpdr.zfp``
+(hpdr/zfp.py:270-353).
+
+Streams are byte-identical to the reference's: ``"<BBB"`` rank, dtype code, rate, the dims as
+u64, then every 4^d block packed into exactly ``1 + e_bits + rate*4^d`` bits.  All block work
+(gather with edge replication, common exponent, reversible lifting, negabinary bit planes) runs in
+``k_zfp_encode`` / ``k_zfp_decode`` of libhpdr_b200.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, dims_arg, lib
+from .errors import ValidationError
+from .tensor import DTYPE_CODES, DTYPE_FROM_CODE, DType, TensorData
+
+BLOCK_SIDE = 4       # zfp.py:30
+MAX_BLOCK_RANK = 3   # zfp.py:31
+E_BITS = {DType.F32: 8, DType.F64: 11}
+Q_BITS = {DType.F32: 32, DType.F64: 64}
+
+
+def compressed_size(dims, dtype: DType, rate: int) -> int:
+    """Exact stream size in bytes for the fix-rate contract (zfp.py:270-278)."""
+    dims = tuple(int(d) for d in dims)
+    if dtype not in Q_BITS:
+        raise ValidationError(f"fix-rate compression needs F32/F64, got {dtype}")
+    size = C.c_uint64()
+    check(lib().hpdr_zfp_compressed_size(DTYPE_CODES[dtype], len(dims), dims_arg(dims), int(rate), C.byref(size)))
+    return int(size.value)
+
+
+def _as_field(u):
+    """(address, dims, dtype code, keep-alive) of a TensorData / ndarray / torch tensor."""
+    if isinstance(u, TensorData):
+        if u.dtype not in Q_BITS:
+            raise ValidationError(f"fix-rate compression needs F32/F64, got {u.dtype}")
+        return u.values.ctypes.data, u.dims, DTYPE_CODES[u.dtype], u.values
+    if isinstance(u, np.ndarray):
+        if u.dtype not in (np.float32, np.float64):
+            raise ValidationError(f"fix-rate compression needs F32/F64, got {u.dtype}")
+        arr = np.ascontiguousarray(u)
+        return arr.ctypes.data, tuple(arr.shape), 0 if arr.dtype == np.float32 else 1, arr
+    if hasattr(u, "data_ptr") and hasattr(u, "is_contiguous"):   # torch.Tensor (host, pinned or CUDA)
+        import torch
+
+        if u.dtype not in (torch.float32, torch.float64):
+            raise ValidationError(f"fix-rate compression needs F32/F64, got {u.dtype}")
+        t = u.contiguous()
+        return int(t.data_ptr()), tuple(t.shape), 0 if t.dtype == torch.float32 else 1, t
+    raise ValidationError(f"unsupported input type {type(u)}")
+
+
+def zfp_compress(u, rate: int, adapter=None, *, device: int | None = None, out=None):
+    """zfp_compress (zfp.py:281-308).  ``adapter`` is accepted and ignored.  Returns ``bytes``; with
+    ``out`` (host uint8 array, pinned or not, or a CUDA uint8 tensor) the stream is written there
+    and its length returned."""
+    addr, dims, code, keep = _as_field(u)
+    dims = tuple(int(d) for d in dims)
+    if not dims:
+        raise ValidationError("dims must be non-empty")
+    ctx = _lib.default_context(device, u if getattr(u, "is_cuda", False) else out)
+    n = C.c_uint64()
+    if out is None:
+        size = compressed_size(dims, DTYPE_FROM_CODE[code], rate) if len(dims) <= MAX_BLOCK_RANK else 0
+        b, p = _lib.new_bytes(size) if size else (b"", 0)
+        check(lib().hpdr_zfp_compress(ctx.handle, C.c_void_p(addr), code, len(dims), dims_arg(dims), int(rate),
+                                      C.c_void_p(p) if p else None, size, C.byref(n)))
+        del keep
+        return b
+    check(lib().hpdr_zfp_compress(ctx.handle, C.c_void_p(addr), code, len(dims), dims_arg(dims), int(rate),
+                                  C.c_void_p(_lib.ptr(out)), int(out.nbytes), C.byref(n)))
+    del keep
+    return int(n.value)
+
+
+def _peek(addr: int, size: int) -> tuple:
+    dt, rk, rate = C.c_int(), C.c_int(), C.c_uint32()
+    dims = (C.c_uint64 * 3)()
+    check(lib().hpdr_zfp_peek(C.c_void_p(addr) if addr else None, size, C.byref(dt), C.byref(rk), dims,
+                              C.byref(rate)))
+    return DTYPE_FROM_CODE[dt.value], tuple(int(dims[i]) for i in range(rk.value)), int(rate.value)
+
+
+def stream_info(data) -> tuple:
+    """(dtype, dims, rate) of a fixed-rate stream, with zfp_decompress's header checks."""
+    buf = np.frombuffer(memoryview(data), dtype=np.uint8)
+    return _peek(buf.ctypes.data if buf.size else 0, buf.size)
+
+
+def zfp_decompress(data, adapter=None, *, device: int | None = None, out=None) -> TensorData:
+    """zfp_decompress (zfp.py:311-353).  ``data`` may be bytes-like or a CUDA uint8 tensor."""
+    if getattr(data, "is_cuda", False):
+        addr, size = int(data.data_ptr()), int(data.numel() * data.element_size())
+        dtype, dims, _ = _peek(addr, size)   # hpdr_zfp_peek copies the header off the device
+    else:
+        buf = np.frombuffer(memoryview(data), dtype=np.uint8)
+        addr, size = (buf.ctypes.data if buf.size else 0), buf.size
+        dtype, dims, _ = stream_info(buf)
+    ctx = _lib.default_context(device, data if getattr(data, "is_cuda", False) else out)
+    res = np.empty(dims, dtype=dtype.np_dtype) if out is None else out
+    check(lib().hpdr_zfp_decompress(ctx.handle, C.c_void_p(addr), size, C.c_void_p(_lib.ptr(res)), int(res.nbytes)))
+    if out is not None:
+        return out
+    return TensorData(dims, dtype, res)
+
+
+__all__ = ["BLOCK_SIDE", "MAX_BLOCK_RANK", "compressed_size", "stream_info", "zfp_compress", "zfp_decompress"]
