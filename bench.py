@@ -183,6 +183,28 @@ def cpu_oracle_time(cfg, a, budget_s=20.0):
                        f"C oracle (port of hpdr/mgard), OpenMP {threads} threads")
 
 
+def cpu_zfp_time(a, rate, budget_s=6.0):
+    """The fixed-rate coder's C port (oracle/zfp_oracle.c) on this host's cores, whole field."""
+    from oracle import oracle as O
+
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    reps, tc, td = 0, 0.0, 0.0
+    while reps < 3 and (tc + td) < budget_s:
+        t0 = time.perf_counter()
+        blob = O.zfp_compress(a, rate)
+        t1 = time.perf_counter()
+        O.zfp_decompress(blob)
+        t2 = time.perf_counter()
+        tc += t1 - t0
+        td += t2 - t1
+        reps += 1
+    nb = a.nbytes * reps
+    return dict(compress_gbs=nb / tc / 1e9, decompress_gbs=nb / td / 1e9, cores=threads,
+                sample=f"whole field ({a.nbytes / 1e6:.0f} MB) x {reps}, C oracle (port of hpdr/zfp.py), "
+                       f"OpenMP {threads} threads")
+
+
 def run_reference(args, cfg, rank):
     if rank != 0:
         return
@@ -227,6 +249,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--zfp-rate", type=int, default=16, help="bits/value of the fixed-rate leg (0: skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -374,6 +397,30 @@ def main():
     def decompress_pipe():
         PL.decompress_pipelined(pipe_in, out=h_out2)
 
+    # fixed-rate block coder (hpdr/zfp.py) on the same field
+    from paper_2503_06322_b200 import zfp as ZF
+
+    zrate = args.zfp_rate if a.ndim <= 3 else 0
+    if zrate:
+        z_len = ZF.compressed_size(a.shape, P.DType.F32 if code == 0 else P.DType.F64, zrate)
+        z_dev = torch.empty(z_len, dtype=torch.uint8, device=dev)
+        z_host = torch.empty(z_len, dtype=torch.uint8).pin_memory()
+        ZF.zfp_compress(d_in, zrate, out=z_dev)
+        z_blob = bytes(z_dev.cpu().numpy())
+        z_host_in = torch.from_numpy(np.frombuffer(z_blob, np.uint8).copy()).pin_memory()
+
+        def zfp_c_dev():
+            ZF.zfp_compress(d_in, zrate, out=z_dev)
+
+        def zfp_d_dev():
+            ZF.zfp_decompress(z_dev, out=d_out)
+
+        def zfp_c_e2e():
+            ZF.zfp_compress(h_in, zrate, out=z_host)
+
+        def zfp_d_e2e():
+            ZF.zfp_decompress(z_host_in, out=h_out)
+
     K = args.steps
     pcie = pcie_roofline(dev)
     with ClockSampler(local) as clk:
@@ -385,6 +432,11 @@ def main():
         pd_ms, _, _ = timed(decompress_pipe, K)
         pa_ms, _, _ = timed(compress_pipe_abs, K)
         pad_ms, _, _ = timed(compress_pipe_adaptive, K)
+        if zrate:
+            zc_ms, zc_l, zkern = timed(zfp_c_dev, K, prof=True)
+            zd_ms, zd_l, zdkern = timed(zfp_d_dev, K, prof=True)
+            zce_ms, _, _ = timed(zfp_c_e2e, K)
+            zde_ms, _, _ = timed(zfp_d_e2e, K)
     clocks = clk.summary()
     _, ptr_c = PL.compress_pipelined(h_in, cfg["eb"], value_range=vr_abs, out=pipe_out, trace=True)
     _, ptr_d = PL.decompress_pipelined(pipe_in, out=h_out2, trace=True)
@@ -465,7 +517,39 @@ def main():
                                for k, v in sorted(dkern.items(), key=lambda kv: -kv[1][1])},
         "clocks": clocks,
     }
+    if zrate:
+        assert bytes(z_host.numpy()) == z_blob, "fixed-rate e2e stream differs from the device-path stream"
+        zerr = float(np.max(np.abs(h_out.numpy().astype(np.float64) - a.astype(np.float64))))
+
+        def zroof(kd, name, ms_step):
+            nl, kms, kbytes, _ = kd[name]
+            ach = (nbytes + z_len) / (kms / nl * 1e-3) / 1e9     # algorithmic: field + stream, once
+            return {"bound": "hbm", "kernel": name, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                    "traffic": ncu_traffic(name), "algorithmic_bytes": nbytes + z_len, "launch_ms": kms / nl,
+                    "launches_per_step": nl / K, "share_of_step": kms / (ms_step * K)}
+
+        t_zc = max(nbytes / (pcie["h2d"] * 1e9), z_len / (pcie["d2h"] * 1e9))
+        t_zd = max(z_len / (pcie["h2d"] * 1e9), nbytes / (pcie["d2h"] * 1e9))
+        line["zfp"] = {
+            "mode": f"fixed-rate block coder (hpdr/zfp.py), rate {zrate} bits/value, reference-identical stream",
+            "rate": zrate, "stream_bytes": z_len, "cr": nbytes / z_len, "max_abs_err": zerr,
+            "compress_gbs": gbs(zc_ms), "compress_ms": zc_ms, "decompress_gbs": gbs(zd_ms), "decompress_ms": zd_ms,
+            "gpu_launches_compress": zc_l, "gpu_launches_decompress": zd_l,
+            "compress_e2e": {"value": gbs(zce_ms), "unit": "GB/s", "h2d_bytes_per_step": nbytes,
+                             "d2h_bytes_per_step": z_len, "ms_per_step": zce_ms,
+                             "pcie_roofline_frac": t_zc / (zce_ms * 1e-3)},
+            "decompress_e2e": {"value": gbs(zde_ms), "unit": "GB/s", "h2d_bytes_per_step": z_len,
+                               "d2h_bytes_per_step": nbytes, "ms_per_step": zde_ms,
+                               "pcie_roofline_frac": t_zd / (zde_ms * 1e-3)},
+            "roofline_encode": zroof(zkern, "k_zfp_encode", zc_ms),
+            "roofline_decode": zroof(zdkern, "k_zfp_decode", zd_ms),
+        }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if zrate:
+            zb = cpu_zfp_time(a, zrate)
+            line["zfp"]["cpu_baseline"] = {"value": zb["compress_gbs"], "unit": "GB/s", "cores": zb["cores"],
+                                           "kind": "port", "sample": zb["sample"],
+                                           "decompress_value": zb["decompress_gbs"]}
         cb = cpu_oracle_time(cfg, a)
         line["cpu_baseline"] = {"value": cb["compress_gbs"], "unit": "GB/s", "cores": cb["cores"], "kind": "port",
                                 "sample": cb["sample"], "decompress_value": cb["decompress_gbs"]}

@@ -115,19 +115,23 @@ __device__ __forceinline__ void scatter_perm(const U (&src)[1 << (2 * D)], U (&d
 }
 
 // MSB-first bit writer into shared 32-bit words (word 0 bit 31 = first stream bit).  Only a
-// thread's first and last words can be shared with its neighbours; atomicOr covers both.
+// thread's first and last words can be shared with its neighbours (atomicOr); the words between
+// are its own (plain stores).
 struct BitWriter {
     uint32_t *s;
-    uint32_t idx;
+    uint32_t idx, first;
     uint64_t acc;
     int n;
-    __device__ BitWriter(uint32_t *sm, uint32_t pos) : s(sm), idx(pos >> 5), acc(0), n(pos & 31) {}
+    __device__ BitWriter(uint32_t *sm, uint32_t pos) : s(sm), idx(pos >> 5), first(pos >> 5), acc(0), n(pos & 31) {}
     __device__ __forceinline__ void put(uint32_t v, int nb) {   // 1 <= nb <= 32, v < 2^nb
         acc = (acc << nb) | v;   // n + nb <= 63 meaningful bits
         n += nb;
         if (n >= 32) {
             n -= 32;
-            atomicOr(&s[idx++], (uint32_t)(acc >> n));
+            const uint32_t word = (uint32_t)(acc >> n);
+            if (idx == first) atomicOr(&s[idx], word);
+            else s[idx] = word;
+            idx++;
         }
     }
     __device__ __forceinline__ void flush() {
@@ -146,40 +150,159 @@ struct BitReader {
     }
 };
 
+// In-register 32x32 bit-matrix transpose, MSB-first: A[OFF+i] bit (31-j) <-> A[OFF+j] bit (31-i).
+// Turns 32 coefficients into 32 bit planes (and back).  The 16- and 8-bit stages are byte
+// permutes; the 4/2/1-bit stages are two shift+LOP3 pairs (the masks satisfy m << j == ~m).
+template <int OFF, int N>
+__device__ __forceinline__ void transpose32(uint32_t (&A)[N]) {
+#pragma unroll
+    for (int i = 0; i < 16; i++) {
+        const uint32_t a = A[OFF + i], b = A[OFF + i + 16];
+        A[OFF + i] = __byte_perm(a, b, 0x3276);        // a.hi16 : b.hi16
+        A[OFF + i + 16] = __byte_perm(a, b, 0x1054);   // a.lo16 : b.lo16
+    }
+#pragma unroll
+    for (int base = 0; base < 32; base += 16)
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const uint32_t a = A[OFF + base + i], b = A[OFF + base + i + 8];
+            A[OFF + base + i] = __byte_perm(a, b, 0x3715);
+            A[OFF + base + i + 8] = __byte_perm(a, b, 0x2604);
+        }
+#pragma unroll
+    for (int lj = 2; lj >= 0; lj--) {
+        const int j = 1 << lj;
+        const uint32_t m = lj == 2 ? 0x0F0F0F0Fu : lj == 1 ? 0x33333333u : 0x55555555u;
+#pragma unroll
+        for (int base = 0; base < 32; base += 2 * j)
+#pragma unroll
+            for (int i = 0; i < j; i++) {
+                const uint32_t a = A[OFF + base + i], b = A[OFF + base + i + j];
+                A[OFF + base + i] = (a & ~m) | ((b >> j) & m);
+                A[OFF + base + i + j] = (b & m) | ((a << j) & ~m);
+            }
+    }
+}
+
+// 2^e, exact: doubles for -1022 <= e <= 1023, floats for -126 <= e <= 127.
+__device__ __forceinline__ double pow2(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
+__device__ __forceinline__ float pow2f(int e) { return __uint_as_float((uint32_t)(e + 127) << 23); }
+
+// exp_align (zfp.py:125-150) for one block: e_max = floor(log2(max|v|)) clamped to -bias, then
+// fixed = rint(ldexp(v, q-2-e_max)).  The reference works in float64; these are exact restatements:
+//  * F32: |v| ordering, the exponent and v * 2^shift are all exact in fp32 (the scaled value keeps
+//    v's 24-bit significand, |v * 2^shift| < 2^31), so the fp32 multiply + round-to-nearest-even
+//    convert equals rint of the float64 product.  Products that underflow round to 0 either way.
+//  * F64: one multiply by 2^shift is exact unless the product is subnormal (< 0.5, so rint gives 0
+//    either way); shift > 1023 only for e_max < -961, where v * 2^(shift-64) is exact and normal.
+template <class T, int M>
+__device__ __forceinline__ void align_block(const T (&v)[M], typename ZSpec<T>::U (&fx)[M], int &emax, bool &zero,
+                                            bool &finite) {
+    using U = typename ZSpec<T>::U;
+    if constexpr (sizeof(T) == 4) {
+        float m = 0.f;
+        finite = true;
+#pragma unroll
+        for (int f = 0; f < M; f++) {
+            const float a = fabsf(v[f]);
+            finite &= a <= 3.40282346638528859812e38f;
+            m = fmaxf(m, a);
+        }
+        zero = m == 0.f;
+        emax = max((int)(__float_as_uint(m) >> 23) - 127, -127);   // subnormal maxima clamp to -127
+        const int shift = 30 - emax;                                  // in [-98, 157]
+        if (shift <= 127) {
+            const float s = pow2f(shift);
+#pragma unroll
+            for (int f = 0; f < M; f++) fx[f] = (U)__float2int_rn(__fmul_rn(v[f], s));
+        } else {
+            const float s = pow2f(shift - 64), s64 = pow2f(64);
+#pragma unroll
+            for (int f = 0; f < M; f++) fx[f] = (U)__float2int_rn(__fmul_rn(__fmul_rn(v[f], s), s64));
+        }
+    } else {
+        double m = 0.0;
+        finite = true;
+#pragma unroll
+        for (int f = 0; f < M; f++) {
+            const double a = fabs(v[f]);
+            finite &= a <= 1.79769313486231570815e308;
+            m = fmax(m, a);
+        }
+        zero = m == 0.0;
+        emax = (int)((__double_as_longlong(m) >> 52) & 0x7ff) - 1023;   // subnormal maxima: -1023
+        const int shift = 62 - emax;                                      // in [-962, 1085]
+        if (shift <= 1023) {
+            const double s = pow2(shift);
+#pragma unroll
+            for (int f = 0; f < M; f++) fx[f] = (U)__double2ll_rn(__dmul_rn(v[f], s));
+        } else {
+            const double s = pow2(shift - 64), s64 = pow2(64);
+#pragma unroll
+            for (int f = 0; f < M; f++) fx[f] = (U)__double2ll_rn(__dmul_rn(__dmul_rn(v[f], s), s64));
+        }
+    }
+}
+
+// exp_restore (zfp.py:153-157): ldexp(float64(fixed), e_max-(q-2)), then the F32 cast -- one
+// rounding of the exact value.  F32 with every nonzero result normal (sc >= -126): int->fp32
+// rounding followed by an exact power-of-two scale is that same single rounding.
+template <class T>
+__device__ __forceinline__ T restore(typename ZSpec<T>::S x, int sc) {
+    if constexpr (sizeof(T) == 4) {
+        if (sc >= -126) return __fmul_rn(__int2float_rn(x), pow2f(sc));
+        return __double2float_rn(__dmul_rn((double)x, pow2(sc)));   // sc >= -157: exact product
+    } else {
+        const double d = __ll2double_rn(x);
+        return sc >= -1022 ? __dmul_rn(d, pow2(sc)) : __dmul_rn(__dmul_rn(d, pow2(sc + 64)), pow2(-64));
+    }
+}
+
 struct ZGrid {
     int64_t n[3];   // extents padded to rank 3 with leading 1s
     int64_t g[3];   // blocks per axis
 };
 
-// Element offsets of the block's 4^D positions, edge-replicated (np.pad mode="edge", zfp.py:98-100).
-template <int D>
-__device__ __forceinline__ void block_rows(const ZGrid &G, int64_t b, int64_t (&row)[16], int64_t (&col)[4]) {
+// A block's element offsets: origin + row[r] + col, edge-replicated (np.pad mode="edge",
+// zfp.py:98-100).  O is int32_t when 3*(n1*n2 + n2) fits, else int64_t.
+template <int D, class O>
+struct BlockAt {
+    int64_t origin;
+    O row[16];     // D=3: row[a*4+c] for in-block (i0=a, i1=c); D=2: row[a*4] for i1=a
+    int col[4];    // clamped axis-2 offsets
+    bool full2;    // no clamping along the last axis
+    bool full;     // no clamping at all (interior block)
+};
+
+template <int D, class O>
+__device__ __forceinline__ void block_at(const ZGrid &G, int64_t b, BlockAt<D, O> &B) {
     const int64_t b2 = b % G.g[2], r = b / G.g[2];
     const int64_t b1 = r % G.g[1], b0 = r / G.g[1];
+    const int64_t x0 = b0 * 4, x1 = b1 * 4, x2 = b2 * 4;
+    B.origin = (x0 * G.n[1] + x1) * G.n[2] + x2;
 #pragma unroll
-    for (int i = 0; i < 4; i++) col[i] = min64(b2 * 4 + i, G.n[2] - 1);
+    for (int i = 0; i < 4; i++) B.col[i] = (int)(min64(x2 + i, G.n[2] - 1) - x2);
+    B.full2 = x2 + 3 < G.n[2];
+    B.full = B.full2 && (D < 2 || x1 + 3 < G.n[1]) && (D < 3 || x0 + 3 < G.n[0]);
 #pragma unroll
     for (int a = 0; a < 4; a++)
 #pragma unroll
         for (int c = 0; c < 4; c++) {
-            const int64_t i0 = D == 3 ? min64(b0 * 4 + a, G.n[0] - 1) : 0;
-            const int64_t i1 = D >= 2 ? min64(b1 * 4 + (D == 3 ? c : a), G.n[1] - 1) : 0;
-            row[a * 4 + c] = (i0 * G.n[1] + i1) * G.n[2];
+            const int64_t da = D == 3 ? min64(x0 + a, G.n[0] - 1) - x0 : 0;
+            const int64_t dc = D == 3 ? min64(x1 + c, G.n[1] - 1) - x1 : D == 2 ? min64(x1 + a, G.n[1] - 1) - x1 : 0;
+            B.row[a * 4 + c] = (O)((da * G.n[1] + dc) * G.n[2]);
         }
 }
 
 template <int D>
-__device__ __forceinline__ int64_t elem_at(const int64_t (&row)[16], const int64_t (&col)[4], int f) {
-    // f = flat in-block position, row-major over the block's D axes
-    if (D == 3) return row[(f >> 4) * 4 + ((f >> 2) & 3)] + col[f & 3];
-    if (D == 2) return row[(f >> 2) * 4] + col[f & 3];
-    return row[0] + col[f & 3];
+__device__ __forceinline__ constexpr int row_of(int f) {   // f = flat in-block position
+    return D == 3 ? (f >> 4) * 4 + ((f >> 2) & 3) : D == 2 ? (f >> 2) * 4 : 0;
 }
 
 // zfp_compress per block (zfp.py:291-303): exp_align :125-150, forward_transform :194-196,
 // bitplane_encode :217-241.  Stream words go to out32 (MSB-first bits, byte-swapped on store so
 // memory holds the np.packbits byte order).
-template <class T, int D>
+template <class T, int D, class O>
 __global__ void __launch_bounds__(kZThreads) k_zfp_encode(const T *__restrict__ in, ZGrid G, int64_t b_lo,
                                                            int64_t b_hi, int rate, uint32_t *__restrict__ out32,
                                                            unsigned *__restrict__ bad) {
@@ -195,28 +318,22 @@ __global__ void __launch_bounds__(kZThreads) k_zfp_encode(const T *__restrict__ 
     for (uint32_t i = threadIdx.x; i < words; i += kZThreads) zs[i] = 0;
     __syncthreads();
     if ((int)threadIdx.x < nblk) {
-        const int64_t b = cta0 + threadIdx.x;
-        int64_t row[16], col[4];
-        block_rows<D>(G, b, row, col);
-        T v[M];   // widened to double on use (exact), as np.asarray(blocks, float64) does
-        double maxabs = 0.0;
-        bool finite = true;
+        BlockAt<D, O> B;
+        block_at<D, O>(G, cta0 + threadIdx.x, B);
+        const T *p = in + B.origin;
+        T v[M];   // np.asarray(blocks, float64): widening is exact, see align_block
+        if (B.full2) {
 #pragma unroll
-        for (int f = 0; f < M; f++) {
-            v[f] = __ldg(in + elem_at<D>(row, col, f));
-            const double a = fabs((double)v[f]);
-            finite &= a <= 1.79769313486231570815e308;   // false for inf and NaN
-            maxabs = fmax(maxabs, a);
+            for (int f = 0; f < M; f++) v[f] = __ldg(p + B.row[row_of<D>(f)] + (f & 3));
+        } else {
+#pragma unroll
+            for (int f = 0; f < M; f++) v[f] = __ldg(p + B.row[row_of<D>(f)] + B.col[f & 3]);
         }
-        if (!finite) atomicOr(bad, 1u);
-        const bool zero = maxabs == 0.0;
-        // floor(log2(maxabs)) exactly (the :139-144 guards make the reference exact too)
-        int emax = zero ? 0 : ilogb(maxabs);
-        emax = max(emax, -Z::bias);
-        const int shift = Z::q - 2 - emax;
         U fx[M];
-#pragma unroll
-        for (int f = 0; f < M; f++) fx[f] = zero ? (U)0 : (U)(S)rint(ldexp((double)v[f], shift));
+        int emax;
+        bool zero, finite;
+        align_block<T, M>(v, fx, emax, zero, finite);
+        if (!finite) atomicOr(bad, 1u);
         transform<D, U, S, true>(fx);
         U c[M];
         gather_perm<D, U>(fx, c, std::make_integer_sequence<int, M>{});
@@ -225,21 +342,41 @@ __global__ void __launch_bounds__(kZThreads) k_zfp_encode(const T *__restrict__ 
         BitWriter bw(zs, (uint32_t)threadIdx.x * w);
         bw.put(zero ? 1u : 0u, 1);
         bw.put(zero ? 0u : (uint32_t)(emax + Z::bias), Z::ebits);
-        for (int t = 0; t < rate; t++) {
-            const int sh = Z::q - 1 - t;
-            if (D == 3) {
-                uint32_t hi = 0, lo = 0;
+        if constexpr (D == 3) {
+            // planes MSB first: transpose the 64 coefficients' top halves into 32 plane pairs
+            uint32_t hi[64];
 #pragma unroll
-                for (int k = 0; k < 32; k++) hi |= (uint32_t)((c[k] >> sh) & 1) << (31 - k);
+            for (int k = 0; k < 64; k++) hi[k] = (uint32_t)(c[k] >> (Z::q - 32));
+            transpose32<0>(hi);
+            transpose32<32>(hi);
 #pragma unroll
-                for (int k = 0; k < 32; k++) lo |= (uint32_t)((c[32 + k] >> sh) & 1) << (31 - k);
-                bw.put(hi, 32);
-                bw.put(lo, 32);
-            } else {
-                uint32_t p = 0;
+            for (int t = 0; t < 32; t++)
+                if (t < rate) {
+                    bw.put(hi[t], 32);
+                    bw.put(hi[32 + t], 32);
+                }
+            if constexpr (Z::q == 64) {
+                if (rate > 32) {
+                    uint32_t lo[64];
 #pragma unroll
-                for (int k = 0; k < M; k++) p |= (uint32_t)((c[k] >> sh) & 1) << (M - 1 - k);
-                bw.put(p, M);
+                    for (int k = 0; k < 64; k++) lo[k] = (uint32_t)c[k];
+                    transpose32<0>(lo);
+                    transpose32<32>(lo);
+#pragma unroll
+                    for (int t = 0; t < 32; t++)
+                        if (32 + t < rate) {
+                            bw.put(lo[t], 32);
+                            bw.put(lo[32 + t], 32);
+                        }
+                }
+            }
+        } else {
+            for (int t = 0; t < rate; t++) {
+                const int sh = Z::q - 1 - t;
+                uint32_t pl = 0;
+#pragma unroll
+                for (int k = 0; k < M; k++) pl |= (uint32_t)((c[k] >> sh) & 1) << (M - 1 - k);
+                bw.put(pl, M);
             }
         }
         bw.flush();
@@ -250,8 +387,8 @@ __global__ void __launch_bounds__(kZThreads) k_zfp_encode(const T *__restrict__ 
 }
 
 // zfp_decompress per block (zfp.py:338-347): bitplane_decode :244-264, inverse_transform,
-// exp_restore :153-157 (ldexp in double, then the cast for F32), zero blocks -> 0.0.
-template <class T, int D>
+// exp_restore :153-157, zero blocks -> 0.0, padding discarded.
+template <class T, int D, class O>
 __global__ void __launch_bounds__(kZThreads) k_zfp_decode(const uint32_t *__restrict__ in32, ZGrid G, int64_t b_lo,
                                                            int64_t b_hi, int rate, T *__restrict__ out) {
     using Z = ZSpec<T>;
@@ -268,26 +405,55 @@ __global__ void __launch_bounds__(kZThreads) k_zfp_decode(const uint32_t *__rest
         zs[i] = i < words ? __byte_perm(__ldg(src + i), 0, 0x0123) : 0u;
     __syncthreads();
     if ((int)threadIdx.x >= nblk) return;
-    const int64_t b = cta0 + threadIdx.x;
     BitReader br{zs, (uint32_t)threadIdx.x * w};
     const bool zero = br.get(1) != 0;
     const int biased = (int)br.get(Z::ebits);
     const int emax = zero ? -Z::bias : biased - Z::bias;
     U c[M];
+    if constexpr (D == 3) {
+        // 32-bit plane halves at a fixed bit phase: one shared load + funnel shift each
+        uint32_t wi = br.pos >> 5;
+        const uint32_t o = br.pos & 31;
+        uint32_t cur = zs[wi];
+        auto next32 = [&]() {
+            const uint32_t nxt = zs[++wi];
+            const uint32_t r = __funnelshift_l(nxt, cur, o);
+            cur = nxt;
+            return r;
+        };
+        uint32_t hi[64];
 #pragma unroll
-    for (int k = 0; k < M; k++) c[k] = 0;
-    for (int t = 0; t < rate; t++) {
-        const int sh = Z::q - 1 - t;
-        if (D == 3) {
-            const uint32_t hi = br.get(32), lo = br.get(32);
+        for (int t = 0; t < 32; t++) {
+            hi[t] = t < rate ? next32() : 0u;
+            hi[32 + t] = t < rate ? next32() : 0u;
+        }
+        transpose32<0>(hi);
+        transpose32<32>(hi);
+        if constexpr (Z::q == 64) {
+            uint32_t lo[64];
 #pragma unroll
-            for (int k = 0; k < 32; k++) c[k] |= (U)((hi >> (31 - k)) & 1) << sh;
+            for (int t = 0; t < 32; t++) {
+                lo[t] = 32 + t < rate ? next32() : 0u;
+                lo[32 + t] = 32 + t < rate ? next32() : 0u;
+            }
+            if (rate > 32) {
+                transpose32<0>(lo);
+                transpose32<32>(lo);
+            }
 #pragma unroll
-            for (int k = 0; k < 32; k++) c[32 + k] |= (U)((lo >> (31 - k)) & 1) << sh;
+            for (int k = 0; k < 64; k++) c[k] = ((U)hi[k] << 32) | lo[k];
         } else {
-            const uint32_t p = br.get(M);
 #pragma unroll
-            for (int k = 0; k < M; k++) c[k] |= (U)((p >> (M - 1 - k)) & 1) << sh;
+            for (int k = 0; k < 64; k++) c[k] = hi[k];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < M; k++) c[k] = 0;
+        for (int t = 0; t < rate; t++) {
+            const int sh = Z::q - 1 - t;
+            const uint32_t pl = br.get(M);
+#pragma unroll
+            for (int k = 0; k < M; k++) c[k] |= (U)((pl >> (M - 1 - k)) & 1) << sh;
         }
     }
 #pragma unroll
@@ -295,16 +461,24 @@ __global__ void __launch_bounds__(kZThreads) k_zfp_decode(const uint32_t *__rest
     U fx[M];
     scatter_perm<D, U>(c, fx, std::make_integer_sequence<int, M>{});
     transform<D, U, S, false>(fx);
-    const int64_t b2 = b % G.g[2], r = b / G.g[2];
-    const int64_t b1 = r % G.g[1], b0 = r / G.g[1];
+    BlockAt<D, O> B;
+    block_at<D, O>(G, cta0 + threadIdx.x, B);
+    T *q = out + B.origin;
     const int sc = emax - (Z::q - 2);
+    if (B.full) {
 #pragma unroll
-    for (int f = 0; f < M; f++) {
-        const int p0 = D == 3 ? f >> 4 : 0, p1 = D == 3 ? (f >> 2) & 3 : D == 2 ? f >> 2 : 0, p2 = f & 3;
-        const int64_t i0 = b0 * 4 + p0, i1 = b1 * 4 + p1, i2 = b2 * 4 + p2;
-        if (i0 >= G.n[0] || i1 >= G.n[1] || i2 >= G.n[2]) continue;   // padding is discarded
-        const double val = zero ? 0.0 : ldexp((double)(S)fx[f], sc);
-        out[(i0 * G.n[1] + i1) * G.n[2] + i2] = (T)val;
+        for (int f = 0; f < M; f++) q[B.row[row_of<D>(f)] + (f & 3)] = zero ? (T)0 : restore<T>((S)fx[f], sc);
+    } else {
+        // a clamped position repeats an earlier one, whose value is the one kept
+        const int64_t b = cta0 + threadIdx.x;
+        const int64_t b2 = b % G.g[2], r = b / G.g[2];
+        const int64_t b1 = r % G.g[1], b0 = r / G.g[1];
+#pragma unroll
+        for (int f = 0; f < M; f++) {
+            const int p0 = D == 3 ? f >> 4 : 0, p1 = D == 3 ? (f >> 2) & 3 : D == 2 ? f >> 2 : 0, p2 = f & 3;
+            if (b0 * 4 + p0 >= G.n[0] || b1 * 4 + p1 >= G.n[1] || b2 * 4 + p2 >= G.n[2]) continue;
+            q[B.row[row_of<D>(f)] + (f & 3)] = zero ? (T)0 : restore<T>((S)fx[f], sc);
+        }
     }
 }
 
@@ -350,60 +524,68 @@ void zfp_shape(int dtype, int rank, const uint64_t *dims, int rate, ZfpShape &z)
 
 size_t zfp_smem(const ZfpShape &z) { return ((size_t)kZThreads * z.w / 32 + 1) * 4; }
 
-template <class T, int D>
+// int32 in-block offsets unless a block spans more than 2^31 elements
+// (HPDR_ZFP_WIDE=1 forces the int64 variant, for its parity test)
+bool zfp_wide(const ZfpShape &z) {
+    static const bool force = getenv("HPDR_ZFP_WIDE") != nullptr;
+    return force || 3 * (z.G.n[1] * z.G.n[2] + z.G.n[2]) + 3 >= (1LL << 31);
+}
+
+template <class T, int D, class O>
 void launch_encode(const ZfpShape &z, const void *in, int64_t lo, int64_t hi, uint32_t *out32, unsigned *bad,
                    cudaStream_t s) {
-    if (hi <= lo) return;
-    const size_t smem = zfp_smem(z);
     static bool attr = false;
     if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_zfp_encode<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        CUDA_CHECK(cudaFuncSetAttribute(k_zfp_encode<T, D, O>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
         attr = true;
     }
     const unsigned grid = (unsigned)((hi - lo + kZThreads - 1) / kZThreads);
     KPROF("k_zfp_encode", (double)(hi - lo) * ((double)(1 << (2 * D)) * sizeof(T) + z.w / 8.0), s);
-    k_zfp_encode<T, D><<<grid, kZThreads, smem, s>>>((const T *)in, z.G, lo, hi, z.rate, out32, bad);
+    k_zfp_encode<T, D, O><<<grid, kZThreads, zfp_smem(z), s>>>((const T *)in, z.G, lo, hi, z.rate, out32, bad);
     LAUNCH_CHECK();
 }
 
-template <class T, int D>
+template <class T, int D, class O>
 void launch_decode(const ZfpShape &z, const uint32_t *in32, int64_t lo, int64_t hi, void *out, cudaStream_t s) {
-    if (hi <= lo) return;
-    const size_t smem = zfp_smem(z) + 4;
     static bool attr = false;
     if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_zfp_decode<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        CUDA_CHECK(cudaFuncSetAttribute(k_zfp_decode<T, D, O>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
         attr = true;
     }
     const unsigned grid = (unsigned)((hi - lo + kZThreads - 1) / kZThreads);
     KPROF("k_zfp_decode", (double)(hi - lo) * ((double)(1 << (2 * D)) * sizeof(T) + z.w / 8.0), s);
-    k_zfp_decode<T, D><<<grid, kZThreads, smem, s>>>(in32, z.G, lo, hi, z.rate, (T *)out);
+    k_zfp_decode<T, D, O><<<grid, kZThreads, zfp_smem(z) + 4, s>>>(in32, z.G, lo, hi, z.rate, (T *)out);
     LAUNCH_CHECK();
+}
+
+template <class T, class O>
+void encode_t(const ZfpShape &z, const void *in, int64_t lo, int64_t hi, uint32_t *out32, unsigned *bad,
+              cudaStream_t s) {
+    if (z.rank == 1) launch_encode<T, 1, O>(z, in, lo, hi, out32, bad, s);
+    else if (z.rank == 2) launch_encode<T, 2, O>(z, in, lo, hi, out32, bad, s);
+    else launch_encode<T, 3, O>(z, in, lo, hi, out32, bad, s);
+}
+
+template <class T, class O>
+void decode_t(const ZfpShape &z, const uint32_t *in32, int64_t lo, int64_t hi, void *out, cudaStream_t s) {
+    if (z.rank == 1) launch_decode<T, 1, O>(z, in32, lo, hi, out, s);
+    else if (z.rank == 2) launch_decode<T, 2, O>(z, in32, lo, hi, out, s);
+    else launch_decode<T, 3, O>(z, in32, lo, hi, out, s);
 }
 
 void encode_range(const ZfpShape &z, const void *in, int64_t lo, int64_t hi, uint32_t *out32, unsigned *bad,
                   cudaStream_t s) {
-    if (z.dtype == 0) {
-        if (z.rank == 1) launch_encode<float, 1>(z, in, lo, hi, out32, bad, s);
-        else if (z.rank == 2) launch_encode<float, 2>(z, in, lo, hi, out32, bad, s);
-        else launch_encode<float, 3>(z, in, lo, hi, out32, bad, s);
-    } else {
-        if (z.rank == 1) launch_encode<double, 1>(z, in, lo, hi, out32, bad, s);
-        else if (z.rank == 2) launch_encode<double, 2>(z, in, lo, hi, out32, bad, s);
-        else launch_encode<double, 3>(z, in, lo, hi, out32, bad, s);
-    }
+    if (hi <= lo) return;
+    const bool wide = zfp_wide(z);
+    if (z.dtype == 0) wide ? encode_t<float, int64_t>(z, in, lo, hi, out32, bad, s) : encode_t<float, int32_t>(z, in, lo, hi, out32, bad, s);
+    else wide ? encode_t<double, int64_t>(z, in, lo, hi, out32, bad, s) : encode_t<double, int32_t>(z, in, lo, hi, out32, bad, s);
 }
 
 void decode_range(const ZfpShape &z, const uint32_t *in32, int64_t lo, int64_t hi, void *out, cudaStream_t s) {
-    if (z.dtype == 0) {
-        if (z.rank == 1) launch_decode<float, 1>(z, in32, lo, hi, out, s);
-        else if (z.rank == 2) launch_decode<float, 2>(z, in32, lo, hi, out, s);
-        else launch_decode<float, 3>(z, in32, lo, hi, out, s);
-    } else {
-        if (z.rank == 1) launch_decode<double, 1>(z, in32, lo, hi, out, s);
-        else if (z.rank == 2) launch_decode<double, 2>(z, in32, lo, hi, out, s);
-        else launch_decode<double, 3>(z, in32, lo, hi, out, s);
-    }
+    if (hi <= lo) return;
+    const bool wide = zfp_wide(z);
+    if (z.dtype == 0) wide ? decode_t<float, int64_t>(z, in32, lo, hi, out, s) : decode_t<float, int32_t>(z, in32, lo, hi, out, s);
+    else wide ? decode_t<double, int64_t>(z, in32, lo, hi, out, s) : decode_t<double, int32_t>(z, in32, lo, hi, out, s);
 }
 
 template <class F>

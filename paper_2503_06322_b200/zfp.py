@@ -93,9 +93,9 @@ def stream_info(data) -> tuple:
 
 def zfp_decompress(data, adapter=None, *, device: int | None = None, out=None) -> TensorData:
     """zfp_decompress (zfp.py:311-353).  ``data`` may be bytes-like or a CUDA uint8 tensor."""
-    if getattr(data, "is_cuda", False):
+    if hasattr(data, "data_ptr"):   # torch tensor: CUDA (read in place) or host / pinned
         addr, size = int(data.data_ptr()), int(data.numel() * data.element_size())
-        dtype, dims, _ = _peek(addr, size)   # hpdr_zfp_peek copies the header off the device
+        dtype, dims, _ = _peek(addr, size)   # hpdr_zfp_peek copies a device header itself
     else:
         buf = np.frombuffer(memoryview(data), dtype=np.uint8)
         addr, size = (buf.ctypes.data if buf.size else 0), buf.size

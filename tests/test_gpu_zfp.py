@@ -101,3 +101,27 @@ def test_config_scale_matches_oracle(oracle, dims, dtype, rate):
     assert blob == ref
     back = Z.zfp_decompress(blob).values
     assert np.array_equal(back.view(np.uint8), oracle.zfp_decompress(ref).view(np.uint8))
+
+
+def test_wide_offset_variant_matches_reference(zfp_golden):
+    """The int64-offset kernels (blocks spanning > 2^31 elements) on the golden cases, forced."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.');"
+        "from paper_2503_06322_b200 import zfp as Z;"
+        "d = np.load('tests/golden/zfp.npz'); import json;"
+        "m = json.load(open('tests/golden/zfp.json'))['cases'];"
+        "bad = [c['id'] for c in m[::5] if Z.zfp_compress(d['in%d' % c['id']], c['rate']) != d['blob%d' % c['id']].tobytes()"
+        " or not np.array_equal(Z.zfp_decompress(d['blob%d' % c['id']].tobytes()).values.view(np.uint8),"
+        " d['out%d' % c['id']].view(np.uint8))];"
+        "print('BAD', bad)"
+    )
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300,
+                       env=dict(os.environ, HPDR_ZFP_WIDE="1"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "BAD []" in r.stdout, r.stdout
