@@ -153,8 +153,12 @@ struct BitReader {
 // In-register 32x32 bit-matrix transpose, MSB-first: A[OFF+i] bit (31-j) <-> A[OFF+j] bit (31-i).
 // Turns 32 coefficients into 32 bit planes (and back).  The 16- and 8-bit stages are byte
 // permutes; the 4/2/1-bit stages are two shift+LOP3 pairs (the masks satisfy m << j == ~m).
+//
+// With `need` < 32 only output rows [0, need) are completed (the encoder's truncated planes):
+// after the 16-row stage, row t depends only on the rows of its own aligned group, so groups
+// starting at or beyond `need` are skipped.
 template <int OFF, int N>
-__device__ __forceinline__ void transpose32(uint32_t (&A)[N]) {
+__device__ __forceinline__ void transpose32(uint32_t (&A)[N], int need = 32) {
 #pragma unroll
     for (int i = 0; i < 16; i++) {
         const uint32_t a = A[OFF + i], b = A[OFF + i + 16];
@@ -163,11 +167,13 @@ __device__ __forceinline__ void transpose32(uint32_t (&A)[N]) {
     }
 #pragma unroll
     for (int base = 0; base < 32; base += 16)
+        if (base < need) {
 #pragma unroll
-        for (int i = 0; i < 8; i++) {
-            const uint32_t a = A[OFF + base + i], b = A[OFF + base + i + 8];
-            A[OFF + base + i] = __byte_perm(a, b, 0x3715);
-            A[OFF + base + i + 8] = __byte_perm(a, b, 0x2604);
+            for (int i = 0; i < 8; i++) {
+                const uint32_t a = A[OFF + base + i], b = A[OFF + base + i + 8];
+                A[OFF + base + i] = __byte_perm(a, b, 0x3715);
+                A[OFF + base + i + 8] = __byte_perm(a, b, 0x2604);
+            }
         }
 #pragma unroll
     for (int lj = 2; lj >= 0; lj--) {
@@ -175,11 +181,13 @@ __device__ __forceinline__ void transpose32(uint32_t (&A)[N]) {
         const uint32_t m = lj == 2 ? 0x0F0F0F0Fu : lj == 1 ? 0x33333333u : 0x55555555u;
 #pragma unroll
         for (int base = 0; base < 32; base += 2 * j)
+            if (base < need) {
 #pragma unroll
-            for (int i = 0; i < j; i++) {
-                const uint32_t a = A[OFF + base + i], b = A[OFF + base + i + j];
-                A[OFF + base + i] = (a & ~m) | ((b >> j) & m);
-                A[OFF + base + i + j] = (b & m) | ((a << j) & ~m);
+                for (int i = 0; i < j; i++) {
+                    const uint32_t a = A[OFF + base + i], b = A[OFF + base + i + j];
+                    A[OFF + base + i] = (a & ~m) | ((b >> j) & m);
+                    A[OFF + base + i + j] = (b & m) | ((a << j) & ~m);
+                }
             }
     }
 }
@@ -211,15 +219,11 @@ __device__ __forceinline__ void align_block(const T (&v)[M], typename ZSpec<T>::
         zero = m == 0.f;
         emax = max((int)(__float_as_uint(m) >> 23) - 127, -127);   // subnormal maxima clamp to -127
         const int shift = 30 - emax;                                  // in [-98, 157]
-        if (shift <= 127) {
-            const float s = pow2f(shift);
+        // 2^shift as two exact factors (2^shift * 1, or 2^(shift-64) * 2^64 above 2^127)
+        const bool big = shift > 127;
+        const float s1 = pow2f(big ? shift - 64 : shift), s2 = big ? pow2f(64) : 1.0f;
 #pragma unroll
-            for (int f = 0; f < M; f++) fx[f] = (U)__float2int_rn(__fmul_rn(v[f], s));
-        } else {
-            const float s = pow2f(shift - 64), s64 = pow2f(64);
-#pragma unroll
-            for (int f = 0; f < M; f++) fx[f] = (U)__float2int_rn(__fmul_rn(__fmul_rn(v[f], s), s64));
-        }
+        for (int f = 0; f < M; f++) fx[f] = (U)__float2int_rn(__fmul_rn(__fmul_rn(v[f], s1), s2));
     } else {
         double m = 0.0;
         finite = true;
@@ -232,29 +236,36 @@ __device__ __forceinline__ void align_block(const T (&v)[M], typename ZSpec<T>::
         zero = m == 0.0;
         emax = (int)((__double_as_longlong(m) >> 52) & 0x7ff) - 1023;   // subnormal maxima: -1023
         const int shift = 62 - emax;                                      // in [-962, 1085]
-        if (shift <= 1023) {
-            const double s = pow2(shift);
+        const bool big = shift > 1023;
+        const double s1 = pow2(big ? shift - 64 : shift), s2 = big ? pow2(64) : 1.0;
 #pragma unroll
-            for (int f = 0; f < M; f++) fx[f] = (U)__double2ll_rn(__dmul_rn(v[f], s));
-        } else {
-            const double s = pow2(shift - 64), s64 = pow2(64);
-#pragma unroll
-            for (int f = 0; f < M; f++) fx[f] = (U)__double2ll_rn(__dmul_rn(__dmul_rn(v[f], s), s64));
-        }
+        for (int f = 0; f < M; f++) fx[f] = (U)__double2ll_rn(__dmul_rn(__dmul_rn(v[f], s1), s2));
     }
 }
 
 // exp_restore (zfp.py:153-157): ldexp(float64(fixed), e_max-(q-2)), then the F32 cast -- one
 // rounding of the exact value.  F32 with every nonzero result normal (sc >= -126): int->fp32
-// rounding followed by an exact power-of-two scale is that same single rounding.
-template <class T>
-__device__ __forceinline__ T restore(typename ZSpec<T>::S x, int sc) {
+// rounding followed by an exact power-of-two scale is that same single rounding; otherwise the
+// float64 product is exact (sc >= -157) and the cast rounds once.  F64: one multiply is correctly
+// rounded for sc >= -1022; below, x * 2^(sc+64) is exact and the * 2^-64 rounds once.
+template <class T, int M>
+__device__ __forceinline__ void restore_block(const typename ZSpec<T>::U (&fx)[M], int sc, T (&r)[M]) {
+    using S = typename ZSpec<T>::S;
     if constexpr (sizeof(T) == 4) {
-        if (sc >= -126) return __fmul_rn(__int2float_rn(x), pow2f(sc));
-        return __double2float_rn(__dmul_rn((double)x, pow2(sc)));   // sc >= -157: exact product
+        if (sc >= -126) {
+            const float s = pow2f(sc);
+#pragma unroll
+            for (int f = 0; f < M; f++) r[f] = __fmul_rn(__int2float_rn((S)fx[f]), s);
+        } else {
+            const double s = pow2(sc);
+#pragma unroll
+            for (int f = 0; f < M; f++) r[f] = __double2float_rn(__dmul_rn((double)(S)fx[f], s));
+        }
     } else {
-        const double d = __ll2double_rn(x);
-        return sc >= -1022 ? __dmul_rn(d, pow2(sc)) : __dmul_rn(__dmul_rn(d, pow2(sc + 64)), pow2(-64));
+        const bool low = sc < -1022;
+        const double s1 = pow2(low ? sc + 64 : sc), s2 = low ? pow2(-64) : 1.0;
+#pragma unroll
+        for (int f = 0; f < M; f++) r[f] = __dmul_rn(__dmul_rn(__ll2double_rn((S)fx[f]), s1), s2);
     }
 }
 
@@ -270,8 +281,7 @@ struct BlockAt {
     int64_t origin;
     O row[16];     // D=3: row[a*4+c] for in-block (i0=a, i1=c); D=2: row[a*4] for i1=a
     int col[4];    // clamped axis-2 offsets
-    bool full2;    // no clamping along the last axis
-    bool full;     // no clamping at all (interior block)
+    uint32_t rvalid;   // bit r: row r lies inside the field (not padding)
 };
 
 template <int D, class O>
@@ -282,8 +292,7 @@ __device__ __forceinline__ void block_at(const ZGrid &G, int64_t b, BlockAt<D, O
     B.origin = (x0 * G.n[1] + x1) * G.n[2] + x2;
 #pragma unroll
     for (int i = 0; i < 4; i++) B.col[i] = (int)(min64(x2 + i, G.n[2] - 1) - x2);
-    B.full2 = x2 + 3 < G.n[2];
-    B.full = B.full2 && (D < 2 || x1 + 3 < G.n[1]) && (D < 3 || x0 + 3 < G.n[0]);
+    B.rvalid = 0;
 #pragma unroll
     for (int a = 0; a < 4; a++)
 #pragma unroll
@@ -291,6 +300,8 @@ __device__ __forceinline__ void block_at(const ZGrid &G, int64_t b, BlockAt<D, O
             const int64_t da = D == 3 ? min64(x0 + a, G.n[0] - 1) - x0 : 0;
             const int64_t dc = D == 3 ? min64(x1 + c, G.n[1] - 1) - x1 : D == 2 ? min64(x1 + a, G.n[1] - 1) - x1 : 0;
             B.row[a * 4 + c] = (O)((da * G.n[1] + dc) * G.n[2]);
+            const bool ok = D == 3 ? (x0 + a < G.n[0] && x1 + c < G.n[1]) : D == 2 ? x1 + a < G.n[1] : a == 0;
+            B.rvalid |= (ok ? 1u : 0u) << (a * 4 + c);
         }
 }
 
@@ -315,19 +326,20 @@ __global__ void __launch_bounds__(kZThreads) k_zfp_encode(const T *__restrict__ 
     const int64_t cta0 = b_lo + (int64_t)blockIdx.x * kZThreads;
     const int nblk = (int)min64(kZThreads, b_hi - cta0);
     const uint32_t words = (uint32_t)(((uint64_t)nblk * w + 31) / 32);
-    for (uint32_t i = threadIdx.x; i < words; i += kZThreads) zs[i] = 0;
+    for (uint32_t i = threadIdx.x; i < (words + 3) / 4; i += kZThreads) reinterpret_cast<uint4 *>(zs)[i] = uint4{0, 0, 0, 0};
     __syncthreads();
     if ((int)threadIdx.x < nblk) {
         BlockAt<D, O> B;
         block_at<D, O>(G, cta0 + threadIdx.x, B);
         const T *p = in + B.origin;
         T v[M];   // np.asarray(blocks, float64): widening is exact, see align_block
-        if (B.full2) {
+        // in-range columns are loaded; padded ones repeat the last in-range column (edge mode)
+        const int c2 = B.col[3];   // last in-range column of this block (0..3)
 #pragma unroll
-            for (int f = 0; f < M; f++) v[f] = __ldg(p + B.row[row_of<D>(f)] + (f & 3));
-        } else {
-#pragma unroll
-            for (int f = 0; f < M; f++) v[f] = __ldg(p + B.row[row_of<D>(f)] + B.col[f & 3]);
+        for (int f = 0; f < M; f++) {
+            const int i = f & 3;
+            if (i == 0 || i <= c2) v[f] = __ldg(p + B.row[row_of<D>(f)] + i);
+            else v[f] = v[f - 1];
         }
         U fx[M];
         int emax;
@@ -337,40 +349,70 @@ __global__ void __launch_bounds__(kZThreads) k_zfp_encode(const T *__restrict__ 
         transform<D, U, S, true>(fx);
         U c[M];
         gather_perm<D, U>(fx, c, std::make_integer_sequence<int, M>{});
+        // zfp.py:204-208 negabinary (c + nb) ^ nb; a zero block is all zeros already (fixed = 0).
+        // For D = 3 the ^ nb is applied to the plane words instead: nb's bit (q-1-t) is set for
+        // even t, so even planes are complemented.
 #pragma unroll
-        for (int k = 0; k < M; k++) c[k] = zero ? (U)0 : (U)((c[k] + Z::nb) ^ Z::nb);   // zfp.py:204-208
-        BitWriter bw(zs, (uint32_t)threadIdx.x * w);
-        bw.put(zero ? 1u : 0u, 1);
-        bw.put(zero ? 0u : (uint32_t)(emax + Z::bias), Z::ebits);
+        for (int k = 0; k < M; k++) c[k] = D == 3 ? (U)(c[k] + Z::nb) : (U)((c[k] + Z::nb) ^ Z::nb);
+        const uint32_t pos0 = (uint32_t)threadIdx.x * w;
         if constexpr (D == 3) {
-            // planes MSB first: transpose the 64 coefficients' top halves into 32 plane pairs
+            // planes MSB first: transpose the 64 coefficients' top halves into 32 plane pairs, then
+            // emit whole words at the thread's fixed bit phase (funnel shifts).  The header and the
+            // first word can share a word with the previous block (atomicOr); the last partial word
+            // with the next one; every word between belongs to this thread alone (plain stores).
+            const uint32_t head = ((zero ? 1u : 0u) << Z::ebits) | (zero ? 0u : (uint32_t)(emax + Z::bias));
+            const uint32_t p1 = pos0 + 1 + Z::ebits;      // first plane bit
+            const uint32_t ph = p1 & 31;                  // bit phase of every plane word
+            uint32_t wi = p1 >> 5;
+            // prev: this block's bits of word wi that precede p1 (the header's tail), in place
+            uint32_t prev;
+            {
+                const uint32_t hb = 1 + Z::ebits, end = (pos0 & 31) + hb;
+                if (end < 32) {
+                    prev = head << (32 - end);                               // header inside word wi
+                } else {
+                    atomicOr(&zs[pos0 >> 5], head >> (end - 32));            // completes the word before
+                    prev = end == 32 ? 0u : head << (64 - end);
+                }
+            }
+            auto word_of = [&](uint32_t x) {
+                const uint32_t word = ph ? (prev | (x >> ph)) : x;
+                prev = ph ? x << (32 - ph) : 0u;
+                return word;
+            };
             uint32_t hi[64];
 #pragma unroll
             for (int k = 0; k < 64; k++) hi[k] = (uint32_t)(c[k] >> (Z::q - 32));
-            transpose32<0>(hi);
-            transpose32<32>(hi);
+            transpose32<0>(hi, rate);
+            transpose32<32>(hi, rate);
+            atomicOr(&zs[wi++], word_of(~hi[0]));   // may hold the previous block's tail (rate >= 1)
+            zs[wi++] = word_of(~hi[32]);
 #pragma unroll
-            for (int t = 0; t < 32; t++)
+            for (int t = 1; t < 32; t++)
                 if (t < rate) {
-                    bw.put(hi[t], 32);
-                    bw.put(hi[32 + t], 32);
+                    zs[wi++] = word_of(t % 2 ? hi[t] : ~hi[t]);
+                    zs[wi++] = word_of(t % 2 ? hi[32 + t] : ~hi[32 + t]);
                 }
             if constexpr (Z::q == 64) {
                 if (rate > 32) {
                     uint32_t lo[64];
 #pragma unroll
                     for (int k = 0; k < 64; k++) lo[k] = (uint32_t)c[k];
-                    transpose32<0>(lo);
-                    transpose32<32>(lo);
+                    transpose32<0>(lo, rate - 32);
+                    transpose32<32>(lo, rate - 32);
 #pragma unroll
                     for (int t = 0; t < 32; t++)
                         if (32 + t < rate) {
-                            bw.put(lo[t], 32);
-                            bw.put(lo[32 + t], 32);
+                            zs[wi++] = word_of(t % 2 ? lo[t] : ~lo[t]);
+                            zs[wi++] = word_of(t % 2 ? lo[32 + t] : ~lo[32 + t]);
                         }
                 }
             }
+            if (ph) atomicOr(&zs[wi], prev);   // trailing partial word, shared with the next block
         } else {
+            BitWriter bw(zs, pos0);
+            bw.put(zero ? 1u : 0u, 1);
+            bw.put(zero ? 0u : (uint32_t)(emax + Z::bias), Z::ebits);
             for (int t = 0; t < rate; t++) {
                 const int sh = Z::q - 1 - t;
                 uint32_t pl = 0;
@@ -378,12 +420,18 @@ __global__ void __launch_bounds__(kZThreads) k_zfp_encode(const T *__restrict__ 
                 for (int k = 0; k < M; k++) pl |= (uint32_t)((c[k] >> sh) & 1) << (M - 1 - k);
                 bw.put(pl, M);
             }
+            bw.flush();
         }
-        bw.flush();
     }
     __syncthreads();
+    // 128 blocks = 4*w words, so every CTA's slice of the stream starts 16-byte aligned
     uint32_t *dst = out32 + (uint64_t)(cta0 - b_lo) * w / 32;
-    for (uint32_t i = threadIdx.x; i < words; i += kZThreads) dst[i] = __byte_perm(zs[i], 0, 0x0123);
+    for (uint32_t i = threadIdx.x; i < words / 4; i += kZThreads) {
+        const uint4 x = reinterpret_cast<const uint4 *>(zs)[i];
+        reinterpret_cast<uint4 *>(dst)[i] = uint4{__byte_perm(x.x, 0, 0x0123), __byte_perm(x.y, 0, 0x0123),
+                                                  __byte_perm(x.z, 0, 0x0123), __byte_perm(x.w, 0, 0x0123)};
+    }
+    for (uint32_t i = words / 4 * 4 + threadIdx.x; i < words; i += kZThreads) dst[i] = __byte_perm(zs[i], 0, 0x0123);
 }
 
 // zfp_decompress per block (zfp.py:338-347): bitplane_decode :244-264, inverse_transform,
@@ -401,7 +449,12 @@ __global__ void __launch_bounds__(kZThreads) k_zfp_decode(const uint32_t *__rest
     const int nblk = (int)min64(kZThreads, b_hi - cta0);
     const uint32_t words = (uint32_t)(((uint64_t)nblk * w + 31) / 32);
     const uint32_t *src = in32 + (uint64_t)(cta0 - b_lo) * w / 32;
-    for (uint32_t i = threadIdx.x; i <= words; i += kZThreads)
+    for (uint32_t i = threadIdx.x; i < words / 4; i += kZThreads) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4 *>(src) + i);
+        reinterpret_cast<uint4 *>(zs)[i] = uint4{__byte_perm(x.x, 0, 0x0123), __byte_perm(x.y, 0, 0x0123),
+                                                 __byte_perm(x.z, 0, 0x0123), __byte_perm(x.w, 0, 0x0123)};
+    }
+    for (uint32_t i = words / 4 * 4 + threadIdx.x; i <= words; i += kZThreads)
         zs[i] = i < words ? __byte_perm(__ldg(src + i), 0, 0x0123) : 0u;
     __syncthreads();
     if ((int)threadIdx.x >= nblk) return;
@@ -409,6 +462,7 @@ __global__ void __launch_bounds__(kZThreads) k_zfp_decode(const uint32_t *__rest
     const bool zero = br.get(1) != 0;
     const int biased = (int)br.get(Z::ebits);
     const int emax = zero ? -Z::bias : biased - Z::bias;
+    const int reff = zero ? 0 : rate;   // a zero block's planes are ignored (zfp.py:263, :346)
     U c[M];
     if constexpr (D == 3) {
         // 32-bit plane halves at a fixed bit phase: one shared load + funnel shift each
@@ -424,8 +478,8 @@ __global__ void __launch_bounds__(kZThreads) k_zfp_decode(const uint32_t *__rest
         uint32_t hi[64];
 #pragma unroll
         for (int t = 0; t < 32; t++) {
-            hi[t] = t < rate ? next32() : 0u;
-            hi[32 + t] = t < rate ? next32() : 0u;
+            hi[t] = t < reff ? next32() : 0u;
+            hi[32 + t] = t < reff ? next32() : 0u;
         }
         transpose32<0>(hi);
         transpose32<32>(hi);
@@ -433,10 +487,10 @@ __global__ void __launch_bounds__(kZThreads) k_zfp_decode(const uint32_t *__rest
             uint32_t lo[64];
 #pragma unroll
             for (int t = 0; t < 32; t++) {
-                lo[t] = 32 + t < rate ? next32() : 0u;
-                lo[32 + t] = 32 + t < rate ? next32() : 0u;
+                lo[t] = 32 + t < reff ? next32() : 0u;
+                lo[32 + t] = 32 + t < reff ? next32() : 0u;
             }
-            if (rate > 32) {
+            if (reff > 32) {
                 transpose32<0>(lo);
                 transpose32<32>(lo);
             }
@@ -449,7 +503,7 @@ __global__ void __launch_bounds__(kZThreads) k_zfp_decode(const uint32_t *__rest
     } else {
 #pragma unroll
         for (int k = 0; k < M; k++) c[k] = 0;
-        for (int t = 0; t < rate; t++) {
+        for (int t = 0; t < reff; t++) {
             const int sh = Z::q - 1 - t;
             const uint32_t pl = br.get(M);
 #pragma unroll
@@ -464,22 +518,12 @@ __global__ void __launch_bounds__(kZThreads) k_zfp_decode(const uint32_t *__rest
     BlockAt<D, O> B;
     block_at<D, O>(G, cta0 + threadIdx.x, B);
     T *q = out + B.origin;
-    const int sc = emax - (Z::q - 2);
-    if (B.full) {
+    T r[M];
+    restore_block<T, M>(fx, emax - (Z::q - 2), r);
+    const int c2 = B.col[3];
 #pragma unroll
-        for (int f = 0; f < M; f++) q[B.row[row_of<D>(f)] + (f & 3)] = zero ? (T)0 : restore<T>((S)fx[f], sc);
-    } else {
-        // a clamped position repeats an earlier one, whose value is the one kept
-        const int64_t b = cta0 + threadIdx.x;
-        const int64_t b2 = b % G.g[2], r = b / G.g[2];
-        const int64_t b1 = r % G.g[1], b0 = r / G.g[1];
-#pragma unroll
-        for (int f = 0; f < M; f++) {
-            const int p0 = D == 3 ? f >> 4 : 0, p1 = D == 3 ? (f >> 2) & 3 : D == 2 ? f >> 2 : 0, p2 = f & 3;
-            if (b0 * 4 + p0 >= G.n[0] || b1 * 4 + p1 >= G.n[1] || b2 * 4 + p2 >= G.n[2]) continue;
-            q[B.row[row_of<D>(f)] + (f & 3)] = zero ? (T)0 : restore<T>((S)fx[f], sc);
-        }
-    }
+    for (int f = 0; f < M; f++)   // padding positions are discarded (unpartition_blocks :122)
+        if (((B.rvalid >> row_of<D>(f)) & 1) && (f & 3) <= c2) q[B.row[row_of<D>(f)] + (f & 3)] = r[f];
 }
 
 struct ZfpShape {
