@@ -10,7 +10,7 @@ LABELS = {"pass1q": "k_level_pass1q", "pass1r": "k_level_pass1r", "pass2": "k_le
 d = sys.argv[1]
 out = sys.argv[2] if len(sys.argv) > 2 else os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                                          "profiles", "ncu_traffic.json")
-res = {}
+res = json.load(open(out)) if os.path.exists(out) else {}   # merge: other kernels keep their captures
 for f in sorted(os.listdir(d)):
     if not f.endswith(".ncu-rep"):
         continue
