@@ -421,6 +421,19 @@ def main():
         def zfp_d_e2e():
             ZF.zfp_decompress(z_host_in, out=h_out)
 
+        # the fixed-rate reducer through the streams pipeline (HPDR container, pipeline id 1)
+        zp_len = len(ZF.compress_pipelined(h_in, zrate))
+        zp_out = torch.empty(zp_len, dtype=torch.uint8).pin_memory().numpy()
+        ZF.compress_pipelined(h_in, zrate, out=zp_out)
+        zp_in = torch.from_numpy(zp_out.copy()).pin_memory().numpy()
+        zp_dec = torch.empty(a.shape, dtype=d_in.dtype).pin_memory().numpy()
+
+        def zfp_pc():
+            ZF.compress_pipelined(h_in, zrate, out=zp_out)
+
+        def zfp_pd():
+            PL.decompress_pipelined(zp_in, out=zp_dec)
+
     K = args.steps
     pcie = pcie_roofline(dev)
     with ClockSampler(local) as clk:
@@ -437,6 +450,8 @@ def main():
             zd_ms, zd_l, zdkern = timed(zfp_d_dev, K, prof=True)
             zce_ms, _, _ = timed(zfp_c_e2e, K)
             zde_ms, _, _ = timed(zfp_d_e2e, K)
+            zpc_ms, _, _ = timed(zfp_pc, K)
+            zpd_ms, _, _ = timed(zfp_pd, K)
     clocks = clk.summary()
     _, ptr_c = PL.compress_pipelined(h_in, cfg["eb"], value_range=vr_abs, out=pipe_out, trace=True)
     _, ptr_d = PL.decompress_pipelined(pipe_in, out=h_out2, trace=True)
@@ -541,6 +556,13 @@ def main():
             "decompress_e2e": {"value": gbs(zde_ms), "unit": "GB/s", "h2d_bytes_per_step": z_len,
                                "d2h_bytes_per_step": nbytes, "ms_per_step": zde_ms,
                                "pcie_roofline_frac": t_zd / (zde_ms * 1e-3)},
+            "pipeline": {"mode": "streams pipeline, ~64 MB chunks, HPDR container (pipeline id 1)",
+                         "container_bytes": zp_len, "compress_e2e_gbs": gbs(zpc_ms), "compress_ms": zpc_ms,
+                         "decompress_e2e_gbs": gbs(zpd_ms), "decompress_ms": zpd_ms,
+                         "compress_pcie_roofline_frac": max(nbytes / (pcie["h2d"] * 1e9),
+                                                            zp_len / (pcie["d2h"] * 1e9)) / (zpc_ms * 1e-3),
+                         "decompress_pcie_roofline_frac": max(zp_len / (pcie["h2d"] * 1e9),
+                                                              nbytes / (pcie["d2h"] * 1e9)) / (zpd_ms * 1e-3)},
             "roofline_encode": zroof(zkern, "k_zfp_encode", zc_ms),
             "roofline_decode": zroof(zdkern, "k_zfp_decode", zd_ms),
         }

@@ -141,6 +141,13 @@ int hpdr_zfp_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, const 
 int hpdr_zfp_peek(const void *stream, uint64_t len, int *dtype, int *rank, uint64_t *dims, uint32_t *rate);
 /* zfp_decompress (zfp.py:311-353): out receives prod(dims) values of the stored dtype. */
 int hpdr_zfp_decompress(hpdr_ctx *ctx, const void *stream, uint64_t len, void *out, uint64_t out_bytes);
+/* run_pipeline with the fixed-rate reducer: dim-0 chunks (chunk_planes, default
+ * ~64 MB in whole 4-plane rows, or the explicit chunk_list), each an independent zfp_compress stream of
+ * its slab, in an HPDR container with pipeline id 1 (params: rate u8).  Decompress with
+ * hpdr_pipeline_decompress (it dispatches on the pipeline id).  trace as hpdr_pipeline_compress. */
+int hpdr_pipeline_zfp_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int rank, const uint64_t *dims,
+                               uint32_t rate, uint64_t chunk_planes, const uint64_t *chunk_list, uint64_t n_list,
+                               void *out, uint64_t out_cap, uint64_t *out_len, double *trace);
 
 /* Kernel launches issued by this thread since the last reset (bench accounting). */
 uint64_t hpdr_launch_count(int reset);

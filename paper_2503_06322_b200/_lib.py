@@ -64,6 +64,8 @@ _SIGS = {
     "hpdr_zfp_peek": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_int), C.POINTER(C.c_int), _u64p,
                                 C.POINTER(C.c_uint32)]),
     "hpdr_zfp_decompress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
+    "hpdr_pipeline_zfp_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _u64p, C.c_uint32, C.c_uint64,
+                                             C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, _u64p, C.c_void_p]),
     "hpdr_pipeline_decompress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p]),
 }
 

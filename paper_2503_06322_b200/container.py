@@ -1,12 +1,14 @@
 """HPDR multi-chunk container.
 
-The reference package defines the format only in its SPEC; every chunk payload here is a
-reference-identical MGARD blob of one dim-0 slab, compressed with the GLOBAL value range so
-the error bound of the whole field holds.
+The reference package defines the format only in its SPEC.  With pipeline id 2 every chunk
+payload is a reference-identical MGARD blob of one dim-0 slab, compressed with the GLOBAL value
+range so the error bound of the whole field holds; with pipeline id 1 every
+chunk is a reference-identical fixed-rate stream (hpdr/zfp.py) of its slab.
 
 Layout (little-endian):
   magic "HPDR" | version u16 | pipeline u8 (0 Huffman, 1 ZFP, 2 MGARD) | dtype u8 | rank u8 |
-  dims u64 x rank | MGARD params: eb_rel f64, dict_size u32, global min f64, global max f64 |
+  dims u64 x rank | params (MGARD: eb_rel f64, dict_size u32, global min f64, global max f64;
+  ZFP: rate u8) |
   chunk count u32 | per chunk: raw offset u64, raw size u64, payload offset u64, payload size u64 |
   header CRC-32 u32 (of every preceding header byte) | payloads
 Offsets are relative to the first payload byte; raw offsets/sizes count elements.
@@ -21,6 +23,7 @@ from .errors import FormatError
 
 MAGIC = b"HPDR"
 VERSION = 1
+PIPELINE_ZFP = 1
 PIPELINE_MGARD = 2
 
 
@@ -43,13 +46,17 @@ class ContainerHeader:
     chunks: list = field(default_factory=list)
     pipeline: int = PIPELINE_MGARD
     version: int = VERSION
+    rate: int = 0   # ZFP containers
 
 
 def header_bytes(h: ContainerHeader) -> bytes:
     out = bytearray(MAGIC)
     out += struct.pack("<HBBB", h.version, h.pipeline, h.dtype, len(h.dims))
     out += struct.pack(f"<{len(h.dims)}Q", *h.dims)
-    out += struct.pack("<dIdd", h.eb_rel, h.dict_size, h.vmin, h.vmax)
+    if h.pipeline == PIPELINE_ZFP:
+        out += struct.pack("<B", h.rate)
+    else:
+        out += struct.pack("<dIdd", h.eb_rel, h.dict_size, h.vmin, h.vmax)
     out += struct.pack("<I", len(h.chunks))
     for c in h.chunks:
         out += struct.pack("<QQQQ", c.raw_offset, c.raw_size, c.payload_offset, c.payload_size)
@@ -79,13 +86,18 @@ def read_container(data) -> tuple:
         version, pipeline, dtype, rank = struct.unpack_from("<HBBB", mv, 4)
         if version != VERSION:
             raise FormatError(f"unsupported container version {version}")
-        if pipeline != PIPELINE_MGARD:
+        if pipeline not in (PIPELINE_MGARD, PIPELINE_ZFP):
             raise FormatError(f"unknown pipeline id {pipeline}")
         pos = 9
         dims = struct.unpack_from(f"<{rank}Q", mv, pos)
         pos += 8 * rank
-        eb_rel, dict_size, vmin, vmax = struct.unpack_from("<dIdd", mv, pos)
-        pos += 28
+        eb_rel, dict_size, vmin, vmax, rate = 0.0, 0, 0.0, 0.0, 0
+        if pipeline == PIPELINE_ZFP:
+            (rate,) = struct.unpack_from("<B", mv, pos)
+            pos += 1
+        else:
+            eb_rel, dict_size, vmin, vmax = struct.unpack_from("<dIdd", mv, pos)
+            pos += 28
         (n,) = struct.unpack_from("<I", mv, pos)
         pos += 4
         chunks = []
@@ -98,13 +110,14 @@ def read_container(data) -> tuple:
     if zlib.crc32(bytes(mv[:pos])) & 0xFFFFFFFF != crc:
         raise FormatError("header checksum mismatch")
     pos += 4
-    h = ContainerHeader(dtype, tuple(dims), eb_rel, dict_size, vmin, vmax, chunks, pipeline, version)
+    h = ContainerHeader(dtype, tuple(dims), eb_rel, dict_size, vmin, vmax, chunks, pipeline, version, rate)
     payloads = []
     prev = -1
     for c in chunks:
-        if c.payload_offset <= prev and c.payload_size:
-            raise FormatError("payload offsets not strictly increasing")
-        prev = c.payload_offset
+        if c.payload_size:   # empty payloads occupy no bytes (their offset repeats the next one)
+            if c.payload_offset <= prev:
+                raise FormatError("payload offsets not strictly increasing")
+            prev = c.payload_offset
         a, b = pos + c.payload_offset, pos + c.payload_offset + c.payload_size
         if b > len(mv):
             raise FormatError("container truncated in payloads")

@@ -35,6 +35,8 @@ void compress_from_coef(hpdr_ctx *ctx, const double *coef, int dtype, int rank, 
 void decompose_chunk(hpdr_ctx *ctx, const void *d_in, int dtype, int rank, const uint64_t *dims, double *coef,
                      unsigned long long *mm);
 void fetch_pending_on(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uint64_t cap, cudaStream_t s, bool sync);
+int zfp_container_decompress(hpdr_ctx *ctx, const uint8_t *c, uint64_t len, void *out, uint64_t out_bytes,
+                             double *trace);   // zfp.cu: pipeline id 1
 
 namespace {
 
@@ -425,6 +427,7 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
         uint16_t ver;
         memcpy(&ver, c + 4, 2);
         if (ver != 1) throw Error{HPDR_ERR_FORMAT, "unsupported container version", -1};
+        if (c[6] == 1) return zfp_container_decompress(ctx, c, len, out, out_bytes, trace);
         if (c[6] != 2) throw Error{HPDR_ERR_FORMAT, "unknown pipeline id", -1};
         const int dtype = c[7], rank = c[8];
         uint64_t pos = 9;

@@ -687,6 +687,64 @@ int zfp_slab_count(const ZfpShape &z, uint64_t in_bytes) {
     return (int)std::min<uint64_t>(16, std::max<uint64_t>(1, in_bytes / (32ull << 20)));
 }
 
+
+// ---- HPDR container with fixed-rate chunks (pipeline id 1, params: rate u8) ----
+uint32_t zcrc32(const uint8_t *p, size_t n) {   // zlib polynomial (container.py uses zlib.crc32)
+    uint32_t c = 0xFFFFFFFFu;
+    for (size_t i = 0; i < n; i++) {
+        c ^= p[i];
+        for (int k = 0; k < 8; k++) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
+    }
+    return c ^ 0xFFFFFFFFu;
+}
+
+struct ZChunk {
+    uint64_t raw_off, raw_size, pay_off, pay_size;
+};
+
+template <class X>
+void zput(std::vector<uint8_t> &v, X x) {
+    const size_t o = v.size();
+    v.resize(o + sizeof(X));
+    memcpy(v.data() + o, &x, sizeof(X));
+}
+
+std::vector<uint8_t> zfp_container_header(int dtype, int rank, const uint64_t *dims, int rate,
+                                          const std::vector<ZChunk> &ch) {
+    std::vector<uint8_t> h = {'H', 'P', 'D', 'R'};
+    zput<uint16_t>(h, 1);
+    zput<uint8_t>(h, 1);   // ZFP
+    zput<uint8_t>(h, (uint8_t)dtype);
+    zput<uint8_t>(h, (uint8_t)rank);
+    for (int d = 0; d < rank; d++) zput<uint64_t>(h, dims[d]);
+    zput<uint8_t>(h, (uint8_t)rate);
+    zput<uint32_t>(h, (uint32_t)ch.size());
+    for (const ZChunk &c : ch) {
+        zput<uint64_t>(h, c.raw_off);
+        zput<uint64_t>(h, c.raw_size);
+        zput<uint64_t>(h, c.pay_off);
+        zput<uint64_t>(h, c.pay_size);
+    }
+    zput<uint32_t>(h, zcrc32(h.data(), h.size()));
+    return h;
+}
+
+// Per-chunk copy/compute timestamps (ms from the first event): H2D start/end, compute start/end,
+// D2H start/end -- the trace layout of hpdr_pipeline_compress.
+struct ZTimer {
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t t0 = nullptr;
+    explicit ZTimer(size_t n) {
+        CUDA_CHECK(cudaEventCreate(&t0));
+        ev.resize(n);
+        for (auto &e : ev) CUDA_CHECK(cudaEventCreate(&e));
+    }
+    ~ZTimer() {
+        if (t0) cudaEventDestroy(t0);
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
 }  // namespace
 }  // namespace hpdr
 
@@ -846,4 +904,229 @@ int hpdr_zfp_decompress(hpdr_ctx *ctx, const void *stream, uint64_t len, void *o
     });
 }
 
+
+// Streams pipeline with fixed-rate chunks (the reducer slot of run_pipeline):
+// dim-0 slabs, each an independent zfp_compress(slab, rate) stream, in an HPDR container with
+// pipeline id 1.  Stream sizes are a function of the slab shape, so the whole container layout is
+// known before any work starts: chunk k's H2D, encode and D2H are issued without host syncs, with
+// two input and two output device buffers (Fig. 7 reuse edges as events: the H2D of chunk k+2
+// waits for chunk k's encode, the encode of chunk k+2 for chunk k's D2H).
+int hpdr_pipeline_zfp_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int rank, const uint64_t *dims,
+                               uint32_t rate, uint64_t chunk_planes, const uint64_t *chunk_list, uint64_t n_list,
+                               void *out, uint64_t out_cap, uint64_t *out_len, double *trace) {
+    return zguard([&] {
+        ZfpShape whole;
+        zfp_shape(dtype, rank, dims, (int)std::min<uint32_t>(rate, 1u << 20), whole);
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        const int isz = dtype == 0 ? 4 : 8;
+        uint64_t plane = 1;   // elements per dim-0 index (the chunking axis is the caller's dims[0])
+        for (int d = 1; d < rank; d++) plane *= dims[d];
+        const uint64_t n0 = dims[0];
+        std::vector<uint64_t> planes;
+        if (chunk_list && n_list) {
+            uint64_t sum = 0;
+            for (uint64_t i = 0; i < n_list; i++) {
+                if (!chunk_list[i]) throw Error{HPDR_ERR_VALIDATION, "chunk of 0 planes", -1};
+                planes.push_back(chunk_list[i]);
+                sum += chunk_list[i];
+            }
+            if (sum != n0) throw Error{HPDR_ERR_VALIDATION, "chunk plane counts do not sum to dims[0]", -1};
+        } else {
+            // default ~64 MB of input per chunk, whole 4-plane block rows
+            uint64_t cp = chunk_planes ? chunk_planes : std::max<uint64_t>(4, ((64ull << 20) / (plane * isz)) / 4 * 4);
+            for (uint64_t a = 0; a < n0; a += cp) planes.push_back(std::min(cp, n0 - a));
+        }
+        const size_t K = planes.size();
+        std::vector<ZChunk> ch(K);
+        std::vector<ZfpShape> zs(K);
+        uint64_t off = 0, raw = 0, max_in = 0, max_pay = 0;
+        for (size_t k = 0; k < K; k++) {
+            uint64_t cd[3] = {planes[k], rank > 1 ? dims[1] : 0, rank > 2 ? dims[2] : 0};
+            zfp_shape(dtype, rank, cd, whole.rate, zs[k]);
+            ch[k] = ZChunk{raw, planes[k] * plane, off, zs[k].total};
+            raw += planes[k] * plane;
+            off += zs[k].total;
+            max_in = std::max(max_in, planes[k] * plane * isz);
+            max_pay = std::max(max_pay, zs[k].payload);
+        }
+        const std::vector<uint8_t> head = zfp_container_header(dtype, rank, dims, whole.rate, ch);
+        *out_len = head.size() + off;
+        if (!out || out_cap < *out_len)
+            throw Error{HPDR_ERR_BUFFER, "output buffer too small: need " + std::to_string(*out_len), -1};
+        const bool out_dev = classify(out) == MemKind::Device;
+        const bool in_dev = classify(host_in) == MemKind::Device;
+        uint8_t *o = (uint8_t *)out;
+        cudaStream_t s = ctx->stream;
+        // container header and the per-chunk stream headers (zfp.py:306-308) are host bytes
+        std::vector<uint8_t> hdrs(head);
+        for (size_t k = 0; k < K; k++) {
+            uint8_t zh[kZHeader + 24];
+            zh[0] = (uint8_t)rank;
+            zh[1] = (uint8_t)dtype;
+            zh[2] = (uint8_t)whole.rate;
+            memcpy(zh + kZHeader, zs[k].dims, 8ull * rank);
+            const uint64_t at = head.size() + ch[k].pay_off;
+            if (out_dev) CUDA_CHECK(cudaMemcpyAsync(o + at, zh, kZHeader + 8ull * rank, cudaMemcpyHostToDevice, s));
+            else memcpy(o + at, zh, kZHeader + 8ull * rank);
+        }
+        if (out_dev) CUDA_CHECK(cudaMemcpyAsync(o, head.data(), head.size(), cudaMemcpyHostToDevice, s));
+        else memcpy(o, head.data(), head.size());
+        unsigned *bad = (unsigned *)ctx->dbuf("zfp_bad", 16);
+        unsigned *bad_h = (unsigned *)ctx->hbuf("zfp_bad_h", 16);
+        CUDA_CHECK(cudaMemsetAsync(bad, 0, 4, s));
+        void *din[2] = {in_dev ? nullptr : ctx->dbuf("zfp_pin0", max_in), in_dev ? nullptr : ctx->dbuf("zfp_pin1", max_in)};
+        uint32_t *dp[2] = {(uint32_t *)ctx->dbuf("zfp_ppay0", max_pay + 8), (uint32_t *)ctx->dbuf("zfp_ppay1", max_pay + 8)};
+        std::unique_ptr<ZTimer> tm(trace ? new ZTimer(6 * K) : nullptr);
+        CUDA_CHECK(cudaEventRecord(ctx->event(480), s));   // everything after the setup above
+        CUDA_CHECK(cudaStreamWaitEvent(ctx->h2d, ctx->event(480), 0));
+        CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(480), 0));
+        if (tm) CUDA_CHECK(cudaEventRecord(tm->t0, s));
+        for (size_t k = 0; k < K; k++) {
+            const int b = (int)(k & 1);
+            const void *src;
+            if (in_dev) {
+                src = (const uint8_t *)host_in + ch[k].raw_off * isz;
+            } else {
+                if (k >= 2) CUDA_CHECK(cudaStreamWaitEvent(ctx->h2d, ctx->event(482 + b), 0));   // encode k-2 read din[b]
+                if (tm) CUDA_CHECK(cudaEventRecord(tm->ev[6 * k], ctx->h2d));
+                CUDA_CHECK(cudaMemcpyAsync(din[b], (const uint8_t *)host_in + ch[k].raw_off * isz, ch[k].raw_size * isz,
+                                           cudaMemcpyHostToDevice, ctx->h2d));
+                if (tm) CUDA_CHECK(cudaEventRecord(tm->ev[6 * k + 1], ctx->h2d));
+                CUDA_CHECK(cudaEventRecord(ctx->event(486 + b), ctx->h2d));
+                CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(486 + b), 0));
+                src = din[b];
+            }
+            if (k >= 2) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(484 + b), 0));   // D2H k-2 read dp[b]
+            if (tm) CUDA_CHECK(cudaEventRecord(tm->ev[6 * k + 2], s));
+            encode_range(zs[k], src, 0, zs[k].nblk, dp[b], bad, s);
+            if (tm) CUDA_CHECK(cudaEventRecord(tm->ev[6 * k + 3], s));
+            CUDA_CHECK(cudaEventRecord(ctx->event(482 + b), s));
+            CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(482 + b), 0));
+            if (tm) CUDA_CHECK(cudaEventRecord(tm->ev[6 * k + 4], ctx->d2h));
+            CUDA_CHECK(cudaMemcpyAsync(o + head.size() + ch[k].pay_off + kZHeader + 8ull * rank, dp[b], zs[k].payload,
+                                       out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->d2h));
+            if (tm) CUDA_CHECK(cudaEventRecord(tm->ev[6 * k + 5], ctx->d2h));
+            CUDA_CHECK(cudaEventRecord(ctx->event(484 + b), ctx->d2h));
+        }
+        CUDA_CHECK(cudaMemcpyAsync(bad_h, bad, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->d2h));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->h2d));
+        if (*bad_h) throw Error{HPDR_ERR_VALIDATION, "non-finite values cannot be aligned", -1};
+        if (tm)
+            for (size_t i = 0; i < 6 * K; i++) {
+                float ms = 0.f;
+                if (in_dev && (i % 6) < 2) {   // no H2D: report the compute start
+                    CUDA_CHECK(cudaEventElapsedTime(&ms, tm->t0, tm->ev[6 * (i / 6) + 2]));
+                } else {
+                    CUDA_CHECK(cudaEventElapsedTime(&ms, tm->t0, tm->ev[i]));
+                }
+                trace[i] = ms;
+            }
+    });
+}
+
 }  // extern "C"
+
+namespace hpdr {
+
+// Container decompress for pipeline id 1 (called by hpdr_pipeline_decompress after the common
+// magic / version checks).  Mirrors the compress runner: chunk k's stream H2D, decode into a slab
+// buffer (or straight into a device output), D2H of the slab, two buffer sets.
+int zfp_container_decompress(hpdr_ctx *ctx, const uint8_t *c, uint64_t len, void *out, uint64_t out_bytes,
+                             double *trace) {
+    return zguard([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        auto need = [&](uint64_t p, uint64_t n) {
+            if (p > len || n > len - p) throw Error{HPDR_ERR_FORMAT, "container truncated", -1};
+        };
+        need(0, 9);
+        const int dtype = c[7], rank = c[8];
+        if (rank < 1 || rank > 3) throw Error{HPDR_ERR_FORMAT, "bad rank for a fixed-rate container", -1};
+        if (dtype != 0 && dtype != 1) throw Error{HPDR_ERR_FORMAT, "fixed-rate container needs F32/F64", -1};
+        uint64_t pos = 9;
+        need(pos, 8ull * rank + 1 + 4);
+        uint64_t dims[3] = {1, 1, 1};
+        memcpy(dims, c + pos, 8ull * rank);
+        pos += 8ull * rank;
+        const int rate = c[pos++];
+        uint32_t K;
+        memcpy(&K, c + pos, 4);
+        pos += 4;
+        need(pos, 32ull * K + 4);
+        std::vector<ZChunk> ch(K);
+        memcpy(ch.data(), c + pos, 32ull * K);
+        pos += 32ull * K;
+        uint32_t crc;
+        memcpy(&crc, c + pos, 4);
+        if (zcrc32(c, pos) != crc) throw Error{HPDR_ERR_FORMAT, "header checksum mismatch", -1};
+        pos += 4;
+        const uint64_t base = pos;
+        ZfpShape whole;
+        zfp_shape(dtype, rank, dims, rate, whole);
+        const int isz = dtype == 0 ? 4 : 8;
+        uint64_t plane = 1;
+        for (int d = 1; d < rank; d++) plane *= dims[d];
+        const uint64_t N = dims[0] * plane;
+        if (out_bytes < N * isz) throw Error{HPDR_ERR_BUFFER, "output buffer too small", -1};
+        std::vector<ZfpShape> zs(K);
+        uint64_t max_pay = 1, max_raw = 1;
+        for (uint32_t k = 0; k < K; k++) {
+            need(base + ch[k].pay_off, ch[k].pay_size);
+            if (ch[k].raw_off + ch[k].raw_size > N || ch[k].raw_off % plane || ch[k].raw_size % plane)
+                throw Error{HPDR_ERR_FORMAT, "chunk outside the field or not whole planes", -1};
+            zfp_parse(c + base + ch[k].pay_off, ch[k].pay_size, zs[k]);   // zfp_decompress's checks per chunk
+            if (zs[k].dtype != dtype || zs[k].rank != rank || zs[k].rate != rate || zs[k].dims[0] * plane != ch[k].raw_size ||
+                (rank > 1 && zs[k].dims[1] != dims[1]) || (rank > 2 && zs[k].dims[2] != dims[2]))
+                throw Error{HPDR_ERR_FORMAT, "chunk stream does not match the container", -1};
+            max_pay = std::max(max_pay, zs[k].payload);
+            max_raw = std::max(max_raw, ch[k].raw_size);
+        }
+        const bool out_dev = classify(out) == MemKind::Device;
+        cudaStream_t s = ctx->stream;
+        uint32_t *dp[2] = {(uint32_t *)ctx->dbuf("zfp_dpay0", max_pay + 8), (uint32_t *)ctx->dbuf("zfp_dpay1", max_pay + 8)};
+        void *dout[2] = {out_dev ? nullptr : ctx->dbuf("zfp_dout0", max_raw * isz),
+                         out_dev ? nullptr : ctx->dbuf("zfp_dout1", max_raw * isz)};
+        std::unique_ptr<ZTimer> tm(trace ? new ZTimer(6 * (size_t)K) : nullptr);
+        CUDA_CHECK(cudaEventRecord(ctx->event(480), s));
+        CUDA_CHECK(cudaStreamWaitEvent(ctx->h2d, ctx->event(480), 0));
+        CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(480), 0));
+        if (tm) CUDA_CHECK(cudaEventRecord(tm->t0, s));
+        for (uint32_t k = 0; k < K; k++) {
+            const int b = (int)(k & 1);
+            const uint64_t hl = kZHeader + 8ull * rank;
+            if (k >= 2) CUDA_CHECK(cudaStreamWaitEvent(ctx->h2d, ctx->event(482 + b), 0));   // decode k-2 read dp[b]
+            if (tm) CUDA_CHECK(cudaEventRecord(tm->ev[6 * k], ctx->h2d));
+            CUDA_CHECK(cudaMemcpyAsync(dp[b], c + base + ch[k].pay_off + hl, zs[k].payload, cudaMemcpyHostToDevice,
+                                       ctx->h2d));
+            if (tm) CUDA_CHECK(cudaEventRecord(tm->ev[6 * k + 1], ctx->h2d));
+            CUDA_CHECK(cudaEventRecord(ctx->event(486 + b), ctx->h2d));
+            CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(486 + b), 0));
+            if (!out_dev && k >= 2) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(484 + b), 0));   // D2H k-2 read dout[b]
+            void *dst = out_dev ? (void *)((uint8_t *)out + ch[k].raw_off * isz) : dout[b];
+            if (tm) CUDA_CHECK(cudaEventRecord(tm->ev[6 * k + 2], s));
+            decode_range(zs[k], dp[b], 0, zs[k].nblk, dst, s);
+            if (tm) CUDA_CHECK(cudaEventRecord(tm->ev[6 * k + 3], s));
+            CUDA_CHECK(cudaEventRecord(ctx->event(482 + b), s));
+            if (!out_dev) {
+                CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(482 + b), 0));
+                if (tm) CUDA_CHECK(cudaEventRecord(tm->ev[6 * k + 4], ctx->d2h));
+                CUDA_CHECK(cudaMemcpyAsync((uint8_t *)out + ch[k].raw_off * isz, dout[b], ch[k].raw_size * isz,
+                                           cudaMemcpyDeviceToHost, ctx->d2h));
+                if (tm) CUDA_CHECK(cudaEventRecord(tm->ev[6 * k + 5], ctx->d2h));
+                CUDA_CHECK(cudaEventRecord(ctx->event(484 + b), ctx->d2h));
+            }
+        }
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->d2h));
+        if (tm)
+            for (size_t i = 0; i < 6 * (size_t)K; i++) {
+                float ms = 0.f;
+                const size_t j = (out_dev && (i % 6) >= 4) ? 6 * (i / 6) + 3 : i;   // no D2H: compute end
+                CUDA_CHECK(cudaEventElapsedTime(&ms, tm->t0, tm->ev[j]));
+                trace[i] = ms;
+            }
+    });
+}
+
+}  // namespace hpdr

@@ -108,4 +108,47 @@ def zfp_decompress(data, adapter=None, *, device: int | None = None, out=None) -
     return TensorData(dims, dtype, res)
 
 
-__all__ = ["BLOCK_SIDE", "MAX_BLOCK_RANK", "compressed_size", "stream_info", "zfp_compress", "zfp_decompress"]
+def compress_pipelined(arr, rate: int, *, chunk_planes: int = 0, chunks=None, device: int | None = None, out=None,
+                       trace: bool = False):
+    """The streams pipeline with the fixed-rate reducer -> HPDR container (pipeline id 1) of
+    per-slab reference-identical streams.  Decompress with ``pipeline.decompress_pipelined``.
+    With ``trace`` returns (bytes, (K, 6) array of H2D / compute / D2H start-end times in ms)."""
+    addr, dims, code, keep = _as_field(arr)
+    dims = tuple(int(d) for d in dims)
+    ctx = _lib.default_context(device, arr if getattr(arr, "is_cuda", False) else out)
+    lst = None if chunks is None else np.ascontiguousarray(chunks, dtype=np.uint64)
+    n = C.c_uint64()
+
+    def run(buf, tr):
+        return lib().hpdr_pipeline_zfp_compress(
+            ctx.handle, C.c_void_p(addr), code, len(dims), dims_arg(dims), int(rate), int(chunk_planes),
+            C.c_void_p(lst.ctypes.data) if lst is not None else None, 0 if lst is None else len(lst),
+            C.c_void_p(_lib.ptr(buf)) if buf is not None else None, 0 if buf is None else int(buf.nbytes),
+            C.byref(n), C.c_void_p(tr.ctypes.data) if tr is not None else None)
+
+    rc = run(None, None) if out is None else _lib.BUFFER   # size query (fixed-rate: exact)
+    if out is None and rc != _lib.BUFFER:
+        check(rc)
+    buf = np.empty(n.value, np.uint8) if out is None else out
+    from .container import read_container
+
+    tr = None
+    if trace:
+        if lst is not None:
+            k = len(lst)
+        else:   # the runner's default: ~64 MB of input per chunk in whole 4-plane rows
+            plane = int(np.prod(dims[1:])) * (4 if code == 0 else 8)
+            cp = chunk_planes or max(4, (64 << 20) // plane // 4 * 4)
+            k = -(-dims[0] // cp)
+        tr = np.zeros(6 * k, np.float64)
+    check(run(buf, tr))
+    del keep
+    data = buf[: n.value].tobytes() if out is None else int(n.value)
+    if not trace:
+        return data
+    h, _ = read_container(buf[: n.value])
+    return data, tr[: 6 * len(h.chunks)].reshape(-1, 6)
+
+
+__all__ = ["BLOCK_SIDE", "MAX_BLOCK_RANK", "compress_pipelined", "compressed_size", "stream_info", "zfp_compress",
+           "zfp_decompress"]

@@ -125,3 +125,46 @@ def test_wide_offset_variant_matches_reference(zfp_golden):
                        env=dict(os.environ, HPDR_ZFP_WIDE="1"))
     assert r.returncode == 0, r.stderr[-2000:]
     assert "BAD []" in r.stdout, r.stdout
+
+
+def _slabs(a, planes):
+    out, p = [], 0
+    for n in planes:
+        out.append(np.ascontiguousarray(a[p:p + n]))
+        p += n
+    return out
+
+
+@pytest.mark.parametrize("dims,dtype,rate,chunks", [((257, 129, 131), np.float32, 16, None),
+                                                    ((130, 66, 35), np.float64, 40, [7, 64, 1, 58]),
+                                                    ((1031, 1029), np.float32, 9, [500, 531])])
+def test_pipeline_container_matches_per_slab_streams(oracle, dims, dtype, rate, chunks):
+    """The fixed-rate reducer through the streams pipeline: an HPDR container (pipeline id 1) whose
+    chunk payloads are byte-identical to the reference stream of each slab."""
+    import torch
+
+    from paper_2503_06322_b200 import pipeline as PL
+    from paper_2503_06322_b200.container import PIPELINE_ZFP, read_container
+
+    oracle.set_threads(16)
+    a = (np.random.default_rng(7).random(dims) * 2 - 1).astype(dtype)
+    pin = torch.from_numpy(a).pin_memory()
+    data, tr = Z.compress_pipelined(pin, rate, chunks=chunks, trace=True, chunk_planes=0 if chunks else 40)
+    h, pays = read_container(data)
+    assert h.pipeline == PIPELINE_ZFP and h.rate == rate and h.dims == dims
+    planes = [c.raw_size // int(np.prod(dims[1:])) for c in h.chunks]
+    if chunks:
+        assert planes == chunks
+    assert tr.shape == (len(planes), 6) and np.all(tr[:, 3] >= tr[:, 2])
+    for slab, p in zip(_slabs(a, planes), pays):
+        assert bytes(p) == oracle.zfp_compress(slab, rate)
+    back = PL.decompress_pipelined(data)
+    ref = np.concatenate([oracle.zfp_decompress(bytes(p)) for p in pays])
+    assert np.array_equal(np.asarray(back.values if hasattr(back, "values") else back).view(np.uint8),
+                          ref.view(np.uint8))
+    # device-resident input and output
+    dev = torch.from_numpy(a).cuda()
+    assert Z.compress_pipelined(dev, rate, chunks=chunks, chunk_planes=0 if chunks else 40) == data
+    dout = torch.empty(dims, dtype=dev.dtype, device="cuda")
+    PL.decompress_pipelined(data, out=dout)
+    assert np.array_equal(dout.cpu().numpy().view(np.uint8), ref.view(np.uint8))

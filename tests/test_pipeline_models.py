@@ -73,3 +73,33 @@ def test_overlap_ratio_spec_examples():
     inside = np.array([[1, 2, 0, 5, 3, 4]], float)
     assert PL.overlap_ratio(inside) == 1.0
     assert PL.overlap_ratio(np.zeros((0, 6))) == 0.0
+
+
+def test_container_headers_round_trip_and_reject_corruption():
+    """HPDR container for both reducers: header bytes round-trip, a flipped header
+    byte fails the CRC, an unknown pipeline id and truncation raise FormatError."""
+    from paper_2503_06322_b200 import container as CT
+    from paper_2503_06322_b200.errors import FormatError
+
+    pays = [b"abc", b"", b"defgh"]
+    for h in (CT.ContainerHeader(0, (9, 4, 5), 1e-3, 4096, -1.0, 2.0,
+                                 [CT.ChunkEntry(0, 40, 0, 3), CT.ChunkEntry(40, 80, 0, 0), CT.ChunkEntry(120, 60, 0, 5)]),
+              CT.ContainerHeader(1, (9, 20), 0.0, 0, 0.0, 0.0,
+                                 [CT.ChunkEntry(0, 60, 0, 3), CT.ChunkEntry(60, 60, 0, 0), CT.ChunkEntry(120, 60, 0, 5)],
+                                 pipeline=CT.PIPELINE_ZFP, rate=17)):
+        data = CT.write_container(h, pays)
+        h2, p2 = CT.read_container(data)
+        assert (h2.pipeline, h2.dtype, h2.dims, h2.rate) == (h.pipeline, h.dtype, h.dims, h.rate)
+        assert [bytes(p) for p in p2] == pays
+        if h.pipeline == CT.PIPELINE_MGARD:
+            assert (h2.eb_rel, h2.dict_size, h2.vmin, h2.vmax) == (1e-3, 4096, -1.0, 2.0)
+        bad = bytearray(data)
+        bad[12] ^= 1
+        with pytest.raises(FormatError):
+            CT.read_container(bytes(bad))
+        bad = bytearray(data)
+        bad[6] = 0
+        with pytest.raises(FormatError):
+            CT.read_container(bytes(bad))
+        with pytest.raises(FormatError):
+            CT.read_container(data[:-1])
