@@ -305,8 +305,8 @@ void restore_coarse(hpdr_ctx *ctx, double *coef, const DevPlan &p, const double 
     long long *hs = (long long *)ctx->hbuf("co_stage", 32 * 8);
     for (size_t k = 0; k < nci; k++) hs[k] = p.host.coarsest[k];
     memcpy(hs + 16, coarse, std::min<size_t>(n_co, 16) * 8);
-    CUDA_CHECK(cudaMemcpyAsync(di, hs, 16 * 8, cudaMemcpyHostToDevice, s));
-    CUDA_CHECK(cudaMemcpyAsync(dv, hs + 16, 16 * 8, cudaMemcpyHostToDevice, s));
+    small_copy(di, hs, 16 * 8, s);
+    small_copy(dv, hs + 16, 16 * 8, s);
     k_set_coarse<<<1, 32, 0, s>>>(coef, di, dv, (int)nci, n_co == 1 && nci != 1);
     LAUNCH_CHECK();
 }
@@ -319,16 +319,16 @@ int scatter_outliers(hpdr_ctx *ctx, double *coef, int64_t n, const uint64_t *h_i
     uint64_t *di = (uint64_t *)ctx->dbuf("dq_oidx", n_out * 8);
     int64_t *db = (int64_t *)ctx->dbuf("dq_obins", n_out * 8);
     int *fl = (int *)ctx->dbuf("dq_flags", 16);
-    CUDA_CHECK(cudaMemcpyAsync(di, h_idx, n_out * 8, cudaMemcpyDefault, s));
-    CUDA_CHECK(cudaMemcpyAsync(db, h_bins, n_out * 8, cudaMemcpyDefault, s));
-    CUDA_CHECK(cudaMemsetAsync(fl, 0, 16, s));
+    small_copy(di, h_idx, n_out * 8, s);
+    small_copy(db, h_bins, n_out * 8, s);
+    zero_async(fl, 16, s);
     {
         KPROF("k_outliers", 24.0 * n_out, s);
         k_outliers<<<grid_for(n_out, 256, 148 * 8), 256, 0, s>>>(coef, n, di, db, n_out, bin_width, fl);
         LAUNCH_CHECK();
     }
     int *h = (int *)ctx->hbuf("dq_flags_h", 16);
-    CUDA_CHECK(cudaMemcpyAsync(h, fl, 4, cudaMemcpyDeviceToHost, s));
+    small_copy(h, fl, 4, s);
     CUDA_CHECK(cudaStreamSynchronize(s));
     if (h[0] & 1) return HPDR_ERR_INDEX;
     if (h[0] & 2) {   // duplicates / unordered (never produced by the encoder): numpy's last-wins order
@@ -376,12 +376,12 @@ void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t 
         // from the coefficient set when there is no dense coarsest level)
         double *hco = (double *)ctx->hbuf("coarse_rb", 16 * 8);
         if (d_coarse) {
-            CUDA_CHECK(cudaMemcpyAsync(hco, d_coarse, nco * 8, cudaMemcpyDeviceToHost, s));
+            small_copy(hco, d_coarse, nco * 8, s);
         } else if (nco) {
             double *dco = (double *)ctx->dbuf("coarse_gather", 16 * 8);
             k_gather_vals<<<1, 32, 0, s>>>(coef_for_coarse, p.coarsest, (int)nco, dco);
             LAUNCH_CHECK();
-            CUDA_CHECK(cudaMemcpyAsync(hco, dco, nco * 8, cudaMemcpyDeviceToHost, s));
+            small_copy(hco, dco, nco * 8, s);
         }
         CUDA_CHECK(cudaStreamSynchronize(s));
         if (nco) memcpy(coarse.data(), hco, nco * 8);
@@ -489,9 +489,9 @@ void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uin
             qo.obins = (long long *)ctx->dbuf("obins_sparse", N * 8);
             qo.hist = (unsigned long long *)ctx->dbuf("hist", (size_t)dict_size * 8);
             qo.flags = (int *)ctx->dbuf("qflags", 16);
-            CUDA_CHECK(cudaMemsetAsync(qo.omask, 0, words * 4, s));
-            CUDA_CHECK(cudaMemsetAsync(qo.hist, 0, (size_t)dict_size * 8, s));
-            CUDA_CHECK(cudaMemsetAsync(qo.flags, 0, 16, s));
+            zero_async(qo.omask, words * 4, s);
+            zero_async(qo.hist, (size_t)dict_size * 8, s);
+            zero_async(qo.flags, 16, s);
             if (streamed) {
                 // the range (relative mode) is complete only after the last chunk; q.bin set inside
                 d_coarse = decompose_quantize_streamed(ctx, p, in, dtype, has_range, range_min, range_max, eb_rel,
@@ -748,7 +748,7 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                 CUDA_CHECK(cudaMemcpyAsync(di, blob + oidx_off, n_out * 8, cudaMemcpyDefault, s));
                 CUDA_CHECK(cudaMemcpyAsync(db, blob + obins_off, n_out * 8, cudaMemcpyDefault, s));
             }
-            CUDA_CHECK(cudaMemsetAsync(fl, 0, 16, s));
+            zero_async(fl, 16, s);
             const int64_t units = S.units;
             const int64_t plane = st0.fsh.n[2] * st0.fsh.n[3];
             const int n0 = (int)st0.fsh.n[1];
@@ -975,7 +975,7 @@ int hpdr_dequantize(hpdr_ctx *ctx, const uint32_t *keys_in, uint64_t n_keys, int
         const uint32_t *keys = (const uint32_t *)device_input(ctx, keys_in, N * 4, "hkeys", s);
         double *coef = classify(coef_out) == MemKind::Device ? coef_out : (double *)ctx->dbuf("coef", N * 8);
         unsigned *kmax = (unsigned *)ctx->dbuf("dq_kmax", 16);
-        CUDA_CHECK(cudaMemsetAsync(kmax, 0, 16, s));
+        zero_async(kmax, 16, s);
         {
             KPROF("k_dequant", 12.0 * N, s);
             k_dequant<<<grid_for(N, 256, 148 * 16), 256, 0, s>>>(keys, N, bin_width, coef, kmax);

@@ -112,6 +112,52 @@ MemKind classify(const void *p) {
     return MemKind::Host;
 }
 
+namespace {
+__global__ void k_small_copy(uint8_t *__restrict__ dst, const uint8_t *__restrict__ src, size_t n) {
+    const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+    if ((((uintptr_t)dst | (uintptr_t)src) & 7) == 0) {
+        const size_t nw = n / 8;
+        for (size_t i = tid; i < nw; i += nt) reinterpret_cast<uint64_t *>(dst)[i] = reinterpret_cast<const uint64_t *>(src)[i];
+        for (size_t i = nw * 8 + tid; i < n; i += nt) dst[i] = src[i];
+    } else {
+        for (size_t i = tid; i < n; i += nt) dst[i] = src[i];
+    }
+}
+__global__ void k_store_u64(uint64_t *dst, uint64_t v) { *dst = v; }
+__global__ void k_zero(uint8_t *__restrict__ dst, size_t n) {
+    const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+    const size_t al = (16 - ((uintptr_t)dst & 15)) & 15, head = al < n ? al : n;
+    for (size_t i = tid; i < head; i += nt) dst[i] = 0;
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst + head);
+    const size_t n4 = (n - head) / 16;
+    for (size_t i = tid; i < n4; i += nt) d4[i] = uint4{0, 0, 0, 0};
+    for (size_t i = head + n4 * 16 + tid; i < n; i += nt) dst[i] = 0;
+}
+}  // namespace
+
+void small_copy(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    if (!bytes) return;
+    if (bytes > (1u << 20) || classify(dst) == MemKind::Host || classify(src) == MemKind::Host) {
+        CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+        return;
+    }
+    const unsigned grid = (unsigned)std::min<size_t>(64, (bytes / 8 + 255) / 256 + 1);
+    k_small_copy<<<grid, 256, 0, s>>>((uint8_t *)dst, (const uint8_t *)src, bytes);
+    LAUNCH_CHECK();
+}
+
+void zero_async(void *dst, size_t bytes, cudaStream_t s) {
+    if (!bytes) return;
+    const unsigned grid = (unsigned)std::min<size_t>(148 * 8, (bytes / 16 + 255) / 256 + 1);
+    k_zero<<<grid, 256, 0, s>>>((uint8_t *)dst, bytes);
+    LAUNCH_CHECK();
+}
+
+void store_u64(void *dst, uint64_t v, cudaStream_t s) {
+    k_store_u64<<<1, 1, 0, s>>>((uint64_t *)dst, v);
+    LAUNCH_CHECK();
+}
+
 void copy_to_device(hpdr_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t s) {
     (void)ctx;
     if (!bytes) return;

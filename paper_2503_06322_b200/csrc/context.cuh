@@ -126,5 +126,14 @@ namespace hpdr {
 enum class MemKind { Host, Pinned, Device };
 MemKind classify(const void *p);
 void copy_to_device(hpdr_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t s);
+// Stream-ordered small copy (<= 1 MB) done by an SM instead of a copy engine, between device memory
+// and/or pinned host memory (UVA): it does not queue behind bulk H2D / D2H transfers in flight on the
+// copy engines (the pipeline's chunk copies), which would otherwise delay every host readback of a
+// histogram or flag by up to a whole chunk transfer.  Pageable or large copies use cudaMemcpyAsync.
+void small_copy(void *dst, const void *src, size_t bytes, cudaStream_t s);
+// cudaMemsetAsync(dst, 0, bytes) as a kernel (same reason as small_copy; any size, 16-byte stores).
+void zero_async(void *dst, size_t bytes, cudaStream_t s);
+// Store one 8-byte value to device memory in stream order (a kernel parameter, no staging copy).
+void store_u64(void *dst, uint64_t v, cudaStream_t s);
 void copy_from_device(hpdr_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t s);
 }  // namespace hpdr

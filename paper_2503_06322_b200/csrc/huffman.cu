@@ -206,15 +206,20 @@ void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict
     uint32_t *d_code = (uint32_t *)ctx->dbuf("enc_code", (size_t)dict_size * 4 + 16);
     uint64_t *ubits = (uint64_t *)ctx->dbuf("enc_ubits", (units + 1) * 8);
     uint64_t *uoff = (uint64_t *)ctx->dbuf(ctx->oname("enc_uoff"), (units + 1) * 8);
-    CUDA_CHECK(cudaMemcpyAsync(d_len, lengths, dict_size, cudaMemcpyHostToDevice, s));
-    CUDA_CHECK(cudaMemcpyAsync(d_code, codes, (size_t)dict_size * 4, cudaMemcpyHostToDevice, s));
+    {   // the codebook through pinned staging + an SM copy (see small_copy)
+        uint8_t *ht = (uint8_t *)ctx->hbuf("enc_tabs_h", (size_t)dict_size * 5 + 16);
+        memcpy(ht, codes, (size_t)dict_size * 4);
+        memcpy(ht + (size_t)dict_size * 4, lengths, dict_size);
+        small_copy(d_code, ht, (size_t)dict_size * 4, s);
+        small_copy(d_len, ht + (size_t)dict_size * 4, dict_size, s);
+    }
     {
         KPROF("k_unit_bits", 4.0 * n + 8.0 * units, s);
         k_unit_bits<<<(unsigned)std::min<int64_t>(units, 148 * 16), kEncThreads, 0, s>>>(keys, n, d_len, dict_size, ubits,
                                                                                           units);
         LAUNCH_CHECK();
     }
-    CUDA_CHECK(cudaMemsetAsync(ubits + units, 0, 8, s));
+    zero_async(ubits + units, 8, s);
     size_t tb = 0;
     CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, ubits, uoff, (int)(units + 1), s));
     void *tmp = ctx->dbuf("cub_tmp", tb);
@@ -225,14 +230,14 @@ void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict
     std::vector<int64_t> ub(G + 1);
     for (int g = 0; g <= G; g++) ub[g] = units * g / G;
     uint64_t *h = (uint64_t *)ctx->hbuf("enc_total", 8 * (G + 2));
-    for (int g = 0; g <= G; g++) CUDA_CHECK(cudaMemcpyAsync(h + g, uoff + ub[g], 8, cudaMemcpyDeviceToHost, s));
+    for (int g = 0; g <= G; g++) small_copy(h + g, uoff + ub[g], 8, s);
     CUDA_CHECK(cudaStreamSynchronize(s));
     res.total_bits = h[G];
     std::vector<uint64_t> gbit(h, h + G + 1);
     const size_t words = (size_t)((res.total_bits + 31) / 32) + 2;
     res.d_words = (uint32_t *)ctx->dbuf(ctx->oname("enc_words"), words * 4);
     res.d_offsets = uoff;
-    CUDA_CHECK(cudaMemsetAsync(res.d_words, 0, words * 4, s));
+    zero_async(res.d_words, words * 4, s);
     if (hooks && hooks->ready) hooks->ready(res);
     const uint64_t pbytes = (res.total_bits + 7) / 8;
     for (int g = 0; g < G; g++) {
@@ -630,7 +635,7 @@ void decode_begin(hpdr_ctx *ctx, const DecodeJob &job, DecodeSession &S, cudaStr
     }
     const size_t tab_bytes = sizeof(DecTables) + kLutSize * 4 + (present.size() + 1) * 4;
     char *d_tab = (char *)ctx->dbuf("dec_tabs", tab_bytes);
-    CUDA_CHECK(cudaMemcpyAsync(d_tab, T, tab_bytes, cudaMemcpyHostToDevice, s));
+    small_copy(d_tab, T, tab_bytes, s);
 
     S.job = job;
     S.max_len = max_len;
@@ -638,19 +643,19 @@ void decode_begin(hpdr_ctx *ctx, const DecodeJob &job, DecodeSession &S, cudaStr
     S.units = (int64_t)job.n_units;
     const int64_t units = S.units;
     S.d_off = (uint64_t *)ctx->dbuf("dec_off", (units + 1) * 8);
-    CUDA_CHECK(cudaMemcpyAsync(S.d_off, job.offsets, units * 8, cudaMemcpyHostToDevice, s));
+    small_copy(S.d_off, job.offsets, units * 8, s);
     S.pbytes = (size_t)((job.total_bits + 7) / 8);
     S.pwords = ((S.pbytes / 4 + 12) & ~size_t(3));   // zero-padded tail words
     S.d_words = (uint32_t *)ctx->dbuf("dec_words", S.pwords * 4);
-    CUDA_CHECK(cudaMemsetAsync((char *)S.d_words + (S.pbytes & ~size_t(3)), 0, S.pwords * 4 - (S.pbytes & ~size_t(3)), s));
+    zero_async((char *)S.d_words + (S.pbytes & ~size_t(3)), S.pwords * 4 - (S.pbytes & ~size_t(3)), s);
     S.uerr = (long long *)ctx->dbuf("dec_err", (units + 1) * 8);
     S.flag = (unsigned long long *)ctx->dbuf("dec_flag", 32);
     S.deferred = (int *)ctx->dbuf("dec_defer", (units + 1) * 4);
-    CUDA_CHECK(cudaMemsetAsync(S.deferred, 0, (units + 1) * 4, s));
+    zero_async(S.deferred, (units + 1) * 4, s);
     unsigned long long init[4] = {~0ULL, 0ULL, 0ULL, 0ULL};
     unsigned long long *hinit = (unsigned long long *)ctx->hbuf("dec_init", 64);
     memcpy(hinit, init, 32);
-    CUDA_CHECK(cudaMemcpyAsync(S.flag, hinit, 32, cudaMemcpyHostToDevice, s));
+    small_copy(S.flag, hinit, 32, s);
     static bool attr = false;
     if (!attr) {
         CUDA_CHECK(cudaFuncSetAttribute(k_decode_warp<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -680,7 +685,7 @@ void decode_begin(hpdr_ctx *ctx, const DecodeJob &job, DecodeSession &S, cudaStr
     S.stats = nullptr;
     if (want_stats) {
         S.stats = (unsigned long long *)ctx->dbuf("dec_stats", 32);
-        CUDA_CHECK(cudaMemsetAsync(S.stats, 0, 32, s));
+        zero_async(S.stats, 32, s);
     }
     if (copy_payload && units > 0)
         CUDA_CHECK(cudaMemcpyAsync(S.d_words, job.packed, S.pbytes, cudaMemcpyDefault, s));
@@ -710,8 +715,8 @@ void decode_units(const DecodeSession &S, int64_t u_lo, int64_t u_hi, bool strea
 void decode_end(hpdr_ctx *ctx, const DecodeSession &S, DecodeResult &res, cudaStream_t s, bool streamed) {
     if (streamed) decode_units(S, 0, S.units, false, s, 1);   // deferred units, now with every byte present
     unsigned long long *h = (unsigned long long *)ctx->hbuf("dec_rb", 64);
-    CUDA_CHECK(cudaMemcpyAsync(h, S.flag, 24, cudaMemcpyDeviceToHost, s));
-    if (S.stats) CUDA_CHECK(cudaMemcpyAsync(h + 4, S.stats, 16, cudaMemcpyDeviceToHost, s));
+    small_copy(h, S.flag, 24, s);
+    if (S.stats) small_copy(h + 4, S.stats, 16, s);
     CUDA_CHECK(cudaStreamSynchronize(s));
     if (S.stats) fprintf(stderr, "[decode] units %lld fallback %llu rounds %llu deferred %llu\n", (long long)S.units, h[4],
                          h[5], h[2]);

@@ -479,7 +479,10 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
             if (x != ctx) CUDA_CHECK(cudaStreamWaitEvent(x->stream, ctx->event(0), 0));
             CUDA_CHECK(cudaStreamWaitEvent(x->h2d, ctx->event(0), 0));
             CUDA_CHECK(cudaStreamWaitEvent(x->d2h, ctx->event(0), 0));
-            uint8_t *dblob = (uint8_t *)x->dbuf("pipe_blob", maxpay);
+            // two blob buffers: chunk k+Q's H2D overlaps chunk k's recomposition (the blob is read by
+            // its decode and outlier scatter only)
+            uint8_t *dblobs[2] = {(uint8_t *)x->dbuf("pipe_blob", maxpay), (uint8_t *)x->dbuf("pipe_blob#1", maxpay)};
+            cudaEvent_t ev_reds[2] = {x->event(304), x->event(305)};
             char *douts[2] = {host_out ? (char *)x->dbuf("pipe_out0", maxraw * isz) : nullptr,
                               host_out ? (char *)x->dbuf("pipe_out1", maxraw * isz) : nullptr};
             cudaEvent_t ev_in = x->event(300), ev_red = x->event(301), ev_outs[2] = {x->event(302), x->event(303)};
@@ -489,7 +492,8 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
                 if (R.failed) return;
                 char *dout = douts[t & 1];
                 cudaEvent_t ev_out = ev_outs[t & 1];
-                if (!first) CUDA_CHECK(cudaStreamWaitEvent(x->h2d, ev_red, 0));   // blob buffer reuse edge
+                uint8_t *dblob = dblobs[t & 1];
+                if (t >= 2) CUDA_CHECK(cudaStreamWaitEvent(x->h2d, ev_reds[t & 1], 0));   // blob buffer reuse edge
                 tm.mark(6 * k, x->h2d);
                 CUDA_CHECK(cudaMemcpyAsync(dblob, c + base + chunks[k].pay_off, chunks[k].pay_size,
                                            cudaMemcpyHostToDevice, x->h2d));
@@ -503,6 +507,7 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
                                 chunks[k].raw_size * isz, false);
                 tm.mark(6 * k + 3, x->stream);
                 CUDA_CHECK(cudaEventRecord(ev_red, x->stream));
+                CUDA_CHECK(cudaEventRecord(ev_reds[t & 1], x->stream));
                 CUDA_CHECK(cudaStreamWaitEvent(x->d2h, ev_red, 0));
                 tm.mark(6 * k + 4, x->d2h);
                 if (host_out)

@@ -187,8 +187,8 @@ void quantize_device(hpdr_ctx *ctx, const double *coef, int64_t n, const std::ve
     int *flags = (int *)ctx->dbuf("qflags", 16);
     unsigned long long *ccount = (unsigned long long *)ctx->dbuf("ochunk", (chunks + 1) * 8);
     unsigned long long *coff = (unsigned long long *)ctx->dbuf("ochunk_off", (chunks + 1) * 8);
-    CUDA_CHECK(cudaMemsetAsync(hist, 0, (size_t)dict_size * 8, s));
-    CUDA_CHECK(cudaMemsetAsync(flags, 0, 16, s));
+    zero_async(hist, (size_t)dict_size * 8, s);
+    zero_async(flags, 16, s);
     Coarsest co;
     co.n = (int)coarsest.size();
     for (int k = 0; k < 16; k++) co.idx[k] = k < co.n ? coarsest[k] : -1;
@@ -221,13 +221,13 @@ void quantize_finish(hpdr_ctx *ctx, int64_t n, uint32_t dict_size, double bin_wi
     size_t tmp_bytes = 0;
     CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, ccount, coff, (int)(chunks + 1), s));
     void *tmp = ctx->dbuf("cub_tmp", tmp_bytes);
-    CUDA_CHECK(cudaMemsetAsync(ccount + chunks, 0, 8, s));
+    zero_async(ccount + chunks, 8, s);
     CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, ccount, coff, (int)(chunks + 1), s));
     count_launch();
     uint64_t *h = (uint64_t *)ctx->hbuf("q_readback", (size_t)dict_size * 8 + 64);
-    CUDA_CHECK(cudaMemcpyAsync(h, coff + chunks, 8, cudaMemcpyDeviceToHost, s));
-    CUDA_CHECK(cudaMemcpyAsync(h + 1, flags, 4, cudaMemcpyDeviceToHost, s));
-    CUDA_CHECK(cudaMemcpyAsync(h + 2, hist, (size_t)dict_size * 8, cudaMemcpyDeviceToHost, s));
+    small_copy(h, coff + chunks, 8, s);
+    small_copy(h + 1, flags, 4, s);
+    small_copy(h + 2, hist, (size_t)dict_size * 8, s);
     CUDA_CHECK(cudaStreamSynchronize(s));
     res.n_outliers = h[0];
     int fl;
@@ -249,8 +249,8 @@ void histogram_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t d
                       bool *bad, cudaStream_t s) {
     unsigned long long *d = (unsigned long long *)ctx->dbuf("hist", (size_t)dict_size * 8);
     int *flags = (int *)ctx->dbuf("qflags", 16);
-    CUDA_CHECK(cudaMemsetAsync(d, 0, (size_t)dict_size * 8, s));
-    CUDA_CHECK(cudaMemsetAsync(flags, 0, 16, s));
+    zero_async(d, (size_t)dict_size * 8, s);
+    zero_async(flags, 16, s);
     size_t smem = dict_size <= kSmemHistMax ? (size_t)dict_size * 4 : 0;
     if (smem > 48 * 1024) CUDA_CHECK(cudaFuncSetAttribute(k_histogram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (n > 0) {
@@ -259,8 +259,8 @@ void histogram_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t d
         LAUNCH_CHECK();
     }
     uint64_t *h = (uint64_t *)ctx->hbuf("q_readback", (size_t)dict_size * 8 + 64);
-    CUDA_CHECK(cudaMemcpyAsync(h, flags, 4, cudaMemcpyDeviceToHost, s));
-    CUDA_CHECK(cudaMemcpyAsync(h + 1, d, (size_t)dict_size * 8, cudaMemcpyDeviceToHost, s));
+    small_copy(h, flags, 4, s);
+    small_copy(h + 1, d, (size_t)dict_size * 8, s);
     CUDA_CHECK(cudaStreamSynchronize(s));
     int fl;
     memcpy(&fl, h, 4);

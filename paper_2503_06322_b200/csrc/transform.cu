@@ -823,14 +823,15 @@ LevelBuffers level_buffers(hpdr_ctx *ctx, DevPlan &p) {
 void minmax_device(hpdr_ctx *ctx, const void *d_in, int dtype, int64_t n, double *vmin, double *vmax, cudaStream_t s) {
     unsigned long long *d = (unsigned long long *)ctx->dbuf("minmax", 32);
     unsigned long long *h = (unsigned long long *)ctx->hbuf("minmax_h", 32);
-    unsigned long long init[3] = {~0ULL, 0ULL, 0ULL};
-    CUDA_CHECK(cudaMemcpyAsync(d, init, 24, cudaMemcpyHostToDevice, s));
+    store_u64(d, ~0ULL, s);
+    store_u64(d + 1, 0ULL, s);
+    store_u64(d + 2, 0ULL, s);
     {
         KPROF("k_minmax", (double)n * (dtype == 0 ? 4 : 8), s);
         k_minmax<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(d_in, dtype, n, d);
         LAUNCH_CHECK();
     }
-    CUDA_CHECK(cudaMemcpyAsync(h, d, 24, cudaMemcpyDeviceToHost, s));
+    small_copy(h, d, 24, s);
     CUDA_CHECK(cudaStreamSynchronize(s));
     if (h[2]) {
         *vmin = __builtin_nan("");
@@ -952,7 +953,9 @@ const double *coarse_levels_quantize(hpdr_ctx *ctx, DevPlan &p, const QuantOut &
     for (auto &e : p.graphs)
         if (e.key == key) g = &e;
     const double binv = q.bin;
-    CUDA_CHECK(cudaMemcpyAsync(bin_dev, &binv, 8, cudaMemcpyHostToDevice, s));   // staged: safe to return
+    uint64_t binbits;
+    memcpy(&binbits, &binv, 8);
+    store_u64(bin_dev, binbits, s);
     if (!g) {
         QuantOut qg = q;
         qg.bin_dev = bin_dev;
@@ -1011,10 +1014,10 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
         q.bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
     } else {
         unsigned long long *h = (unsigned long long *)ctx->hbuf("minmax_h", 32);
-        h[0] = ~0ULL;
-        h[1] = 0ULL;
-        h[2] = 0ULL;
-        CUDA_CHECK(cudaMemcpyAsync(mm, h, 24, cudaMemcpyHostToDevice, s));
+        (void)h;
+        store_u64(mm, ~0ULL, s);
+        store_u64(mm + 1, 0ULL, s);
+        store_u64(mm + 2, 0ULL, s);
     }
     // coarse outputs of transition 0 whose 5-plane stencil lies within the first `arrived` planes
     const AxisTables &ax0 = p.host.steps[0].ax[1];
@@ -1062,7 +1065,7 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
         *u_max = range_max;
     } else {
         unsigned long long *h = (unsigned long long *)ctx->hbuf("minmax_h", 32);
-        CUDA_CHECK(cudaMemcpyAsync(h, mm, 24, cudaMemcpyDeviceToHost, s));
+        small_copy(h, mm, 24, s);
         CUDA_CHECK(cudaStreamSynchronize(s));
         auto val = [](unsigned long long k) {
             unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k;

@@ -806,7 +806,7 @@ int hpdr_zfp_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, const 
         uint32_t *pay = (uint32_t *)ctx->dbuf("zfp_pay", z.payload + 8);
         unsigned *bad = (unsigned *)ctx->dbuf("zfp_bad", 16);
         unsigned *bad_h = (unsigned *)ctx->hbuf("zfp_bad_h", 16);
-        CUDA_CHECK(cudaMemsetAsync(bad, 0, 4, s));
+        zero_async(bad, 4, s);
         const void *din = in;
         const std::vector<int64_t> cut = zfp_slabs(z, in_dev ? 1 : zfp_slab_count(z, n * isz));
         const int K = (int)cut.size() - 1;
@@ -973,7 +973,7 @@ int hpdr_pipeline_zfp_compress(hpdr_ctx *ctx, const void *host_in, int dtype, in
         else memcpy(o, head.data(), head.size());
         unsigned *bad = (unsigned *)ctx->dbuf("zfp_bad", 16);
         unsigned *bad_h = (unsigned *)ctx->hbuf("zfp_bad_h", 16);
-        CUDA_CHECK(cudaMemsetAsync(bad, 0, 4, s));
+        zero_async(bad, 4, s);
         void *din[2] = {in_dev ? nullptr : ctx->dbuf("zfp_pin0", max_in), in_dev ? nullptr : ctx->dbuf("zfp_pin1", max_in)};
         uint32_t *dp[2] = {(uint32_t *)ctx->dbuf("zfp_ppay0", max_pay + 8), (uint32_t *)ctx->dbuf("zfp_ppay1", max_pay + 8)};
         std::unique_ptr<ZTimer> tm(trace ? new ZTimer(6 * K) : nullptr);
