@@ -27,24 +27,6 @@ __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double lerp(double va, double vb, double t) { return dadd(va, dmul(t, dsub(vb, va))); }
 
 
-// b = rint(mc / bin) (quantize.py:73-76: IEEE division, half to even) with one multiply by
-// rb = RN(1/bin): the correctly rounded quotient q and qa = RN(mc * rb) differ by < |q| 2^-51, so
-// rint(qa) == rint(q) unless qa lies within that distance of a half-integer -- then (and for
-// |qa| >= 2^61) the IEEE division decides.  Returns false when |mc / bin| >= 2^62 (bin overflow).
-__device__ __forceinline__ bool quant_bin(double mc, double bin, double rb, long long &b) {
-    const double qa = dmul(mc, rb);
-    const double r = rint(qa);
-    const double dist = 0.5 - fabs(dsub(qa, r));
-    if (dist > fabs(qa) * 0x1p-49 && fabs(qa) < 0x1p61) {
-        b = (long long)r;
-        return true;
-    }
-    const double sc = mc / bin;
-    if (fabs(sc) >= 4611686018427387904.0) return false;
-    b = (long long)rint(sc);
-    return true;
-}
-
 // Histogram count of `key` (shared-memory bins flushed once per block).
 // (__match_any_sync aggregation measured slower here: 2.67 vs 1.73 ms for the level-0 pass)
 __device__ __forceinline__ void hist_add(uint32_t *sh, unsigned long long *g, bool sh_ok, uint32_t key) {
@@ -52,11 +34,15 @@ __device__ __forceinline__ void hist_add(uint32_t *sh, unsigned long long *g, bo
     else atomicAdd(&g[key], 1ULL);
 }
 
-// One fine node's quantization (quantize.py:73-84), in the double domain: r = rint(c / bin) as an
-// integral double (quant_bin's verified reciprocal product, IEEE division in the rare tie band),
-// outlier iff |r| >= dict/2, key = zigzag(r) (exact: non-outlier |r| < 2^15), histogram.
+// The bin width: a launch parameter, or read from device memory (CUDA-graph replays).
 __device__ __forceinline__ double qbin(const QuantOut &q) { return q.bin_dev ? *q.bin_dev : q.bin; }
 
+// One fine node's quantization (quantize.py:73-84), in the double domain.  r = rint(mc / bin)
+// (IEEE division, half to even) is computed with one multiply by rb = RN(1/bin): the correctly
+// rounded quotient q and qa = RN(mc * rb) differ by < |q| 2^-51, so rint(qa) == rint(q) unless qa
+// lies within that distance of a half-integer -- then (and for |qa| >= 2^61) the IEEE division
+// decides; |mc / bin| >= 2^62 is the bin overflow.  Outlier iff |r| >= dict/2, key = zigzag(r)
+// (exact: non-outlier |r| < 2^15), histogram.
 __device__ __forceinline__ void quant_node(double mc, const QuantOut &q, double rbin, int64_t f, int &fl,
                                            uint32_t *sh_hist, bool sh_ok) {
     double r = 0.0;
@@ -184,17 +170,6 @@ __device__ __forceinline__ void march_push(March &M, const PlaneInfo *__restrict
     M.m1 = x;
 }
 
-__device__ __forceinline__ PlaneInfo load_pi(const PlaneInfo *__restrict__ p) {
-    PlaneInfo r;
-    const double2 *q = reinterpret_cast<const double2 *>(p);   // 80 bytes = 5 x 16 B
-#pragma unroll
-    for (int k = 0; k < 5; k++) {
-        const double2 v = __ldg(q + k);
-        memcpy((char *)&r + 16 * k, &v, 16);
-    }
-    return r;
-}
-
 // The interpolation part of a PlaneInfo record (what pass 1 needs per plane).
 struct PiHead {
     int fa, fb, ca, fo;
@@ -219,16 +194,6 @@ __device__ __forceinline__ PiHead identity_head(int j) {
     h.fo = 0;
     h.t = 0.0;
     return h;
-}
-
-__device__ __forceinline__ PlaneInfo identity_pi(int j) {
-    PlaneInfo r;
-    r.fa = r.fb = r.ca = r.cb = j;
-    r.t = r.md = r.ml = r.mu = r.ewr = r.ewl = 0.0;
-    r.fo = 0;
-    r.emit = -1;
-    r.e_rr = r.e_rl = 0;
-    return r;
 }
 
 __device__ __forceinline__ void slab_range(int nc, int nz, int z, int &lo, int &hi) {

@@ -486,7 +486,6 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
             char *douts[2] = {host_out ? (char *)x->dbuf("pipe_out0", maxraw * isz) : nullptr,
                               host_out ? (char *)x->dbuf("pipe_out1", maxraw * isz) : nullptr};
             cudaEvent_t ev_in = x->event(300), ev_red = x->event(301), ev_outs[2] = {x->event(302), x->event(303)};
-            bool first = true;
             uint64_t t = 0;
             for (uint64_t k = q; k < K; k += Q, t++) {
                 if (R.failed) return;
@@ -515,7 +514,6 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
                                                cudaMemcpyDeviceToHost, x->d2h));
                 tm.mark(6 * k + 5, x->d2h);
                 CUDA_CHECK(cudaEventRecord(ev_out, x->d2h));
-                first = false;
             }
             CUDA_CHECK(cudaStreamSynchronize(x->d2h));
             CUDA_CHECK(cudaStreamSynchronize(x->stream));

@@ -18,10 +18,6 @@ struct Coarsest {
     int n;
 };
 
-__device__ __forceinline__ uint32_t zigzag32(long long b) {
-    return (uint32_t)(((unsigned long long)b << 1) ^ (unsigned long long)(b >> 63));
-}
-
 // Warp-aggregated increment: lanes with equal keys add once (key 0 dominates real data).
 __device__ __forceinline__ void hist_add(uint32_t *sh, unsigned long long *g, bool use_sh, uint32_t key, unsigned mask) {
     unsigned peers = __match_any_sync(mask, key);
@@ -62,7 +58,7 @@ __global__ void __launch_bounds__(kQThreads) k_quantize(const double *__restrict
             if (wbase >= n) break;
             const int64_t i = wbase + lane;
             const bool valid = i < n;
-            // b = rint(c / bin) as an integral double (quantize.py:73-76; exact, see fused.cu quant_bin)
+            // b = rint(c / bin) as an integral double (quantize.py:73-76; exact, see fused.cu quant_node)
             double r = 0.0;
             if (valid) {
                 if (!isfinite(v[u])) {

@@ -32,13 +32,10 @@ __global__ void k_to_f64(const void *__restrict__ in, int dtype, double *__restr
     }
 }
 
+// Order-preserving integer key of a double (-0 < +0; NaNs are tracked separately).
 __device__ __forceinline__ unsigned long long ord_key(double v) {
     unsigned long long u = (unsigned long long)__double_as_longlong(v);
     return (u >> 63) ? ~u : (u | 0x8000000000000000ULL);
-}
-__device__ __forceinline__ double ord_val(unsigned long long k) {
-    unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k;
-    return __longlong_as_double((long long)u);
 }
 
 __global__ void k_minmax(const void *__restrict__ in, int dtype, int64_t n, unsigned long long *res) {
@@ -287,13 +284,6 @@ __device__ __forceinline__ double div_fast(double a, double b, double r, bool &b
     return q1;
 }
 
-// div_fast with the exact fallback inline (for in-place sweeps that cannot redo a line)
-__device__ __forceinline__ double div_checked(double a, double b, double r) {
-    bool bad = false;
-    const double q = div_fast(a, b, r, bad);
-    return bad ? ddiv(a, b) : q;
-}
-
 // ---------------------------------------------------------------- IPK: batched Thomas solves
 // Strided axis: one thread per line, threads along the contiguous inner index (coalesced).
 __global__ void k_thomas_strided(double *__restrict__ arr, int64_t outer, int32_t n, int64_t inner,
@@ -420,7 +410,7 @@ __global__ void __launch_bounds__(128) k_thomas_reg(double *__restrict__ arr, in
 #pragma unroll
             for (int k = 0; k < U; k++) cur[k] = nxt[k];
         }
-        double last = ddiv(prev, __ldg(tb + n - 1));   // (__ddiv_rn beat div_checked here)
+        double last = ddiv(prev, __ldg(tb + n - 1));   // (__ddiv_rn beat a checked fast division here)
         x[(int64_t)(n - 1) * inner] = last;
         // back substitution: x_i = (x_i - u_i x_{i+1}) / b'_i, i = n-2 .. 0
         load(cur, n - 1 - U);
@@ -1013,8 +1003,6 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
         const double eb_abs = eb_rel * (range_max - range_min);
         q.bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
     } else {
-        unsigned long long *h = (unsigned long long *)ctx->hbuf("minmax_h", 32);
-        (void)h;
         store_u64(mm, ~0ULL, s);
         store_u64(mm + 1, 0ULL, s);
         store_u64(mm + 2, 0ULL, s);
