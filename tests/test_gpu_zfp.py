@@ -168,3 +168,33 @@ def test_pipeline_container_matches_per_slab_streams(oracle, dims, dtype, rate, 
     dout = torch.empty(dims, dtype=dev.dtype, device="cuda")
     PL.decompress_pipelined(data, out=dout)
     assert np.array_equal(dout.cpu().numpy().view(np.uint8), ref.view(np.uint8))
+
+
+def test_pipeline_container_errors():
+    """Fixed-rate container: a non-finite chunk raises ValidationError; a corrupted header (CRC) or a
+    truncated container raise FormatError; a chunk stream that fails its own checks raises the
+    reducer's error."""
+    from paper_2503_06322_b200 import pipeline as PL
+    from paper_2503_06322_b200.errors import FormatError
+
+    a = (np.random.default_rng(3).random((40, 33, 17)) * 2 - 1).astype(np.float32)
+    bad = a.copy()
+    bad[37, 5, 5] = np.inf
+    with pytest.raises(ValidationError):
+        Z.compress_pipelined(bad, 12, chunk_planes=8)
+    data = Z.compress_pipelined(a, 12, chunk_planes=8)
+    hdr = bytearray(data)
+    hdr[10] ^= 0x40   # inside the dims: CRC mismatch
+    with pytest.raises(FormatError):
+        PL.decompress_pipelined(bytes(hdr))
+    with pytest.raises(FormatError):
+        PL.decompress_pipelined(data[: len(data) - 5])
+    from paper_2503_06322_b200.container import read_container
+
+    h, pays = read_container(data)
+    # a chunk stream whose own header disagrees with the container (rate byte of chunk 0)
+    off = len(data) - sum(c.payload_size for c in h.chunks) + h.chunks[0].payload_offset
+    mut = bytearray(data)
+    mut[off + 2] = 13   # the chunk's own checks (zfp.py:333-334) or the container's consistency check
+    with pytest.raises((FormatError, CorruptStreamError)):
+        PL.decompress_pipelined(bytes(mut))
