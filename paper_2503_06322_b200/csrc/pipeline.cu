@@ -249,7 +249,19 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
         const int Q = pipe_queues(K);
         std::vector<hpdr_ctx *> qc(Q);
         for (int q = 0; q < Q; q++) qc[q] = ctx->queue(q);
+        // relative mode: phase B (quantize + code + copy out, once the range is known) runs on QB
+        // contexts of its own (streams, buffers), so chunk k's phase B is not queued behind the
+        // phase-A decompositions of later chunks.  QB = Q threads by default (measured: 3 / 6 / 9 phase-B
+        // threads -> 13.3 / 13.6 / 14.3 ms at 513^3); HPDR_PIPE_QUEUES_B (>= Q) overrides.
+        static const int qb_env = [] {
+            const char *e = getenv("HPDR_PIPE_QUEUES_B");
+            return e ? std::max(1, atoi(e)) : 0;
+        }();
+        const int QB = two_phase ? (int)std::min<uint64_t>(K, (uint64_t)(qb_env ? std::max(qb_env, Q) : Q)) : Q;
+        std::vector<hpdr_ctx *> qb(QB);
+        for (int q = 0; q < QB; q++) qb[q] = two_phase ? ctx->queue(Q + q) : qc[q];
         for (hpdr_ctx *x : qc) x->graphs_ok = false;   // several host threads on one device
+        for (hpdr_ctx *x : qb) x->graphs_ok = false;
         struct GraphsBack {
             hpdr_ctx *c;
             ~GraphsBack() { c->graphs_ok = true; }
@@ -302,6 +314,7 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
                 for (int d = 1; d < rank; d++) sd[d] = dims[d];
                 decompose_chunk(c, din, dtype, rank, sd, coef_all + chunks[k].raw_off, nullptr);
                 CUDA_CHECK(cudaEventRecord(ev_red, c->stream));
+                CUDA_CHECK(cudaEventRecord(c->event(320 + k), c->stream));   // chunk k's coefficients
                 first = false;
             }
             CUDA_CHECK(cudaMemcpyAsync(hmm, mm, 24, cudaMemcpyDeviceToHost, c->h2d));
@@ -314,34 +327,45 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
                 minmax_from_keys(gkey, &vmin, &vmax);
                 rcv.notify_all();
             } else {
-                rcv.wait(lk, [&] { return reported == Q || RR.failed; });
+                rcv.wait(lk, [&] { return reported >= Q || RR.failed; });
             }
             return !RR.failed;
         };
-        const int QB = Q;
+        const int QA = Q;   // phase-A threads (relative mode); every thread runs phase B
         QueueRun R;
-        R.run(QB, [&](int q) {
+        R.run(std::max(QA, QB), [&](int q) {
+            if (q >= QB) {   // phase A only (cannot happen: QB >= QA)
+                if (two_phase) phase_a(q, R);
+                return;
+            }
             const int Q = QB;
-            hpdr_ctx *c = qc[q];
-            CUDA_CHECK(cudaSetDevice(c->device));
+            hpdr_ctx *c = q < QA ? qc[q] : nullptr;
+            CUDA_CHECK(cudaSetDevice(ctx->device));
             if (two_phase) {
                 try {
-                    if (!phase_a(q, R)) return;
+                    if (q < QA) {
+                        if (!phase_a(q, R)) return;
+                    } else {   // phase-B-only thread: wait for the range
+                        std::unique_lock<std::mutex> lk(rmu);
+                        rcv.wait(lk, [&] { return reported >= QA || R.failed; });
+                        if (R.failed) return;
+                    }
                 } catch (...) {
                     {
                         std::lock_guard<std::mutex> g(rmu);
-                        reported = Q;   // release the others; R.fail() marks the run failed
+                        reported = std::max(reported, QA);   // release the others; R.fail() marks the run failed
                     }
                     rcv.notify_all();
                     throw;
                 }
+                c = qb[q];
             }
             if (c != ctx) {
                 CUDA_CHECK(cudaStreamWaitEvent(c->stream, ctx->event(0), 0));
             }
             CUDA_CHECK(cudaStreamWaitEvent(c->h2d, ctx->event(0), 0));
             CUDA_CHECK(cudaStreamWaitEvent(c->d2h, ctx->event(0), 0));
-            char *din = (char *)c->dbuf("pipe_in", cbytes);
+            char *din = two_phase ? nullptr : (char *)c->dbuf("pipe_in", cbytes);
             // event ids 300-303 are reserved for the runner; the output buffer sets alternate
             cudaEvent_t ev_in = c->event(300), ev_red = c->event(301), ev_outs[2] = {c->event(302), c->event(303)};
             bool first = true;
@@ -360,6 +384,8 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
                     CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_in, 0));
                 }
                 if (t >= 2) CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_out, 0));   // output set reuse edge (k - 2Q)
+                if (two_phase)   // chunk k decomposed by phase-A queue k mod QA
+                    CUDA_CHECK(cudaStreamWaitEvent(c->stream, qc[k % QA]->event(320 + k), 0));
                 if (!two_phase) tm.mark(6 * k + 2, c->stream);
                 uint64_t sd[4] = {chunks[k].raw_size / plane, 0, 0, 0};
                 for (int d = 1; d < rank; d++) sd[d] = dims[d];
