@@ -5,7 +5,7 @@ The report file name is the bench's kernel label (pass1q.ncu-rep -> k_level_pass
 """
 import csv, io, json, os, subprocess, sys
 
-LABELS = {"pass1q": "k_level_pass1q", "pass1r": "k_level_pass1r", "pass2": "k_level_pass2",
+LABELS = {"pass1q": "k_level_pass1q", "pass1r": "k_level_pass1r", "pass2": "k_level_pass2", "minmax": "k_minmax",
           "final": "k_level_final", "decode": "k_decode", "encode": "k_encode", "thomas": "k_thomas"}
 d = sys.argv[1]
 out = sys.argv[2] if len(sys.argv) > 2 else os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
