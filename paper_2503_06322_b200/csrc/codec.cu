@@ -72,9 +72,11 @@ struct Reader {
 
 // Device-resident input: copy host data to a context buffer when needed.
 const void *device_input(hpdr_ctx *ctx, const void *in, size_t bytes, const char *name, cudaStream_t s) {
-    if (classify(in) == MemKind::Device) return in;
+    const MemKind k = classify(in);
+    if (k == MemKind::Device) return in;
     void *d = ctx->dbuf(name, bytes);
-    CUDA_CHECK(cudaMemcpyAsync(d, in, bytes, cudaMemcpyDefault, s));
+    if (k == MemKind::Host) stage_h2d(ctx, d, in, bytes, s);   // pageable: pinned staging ring
+    else CUDA_CHECK(cudaMemcpyAsync(d, in, bytes, cudaMemcpyDefault, s));
     return d;
 }
 
@@ -133,7 +135,8 @@ uint64_t fetch_pending(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uin
                        bool payload) {
     if (!P.valid) fail(HPDR_ERR_VALIDATION, "no pending compressed stream in this context");
     if (cap < P.total_len) fail(HPDR_ERR_BUFFER, "output buffer too small: need " + std::to_string(P.total_len));
-    const bool dev = classify(out) == MemKind::Device;
+    const MemKind ok = classify(out);
+    const bool dev = ok == MemKind::Device;
     uint8_t *o = (uint8_t *)out;
     uint64_t pos = 0;
     auto host_bytes = [&](const void *src, size_t n) {
@@ -144,7 +147,8 @@ uint64_t fetch_pending(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uin
     };
     auto dev_bytes = [&](const void *src, size_t n) {
         if (!n) return;
-        CUDA_CHECK(cudaMemcpyAsync(o + pos, src, n, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+        if (ok == MemKind::Host && n >= (1u << 20)) stage_d2h(ctx, o + pos, src, n, s);   // pageable (Python bytes)
+        else CUDA_CHECK(cudaMemcpyAsync(o + pos, src, n, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
         pos += n;
     };
     if (!P.huffman_only) {
@@ -745,8 +749,13 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
             int64_t *db = (int64_t *)ctx->dbuf("dq_obins", n_out * 8);
             int *fl = (int *)ctx->dbuf("dq_flags", 16);
             if (n_out) {
-                CUDA_CHECK(cudaMemcpyAsync(di, blob + oidx_off, n_out * 8, cudaMemcpyDefault, s));
-                CUDA_CHECK(cudaMemcpyAsync(db, blob + obins_off, n_out * 8, cudaMemcpyDefault, s));
+                if (classify(blob) == MemKind::Host && n_out * 8 >= (1u << 20)) {
+                    stage_h2d(ctx, di, blob + oidx_off, n_out * 8, s);
+                    stage_h2d(ctx, db, blob + obins_off, n_out * 8, s);
+                } else {
+                    CUDA_CHECK(cudaMemcpyAsync(di, blob + oidx_off, n_out * 8, cudaMemcpyDefault, s));
+                    CUDA_CHECK(cudaMemcpyAsync(db, blob + obins_off, n_out * 8, cudaMemcpyDefault, s));
+                }
             }
             zero_async(fl, 16, s);
             const int64_t units = S.units;
@@ -783,6 +792,7 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
             }();
             CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
             CUDA_CHECK(cudaStreamWaitEvent(ctx->h2d, ctx->event(0), 0));   // tables / buffers ready
+            const bool pageable_blob = classify(hh.packed) == MemKind::Host;
             size_t copied = 0;
             int c_done = 0;
             for (int g = 0; g < G; g++) {
@@ -791,8 +801,11 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                 const size_t want = ub < units ? std::min<size_t>(S.pbytes, ((size_t)(uoffs[ub] / 8) + 64) & ~size_t(3))
                                                : S.pbytes;
                 if (want > copied) {
-                    CUDA_CHECK(cudaMemcpyAsync((char *)S.d_words + copied, hh.packed + copied, want - copied,
-                                               cudaMemcpyHostToDevice, ctx->h2d));
+                    if (pageable_blob)   // Python bytes: staged while the previous group decodes
+                        stage_h2d(ctx, (char *)S.d_words + copied, hh.packed + copied, want - copied, ctx->h2d);
+                    else
+                        CUDA_CHECK(cudaMemcpyAsync((char *)S.d_words + copied, hh.packed + copied, want - copied,
+                                                   cudaMemcpyHostToDevice, ctx->h2d));
                     copied = want;
                 }
                 CUDA_CHECK(cudaEventRecord(ctx->event(100 + g), ctx->h2d));

@@ -3,7 +3,12 @@
 
 #include <algorithm>
 #include <atomic>
+#include <sys/mman.h>
+
+#include <condition_variable>
 #include <mutex>
+#include <thread>
+#include <vector>
 
 #include "context.cuh"
 
@@ -151,6 +156,120 @@ void zero_async(void *dst, size_t bytes, cudaStream_t s) {
     const unsigned grid = (unsigned)std::min<size_t>(148 * 8, (bytes / 16 + 255) / 256 + 1);
     k_zero<<<grid, 256, 0, s>>>((uint8_t *)dst, bytes);
     LAUNCH_CHECK();
+}
+
+namespace {
+constexpr size_t kStageChunk = 16u << 20;
+constexpr unsigned kStageSlots = 4;
+int host_threads() {
+    static const int t = std::max(1, std::min(16, (int)std::thread::hardware_concurrency()));
+    return t;
+}
+}  // namespace
+
+namespace {
+// A persistent pool of memcpy workers (spawning threads per 16 MB slot costs more than the copy).
+struct CopyPool {
+    std::mutex mu;
+    std::condition_variable cv, done_cv;
+    std::vector<std::thread> th;
+    char *dst = nullptr;
+    const char *src = nullptr;
+    size_t n = 0, per = 0;
+    uint64_t gen = 0;
+    int pending = 0, workers = 0;
+    bool stop = false;
+    explicit CopyPool(int w) : workers(w) {
+        for (int i = 0; i < w; i++)
+            th.emplace_back([this, i] {
+                uint64_t seen = 0;
+                for (;;) {
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [&] { return stop || gen != seen; });
+                    if (stop) return;
+                    seen = gen;
+                    char *d = dst;
+                    const char *s = src;
+                    const size_t a = (size_t)(i + 1) * per, nn = n;
+                    lk.unlock();
+                    if (a < nn) memcpy(d + a, s + a, std::min(nn, a + per) - a);
+                    lk.lock();
+                    if (--pending == 0) done_cv.notify_one();
+                }
+            });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> g(mu);
+            stop = true;
+        }
+        cv.notify_all();
+        for (auto &t : th) t.join();
+    }
+    void copy(void *d, const void *s, size_t nn) {   // one caller at a time (guarded by call_mu)
+        std::lock_guard<std::mutex> call(call_mu);
+        const int T = workers + 1;
+        {
+            std::lock_guard<std::mutex> g(mu);
+            dst = (char *)d;
+            src = (const char *)s;
+            n = nn;
+            per = ((nn + T - 1) / T + 4095) & ~size_t(4095);
+            pending = workers;
+            gen++;
+        }
+        cv.notify_all();
+        memcpy(d, s, std::min(nn, per));   // slice 0 on the calling thread
+        std::unique_lock<std::mutex> lk(mu);
+        done_cv.wait(lk, [&] { return pending == 0; });
+    }
+    std::mutex call_mu;
+};
+}  // namespace
+
+void parallel_memcpy(void *dst, const void *src, size_t n) {
+    if (n < (4u << 20) || host_threads() == 1) {
+        memcpy(dst, src, n);
+        return;
+    }
+    static CopyPool *pool = new CopyPool(host_threads() - 1);   // intentionally leaked (process lifetime)
+    pool->copy(dst, src, n);
+}
+
+void stage_h2d(hpdr_ctx *ctx, void *dst, const void *src, size_t n, cudaStream_t st) {
+    char *ring = (char *)ctx->hbuf("stage_in", kStageChunk * kStageSlots);
+    for (size_t off = 0; off < n; off += kStageChunk) {
+        const unsigned slot = ctx->stage_next++ % kStageSlots;
+        cudaEvent_t ev = ctx->event(500 + slot);
+        CUDA_CHECK(cudaEventSynchronize(ev));   // the slot's previous DMA has read it
+        const size_t m = std::min(kStageChunk, n - off);
+        parallel_memcpy(ring + slot * kStageChunk, (const char *)src + off, m);
+        CUDA_CHECK(cudaMemcpyAsync((char *)dst + off, ring + slot * kStageChunk, m, cudaMemcpyHostToDevice, st));
+        CUDA_CHECK(cudaEventRecord(ev, st));
+    }
+}
+
+void stage_d2h(hpdr_ctx *ctx, void *dst, const void *src, size_t n, cudaStream_t st) {
+    char *ring = (char *)ctx->hbuf("stage_out", kStageChunk * kStageSlots);
+    if (n >= (8u << 20)) {   // a fresh destination faults page by page: ask for huge pages (advisory)
+        const uintptr_t a = ((uintptr_t)dst + (2u << 20) - 1) & ~uintptr_t((2u << 20) - 1);
+        const uintptr_t e = ((uintptr_t)dst + n) & ~uintptr_t((2u << 20) - 1);
+        if (e > a) madvise((void *)a, e - a, MADV_HUGEPAGE);
+    }
+    const size_t chunks = (n + kStageChunk - 1) / kStageChunk;
+    size_t issued = 0;
+    for (size_t done = 0; done < chunks; done++) {
+        for (; issued < chunks && issued < done + kStageSlots; issued++) {
+            const size_t off = issued * kStageChunk, m = std::min(kStageChunk, n - off);
+            const unsigned slot = (unsigned)(issued % kStageSlots);
+            CUDA_CHECK(cudaMemcpyAsync(ring + slot * kStageChunk, (const char *)src + off, m, cudaMemcpyDeviceToHost, st));
+            CUDA_CHECK(cudaEventRecord(ctx->event(504 + slot), st));
+        }
+        const unsigned slot = (unsigned)(done % kStageSlots);
+        CUDA_CHECK(cudaEventSynchronize(ctx->event(504 + slot)));
+        const size_t off = done * kStageChunk;
+        parallel_memcpy((char *)dst + off, ring + slot * kStageChunk, std::min(kStageChunk, n - off));
+    }
 }
 
 void store_u64(void *dst, uint64_t v, cudaStream_t s) {

@@ -104,6 +104,7 @@ struct hpdr_ctx {
     // CUDA-graph replays of the coarse levels; off while several host threads drive contexts of the
     // same device (a capture in one thread forbids device-wide synchronisation in the others)
     bool graphs_ok = true;
+    unsigned stage_next = 0;   // next slot of the pinned H2D staging ring (stage_h2d)
     std::string oname(const char *base, int slot) const { return slot ? std::string(base) + "#1" : std::string(base); }
     std::string oname(const char *base) const { return oname(base, out_slot); }
 
@@ -133,6 +134,14 @@ void copy_to_device(hpdr_ctx *ctx, void *dst, const void *src, size_t bytes, cud
 void small_copy(void *dst, const void *src, size_t bytes, cudaStream_t s);
 // cudaMemsetAsync(dst, 0, bytes) as a kernel (same reason as small_copy; any size, 16-byte stores).
 void zero_async(void *dst, size_t bytes, cudaStream_t s);
+// Pageable host memory (plain numpy arrays, Python bytes) moves through pinned staging rings at
+// full PCIe speed instead of the driver's slow pageable path: host-side copies are split across
+// threads and overlap the DMA of the previous slot.
+//   stage_h2d: returns once every DMA is issued on st (the last slots may still be in flight);
+//   stage_d2h: DMA on st after its prior work, returns when dst holds the data.
+void parallel_memcpy(void *dst, const void *src, size_t n);
+void stage_h2d(hpdr_ctx *ctx, void *dst, const void *src, size_t n, cudaStream_t st);
+void stage_d2h(hpdr_ctx *ctx, void *dst, const void *src, size_t n, cudaStream_t st);
 // Store one 8-byte value to device memory in stream order (a kernel parameter, no staging copy).
 void store_u64(void *dst, uint64_t v, cudaStream_t s);
 void copy_from_device(hpdr_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t s);

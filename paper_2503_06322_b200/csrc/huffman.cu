@@ -687,8 +687,10 @@ void decode_begin(hpdr_ctx *ctx, const DecodeJob &job, DecodeSession &S, cudaStr
         S.stats = (unsigned long long *)ctx->dbuf("dec_stats", 32);
         zero_async(S.stats, 32, s);
     }
-    if (copy_payload && units > 0)
-        CUDA_CHECK(cudaMemcpyAsync(S.d_words, job.packed, S.pbytes, cudaMemcpyDefault, s));
+    if (copy_payload && units > 0) {
+        if (classify(job.packed) == MemKind::Host && S.pbytes >= (1u << 20)) stage_h2d(ctx, S.d_words, job.packed, S.pbytes, s);
+        else CUDA_CHECK(cudaMemcpyAsync(S.d_words, job.packed, S.pbytes, cudaMemcpyDefault, s));
+    }
 }
 
 void decode_units(const DecodeSession &S, int64_t u_lo, int64_t u_hi, bool streamed, cudaStream_t s, int redo) {

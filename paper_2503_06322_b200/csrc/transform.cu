@@ -1020,10 +1020,15 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
     // the event the compute stream waits on before touching chunk k
     CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
     CUDA_CHECK(cudaStreamWaitEvent(ctx->h2d, ctx->event(0), 0));   // buffers are free once prior work is done
-    auto issue = [&](int k) {
+    const bool pageable_in = classify(host_in) == MemKind::Host;
+    auto issue = [&](int k) {   // pageable input: staged while the previous chunk is being reduced
         const int64_t a = (int64_t)k * chunk, e = std::min<int64_t>(n0, a + chunk);
-        CUDA_CHECK(cudaMemcpyAsync(d_in + a * plane_bytes, (const char *)host_in + a * plane_bytes,
-                                   (e - a) * plane_bytes, cudaMemcpyHostToDevice, ctx->h2d));
+        if (pageable_in)
+            stage_h2d(ctx, d_in + a * plane_bytes, (const char *)host_in + a * plane_bytes, (e - a) * plane_bytes,
+                      ctx->h2d);
+        else
+            CUDA_CHECK(cudaMemcpyAsync(d_in + a * plane_bytes, (const char *)host_in + a * plane_bytes,
+                                       (e - a) * plane_bytes, cudaMemcpyHostToDevice, ctx->h2d));
         CUDA_CHECK(cudaEventRecord(ctx->event(1 + k), ctx->h2d));
     };
     issue(0);
@@ -1224,7 +1229,8 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
         cast_output(rec, out, out_dtype, p.n_total, s);
         if (host_out) {
             static const int isz[7] = {4, 8, 4, 8, 4, 8, 1};
-            CUDA_CHECK(cudaMemcpyAsync(host_out, out, p.n_total * isz[out_dtype], cudaMemcpyDeviceToHost, s));
+            if (classify(host_out) == MemKind::Host) stage_d2h(ctx, host_out, out, p.n_total * isz[out_dtype], s);
+            else CUDA_CHECK(cudaMemcpyAsync(host_out, out, p.n_total * isz[out_dtype], cudaMemcpyDeviceToHost, s));
         }
         return;
     }
@@ -1319,13 +1325,24 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
             chunk = std::min(chunk, n0);
             CUDA_CHECK(cudaEventRecord(ctx->event(0), ctx->d2h));
             CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(0), 0));   // previous call's copies are done
-            for (int a = 0, k = 0; a < n0; a += chunk, k++) {
+            // every slab is launched first; its D2H follows its event (pageable destinations through the
+            // pinned staging ring, host-blocking, while the GPU runs the later slabs)
+            const bool pageable_out = classify(host_out) == MemKind::Host;
+            int nslab = 0;
+            for (int a = 0, k = 0; a < n0; a += chunk, k++, nslab++) {
                 const int e = std::min(n0, a + chunk);
                 fused_final(p, 0, b.cg, coef, out, out_dtype, s, a, e);
                 CUDA_CHECK(cudaEventRecord(ctx->event(1 + k), s));
+            }
+            for (int a = 0, k = 0; k < nslab; a += chunk, k++) {
+                const int e = std::min(n0, a + chunk);
                 CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(1 + k), 0));
-                CUDA_CHECK(cudaMemcpyAsync((char *)host_out + a * plane_bytes, (const char *)out + a * plane_bytes,
-                                           (e - a) * plane_bytes, cudaMemcpyDeviceToHost, ctx->d2h));
+                if (pageable_out)
+                    stage_d2h(ctx, (char *)host_out + a * plane_bytes, (const char *)out + a * plane_bytes,
+                              (e - a) * plane_bytes, ctx->d2h);
+                else
+                    CUDA_CHECK(cudaMemcpyAsync((char *)host_out + a * plane_bytes, (const char *)out + a * plane_bytes,
+                                               (e - a) * plane_bytes, cudaMemcpyDeviceToHost, ctx->d2h));
             }
             CUDA_CHECK(cudaStreamSynchronize(ctx->d2h));
         } else if (st_i == 0 && direct) {
@@ -1337,7 +1354,8 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
     if (!direct) cast_output(b.lvl0, out, out_dtype, p.n_total, s);
     if (host_out && !direct) {
         static const int isz[7] = {4, 8, 4, 8, 4, 8, 1};
-        CUDA_CHECK(cudaMemcpyAsync(host_out, out, p.n_total * isz[out_dtype], cudaMemcpyDeviceToHost, s));
+        if (classify(host_out) == MemKind::Host) stage_d2h(ctx, host_out, out, p.n_total * isz[out_dtype], s);
+        else CUDA_CHECK(cudaMemcpyAsync(host_out, out, p.n_total * isz[out_dtype], cudaMemcpyDeviceToHost, s));
     }
 }
 

@@ -12,6 +12,7 @@
 // blocks are coded as soon as their planes are resident, and the finished stream bytes go out
 // on the d2h stream while the next slab is coded (decompress mirrors it).
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <utility>
 
@@ -789,7 +790,8 @@ int hpdr_zfp_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, const 
         const int isz = dtype == 0 ? 4 : 8;
         const uint64_t n = (uint64_t)z.G.n[0] * z.G.n[1] * z.G.n[2];
         const uint64_t plane_bytes = (uint64_t)z.G.n[1] * z.G.n[2] * isz;
-        const bool in_dev = classify(in) == MemKind::Device;
+        const MemKind ik = classify(in);
+        const bool in_dev = ik == MemKind::Device, in_pageable = ik == MemKind::Host;
         const MemKind ok = classify(out);
         const bool out_dev = ok == MemKind::Device;
         cudaStream_t s = ctx->stream;
@@ -821,9 +823,13 @@ int hpdr_zfp_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, const 
                 const int64_t last_row = (hi - 1) / z.blocks_per_plane;
                 const uint64_t need = std::min<uint64_t>((uint64_t)z.G.n[0], (uint64_t)(last_row + 1) * 4);
                 if (need > in_done) {
-                    CUDA_CHECK(cudaMemcpyAsync((uint8_t *)din + in_done * plane_bytes,
-                                               (const uint8_t *)in + in_done * plane_bytes,
-                                               (need - in_done) * plane_bytes, cudaMemcpyHostToDevice, ctx->h2d));
+                    if (in_pageable)   // staged while the previous slab is coded
+                        stage_h2d(ctx, (uint8_t *)din + in_done * plane_bytes, (const uint8_t *)in + in_done * plane_bytes,
+                                  (need - in_done) * plane_bytes, ctx->h2d);
+                    else
+                        CUDA_CHECK(cudaMemcpyAsync((uint8_t *)din + in_done * plane_bytes,
+                                                   (const uint8_t *)in + in_done * plane_bytes,
+                                                   (need - in_done) * plane_bytes, cudaMemcpyHostToDevice, ctx->h2d));
                     in_done = need;
                 }
                 CUDA_CHECK(cudaEventRecord(ctx->event(400 + k), ctx->h2d));
@@ -845,7 +851,7 @@ int hpdr_zfp_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, const 
         CUDA_CHECK(cudaStreamSynchronize(s));
         CUDA_CHECK(cudaStreamSynchronize(ctx->d2h));
         if (*bad_h) throw Error{HPDR_ERR_VALIDATION, "non-finite values cannot be aligned", -1};
-        if (stage) memcpy(o + hl, stage, z.payload);
+        if (stage) parallel_memcpy(o + hl, stage, z.payload);
     });
 }
 
@@ -875,12 +881,19 @@ int hpdr_zfp_decompress(hpdr_ctx *ctx, const void *stream, uint64_t len, void *o
         const int K = (int)cut.size() - 1;
         uint64_t rows_out = 0;   // output planes copied out
         uint64_t pay_in = 0;     // payload bytes resident
+        const bool in_pageable = !in_dev && classify(stream) == MemKind::Host;
+        const bool out_pageable = ok == MemKind::Host;
+        std::vector<std::array<uint64_t, 3>> outs;
         for (int k = 0; k < K; k++) {
             const int64_t lo = cut[k], hi = cut[k + 1];
             const uint64_t need = k == K - 1 ? z.payload : ((uint64_t)hi * z.w + 7) / 8;
             if (need > pay_in) {
-                CUDA_CHECK(cudaMemcpyAsync((uint8_t *)pay + pay_in, (const uint8_t *)stream + hl + pay_in, need - pay_in,
-                                           in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->h2d));
+                if (in_pageable)
+                    stage_h2d(ctx, (uint8_t *)pay + pay_in, (const uint8_t *)stream + hl + pay_in, need - pay_in, ctx->h2d);
+                else
+                    CUDA_CHECK(cudaMemcpyAsync((uint8_t *)pay + pay_in, (const uint8_t *)stream + hl + pay_in,
+                                               need - pay_in, in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                               ctx->h2d));
                 pay_in = need;
             }
             CUDA_CHECK(cudaEventRecord(ctx->event(440 + k), ctx->h2d));
@@ -892,12 +905,21 @@ int hpdr_zfp_decompress(hpdr_ctx *ctx, const void *stream, uint64_t len, void *o
                                              : std::min<uint64_t>((uint64_t)z.G.n[0], (uint64_t)(hi / z.blocks_per_plane) * 4);
             if (rows > rows_out) {
                 CUDA_CHECK(cudaEventRecord(ctx->event(460 + k), s));
-                CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(460 + k), 0));
-                CUDA_CHECK(cudaMemcpyAsync((uint8_t *)out + rows_out * plane_elems * isz,
-                                           (uint8_t *)dout + rows_out * plane_elems * isz,
-                                           (rows - rows_out) * plane_elems * isz, cudaMemcpyDeviceToHost, ctx->d2h));
+                if (out_pageable) {
+                    outs.push_back({rows_out, rows, (uint64_t)k});   // copied out below, after every slab is queued
+                } else {
+                    CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(460 + k), 0));
+                    CUDA_CHECK(cudaMemcpyAsync((uint8_t *)out + rows_out * plane_elems * isz,
+                                               (uint8_t *)dout + rows_out * plane_elems * isz,
+                                               (rows - rows_out) * plane_elems * isz, cudaMemcpyDeviceToHost, ctx->d2h));
+                }
                 rows_out = rows;
             }
+        }
+        for (const auto &r : outs) {   // pageable output: pinned staging ring, host-blocking
+            CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(460 + (int)r[2]), 0));
+            stage_d2h(ctx, (uint8_t *)out + r[0] * plane_elems * isz, (uint8_t *)dout + r[0] * plane_elems * isz,
+                      (r[1] - r[0]) * plane_elems * isz, ctx->d2h);
         }
         CUDA_CHECK(cudaStreamSynchronize(s));
         CUDA_CHECK(cudaStreamSynchronize(ctx->d2h));
