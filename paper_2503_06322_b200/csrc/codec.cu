@@ -70,6 +70,12 @@ struct Reader {
     }
 };
 
+// Device -> host copy of a result: pageable destinations through the pinned staging ring.
+void result_to_host(hpdr_ctx *ctx, void *dst, const void *src, size_t n, cudaStream_t s) {
+    if (n >= (1u << 20) && classify(dst) == MemKind::Host) stage_d2h(ctx, dst, src, n, s);
+    else CUDA_CHECK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s));
+}
+
 // Device-resident input: copy host data to a context buffer when needed.
 const void *device_input(hpdr_ctx *ctx, const void *in, size_t bytes, const char *name, cudaStream_t s) {
     const MemKind k = classify(in);
@@ -921,7 +927,7 @@ int hpdr_decompose(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uin
         minmax_device(ctx, d_in, dtype, N, u_min, u_max, s);
         double *coef = classify(coef_out) == MemKind::Device ? coef_out : (double *)ctx->dbuf("coef", N * 8);
         decompose_device(ctx, p, d_in, dtype, coef, s);
-        if (coef != coef_out) CUDA_CHECK(cudaMemcpyAsync(coef_out, coef, N * 8, cudaMemcpyDeviceToHost, s));
+        if (coef != coef_out) result_to_host(ctx, coef_out, coef, N * 8, s);
         CUDA_CHECK(cudaStreamSynchronize(s));
     });
 }
@@ -935,7 +941,7 @@ int hpdr_recompose(hpdr_ctx *ctx, const double *coef_in, int rank, const uint64_
         const double *coef = (const double *)device_input(ctx, coef_in, N * 8, "coef", s);
         double *rec = classify(out) == MemKind::Device ? out : (double *)ctx->dbuf("out_stage", N * 8);
         recompose_into(ctx, p, coef, rec, 1, s);
-        if (rec != out) CUDA_CHECK(cudaMemcpyAsync(out, rec, N * 8, cudaMemcpyDeviceToHost, s));
+        if (rec != out) result_to_host(ctx, out, rec, N * 8, s);
         CUDA_CHECK(cudaStreamSynchronize(s));
     });
 }
@@ -1002,7 +1008,7 @@ int hpdr_dequantize(hpdr_ctx *ctx, const uint32_t *keys_in, uint64_t n_keys, int
         int rc = scatter_outliers(ctx, coef, N, outlier_idx, outlier_bins, n_outliers, bin_width, s);
         if (rc == HPDR_ERR_INDEX) fail(rc, "outlier index out of bounds for axis 0 with size " + std::to_string(N));
         restore_coarse(ctx, coef, p, coarse, n_coarse, s);
-        if (coef != coef_out) CUDA_CHECK(cudaMemcpyAsync(coef_out, coef, N * 8, cudaMemcpyDeviceToHost, s));
+        if (coef != coef_out) result_to_host(ctx, coef_out, coef, N * 8, s);
         CUDA_CHECK(cudaStreamSynchronize(s));
     });
 }
@@ -1083,7 +1089,7 @@ int hpdr_huffman_decompress(hpdr_ctx *ctx, const void *in, uint64_t len, uint32_
         const bool dev = classify(keys_out) == MemKind::Device;
         uint32_t *keys = dev ? keys_out : (uint32_t *)ctx->dbuf("hkeys", hh.n_sym * 4 + 64);
         run_decode(ctx, hh, keys, nullptr, 1.0, 0xffffffffu, s);
-        if (!dev) CUDA_CHECK(cudaMemcpyAsync(keys_out, keys, hh.n_sym * 4, cudaMemcpyDeviceToHost, s));
+        if (!dev) result_to_host(ctx, keys_out, keys, hh.n_sym * 4, s);
         CUDA_CHECK(cudaStreamSynchronize(s));
     });
 }
