@@ -56,6 +56,8 @@ const char *hpdr_last_error(int64_t *bit_offset);
 
 /* Pinned host memory (cudaHostAlloc) for zero-staging transfers. */
 void    *hpdr_host_alloc(uint64_t bytes);
+/* Host memcpy split across the library's copy threads (large results into Python-owned memory). */
+void     hpdr_host_copy(void *dst, const void *src, uint64_t n);
 void     hpdr_host_free(void *p);
 
 /* ---- whole-path entry points: hpdr/mgard/codec.py ---- */

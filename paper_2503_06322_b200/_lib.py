@@ -31,6 +31,7 @@ _SIGS = {
     "hpdr_ctx_trim": (None, [C.c_void_p]),
     "hpdr_last_error": (C.c_char_p, [_i64p]),
     "hpdr_host_alloc": (C.c_void_p, [C.c_uint64]),
+    "hpdr_host_copy": (None, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "hpdr_host_free": (None, [C.c_void_p]),
     "hpdr_mgard_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _u64p, C.c_double, C.c_uint32,
                                       C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_uint64, _u64p]),
@@ -210,6 +211,32 @@ _pybytes_new.argtypes = [C.c_void_p, C.c_ssize_t]
 _pybytes_ptr = C.pythonapi.PyBytes_AsString
 _pybytes_ptr.restype = C.c_void_p
 _pybytes_ptr.argtypes = [C.py_object]
+
+
+_scratch = threading.local()
+
+
+def pinned_scratch(nbytes: int) -> np.ndarray:
+    """A per-thread, grow-only pinned host buffer (uint8) of at least nbytes, owned by the library
+    (for results whose size is only known after the call, e.g. a pipeline container)."""
+    cur = getattr(_scratch, "buf", None)
+    if cur is None or cur[1] < nbytes:
+        if cur is not None:
+            lib().hpdr_host_free(C.c_void_p(cur[0]))
+        p = lib().hpdr_host_alloc(int(nbytes))
+        if not p:
+            raise AllocationError(f"cudaHostAlloc of {nbytes} bytes failed")
+        cur = (p, int(nbytes))
+        _scratch.buf = cur
+    return np.ctypeslib.as_array((C.c_uint8 * cur[1]).from_address(cur[0]))
+
+
+def bytes_from(buf: np.ndarray, n: int) -> bytes:
+    """bytes(buf[:n]) with the copy split across the library's threads."""
+    b, p = new_bytes(n)
+    if n:
+        lib().hpdr_host_copy(C.c_void_p(p), C.c_void_p(buf.ctypes.data), int(n))
+    return b
 
 
 def new_bytes(n: int):

@@ -598,6 +598,8 @@ uint64_t hpdr_ctx_alloc_events(const hpdr_ctx *c) {
 }
 int hpdr_ctx_device(const hpdr_ctx *c) { return c ? c->device : -1; }
 
+void hpdr_host_copy(void *dst, const void *src, uint64_t n) { hpdr::parallel_memcpy(dst, src, n); }
+
 void *hpdr_host_alloc(uint64_t bytes) {
     void *p = nullptr;
     if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {

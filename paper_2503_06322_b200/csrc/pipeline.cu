@@ -229,6 +229,7 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
             for (uint64_t a = 0; a < n0; a += chunk_planes) sizes.push_back(std::min(chunk_planes, n0 - a));
         }
         const uint64_t K = sizes.size();
+        const bool in_pageable = classify(host_in) == MemKind::Host;   // staged through pinned rings
         double vmin = range_min, vmax = range_max;
         // Relative mode needs the global range before any chunk is quantized.  The
         // decomposition does not depend on it, so by default the chunks are streamed in and
@@ -303,8 +304,11 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
                 if (RR.failed) return false;
                 if (!first) CUDA_CHECK(cudaStreamWaitEvent(c->h2d, ev_red, 0));   // input buffer reuse edge
                 tm.mark(6 * k, c->h2d);
-                CUDA_CHECK(cudaMemcpyAsync(din, (const char *)host_in + chunks[k].raw_off * isz,
-                                           chunks[k].raw_size * isz, cudaMemcpyHostToDevice, c->h2d));
+                if (in_pageable)
+                    stage_h2d(c, din, (const char *)host_in + chunks[k].raw_off * isz, chunks[k].raw_size * isz, c->h2d);
+                else
+                    CUDA_CHECK(cudaMemcpyAsync(din, (const char *)host_in + chunks[k].raw_off * isz,
+                                               chunks[k].raw_size * isz, cudaMemcpyHostToDevice, c->h2d));
                 tm.mark(6 * k + 1, c->h2d);
                 minmax_accumulate(din, dtype, (int64_t)chunks[k].raw_size, mm, c->h2d);
                 CUDA_CHECK(cudaEventRecord(ev_in, c->h2d));
@@ -377,8 +381,12 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
                 if (!two_phase) {
                     if (!first) CUDA_CHECK(cudaStreamWaitEvent(c->h2d, ev_red, 0));   // input buffer reuse edge
                     tm.mark(6 * k, c->h2d);
-                    CUDA_CHECK(cudaMemcpyAsync(din, (const char *)host_in + chunks[k].raw_off * isz,
-                                               chunks[k].raw_size * isz, cudaMemcpyHostToDevice, c->h2d));
+                    if (in_pageable)
+                        stage_h2d(c, din, (const char *)host_in + chunks[k].raw_off * isz, chunks[k].raw_size * isz,
+                                  c->h2d);
+                    else
+                        CUDA_CHECK(cudaMemcpyAsync(din, (const char *)host_in + chunks[k].raw_off * isz,
+                                                   chunks[k].raw_size * isz, cudaMemcpyHostToDevice, c->h2d));
                     tm.mark(6 * k + 1, c->h2d);
                     CUDA_CHECK(cudaEventRecord(ev_in, c->h2d));
                     CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_in, 0));
@@ -486,7 +494,9 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
             maxpay = std::max(maxpay, ch.pay_size);
             maxraw = std::max(maxraw, ch.raw_size);
         }
-        const bool host_out = classify(out) != MemKind::Device;
+        const MemKind omk = classify(out);
+        const bool host_out = omk != MemKind::Device, out_pageable = omk == MemKind::Host;
+        const bool blob_pageable = classify(container) == MemKind::Host;
         const int Q = pipe_queues(K);
         std::vector<hpdr_ctx *> qc(Q);
         for (int q = 0; q < Q; q++) qc[q] = ctx->queue(q);
@@ -520,8 +530,11 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
                 uint8_t *dblob = dblobs[t & 1];
                 if (t >= 2) CUDA_CHECK(cudaStreamWaitEvent(x->h2d, ev_reds[t & 1], 0));   // blob buffer reuse edge
                 tm.mark(6 * k, x->h2d);
-                CUDA_CHECK(cudaMemcpyAsync(dblob, c + base + chunks[k].pay_off, chunks[k].pay_size,
-                                           cudaMemcpyHostToDevice, x->h2d));
+                if (blob_pageable)
+                    stage_h2d(x, dblob, c + base + chunks[k].pay_off, chunks[k].pay_size, x->h2d);
+                else
+                    CUDA_CHECK(cudaMemcpyAsync(dblob, c + base + chunks[k].pay_off, chunks[k].pay_size,
+                                               cudaMemcpyHostToDevice, x->h2d));
                 tm.mark(6 * k + 1, x->h2d);
                 CUDA_CHECK(cudaEventRecord(ev_in, x->h2d));
                 CUDA_CHECK(cudaStreamWaitEvent(x->stream, ev_in, 0));
@@ -535,7 +548,9 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
                 CUDA_CHECK(cudaEventRecord(ev_reds[t & 1], x->stream));
                 CUDA_CHECK(cudaStreamWaitEvent(x->d2h, ev_red, 0));
                 tm.mark(6 * k + 4, x->d2h);
-                if (host_out)
+                if (host_out && out_pageable)   // host-blocking; the other queues keep the GPU busy
+                    stage_d2h(x, (char *)out + chunks[k].raw_off * isz, dout, chunks[k].raw_size * isz, x->d2h);
+                else if (host_out)
                     CUDA_CHECK(cudaMemcpyAsync((char *)out + chunks[k].raw_off * isz, dout, chunks[k].raw_size * isz,
                                                cudaMemcpyDeviceToHost, x->d2h));
                 tm.mark(6 * k + 5, x->d2h);

@@ -221,7 +221,7 @@ def compress_pipelined(arr, eb_rel: float, dict_size: int = 4096, value_range=No
     k = len(lst) if lst is not None else -(-dims[0] // chunk_planes) if chunk_planes else 0
     nbytes = int(np.prod(dims)) * (4 if code == 0 else 8)
     cap = nbytes + (1 << 20) if out is None else int(out.nbytes)
-    buf = np.empty(cap, np.uint8) if out is None else out
+    buf = _lib.pinned_scratch(cap) if out is None else out   # reused pinned scratch, then one bytes copy
     tr = np.zeros(6 * max(k, 1) + 6 * 4096, np.float64) if trace else None
     n = C.c_uint64()
 
@@ -238,7 +238,7 @@ def compress_pipelined(arr, eb_rel: float, dict_size: int = 4096, value_range=No
         rc = run(buf)
     check(rc)
     del keep
-    data = buf[: n.value].tobytes() if out is None else int(n.value)
+    data = _lib.bytes_from(buf, n.value) if out is None else int(n.value)
     if not trace:
         return data
     from .container import read_container
