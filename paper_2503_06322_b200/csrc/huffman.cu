@@ -297,7 +297,11 @@ __device__ __forceinline__ uint32_t dw_lookup(uint32_t win, const uint32_t *lut,
     const uint32_t e = lut[win >> (32 - kLutBits)];
     L = (int)(e & 0xffu);
     if (L) return e >> 8;
-    for (int l = kLutBits + 1; l <= max_len; l++) {
+    // longer codes: the entry holds the shortest code length that has this kLutBits-bit prefix
+    // (0: no codeword starts with it); shorter lengths cannot match, so the scan starts there
+    const int l0 = (int)((e >> 8) & 0xffu);
+    if (!l0) return 0;
+    for (int l = l0; l <= max_len; l++) {
         const long long idx = (long long)(win >> (32 - l)) - T.first_code[l];
         if (idx >= 0 && idx < T.cnt[l]) {
             L = l;
@@ -633,6 +637,16 @@ void decode_begin(hpdr_ctx *ctx, const DecodeJob &job, DecodeSession &S, cudaStr
         }
         lut[v] = e;
     }
+    // prefixes of codes longer than kLutBits: the shortest such length per prefix (canonical codes
+    // of length l cover the prefixes [first >> (l - kLutBits), (first + cnt - 1) >> (l - kLutBits)])
+    if (max_len > kLutBits && max_len <= 32)
+        for (int l = kLutBits + 1; l <= max_len; l++) {
+            if (!T->cnt[l]) continue;
+            const unsigned long long f = (unsigned long long)T->first_code[l];
+            const unsigned long long lo = f >> (l - kLutBits), hi = (f + T->cnt[l] - 1) >> (l - kLutBits);
+            for (unsigned long long v = lo; v <= hi && v < (unsigned long long)kLutSize; v++)
+                if (!lut[v]) lut[v] = (uint32_t)l << 8;
+        }
     const size_t tab_bytes = sizeof(DecTables) + kLutSize * 4 + (present.size() + 1) * 4;
     char *d_tab = (char *)ctx->dbuf("dec_tabs", tab_bytes);
     small_copy(d_tab, T, tab_bytes, s);
