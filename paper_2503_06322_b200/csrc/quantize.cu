@@ -119,26 +119,37 @@ __global__ void k_chunk_counts(const uint32_t *__restrict__ omask, int64_t words
     if (threadIdx.x == 0) counts[c] = tot;
 }
 
+// Ordered outlier compaction (quantize.py:80-83: ascending flat index).  Per 256-word step the block
+// scans the words' popcounts; then each warp takes whole words with one lane per node, so the
+// index / bin writes and the sparse-bin reads are coalesced (consecutive positions / nodes).
 __global__ void k_write_outliers(const uint32_t *__restrict__ omask, int64_t words, const double *__restrict__ coef,
                                  const long long *__restrict__ sparse, double bin, const unsigned long long *__restrict__ chunk_off,
                                  uint64_t *__restrict__ oidx, int64_t *__restrict__ obins) {
     typedef cub::BlockScan<unsigned, 256> BS;
     __shared__ typename BS::TempStorage tmp;
+    __shared__ uint32_t smask[256];
+    __shared__ unsigned spre[256];
     const int64_t c = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned long long base = chunk_off[c];
-    for (int64_t w0 = c * kChunkWords; w0 < min64(words, (c + 1) * kChunkWords); w0 += blockDim.x) {
+    const int64_t w_end = min64(words, (c + 1) * kChunkWords);
+    for (int64_t w0 = c * kChunkWords; w0 < w_end; w0 += blockDim.x) {
         const int64_t w = w0 + threadIdx.x;
-        uint32_t m = (w < words && w < (c + 1) * kChunkWords) ? omask[w] : 0u;
+        const uint32_t m = w < w_end ? omask[w] : 0u;
         unsigned pre, tot;
         BS(tmp).ExclusiveSum((unsigned)__popc(m), pre, tot);
-        unsigned long long pos = base + pre;
-        while (m) {
-            int bit = __ffs(m) - 1;
-            m &= m - 1;
-            int64_t i = w * 32 + bit;
-            oidx[pos] = (uint64_t)i;
-            obins[pos] = sparse ? sparse[i] : (long long)rint(coef[i] / bin);
-            pos++;
+        smask[threadIdx.x] = m;
+        spre[threadIdx.x] = pre;
+        __syncthreads();
+        for (int k = warp; k < 256; k += 8) {
+            const uint32_t mk = smask[k];
+            if (!mk) continue;
+            if ((mk >> lane) & 1u) {
+                const unsigned long long pos = base + spre[k] + __popc(mk & ((1u << lane) - 1u));
+                const int64_t i = (w0 + k) * 32 + lane;
+                oidx[pos] = (uint64_t)i;
+                obins[pos] = sparse ? sparse[i] : (long long)rint(coef[i] / bin);
+            }
         }
         base += tot;
         __syncthreads();
