@@ -650,6 +650,7 @@ int zguard(F &&f) {
 // Header checks of zfp_decompress, in the reference's order (zfp.py:314-334).
 void zfp_parse(const uint8_t *d, uint64_t len, ZfpShape &z) {
     if (len < (uint64_t)kZHeader) throw Error{HPDR_ERR_CORRUPT, "stream shorter than header", -1};
+    if (!d) throw Error{HPDR_ERR_VALIDATION, "null stream pointer", -1};
     const int rank = d[0], code = d[1], rate = d[2];
     if (rank < 1 || rank > 3 || code > 6) throw Error{HPDR_ERR_CORRUPT, "bad rank or dtype code", -1};
     if (code != 0 && code != 1) throw Error{HPDR_ERR_CORRUPT, "stored dtype is not a float type", -1};
@@ -781,11 +782,13 @@ int hpdr_zfp_peek(const void *stream, uint64_t len, int *dtype, int *rank, uint6
 int hpdr_zfp_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, uint32_t rate,
                       void *out, uint64_t out_cap, uint64_t *out_len) {
     return zguard([&] {
+        if (!ctx || !dims || !out_len) throw Error{HPDR_ERR_VALIDATION, "null argument", -1};
         ZfpShape z;
         zfp_shape(dtype, rank, dims, (int)std::min<uint32_t>(rate, 1u << 20), z);
         *out_len = z.total;
         if (!out || out_cap < z.total)
             throw Error{HPDR_ERR_BUFFER, "output buffer too small: need " + std::to_string(z.total), -1};
+        if (!in) throw Error{HPDR_ERR_VALIDATION, "null input pointer", -1};
         CUDA_CHECK(cudaSetDevice(ctx->device));
         const int isz = dtype == 0 ? 4 : 8;
         const uint64_t n = (uint64_t)z.G.n[0] * z.G.n[1] * z.G.n[2];
