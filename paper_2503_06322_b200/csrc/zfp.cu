@@ -5,8 +5,8 @@
 // the coder embarrassingly parallel: one thread owns one block end to end (gather with edge
 // replication, common exponent, fixed point, reversible lifting, negabinary, bit planes), and a
 // CTA of 128 threads owns 128 consecutive blocks = 16*w whole bytes of stream, assembled in
-// shared memory and stored with coalesced 32-bit words.  The kernels are HBM-bound
-// (4 or 8 B/value in, rate/8 B/value out) -- see DESIGN.md section 10.
+// shared memory and stored with coalesced 16-byte vector stores.  The roofline is HBM (4 or 8
+// B/value in, rate/8 B/value out); measured at 0.4-0.5 of it, issue-bound -- DESIGN.md section 10.
 //
 // The host side streams: the input is copied in dim-0 slabs on the h2d stream, each slab's
 // blocks are coded as soon as their planes are resident, and the finished stream bytes go out
