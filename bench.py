@@ -340,6 +340,9 @@ def main():
     def decompress_e2e():
         P.mgard_decompress(blob_view, out=h_out)
 
+    # inputs smaller than the 126 MB L2: a 256 MB buffer written between timed steps
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev) if nbytes < (126 << 20) else None
+
     def timed(fn, steps, prof=False, clocks=None):
         for _ in range(args.warmup):
             fn()
@@ -351,18 +354,30 @@ def main():
         _lib.launch_count(reset=True)
         if prof:
             _lib.prof_enable(True)
-        e0.record(stream)
-        for _ in range(steps):
-            fn()
-        e1.record(stream)
-        e1.synchronize()
+        if flush is None:   # inputs larger than L2: one timed region over all steps
+            e0.record(stream)
+            for _ in range(steps):
+                fn()
+            e1.record(stream)
+            e1.synchronize()
+            total = e0.elapsed_time(e1)
+        else:               # inputs smaller than L2: each step timed alone, L2 flushed in between
+            total = 0.0
+            for _ in range(steps):
+                flush.add_(1)
+                torch.cuda.synchronize(dev)
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+                e1.synchronize()
+                total += e0.elapsed_time(e1)
         torch.cuda.synchronize(dev)
         launches = _lib.launch_count()
         kern = _lib.prof_read() if prof else None
         if prof:
             _lib.prof_enable(False)
         barrier()
-        ms = max_over_ranks(e0.elapsed_time(e1))
+        ms = max_over_ranks(total)
         return ms / steps, launches, kern
 
     # M2: the paper's chunked streams pipeline (HPDR container of per-chunk reference blobs).
@@ -509,7 +524,7 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["workload"], "shape": list(cfg["shape"]), "input_dtype": cfg["dtype"],
                    "eb_rel": cfg["eb"], "direction": "compress", "l2": "inputs larger than L2 (no flush needed)"
-                   if nbytes > 126e6 else "inputs smaller than L2",
+                   if nbytes > 126e6 else "inputs smaller than L2: 256 MB buffer written between separately timed steps",
                    "parallelism": f"block-partitioned x{world} (global range all-reduce only)",
                    "mode": "M1: mgard_compress drop-in, one reference-identical blob per rank"},
         "e2e": {"value": gbs(e_ms), "unit": "GB/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": blob_len,
