@@ -373,7 +373,7 @@ __global__ void k_gather_vals(const double *__restrict__ src, const long long *_
 void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t *dims, double eb_rel,
                  uint32_t dict_size, double u_min, double u_max, double eb_abs, double bin, const QuantResult &q,
                  uint32_t *keys, const double *d_coarse, const double *coef_for_coarse, void *fetch_out,
-                 uint64_t fetch_cap) {
+                 uint64_t fetch_cap, bool coarse_ready = false) {
     {
         const int64_t N = p.n_total;
         const int L = p.host.L;
@@ -385,7 +385,9 @@ void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t 
         // one copy into pinned staging (the coarsest set is <= 16 values; gathered on the device
         // from the coefficient set when there is no dense coarsest level)
         double *hco = (double *)ctx->hbuf("coarse_rb", 16 * 8);
-        if (d_coarse) {
+        if (coarse_ready) {
+            // read back with the histogram (quantize_finish's round trip)
+        } else if (d_coarse) {
             small_copy(hco, d_coarse, nco * 8, s);
         } else if (nco) {
             double *dco = (double *)ctx->dbuf("coarse_gather", 16 * 8);
@@ -393,7 +395,7 @@ void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t 
             LAUNCH_CHECK();
             small_copy(hco, dco, nco * 8, s);
         }
-        CUDA_CHECK(cudaStreamSynchronize(s));
+        if (!coarse_ready) CUDA_CHECK(cudaStreamSynchronize(s));
         if (nco) memcpy(coarse.data(), hco, nco * 8);
         auto &P = ctx->pending;
         P = hpdr_ctx::Pending();
@@ -488,6 +490,7 @@ void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uin
         QuantResult q;
         const double *d_coarse;
         double eb_abs = 0.0, bin = 1.0;
+        bool coarse_ready = false;
         if (fused) {
             // quantize-on-write: keys, outlier mask and histogram come out of the level kernels
             QuantOut qo;
@@ -516,6 +519,10 @@ void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uin
                 d_coarse = decompose_quantize(ctx, p, d_in, dtype, qo, s);
             }
             phase_mark("decomposed", s);
+            if (d_coarse && !p.host.coarsest.empty()) {   // the coarsest values ride the next host round trip
+                small_copy(ctx->hbuf("coarse_rb", 16 * 8), d_coarse, p.host.coarsest.size() * 8, s);
+                coarse_ready = true;
+            }
             quantize_finish(ctx, N, dict_size, bin, nullptr, qo.obins, q, s);
             phase_mark("outliers", s);
         } else {
@@ -526,7 +533,7 @@ void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uin
             quantize_device(ctx, coef, N, p.host.coarsest, bin, dict_size, keys, q, s);
         }
         finish_blob(ctx, p, dtype, rank, dims, eb_rel, dict_size, u_min, u_max, eb_abs, bin, q, keys, d_coarse, nullptr,
-                    fetch_out, fetch_cap);
+                    fetch_out, fetch_cap, coarse_ready);
     }
 }
 
