@@ -271,3 +271,28 @@ def test_device_resident_blob_decompress(oracle):
     assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
     with pytest.raises(CorruptStreamError):
         P.mgard_decompress(d[:60])
+
+
+def test_pageable_staging_matches_pinned_and_device():
+    """Plain numpy / bytes (pageable) go through the pinned staging rings: results must equal the
+    pinned-host and device-resident paths byte for byte (sizes that leave partial 16 MB slots)."""
+    torch = pytest.importorskip("torch")
+    from paper_2503_06322_b200 import zfp as Z
+
+    a = S.smooth_noise((301, 300, 203), seed=5)          # 73 MB fp32: 5 slots, a partial last one
+    pin = torch.from_numpy(a.copy()).pin_memory()
+    dev = torch.from_numpy(a).cuda()
+    blob = P.mgard_compress(a, 1e-4)
+    assert blob == P.mgard_compress(pin, 1e-4) == P.mgard_compress(dev, 1e-4)
+    y = P.mgard_decompress(blob).values
+    yp = torch.empty(a.shape, dtype=torch.float32).pin_memory()
+    P.mgard_decompress(torch.from_numpy(np.frombuffer(blob, np.uint8).copy()).pin_memory().numpy(), out=yp.numpy())
+    assert np.array_equal(y.view(np.uint32), yp.numpy().view(np.uint32))
+    # a bytes slice at an odd offset (unaligned pageable source)
+    buf = bytearray(b"\x00" * 3 + blob)
+    y2 = P.mgard_decompress(memoryview(buf)[3:]).values
+    assert np.array_equal(y.view(np.uint32), y2.view(np.uint32))
+    z = Z.zfp_compress(a, 11)
+    assert z == Z.zfp_compress(pin, 11)
+    assert np.array_equal(Z.zfp_decompress(z).values.view(np.uint32),
+                          Z.zfp_decompress(torch.from_numpy(np.frombuffer(z, np.uint8).copy()).cuda()).values.view(np.uint32))
