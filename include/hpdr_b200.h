@@ -50,6 +50,18 @@ int      hpdr_ctx_device(const hpdr_ctx *ctx);
 /* Release cached device buffers (keeps the context usable). */
 void     hpdr_ctx_trim(hpdr_ctx *ctx);
 
+/* Job-wide value range for block-partitioned compression (the multi-GPU path
+ * of SURVEY 8(e)).  In relative mode (has_range = 0) hpdr_mgard_compress calls hook(user, &vmin,
+ * &vmax) on the calling host thread once this block's min / max are known -- after the
+ * range-independent decomposition of a streamed host input has been issued, before anything is
+ * quantized -- and compresses with the values the hook leaves there, exactly as
+ * mgard_compress(block, eb_rel, value_range=(vmin, vmax)) (quantize.py:66, codec.py:47-48).  A
+ * rank-per-GPU job puts its min/max all-reduce (16 bytes) here, so the exchange overlaps the
+ * input transfer instead of costing an extra pass over the field.  A non-zero return fails the
+ * call with HPDR_ERR_VALIDATION.  hook = NULL removes it. */
+typedef int (*hpdr_range_hook)(void *user, double *vmin, double *vmax);
+void     hpdr_ctx_set_range_hook(hpdr_ctx *ctx, hpdr_range_hook hook, void *user);
+
 /* Thread-local error message of the last failing call; *bit_offset receives
  * CorruptStreamError.bit_offset (-1 when unknown), may be NULL. */
 const char *hpdr_last_error(int64_t *bit_offset);

@@ -29,6 +29,7 @@ _SIGS = {
     "hpdr_ctx_alloc_events": (C.c_uint64, [C.c_void_p]),
     "hpdr_ctx_device": (C.c_int, [C.c_void_p]),
     "hpdr_ctx_trim": (None, [C.c_void_p]),
+    "hpdr_ctx_set_range_hook": (None, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "hpdr_last_error": (C.c_char_p, [_i64p]),
     "hpdr_host_alloc": (C.c_void_p, [C.c_uint64]),
     "hpdr_host_copy": (None, [C.c_void_p, C.c_void_p, C.c_uint64]),

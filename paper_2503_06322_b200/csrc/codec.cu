@@ -441,8 +441,8 @@ void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t 
             };
             hooks.group_done = [&](int g, uint64_t lo, uint64_t hi) {
                 if (!streamed_fetch || hi <= lo) return;
-                CUDA_CHECK(cudaEventRecord(ctx->event(1 + g), s));
-                CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(1 + g), 0));
+                CUDA_CHECK(cudaEventRecord(ctx->event(EvEncGroup, g), s));
+                CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(EvEncGroup, g), 0));
                 const bool dev = ok == MemKind::Device;
                 CUDA_CHECK(cudaMemcpyAsync((char *)fetch_out + pay_pos + lo, (const char *)ctx->dbuf(ctx->oname("enc_words"), 16) + lo,
                                            hi - lo, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->d2h));
@@ -484,7 +484,10 @@ void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uin
         phase_mark("start", s);
         const void *d_in = streamed ? nullptr : device_input(ctx, in, (size_t)N * itemsize(dtype), "input", s);
         double u_min = range_min, u_max = range_max;
-        if (!has_range && !streamed) minmax_device(ctx, d_in, dtype, N, &u_min, &u_max, s);
+        if (!has_range && !streamed) {
+            minmax_device(ctx, d_in, dtype, N, &u_min, &u_max, s);
+            apply_range_hook(ctx, &u_min, &u_max);
+        }
         phase_mark("minmax", s);
         uint32_t *keys = (uint32_t *)ctx->dbuf("keys", N * 4 + 64);
         QuantResult q;
@@ -821,9 +824,9 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                                                    cudaMemcpyHostToDevice, ctx->h2d));
                     copied = want;
                 }
-                CUDA_CHECK(cudaEventRecord(ctx->event(100 + g), ctx->h2d));
+                CUDA_CHECK(cudaEventRecord(ctx->event(EvDecIn, g), ctx->h2d));
                 phase_mark("h2d", ctx->h2d);
-                CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(100 + g), 0));
+                CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(EvDecIn, g), 0));
                 decode_units(S, ua, ub, true, s);
                 phase_mark("dec", s);
                 const uint64_t o_lo = lower((uint64_t)ua * kBlockSymbols);
@@ -836,8 +839,8 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                 const int planes_done = ub == units ? n0 : (int)std::min<int64_t>(n0, (ub * kBlockSymbols) / plane);
                 const int c_ready = ready(planes_done);
                 if (c_ready > c_done) {
-                    CUDA_CHECK(cudaEventRecord(ctx->event(140 + g), s));
-                    CUDA_CHECK(cudaStreamWaitEvent(ctx->aux, ctx->event(140 + g), 0));
+                    CUDA_CHECK(cudaEventRecord(ctx->event(EvDecCorr, g), s));
+                    CUDA_CHECK(cudaStreamWaitEvent(ctx->aux, ctx->event(EvDecCorr, g), 0));
                     fused_pass1_recompose(p, 0, coef, Z0f, ctx->aux, c_done, c_ready);
                     fused_pass2(p, 0, Z0f, T0f, ctx->aux, c_done, c_ready);
                     phase_mark("corr", ctx->aux);

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <sched.h>
 #include <sys/mman.h>
 
 #include <condition_variable>
@@ -112,7 +113,16 @@ MemKind classify(const void *p) {
         cudaGetLastError();
         return MemKind::Host;
     }
-    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return MemKind::Device;
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+        // every entry point runs with the context's device current: a buffer of another GPU
+        // would be read / written through the wrong device's kernels
+        int cur = -1;
+        if (a.type == cudaMemoryTypeDevice && cudaGetDevice(&cur) == cudaSuccess && a.device != cur)
+            throw Error{HPDR_ERR_VALIDATION,
+                        "device buffer is on GPU " + std::to_string(a.device) + " but the context is on GPU " +
+                            std::to_string(cur), -1};
+        return MemKind::Device;
+    }
     if (a.type == cudaMemoryTypeHost) return MemKind::Pinned;
     return MemKind::Host;
 }
@@ -161,8 +171,19 @@ void zero_async(void *dst, size_t bytes, cudaStream_t s) {
 namespace {
 constexpr size_t kStageChunk = 16u << 20;
 constexpr unsigned kStageSlots = 4;
+// Host copy threads of this process: HPDR_COPY_THREADS, else the CPUs this process may run on
+// (its affinity mask -- a rank bound to its GPU's NUMA node sees that node's CPUs) divided among
+// the ranks sharing them (HPDR_RANKS_PER_NUMA, set by numa.bind_to_gpu), at most 16.
 int host_threads() {
-    static const int t = std::max(1, std::min(16, (int)std::thread::hardware_concurrency()));
+    static const int t = [] {
+        if (const char *e = getenv("HPDR_COPY_THREADS")) return std::max(1, std::min(64, atoi(e)));
+        int cpus = (int)std::thread::hardware_concurrency();
+        cpu_set_t set;
+        if (sched_getaffinity(0, sizeof(set), &set) == 0) cpus = CPU_COUNT(&set);
+        int share = 1;
+        if (const char *e = getenv("HPDR_RANKS_PER_NUMA")) share = std::max(1, atoi(e));
+        return std::max(1, std::min(16, cpus / share));
+    }();
     return t;
 }
 }  // namespace
@@ -240,7 +261,7 @@ void stage_h2d(hpdr_ctx *ctx, void *dst, const void *src, size_t n, cudaStream_t
     char *ring = (char *)ctx->hbuf("stage_in", kStageChunk * kStageSlots);
     for (size_t off = 0; off < n; off += kStageChunk) {
         const unsigned slot = ctx->stage_next++ % kStageSlots;
-        cudaEvent_t ev = ctx->event(500 + slot);
+        cudaEvent_t ev = ctx->event(EvStageIn, slot);
         CUDA_CHECK(cudaEventSynchronize(ev));   // the slot's previous DMA has read it
         const size_t m = std::min(kStageChunk, n - off);
         parallel_memcpy(ring + slot * kStageChunk, (const char *)src + off, m);
@@ -263,13 +284,19 @@ void stage_d2h(hpdr_ctx *ctx, void *dst, const void *src, size_t n, cudaStream_t
             const size_t off = issued * kStageChunk, m = std::min(kStageChunk, n - off);
             const unsigned slot = (unsigned)(issued % kStageSlots);
             CUDA_CHECK(cudaMemcpyAsync(ring + slot * kStageChunk, (const char *)src + off, m, cudaMemcpyDeviceToHost, st));
-            CUDA_CHECK(cudaEventRecord(ctx->event(504 + slot), st));
+            CUDA_CHECK(cudaEventRecord(ctx->event(EvStageOut, slot), st));
         }
         const unsigned slot = (unsigned)(done % kStageSlots);
-        CUDA_CHECK(cudaEventSynchronize(ctx->event(504 + slot)));
+        CUDA_CHECK(cudaEventSynchronize(ctx->event(EvStageOut, slot)));
         const size_t off = done * kStageChunk;
         parallel_memcpy((char *)dst + off, ring + slot * kStageChunk, std::min(kStageChunk, n - off));
     }
+}
+
+void apply_range_hook(hpdr_ctx *ctx, double *vmin, double *vmax) {
+    if (!ctx->range_hook) return;
+    if (ctx->range_hook(ctx->range_user, vmin, vmax) != 0)
+        throw Error{HPDR_ERR_VALIDATION, "range hook failed", -1};
 }
 
 void store_u64(void *dst, uint64_t v, cudaStream_t s) {
@@ -356,13 +383,14 @@ hpdr_ctx *hpdr_ctx::queue(int q) {
     return queues[q - 1];
 }
 
-cudaEvent_t hpdr_ctx::event(size_t i) {
-    while (events.size() <= i) {
+cudaEvent_t hpdr_ctx::event(EvNs ns, size_t i) {
+    std::vector<cudaEvent_t> &v = events[ns];
+    while (v.size() <= i) {
         cudaEvent_t e;
         CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        events.push_back(e);
+        v.push_back(e);
     }
-    return events[i];
+    return v[i];
 }
 
 namespace {
@@ -581,7 +609,8 @@ void hpdr_ctx_destroy(hpdr_ctx *c) {
     c->queues.clear();
     hpdr_ctx_trim(c);
     for (auto &kv : c->plans) cudaFree(kv.second->dbuf);
-    for (cudaEvent_t e : c->events) cudaEventDestroy(e);
+    for (auto &v : c->events)
+        for (cudaEvent_t e : v) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->h2d);
     cudaStreamDestroy(c->d2h);
@@ -597,6 +626,12 @@ uint64_t hpdr_ctx_alloc_events(const hpdr_ctx *c) {
     return n;
 }
 int hpdr_ctx_device(const hpdr_ctx *c) { return c ? c->device : -1; }
+
+void hpdr_ctx_set_range_hook(hpdr_ctx *c, hpdr_range_hook hook, void *user) {
+    if (!c) return;
+    c->range_hook = hook;
+    c->range_user = user;
+}
 
 void hpdr_host_copy(void *dst, const void *src, uint64_t n) { hpdr::parallel_memcpy(dst, src, n); }
 

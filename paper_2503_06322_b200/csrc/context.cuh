@@ -68,6 +68,26 @@ struct Buffer {
 
 struct hpdr_ctx_impl;
 
+// Event families: each purpose indexes its own pool, so a per-slab / per-chunk index can never
+// alias another family's event (e.g. a 600-slab decompress vs the staging ring's slots).
+enum EvNs : int {
+    EvFixed = 0,    // single-purpose events, small fixed ids
+    EvChunkIn,      // streamed decompose: H2D of input chunk k landed
+    EvSlabOut,      // recompose: output slab k written (its D2H may start)
+    EvStageIn,      // pinned H2D staging ring slot
+    EvStageOut,     // pinned D2H staging ring slot
+    EvEncGroup,     // Huffman encode unit group g packed
+    EvDecIn,        // streamed decode: payload group g landed
+    EvDecCorr,      // streamed decode: group g decoded (finest correction may proceed)
+    EvLevel,        // recompose: correction of level l computed on a side stream
+    EvPipeCoef,     // pipeline: chunk k's coefficients ready
+    EvZfpIn,        // fixed-rate host path: input slab k landed
+    EvZfpOut,       // fixed-rate host path: slab k coded
+    EvZfpDecIn,     // fixed-rate decode host path: stream slab k landed
+    EvZfpDecOut,    // fixed-rate decode host path: output slab k written
+    EvNsCount
+};
+
 }  // namespace hpdr
 
 struct hpdr_ctx {
@@ -78,6 +98,8 @@ struct hpdr_ctx {
     cudaStream_t aux = nullptr;       // side compute (work independent of the level chain)
     cudaStream_t side[4] = {};        // more side streams (independent per-level corrections)
     uint64_t alloc_events = 0;
+    hpdr_range_hook range_hook = nullptr;   // job-wide range exchange (hpdr_ctx_set_range_hook)
+    void *range_user = nullptr;
     std::map<std::string, hpdr::Buffer> dev;      // named device buffers (grow-only)
     std::map<std::string, hpdr::Buffer> pinned;   // named pinned host buffers (grow-only)
     std::map<std::vector<uint64_t>, std::unique_ptr<hpdr::DevPlan>> plans;
@@ -108,12 +130,13 @@ struct hpdr_ctx {
     std::string oname(const char *base, int slot) const { return slot ? std::string(base) + "#1" : std::string(base); }
     std::string oname(const char *base) const { return oname(base, out_slot); }
 
-    std::vector<cudaEvent_t> events;   // reusable sync events (no timing)
+    std::vector<cudaEvent_t> events[hpdr::EvNsCount];   // reusable sync events (no timing), per family
     // Extra queue contexts of the streams pipeline (paper Fig. 7's queues): each has its own
     // streams, buffers and plan cache, and is driven by its own host thread.  Owned.
     std::vector<hpdr_ctx *> queues;
     hpdr_ctx *queue(int q);   // q = 0: this context
-    cudaEvent_t event(size_t i);
+    cudaEvent_t event(hpdr::EvNs ns, size_t i);
+    cudaEvent_t event(size_t i) { return event(hpdr::EvFixed, i); }
 
     void *dbuf(const std::string &name, size_t bytes);
     void *hbuf(const std::string &name, size_t bytes);
@@ -144,5 +167,7 @@ void stage_h2d(hpdr_ctx *ctx, void *dst, const void *src, size_t n, cudaStream_t
 void stage_d2h(hpdr_ctx *ctx, void *dst, const void *src, size_t n, cudaStream_t st);
 // Store one 8-byte value to device memory in stream order (a kernel parameter, no staging copy).
 void store_u64(void *dst, uint64_t v, cudaStream_t s);
+// Relative mode: pass this block's min / max through the context's range hook (if any).
+void apply_range_hook(hpdr_ctx *ctx, double *vmin, double *vmax);
 void copy_from_device(hpdr_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t s);
 }  // namespace hpdr

@@ -40,19 +40,21 @@ int zfp_container_decompress(hpdr_ctx *ctx, const uint8_t *c, uint64_t len, void
 
 namespace {
 
-uint32_t crc32(const uint8_t *p, size_t n) {   // zlib polynomial, as container.py's zlib.crc32
-    static uint32_t table[256];
-    static bool init = false;
-    if (!init) {
+struct CrcTable {
+    uint32_t t[256];
+    CrcTable() {
         for (uint32_t i = 0; i < 256; i++) {
             uint32_t c = i;
             for (int k = 0; k < 8; k++) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
-            table[i] = c;
+            t[i] = c;
         }
-        init = true;
     }
+};
+
+uint32_t crc32(const uint8_t *p, size_t n) {   // zlib polynomial, as container.py's zlib.crc32
+    static const CrcTable table;                // thread-safe one-time initialisation
     uint32_t c = 0xFFFFFFFFu;
-    for (size_t i = 0; i < n; i++) c = table[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+    for (size_t i = 0; i < n; i++) c = table.t[(c ^ p[i]) & 0xFF] ^ (c >> 8);
     return c ^ 0xFFFFFFFFu;
 }
 
@@ -308,7 +310,7 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
                     stage_h2d(c, din, (const char *)host_in + chunks[k].raw_off * isz, chunks[k].raw_size * isz, c->h2d);
                 else
                     CUDA_CHECK(cudaMemcpyAsync(din, (const char *)host_in + chunks[k].raw_off * isz,
-                                               chunks[k].raw_size * isz, cudaMemcpyHostToDevice, c->h2d));
+                                               chunks[k].raw_size * isz, cudaMemcpyDefault, c->h2d));
                 tm.mark(6 * k + 1, c->h2d);
                 minmax_accumulate(din, dtype, (int64_t)chunks[k].raw_size, mm, c->h2d);
                 CUDA_CHECK(cudaEventRecord(ev_in, c->h2d));
@@ -318,7 +320,7 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
                 for (int d = 1; d < rank; d++) sd[d] = dims[d];
                 decompose_chunk(c, din, dtype, rank, sd, coef_all + chunks[k].raw_off, nullptr);
                 CUDA_CHECK(cudaEventRecord(ev_red, c->stream));
-                CUDA_CHECK(cudaEventRecord(c->event(320 + k), c->stream));   // chunk k's coefficients
+                CUDA_CHECK(cudaEventRecord(c->event(EvPipeCoef, k), c->stream));   // chunk k's coefficients
                 first = false;
             }
             CUDA_CHECK(cudaMemcpyAsync(hmm, mm, 24, cudaMemcpyDeviceToHost, c->h2d));
@@ -386,14 +388,14 @@ int hpdr_pipeline_compress(hpdr_ctx *ctx, const void *host_in, int dtype, int ra
                                   c->h2d);
                     else
                         CUDA_CHECK(cudaMemcpyAsync(din, (const char *)host_in + chunks[k].raw_off * isz,
-                                                   chunks[k].raw_size * isz, cudaMemcpyHostToDevice, c->h2d));
+                                                   chunks[k].raw_size * isz, cudaMemcpyDefault, c->h2d));
                     tm.mark(6 * k + 1, c->h2d);
                     CUDA_CHECK(cudaEventRecord(ev_in, c->h2d));
                     CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_in, 0));
                 }
                 if (t >= 2) CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_out, 0));   // output set reuse edge (k - 2Q)
                 if (two_phase)   // chunk k decomposed by phase-A queue k mod QA
-                    CUDA_CHECK(cudaStreamWaitEvent(c->stream, qc[k % QA]->event(320 + k), 0));
+                    CUDA_CHECK(cudaStreamWaitEvent(c->stream, qc[k % QA]->event(EvPipeCoef, k), 0));
                 if (!two_phase) tm.mark(6 * k + 2, c->stream);
                 uint64_t sd[4] = {chunks[k].raw_size / plane, 0, 0, 0};
                 for (int d = 1; d < rank; d++) sd[d] = dims[d];
@@ -534,7 +536,7 @@ int hpdr_pipeline_decompress(hpdr_ctx *ctx, const void *container, uint64_t len,
                     stage_h2d(x, dblob, c + base + chunks[k].pay_off, chunks[k].pay_size, x->h2d);
                 else
                     CUDA_CHECK(cudaMemcpyAsync(dblob, c + base + chunks[k].pay_off, chunks[k].pay_size,
-                                               cudaMemcpyHostToDevice, x->h2d));
+                                               cudaMemcpyDefault, x->h2d));
                 tm.mark(6 * k + 1, x->h2d);
                 CUDA_CHECK(cudaEventRecord(ev_in, x->h2d));
                 CUDA_CHECK(cudaStreamWaitEvent(x->stream, ev_in, 0));

@@ -1028,13 +1028,13 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
                       ctx->h2d);
         else
             CUDA_CHECK(cudaMemcpyAsync(d_in + a * plane_bytes, (const char *)host_in + a * plane_bytes,
-                                       (e - a) * plane_bytes, cudaMemcpyHostToDevice, ctx->h2d));
-        CUDA_CHECK(cudaEventRecord(ctx->event(1 + k), ctx->h2d));
+                                       (e - a) * plane_bytes, cudaMemcpyDefault, ctx->h2d));
+        CUDA_CHECK(cudaEventRecord(ctx->event(EvChunkIn, k), ctx->h2d));
     };
     issue(0);
     int c_done = 0;
     for (int k = 0; k < K; k++) {
-        CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(1 + k), 0));
+        CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(EvChunkIn, k), 0));
         const int64_t a = (int64_t)k * chunk, e = std::min<int64_t>(n0, a + chunk);
         if (!has_range) {
             const int64_t cnt = (e - a) * plane_elems;
@@ -1068,6 +1068,7 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
         };
         *u_min = h[2] ? __builtin_nan("") : val(h[0]);
         *u_max = h[2] ? __builtin_nan("") : val(h[1]);
+        apply_range_hook(ctx, u_min, u_max);   // job-wide range of a block-partitioned field
         const double eb_abs = eb_rel * (*u_max - *u_min);
         q.bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
         // the fine coefficients are final: quantize them on the side stream while the level chain
@@ -1291,8 +1292,8 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
             fused_pass2(p, st_i, Zl, T, x);
             thomas_all(p, st_i, T, x);
             Tl[st_i] = T;
-            ev_l[st_i] = 200 + st_i;
-            CUDA_CHECK(cudaEventRecord(ctx->event(200 + st_i), x));
+            ev_l[st_i] = st_i;
+            CUDA_CHECK(cudaEventRecord(ctx->event(EvLevel, st_i), x));
         }
     }
     for (int st_i = L - 2; st_i >= 0; st_i--) {
@@ -1304,7 +1305,7 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
             CUDA_CHECK(cudaStreamWaitEvent(s, ev_side, 0));
         } else if (Tl[st_i]) {
             T = Tl[st_i];
-            CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(ev_l[st_i]), 0));
+            CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(EvLevel, ev_l[st_i]), 0));
         } else {
             fused_pass1_recompose(p, st_i, coef, Z0, s);
             fused_pass2(p, st_i, Z0, b.t0, s);
@@ -1332,11 +1333,11 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
             for (int a = 0, k = 0; a < n0; a += chunk, k++, nslab++) {
                 const int e = std::min(n0, a + chunk);
                 fused_final(p, 0, b.cg, coef, out, out_dtype, s, a, e);
-                CUDA_CHECK(cudaEventRecord(ctx->event(1 + k), s));
+                CUDA_CHECK(cudaEventRecord(ctx->event(EvSlabOut, k), s));
             }
             for (int a = 0, k = 0; k < nslab; a += chunk, k++) {
                 const int e = std::min(n0, a + chunk);
-                CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(1 + k), 0));
+                CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(EvSlabOut, k), 0));
                 if (pageable_out)
                     stage_d2h(ctx, (char *)host_out + a * plane_bytes, (const char *)out + a * plane_bytes,
                               (e - a) * plane_bytes, ctx->d2h);

@@ -835,15 +835,15 @@ int hpdr_zfp_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, const 
                                                    (need - in_done) * plane_bytes, cudaMemcpyHostToDevice, ctx->h2d));
                     in_done = need;
                 }
-                CUDA_CHECK(cudaEventRecord(ctx->event(400 + k), ctx->h2d));
-                CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(400 + k), 0));
+                CUDA_CHECK(cudaEventRecord(ctx->event(EvZfpIn, k), ctx->h2d));
+                CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(EvZfpIn, k), 0));
             }
             encode_range(z, din, lo, hi, pay + (uint64_t)lo * z.w / 32, bad, s);
             // stream bytes [lo*w/8, hi*w/8) are final (lo, hi multiples of 32 blocks, or the end)
             const uint64_t a = (uint64_t)lo * z.w / 8;
             const uint64_t e = k == K - 1 ? z.payload : (uint64_t)hi * z.w / 8;
-            CUDA_CHECK(cudaEventRecord(ctx->event(420 + k), s));
-            CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(420 + k), 0));
+            CUDA_CHECK(cudaEventRecord(ctx->event(EvZfpOut, k), s));
+            CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(EvZfpOut, k), 0));
             if (out_dev)
                 CUDA_CHECK(cudaMemcpyAsync(o + hl + a, (uint8_t *)pay + a, e - a, cudaMemcpyDeviceToDevice, ctx->d2h));
             else
@@ -899,19 +899,19 @@ int hpdr_zfp_decompress(hpdr_ctx *ctx, const void *stream, uint64_t len, void *o
                                                ctx->h2d));
                 pay_in = need;
             }
-            CUDA_CHECK(cudaEventRecord(ctx->event(440 + k), ctx->h2d));
-            CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(440 + k), 0));
+            CUDA_CHECK(cudaEventRecord(ctx->event(EvZfpDecIn, k), ctx->h2d));
+            CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(EvZfpDecIn, k), 0));
             decode_range(z, pay + (uint64_t)lo * z.w / 32, lo, hi, dout, s);
             if (out_dev) continue;
             // output planes whose block rows are complete
             const uint64_t rows = k == K - 1 ? (uint64_t)z.G.n[0]
                                              : std::min<uint64_t>((uint64_t)z.G.n[0], (uint64_t)(hi / z.blocks_per_plane) * 4);
             if (rows > rows_out) {
-                CUDA_CHECK(cudaEventRecord(ctx->event(460 + k), s));
+                CUDA_CHECK(cudaEventRecord(ctx->event(EvZfpDecOut, k), s));
                 if (out_pageable) {
                     outs.push_back({rows_out, rows, (uint64_t)k});   // copied out below, after every slab is queued
                 } else {
-                    CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(460 + k), 0));
+                    CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(EvZfpDecOut, k), 0));
                     CUDA_CHECK(cudaMemcpyAsync((uint8_t *)out + rows_out * plane_elems * isz,
                                                (uint8_t *)dout + rows_out * plane_elems * isz,
                                                (rows - rows_out) * plane_elems * isz, cudaMemcpyDeviceToHost, ctx->d2h));
@@ -920,7 +920,7 @@ int hpdr_zfp_decompress(hpdr_ctx *ctx, const void *stream, uint64_t len, void *o
             }
         }
         for (const auto &r : outs) {   // pageable output: pinned staging ring, host-blocking
-            CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(460 + (int)r[2]), 0));
+            CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(EvZfpDecOut, (size_t)r[2]), 0));
             stage_d2h(ctx, (uint8_t *)out + r[0] * plane_elems * isz, (uint8_t *)dout + r[0] * plane_elems * isz,
                       (r[1] - r[0]) * plane_elems * isz, ctx->d2h);
         }

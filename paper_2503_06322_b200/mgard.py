@@ -62,7 +62,11 @@ class QuantizedSet:
 # ----------------------------------------------------------------------------- helpers
 def _native(cache: ContextCache | None, key: ContextKey | None, device: int | None, obj=None):
     if cache is not None and key is not None:
-        return cache.acquire(key).native
+        # a CUDA tensor argument runs on its own GPU; otherwise device=, else the cache's device
+        dev = device
+        if dev is None and getattr(getattr(obj, "device", None), "type", None) == "cuda":
+            dev = _lib.default_device(obj)
+        return cache.acquire(key, device=dev).native
     return _lib.default_context(device, obj)
 
 
@@ -149,7 +153,9 @@ def blob_info(data) -> tuple:
 def mgard_decompress(data, adapter=None, cache: ContextCache | None = None, *, device: int | None = None,
                      out=None) -> TensorData:
     """Decode, dequantize and recompose on the GPU (codec.py:59-113).  ``data`` may also be a
-    CUDA uint8 tensor (a device-resident blob, read in place)."""
+    CUDA uint8 tensor (a device-resident blob, read in place) or a host uint8 tensor."""
+    if hasattr(data, "numpy") and hasattr(data, "data_ptr") and not getattr(data, "is_cuda", False):
+        data = data.numpy()   # host torch tensor (pinned or not): a zero-copy numpy view
     if getattr(data, "is_cuda", False):
         addr, size = int(data.data_ptr()), int(data.numel() * data.element_size())
         buf = data[: min(size, 128)].cpu().numpy().view(np.uint8)   # header only
@@ -164,7 +170,7 @@ def mgard_decompress(data, adapter=None, cache: ContextCache | None = None, *, d
         eb_rel = float(np.frombuffer(buf[hdr + 1:hdr + 9].tobytes(), "<f8")[0]) if buf.size >= hdr + 13 else 0.0
         dsz = int(np.frombuffer(buf[hdr + 9:hdr + 13].tobytes(), "<u4")[0]) if buf.size >= hdr + 13 else 0
         key = ContextKey.make("mgard", dims, DTYPE_FROM_CODE[code].value, eb_rel=eb_rel, dict_size=dsz)
-        ctx = cache.acquire(key).native
+        ctx = _native(cache, key, device, data if getattr(data, "is_cuda", False) else out)
     dt = DTYPE_FROM_CODE.get(code, DType.F64)
     n_elem = int(np.prod(dims)) if dims and 1 <= rank <= 4 else 0
     if out is None:

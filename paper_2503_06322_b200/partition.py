@@ -14,6 +14,8 @@ exercised on CPU (gloo) with the parity oracle; the defaults are the GPU path.
 """
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 
 from .container import ChunkEntry, ContainerHeader, read_container, slab_bounds, write_container
@@ -79,21 +81,108 @@ def decompress_slabs(data, decompressor=None) -> np.ndarray:
     return out
 
 
+_HOOK_T = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double))
+
+
+def _collective_device(group):
+    import torch
+    import torch.distributed as dist
+
+    if dist.is_initialized() and dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def allreduce_range(lo: float, hi: float, group=None) -> tuple:
+    """Job-wide (min, max): one all-reduce of (-min, max), 16 bytes."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return float(lo), float(hi)
+    t = torch.tensor([-lo, hi], dtype=torch.float64, device=_collective_device(group))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return -float(t[0]), float(t[1])
+
+
+class RangeExchange:
+    """Installs the job-wide min/max all-reduce as a device context's range hook
+    (hpdr_ctx_set_range_hook) for the duration of a ``with`` block.
+
+    A relative-mode ``mgard_compress`` of this rank's block then calls the all-reduce from inside
+    the library as soon as the block's own min / max are known -- for a streamed host input that
+    is after the last chunk has landed and been decomposed -- and quantizes with the job-wide
+    range: the blob equals ``mgard_compress(block, eb_rel, value_range=global)`` and the exchange
+    costs no extra pass over the field.  ``last`` holds the range of the latest call."""
+
+    def __init__(self, ctx=None, group=None):
+        from . import _lib
+
+        self.ctx = ctx if ctx is not None else _lib.default_context()
+        self.group = group
+        self.last = None
+        self.error = None
+        self._cb = _HOOK_T(self._hook)
+
+    def _hook(self, _user, pmin, pmax):
+        try:
+            self.last = allreduce_range(pmin[0], pmax[0], self.group)
+            pmin[0], pmax[0] = self.last
+            return 0
+        except Exception as e:   # noqa: BLE001 - reported as a ValidationError by the library
+            self.error = e
+            return 1
+
+    def __enter__(self):
+        from . import _lib
+
+        _lib.lib().hpdr_ctx_set_range_hook(self.ctx.handle, C.cast(self._cb, C.c_void_p), None)
+        return self
+
+    def __exit__(self, *exc):
+        from . import _lib
+
+        _lib.lib().hpdr_ctx_set_range_hook(self.ctx.handle, None, None)
+        return False
+
+
 def distributed_compress(block: np.ndarray, eb_rel: float, group=None, dict_size: int = 4096, value_range=None,
-                         compressor=None, minmax=None):
+                         compressor=None, minmax=None, *, out=None):
     """Compress this rank's dim-0 block with the job-wide range.
 
-    Returns (blob, sizes of every rank's blob, (vmin, vmax)).  Collectives: one all-reduce of
-    two doubles (skipped when value_range is given) and one all-gather of one int64.
+    Returns (blob, sizes of every rank's blob, (vmin, vmax)); with ``out`` (a pinned / device
+    buffer) the blob is written there and its length stands in for it.  Collectives: one
+    all-reduce of two doubles (skipped when value_range is given) and one all-gather of one
+    int64.  With the default (GPU) compressor the all-reduce runs inside the compress call
+    (RangeExchange), overlapped with the block's transfer and decomposition.
     """
     import torch
     import torch.distributed as dist
 
-    compressor = compressor or _default_compressor
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    dev = torch.device("cpu")
-    if dist.is_initialized() and dist.get_backend(group) == "nccl":
-        dev = torch.device("cuda", torch.cuda.current_device())
+    dev = _collective_device(group)
+    if compressor is None and minmax is None and value_range is None:
+        from . import _lib
+        from .mgard import mgard_compress
+
+        ctx = _lib.default_context(None, block if getattr(block, "is_cuda", False) else out)
+        with RangeExchange(ctx, group) as rx:
+            try:
+                blob = mgard_compress(block, eb_rel, dict_size, out=out)
+            except ValidationError:
+                if rx.error is not None:
+                    raise rx.error
+                raise
+        value_range = rx.last if rx.last is not None else value_range
+        n = blob if out is not None else len(blob)
+        sizes = [int(n)]
+        if world > 1:
+            t = torch.tensor([int(n)], dtype=torch.int64, device=dev)
+            g = [torch.zeros_like(t) for _ in range(world)]
+            dist.all_gather(g, t, group=group)
+            sizes = [int(x.item()) for x in g]
+        return blob, sizes, value_range
+    compressor = compressor or _default_compressor
     if value_range is None:
         lo, hi = (minmax or _default_minmax)(block)
         if world > 1:

@@ -124,6 +124,15 @@ def adaptive_schedule(n0: int, plane_bytes: int, model: ThroughputModel, transpo
     return planes
 
 
+def _host_view(arr) -> np.ndarray:
+    """A numpy view (or, for a CUDA tensor, a host copy) of an input array."""
+    if hasattr(arr, "numpy"):
+        return arr.cpu().numpy() if getattr(arr, "is_cuda", False) else arr.numpy()
+    if hasattr(arr, "values") and hasattr(arr, "dims"):   # TensorData
+        return np.asarray(arr.values)
+    return np.asarray(arr)
+
+
 def profile_models(arr, eb_rel: float, sizes_mb=(16, 32, 64, 128, 256), *, device: int | None = None,
                    reps: int = 2):
     """Fit Φ and Θ on this device (§V-C): Φ(C) = compress throughput of a device-resident
@@ -134,7 +143,7 @@ def profile_models(arr, eb_rel: float, sizes_mb=(16, 32, 64, 128, 256), *, devic
     from .mgard import _as_input, mgard_compress
 
     addr, dims, code, keep = _as_input(arr)
-    a = np.asarray(arr) if not hasattr(arr, "numpy") else arr.numpy()
+    a = _host_view(arr)
     plane_bytes = a[0].nbytes
     ctx = _lib.default_context(device, arr if getattr(arr, 'is_cuda', False) else None)
     samples = []
@@ -174,7 +183,7 @@ def compress_adaptive(arr, eb_rel: float, dict_size: int = 4096, value_range=Non
                       trace: bool = False):
     """Algorithm 4 end to end: chunk sizes from the fitted Φ / Θ (profile_models, or `models`),
     then the streams pipeline over that schedule.  Returns what compress_pipelined returns."""
-    a = np.asarray(arr) if not hasattr(arr, "numpy") else arr.numpy()
+    a = _host_view(arr)
     if models is None:
         phi, theta, _ = profile_models(arr, eb_rel, device=device)
     else:
@@ -214,7 +223,7 @@ def compress_pipelined(arr, eb_rel: float, dict_size: int = 4096, value_range=No
 
     addr, dims, code, keep = _as_input(arr)
     dims = _dims_ok(dims)
-    ctx = _lib.default_context(device)
+    ctx = _lib.default_context(device, arr if getattr(arr, "is_cuda", False) else out)
     has = value_range is not None
     r0, r1 = (float(value_range[0]), float(value_range[1])) if has else (0.0, 0.0)
     lst = None if chunks is None else np.ascontiguousarray(chunks, dtype=np.uint64)
@@ -256,7 +265,7 @@ def decompress_pipelined(data, *, device: int | None = None, out=None, trace: bo
     h, _ = read_container(buf)
     res = np.empty(h.dims, DTYPE_FROM_CODE[h.dtype].np_dtype) if out is None else out
     tr = np.zeros(6 * max(1, len(h.chunks)), np.float64) if trace else None
-    ctx = _lib.default_context(device)
+    ctx = _lib.default_context(device, data if getattr(data, "is_cuda", False) else out)
     check(lib().hpdr_pipeline_decompress(ctx.handle, C.c_void_p(buf.ctypes.data), buf.size,
                                          C.c_void_p(_lib.ptr(res)), int(res.nbytes),
                                          C.c_void_p(tr.ctypes.data) if tr is not None else None))

@@ -60,15 +60,26 @@ def grf(shape, m: int = 8, seed: int = 0, dtype=np.float32) -> np.ndarray:
     return out.astype(dtype)
 
 
-def smooth_noise(shape, seed: int = 0, noise: float = 1e-3, dtype=np.float32) -> np.ndarray:
+def smooth_noise(shape, seed: int = 0, noise: float = 1e-3, dtype=np.float32, planes=None) -> np.ndarray:
     """f = 4x(1-x)(1-2y)^2 + 4z(1-z)(2z-1) + noise*(2u-1) on the unit cube
-    (the last three axes; leading axes repeat the pattern)."""
+    (the last three axes; leading axes repeat the pattern).
+
+    ``planes=(lo, hi)`` (3-D only) returns exactly ``smooth_noise(shape)[lo:hi]`` without
+    generating the rest: the uniform stream is advanced past the first lo planes' draws (one
+    64-bit draw per value), so a rank can build its own dim-0 block of a field that does not fit
+    one host (C4 / C5 block partitions)."""
     orig = tuple(int(s) for s in shape)
     shape = orig
     while len(shape) < 3:
         shape = (1,) + shape
-    lead = shape[:-3]
     n0, n1, n2 = shape[-3:]
+    lo, hi = 0, n0
+    if planes is not None:
+        if len(orig) != 3:
+            raise ValueError("planes= needs a 3-D shape")
+        lo, hi = int(planes[0]), int(planes[1])
+        if not 0 <= lo <= hi <= n0:
+            raise ValueError("planes out of range")
 
     def coord(n):
         return np.arange(n, dtype=np.float64) / float(max(n - 1, 1))
@@ -78,12 +89,14 @@ def smooth_noise(shape, seed: int = 0, noise: float = 1e-3, dtype=np.float32) ->
     qy = (1.0 - 2.0 * y) * (1.0 - 2.0 * y)
     rz = 4.0 * z * (1.0 - z) * (2.0 * z - 1.0)
     rng = np.random.default_rng(seed)
-    out = np.empty(shape, dtype=dtype)
-    flat = out.reshape((-1, n0, n1, n2))
+    if lo:
+        rng.bit_generator.advance(lo * n1 * n2)
+    out = np.empty(shape[:-3] + (hi - lo, n1, n2), dtype=dtype)
+    flat = out.reshape((-1, hi - lo, n1, n2))
     slab = max(1, (1 << 24) // max(1, n1 * n2))   # consecutive draws: same stream as one call
     for i in range(flat.shape[0]):
-        for a in range(0, n0, slab):
-            b = min(n0, a + slab)
+        for a in range(lo, hi, slab):
+            b = min(hi, a + slab)
             f = px[a:b, None, None] * qy[None, :, None]
             f = f + rz[None, None, :]
             u = rng.random((b - a, n1, n2))
@@ -91,8 +104,8 @@ def smooth_noise(shape, seed: int = 0, noise: float = 1e-3, dtype=np.float32) ->
             u -= 1.0
             u *= noise
             f += u
-            flat[i, a:b] = f
-    return out.reshape(orig)
+            flat[i, a - lo:b - lo] = f
+    return out.reshape(orig if planes is None else (hi - lo, n1, n2))
 
 
 def _e(x: np.ndarray) -> np.ndarray:
