@@ -15,90 +15,14 @@
 // a cp.async shared-memory ring several steps ahead of the arithmetic (the dependency chain of
 // the march never waits on DRAM).  Every value is produced with the reference's operation
 // order (explicit _rn intrinsics): results are bit-identical to numpy.
-#include "fused.cuh"
+#include "level_dev.cuh"
 
 namespace hpdr {
 
 namespace {
 
-__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double lerp(double va, double vb, double t) { return dadd(va, dmul(t, dsub(vb, va))); }
+using namespace lvl;
 
-
-// Histogram count of `key` (shared-memory bins flushed once per block).
-// (__match_any_sync aggregation measured slower here: 2.67 vs 1.73 ms for the level-0 pass)
-__device__ __forceinline__ void hist_add(uint32_t *sh, unsigned long long *g, bool sh_ok, uint32_t key) {
-    if (sh_ok) atomicAdd(&sh[key], 1u);
-    else atomicAdd(&g[key], 1ULL);
-}
-
-// The bin width: a launch parameter, or read from device memory (CUDA-graph replays).
-__device__ __forceinline__ double qbin(const QuantOut &q) { return q.bin_dev ? *q.bin_dev : q.bin; }
-
-// One fine node's quantization (quantize.py:73-84), in the double domain.  r = rint(mc / bin)
-// (IEEE division, half to even) is computed with one multiply by rb = RN(1/bin): the correctly
-// rounded quotient q and qa = RN(mc * rb) differ by < |q| 2^-51, so rint(qa) == rint(q) unless qa
-// lies within that distance of a half-integer -- then (and for |qa| >= 2^61) the IEEE division
-// decides; |mc / bin| >= 2^62 is the bin overflow.  Outlier iff |r| >= dict/2, key = zigzag(r)
-// (exact: non-outlier |r| < 2^15), histogram.
-__device__ __forceinline__ void quant_node(double mc, const QuantOut &q, double rbin, int64_t f, int &fl,
-                                           uint32_t *sh_hist, bool sh_ok) {
-    double r = 0.0;
-    if (!isfinite(mc)) {
-        fl |= 1;
-    } else {
-        const double qa = dmul(mc, rbin);
-        r = rint(qa);
-        const double dist = 0.5 - fabs(dsub(qa, r));
-        if (!(dist > fabs(qa) * 0x1p-49 && fabs(qa) < 0x1p61)) {
-            const double sc = mc / qbin(q);
-            if (fabs(sc) >= 4611686018427387904.0) {
-                fl |= 2;
-                r = 0.0;
-            } else {
-                r = rint(sc);
-            }
-        }
-    }
-    uint32_t key = 0;
-    if (fabs(r) >= (double)q.half) {   // outlier (:80-83)
-        q.obins[f] = (long long)r;
-        atomicOr(&q.omask[f >> 5], 1u << (f & 31));
-    } else {
-        key = (uint32_t)(r >= 0.0 ? 2.0 * r : -2.0 * r - 1.0);   // zigzag (quantize.py:24-31)
-    }
-    q.keys[f] = key;
-    hist_add(sh_hist, q.hist, sh_ok, key);
-}
-
-// Per-thread description of one axis at a fine index j: coarse neighbours (fine indices fa/fb,
-// coarse indices ca/cb), weight t and whether j is a fine-only node along this axis.
-struct Nb {
-    int fa, fb, ca, cb;
-    double t;
-    bool fo;
-};
-
-template <bool A>
-__device__ __forceinline__ Nb neighbours(const DevAxis &ax, int j) {
-    Nb r;
-    if (!A) {
-        r.fa = r.fb = r.ca = r.cb = j;
-        r.t = 0.0;
-        r.fo = false;
-        return r;
-    }
-    const int b = __ldg(ax.pb + j);
-    r.fo = b >= 0;
-    r.ca = __ldg(ax.pa + j);
-    r.cb = r.fo ? b : r.ca;
-    r.fa = __ldg(ax.fa + j);
-    r.fb = __ldg(ax.fb + j);
-    r.t = r.fo ? __ldg(ax.pt + j) : 0.0;
-    return r;
-}
 
 // Sliding mass-multiply + restriction along the march axis (transform.py:206-226 then :181-203):
 //   y(j) = (md_j x_j + ml_j x_{j-1}) + mu_j x_{j+1}
@@ -196,27 +120,6 @@ __device__ __forceinline__ PiHead identity_head(int j) {
     return h;
 }
 
-__device__ __forceinline__ void slab_range(int nc, int nz, int z, int &lo, int &hi) {
-    const int base = nc / nz, rem = nc % nz;
-    lo = z * base + min(z, rem);
-    hi = lo + base + (z < rem ? 1 : 0);
-}
-
-// Fine-plane range a slab of coarse outputs [c_lo, c_hi) marches over / owns.
-template <bool A0>
-__device__ __forceinline__ void slab_planes(const DevAxis &ax0, int n0, int nc0, int c_lo, int c_hi, int &j_start,
-                                            int &j_end, int &own_lo, int &own_hi) {
-    if (A0) {
-        j_start = max(0, __ldg(ax0.r0 + c_lo) - 2);
-        j_end = min(n0 - 1, __ldg(ax0.r0 + c_hi - 1) + 2);
-        own_lo = c_lo == 0 ? 0 : __ldg(ax0.r0 + c_lo);
-        own_hi = c_hi == nc0 ? n0 : __ldg(ax0.r0 + c_hi);
-    } else {
-        j_start = own_lo = c_lo;
-        j_end = c_hi - 1;
-        own_hi = c_hi;
-    }
-}
 
 template <typename T>
 __device__ __forceinline__ void cp_elem(T *s, const T *g) {
@@ -1119,6 +1022,13 @@ void fused_pass1_decompose(const DevPlan &p, int st_i, const void *F, bool f32, 
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
     KPROF("k_level_pass1", frac * ((f32 ? 4.0 : 8.0) * nf + 8.0 * (nf - nc) + 8.0 * nc + 8.0 * z0_size(p, st_i)), s);
     const QuantOut q{};
+    if (v.act == 7 && quad_eligible(p, st_i)) {
+        if (f32) launch_pass1_quad<0, float>((const float *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
+                                             coef, Z0, Cg, q, c_lo, c_hi - c_lo, s);
+        else launch_pass1_quad<0, double>((const double *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
+                                          coef, Z0, Cg, q, c_lo, c_hi - c_lo, s);
+        return;
+    }
     if (f32) launch_pass1<0, float>(v.act, (const float *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
                                     coef, nullptr, Z0, Cg, q, c_lo, c_hi - c_lo, s);
     else launch_pass1<0, double>(v.act, (const double *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
@@ -1133,6 +1043,13 @@ void fused_pass1_quantize(const DevPlan &p, int st_i, const void *F, bool f32, c
     const double frac = (double)(c_hi - c_lo) / fused_out_planes(p, st_i);
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
     KPROF(st_i == 0 ? "k_level_pass1q" : "k_level_pass1q_coarse", frac * ((f32 ? 4.0 : 8.0) * nf + 4.0 * (nf - nc) + 8.0 * nc + 8.0 * z0_size(p, st_i)), s);
+    if (v.act == 7 && quad_eligible(p, st_i)) {
+        if (f32) launch_pass1_quad<2, float>((const float *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
+                                             nullptr, Z0, Cg, q, c_lo, c_hi - c_lo, s);
+        else launch_pass1_quad<2, double>((const double *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
+                                          nullptr, Z0, Cg, q, c_lo, c_hi - c_lo, s);
+        return;
+    }
     if (f32) launch_pass1<2, float>(v.act, (const float *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
                                     nullptr, nullptr, Z0, Cg, q, c_lo, c_hi - c_lo, s);
     else launch_pass1<2, double>(v.act, (const double *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,

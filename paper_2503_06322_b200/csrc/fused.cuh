@@ -26,6 +26,13 @@ struct QuantOut {
     int *flags;                   // bit0 non-finite, bit1 |c/bin| >= 2^62
 };
 
+// quad.cu: pass 1 with one 2 x 2 node quad per thread (regular all-active 3-D transitions).
+bool quad_eligible(const DevPlan &p, int st_i);
+template <int MODE, typename TIn>
+void launch_pass1_quad(const TIn *F, int n0, int n1, int n2, const DevAxis &a0, const DevAxis &a1, const DevAxis &a2,
+                       const LevelMap &lm, double *coef, double *Z0, double *Cg, const QuantOut &q, int c_base,
+                       int c_count, cudaStream_t s);
+
 // Decompose transition st_i writing keys instead of fp64 coefficients.
 void fused_pass1_quantize(const DevPlan &p, int st_i, const void *F, bool f32, const QuantOut &q, double *Z0,
                           double *Cg, cudaStream_t s, int c_lo = 0, int c_hi = -1);

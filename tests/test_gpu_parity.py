@@ -200,9 +200,14 @@ sys.path.insert(0, %r)
 import paper_2503_06322_b200 as P
 from oracle import oracle as O
 from paper_2503_06322_b200 import synthetic as S
-for shape in [(33, 34, 35), (16, 5, 7), (65, 40), (1000,), (12, 10, 9)]:
-    a = S.smooth_noise(shape, seed=3)
+import torch
+cases = [((33, 34, 35), np.float32), ((16, 5, 7), np.float32), ((65, 40), np.float32), ((1000,), np.float32),
+         ((12, 10, 9), np.float32), ((40, 36, 64), np.float32), ((67, 20, 34), np.float64), ((9, 48, 16), np.float64)]
+for shape, dt in cases:
+    a = S.smooth_noise(shape, seed=3, dtype=dt)
     for vr in (None, (-1.0, 2.0)):
+        bd = P.mgard_compress(torch.from_numpy(a).cuda(), 1e-3, value_range=vr)
+        assert bd == O.mgard_compress(a, 1e-3, value_range=vr), (shape, vr, "device input")
         b = P.mgard_compress(a, 1e-3, value_range=vr)
         assert b == O.mgard_compress(a, 1e-3, value_range=vr), (shape, vr)
         y = P.mgard_decompress(b).values
@@ -211,9 +216,11 @@ print("variant ok")
 """
 
 
-@pytest.mark.parametrize("env", [{"HPDR_GENERIC": "1"}, {"HPDR_NO_STREAM": "1"}])
+@pytest.mark.parametrize("env", [{"HPDR_GENERIC": "1"}, {"HPDR_NO_STREAM": "1"}, {"HPDR_NO_QUAD": "1"},
+                                 {"HPDR_NO_TMA": "1"}, {"HPDR_QUAD_SLABS": "3"}, {}])
 def test_execution_variants_bit_identical(env):
-    """The per-axis (generic) path and the non-streamed fused path give the same blobs."""
+    """Every execution variant gives the reference's blobs: the per-axis (generic) path, the non-streamed
+    fused path, pass 1 without quads, the quad kernel without TMA, and forced slab splits."""
     import subprocess
     import sys
 
