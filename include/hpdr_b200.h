@@ -71,6 +71,10 @@ void    *hpdr_host_alloc(uint64_t bytes);
 /* Host memcpy split across the library's copy threads (large results into Python-owned memory). */
 void     hpdr_host_copy(void *dst, const void *src, uint64_t n);
 void     hpdr_host_free(void *p);
+/* Page-lock an existing host range (cudaHostRegister, portable) so transfers DMA straight from /
+ * to it; returns HPDR_ERR_ALLOCATION on failure.  A range that is already registered is OK. */
+int      hpdr_host_register(void *p, uint64_t bytes);
+void     hpdr_host_unregister(void *p);
 
 /* ---- whole-path entry points: hpdr/mgard/codec.py ---- */
 

@@ -34,6 +34,8 @@ _SIGS = {
     "hpdr_host_alloc": (C.c_void_p, [C.c_uint64]),
     "hpdr_host_copy": (None, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "hpdr_host_free": (None, [C.c_void_p]),
+    "hpdr_host_register": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "hpdr_host_unregister": (None, [C.c_void_p]),
     "hpdr_mgard_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _u64p, C.c_double, C.c_uint32,
                                       C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_uint64, _u64p]),
     "hpdr_mgard_fetch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),

@@ -649,4 +649,20 @@ void hpdr_host_free(void *p) {
     if (p) cudaFreeHost(p);
 }
 
+int hpdr_host_register(void *p, uint64_t bytes) {
+    if (!p || !bytes) return HPDR_OK;
+    const cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable);
+    if (e == cudaSuccess || e == cudaErrorHostMemoryAlreadyRegistered) {
+        cudaGetLastError();
+        return HPDR_OK;
+    }
+    cudaGetLastError();
+    set_error(HPDR_ERR_ALLOCATION, std::string("cudaHostRegister failed: ") + cudaGetErrorString(e));
+    return HPDR_ERR_ALLOCATION;
+}
+
+void hpdr_host_unregister(void *p) {
+    if (p && cudaHostUnregister(p) != cudaSuccess) cudaGetLastError();
+}
+
 }  // extern "C"

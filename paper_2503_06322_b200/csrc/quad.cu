@@ -25,7 +25,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
-#include <mutex>
+#include <type_traits>
 
 #include "level_dev.cuh"
 
@@ -36,22 +36,20 @@ namespace {
 using namespace lvl;
 
 constexpr int kQX = 16, kQY = 8;                        // quads per block (x, y): 128 threads
+constexpr int kQThreads = kQX * kQY;
 constexpr int kTileX = 2 * kQX, kTileY = 2 * kQY;       // 32 x 16 nodes
 constexpr int kRows = kTileY + 1;                       // + one halo row
-constexpr int kQRing = 8;                               // ring slots (power of two)
-constexpr int kLook = 5;                                // planes issued ahead of the march
 constexpr int kQHist = 4096;
 
+// Ring geometry (static shared memory, < 48 KB): fp32 planes 8 slots / 5 ahead, fp64 6 / 3.
 template <typename T>
 struct QuadGeom {
     static constexpr int pitch = sizeof(T) == 4 ? 36 : 34;   // row pitch: 33 used, 16-byte multiple
-    static constexpr int slot_elems = kRows * pitch;
-    static constexpr int slot_bytes = (slot_elems * (int)sizeof(T) + 127) / 128 * 128;
-    static constexpr int ring_bytes = kQRing * slot_bytes;
-    static constexpr int pi_off = ring_bytes;                           // PlaneInfo ring
-    static constexpr int hist_off = pi_off + kQRing * (int)sizeof(PlaneInfo);
-    static constexpr int bar_off = hist_off + kQHist * 4;               // full[8], empty[8]
-    static constexpr int smem = bar_off + 2 * kQRing * 8;
+    static constexpr int slot_bytes = (kRows * pitch * (int)sizeof(T) + 127) / 128 * 128;
+    static constexpr int slot_elems = slot_bytes / (int)sizeof(T);
+    static constexpr int R = sizeof(T) == 4 ? 8 : 6;          // slots
+    static constexpr int LA = R - 3;                          // planes issued ahead of the march
+    static constexpr unsigned tile_bytes = kRows * pitch * sizeof(T);
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -89,35 +87,57 @@ __device__ __forceinline__ void bulk_load(unsigned dst, const void *src, unsigne
                  : "memory");
 }
 
+// Predicated stores / shared-histogram increments (no branch, no reconvergence point).
+__device__ __forceinline__ void st_u32_if(uint32_t *p, uint32_t v, bool c) {
+    asm volatile("{.reg .pred p; setp.ne.b32 p, %2, 0; @p st.global.u32 [%0], %1;}" ::"l"(p), "r"(v), "r"((int)c));
+}
+__device__ __forceinline__ void st_f64_if(double *p, double v, bool c) {
+    asm volatile("{.reg .pred p; setp.ne.b32 p, %2, 0; @p st.global.f64 [%0], %1;}" ::"l"(p), "d"(v), "r"((int)c));
+}
+__device__ __forceinline__ void hist_inc_if(unsigned saddr, bool c) {
+    asm volatile("{.reg .pred p; setp.ne.b32 p, %1, 0; @p red.shared.add.u32 [%0], 1;}" ::"r"(saddr), "r"((int)c));
+}
+// A 64-bit base the compiler cannot re-associate with the per-node 32-bit offsets (one IMAD.WIDE each).
 template <typename T>
-__device__ __forceinline__ double ld1(const T *s) { return (double)*s; }
+__device__ __forceinline__ T *opaque(T *p) {
+    asm("mov.b64 %0, %0;" : "+l"(p));
+    return p;
+}
 
-// Four marches along axis 0 sharing one PlaneInfo stream (march_push of fused.cu, unrolled x4).
-struct Quad4 {
-    double m1[4], m2[4], ya[4], yb[4], yc[4];
-};
+// (v0, v1) at an even element offset of a ring slot, widened to double.
+__device__ __forceinline__ void ld2(const float *s, double &a, double &b) {
+    const float2 v = *reinterpret_cast<const float2 *>(s);
+    a = (double)v.x;
+    b = (double)v.y;
+}
+__device__ __forceinline__ void ld2(const double *s, double &a, double &b) {
+    const double2 v = *reinterpret_cast<const double2 *>(s);
+    a = v.x;
+    b = v.y;
+}
 
-template <int MODE, typename TIn, bool TMA>
-__global__ void __launch_bounds__(kQX *kQY, 4)
+// 4 blocks (16 warps) per SM; the cp.async producer needs more registers than 128, so that
+// variant runs 3 blocks per SM without spills
+template <int MODE, typename TIn, bool TMA, bool SH>
+__global__ void __launch_bounds__(kQThreads, TMA ? 4 : 3)
     k_pass1_quad(const __grid_constant__ CUtensorMap tmap, const TIn *__restrict__ F, int n0, int n1, int n2,
                  DevAxis ax0, DevAxis ax1, DevAxis ax2, LevelMap lm, double *__restrict__ coef, double *__restrict__ Z0,
                  double *__restrict__ Cg, QuantOut q, int c_base, int c_count, int z0_vec) {
     using G = QuadGeom<TIn>;
-    extern __shared__ __align__(128) unsigned char smem[];
-    TIn *ring = reinterpret_cast<TIn *>(smem);
-    const PlaneInfo *piring = reinterpret_cast<const PlaneInfo *>(smem + G::pi_off);
-    uint32_t *sh_hist = reinterpret_cast<uint32_t *>(smem + G::hist_off);
-    const unsigned ring_s = smem_u32(smem), pir_s = ring_s + G::pi_off;
-    const unsigned full_s = ring_s + G::bar_off, empty_s = full_s + kQRing * 8;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool sh_ok = MODE == 2 && q.dict <= kQHist;
+    constexpr int R = G::R, LA = G::LA;
+    __shared__ __align__(128) TIn ring[R * G::slot_elems];
+    __shared__ __align__(16) PlaneInfo piring[R];
+    __shared__ uint32_t sh_hist[MODE == 2 ? kQHist + 1 : 1];   // + a dummy bin
+    __shared__ __align__(8) unsigned long long bars[2 * R];   // full[R], empty[R]
+    const int tid = threadIdx.x, lane = tid & 31;
+    constexpr bool sh_ok = MODE == 2 && SH;   // dict <= 4096: shared-memory histogram
     const double rbin = MODE == 2 ? 1.0 / qbin(q) : 0.0;
     if (MODE == 2 && sh_ok)
-        for (uint32_t k = tid; k < q.dict; k += kQX * kQY) sh_hist[k] = 0;
+        for (uint32_t k = tid; k < q.dict; k += kQThreads) sh_hist[k] = 0;
     if (TMA && tid == 0) {
-        for (int s = 0; s < kQRing; s++) {
-            mbar_init(full_s + s * 8, 1);
-            mbar_init(empty_s + s * 8, (kQX * kQY) / 32);
+        for (int s = 0; s < R; s++) {
+            mbar_init(smem_u32(&bars[s]), 1);
+            mbar_init(smem_u32(&bars[R + s]), kQThreads / 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -137,79 +157,66 @@ __global__ void __launch_bounds__(kQX *kQY, 4)
         const int nplanes = j_end - j_start + 1;
         const int plane = n1 * n2;   // < 2^31 (checked by the launcher)
         // ---- per-thread quad geometry (constant over the march)
+        // node k: 0 (r0, c0), 1 (r0, c0 + 1), 2 (r0 + 1, c0), 3 (r0 + 1, c0 + 1); rows / columns r0, c0
+        // are coarse (even), r0 + 1 / c0 + 1 fine-only unless they are the coarse tail
         const bool a00 = r0 < n1 && c0 < n2;
-        const bool rowB = r0 + 1 < n1, colB = c0 + 1 < n2;
-        bool rowfo = false, colfo = false;
-        double t1 = 0.0, t2 = 0.0;
-        if (a00 && rowB) {
-            rowfo = __ldg(ax1.pb + r0 + 1) >= 0;
-            if (rowfo) t1 = __ldg(ax1.pt + r0 + 1);
-        }
-        if (a00 && colB) {
-            colfo = __ldg(ax2.pb + c0 + 1) >= 0;
-            if (colfo) t2 = __ldg(ax2.pt + c0 + 1);
-        }
+        const bool rowB = a00 && r0 + 1 < n1, colB = a00 && c0 + 1 < n2;
+        const bool rowfo = rowB && __ldg(ax1.pb + r0 + 1) >= 0;
+        const bool colfo = colB && __ldg(ax2.pb + c0 + 1) >= 0;
+        const double t1 = rowfo ? __ldg(ax1.pt + r0 + 1) : 0.0;
+        const double t2 = colfo ? __ldg(ax2.pt + c0 + 1) : 0.0;
         const int rB = rowfo ? r0 + 2 : (rowB ? r0 + 1 : r0);
-        const int cB = colfo ? c0 + 2 : (colB ? c0 + 1 : c0);
-        // node k: 0 (r0, c0), 1 (r0, c0 + 1), 2 (r0 + 1, c0), 3 (r0 + 1, c0 + 1)
-        bool act[4];
-        act[0] = a00;
-        act[1] = a00 && colB;
-        act[2] = a00 && rowB;
-        act[3] = a00 && rowB && colB;
-        const bool nfo[4] = {false, colfo, rowfo, rowfo || colfo};   // fine-only within the plane
-        const int so_r0 = (r0 - Y0) * G::pitch + (c0 - X0);          // smem offsets within a slot
-        const int so_r1 = so_r0 + G::pitch;
+        const int dcB = colfo ? 2 : (colB ? 1 : 0);
+        // act: active nodes; nfo: fine-only within the plane (nodes 1-3), coarse nodes are 0 and the tails
+        const unsigned act = (a00 ? 1u : 0u) | (colB ? 2u : 0u) | (rowB ? 4u : 0u) | (rowB && colB ? 8u : 0u);
+        const unsigned nfo = (colfo ? 2u : 0u) | (rowfo ? 4u : 0u) | (rowfo || colfo ? 8u : 0u);
+        const int so_r0 = (r0 - Y0) * G::pitch + (c0 - X0);   // element offsets within a slot
         const int so_rB = (rB - Y0) * G::pitch + (c0 - X0);
-        const int dcB = cB - c0;
-        int col[4], fcol[4], cgc[4];
-        {
-            const int rr[4] = {r0, r0, r0 + 1, r0 + 1}, cc[4] = {c0, c0 + 1, c0, c0 + 1};
-            const int nc2 = ax2.nc;
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                col[k] = rr[k] * n2 + cc[k];
-                fcol[k] = act[k] ? __ldg(lm.m1 + rr[k]) * (int)lm.D2 + __ldg(lm.m2 + cc[k]) : 0;
-                cgc[k] = act[k] ? __ldg(ax1.pa + rr[k]) * nc2 + __ldg(ax2.pa + cc[k]) : 0;
-            }
+        const int col0 = r0 * n2 + c0;
+        int fcol0 = 0, fd1 = 0, fd2 = 0, cgc0 = 0;
+        if (a00) {
+            const int m1a = __ldg(lm.m1 + r0), m2a = __ldg(lm.m2 + c0);
+            fcol0 = m1a * (int)lm.D2 + m2a;
+            if (rowB) fd1 = (__ldg(lm.m1 + r0 + 1) - m1a) * (int)lm.D2;
+            if (colB) fd2 = __ldg(lm.m2 + c0 + 1) - m2a;
+            cgc0 = __ldg(ax1.pa + r0) * ax2.nc + __ldg(ax2.pa + c0);
         }
+        const int fcol[4] = {fcol0, fcol0 + fd2, fcol0 + fd1, fcol0 + fd1 + fd2};
+        const int cgc[4] = {cgc0, cgc0 + 1, cgc0 + ax2.nc, cgc0 + ax2.nc + 1};   // consecutive coarse nodes
         const int64_t fplane = lm.D1 * lm.D2;
         const int64_t cgplane = (int64_t)ax1.nc * ax2.nc;
 
-        // ---- producer side
-        auto slot_of = [&](int i) { return i & (kQRing - 1); };
-        // non-TMA: this thread's share of a tile (33 columns x 17 rows)
-        constexpr int kTileElems = kRows * (kTileX + 1);
-        constexpr int kPer = (kTileElems + kQX * kQY - 1) / (kQX * kQY);
-        int ld_s[kPer], ld_g[kPer];
-        if (!TMA) {
-#pragma unroll
-            for (int k = 0; k < kPer; k++) {
-                const int e = tid + k * kQX * kQY;
-                const int yy = e / (kTileX + 1), xx = e - yy * (kTileX + 1);
-                const bool ok = e < kTileElems && Y0 + yy < n1 && X0 + xx < n2;
-                ld_s[k] = ok ? (yy * G::pitch + xx) * (int)sizeof(TIn) : -1;
-                ld_g[k] = (Y0 + yy) * n2 + X0 + xx;
-            }
-        }
-        auto issue = [&](int i) {   // plane j_start + i into its slot
+        // ---- producer side (non-TMA: warp w copies tile rows w, w + 4, ..., lane l column l, lane 0 also
+        // column 32; row offsets are recomputed per plane, which is cheaper than holding them)
+        const int warp = tid >> 5;
+        const bool lane_in = X0 + lane < n2, col32_in = lane == 0 && X0 + kTileX < n2;
+        const unsigned ring_s = smem_u32(ring), pir_s = smem_u32(piring);
+        const unsigned full_s = smem_u32(bars), empty_s = full_s + R * 8;
+        auto issue = [&](int i) {   // plane j_start + i into slot i % R
             const int p = j_start + i;
-            const int s = slot_of(i);
+            const int s = i % R;
             if (TMA) {
                 if (tid == 0 && i < nplanes) {
-                    if (i >= kQRing) mbar_wait(empty_s + s * 8, ((i >> 3) + 1) & 1);   // plane i - 8 released
+                    if (i >= R) mbar_wait(empty_s + s * 8, ((i / R) + 1) & 1);   // plane i - R released
                     const unsigned fb = full_s + s * 8;
-                    mbar_expect_tx(fb, (unsigned)(kRows * G::pitch * sizeof(TIn) + sizeof(PlaneInfo)));
+                    mbar_expect_tx(fb, G::tile_bytes + (unsigned)sizeof(PlaneInfo));
                     tma_load_3d(ring_s + s * G::slot_bytes, &tmap, X0, Y0, p, fb);
                     bulk_load(pir_s + s * (unsigned)sizeof(PlaneInfo), ax0.pi + p, (unsigned)sizeof(PlaneInfo), fb);
                 }
             } else {
                 if (i < nplanes) {
-                    const TIn *gp = F + (int64_t)p * plane;
-                    const unsigned sb = ring_s + s * G::slot_bytes;
+                    const TIn *gp = F + (int64_t)p * plane + X0 + lane;
+                    const unsigned sb = ring_s + s * G::slot_bytes + lane * (unsigned)sizeof(TIn);
 #pragma unroll
-                    for (int k = 0; k < kPer; k++)
-                        if (ld_s[k] >= 0) cp_async_s<sizeof(TIn)>(sb + ld_s[k], gp + ld_g[k]);
+                    for (int k = 0; k < (kRows + 3) / 4; k++) {
+                        const int r = warp + 4 * k;
+                        if (r < kRows && Y0 + r < n1) {
+                            const TIn *g = gp + (Y0 + r) * n2;
+                            const unsigned so = sb + r * G::pitch * (unsigned)sizeof(TIn);
+                            if (lane_in) cp_async_s<sizeof(TIn)>(so, g);
+                            if (col32_in) cp_async_s<sizeof(TIn)>(so + kTileX * (unsigned)sizeof(TIn), g + kTileX);
+                        }
+                    }
                     if (tid < 5)
                         cp_async_s<16>(pir_s + s * (unsigned)sizeof(PlaneInfo) + tid * 16,
                                        reinterpret_cast<const char *>(ax0.pi + p) + tid * 16);
@@ -217,99 +224,101 @@ __global__ void __launch_bounds__(kQX *kQY, 4)
                 cp_async_commit();
             }
         };
-        auto wait_plane = [&](int i) {   // TMA: plane i has landed
-            if (TMA && i < nplanes) mbar_wait(full_s + slot_of(i) * 8, (i >> 3) & 1);
-        };
 
-        Quad4 M;
+        // Four axis-0 marches (march_push of fused.cu).  Planes alternate parity, so the window
+        // x(j-1), x(j-2) and y(k-2), y(k-1) is kept by parity (X[p], Y[p]) instead of shifted: every
+        // step is instantiated for its parity and no march value is ever copied.
+        double X[2][4], Y[2][4];
 #pragma unroll
-        for (int k = 0; k < 4; k++) M.m1[k] = M.m2[k] = M.ya[k] = M.yb[k] = M.yc[k] = 0.0;
+        for (int k = 0; k < 4; k++) X[0][k] = X[1][k] = Y[0][k] = Y[1][k] = 0.0;
         const int y_from = j_start == 0 ? 1 : j_start + 2;   // first j whose y(j - 1) is computable
 
-        // one y(k) per march from record P: y = (md x_k + ml x_{k-1}) + mu x_{k+1}, then emission
-        auto emit_y = [&](const PlaneInfo *P, int kk, const double *xk, const double *xkm1, const double *xkp1,
-                          bool has_up) {
-            const double md = P->md, ml = P->ml, mu = P->mu;
-            const int4 e = *reinterpret_cast<const int4 *>(&P->fo);   // fo, emit, e_rr, e_rl
-            double v[4];
+        // restriction z(e.y) = (y(r0) + wr y(rr)) + wl y(rl) from the window (ya, yb, yc), stored to Z0
+        auto restrict_out = [&](const PlaneInfo &P, const double *ya, const double *yb, const double *yc) {
+            const int4 e = *reinterpret_cast<const int4 *>(&P.fo);   // fo, emit, e_rr, e_rl
+            if (e.y >= c_lo && e.y < c_hi) {
+                const double wr = P.ewr, wl = P.ewl;
+                double z[4];
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    if (e.z) {
+                        z[k] = dadd(yb[k], dmul(wr, yc[k]));
+                        if (e.w) z[k] = dadd(z[k], dmul(wl, ya[k]));
+                    } else {
+                        z[k] = yc[k];
+                        if (e.w) z[k] = dadd(z[k], dmul(wl, yb[k]));
+                    }
+                }
+                double *zp = Z0 + (int64_t)e.y * plane + col0;
+                if (z0_vec) {   // rows even-aligned: (c0, c0 + 1) pairs as 16-byte stores
+                    if (act & 2) *reinterpret_cast<double2 *>(zp) = make_double2(z[0], z[1]);
+                    else if (act & 1) zp[0] = z[0];
+                    if (act & 8) *reinterpret_cast<double2 *>(zp + n2) = make_double2(z[2], z[3]);
+                    else if (act & 4) zp[n2] = z[2];
+                } else {
+                    if (act & 1) zp[0] = z[0];
+                    if (act & 2) zp[1] = z[1];
+                    if (act & 4) zp[n2] = z[2];
+                    if (act & 8) zp[n2 + 1] = z[3];
+                }
+            }
+        };
+        // y(kk) = (md x(kk) + ml x(kk-1)) + mu x(kk+1) for the four marches
+        auto y_of = [&](const PlaneInfo &P, int kk, const double *xk, const double *xkm1, const double *xkp1,
+                        bool has_up, double *v) {
+            const double md = P.md, ml = P.ml, mu = P.mu;
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 v[k] = dmul(md, xk[k]);
                 if (kk >= 1) v[k] = dadd(v[k], dmul(ml, xkm1[k]));
                 if (has_up) v[k] = dadd(v[k], dmul(mu, xkp1[k]));
-                M.ya[k] = M.yb[k];
-                M.yb[k] = M.yc[k];
-                M.yc[k] = v[k];
-            }
-            if (e.y >= c_lo && e.y < c_hi) {
-                const double wr = P->ewr, wl = P->ewl;
-                double z[4];
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    if (e.z) {
-                        z[k] = dadd(M.yb[k], dmul(wr, M.yc[k]));
-                        if (e.w) z[k] = dadd(z[k], dmul(wl, M.ya[k]));
-                    } else {
-                        z[k] = M.yc[k];
-                        if (e.w) z[k] = dadd(z[k], dmul(wl, M.yb[k]));
-                    }
-                }
-                double *zp = Z0 + (int64_t)e.y * plane;
-                if (z0_vec) {   // rows even-aligned: (c0, c0 + 1) pairs as 16-byte stores
-                    if (act[1]) *reinterpret_cast<double2 *>(zp + col[0]) = make_double2(z[0], z[1]);
-                    else if (act[0]) zp[col[0]] = z[0];
-                    if (act[3]) *reinterpret_cast<double2 *>(zp + col[2]) = make_double2(z[2], z[3]);
-                    else if (act[2]) zp[col[2]] = z[2];
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 4; k++)
-                        if (act[k]) zp[col[k]] = z[k];
-                }
             }
         };
 
         // ---- prologue
 #pragma unroll 1
-        for (int i = 0; i < kLook; i++) issue(i);
+        for (int i = 0; i < LA; i++) issue(i);
         if (!TMA) {
-            cp_async_wait<kLook - 1>();   // plane 0
+            cp_async_wait<LA - 1>();   // plane 0
             __syncthreads();
+        } else {
+            mbar_wait(full_s, 0);
         }
-        wait_plane(0);
+        int m0_next = __ldg(lm.m0 + j_start);
 
-#pragma unroll 1
-        for (int i = 0; i < nplanes; i++) {
+        auto step = [&](auto parity, int i) {
+            constexpr int pe = decltype(parity)::value, po = 1 - pe;   // parity of j, of j - 1
             const int j = j_start + i;
             if (TMA) {
-                issue(i + kLook);
-                wait_plane(i + 1);
+                issue(i + LA);
+                if (i + 1 < nplanes) mbar_wait(full_s + ((unsigned)(i + 1) % R) * 8, ((unsigned)(i + 1) / R) & 1);
             } else {
-                cp_async_wait<kLook - 2>();   // planes <= i + 1 landed (own copies)
-                __syncthreads();              // ... everyone's; slots of planes <= i - 2 free
-                issue(i + kLook);
+                cp_async_wait<LA - 2>();   // planes <= i + 1 landed (own copies)
+                __syncthreads();           // ... everyone's; slots of planes <= i - 2 free
+                issue(i + LA);
             }
-            const PlaneInfo *pj = piring + slot_of(i);
-            const int4 hd = *reinterpret_cast<const int4 *>(pj);   // fa, fb, ca, cb
-            const bool pfo = pj->fo != 0;
-            const TIn *so = ring + slot_of(i) * (G::slot_bytes / (int)sizeof(TIn));
+            const int m0j = m0_next;
+            if (i + 1 < nplanes) m0_next = __ldg(lm.m0 + j + 1);
+            const PlaneInfo &pj = piring[(unsigned)i % R];
+            const int4 hd = *reinterpret_cast<const int4 *>(&pj);   // fa, fb, ca, cb
+            const bool pfo = pj.fo != 0;
+            const TIn *so = ring + ((unsigned)i % R) * G::slot_elems;
             double own[4], P00, P0B, PB0, PBB;
-            own[0] = ld1(so + so_r0);
-            own[1] = ld1(so + so_r0 + 1);
-            own[2] = ld1(so + so_r1);
-            own[3] = ld1(so + so_r1 + 1);
+            ld2(so + so_r0, own[0], own[1]);
+            ld2(so + so_r0 + G::pitch, own[2], own[3]);
             if (pfo) {   // fine-only plane: P0 = lerp(F[fa], F[fb], t0) at the four corners
-                const double t0 = pj->t;
-                const TIn *sa = ring + slot_of(hd.x - j_start) * (G::slot_bytes / (int)sizeof(TIn));
-                const TIn *sb = ring + slot_of(hd.y - j_start) * (G::slot_bytes / (int)sizeof(TIn));
-                P00 = lerp(ld1(sa + so_r0), ld1(sb + so_r0), t0);
-                P0B = lerp(ld1(sa + so_r0 + dcB), ld1(sb + so_r0 + dcB), t0);
-                PB0 = lerp(ld1(sa + so_rB), ld1(sb + so_rB), t0);
-                PBB = lerp(ld1(sa + so_rB + dcB), ld1(sb + so_rB + dcB), t0);
+                const double t0 = pj.t;
+                const TIn *sa = ring + ((unsigned)(hd.x - j_start) % R) * G::slot_elems;
+                const TIn *sb = ring + ((unsigned)(hd.y - j_start) % R) * G::slot_elems;
+                P00 = lerp((double)sa[so_r0], (double)sb[so_r0], t0);
+                P0B = lerp((double)sa[so_r0 + dcB], (double)sb[so_r0 + dcB], t0);
+                PB0 = lerp((double)sa[so_rB], (double)sb[so_rB], t0);
+                PBB = lerp((double)sa[so_rB + dcB], (double)sb[so_rB + dcB], t0);
             } else {
                 P00 = own[0];
-                P0B = ld1(so + so_r0 + dcB);
-                PB0 = ld1(so + so_rB);
-                PBB = ld1(so + so_rB + dcB);
+                P0B = (double)so[so_r0 + dcB];
+                PB0 = (double)so[so_rB];
+                PBB = (double)so[so_rB + dcB];
             }
             double mc[4];
             {
@@ -320,45 +329,88 @@ __global__ void __launch_bounds__(kQX *kQY, 4)
                 mc[2] = dsub(own[2], p1a);
                 mc[3] = dsub(own[3], colfo ? lerp(p1a, p1b, t2) : p1b);
             }
-            if (j >= own_lo && j < own_hi) {
-                const int64_t fb = (int64_t)__ldg(lm.m0 + j) * fplane;
+            if (j >= own_lo && j < own_hi) {   // uniform
+                const int64_t fb = (int64_t)m0j * fplane;
+                const unsigned fine = act & (pfo ? 15u : nfo), coarse = act & ~fine;
+                if (coarse) {
+                    double *cgp = opaque(Cg + (int64_t)hd.z * cgplane);
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    if (!act[k]) continue;
-                    if (!pfo && !nfo[k]) {
-                        Cg[(int64_t)hd.z * cgplane + cgc[k]] = own[k];
-                    } else if (MODE == 0) {
-                        coef[fb + fcol[k]] = mc[k];
-                    } else {
-                        quant_node(mc[k], q, rbin, fb + fcol[k], fl, sh_hist, sh_ok);
+                    for (int k = 0; k < 4; k++) st_f64_if(cgp + cgc[k], own[k], coarse & (1u << k));
+                }
+                if (MODE == 0) {
+                    double *cp = opaque(coef + fb);
+#pragma unroll
+                    for (int k = 0; k < 4; k++) st_f64_if(cp + (unsigned)fcol[k], mc[k], fine & (1u << k));
+                } else {
+                    // fast path (quant_node for an in-range, comfortably rounded quotient), branch-free
+                    uint32_t *kp = opaque(q.keys + fb);
+                    unsigned slow = 0;
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        const double qa = dmul(mc[k], rbin);
+                        const double r = rint(qa);
+                        const bool ok = (0.5 - fabs(dsub(qa, r))) > fabs(qa) * 0x1p-49 && fabs(r) < (double)q.half;
+                        const int ri = (int)r;
+                        const uint32_t key = ((uint32_t)ri << 1) ^ (uint32_t)(ri >> 31);
+                        const bool fk = (fine >> k) & 1u;
+                        st_u32_if(kp + (unsigned)fcol[k], key, fk && ok);
+                        if (sh_ok) atomicAdd(&sh_hist[fk && ok ? key : (uint32_t)kQHist], 1u);
+                        else if (fk && ok) atomicAdd(&q.hist[key], 1ULL);
+                        slow |= (fk && !ok) ? 1u << k : 0u;
+                    }
+                    if (slow) {   // outliers, near-half quotients, non-finite values: the full rule
+#pragma unroll 1
+                        for (int k = 0; k < 4; k++)
+                            if (slow & (1u << k)) {
+                                const double mk = k == 0 ? mc[0] : k == 1 ? mc[1] : k == 2 ? mc[2] : mc[3];
+                                const int fk = fcol0 + ((k & 1) ? fd2 : 0) + ((k & 2) ? fd1 : 0);
+                                quant_node(mk, q, rbin, fb + fk, fl, sh_hist, sh_ok);
+                            }
                     }
                 }
             }
             // axis-0 marches (march_push): y(j - 1) once x(j) is known, y(j) at the last plane
-            if (j >= y_from) emit_y(piring + slot_of(i - 1), j - 1, M.m1, M.m2, mc, true);
-            if (j == n0 - 1 && (j > j_start || j == 0)) emit_y(pj, j, mc, M.m1, mc, false);
+            if (j >= y_from) {
+                const PlaneInfo &pm = piring[(unsigned)(i + R - 1) % R];
+                double v[4];
+                y_of(pm, j - 1, X[po], X[pe], mc, true, v);
+                restrict_out(pm, Y[po], Y[pe], v);   // window y(j-3), y(j-2), y(j-1)
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                M.m2[k] = M.m1[k];
-                M.m1[k] = mc[k];
+                for (int k = 0; k < 4; k++) Y[po][k] = v[k];
             }
+            if (j == n0 - 1 && (j > j_start || j == 0)) {
+                double v[4];
+                y_of(pj, j, mc, X[po], mc, false, v);
+                restrict_out(pj, Y[pe], Y[po], v);   // window y(j-2), y(j-1), y(j)
+            }
+#pragma unroll
+            for (int k = 0; k < 4; k++) X[pe][k] = mc[k];
             if (TMA && i >= 1) {   // plane i - 1 is no longer read by this warp
                 __syncwarp();
-                if (lane == 0) mbar_arrive(empty_s + slot_of(i - 1) * 8);
+                if (lane == 0) mbar_arrive(empty_s + ((unsigned)(i - 1) % R) * 8);
             }
+        };
+        using P0 = std::integral_constant<int, 0>;
+        using P1 = std::integral_constant<int, 1>;
+        int i0 = 0;
+        if (j_start & 1) step(P1{}, i0++);   // a slab may start on an odd plane (single-plane chunks)
+#pragma unroll 1
+        for (; i0 + 1 < nplanes; i0 += 2) {
+            step(P0{}, i0);
+            step(P1{}, i0 + 1);
         }
+        if (i0 < nplanes) step(P0{}, i0);
         if (!TMA) cp_async_wait<0>();
     }
     if (MODE == 2) {
         if (fl) atomicOr(q.flags, fl);
         __syncthreads();
         if (sh_ok)
-            for (uint32_t k = tid; k < q.dict; k += kQX * kQY) {
+            for (uint32_t k = tid; k < q.dict; k += kQThreads) {
                 const uint32_t c = sh_hist[k];
                 if (c) atomicAdd(&q.hist[k], (unsigned long long)c);
             }
     }
-    (void)warp;
 }
 
 // ---- host side
@@ -391,16 +443,11 @@ bool make_tmap(CUtensorMap &m, const TIn *F, int n0, int n1, int n2) {
     return r == CUDA_SUCCESS;
 }
 
-template <int MODE, typename TIn, bool TMA>
+template <int MODE, typename TIn, bool TMA, bool SH>
 void launch_one(dim3 grid, const CUtensorMap &tm, const TIn *F, int n0, int n1, int n2, const DevAxis &a0,
                 const DevAxis &a1, const DevAxis &a2, const LevelMap &lm, double *coef, double *Z0, double *Cg,
                 const QuantOut &q, int c_base, int c_count, int z0_vec, cudaStream_t s) {
-    constexpr int smem = QuadGeom<TIn>::smem;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(k_pass1_quad<MODE, TIn, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    });
-    k_pass1_quad<MODE, TIn, TMA><<<grid, kQX * kQY, smem, s>>>(tm, F, n0, n1, n2, a0, a1, a2, lm, coef, Z0, Cg, q,
+    k_pass1_quad<MODE, TIn, TMA, SH><<<grid, kQThreads, 0, s>>>(tm, F, n0, n1, n2, a0, a1, a2, lm, coef, Z0, Cg, q,
                                                                c_base, c_count, z0_vec);
 }
 
@@ -444,12 +491,14 @@ void launch_pass1_quad(const TIn *F, int n0, int n1, int n2, const DevAxis &a0, 
     static const bool no_tma = getenv("HPDR_NO_TMA") != nullptr;
     const bool tma = !no_tma && ((int64_t)n2 * sizeof(TIn)) % 16 == 0 && ((uintptr_t)F & 15) == 0 &&
                      make_tmap(tm, F, n0, n1, n2);
-    if (tma)
-        launch_one<MODE, TIn, true>(grid, tm, F, n0, n1, n2, a0, a1, a2, lm, coef, Z0, Cg, q, c_base, c_count, z0_vec,
-                                    s);
-    else
-        launch_one<MODE, TIn, false>(grid, tm, F, n0, n1, n2, a0, a1, a2, lm, coef, Z0, Cg, q, c_base, c_count, z0_vec,
-                                     s);
+    const bool sh = MODE == 2 && q.dict <= (uint32_t)kQHist;
+    if (tma) {
+        if (sh) launch_one<MODE, TIn, true, true>(grid, tm, F, n0, n1, n2, a0, a1, a2, lm, coef, Z0, Cg, q, c_base, c_count, z0_vec, s);
+        else launch_one<MODE, TIn, true, false>(grid, tm, F, n0, n1, n2, a0, a1, a2, lm, coef, Z0, Cg, q, c_base, c_count, z0_vec, s);
+    } else {
+        if (sh) launch_one<MODE, TIn, false, true>(grid, tm, F, n0, n1, n2, a0, a1, a2, lm, coef, Z0, Cg, q, c_base, c_count, z0_vec, s);
+        else launch_one<MODE, TIn, false, false>(grid, tm, F, n0, n1, n2, a0, a1, a2, lm, coef, Z0, Cg, q, c_base, c_count, z0_vec, s);
+    }
     LAUNCH_CHECK();
 }
 

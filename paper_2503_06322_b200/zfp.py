@@ -12,7 +12,7 @@ import ctypes as C
 
 import numpy as np
 
-from . import _lib
+from . import _lib, hostmem
 from ._lib import check, dims_arg, lib
 from .errors import ValidationError
 from .tensor import DTYPE_CODES, DTYPE_FROM_CODE, DType, TensorData
@@ -62,6 +62,7 @@ def zfp_compress(u, rate: int, adapter=None, *, device: int | None = None, out=N
     dims = tuple(int(d) for d in dims)
     if not dims:
         raise ValidationError("dims must be non-empty")
+    hostmem.register_input(keep)
     ctx = _lib.default_context(device, u if getattr(u, "is_cuda", False) else out)
     n = C.c_uint64()
     if out is None:
@@ -101,7 +102,7 @@ def zfp_decompress(data, adapter=None, *, device: int | None = None, out=None) -
         addr, size = (buf.ctypes.data if buf.size else 0), buf.size
         dtype, dims, _ = stream_info(buf)
     ctx = _lib.default_context(device, data if getattr(data, "is_cuda", False) else out)
-    res = np.empty(dims, dtype=dtype.np_dtype) if out is None else out
+    res = hostmem.empty(dims, dtype.np_dtype) if out is None else out
     check(lib().hpdr_zfp_decompress(ctx.handle, C.c_void_p(addr), size, C.c_void_p(_lib.ptr(res)), int(res.nbytes)))
     if out is not None:
         return out
