@@ -169,7 +169,9 @@ int hpdr_pipeline_zfp_compress(hpdr_ctx *ctx, const void *host_in, int dtype, in
 
 /* Kernel launches issued by this thread since the last reset (bench accounting). */
 uint64_t hpdr_launch_count(int reset);
-/* Live per-kernel CUDA-event timing with algorithmic bytes (bench roofline).  Enabling
+/* Live per-kernel CUDA-event timing with algorithmic bytes (bench roofline).  on = 1: events on
+ * the launching stream (kernels on side streams may overlap); on = 2: serialized, the device is
+ * synchronized before and after every profiled launch (per-kernel times that add up).  Enabling
  * clears previous records; hpdr_prof_read writes {"kernel": [launches, total_ms,
  * total_bytes, max_ms], ...} as JSON and clears. */
 void     hpdr_prof_enable(int on);

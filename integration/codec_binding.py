@@ -71,8 +71,9 @@ def install(codec, lib_path: str = _LIB, device: int = 0):
         rc = L.hpdr_mgard_peek(addr, C.c_uint64(buf.size), C.byref(dt), C.byref(rk), dims)
         if rc:
             _raise(rc)
-        dtype = DTYPE_FROM_CODE[dt.value]
-        shape = tuple(int(dims[i]) for i in range(rk.value))
+        # an unknown dtype code or rank is reported by the decoder with the reference's exception
+        dtype = DTYPE_FROM_CODE.get(dt.value, DType.F64)
+        shape = tuple(int(dims[i]) for i in range(rk.value)) if 1 <= rk.value <= 4 else (1,)
         out = np.empty(shape, dtype.np_dtype)
         rc = L.hpdr_mgard_decompress(ctx, addr, C.c_uint64(buf.size), C.c_void_p(out.ctypes.data),
                                      C.c_uint64(out.nbytes))

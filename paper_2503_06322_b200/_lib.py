@@ -252,8 +252,9 @@ def launch_count(reset: bool = False) -> int:
     return int(lib().hpdr_launch_count(1 if reset else 0))
 
 
-def prof_enable(on: bool = True):
-    lib().hpdr_prof_enable(1 if on else 0)
+def prof_enable(on=True):
+    """on: False / True (live events) / "serial" (device synchronized around every launch)."""
+    lib().hpdr_prof_enable(2 if on == "serial" else (1 if on else 0))
 
 
 def prof_read() -> dict:

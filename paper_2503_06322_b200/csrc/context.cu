@@ -79,6 +79,7 @@ struct ProfRec {
 };
 std::mutex g_prof_mu;
 bool g_prof_on = false;
+bool g_prof_serial = false;   // mode 2: the device is idle before and after every profiled launch
 std::vector<ProfRec> g_prof;
 std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_pool;
 size_t g_prof_used = 0;
@@ -88,6 +89,7 @@ bool prof_enabled() { return g_prof_on; }
 
 ProfScope::ProfScope(const char *name, double bytes, cudaStream_t s) : slot(-1), stream(s) {
     if (!g_prof_on) return;
+    if (g_prof_serial) cudaDeviceSynchronize();   // no other kernel overlaps this one
     std::lock_guard<std::mutex> g(g_prof_mu);
     if (g_prof_used == g_prof_pool.size()) {
         cudaEvent_t a, b;
@@ -102,8 +104,11 @@ ProfScope::ProfScope(const char *name, double bytes, cudaStream_t s) : slot(-1),
 
 ProfScope::~ProfScope() {
     if (slot < 0) return;
-    std::lock_guard<std::mutex> g(g_prof_mu);
-    if (slot < (int)g_prof.size()) cudaEventRecord(g_prof[slot].b, stream);
+    {
+        std::lock_guard<std::mutex> g(g_prof_mu);
+        if (slot < (int)g_prof.size()) cudaEventRecord(g_prof[slot].b, stream);
+    }
+    if (g_prof_serial) cudaDeviceSynchronize();
 }
 
 MemKind classify(const void *p) {
@@ -530,6 +535,7 @@ uint64_t hpdr_launch_count(int reset) {
 void hpdr_prof_enable(int on) {
     std::lock_guard<std::mutex> g(g_prof_mu);
     g_prof_on = on != 0;
+    g_prof_serial = on == 2;
     g_prof.clear();
     g_prof_used = 0;
 }

@@ -128,13 +128,6 @@ def mgard_compress(u, eb_rel: float, dict_size: int = DEFAULT_DICT_SIZE, adapter
     r0, r1 = (float(value_range[0]), float(value_range[1])) if has else (0.0, 0.0)
     n = C.c_uint64()
     out_addr, out_cap = (None, 0) if out is None else (_lib.ptr(out), int(out.nbytes))
-    scratch = None
-    if out is None and not getattr(u, "is_cuda", False):
-        # a repeated large host call: the blob's D2H overlaps the encode into a pooled pinned buffer,
-        # then one parallel host copy makes the bytes (instead of a staged fetch after the call)
-        scratch = hostmem.scratch(int(np.prod(dims)) * (4 if code == 0 else 8) + (16 << 20))
-        if scratch is not None:
-            out_addr, out_cap = scratch.ctypes.data, int(scratch.nbytes)
     check(lib().hpdr_mgard_compress(ctx.handle, C.c_void_p(addr), code, len(dims), dims_arg(dims),
                                     float(eb_rel), int(dict_size), int(has), r0, r1,
                                     C.c_void_p(out_addr) if out_addr else None, out_cap, C.byref(n)))
@@ -143,8 +136,6 @@ def mgard_compress(u, eb_rel: float, dict_size: int = DEFAULT_DICT_SIZE, adapter
         if n.value > out_cap:
             check(lib().hpdr_mgard_fetch(ctx.handle, C.c_void_p(out_addr), out_cap))
         return int(n.value)
-    if scratch is not None and n.value <= scratch.nbytes:   # the blob already streamed into pinned memory
-        return _lib.bytes_from(scratch, n.value)
     b, p = _lib.new_bytes(n.value)
     check(lib().hpdr_mgard_fetch(ctx.handle, C.c_void_p(p), n.value))
     return b

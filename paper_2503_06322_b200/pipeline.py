@@ -14,6 +14,7 @@ Host-side scheduling (this module):
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -209,6 +210,43 @@ def overlap_ratio(trace: np.ndarray) -> float:
         for ca, cb in comp:
             ov += max(0.0, min(b, cb) - max(a, ca))
     return min(1.0, ov / total)
+
+
+TRACE_COLUMNS = ("task_kind", "chunk_id", "queue", "start_ns", "end_ns")
+QUEUES = 3   # chunks go round-robin to the three queues of Fig. 7 (pipeline.cu)
+
+
+def trace_rows(trace: np.ndarray, queues: int = QUEUES):
+    """A runner trace (K, 6) in ms as SPEC.md's export rows (task_kind, chunk_id, queue, start_ns,
+    end_ns): one H2D, COMPUTE and D2H task per chunk, times relative to the earliest start."""
+    t = np.asarray(trace, dtype=np.float64).reshape(-1, 6)
+    if t.size == 0:
+        return []
+    t0 = float(t.min())
+    rows = []
+    for k, r in enumerate(t):
+        for kind, (a, b) in zip(("H2D", "COMPUTE", "D2H"), ((r[0], r[1]), (r[2], r[3]), (r[4], r[5]))):
+            rows.append((kind, k, k % queues, int(round((a - t0) * 1e6)), int(round((b - t0) * 1e6))))
+    rows.sort(key=lambda x: (x[3], x[1]))
+    return rows
+
+
+def write_trace_csv(trace: np.ndarray, f, queues: int = QUEUES) -> int:
+    """SPEC.md trace export (External Interfaces): CSV with columns task_kind, chunk_id, queue,
+    start_ns, end_ns.  ``f`` is a path or a text file object; returns the number of task rows."""
+    import csv
+
+    rows = trace_rows(trace, queues)
+    own = isinstance(f, (str, bytes, os.PathLike))
+    fh = open(f, "w", newline="") if own else f
+    try:
+        w = csv.writer(fh)
+        w.writerow(TRACE_COLUMNS)
+        w.writerows(rows)
+    finally:
+        if own:
+            fh.close()
+    return len(rows)
 
 
 # ----------------------------------------------------------------------------- runner

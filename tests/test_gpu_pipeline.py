@@ -41,6 +41,12 @@ def test_pipeline_explicit_schedule_and_trace():
     y, tr2 = PL.decompress_pipelined(data, trace=True)
     assert np.max(np.abs(y.astype(np.float64) - a)) <= 1e-3 * 3.0
     assert 0.0 <= PL.overlap_ratio(tr) <= 1.0 and 0.0 <= PL.overlap_ratio(tr2) <= 1.0
+    import io
+
+    f = io.StringIO()   # SPEC.md trace export of the real runner's timeline
+    assert PL.write_trace_csv(tr, f) == 15
+    lines = f.getvalue().splitlines()
+    assert lines[0] == ",".join(PL.TRACE_COLUMNS) and all(len(x.split(",")) == 5 for x in lines[1:])
     with pytest.raises(P.ValidationError):
         PL.compress_pipelined(a, 1e-3, chunks=[1, 2, 3])
 

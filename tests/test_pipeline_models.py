@@ -103,3 +103,29 @@ def test_container_headers_round_trip_and_reject_corruption():
             CT.read_container(bytes(bad))
         with pytest.raises(FormatError):
             CT.read_container(data[:-1])
+
+
+def test_trace_csv_export_spec_columns(tmp_path):
+    """SPEC.md External Interfaces: CSV (task_kind, chunk_id, queue, start_ns, end_ns)."""
+    import csv
+
+    tr = np.array([[0.0, 1.0, 1.0, 3.0, 3.0, 4.0],
+                   [1.0, 2.0, 3.0, 5.0, 5.0, 6.0],
+                   [2.0, 3.0, 5.0, 7.0, 7.0, 8.0],
+                   [3.0, 4.0, 7.0, 9.0, 9.0, 10.0]])
+    p = tmp_path / "trace.csv"
+    assert PL.write_trace_csv(tr, str(p)) == 12
+    rows = list(csv.reader(open(p)))
+    assert tuple(rows[0]) == PL.TRACE_COLUMNS
+    body = [(r[0], int(r[1]), int(r[2]), int(r[3]), int(r[4])) for r in rows[1:]]
+    assert sorted({r[0] for r in body}) == ["COMPUTE", "D2H", "H2D"]
+    assert all(q == k % 3 for _, k, q, _, _ in body)                       # round-robin queues
+    assert ("COMPUTE", 1, 1, 3_000_000, 5_000_000) in body                  # ms -> ns, origin at 0
+    assert [r[3] for r in body] == sorted(r[3] for r in body)
+    # the CSV is the same timeline overlap_ratio measures
+    back = np.zeros_like(tr)
+    col = {"H2D": 0, "COMPUTE": 2, "D2H": 4}
+    for kind, k, _, a, b in body:
+        back[k, col[kind]], back[k, col[kind] + 1] = a / 1e6, b / 1e6
+    assert PL.overlap_ratio(back) == pytest.approx(PL.overlap_ratio(tr))
+    assert PL.write_trace_csv(np.zeros((0, 6)), str(tmp_path / "empty.csv")) == 0
