@@ -136,6 +136,7 @@ __global__ void k_write_outliers(const uint32_t *__restrict__ omask, int64_t wor
     for (int64_t w0 = c * kChunkWords; w0 < w_end; w0 += blockDim.x) {
         const int64_t w = w0 + threadIdx.x;
         const uint32_t m = w < w_end ? omask[w] : 0u;
+        if (!__syncthreads_or(m != 0u)) continue;   // no outlier in these 256 words (the common case)
         unsigned pre, tot;
         BS(tmp).ExclusiveSum((unsigned)__popc(m), pre, tot);
         smask[threadIdx.x] = m;

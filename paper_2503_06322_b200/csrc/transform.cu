@@ -285,10 +285,22 @@ __device__ __forceinline__ double div_fast(double a, double b, double r, bool &b
 }
 
 // ---------------------------------------------------------------- IPK: batched Thomas solves
+// Optional epilogue of the last sweep of a correction solve: instead of the correction x itself, write
+// dst = base + x (decompose: coarse + corr, transform.py:317) -- the elementwise k_add folded into
+// the solve (the correction buffer then holds intermediate values only).
+struct Epi {
+    const double *base = nullptr;
+    double *dst = nullptr;
+};
+__device__ __forceinline__ void epi_store(double *arr, int64_t i, double v, const Epi &e) {
+    if (e.dst) e.dst[i] = dadd(e.base[i], v);
+    else arr[i] = v;
+}
+
 // Strided axis: one thread per line, threads along the contiguous inner index (coalesced).
 __global__ void k_thomas_strided(double *__restrict__ arr, int64_t outer, int32_t n, int64_t inner,
                                  const double *__restrict__ tw, const double *__restrict__ tb,
-                                 const double *__restrict__ tu) {
+                                 const double *__restrict__ tu, Epi epi) {
     const int64_t lines = outer * inner;
     for (int64_t ln = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ln < lines; ln += (int64_t)gridDim.x * blockDim.x) {
         int64_t p = ln / inner, q = ln - p * inner;
@@ -300,11 +312,12 @@ __global__ void k_thomas_strided(double *__restrict__ arr, int64_t outer, int32_
             prev = v;
         }
         double last = ddiv(prev, tb[n - 1]);
-        x[(int64_t)(n - 1) * inner] = last;
+        const int64_t o = x - arr;
+        epi_store(arr, o + (int64_t)(n - 1) * inner, last, epi);
         for (int i = n - 2; i >= 0; i--) {
             double v = dsub(x[(int64_t)i * inner], dmul(tu[i], last));
             v = ddiv(v, tb[i]);
-            x[(int64_t)i * inner] = v;
+            epi_store(arr, o + (int64_t)i * inner, v, epi);
             last = v;
         }
     }
@@ -317,7 +330,7 @@ __global__ void __launch_bounds__(kThomasWarps * 32) k_thomas_contig(double *__r
                                                                      const double *__restrict__ tw,
                                                                      const double *__restrict__ tb,
                                                                      const double *__restrict__ tu,
-                                                                     const double *__restrict__ tr) {
+                                                                     const double *__restrict__ tr, Epi epi) {
     __shared__ double tile[kThomasWarps][32][33];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double (*T)[33] = tile[w];
@@ -368,7 +381,7 @@ __global__ void __launch_bounds__(kThomasWarps * 32) k_thomas_contig(double *__r
             }
             __syncwarp();
             for (int r = 0; r < nl; r++)
-                if (lane < m) arr[(base + r) * n + t0 + lane] = T[r][lane];
+                if (lane < m) epi_store(arr, (base + r) * n + t0 + lane, T[r][lane], epi);
             __syncwarp();
         }
     }
@@ -380,11 +393,13 @@ __global__ void __launch_bounds__(kThomasWarps * 32) k_thomas_contig(double *__r
 template <int U>
 __global__ void __launch_bounds__(128) k_thomas_reg(double *__restrict__ arr, int64_t outer, int32_t n, int64_t inner,
                                                     const double *__restrict__ tw, const double *__restrict__ tb,
-                                                    const double *__restrict__ tu, const double *__restrict__ tr) {
+                                                    const double *__restrict__ tu, const double *__restrict__ tr,
+                                                    Epi epi) {
     const int64_t lines = outer * inner;
     for (int64_t ln = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ln < lines; ln += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = ln / inner, q = ln - p * inner;
         double *x = arr + p * (int64_t)n * inner + q;
+        const int64_t o = p * (int64_t)n * inner + q;
         double cur[U], nxt[U];
         auto load = [&](double *buf, int i0) {
 #pragma unroll
@@ -411,7 +426,7 @@ __global__ void __launch_bounds__(128) k_thomas_reg(double *__restrict__ arr, in
             for (int k = 0; k < U; k++) cur[k] = nxt[k];
         }
         double last = ddiv(prev, __ldg(tb + n - 1));   // (__ddiv_rn beat a checked fast division here)
-        x[(int64_t)(n - 1) * inner] = last;
+        epi_store(arr, o + (int64_t)(n - 1) * inner, last, epi);
         // back substitution: x_i = (x_i - u_i x_{i+1}) / b'_i, i = n-2 .. 0
         load(cur, n - 1 - U);
         for (int i1 = n - 2; i1 >= 0; i1 -= U) {
@@ -422,7 +437,7 @@ __global__ void __launch_bounds__(128) k_thomas_reg(double *__restrict__ arr, in
                 if (i >= 0) {
                     double v = dsub(cur[k], dmul(__ldg(tu + i), last));
                     v = ddiv(v, __ldg(tb + i));
-                    x[(int64_t)i * inner] = v;
+                    epi_store(arr, o + (int64_t)i * inner, v, epi);
                     last = v;
                 }
             }
@@ -444,7 +459,7 @@ template <bool CONTIG>
 __global__ void __launch_bounds__(32) k_thomas_tile(double *__restrict__ arr, int64_t outer, int32_t n,
                                                     int64_t inner, int32_t ls, const double *__restrict__ tw,
                                                     const double *__restrict__ tb, const double *__restrict__ tu,
-                                                    const double *__restrict__ tr) {
+                                                    const double *__restrict__ tr, Epi epi) {
     extern __shared__ __align__(16) double tsm[];
     const int lane = threadIdx.x;
     // element (line l, position i) of the tile
@@ -548,12 +563,12 @@ __global__ void __launch_bounds__(32) k_thomas_tile(double *__restrict__ arr, in
         // write back
         if (CONTIG) {
             for (int l = 0; l < nl; l++) {
-                double *dst = arr + (l0 + l) * (int64_t)n;
-                for (int i = lane; i < n; i += 32) dst[i] = at(l, i);
+                const int64_t o = (l0 + l) * (int64_t)n;
+                for (int i = lane; i < n; i += 32) epi_store(arr, o + i, at(l, i), epi);
             }
         } else if (lane < nl) {
-            double *dst = arr + p * (int64_t)n * inner + q0 + lane;
-            for (int i = 0; i < n; i++) dst[(int64_t)i * inner] = at(lane, i);
+            const int64_t o = p * (int64_t)n * inner + q0 + lane;
+            for (int i = 0; i < n; i++) epi_store(arr, o + (int64_t)i * inner, at(lane, i), epi);
         }
         __syncwarp();
     }
@@ -592,7 +607,7 @@ struct AxesArg {
     DevAxis ax[4];
 };
 
-__global__ void __launch_bounds__(512) k_thomas_small(double *__restrict__ arr, Shape4 sh, AxesArg A) {
+__global__ void __launch_bounds__(512) k_thomas_small(double *__restrict__ arr, Shape4 sh, AxesArg A, Epi epi) {
     extern __shared__ double g[];
     const int64_t N = sh.size();
     for (int64_t i = threadIdx.x; i < N; i += blockDim.x) g[i] = arr[i];
@@ -622,7 +637,7 @@ __global__ void __launch_bounds__(512) k_thomas_small(double *__restrict__ arr, 
         }
         __syncthreads();
     }
-    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) arr[i] = g[i];
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) epi_store(arr, i, g[i], epi);
 }
 
 // ---------------------------------------------------------------- elementwise
@@ -691,10 +706,10 @@ void mass_restrict(const double *src, double *dst, const Shape4 &fsh, int a, con
     LAUNCH_CHECK();
 }
 
-void thomas(double *arr, const Shape4 &csh, int a, const DevAxis &ax, cudaStream_t s) {
+void thomas(double *arr, const Shape4 &csh, int a, const DevAxis &ax, cudaStream_t s, Epi epi = Epi{}) {
     int64_t outer, inner;
     view(csh, a, outer, inner);
-    KPROF(inner == 1 ? "k_thomas_contig" : "k_thomas_strided", 16.0 * outer * inner * ax.nc, s);
+    KPROF(inner == 1 ? "k_thomas_contig" : "k_thomas_strided", (epi.dst ? 24.0 : 16.0) * outer * inner * ax.nc, s);
     // strided axes: register-blocked lines (coalesced across threads); contiguous axis: the
     // warp-tile transpose kernel measured faster (0.39 vs 0.45 ms at 257^3 coarse grid)
     static const bool legacy = getenv("HPDR_THOMAS_LEGACY") != nullptr;
@@ -716,7 +731,7 @@ void thomas(double *arr, const Shape4 &csh, int a, const DevAxis &ax, cudaStream
             }
             const int64_t tiles = (outer + 31) / 32;
             k_thomas_tile<true><<<(unsigned)std::min<int64_t>(tiles, 148 * 32), 32, smem, s>>>(
-                arr, outer, n, inner, ls, ax.tw, ax.tb, ax.tu, ax.tr);
+                arr, outer, n, inner, ls, ax.tw, ax.tb, ax.tu, ax.tr, epi);
         } else {
             const size_t smem = (size_t)32 * n * 8;
             static int attr_s = 0;
@@ -727,18 +742,20 @@ void thomas(double *arr, const Shape4 &csh, int a, const DevAxis &ax, cudaStream
             }
             const int64_t tiles = outer * ((inner + 31) / 32);
             k_thomas_tile<false><<<(unsigned)std::min<int64_t>(tiles, 148 * 32), 32, smem, s>>>(
-                arr, outer, n, inner, 0, ax.tw, ax.tb, ax.tu, ax.tr);
+                arr, outer, n, inner, 0, ax.tw, ax.tb, ax.tu, ax.tr, epi);
         }
     } else if (!legacy && inner > 1) {
         const int64_t lines = outer * inner;
-        k_thomas_reg<8><<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb, ax.tu, ax.tr);
+        k_thomas_reg<8><<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb, ax.tu, ax.tr,
+                                                                        epi);
     } else if (inner == 1) {
         int64_t lines = outer;
         unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((lines + 127) / 128, 148 * 16));
-        k_thomas_contig<<<g, kThomasWarps * 32, 0, s>>>(arr, lines, ax.nc, ax.tw, ax.tb, ax.tu, ax.tr);
+        k_thomas_contig<<<g, kThomasWarps * 32, 0, s>>>(arr, lines, ax.nc, ax.tw, ax.tb, ax.tu, ax.tr, epi);
     } else {
         int64_t lines = outer * inner;
-        k_thomas_strided<<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb, ax.tu);
+        k_thomas_strided<<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb, ax.tu,
+                                                                         epi);
     }
     LAUNCH_CHECK();
 }
@@ -900,11 +917,7 @@ const double *decompose_fused(hpdr_ctx *ctx, DevPlan &p, const void *d_in, int d
         if (q) fused_pass1_quantize(p, st_i, F, st_i == 0 && dtype == 0, *q, Z0, b.cg, s);
         else fused_pass1_decompose(p, st_i, F, st_i == 0 && dtype == 0, coef, Z0, b.cg, s);
         fused_pass2(p, st_i, Z0, b.t0, s);
-        thomas_all(p, st_i, b.t0, s);
-        const int64_t nc = st.csh.size();
-        KPROF("k_add", 24.0 * nc, s);
-        k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, Dn, nc);   // coarse + corr
-        LAUNCH_CHECK();
+        thomas_all(p, st_i, b.t0, s, b.cg, Dn);   // Dn = coarse + corr, fused into the last sweep
     }
     return level_ptr(b, p, L - 1);
 }
@@ -921,11 +934,7 @@ const double *coarse_levels_quantize(hpdr_ctx *ctx, DevPlan &p, const QuantOut &
             const DevStep &st = p.steps[st_i];
             fused_pass1_quantize(p, st_i, level_ptr(b, p, st_i), false, qq, Z0, b.cg, s);
             fused_pass2(p, st_i, Z0, b.t0, s);
-            thomas_all(p, st_i, b.t0, s);
-            const int64_t nc = st.csh.size();
-            KPROF("k_add", 24.0 * nc, s);
-            k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, level_ptr(b, p, st_i + 1), nc);
-            LAUNCH_CHECK();
+            thomas_all(p, st_i, b.t0, s, b.cg, level_ptr(b, p, st_i + 1));
         }
         quantize_coarsest(p, level_ptr(b, p, L - 1), qq, s);
     };
@@ -1082,11 +1091,7 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
     phase_mark("fine_quantized", s);
     // the rest of transition 0 (IPK + coarse update) and the coarser levels
     {
-        thomas_all(p, 0, b.t0, s);
-        const int64_t nc = st0.csh.size();
-        KPROF("k_add", 24.0 * nc, s);
-        k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(b.cg, b.t0, level_ptr(b, p, 1), nc);
-        LAUNCH_CHECK();
+        thomas_all(p, 0, b.t0, s, b.cg, level_ptr(b, p, 1));
     }
     const double *DL = coarse_levels_quantize(ctx, p, q, s);
     phase_mark("levels_done", s);
@@ -1200,9 +1205,12 @@ int64_t z0_elems(const DevPlan &p, int st_i) {
     return (int64_t)(st.ax[1].active ? st.csh.n[1] : st.fsh.n[1]) * st.fsh.n[2] * st.fsh.n[3];
 }
 
-void thomas_all(const DevPlan &p, int st_i, double *T, cudaStream_t s) {
+void thomas_all(const DevPlan &p, int st_i, double *T, cudaStream_t s, const double *add_base, double *add_dst) {
     const DevStep &st = p.steps[st_i];
     Shape4 sh = st.csh;
+    Epi epi;
+    epi.base = add_base;
+    epi.dst = add_dst;
     static const bool no_small = getenv("HPDR_THOMAS_NOSMALL") != nullptr;
     if (!no_small && sh.size() <= kThomasSmallMax) {
         static bool attr = false;
@@ -1213,13 +1221,22 @@ void thomas_all(const DevPlan &p, int st_i, double *T, cudaStream_t s) {
         }
         AxesArg A;
         for (int a = 0; a < 4; a++) A.ax[a] = st.ax[a];
-        KPROF("k_thomas_small", 16.0 * sh.size(), s);
-        k_thomas_small<<<1, 512, (size_t)sh.size() * 8, s>>>(T, sh, A);
+        KPROF("k_thomas_small", (add_dst ? 24.0 : 16.0) * sh.size(), s);
+        k_thomas_small<<<1, 512, (size_t)sh.size() * 8, s>>>(T, sh, A, epi);
         LAUNCH_CHECK();
         return;
     }
+    int last = -1;
     for (int a = 0; a < 4; a++)
-        if (st.ax[a].active) thomas(T, sh, a, st.ax[a], s);
+        if (st.ax[a].active) last = a;
+    for (int a = 0; a < 4; a++)
+        if (st.ax[a].active) thomas(T, sh, a, st.ax[a], s, a == last ? epi : Epi{});
+    if (last < 0 && add_dst) {   // no active axis: the correction is the right-hand side itself
+        const int64_t nc = sh.size();
+        KPROF("k_add", 24.0 * nc, s);
+        k_add<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(add_base, T, add_dst, nc);
+        LAUNCH_CHECK();
+    }
 }
 
 void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s,

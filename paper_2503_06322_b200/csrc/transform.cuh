@@ -55,7 +55,10 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
 // Elements of pass 1's output Z0 at transition st_i.
 int64_t z0_elems(const DevPlan &p, int st_i);
 // Thomas solves of every active axis of transition st_i's coarse grid, in place.
-void thomas_all(const DevPlan &p, int st_i, double *T, cudaStream_t s);
+// All IPK solves of transition st_i on T (in place); with add_dst, the last sweep writes
+// add_dst = add_base + correction instead (coarse + corr folded into the solve).
+void thomas_all(const DevPlan &p, int st_i, double *T, cudaStream_t s, const double *add_base = nullptr,
+                double *add_dst = nullptr);
 
 // True when the fused level kernels serve these dims (ranks <= 3) and HPDR_GENERIC != 1.
 bool use_fused(const DevPlan &p);
