@@ -94,9 +94,6 @@ __device__ __forceinline__ void st_u32_if(uint32_t *p, uint32_t v, bool c) {
 __device__ __forceinline__ void st_f64_if(double *p, double v, bool c) {
     asm volatile("{.reg .pred p; setp.ne.b32 p, %2, 0; @p st.global.f64 [%0], %1;}" ::"l"(p), "d"(v), "r"((int)c));
 }
-__device__ __forceinline__ void hist_inc_if(unsigned saddr, bool c) {
-    asm volatile("{.reg .pred p; setp.ne.b32 p, %1, 0; @p red.shared.add.u32 [%0], 1;}" ::"r"(saddr), "r"((int)c));
-}
 // A 64-bit base the compiler cannot re-associate with the per-node 32-bit offsets (one IMAD.WIDE each).
 template <typename T>
 __device__ __forceinline__ T *opaque(T *p) {

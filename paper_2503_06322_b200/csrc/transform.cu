@@ -292,12 +292,14 @@ struct Epi {
     const double *base = nullptr;
     double *dst = nullptr;
 };
+template <bool EPI>
 __device__ __forceinline__ void epi_store(double *arr, int64_t i, double v, const Epi &e) {
-    if (e.dst) e.dst[i] = dadd(e.base[i], v);
+    if (EPI) e.dst[i] = dadd(__ldg(e.base + i), v);
     else arr[i] = v;
 }
 
 // Strided axis: one thread per line, threads along the contiguous inner index (coalesced).
+template <bool EPI>
 __global__ void k_thomas_strided(double *__restrict__ arr, int64_t outer, int32_t n, int64_t inner,
                                  const double *__restrict__ tw, const double *__restrict__ tb,
                                  const double *__restrict__ tu, Epi epi) {
@@ -313,11 +315,11 @@ __global__ void k_thomas_strided(double *__restrict__ arr, int64_t outer, int32_
         }
         double last = ddiv(prev, tb[n - 1]);
         const int64_t o = x - arr;
-        epi_store(arr, o + (int64_t)(n - 1) * inner, last, epi);
+        epi_store<EPI>(arr, o + (int64_t)(n - 1) * inner, last, epi);
         for (int i = n - 2; i >= 0; i--) {
             double v = dsub(x[(int64_t)i * inner], dmul(tu[i], last));
             v = ddiv(v, tb[i]);
-            epi_store(arr, o + (int64_t)i * inner, v, epi);
+            epi_store<EPI>(arr, o + (int64_t)i * inner, v, epi);
             last = v;
         }
     }
@@ -326,6 +328,7 @@ __global__ void k_thomas_strided(double *__restrict__ arr, int64_t outer, int32_
 // Contiguous axis: each warp owns 32 lines and walks them in 32x32 shared-memory tiles,
 // loading and storing tile rows coalesced and running one line per lane.
 constexpr int kThomasWarps = 4;
+template <bool EPI>
 __global__ void __launch_bounds__(kThomasWarps * 32) k_thomas_contig(double *__restrict__ arr, int64_t lines, int32_t n,
                                                                      const double *__restrict__ tw,
                                                                      const double *__restrict__ tb,
@@ -380,8 +383,20 @@ __global__ void __launch_bounds__(kThomasWarps * 32) k_thomas_contig(double *__r
                 }
             }
             __syncwarp();
-            for (int r = 0; r < nl; r++)
-                if (lane < m) epi_store(arr, (base + r) * n + t0 + lane, T[r][lane], epi);
+            if (EPI) {   // coarse + corr: the coarse values of the tile rows in flight together
+                for (int r0 = 0; r0 < nl; r0 += 8) {
+                    double cv[8];
+#pragma unroll
+                    for (int k = 0; k < 8; k++)
+                        cv[k] = (r0 + k < nl && lane < m) ? __ldg(epi.base + (base + r0 + k) * n + t0 + lane) : 0.0;
+#pragma unroll
+                    for (int k = 0; k < 8; k++)
+                        if (r0 + k < nl && lane < m) epi.dst[(base + r0 + k) * n + t0 + lane] = dadd(cv[k], T[r0 + k][lane]);
+                }
+            } else {
+                for (int r = 0; r < nl; r++)
+                    if (lane < m) arr[(base + r) * n + t0 + lane] = T[r][lane];
+            }
             __syncwarp();
         }
     }
@@ -390,7 +405,7 @@ __global__ void __launch_bounds__(kThomasWarps * 32) k_thomas_contig(double *__r
 // Register-blocked sweeps: one thread per line, U values of the line loaded ahead of the
 // recurrence (double-buffered), so the sequential dependency never waits on DRAM.  Works for
 // strided (inner > 1, coalesced across threads) and contiguous (inner == 1) lines alike.
-template <int U>
+template <int U, bool EPI>
 __global__ void __launch_bounds__(128) k_thomas_reg(double *__restrict__ arr, int64_t outer, int32_t n, int64_t inner,
                                                     const double *__restrict__ tw, const double *__restrict__ tb,
                                                     const double *__restrict__ tu, const double *__restrict__ tr,
@@ -426,7 +441,7 @@ __global__ void __launch_bounds__(128) k_thomas_reg(double *__restrict__ arr, in
             for (int k = 0; k < U; k++) cur[k] = nxt[k];
         }
         double last = ddiv(prev, __ldg(tb + n - 1));   // (__ddiv_rn beat a checked fast division here)
-        epi_store(arr, o + (int64_t)(n - 1) * inner, last, epi);
+        epi_store<EPI>(arr, o + (int64_t)(n - 1) * inner, last, epi);
         // back substitution: x_i = (x_i - u_i x_{i+1}) / b'_i, i = n-2 .. 0
         load(cur, n - 1 - U);
         for (int i1 = n - 2; i1 >= 0; i1 -= U) {
@@ -437,7 +452,7 @@ __global__ void __launch_bounds__(128) k_thomas_reg(double *__restrict__ arr, in
                 if (i >= 0) {
                     double v = dsub(cur[k], dmul(__ldg(tu + i), last));
                     v = ddiv(v, __ldg(tb + i));
-                    epi_store(arr, o + (int64_t)i * inner, v, epi);
+                    epi_store<EPI>(arr, o + (int64_t)i * inner, v, epi);
                     last = v;
                 }
             }
@@ -455,7 +470,7 @@ __global__ void __launch_bounds__(128) k_thomas_reg(double *__restrict__ arr, in
 // then the tile is written back coalesced: 16 bytes of DRAM traffic per node.
 constexpr int kThomasTileMaxN = 880;   // 32 lines x 880 x 8 B = 220 KB of shared memory
 
-template <bool CONTIG>
+template <bool CONTIG, bool EPI>
 __global__ void __launch_bounds__(32) k_thomas_tile(double *__restrict__ arr, int64_t outer, int32_t n,
                                                     int64_t inner, int32_t ls, const double *__restrict__ tw,
                                                     const double *__restrict__ tb, const double *__restrict__ tu,
@@ -564,11 +579,11 @@ __global__ void __launch_bounds__(32) k_thomas_tile(double *__restrict__ arr, in
         if (CONTIG) {
             for (int l = 0; l < nl; l++) {
                 const int64_t o = (l0 + l) * (int64_t)n;
-                for (int i = lane; i < n; i += 32) epi_store(arr, o + i, at(l, i), epi);
+                for (int i = lane; i < n; i += 32) epi_store<EPI>(arr, o + i, at(l, i), epi);
             }
         } else if (lane < nl) {
             const int64_t o = p * (int64_t)n * inner + q0 + lane;
-            for (int i = 0; i < n; i++) epi_store(arr, o + (int64_t)i * inner, at(lane, i), epi);
+            for (int i = 0; i < n; i++) epi_store<EPI>(arr, o + (int64_t)i * inner, at(lane, i), epi);
         }
         __syncwarp();
     }
@@ -607,6 +622,7 @@ struct AxesArg {
     DevAxis ax[4];
 };
 
+template <bool EPI>
 __global__ void __launch_bounds__(512) k_thomas_small(double *__restrict__ arr, Shape4 sh, AxesArg A, Epi epi) {
     extern __shared__ double g[];
     const int64_t N = sh.size();
@@ -637,7 +653,7 @@ __global__ void __launch_bounds__(512) k_thomas_small(double *__restrict__ arr, 
         }
         __syncthreads();
     }
-    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) epi_store(arr, i, g[i], epi);
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) epi_store<EPI>(arr, i, g[i], epi);
 }
 
 // ---------------------------------------------------------------- elementwise
@@ -725,37 +741,56 @@ void thomas(double *arr, const Shape4 &csh, int a, const DevAxis &ax, cudaStream
             const size_t smem = (size_t)32 * ls * 8;
             static int attr_c = 0;
             if (smem > 48 * 1024 && attr_c < (int)smem) {
-                CUDA_CHECK(cudaFuncSetAttribute(k_thomas_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)(32 * (kThomasTileMaxN | 1) * 8)));
+                for (auto f : {k_thomas_tile<true, false>, k_thomas_tile<true, true>})
+                    CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)(32 * (kThomasTileMaxN | 1) * 8)));
                 attr_c = 32 * (kThomasTileMaxN | 1) * 8;
             }
             const int64_t tiles = (outer + 31) / 32;
-            k_thomas_tile<true><<<(unsigned)std::min<int64_t>(tiles, 148 * 32), 32, smem, s>>>(
-                arr, outer, n, inner, ls, ax.tw, ax.tb, ax.tu, ax.tr, epi);
+            if (epi.dst)
+                k_thomas_tile<true, true><<<(unsigned)std::min<int64_t>(tiles, 148 * 32), 32, smem, s>>>(
+                    arr, outer, n, inner, ls, ax.tw, ax.tb, ax.tu, ax.tr, epi);
+            else
+                k_thomas_tile<true, false><<<(unsigned)std::min<int64_t>(tiles, 148 * 32), 32, smem, s>>>(
+                    arr, outer, n, inner, ls, ax.tw, ax.tb, ax.tu, ax.tr, epi);
         } else {
             const size_t smem = (size_t)32 * n * 8;
             static int attr_s = 0;
             if (smem > 48 * 1024 && attr_s < (int)smem) {
-                CUDA_CHECK(cudaFuncSetAttribute(k_thomas_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)(32 * kThomasTileMaxN * 8)));
+                for (auto f : {k_thomas_tile<false, false>, k_thomas_tile<false, true>})
+                    CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)(32 * kThomasTileMaxN * 8)));
                 attr_s = 32 * kThomasTileMaxN * 8;
             }
             const int64_t tiles = outer * ((inner + 31) / 32);
-            k_thomas_tile<false><<<(unsigned)std::min<int64_t>(tiles, 148 * 32), 32, smem, s>>>(
-                arr, outer, n, inner, 0, ax.tw, ax.tb, ax.tu, ax.tr, epi);
+            if (epi.dst)
+                k_thomas_tile<false, true><<<(unsigned)std::min<int64_t>(tiles, 148 * 32), 32, smem, s>>>(
+                    arr, outer, n, inner, 0, ax.tw, ax.tb, ax.tu, ax.tr, epi);
+            else
+                k_thomas_tile<false, false><<<(unsigned)std::min<int64_t>(tiles, 148 * 32), 32, smem, s>>>(
+                    arr, outer, n, inner, 0, ax.tw, ax.tb, ax.tu, ax.tr, epi);
         }
     } else if (!legacy && inner > 1) {
         const int64_t lines = outer * inner;
-        k_thomas_reg<8><<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb, ax.tu, ax.tr,
-                                                                        epi);
+        if (epi.dst)
+            k_thomas_reg<8, true><<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb,
+                                                                              ax.tu, ax.tr, epi);
+        else
+            k_thomas_reg<8, false><<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb,
+                                                                               ax.tu, ax.tr, epi);
     } else if (inner == 1) {
         int64_t lines = outer;
         unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((lines + 127) / 128, 148 * 16));
-        k_thomas_contig<<<g, kThomasWarps * 32, 0, s>>>(arr, lines, ax.nc, ax.tw, ax.tb, ax.tu, ax.tr, epi);
+        if (epi.dst) k_thomas_contig<true><<<g, kThomasWarps * 32, 0, s>>>(arr, lines, ax.nc, ax.tw, ax.tb, ax.tu, ax.tr, epi);
+        else k_thomas_contig<false><<<g, kThomasWarps * 32, 0, s>>>(arr, lines, ax.nc, ax.tw, ax.tb, ax.tu, ax.tr, epi);
     } else {
         int64_t lines = outer * inner;
-        k_thomas_strided<<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb, ax.tu,
-                                                                         epi);
+        if (epi.dst)
+            k_thomas_strided<true><<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb,
+                                                                               ax.tu, epi);
+        else
+            k_thomas_strided<false><<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(arr, outer, ax.nc, inner, ax.tw, ax.tb,
+                                                                                ax.tu, epi);
     }
     LAUNCH_CHECK();
 }
@@ -1215,14 +1250,15 @@ void thomas_all(const DevPlan &p, int st_i, double *T, cudaStream_t s, const dou
     if (!no_small && sh.size() <= kThomasSmallMax) {
         static bool attr = false;
         if (!attr) {
-            CUDA_CHECK(cudaFuncSetAttribute(k_thomas_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            kThomasSmallMax * 8));
+            for (auto f : {k_thomas_small<false>, k_thomas_small<true>})
+                CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kThomasSmallMax * 8));
             attr = true;
         }
         AxesArg A;
         for (int a = 0; a < 4; a++) A.ax[a] = st.ax[a];
         KPROF("k_thomas_small", (add_dst ? 24.0 : 16.0) * sh.size(), s);
-        k_thomas_small<<<1, 512, (size_t)sh.size() * 8, s>>>(T, sh, A, epi);
+        if (add_dst) k_thomas_small<true><<<1, 512, (size_t)sh.size() * 8, s>>>(T, sh, A, epi);
+        else k_thomas_small<false><<<1, 512, (size_t)sh.size() * 8, s>>>(T, sh, A, epi);
         LAUNCH_CHECK();
         return;
     }
