@@ -132,7 +132,7 @@ void huffman_stage(hpdr_ctx *ctx, const uint32_t *d_keys, int64_t n, uint32_t di
         return;
     }
     put<uint32_t>(mid, (uint32_t)((n + kBlockSymbols - 1) / kBlockSymbols));
-    encode_device(ctx, d_keys, n, dict, lens.data(), codes.data(), enc, s, hooks);
+    encode_device(ctx, d_keys, n, dict, lens.data(), codes.data(), enc, s, hooks, hist.data());
 }
 
 // Write the pending stream (head | outliers | mid | offsets | total_bits | packed) to out; with
@@ -424,7 +424,7 @@ void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t 
         uint64_t pay_pos = 0;
         const MemKind ok = fetch_out ? classify(fetch_out) : MemKind::Host;
         if (fetch_out && ok != MemKind::Host) {
-            hooks.groups = 8;
+            hooks.groups = N >= (16LL << 20) ? 8 : 1;   // small streams: one launch, no group read-back
             hooks.ready = [&](const EncodeResult &e) {
                 const uint64_t total = P.head.size() + 16 * P.n_out + P.mid.size() + 8 * e.n_units + 8 + (e.total_bits + 7) / 8;
                 if (fetch_cap < total) return;

@@ -818,7 +818,8 @@ __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__rest
 constexpr int kFRing = 8;
 
 template <bool A0, bool A1, bool A2, typename TOut>
-__global__ void __launch_bounds__(256) k_level_final(const double *__restrict__ cv, int n0, int n1, int n2,
+__global__ void __launch_bounds__(256) k_level_final(const double *__restrict__ cv, const double *__restrict__ corr,
+                                                     int n0, int n1, int n2,
                                                      DevAxis ax0, DevAxis ax1, DevAxis ax2, LevelMap lm,
                                                      const double *__restrict__ coef, TOut *__restrict__ D, int j_base,
                                                      int j_count) {
@@ -871,8 +872,13 @@ __global__ void __launch_bounds__(256) k_level_final(const double *__restrict__ 
     auto stage = [&](int j) {
         if (j >= hi || tid >= RC) return;
         const Nb b0 = neighbours<A0>(ax0, j);
-        const double va = __ldg(cv + (int64_t)b0.ca * cplane + foff);
-        sP0[j & 1][tid] = b0.fo ? lerp(va, __ldg(cv + (int64_t)b0.cb * cplane + foff), b0.t) : va;
+        const int64_t ia = (int64_t)b0.ca * cplane + foff, ib = (int64_t)b0.cb * cplane + foff;
+        double va = __ldg(cv + ia), vb = b0.fo ? __ldg(cv + ib) : 0.0;
+        if (corr) {   // coarse - corr (the elementwise k_sub folded in)
+            va = dsub(va, __ldg(corr + ia));
+            if (b0.fo) vb = dsub(vb, __ldg(corr + ib));
+        }
+        sP0[j & 1][tid] = b0.fo ? lerp(va, vb, b0.t) : va;
     };
     for (int k = 0; k < kFRing - 1; k++) issue(lo + k);
     stage(lo);
@@ -960,7 +966,7 @@ void launch_pass2(int act, const double *Z0, int m0, int n1, int n2, const DevAx
 }
 
 template <typename TOut>
-void launch_final(int act, const double *cv, int n0, int n1, int n2, const DevAxis &a0, const DevAxis &a1,
+void launch_final(int act, const double *cv, const double *corr, int n0, int n1, int n2, const DevAxis &a0, const DevAxis &a1,
                   const DevAxis &a2, const LevelMap &lm, const double *coef, TOut *D, int j_base, int j_count,
                   cudaStream_t s) {
     if (j_count <= 0) return;
@@ -968,7 +974,7 @@ void launch_final(int act, const double *cv, int n0, int n1, int n2, const DevAx
     dim3 block(32, 8);
 #define FL(M)                                                                                                      \
     case M:                                                                                                        \
-        k_level_final<(M & 1) != 0, (M & 2) != 0, (M & 4) != 0, TOut><<<grid, block, 0, s>>>(cv, n0, n1, n2, a0, \
+        k_level_final<(M & 1) != 0, (M & 2) != 0, (M & 4) != 0, TOut><<<grid, block, 0, s>>>(cv, corr, n0, n1, n2, a0, \
                                                                                               a1, a2, lm, coef, D, j_base, j_count); \
         break;
     switch (act) { FL(1) FL(2) FL(3) FL(4) FL(5) FL(6) FL(7) default: break; }
@@ -1043,7 +1049,10 @@ void fused_pass1_quantize(const DevPlan &p, int st_i, const void *F, bool f32, c
     const double frac = (double)(c_hi - c_lo) / fused_out_planes(p, st_i);
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
     KPROF(st_i == 0 ? "k_level_pass1q" : "k_level_pass1q_coarse", frac * ((f32 ? 4.0 : 8.0) * nf + 4.0 * (nf - nc) + 8.0 * nc + 8.0 * z0_size(p, st_i)), s);
-    if (v.act == 7 && quad_eligible(p, st_i)) {
+    // the quad kernel's plane ring pays off on large levels; tiny ones (latency-bound) take the
+    // single-node kernel (HPDR_QUAD_MIN: smallest fine level, in nodes, that uses quads)
+    static const int64_t quad_min = getenv("HPDR_QUAD_MIN") ? atoll(getenv("HPDR_QUAD_MIN")) : (1LL << 18);
+    if (v.act == 7 && nf >= quad_min && quad_eligible(p, st_i)) {
         if (f32) launch_pass1_quad<2, float>((const float *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
                                              nullptr, Z0, Cg, q, c_lo, c_hi - c_lo, s);
         else launch_pass1_quad<2, double>((const double *)F, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm,
@@ -1105,18 +1114,18 @@ void fused_pass2(const DevPlan &p, int st_i, const double *Z0, double *B, cudaSt
 }
 
 void fused_final(const DevPlan &p, int st_i, const double *cv, const double *coef, void *D, int out_dtype,
-                 cudaStream_t s, int j_lo, int j_hi) {
+                 cudaStream_t s, int j_lo, int j_hi, const double *corr) {
     const DevStep &st = p.steps[st_i];
     const View v = view_of(p, st_i);
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
     if (j_hi < 0 || j_hi > v.n0) j_hi = v.n0;
     const double frac = (double)(j_hi - j_lo) / v.n0;
-    KPROF("k_level_final", frac * (8.0 * nc + 8.0 * (nf - nc) + (out_dtype == 0 ? 4.0 : 8.0) * nf), s);
+    KPROF("k_level_final", frac * ((corr ? 16.0 : 8.0) * nc + 8.0 * (nf - nc) + (out_dtype == 0 ? 4.0 : 8.0) * nf), s);
     if (out_dtype == 0)
-        launch_final<float>(v.act, cv, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, coef, (float *)D, j_lo,
+        launch_final<float>(v.act, cv, corr, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, coef, (float *)D, j_lo,
                             j_hi - j_lo, s);
     else
-        launch_final<double>(v.act, cv, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, coef, (double *)D, j_lo,
+        launch_final<double>(v.act, cv, corr, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, coef, (double *)D, j_lo,
                              j_hi - j_lo, s);
 }
 

@@ -53,8 +53,9 @@ void fused_pass2(const DevPlan &p, int st_i, const double *Z0, double *B, cudaSt
                  int p_hi = -1);
 // Output planes of pass 1 along axis 0 (coarse count, or the fine count when axis 0 is inactive).
 int fused_out_planes(const DevPlan &p, int st_i);
-// D = P(cv) + mc on the fine level; out_dtype 0 writes float, otherwise double.
+// D = P(cv) + mc on the fine level; out_dtype 0 writes float, otherwise double.  With corr the coarse
+// values are cv - corr (transform.py:345, coarse - correction), formed as they are read.
 void fused_final(const DevPlan &p, int st_i, const double *cv, const double *coef, void *D, int out_dtype,
-                 cudaStream_t s, int j_lo = 0, int j_hi = -1);
+                 cudaStream_t s, int j_lo = 0, int j_hi = -1, const double *corr = nullptr);
 
 }  // namespace hpdr

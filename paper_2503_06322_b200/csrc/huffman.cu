@@ -43,13 +43,23 @@ void mk_lengths(std::vector<int64_t> &a) {
 }  // namespace
 
 int canonical_codes(const uint8_t *lengths, uint32_t dict_size, uint32_t *codes) {
-    std::vector<uint32_t> order;
+    // (length, key) order by a counting sort over the lengths (huffman.py:188-204)
+    uint32_t start[256] = {0};
     for (uint32_t k = 0; k < dict_size; k++) {
         codes[k] = 0;
-        if (lengths[k]) order.push_back(k);
+        start[lengths[k]]++;
     }
-    if (order.empty()) return HPDR_OK;
-    std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return lengths[x] < lengths[y]; });
+    uint32_t acc = 0;
+    for (int L = 1; L < 256; L++) {
+        const uint32_t c = start[L];
+        start[L] = acc;
+        acc += c;
+    }
+    if (!acc) return HPDR_OK;
+    static thread_local std::vector<uint32_t> order;
+    order.resize(acc);
+    for (uint32_t k = 0; k < dict_size; k++)
+        if (lengths[k]) order[start[lengths[k]]++] = k;
     uint64_t code = 0;
     int prev = lengths[order[0]];
     for (uint32_t k : order) {
@@ -67,25 +77,53 @@ int canonical_codes(const uint8_t *lengths, uint32_t dict_size, uint32_t *codes)
 }
 
 int build_codebook(const uint64_t *counts, uint32_t dict_size, uint8_t *lengths, uint32_t *codes, std::string &err) {
-    std::vector<uint32_t> present;
+    // Present keys in stable ascending (count, key) order (huffman.py:174): the composite
+    // count << 16 | key (keys < 2^16) sorted by an LSD radix sort over the bits in use.
+    static thread_local std::vector<uint64_t> v, tmp;
+    static thread_local std::vector<int64_t> a;
+    v.clear();
+    uint64_t mx = 0;
     for (uint32_t k = 0; k < dict_size; k++) {
         lengths[k] = 0;
         codes[k] = 0;
-        if (counts[k]) present.push_back(k);
+        if (counts[k]) {
+            v.push_back((counts[k] << 16) | k);
+            mx = std::max<uint64_t>(mx, counts[k]);
+        }
     }
-    if (present.empty()) { err = "frequency table has no nonzero counts"; return HPDR_ERR_VALIDATION; }
-    if (present.size() == 1) { lengths[present[0]] = 1; return HPDR_OK; }
-    // stable ascending (count, key) order, huffman.py:174
-    std::stable_sort(present.begin(), present.end(), [&](uint32_t x, uint32_t y) { return counts[x] < counts[y]; });
-    std::vector<int64_t> a(present.size());
-    for (size_t i = 0; i < present.size(); i++) a[i] = (int64_t)counts[present[i]];
-    mk_lengths(a);
-    const int64_t mx = *std::max_element(a.begin(), a.end());
-    if (mx > kMaxCodeLen) {
-        err = "codeword length " + std::to_string(mx) + " exceeds " + std::to_string(kMaxCodeLen);
+    const size_t n = v.size();
+    if (n == 0) { err = "frequency table has no nonzero counts"; return HPDR_ERR_VALIDATION; }
+    if (n == 1) { lengths[v[0] & 0xffff] = 1; return HPDR_OK; }
+    if (mx >> 48) {   // counts beyond 2^48: comparison sort on (count, key)
+        std::vector<uint32_t> present;
+        for (uint32_t k = 0; k < dict_size; k++)
+            if (counts[k]) present.push_back(k);
+        std::stable_sort(present.begin(), present.end(), [&](uint32_t x, uint32_t y) { return counts[x] < counts[y]; });
+        a.resize(n);
+        for (size_t i = 0; i < n; i++) a[i] = (int64_t)counts[present[i]];
+        mk_lengths(a);
+        for (size_t i = 0; i < n; i++) lengths[present[i]] = (uint8_t)std::min<int64_t>(a[i], 255);
+    } else {
+        int bits = 16;
+        while (bits < 64 && (mx >> (bits - 16))) bits++;
+        tmp.resize(n);
+        for (int sh = 0; sh < bits; sh += 11) {
+            uint32_t c[2049] = {0};
+            for (size_t i = 0; i < n; i++) c[((v[i] >> sh) & 2047) + 1]++;
+            for (int d = 0; d < 2048; d++) c[d + 1] += c[d];
+            for (size_t i = 0; i < n; i++) tmp[c[(v[i] >> sh) & 2047]++] = v[i];
+            v.swap(tmp);
+        }
+        a.resize(n);
+        for (size_t i = 0; i < n; i++) a[i] = (int64_t)(v[i] >> 16);
+        mk_lengths(a);
+        for (size_t i = 0; i < n; i++) lengths[v[i] & 0xffff] = (uint8_t)std::min<int64_t>(a[i], 255);
+    }
+    const int64_t mxl = *std::max_element(a.begin(), a.begin() + n);
+    if (mxl > kMaxCodeLen) {
+        err = "codeword length " + std::to_string(mxl) + " exceeds " + std::to_string(kMaxCodeLen);
         return HPDR_ERR_VALIDATION;
     }
-    for (size_t i = 0; i < present.size(); i++) lengths[present[i]] = (uint8_t)a[i];
     return canonical_codes(lengths, dict_size, codes);
 }
 
@@ -199,7 +237,8 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const uint32_t *__restri
 }  // namespace
 
 void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict_size, const uint8_t *lengths,
-                   const uint32_t *codes, EncodeResult &res, cudaStream_t s, const EncodeHooks *hooks) {
+                   const uint32_t *codes, EncodeResult &res, cudaStream_t s, const EncodeHooks *hooks,
+                   const uint64_t *hist) {
     const int64_t units = (n + kBlockSymbols - 1) / kBlockSymbols;
     res.n_units = units;
     uint8_t *d_len = (uint8_t *)ctx->dbuf("enc_len", dict_size + 16);
@@ -229,11 +268,18 @@ void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict
     const int G = hooks && hooks->groups > 1 ? (int)std::min<int64_t>(hooks->groups, std::max<int64_t>(1, units)) : 1;
     std::vector<int64_t> ub(G + 1);
     for (int g = 0; g <= G; g++) ub[g] = units * g / G;
-    uint64_t *h = (uint64_t *)ctx->hbuf("enc_total", 8 * (G + 2));
-    for (int g = 0; g <= G; g++) small_copy(h + g, uoff + ub[g], 8, s);
-    CUDA_CHECK(cudaStreamSynchronize(s));
-    res.total_bits = h[G];
-    std::vector<uint64_t> gbit(h, h + G + 1);
+    std::vector<uint64_t> gbit(G + 1, 0);
+    if (hist && G == 1) {   // sum of count x length: the stream size is known without waiting for the scan
+        uint64_t tot = 0;
+        for (uint32_t k = 0; k < dict_size; k++) tot += hist[k] * lengths[k];
+        res.total_bits = gbit[1] = tot;
+    } else {   // group boundaries (bit offsets) for the streamed fetch
+        uint64_t *h = (uint64_t *)ctx->hbuf("enc_total", 8 * (G + 2));
+        for (int g = 0; g <= G; g++) small_copy(h + g, uoff + ub[g], 8, s);
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        res.total_bits = h[G];
+        gbit.assign(h, h + G + 1);
+    }
     const size_t words = (size_t)((res.total_bits + 31) / 32) + 2;
     res.d_words = (uint32_t *)ctx->dbuf(ctx->oname("enc_words"), words * 4);
     res.d_offsets = uoff;

@@ -480,7 +480,10 @@ void launch_pass1_quad(const TIn *F, int n0, int n1, int n2, const DevAxis &a0, 
     static const int slab_env = getenv("HPDR_QUAD_SLABS") ? atoi(getenv("HPDR_QUAD_SLABS")) : 0;
     const int64_t want = 148LL * 4 * 8;   // >= 8 waves of 4 resident blocks per SM
     int slabs = slab_env > 0 ? slab_env : (int)((want + (int64_t)gx * gy - 1) / ((int64_t)gx * gy));
-    slabs = std::max(1, std::min(slabs, std::max(1, c_count / 8)));
+    // >= 8 coarse planes per slab when that still fills the GPU; small grids (latency-bound marches)
+    // go down to 2
+    const int min_planes = (int64_t)gx * gy * std::max(1, c_count / 8) >= want ? 8 : 2;
+    slabs = std::max(1, std::min(slabs, std::max(1, c_count / min_planes)));
     const dim3 grid(gx, gy, (unsigned)slabs);
     const int z0_vec = ((int64_t)n1 * n2 % 2 == 0 && n2 % 2 == 0) ? 1 : 0;
     CUtensorMap tm;

@@ -10,7 +10,15 @@ namespace {
 
 constexpr int kQThreads = 256;
 constexpr int kSmemHistMax = 16384;          // u32 shared counters (64 KB)
-constexpr int kChunkWords = 1024;            // outlier-mask words per compaction block
+constexpr int kChunkWords = 1024;            // outlier-mask words per compaction block (large masks)
+
+// Compaction block size: 1024 mask words, down to 256 (one scan step) for small masks so that the
+// latency-bound compaction still spreads over every SM.
+int chunk_words(int64_t words) {
+    int cw = kChunkWords;
+    while (cw > 256 && words / cw < 2 * kNumSMs) cw /= 2;
+    return cw;
+}
 constexpr double kBinLimit = 4611686018427387904.0;   // 2^62, quantize.py:21
 
 struct Coarsest {
@@ -108,12 +116,12 @@ __global__ void __launch_bounds__(kQThreads) k_quantize(const double *__restrict
     }
 }
 
-__global__ void k_chunk_counts(const uint32_t *__restrict__ omask, int64_t words, unsigned long long *__restrict__ counts) {
+__global__ void k_chunk_counts(const uint32_t *__restrict__ omask, int64_t words, int cw, unsigned long long *__restrict__ counts) {
     typedef cub::BlockReduce<unsigned, 256> BR;
     __shared__ typename BR::TempStorage tmp;
     const int64_t c = blockIdx.x;
     unsigned s = 0;
-    for (int64_t w = c * kChunkWords + threadIdx.x; w < min64(words, (c + 1) * kChunkWords); w += blockDim.x)
+    for (int64_t w = c * cw + threadIdx.x; w < min64(words, (c + 1) * cw); w += blockDim.x)
         s += __popc(omask[w]);
     unsigned tot = BR(tmp).Sum(s);
     if (threadIdx.x == 0) counts[c] = tot;
@@ -122,7 +130,7 @@ __global__ void k_chunk_counts(const uint32_t *__restrict__ omask, int64_t words
 // Ordered outlier compaction (quantize.py:80-83: ascending flat index).  Per 256-word step the block
 // scans the words' popcounts; then each warp takes whole words with one lane per node, so the
 // index / bin writes and the sparse-bin reads are coalesced (consecutive positions / nodes).
-__global__ void k_write_outliers(const uint32_t *__restrict__ omask, int64_t words, const double *__restrict__ coef,
+__global__ void k_write_outliers(const uint32_t *__restrict__ omask, int64_t words, int cw, const double *__restrict__ coef,
                                  const long long *__restrict__ sparse, double bin, const unsigned long long *__restrict__ chunk_off,
                                  uint64_t *__restrict__ oidx, int64_t *__restrict__ obins) {
     typedef cub::BlockScan<unsigned, 256> BS;
@@ -132,8 +140,8 @@ __global__ void k_write_outliers(const uint32_t *__restrict__ omask, int64_t wor
     const int64_t c = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned long long base = chunk_off[c];
-    const int64_t w_end = min64(words, (c + 1) * kChunkWords);
-    for (int64_t w0 = c * kChunkWords; w0 < w_end; w0 += blockDim.x) {
+    const int64_t w_end = min64(words, (c + 1) * cw);
+    for (int64_t w0 = c * cw; w0 < w_end; w0 += blockDim.x) {
         const int64_t w = w0 + threadIdx.x;
         const uint32_t m = w < w_end ? omask[w] : 0u;
         if (!__syncthreads_or(m != 0u)) continue;   // no outlier in these 256 words (the common case)
@@ -189,12 +197,9 @@ __global__ void k_histogram(const uint32_t *__restrict__ keys, int64_t n, uint32
 void quantize_device(hpdr_ctx *ctx, const double *coef, int64_t n, const std::vector<int64_t> &coarsest,
                      double bin_width, uint32_t dict_size, uint32_t *keys, QuantResult &res, cudaStream_t s) {
     const int64_t words = (n + 31) / 32;
-    const int64_t chunks = (words + kChunkWords - 1) / kChunkWords;
     uint32_t *omask = (uint32_t *)ctx->dbuf("omask", words * 4);
     unsigned long long *hist = (unsigned long long *)ctx->dbuf("hist", (size_t)dict_size * 8);
     int *flags = (int *)ctx->dbuf("qflags", 16);
-    unsigned long long *ccount = (unsigned long long *)ctx->dbuf("ochunk", (chunks + 1) * 8);
-    unsigned long long *coff = (unsigned long long *)ctx->dbuf("ochunk_off", (chunks + 1) * 8);
     zero_async(hist, (size_t)dict_size * 8, s);
     zero_async(flags, 16, s);
     Coarsest co;
@@ -215,7 +220,8 @@ void quantize_device(hpdr_ctx *ctx, const double *coef, int64_t n, const std::ve
 void quantize_finish(hpdr_ctx *ctx, int64_t n, uint32_t dict_size, double bin_width, const double *coef,
                      const long long *obins_sparse, QuantResult &res, cudaStream_t s) {
     const int64_t words = (n + 31) / 32;
-    const int64_t chunks = (words + kChunkWords - 1) / kChunkWords;
+    const int cw = chunk_words(words);
+    const int64_t chunks = (words + cw - 1) / cw;
     uint32_t *omask = (uint32_t *)ctx->dbuf("omask", words * 4);
     unsigned long long *hist = (unsigned long long *)ctx->dbuf("hist", (size_t)dict_size * 8);
     int *flags = (int *)ctx->dbuf("qflags", 16);
@@ -223,7 +229,7 @@ void quantize_finish(hpdr_ctx *ctx, int64_t n, uint32_t dict_size, double bin_wi
     unsigned long long *coff = (unsigned long long *)ctx->dbuf("ochunk_off", (chunks + 1) * 8);
     {
         KPROF("k_chunk_counts", 4.0 * words, s);
-        k_chunk_counts<<<(unsigned)chunks, 256, 0, s>>>(omask, words, ccount);
+        k_chunk_counts<<<(unsigned)chunks, 256, 0, s>>>(omask, words, cw, ccount);
         LAUNCH_CHECK();
     }
     size_t tmp_bytes = 0;
@@ -247,7 +253,7 @@ void quantize_finish(hpdr_ctx *ctx, int64_t n, uint32_t dict_size, double bin_wi
     res.d_outlier_bins = (int64_t *)ctx->dbuf(ctx->oname("obins"), res.n_outliers * 8);
     if (res.n_outliers) {
         KPROF("k_write_outliers", 4.0 * words + 24.0 * res.n_outliers, s);
-        k_write_outliers<<<(unsigned)chunks, 256, 0, s>>>(omask, words, coef, obins_sparse, bin_width, coff,
+        k_write_outliers<<<(unsigned)chunks, 256, 0, s>>>(omask, words, cw, coef, obins_sparse, bin_width, coff,
                                                           res.d_outlier_idx, res.d_outlier_bins);
         LAUNCH_CHECK();
     }

@@ -55,7 +55,8 @@ struct EncodeHooks {
     std::function<void(int, uint64_t, uint64_t)> group_done;
 };
 void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict_size, const uint8_t *lengths,
-                   const uint32_t *codes, EncodeResult &res, cudaStream_t s, const EncodeHooks *hooks = nullptr);
+                   const uint32_t *codes, EncodeResult &res, cudaStream_t s, const EncodeHooks *hooks = nullptr,
+                   const uint64_t *hist = nullptr);   // host histogram: total bits without a device read-back
 
 // ---- huffman.py:207-358 (device) ---------------------------------------------------
 struct DecodeJob {

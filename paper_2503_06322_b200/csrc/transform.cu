@@ -575,15 +575,45 @@ __global__ void __launch_bounds__(32) k_thomas_tile(double *__restrict__ arr, in
             }
         }
         __syncwarp();
-        // write back
+        // write back (with the coarse + corr epilogue the coarse values of 8 elements are loaded
+        // together, ahead of their stores)
         if (CONTIG) {
-            for (int l = 0; l < nl; l++) {
-                const int64_t o = (l0 + l) * (int64_t)n;
-                for (int i = lane; i < n; i += 32) epi_store<EPI>(arr, o + i, at(l, i), epi);
+            const int tot = nl * n;
+            const int64_t o = l0 * (int64_t)n;   // the tile's lines are contiguous
+            for (int j0 = lane; j0 < tot; j0 += 32 * 8) {
+                double cv[8];
+                if (EPI) {
+#pragma unroll
+                    for (int k = 0; k < 8; k++) {
+                        const int j = j0 + 32 * k;
+                        cv[k] = j < tot ? __ldg(epi.base + o + j) : 0.0;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    const int j = j0 + 32 * k;
+                    if (j < tot) {
+                        const int l = j / n, i = j - l * n;
+                        if (EPI) epi.dst[o + j] = dadd(cv[k], at(l, i));
+                        else arr[o + j] = at(l, i);
+                    }
+                }
             }
         } else if (lane < nl) {
             const int64_t o = p * (int64_t)n * inner + q0 + lane;
-            for (int i = 0; i < n; i++) epi_store<EPI>(arr, o + (int64_t)i * inner, at(lane, i), epi);
+            for (int i0 = 0; i0 < n; i0 += 8) {
+                double cv[8];
+                if (EPI) {
+#pragma unroll
+                    for (int k = 0; k < 8; k++) cv[k] = i0 + k < n ? __ldg(epi.base + o + (int64_t)(i0 + k) * inner) : 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; k++)
+                    if (i0 + k < n) {
+                        if (EPI) epi.dst[o + (int64_t)(i0 + k) * inner] = dadd(cv[k], at(lane, i0 + k));
+                        else arr[o + (int64_t)(i0 + k) * inner] = at(lane, i0 + k);
+                    }
+            }
         }
         __syncwarp();
     }
@@ -617,15 +647,44 @@ __global__ void k_selftest_div(uint64_t n, uint64_t seed, unsigned long long *mi
 // same recurrence and rounding as k_thomas_reg.  Replaces up to 3 latency-bound launches per small
 // level (the coarse end of every hierarchy, and every level of a thin pipeline chunk).
 constexpr int kThomasSmallMax = 16384;   // doubles (128 KB of shared memory)
+constexpr int kThomasSmallTabs = 8192;   // staged table doubles (64 KB)
 
 struct AxesArg {
     DevAxis ax[4];
 };
 
 template <bool EPI>
-__global__ void __launch_bounds__(512) k_thomas_small(double *__restrict__ arr, Shape4 sh, AxesArg A, Epi epi) {
+__global__ void __launch_bounds__(512) k_thomas_small(double *__restrict__ arr, Shape4 sh, AxesArg A, Epi epi,
+                                                      int stage_tabs) {
     extern __shared__ double g[];
     const int64_t N = sh.size();
+    // the axes' (w, b', u) tables ride along in shared memory (loaded together with the grid, so the
+    // recurrences never wait on a cold table load)
+    double *tabs = g + N;
+    const double *tw[4], *tb[4], *tu[4], *tr[4];
+    {
+        int off = 0;
+        for (int a = 0; a < 4; a++) {
+            const DevAxis &ax = A.ax[a];
+            tw[a] = ax.tw;
+            tb[a] = ax.tb;
+            tu[a] = ax.tu;
+            tr[a] = ax.tr;
+            if (!ax.active || !stage_tabs) continue;
+            const int n = ax.nc;
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                tabs[off + i] = __ldg(ax.tw + i);
+                tabs[off + n + i] = __ldg(ax.tb + i);
+                tabs[off + 2 * n + i] = __ldg(ax.tu + i);
+                tabs[off + 3 * n + i] = __ldg(ax.tr + i);
+            }
+            tw[a] = tabs + off;
+            tb[a] = tabs + off + n;
+            tu[a] = tabs + off + 2 * n;
+            tr[a] = tabs + off + 3 * n;
+            off += 4 * n;
+        }
+    }
     for (int64_t i = threadIdx.x; i < N; i += blockDim.x) g[i] = arr[i];
     __syncthreads();
     for (int a = 0; a < 4; a++) {
@@ -635,19 +694,26 @@ __global__ void __launch_bounds__(512) k_thomas_small(double *__restrict__ arr, 
         for (int d = 0; d < a; d++) outer *= sh.n[d];
         for (int d = a + 1; d < 4; d++) inner *= sh.n[d];
         const int n = ax.nc;
+        const double *W = tw[a], *B = tb[a], *U = tu[a], *Rr = tr[a];
+        // verified fast division (div_fast), exact __ddiv_rn for the rare operand it cannot certify
+        auto div = [](double x, double b, double r) {
+            bool bad = false;
+            const double q = div_fast(x, b, r, bad);
+            return bad ? ddiv(x, b) : q;
+        };
         const int64_t lines = outer * inner;
         for (int64_t ln = threadIdx.x; ln < lines; ln += blockDim.x) {
             const int64_t p = ln / inner, q = ln - p * inner;
             double *x = g + p * (int64_t)n * inner + q;
             double prev = x[0];
             for (int i = 1; i < n; i++) {
-                prev = dsub(x[(int64_t)i * inner], dmul(__ldg(ax.tw + i), prev));
+                prev = dsub(x[(int64_t)i * inner], dmul(W[i], prev));
                 x[(int64_t)i * inner] = prev;
             }
-            double last = ddiv(prev, __ldg(ax.tb + n - 1));
+            double last = div(prev, B[n - 1], Rr[n - 1]);
             x[(int64_t)(n - 1) * inner] = last;
             for (int i = n - 2; i >= 0; i--) {
-                last = ddiv(dsub(x[(int64_t)i * inner], dmul(__ldg(ax.tu + i), last)), __ldg(ax.tb + i));
+                last = div(dsub(x[(int64_t)i * inner], dmul(U[i], last)), B[i], Rr[i]);
                 x[(int64_t)i * inner] = last;
             }
         }
@@ -1251,14 +1317,20 @@ void thomas_all(const DevPlan &p, int st_i, double *T, cudaStream_t s, const dou
         static bool attr = false;
         if (!attr) {
             for (auto f : {k_thomas_small<false>, k_thomas_small<true>})
-                CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kThomasSmallMax * 8));
+                CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (kThomasSmallMax + kThomasSmallTabs) * 8));
             attr = true;
         }
         AxesArg A;
         for (int a = 0; a < 4; a++) A.ax[a] = st.ax[a];
+        int tab = 0;
+        for (int a = 0; a < 4; a++)
+            if (st.ax[a].active) tab += 4 * st.ax[a].nc;
+        const int stage = tab <= kThomasSmallTabs ? 1 : 0;
+        const size_t smem = (size_t)(sh.size() + (stage ? tab : 0)) * 8;
         KPROF("k_thomas_small", (add_dst ? 24.0 : 16.0) * sh.size(), s);
-        if (add_dst) k_thomas_small<true><<<1, 512, (size_t)sh.size() * 8, s>>>(T, sh, A, epi);
-        else k_thomas_small<false><<<1, 512, (size_t)sh.size() * 8, s>>>(T, sh, A, epi);
+        if (add_dst) k_thomas_small<true><<<1, 512, smem, s>>>(T, sh, A, epi, stage);
+        else k_thomas_small<false><<<1, 512, smem, s>>>(T, sh, A, epi, stage);
         LAUNCH_CHECK();
         return;
     }
@@ -1364,12 +1436,7 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
             fused_pass2(p, st_i, Z0, b.t0, s);
             thomas_all(p, st_i, b.t0, s);
         }
-        const int64_t nc = st.csh.size();
-        {
-            KPROF("k_sub", 24.0 * nc, s);
-            k_sub<<<grid_for(nc, 256, 148 * 16), 256, 0, s>>>(Dc, T, b.cg, nc);   // coarse - corr
-            LAUNCH_CHECK();
-        }
+        // coarse - corr is formed inside the final level kernel as it reads the coarse values
         if (st_i == 0) phase_mark("coarse_levels_done", s);
         if (st_i == 0 && direct && host_out) {
             // finest level in dim-0 slabs; each slab's D2H (copy stream) overlaps the next slab
@@ -1385,7 +1452,7 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
             int nslab = 0;
             for (int a = 0, k = 0; a < n0; a += chunk, k++, nslab++) {
                 const int e = std::min(n0, a + chunk);
-                fused_final(p, 0, b.cg, coef, out, out_dtype, s, a, e);
+                fused_final(p, 0, Dc, coef, out, out_dtype, s, a, e, T);
                 CUDA_CHECK(cudaEventRecord(ctx->event(EvSlabOut, k), s));
             }
             for (int a = 0, k = 0; k < nslab; a += chunk, k++) {
@@ -1400,9 +1467,9 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
             }
             CUDA_CHECK(cudaStreamSynchronize(ctx->d2h));
         } else if (st_i == 0 && direct) {
-            fused_final(p, st_i, b.cg, coef, out, out_dtype, s);
+            fused_final(p, st_i, Dc, coef, out, out_dtype, s, 0, -1, T);
         } else {
-            fused_final(p, st_i, b.cg, coef, level_ptr(b, p, st_i), 1, s);
+            fused_final(p, st_i, Dc, coef, level_ptr(b, p, st_i), 1, s, 0, -1, T);
         }
     }
     if (!direct) cast_output(b.lvl0, out, out_dtype, p.n_total, s);
