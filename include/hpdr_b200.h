@@ -71,6 +71,11 @@ void    *hpdr_host_alloc(uint64_t bytes);
 /* Host memcpy split across the library's copy threads (large results into Python-owned memory). */
 void     hpdr_host_copy(void *dst, const void *src, uint64_t n);
 void     hpdr_host_free(void *p);
+/* First-touch a fresh pageable buffer on background threads (zero-filling it, huge pages where the
+ * kernel allows); returns a handle for hpdr_host_prefault_wait, which must return before anything
+ * else writes the buffer. */
+void    *hpdr_host_prefault_begin(void *p, uint64_t bytes);
+void     hpdr_host_prefault_wait(void *handle);
 /* Page-lock an existing host range (cudaHostRegister, portable) so transfers DMA straight from /
  * to it; returns HPDR_ERR_ALLOCATION on failure.  A range that is already registered is OK. */
 int      hpdr_host_register(void *p, uint64_t bytes);
@@ -87,6 +92,18 @@ int hpdr_mgard_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, cons
                         double range_max, void *out, uint64_t out_cap, uint64_t *blob_len);
 /* Copy the last compressed blob into out (host or device pointer). */
 int hpdr_mgard_fetch(hpdr_ctx *ctx, void *out, uint64_t out_cap);
+
+/* Destination allocator: a writable buffer of `bytes` (pageable or pinned host, or device), or
+ * NULL on failure. */
+typedef void *(*hpdr_alloc_fn)(void *user, uint64_t bytes);
+/* mgard_compress (codec.py:25-56) into a buffer the caller allocates through alloc(user, size)
+ * as soon as the blob size is known (the codebook fixes it, before the payload is packed); the
+ * blob then streams into it behind the encode launches.  alloc is called exactly once on
+ * success.  Replaces the compress + fetch pair for callers that must own a fresh result object
+ * (the reference returns a new `bytes`). */
+int hpdr_mgard_compress_alloc(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims,
+                              double eb_rel, uint32_t dict_size, int has_range, double range_min,
+                              double range_max, hpdr_alloc_fn alloc, void *user, uint64_t *blob_len);
 
 /* Parse the blob header: dtype code, rank and dims (codec.py:62-84). */
 int hpdr_mgard_peek(const void *blob, uint64_t len, int *dtype, int *rank, uint64_t *dims);

@@ -34,11 +34,15 @@ _SIGS = {
     "hpdr_host_alloc": (C.c_void_p, [C.c_uint64]),
     "hpdr_host_copy": (None, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "hpdr_host_free": (None, [C.c_void_p]),
+    "hpdr_host_prefault_begin": (C.c_void_p, [C.c_void_p, C.c_uint64]),
+    "hpdr_host_prefault_wait": (None, [C.c_void_p]),
     "hpdr_host_register": (C.c_int, [C.c_void_p, C.c_uint64]),
     "hpdr_host_unregister": (None, [C.c_void_p]),
     "hpdr_mgard_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _u64p, C.c_double, C.c_uint32,
                                       C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_uint64, _u64p]),
     "hpdr_mgard_fetch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
+    "hpdr_mgard_compress_alloc": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _u64p, C.c_double, C.c_uint32,
+                                            C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_void_p, _u64p]),
     "hpdr_mgard_peek": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_int), C.POINTER(C.c_int), _u64p]),
     "hpdr_mgard_decompress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
     "hpdr_decompose": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _u64p, C.c_void_p, _dp, _dp]),
@@ -240,6 +244,71 @@ def bytes_from(buf: np.ndarray, n: int) -> bytes:
     if n:
         lib().hpdr_host_copy(C.c_void_p(p), C.c_void_p(buf.ctypes.data), int(n))
     return b
+
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_void_p, C.c_uint64)   # hpdr_alloc_fn
+
+
+_pybytes_resize = C.pythonapi._PyBytes_Resize
+_pybytes_resize.argtypes = [C.POINTER(C.py_object), C.c_ssize_t]
+_pybytes_resize.restype = C.c_int
+
+
+class BytesSink:
+    """hpdr_alloc_fn that hands the library the result ``bytes`` once the blob size is known.
+
+    With ``hint`` (the size of a previous blob of the same shape) a slightly larger bytes object is
+    created up front and first-touched on background threads while the GPU works (a fresh
+    destination otherwise pays its page faults inside the staged copy); ``take`` then trims it to
+    the exact size in place (``_PyBytes_Resize``: a shrinking realloc, no copy)."""
+
+    MIN_HINT = 64 << 20
+
+    def __init__(self, hint: int = 0):
+        self.obj = None
+        self.n = 0
+        self.fn = ALLOC_FN(self._alloc)
+        self._pre = None   # (bytes, address, capacity, prefault handle)
+        if hint >= self.MIN_HINT:
+            cap = int(hint * 1.02) + (1 << 20)
+            try:
+                b, p = new_bytes(cap)
+            except MemoryError:
+                return
+            self._pre = (b, p, cap, lib().hpdr_host_prefault_begin(C.c_void_p(p), cap))
+
+    def _join(self):
+        if self._pre is not None and self._pre[3]:
+            lib().hpdr_host_prefault_wait(C.c_void_p(self._pre[3]))
+            self._pre = self._pre[:3] + (None,)
+
+    def _alloc(self, _user, n):
+        self.n = int(n)
+        try:
+            self._join()
+            if self._pre is not None and n <= self._pre[2]:
+                self.obj, p = self._pre[0], self._pre[1]
+                self._pre = None
+                return p
+            self._pre = None
+            self.obj, p = new_bytes(n)
+            return p
+        except MemoryError:
+            return None
+
+    def take(self):
+        """The result: exactly ``n`` bytes."""
+        self._join()
+        self._pre = None
+        obj, self.obj = self.obj, None
+        if obj is None or len(obj) == self.n:
+            return obj
+        box = C.py_object(obj)
+        del obj
+        # the box must hold the only reference (getrefcount adds the temporary of box.value)
+        if sys.getrefcount(box.value) == 2 and _pybytes_resize(C.byref(box), self.n) == 0:
+            return box.value
+        return bytes(memoryview(box.value)[: self.n])
 
 
 def new_bytes(n: int):

@@ -373,7 +373,7 @@ __global__ void k_gather_vals(const double *__restrict__ src, const long long *_
 void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t *dims, double eb_rel,
                  uint32_t dict_size, double u_min, double u_max, double eb_abs, double bin, const QuantResult &q,
                  uint32_t *keys, const double *d_coarse, const double *coef_for_coarse, void *fetch_out,
-                 uint64_t fetch_cap, bool coarse_ready = false) {
+                 uint64_t fetch_cap, bool coarse_ready = false, const OutAlloc *alloc = nullptr) {
     {
         const int64_t N = p.n_total;
         const int L = p.host.L;
@@ -422,11 +422,23 @@ void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t 
         EncodeHooks hooks;
         bool streamed_fetch = false;
         uint64_t pay_pos = 0;
-        const MemKind ok = fetch_out ? classify(fetch_out) : MemKind::Host;
-        if (fetch_out && ok != MemKind::Host) {
+        MemKind ok = fetch_out ? classify(fetch_out) : MemKind::Host;
+        // pageable destinations (the drop-in's Python bytes, allocated through `alloc` once the size is
+        // known): the head and each payload group go out through the pinned staging ring after the
+        // encode launches are all enqueued (host-blocking copies must not hold up the launches)
+        std::vector<std::pair<uint64_t, uint64_t>> pg_ranges;
+        std::vector<int> pg_groups;
+        hpdr_ctx::Pending PQ;
+        if ((fetch_out && ok != MemKind::Host) || (!fetch_out && alloc)) {
             hooks.groups = N >= (16LL << 20) ? 8 : 1;   // small streams: one launch, no group read-back
             hooks.ready = [&](const EncodeResult &e) {
                 const uint64_t total = P.head.size() + 16 * P.n_out + P.mid.size() + 8 * e.n_units + 8 + (e.total_bits + 7) / 8;
+                if (!fetch_out) {
+                    fetch_out = alloc->fn(alloc->user, total);
+                    if (!fetch_out) fail(HPDR_ERR_ALLOCATION, "output allocation failed");
+                    fetch_cap = total;
+                    ok = classify(fetch_out);
+                }
                 if (fetch_cap < total) return;
                 streamed_fetch = true;
                 hpdr_ctx::Pending Q = P;
@@ -437,18 +449,33 @@ void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t 
                 Q.valid = true;
                 CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
                 CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(0), 0));
-                pay_pos = fetch_pending(ctx, Q, fetch_out, fetch_cap, ctx->d2h, false, /*payload=*/false);
+                if (ok == MemKind::Host) PQ = Q;   // pageable: after the launches
+                else pay_pos = fetch_pending(ctx, Q, fetch_out, fetch_cap, ctx->d2h, false, /*payload=*/false);
             };
             hooks.group_done = [&](int g, uint64_t lo, uint64_t hi) {
                 if (!streamed_fetch || hi <= lo) return;
                 CUDA_CHECK(cudaEventRecord(ctx->event(EvEncGroup, g), s));
+                if (ok == MemKind::Host) {
+                    pg_ranges.emplace_back(lo, hi);
+                    pg_groups.push_back(g);
+                    return;
+                }
                 CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(EvEncGroup, g), 0));
                 const bool dev = ok == MemKind::Device;
                 CUDA_CHECK(cudaMemcpyAsync((char *)fetch_out + pay_pos + lo, (const char *)ctx->dbuf(ctx->oname("enc_words"), 16) + lo,
                                            hi - lo, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->d2h));
             };
         }
-        huffman_stage(ctx, keys, N, dict_size, q.hist, P.mid, enc, single, s, fetch_out ? &hooks : nullptr);
+        huffman_stage(ctx, keys, N, dict_size, q.hist, P.mid, enc, single, s,
+                      (fetch_out || alloc) ? &hooks : nullptr);
+        if (streamed_fetch && ok == MemKind::Host) {
+            pay_pos = fetch_pending(ctx, PQ, fetch_out, fetch_cap, ctx->d2h, false, /*payload=*/false);
+            const char *words = (const char *)ctx->dbuf(ctx->oname("enc_words"), 16);
+            std::vector<StageRange> rs;
+            for (size_t g = 0; g < pg_ranges.size(); g++)
+                rs.push_back({pg_ranges[g].first, pg_ranges[g].second, ctx->event(EvEncGroup, pg_groups[g])});
+            stage_d2h_ranges(ctx, (char *)fetch_out + pay_pos, words, rs, ctx->d2h);
+        }
         phase_mark("encoded", s);
         P.single_key = single;
         P.n_units = enc.n_units;
@@ -465,7 +492,7 @@ void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t 
 // slot ctx->out_slot).  allow_stream: a host input may be streamed in dim-0 chunks.
 void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, double eb_rel,
                    uint32_t dict_size, int has_range, double range_min, double range_max, bool allow_stream,
-                   void *fetch_out, uint64_t fetch_cap) {
+                   void *fetch_out, uint64_t fetch_cap, const OutAlloc *alloc) {
     {
         ctx->pending.valid = false;
         if (dtype != 0 && dtype != 1) fail(HPDR_ERR_VALIDATION, "lossy compression needs F32/F64");
@@ -536,7 +563,7 @@ void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uin
             quantize_device(ctx, coef, N, p.host.coarsest, bin, dict_size, keys, q, s);
         }
         finish_blob(ctx, p, dtype, rank, dims, eb_rel, dict_size, u_min, u_max, eb_abs, bin, q, keys, d_coarse, nullptr,
-                    fetch_out, fetch_cap, coarse_ready);
+                    fetch_out, fetch_cap, coarse_ready, alloc);
     }
 }
 
@@ -587,11 +614,36 @@ int hpdr_mgard_compress(hpdr_ctx *ctx, const void *in, int dtype, int rank, cons
     return guard([&] {
         CUDA_CHECK(cudaSetDevice(ctx->device));
         ctx->out_slot = 0;
-        compress_core(ctx, in, dtype, rank, dims, eb_rel, dict_size, has_range, range_min, range_max, true, out, out_cap);
+        compress_core(ctx, in, dtype, rank, dims, eb_rel, dict_size, has_range, range_min, range_max, true, out, out_cap,
+                      nullptr);
         *blob_len = ctx->pending.total_len;
         if (ctx->pending.fetched) CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         else if (out && out_cap >= ctx->pending.total_len) fetch_pending(ctx, out, out_cap);
         else CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        phase_mark("fetched", ctx->stream);
+        phase_dump("mgard_compress");
+    });
+}
+
+int hpdr_mgard_compress_alloc(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, double eb_rel,
+                              uint32_t dict_size, int has_range, double range_min, double range_max,
+                              hpdr_alloc_fn alloc, void *user, uint64_t *blob_len) {
+    return guard([&] {
+        if (!alloc) fail(HPDR_ERR_VALIDATION, "alloc callback is required");
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        ctx->out_slot = 0;
+        const OutAlloc oa{alloc, user};
+        compress_core(ctx, in, dtype, rank, dims, eb_rel, dict_size, has_range, range_min, range_max, true, nullptr, 0,
+                      &oa);
+        *blob_len = ctx->pending.total_len;
+        if (ctx->pending.fetched) {
+            CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        } else {   // not streamed (single-key / generic paths): allocate now and copy out
+            void *dst = alloc(user, ctx->pending.total_len);
+            if (!dst && ctx->pending.total_len) fail(HPDR_ERR_ALLOCATION, "output allocation failed");
+            if (ctx->pending.total_len) fetch_pending(ctx, dst, ctx->pending.total_len);
+            else CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        }
         phase_mark("fetched", ctx->stream);
         phase_dump("mgard_compress");
     });

@@ -174,7 +174,7 @@ void zero_async(void *dst, size_t bytes, cudaStream_t s) {
 }
 
 namespace {
-constexpr size_t kStageChunk = 16u << 20;
+constexpr size_t kStageChunk = 32u << 20;   // 2 MB per copy thread
 constexpr unsigned kStageSlots = 4;
 // Host copy threads of this process: HPDR_COPY_THREADS, else the CPUs this process may run on
 // (its affinity mask -- a rank bound to its GPU's NUMA node sees that node's CPUs) divided among
@@ -201,7 +201,14 @@ struct CopyPool {
     std::vector<std::thread> th;
     char *dst = nullptr;
     const char *src = nullptr;
-    size_t n = 0, per = 0;
+    size_t n = 0, per = 0, align = 4096;
+    // slice boundary k (0..workers+1): on a page boundary of the destination, so every (huge) page
+    // of a fresh destination is first touched -- and faulted in -- by exactly one thread
+    size_t cut(int k) const {
+        if (k >= workers + 1) return n;
+        const uintptr_t b = (uintptr_t)dst, t = (b + (size_t)k * per + align - 1) & ~(uintptr_t)(align - 1);
+        return std::min(n, (size_t)(t - b));
+    }
     uint64_t gen = 0;
     int pending = 0, workers = 0;
     bool stop = false;
@@ -216,9 +223,9 @@ struct CopyPool {
                     seen = gen;
                     char *d = dst;
                     const char *s = src;
-                    const size_t a = (size_t)(i + 1) * per, nn = n;
+                    const size_t a = cut(i + 1), e = cut(i + 2);
                     lk.unlock();
-                    if (a < nn) memcpy(d + a, s + a, std::min(nn, a + per) - a);
+                    if (a < e) memcpy(d + a, s + a, e - a);
                     lk.lock();
                     if (--pending == 0) done_cv.notify_one();
                 }
@@ -240,12 +247,13 @@ struct CopyPool {
             dst = (char *)d;
             src = (const char *)s;
             n = nn;
-            per = ((nn + T - 1) / T + 4095) & ~size_t(4095);
+            per = (nn + T - 1) / T;
+            align = per >= (2u << 20) ? (2u << 20) : 4096;
             pending = workers;
             gen++;
         }
         cv.notify_all();
-        memcpy(d, s, std::min(nn, per));   // slice 0 on the calling thread
+        memcpy(d, s, cut(1));   // slice 0 on the calling thread
         std::unique_lock<std::mutex> lk(mu);
         done_cv.wait(lk, [&] { return pending == 0; });
     }
@@ -272,6 +280,40 @@ void stage_h2d(hpdr_ctx *ctx, void *dst, const void *src, size_t n, cudaStream_t
         parallel_memcpy(ring + slot * kStageChunk, (const char *)src + off, m);
         CUDA_CHECK(cudaMemcpyAsync((char *)dst + off, ring + slot * kStageChunk, m, cudaMemcpyHostToDevice, st));
         CUDA_CHECK(cudaEventRecord(ev, st));
+    }
+}
+
+void stage_d2h_ranges(hpdr_ctx *ctx, char *dst, const char *src, const std::vector<StageRange> &ranges,
+                      cudaStream_t st) {
+    // one continuous pass through the ring over every range (no drain between ranges); a range's
+    // first chunk waits on the range's event, so the copies follow the producer range by range
+    char *ring = (char *)ctx->hbuf("stage_out", kStageChunk * kStageSlots);
+    struct Chunk {
+        size_t off, len;
+        cudaEvent_t wait;
+    };
+    std::vector<Chunk> ch;
+    for (const StageRange &r : ranges) {
+        if (r.hi > r.lo && r.hi - r.lo >= (8u << 20)) {
+            const uintptr_t a = ((uintptr_t)(dst + r.lo) + (2u << 20) - 1) & ~uintptr_t((2u << 20) - 1);
+            const uintptr_t e = ((uintptr_t)(dst + r.hi)) & ~uintptr_t((2u << 20) - 1);
+            if (e > a) madvise((void *)a, e - a, MADV_HUGEPAGE);
+        }
+        for (size_t o = r.lo; o < r.hi; o += kStageChunk)
+            ch.push_back({o, std::min(kStageChunk, r.hi - o), o == r.lo ? r.ready : nullptr});
+    }
+    size_t issued = 0;
+    for (size_t done = 0; done < ch.size(); done++) {
+        for (; issued < ch.size() && issued < done + kStageSlots; issued++) {
+            const unsigned slot = (unsigned)(issued % kStageSlots);
+            if (ch[issued].wait) CUDA_CHECK(cudaStreamWaitEvent(st, ch[issued].wait, 0));
+            CUDA_CHECK(cudaMemcpyAsync(ring + slot * kStageChunk, src + ch[issued].off, ch[issued].len,
+                                       cudaMemcpyDeviceToHost, st));
+            CUDA_CHECK(cudaEventRecord(ctx->event(EvStageOut, slot), st));
+        }
+        const unsigned slot = (unsigned)(done % kStageSlots);
+        CUDA_CHECK(cudaEventSynchronize(ctx->event(EvStageOut, slot)));
+        parallel_memcpy(dst + ch[done].off, ring + slot * kStageChunk, ch[done].len);
     }
 }
 
@@ -640,6 +682,40 @@ void hpdr_ctx_set_range_hook(hpdr_ctx *c, hpdr_range_hook hook, void *user) {
 }
 
 void hpdr_host_copy(void *dst, const void *src, uint64_t n) { hpdr::parallel_memcpy(dst, src, n); }
+
+// First-touch a fresh pageable buffer on background threads (huge pages where the kernel allows),
+// so that a later staged copy into it runs at warm-memory speed.  The touch writes zeros: nothing
+// else may write the buffer before hpdr_host_prefault_wait returns.
+struct hpdr_prefault {
+    std::vector<std::thread> th;
+};
+
+void *hpdr_host_prefault_begin(void *p, uint64_t n) {
+    if (!p || !n) return nullptr;
+    const uintptr_t a = ((uintptr_t)p + (2u << 20) - 1) & ~uintptr_t((2u << 20) - 1);
+    const uintptr_t e = ((uintptr_t)p + n) & ~uintptr_t((2u << 20) - 1);
+    if (e > a) madvise((void *)a, e - a, MADV_HUGEPAGE);
+    auto *h = new hpdr_prefault;
+    const int T = std::max(1, std::min(4, hpdr::host_threads() / 4));   // light: the input DMA shares host memory
+    const size_t per = ((n + T - 1) / T + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
+    for (int t = 0; t < T; t++) {
+        const size_t lo = (size_t)t * per;
+        if (lo >= n) break;
+        const size_t hi = std::min<size_t>(n, lo + per);
+        h->th.emplace_back([p, lo, hi] {
+            char *c = (char *)p;
+            for (size_t o = lo; o < hi; o += 4096) c[o] = 0;
+        });
+    }
+    return h;
+}
+
+void hpdr_host_prefault_wait(void *handle) {
+    auto *h = (hpdr_prefault *)handle;
+    if (!h) return;
+    for (auto &t : h->th) t.join();
+    delete h;
+}
 
 void *hpdr_host_alloc(uint64_t bytes) {
     void *p = nullptr;

@@ -165,6 +165,14 @@ void zero_async(void *dst, size_t bytes, cudaStream_t s);
 void parallel_memcpy(void *dst, const void *src, size_t n);
 void stage_h2d(hpdr_ctx *ctx, void *dst, const void *src, size_t n, cudaStream_t st);
 void stage_d2h(hpdr_ctx *ctx, void *dst, const void *src, size_t n, cudaStream_t st);
+// Byte ranges [lo, hi) of src -> dst (pageable), each released by its event, through one
+// continuous pass of the pinned staging ring.
+struct StageRange {
+    size_t lo, hi;
+    cudaEvent_t ready;
+};
+void stage_d2h_ranges(hpdr_ctx *ctx, char *dst, const char *src, const std::vector<StageRange> &ranges,
+                      cudaStream_t st);
 // Store one 8-byte value to device memory in stream order (a kernel parameter, no staging copy).
 void store_u64(void *dst, uint64_t v, cudaStream_t s);
 // Relative mode: pass this block's min / max through the context's range hook (if any).

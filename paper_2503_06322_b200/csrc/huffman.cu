@@ -1,5 +1,7 @@
 // huffman.cu -- canonical Huffman: host codebook (huffman.py:107-204) and device
 // encode (huffman.py:228-289) / decode (huffman.py:207-358) kernels.
+#include <string.h>
+
 #include <algorithm>
 #include <type_traits>
 #include <cub/cub.cuh>
@@ -42,24 +44,22 @@ void mk_lengths(std::vector<int64_t> &a) {
 
 }  // namespace
 
-int canonical_codes(const uint8_t *lengths, uint32_t dict_size, uint32_t *codes) {
-    // (length, key) order by a counting sort over the lengths (huffman.py:188-204)
-    uint32_t start[256] = {0};
-    for (uint32_t k = 0; k < dict_size; k++) {
-        codes[k] = 0;
-        start[lengths[k]]++;
-    }
-    uint32_t acc = 0;
-    for (int L = 1; L < 256; L++) {
-        const uint32_t c = start[L];
+namespace {
+// Canonical codes in (length, key) order (huffman.py:188-204) over the present keys `keys`
+// (ascending): a counting sort by length, then the reference's code recurrence.
+int canonical_from(const uint8_t *lengths, const uint32_t *keys, size_t n, uint32_t *codes) {
+    if (!n) return HPDR_OK;
+    uint32_t cnt[4][256];   // interleaved counters: no store-to-load chain on runs of equal lengths
+    memset(cnt, 0, sizeof(cnt));
+    for (size_t i = 0; i < n; i++) cnt[i & 3][lengths[keys[i]]]++;
+    uint32_t start[256], acc = 0;
+    for (int L = 0; L < 256; L++) {
         start[L] = acc;
-        acc += c;
+        acc += cnt[0][L] + cnt[1][L] + cnt[2][L] + cnt[3][L];
     }
-    if (!acc) return HPDR_OK;
     static thread_local std::vector<uint32_t> order;
-    order.resize(acc);
-    for (uint32_t k = 0; k < dict_size; k++)
-        if (lengths[k]) order[start[lengths[k]]++] = k;
+    order.resize(n);
+    for (size_t i = 0; i < n; i++) order[start[lengths[keys[i]]]++] = keys[i];
     uint64_t code = 0;
     int prev = lengths[order[0]];
     for (uint32_t k : order) {
@@ -75,56 +75,80 @@ int canonical_codes(const uint8_t *lengths, uint32_t dict_size, uint32_t *codes)
     }
     return HPDR_OK;
 }
+}  // namespace
+
+int canonical_codes(const uint8_t *lengths, uint32_t dict_size, uint32_t *codes) {
+    static thread_local std::vector<uint32_t> keys;
+    keys.resize(dict_size);
+    size_t n = 0;
+    for (uint32_t k = 0; k < dict_size; k++) {
+        codes[k] = 0;
+        keys[n] = k;
+        n += lengths[k] != 0;
+    }
+    return canonical_from(lengths, keys.data(), n, codes);
+}
 
 int build_codebook(const uint64_t *counts, uint32_t dict_size, uint8_t *lengths, uint32_t *codes, std::string &err) {
-    // Present keys in stable ascending (count, key) order (huffman.py:174): the composite
-    // count << 16 | key (keys < 2^16) sorted by an LSD radix sort over the bits in use.
+    // Present keys in stable ascending (count, key) order (huffman.py:174): collected in key order,
+    // then a stable LSD radix sort on the count bits alone (ceil(bits / 11) passes).
     static thread_local std::vector<uint64_t> v, tmp;
     static thread_local std::vector<int64_t> a;
-    v.clear();
+    static thread_local std::vector<uint32_t> pk;   // present keys, ascending
+    memset(lengths, 0, dict_size);
+    memset(codes, 0, (size_t)dict_size * 4);
+    v.resize(dict_size);
+    size_t n = 0;
     uint64_t mx = 0;
     for (uint32_t k = 0; k < dict_size; k++) {
-        lengths[k] = 0;
-        codes[k] = 0;
-        if (counts[k]) {
-            v.push_back((counts[k] << 16) | k);
-            mx = std::max<uint64_t>(mx, counts[k]);
-        }
+        const uint64_t c = counts[k];
+        v[n] = (c << 16) | k;
+        n += c != 0;
+        mx |= c;
     }
-    const size_t n = v.size();
     if (n == 0) { err = "frequency table has no nonzero counts"; return HPDR_ERR_VALIDATION; }
     if (n == 1) { lengths[v[0] & 0xffff] = 1; return HPDR_OK; }
+    pk.resize(n);
+    for (size_t i = 0; i < n; i++) pk[i] = (uint32_t)(v[i] & 0xffff);
+    a.resize(n);
     if (mx >> 48) {   // counts beyond 2^48: comparison sort on (count, key)
         std::vector<uint32_t> present;
         for (uint32_t k = 0; k < dict_size; k++)
             if (counts[k]) present.push_back(k);
         std::stable_sort(present.begin(), present.end(), [&](uint32_t x, uint32_t y) { return counts[x] < counts[y]; });
-        a.resize(n);
-        for (size_t i = 0; i < n; i++) a[i] = (int64_t)counts[present[i]];
-        mk_lengths(a);
-        for (size_t i = 0; i < n; i++) lengths[present[i]] = (uint8_t)std::min<int64_t>(a[i], 255);
+        for (size_t i = 0; i < n; i++) {
+            a[i] = (int64_t)counts[present[i]];
+            v[i] = present[i];
+        }
     } else {
-        int bits = 16;
-        while (bits < 64 && (mx >> (bits - 16))) bits++;
+        int cb = 1;
+        while (cb < 48 && (mx >> cb)) cb++;
+        const int passes = (cb + 10) / 11, digit = (cb + passes - 1) / passes;
+        const uint32_t mask = (1u << digit) - 1;
         tmp.resize(n);
-        for (int sh = 0; sh < bits; sh += 11) {
-            uint32_t c[2049] = {0};
-            for (size_t i = 0; i < n; i++) c[((v[i] >> sh) & 2047) + 1]++;
-            for (int d = 0; d < 2048; d++) c[d + 1] += c[d];
-            for (size_t i = 0; i < n; i++) tmp[c[(v[i] >> sh) & 2047]++] = v[i];
+        static thread_local std::vector<uint32_t> cbuf;
+        cbuf.resize(4 * 2049);
+        uint32_t *c = cbuf.data();
+        for (int ps = 0, sh = 16; ps < passes; ps++, sh += digit) {
+            memset(c, 0, sizeof(uint32_t) * 4 * 2049);
+            for (size_t i = 0; i < n; i++) c[(i & 3) * 2049 + ((v[i] >> sh) & mask) + 1]++;
+            for (uint32_t d = 0; d <= mask; d++) c[d + 1] += c[d] + c[2049 + d + 1] + c[2 * 2049 + d + 1] + c[3 * 2049 + d + 1];
+            for (size_t i = 0; i < n; i++) tmp[c[(v[i] >> sh) & mask]++] = v[i];
             v.swap(tmp);
         }
-        a.resize(n);
         for (size_t i = 0; i < n; i++) a[i] = (int64_t)(v[i] >> 16);
-        mk_lengths(a);
-        for (size_t i = 0; i < n; i++) lengths[v[i] & 0xffff] = (uint8_t)std::min<int64_t>(a[i], 255);
     }
-    const int64_t mxl = *std::max_element(a.begin(), a.begin() + n);
+    mk_lengths(a);
+    int64_t mxl = 0;
+    for (size_t i = 0; i < n; i++) {
+        lengths[v[i] & 0xffff] = (uint8_t)std::min<int64_t>(a[i], 255);
+        mxl = std::max(mxl, a[i]);
+    }
     if (mxl > kMaxCodeLen) {
         err = "codeword length " + std::to_string(mxl) + " exceeds " + std::to_string(kMaxCodeLen);
         return HPDR_ERR_VALIDATION;
     }
-    return canonical_codes(lengths, dict_size, codes);
+    return canonical_from(lengths, pk.data(), n, codes);
 }
 
 // ===================================================================== encode

@@ -27,7 +27,7 @@ namespace hpdr {
 
 void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uint64_t *dims, double eb_rel,
                    uint32_t dict_size, int has_range, double range_min, double range_max, bool allow_stream,
-                   void *fetch_out = nullptr, uint64_t fetch_cap = 0);
+                   void *fetch_out = nullptr, uint64_t fetch_cap = 0, const OutAlloc *alloc = nullptr);
 void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uint8_t *dev_blob, void *out,
                      uint64_t out_bytes, bool sync);
 void compress_from_coef(hpdr_ctx *ctx, const double *coef, int dtype, int rank, const uint64_t *dims, double eb_rel,

@@ -49,6 +49,12 @@ struct EncodeResult {
 // Optional hooks: ready(res) once offsets / total_bits are known (before the packing kernels);
 // group_done(g, lo, hi) after unit group g's packing launch, bytes [lo, hi) of the packed stream
 // are then final in stream order.
+// Caller-side allocation of a compressed stream's destination once its size is known.
+struct OutAlloc {
+    hpdr_alloc_fn fn;
+    void *user;
+};
+
 struct EncodeHooks {
     int groups = 1;
     std::function<void(const EncodeResult &)> ready;

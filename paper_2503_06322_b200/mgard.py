@@ -107,6 +107,11 @@ def _dims_ok(dims):
 
 
 # ----------------------------------------------------------------------------- codec
+# blob size of the last call per (context, dims, dtype, eb_rel, dict_size, mode): the next result's
+# bytes object is created (and first-touched) from it while the GPU works
+_SIZE_HINTS: dict = {}
+
+
 def mgard_compress(u, eb_rel: float, dict_size: int = DEFAULT_DICT_SIZE, adapter=None,
                    cache: ContextCache | None = None, value_range=None, *, device: int | None = None,
                    out=None):
@@ -127,18 +132,30 @@ def mgard_compress(u, eb_rel: float, dict_size: int = DEFAULT_DICT_SIZE, adapter
     has = value_range is not None
     r0, r1 = (float(value_range[0]), float(value_range[1])) if has else (0.0, 0.0)
     n = C.c_uint64()
-    out_addr, out_cap = (None, 0) if out is None else (_lib.ptr(out), int(out.nbytes))
+    if out is None:
+        # a fresh `bytes` (codec.py:56), created once the size is known so that the blob streams
+        # into it behind the payload encode
+        hkey = (id(ctx), tuple(dims), code, float(eb_rel), int(dict_size), has)
+        sink = _lib.BytesSink(_SIZE_HINTS.get(hkey, 0))
+        try:
+            check(lib().hpdr_mgard_compress_alloc(ctx.handle, C.c_void_p(addr), code, len(dims), dims_arg(dims),
+                                                  float(eb_rel), int(dict_size), int(has), r0, r1, sink.fn, None,
+                                                  C.byref(n)))
+        finally:
+            del keep
+            blob = sink.take()
+        if len(_SIZE_HINTS) > 64:
+            _SIZE_HINTS.clear()
+        _SIZE_HINTS[hkey] = int(n.value)
+        return blob
+    out_addr, out_cap = _lib.ptr(out), int(out.nbytes)
     check(lib().hpdr_mgard_compress(ctx.handle, C.c_void_p(addr), code, len(dims), dims_arg(dims),
                                     float(eb_rel), int(dict_size), int(has), r0, r1,
                                     C.c_void_p(out_addr) if out_addr else None, out_cap, C.byref(n)))
     del keep
-    if out is not None:
-        if n.value > out_cap:
-            check(lib().hpdr_mgard_fetch(ctx.handle, C.c_void_p(out_addr), out_cap))
-        return int(n.value)
-    b, p = _lib.new_bytes(n.value)
-    check(lib().hpdr_mgard_fetch(ctx.handle, C.c_void_p(p), n.value))
-    return b
+    if n.value > out_cap:
+        check(lib().hpdr_mgard_fetch(ctx.handle, C.c_void_p(out_addr), out_cap))
+    return int(n.value)
 
 
 def blob_info(data) -> tuple:

@@ -59,3 +59,30 @@ def test_fixed_rate_reused_buffers_identical():
     for _ in range(3):
         assert P.zfp_compress(a, 12) == ref
         assert np.array_equal(P.zfp_decompress(ref).values.view(np.uint8), ref_out.view(np.uint8))
+
+
+def test_bytes_result_size_hint_paths(oracle):
+    """compress -> bytes through the size-hinted, pre-touched result buffer: exact hint, a smaller
+    blob (trimmed in place) and a larger blob (fresh allocation) all return the oracle's blob, as an
+    exact-length immutable bytes."""
+    from paper_2503_06322_b200 import _lib, mgard
+
+    old = _lib.BytesSink.MIN_HINT
+    _lib.BytesSink.MIN_HINT = 0
+    mgard._SIZE_HINTS.clear()
+    try:
+        a = S.smooth_noise((60, 70, 80), seed=8)
+        ref = oracle.mgard_compress(a, 1e-4)
+        for _ in range(3):                                # no hint, then the exact hint
+            b = P.mgard_compress(a, 1e-4)
+            assert type(b) is bytes and b == ref
+        smaller = oracle.mgard_compress(a, 1e-2)          # the hint is keyed by eb_rel: seed it
+        big = oracle.mgard_compress(a, 1e-5)
+        key = next(iter(mgard._SIZE_HINTS))
+        for eb, want in ((1e-2, smaller), (1e-5, big)):
+            k = (key[0], key[1], key[2], eb, key[4], key[5])
+            mgard._SIZE_HINTS[k] = len(ref)               # hint larger than 1e-2's blob, smaller than 1e-5's
+            b = P.mgard_compress(a, eb)
+            assert type(b) is bytes and b == want
+    finally:
+        _lib.BytesSink.MIN_HINT = old

@@ -152,3 +152,25 @@ def _torch_cuda_initialized():
         return bool(t is not None and t.cuda.is_initialized())
     except Exception:   # noqa: BLE001
         return False
+
+
+def test_bytes_sink_trims_in_place_and_keeps_content():
+    """The drop-in's result allocator (_lib.BytesSink): a size-hinted, pre-touched bytes object is
+    trimmed to the exact blob size in place; a larger blob gets a fresh object; content is kept."""
+    import ctypes as C
+
+    from paper_2503_06322_b200 import _lib
+
+    old = _lib.BytesSink.MIN_HINT
+    _lib.BytesSink.MIN_HINT = 0
+    try:
+        for hint, n in ((4 << 20, 3 << 20), (1 << 20, 3 << 20), (0, 5000)):
+            s = _lib.BytesSink(hint)
+            p = s._alloc(None, n)
+            C.memset(p, 0x5A, n)
+            C.memset(p + n // 2, 0x33, 1)
+            b = s.take()
+            assert type(b) is bytes and len(b) == n
+            assert b[0] == 0x5A and b[n - 1] == 0x5A and b[n // 2] == 0x33
+    finally:
+        _lib.BytesSink.MIN_HINT = old

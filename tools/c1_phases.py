@@ -20,8 +20,14 @@ for _ in range(3):
     m = P.mgard_compress(h, 1e-3, value_range=(0.0, 1.0), out=blob)
     P.mgard_decompress(blob[:m], out=out)
 torch.cuda.synchronize()
+d = h.cuda()
+dblob = torch.empty(a.nbytes * 2, dtype=torch.uint8, device="cuda")
+dout = torch.empty(a.shape, dtype=torch.float32, device="cuda")
+md = P.mgard_compress(d, 1e-3, value_range=(0.0, 1.0), out=dblob)
 for name, fn in (("compress", lambda: P.mgard_compress(h, 1e-3, value_range=(0.0, 1.0), out=blob)),
-                 ("decompress", lambda: P.mgard_decompress(blob[:m], out=out))):
+                 ("decompress", lambda: P.mgard_decompress(blob[:m], out=out)),
+                 ("compress device in/out", lambda: P.mgard_compress(d, 1e-3, value_range=(0.0, 1.0), out=dblob)),
+                 ("decompress device in/out", lambda: P.mgard_decompress(dblob[:md], out=dout))):
     t = time.perf_counter()
     for _ in range(reps):
         fn()
