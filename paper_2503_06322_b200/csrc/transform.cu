@@ -1455,15 +1455,19 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
                 fused_final(p, 0, Dc, coef, out, out_dtype, s, a, e, T);
                 CUDA_CHECK(cudaEventRecord(ctx->event(EvSlabOut, k), s));
             }
-            for (int a = 0, k = 0; k < nslab; a += chunk, k++) {
-                const int e = std::min(n0, a + chunk);
-                CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(EvSlabOut, k), 0));
-                if (pageable_out)
-                    stage_d2h(ctx, (char *)host_out + a * plane_bytes, (const char *)out + a * plane_bytes,
-                              (e - a) * plane_bytes, ctx->d2h);
-                else
+            if (pageable_out) {   // one continuous pass of the staging ring, slab events releasing the chunks
+                std::vector<StageRange> rs;
+                for (int a = 0, k = 0; k < nslab; a += chunk, k++)
+                    rs.push_back({(size_t)a * plane_bytes, (size_t)std::min(n0, a + chunk) * plane_bytes,
+                                  ctx->event(EvSlabOut, k)});
+                stage_d2h_ranges(ctx, (char *)host_out, (const char *)out, rs, ctx->d2h);
+            } else {
+                for (int a = 0, k = 0; k < nslab; a += chunk, k++) {
+                    const int e = std::min(n0, a + chunk);
+                    CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(EvSlabOut, k), 0));
                     CUDA_CHECK(cudaMemcpyAsync((char *)host_out + a * plane_bytes, (const char *)out + a * plane_bytes,
                                                (e - a) * plane_bytes, cudaMemcpyDeviceToHost, ctx->d2h));
+                }
             }
             CUDA_CHECK(cudaStreamSynchronize(ctx->d2h));
         } else if (st_i == 0 && direct) {
