@@ -868,17 +868,32 @@ __global__ void __launch_bounds__(256) k_level_final(const double *__restrict__ 
         }
         cp_async_commit();
     };
-    // P0 of plane j over the footprint (transform.py:264-268: axis 0 first)
+    // P0 of plane j over the footprint (transform.py:264-268: axis 0 first).  Each footprint thread
+    // keeps the last two coarse planes it read (slot c & 1), so a coarse plane shared by consecutive
+    // fine planes is loaded once; with corr the cached value is coarse - corr (the elementwise k_sub
+    // of transform.py:345 folded in).
+    int cc0 = -1, cc1 = -1;
+    double cv0 = 0.0, cv1 = 0.0;
+    auto coarse = [&](int c) -> double {
+        if (c == cc0) return cv0;
+        if (c == cc1) return cv1;
+        const int64_t i = (int64_t)c * cplane + foff;
+        double v = __ldg(cv + i);
+        if (corr) v = dsub(v, __ldg(corr + i));
+        if (c & 1) {
+            cc1 = c;
+            cv1 = v;
+        } else {
+            cc0 = c;
+            cv0 = v;
+        }
+        return v;
+    };
     auto stage = [&](int j) {
         if (j >= hi || tid >= RC) return;
         const Nb b0 = neighbours<A0>(ax0, j);
-        const int64_t ia = (int64_t)b0.ca * cplane + foff, ib = (int64_t)b0.cb * cplane + foff;
-        double va = __ldg(cv + ia), vb = b0.fo ? __ldg(cv + ib) : 0.0;
-        if (corr) {   // coarse - corr (the elementwise k_sub folded in)
-            va = dsub(va, __ldg(corr + ia));
-            if (b0.fo) vb = dsub(vb, __ldg(corr + ib));
-        }
-        sP0[j & 1][tid] = b0.fo ? lerp(va, vb, b0.t) : va;
+        const double va = coarse(b0.ca);
+        sP0[j & 1][tid] = b0.fo ? lerp(va, coarse(b0.cb), b0.t) : va;
     };
     for (int k = 0; k < kFRing - 1; k++) issue(lo + k);
     stage(lo);
