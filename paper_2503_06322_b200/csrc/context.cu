@@ -157,7 +157,11 @@ __global__ void k_zero(uint8_t *__restrict__ dst, size_t n) {
 
 void small_copy(void *dst, const void *src, size_t bytes, cudaStream_t s) {
     if (!bytes) return;
-    if (bytes > (1u << 20) || classify(dst) == MemKind::Host || classify(src) == MemKind::Host) {
+    // an SM copy beats a DMA launch for small pieces; across PCIe (pinned host memory) only up to
+    // ~128 KB -- zero-copy reads by a few blocks are latency-bound beyond that
+    const MemKind kd = classify(dst), ks = classify(src);
+    const size_t cap = (kd == MemKind::Pinned || ks == MemKind::Pinned) ? (128u << 10) : (1u << 20);
+    if (bytes > cap || kd == MemKind::Host || ks == MemKind::Host) {
         CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
         return;
     }

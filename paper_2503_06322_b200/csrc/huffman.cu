@@ -669,15 +669,18 @@ __global__ void k_fill(uint32_t *keys, double *coef, int64_t n, uint32_t sym, do
 void decode_begin(hpdr_ctx *ctx, const DecodeJob &job, DecodeSession &S, cudaStream_t s, bool copy_payload) {
     // _decode_tables (huffman.py:207-225) and the 12-bit lookup table
     const uint32_t dict = job.dict_size;
-    std::vector<uint32_t> present;
+    // present keys in (length, key) order: a counting sort over the lengths
+    uint32_t lstart[257] = {0};
     int max_len = 0;
+    for (uint32_t k = 0; k < dict; k++) {
+        lstart[job.lengths[k] + 1]++;
+        max_len = std::max<int>(max_len, job.lengths[k]);
+    }
+    lstart[1] = 0;   // absent keys (length 0) are not ranked
+    for (int l = 1; l < 256; l++) lstart[l + 1] += lstart[l];
+    std::vector<uint32_t> present(lstart[256]);
     for (uint32_t k = 0; k < dict; k++)
-        if (job.lengths[k]) {
-            present.push_back(k);
-            max_len = std::max<int>(max_len, job.lengths[k]);
-        }
-    std::stable_sort(present.begin(), present.end(),
-                     [&](uint32_t x, uint32_t y) { return job.lengths[x] < job.lengths[y]; });
+        if (job.lengths[k]) present[lstart[job.lengths[k]]++] = k;
     DecTables *T = (DecTables *)ctx->hbuf("dec_tabs", sizeof(DecTables) + kLutSize * 4 + (present.size() + 1) * 4);
     memset(T, 0, sizeof(DecTables));
     for (uint32_t k : present) T->cnt[job.lengths[k]]++;
@@ -694,18 +697,19 @@ void decode_begin(hpdr_ctx *ctx, const DecodeJob &job, DecodeSession &S, cudaStr
     uint32_t *lut = (uint32_t *)(T + 1);
     uint32_t *sbr = lut + kLutSize;
     for (size_t i = 0; i < present.size(); i++) sbr[i] = present[i];
+    // 12-bit lookup: entry v = the shortest code that is a prefix of v (codes of length l fill the
+    // entries [c << (12 - l), (c + 1) << (12 - l)); shorter lengths first, filled entries kept)
     const int lut_len = std::min(kLutBits, max_len);
-    for (uint32_t v = 0; v < (uint32_t)kLutSize; v++) {
-        uint32_t e = 0;
-        for (int l = 1; l <= lut_len && max_len <= 32; l++) {
-            long long c = (long long)(v >> (kLutBits - l));
-            long long idx = c - T->first_code[l];
-            if (idx >= 0 && idx < T->cnt[l]) {
-                e = (sbr[T->first_rank[l] + idx] << 8) | (uint32_t)l;
-                break;
-            }
+    memset(lut, 0, kLutSize * 4);
+    for (int l = 1; l <= lut_len && max_len <= 32; l++) {
+        for (long long idx = 0; idx < T->cnt[l]; idx++) {
+            const unsigned long long c = (unsigned long long)(T->first_code[l] + idx);
+            const unsigned long long lo = c << (kLutBits - l), hi = (c + 1) << (kLutBits - l);
+            if (lo >= (unsigned long long)kLutSize) break;
+            const uint32_t e = (sbr[T->first_rank[l] + idx] << 8) | (uint32_t)l;
+            for (unsigned long long v = lo; v < hi && v < (unsigned long long)kLutSize; v++)
+                if (!lut[v]) lut[v] = e;
         }
-        lut[v] = e;
     }
     // prefixes of codes longer than kLutBits: the shortest such length per prefix (canonical codes
     // of length l cover the prefixes [first >> (l - kLutBits), (first + cnt - 1) >> (l - kLutBits)])

@@ -1105,7 +1105,9 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
     double *coef = has_range ? nullptr : (double *)ctx->dbuf("coef", N * 8);
     // chunks of >= 32 MB (and >= 4 planes) along dim 0
     const int64_t plane_bytes = plane_elems * (int64_t)isz;
-    int chunk = (int)std::max<int64_t>(4, ((32LL << 20) + plane_bytes - 1) / std::max<int64_t>(plane_bytes, 1));
+    // (a small field still arrives in >= 4 pieces, so its finest pass overlaps the copy)
+    const int64_t target = std::min<int64_t>(32LL << 20, std::max<int64_t>(1LL << 20, (int64_t)n0 * plane_bytes / 4));
+    int chunk = (int)std::max<int64_t>(4, (target + plane_bytes - 1) / std::max<int64_t>(plane_bytes, 1));
     chunk = std::min(chunk, n0);
     const int K = (n0 + chunk - 1) / chunk;
     unsigned long long *mm = (unsigned long long *)ctx->dbuf("minmax", 32);
@@ -1442,7 +1444,8 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
             // finest level in dim-0 slabs; each slab's D2H (copy stream) overlaps the next slab
             const int n0 = (int)st.fsh.n[1];
             const int64_t plane_bytes = st.fsh.n[2] * st.fsh.n[3] * (out_dtype == 0 ? 4 : 8);
-            int chunk = (int)std::max<int64_t>(4, ((32LL << 20) + plane_bytes - 1) / std::max<int64_t>(plane_bytes, 1));
+            const int64_t target = std::min<int64_t>(32LL << 20, std::max<int64_t>(1LL << 20, (int64_t)n0 * plane_bytes / 4));
+            int chunk = (int)std::max<int64_t>(4, (target + plane_bytes - 1) / std::max<int64_t>(plane_bytes, 1));
             chunk = std::min(chunk, n0);
             CUDA_CHECK(cudaEventRecord(ctx->event(0), ctx->d2h));
             CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(0), 0));   // previous call's copies are done
