@@ -32,6 +32,14 @@ def install(codec, lib_path: str = _LIB, device: int = 0):
     L = C.CDLL(lib_path)
     L.hpdr_last_error.restype = C.c_char_p
     L.hpdr_last_error.argtypes = [C.POINTER(C.c_int64)]
+    ALLOC = C.CFUNCTYPE(C.c_void_p, C.c_void_p, C.c_uint64)   # hpdr_alloc_fn
+    L.hpdr_mgard_compress_alloc.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_uint64),
+                                            C.c_double, C.c_uint32, C.c_int, C.c_double, C.c_double, ALLOC,
+                                            C.c_void_p, C.POINTER(C.c_uint64)]
+    pybytes_new = C.pythonapi.PyBytes_FromStringAndSize
+    pybytes_new.restype, pybytes_new.argtypes = C.py_object, [C.c_void_p, C.c_ssize_t]
+    pybytes_ptr = C.pythonapi.PyBytes_AsString
+    pybytes_ptr.restype, pybytes_ptr.argtypes = C.c_void_p, [C.py_object]
     ctx = C.c_void_p()
     if L.hpdr_ctx_create(int(device), C.byref(ctx)) != 0:
         raise RuntimeError("hpdr_ctx_create failed: " + L.hpdr_last_error(None).decode())
@@ -52,17 +60,21 @@ def install(codec, lib_path: str = _LIB, device: int = 0):
         n = C.c_uint64()
         has = value_range is not None
         lo, hi = value_range if has else (0.0, 0.0)
-        rc = L.hpdr_mgard_compress(ctx, C.c_void_p(arr.ctypes.data), DTYPE_CODES[u.dtype], len(u.dims), dims,
-                                   C.c_double(eb_rel), C.c_uint32(dict_size), int(has), C.c_double(lo),
-                                   C.c_double(hi), None, C.c_uint64(0), C.byref(n))
+        # the result bytes object is created by the library's allocator callback once the blob size is
+        # known, and the blob streams into it behind the payload encode (no second copy)
+        res = {}
+
+        def alloc(_user, size):
+            res["b"] = pybytes_new(None, size)
+            return pybytes_ptr(res["b"])
+
+        cb = ALLOC(alloc)
+        rc = L.hpdr_mgard_compress_alloc(ctx, C.c_void_p(arr.ctypes.data), DTYPE_CODES[u.dtype], len(u.dims),
+                                         dims, C.c_double(eb_rel), C.c_uint32(dict_size), int(has), C.c_double(lo),
+                                         C.c_double(hi), cb, None, C.byref(n))
         if rc:
             _raise(rc)
-        out = bytearray(n.value)
-        rc = L.hpdr_mgard_fetch(ctx, (C.c_char * n.value).from_buffer(out) if n.value else None,
-                                C.c_uint64(n.value))
-        if rc:
-            _raise(rc)
-        return bytes(out)
+        return res["b"]
 
     def mgard_decompress(data, adapter=None, cache=None):
         buf = np.frombuffer(memoryview(data), np.uint8)
