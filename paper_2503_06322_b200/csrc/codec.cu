@@ -429,6 +429,7 @@ void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t 
         std::vector<std::pair<uint64_t, uint64_t>> pg_ranges;
         std::vector<int> pg_groups;
         hpdr_ctx::Pending PQ;
+        const char *words_dev = nullptr;   // the packed payload (EncodeResult::d_words)
         if ((fetch_out && ok != MemKind::Host) || (!fetch_out && alloc)) {
             hooks.groups = N >= (16LL << 20) ? 8 : 1;   // small streams: one launch, no group read-back
             hooks.ready = [&](const EncodeResult &e) {
@@ -441,6 +442,7 @@ void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t 
                 }
                 if (fetch_cap < total) return;
                 streamed_fetch = true;
+                words_dev = (const char *)e.d_words;
                 hpdr_ctx::Pending Q = P;
                 Q.n_units = e.n_units;
                 Q.total_bits = e.total_bits;
@@ -462,15 +464,15 @@ void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t 
                 }
                 CUDA_CHECK(cudaStreamWaitEvent(ctx->d2h, ctx->event(EvEncGroup, g), 0));
                 const bool dev = ok == MemKind::Device;
-                CUDA_CHECK(cudaMemcpyAsync((char *)fetch_out + pay_pos + lo, (const char *)ctx->dbuf(ctx->oname("enc_words"), 16) + lo,
-                                           hi - lo, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->d2h));
+                CUDA_CHECK(cudaMemcpyAsync((char *)fetch_out + pay_pos + lo, words_dev + lo, hi - lo,
+                                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->d2h));
             };
         }
         huffman_stage(ctx, keys, N, dict_size, q.hist, P.mid, enc, single, s,
                       (fetch_out || alloc) ? &hooks : nullptr);
         if (streamed_fetch && ok == MemKind::Host) {
             pay_pos = fetch_pending(ctx, PQ, fetch_out, fetch_cap, ctx->d2h, false, /*payload=*/false);
-            const char *words = (const char *)ctx->dbuf(ctx->oname("enc_words"), 16);
+            const char *words = words_dev;
             std::vector<StageRange> rs;
             for (size_t g = 0; g < pg_ranges.size(); g++)
                 rs.push_back({pg_ranges[g].first, pg_ranges[g].second, ctx->event(EvEncGroup, pg_groups[g])});

@@ -58,4 +58,14 @@ int fused_out_planes(const DevPlan &p, int st_i);
 void fused_final(const DevPlan &p, int st_i, const double *cv, const double *coef, void *D, int out_dtype,
                  cudaStream_t s, int j_lo = 0, int j_hi = -1, const double *corr = nullptr);
 
+// tiny.cu: every transition from the first one whose fine level fits one block (>= st_min; -1 none)
+// run in one kernel, levels resident in shared memory.
+int tiny_start(const DevPlan &p, int st_min);
+// Quantizing decomposition of transitions st_a .. L-2 from the dense level F0; the coarsest level to
+// DL, quantized raw (replaces per-level pass 1 / pass 2 / Thomas and quantize_coarsest).
+void tiny_decompose_quantize(const DevPlan &p, int st_a, const double *F0, double *DL, const QuantOut &q,
+                             cudaStream_t s);
+// Recomposition of transitions L-2 .. st_a from the coefficient set; level st_a's dense values to D.
+void tiny_recompose(const DevPlan &p, int st_a, const double *coef, double *D, cudaStream_t s);
+
 }  // namespace hpdr

@@ -12,6 +12,28 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double lerp(double va, double vb, double t) { return dadd(va, dmul(t, dsub(vb, va))); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// Verified fast IEEE division for the back substitution.  q1 = q0 + (a - b q0) r with
+// r = RN(1/b) (host table) is accepted only when its exact residual a - b q1 (an FMA) proves
+// |a/b - q1| < half the smaller gap next to q1, i.e. q1 == RN(a/b) = __ddiv_rn(a, b); anything
+// else (ties, subnormal / huge / non-finite values) raises `bad` and the caller redoes the line
+// with __ddiv_rn.  Zeros take a * r, which carries the IEEE sign of a / b.
+__device__ __forceinline__ double div_fast(double a, double b, double r, bool &bad) {
+    if (a == 0.0) return __dmul_rn(a, r);
+    const double q0 = __dmul_rn(a, r);
+    const double q1 = __fma_rn(__fma_rn(-q0, b, a), r, q0);
+    const double rem = __fma_rn(-q1, b, a);
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(q1);
+    const int ex = (int)((bits >> 52) & 0x7ff);
+    const int mant0 = (bits & 0xfffffffffffffULL) == 0;
+    // h = 2^(E - 53) (2^(E - 54) at a power of two), E the unbiased exponent of q1
+    const double h = __longlong_as_double((long long)(ex - 53 - mant0) << 52);
+    const double bound = fabs(b) * h;   // exact: power-of-two scaling of a normal value
+    bad |= !(ex > 120 && ex < 1900) || !(bound > 1e-290) || !(fabs(rem) < bound);
+    return q1;
+}
+
 
 
 // Histogram count of `key` (shared-memory bins flushed once per block).

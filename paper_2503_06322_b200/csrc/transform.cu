@@ -9,6 +9,7 @@
 #include <stdlib.h>
 
 #include "fused.cuh"
+#include "level_dev.cuh"
 
 namespace hpdr {
 
@@ -17,7 +18,7 @@ namespace {
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+using lvl::ddiv;
 
 // ---------------------------------------------------------------- input conversion / range
 __global__ void k_to_f64(const void *__restrict__ in, int dtype, double *__restrict__ out, int64_t n) {
@@ -264,25 +265,8 @@ __global__ void k_mass_restrict(const double *__restrict__ src, double *__restri
     }
 }
 
-// Verified fast IEEE division for the back substitution.  q1 = q0 + (a - b q0) r with
-// r = RN(1/b) (host table) is accepted only when its exact residual a - b q1 (an FMA) proves
-// |a/b - q1| < half the smaller gap next to q1, i.e. q1 == RN(a/b) = __ddiv_rn(a, b); anything
-// else (ties, subnormal / huge / non-finite values) raises `bad` and the caller redoes the line
-// with __ddiv_rn.  Zeros take a * r, which carries the IEEE sign of a / b.
-__device__ __forceinline__ double div_fast(double a, double b, double r, bool &bad) {
-    if (a == 0.0) return dmul(a, r);
-    const double q0 = dmul(a, r);
-    const double q1 = __fma_rn(__fma_rn(-q0, b, a), r, q0);
-    const double rem = __fma_rn(-q1, b, a);
-    const unsigned long long bits = (unsigned long long)__double_as_longlong(q1);
-    const int ex = (int)((bits >> 52) & 0x7ff);
-    const int mant0 = (bits & 0xfffffffffffffULL) == 0;
-    // h = 2^(E - 53) (2^(E - 54) at a power of two), E the unbiased exponent of q1
-    const double h = __longlong_as_double((long long)(ex - 53 - mant0) << 52);
-    const double bound = fabs(b) * h;   // exact: power-of-two scaling of a normal value
-    bad |= !(ex > 120 && ex < 1900) || !(bound > 1e-290) || !(fabs(rem) < bound);
-    return q1;
-}
+// div_fast: the verified fast IEEE division of the back substitution (level_dev.cuh).
+using lvl::div_fast;
 
 // ---------------------------------------------------------------- IPK: batched Thomas solves
 // Optional epilogue of the last sweep of a correction solve: instead of the correction x itself, write
@@ -1030,9 +1014,13 @@ const double *coarse_levels_quantize(hpdr_ctx *ctx, DevPlan &p, const QuantOut &
     LevelBuffers b = fused_buffers(ctx, p);
     const int L = p.host.L;
     double *Z0 = b.mc;
+    const int tiny = tiny_start(p, 1);   // the small end of the hierarchy in one block
     auto body = [&](const QuantOut &qq) {
         for (int st_i = 1; st_i + 1 < L; st_i++) {
-            const DevStep &st = p.steps[st_i];
+            if (st_i == tiny) {
+                tiny_decompose_quantize(p, st_i, level_ptr(b, p, st_i), level_ptr(b, p, L - 1), qq, s);
+                return;
+            }
             fused_pass1_quantize(p, st_i, level_ptr(b, p, st_i), false, qq, Z0, b.cg, s);
             fused_pass2(p, st_i, Z0, b.t0, s);
             thomas_all(p, st_i, b.t0, s, b.cg, level_ptr(b, p, st_i + 1));
@@ -1369,9 +1357,14 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
     Shape4 shL;
     for (int d = 0; d < 4; d++) shL.n[d] = p.host.cnt[d][L - 1];
     Sel4 none{};
-    k_gather_level<<<rows_grid(shL), 256, 0, s>>>(coef, p.dims, level_map(p, L - 1), none, level_ptr(b, p, L - 1),
-                                                  shL, 0);
-    LAUNCH_CHECK();
+    // transitions tiny .. L-2 (the small end) run in one block on the main stream
+    const int tiny = tiny_start(p, 1);
+    const int top = tiny >= 1 ? tiny : L - 1;   // chain below handles transitions top-1 .. 0
+    if (tiny < 1) {
+        k_gather_level<<<rows_grid(shL), 256, 0, s>>>(coef, p.dims, level_map(p, L - 1), none,
+                                                      level_ptr(b, p, L - 1), shL, 0);
+        LAUNCH_CHECK();
+    }
     // A level's correction depends only on its own coefficients (transform.py:342-345), so the
     // finest one -- the bulk of the correction work -- runs on the side stream while the coarser
     // levels are recomposed; only coarse - corr of the finest transition waits for it.
@@ -1400,7 +1393,7 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
     std::vector<int> ev_l(L, -1);
     if (L > 2) {
         int64_t zc = 0, tc = 0;
-        for (int st_i = 1; st_i + 1 < L; st_i++) {
+        for (int st_i = 1; st_i < top; st_i++) {
             zc += (z0_elems(p, st_i) + 31) & ~int64_t(31);
             tc += (p.steps[st_i].csh.size() + 31) & ~int64_t(31);
         }
@@ -1409,7 +1402,7 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
         // event ids: 199 / 200 + level (distinct from the streamed decode's and the slab loop's)
         CUDA_CHECK(cudaEventRecord(ctx->event(199), s));   // coef ready
         int k = 0;
-        for (int st_i = L - 2; st_i >= 1; st_i--, k++) {
+        for (int st_i = top - 1; st_i >= 1; st_i--, k++) {
             cudaStream_t x = ctx->side[k % 4];
             if (k < 4) CUDA_CHECK(cudaStreamWaitEvent(x, ctx->event(199), 0));
             double *Zl = zarena, *T = tarena;
@@ -1423,7 +1416,8 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
             CUDA_CHECK(cudaEventRecord(ctx->event(EvLevel, st_i), x));
         }
     }
-    for (int st_i = L - 2; st_i >= 0; st_i--) {
+    if (tiny >= 1) tiny_recompose(p, tiny, coef, level_ptr(b, p, tiny), s);
+    for (int st_i = top - 1; st_i >= 0; st_i--) {
         const DevStep &st = p.steps[st_i];
         double *Dc = level_ptr(b, p, st_i + 1);
         const double *T = b.t0;

@@ -879,6 +879,7 @@ int hpdr_zfp_decompress(hpdr_ctx *ctx, const void *stream, uint64_t len, void *o
         const bool out_dev = ok == MemKind::Device;
         cudaStream_t s = ctx->stream;
         uint32_t *pay = (uint32_t *)ctx->dbuf("zfp_dpay", z.payload + 8);
+        zero_async((uint8_t *)pay + z.payload, 8, s);   // the staged tail word past the payload reads zeros
         void *dout = out_dev ? out : ctx->dbuf("zfp_out", n * isz);
         const std::vector<int64_t> cut = zfp_slabs(z, (in_dev && out_dev) ? 1 : zfp_slab_count(z, n * isz));
         const int K = (int)cut.size() - 1;
@@ -1124,6 +1125,7 @@ int zfp_container_decompress(hpdr_ctx *ctx, const uint8_t *c, uint64_t len, void
             if (tm) CUDA_CHECK(cudaEventRecord(tm->ev[6 * k], ctx->h2d));
             CUDA_CHECK(cudaMemcpyAsync(dp[b], c + base + ch[k].pay_off + hl, zs[k].payload, cudaMemcpyHostToDevice,
                                        ctx->h2d));
+            zero_async((uint8_t *)dp[b] + zs[k].payload, 8, ctx->h2d);   // tail word past the payload
             if (tm) CUDA_CHECK(cudaEventRecord(tm->ev[6 * k + 1], ctx->h2d));
             CUDA_CHECK(cudaEventRecord(ctx->event(486 + b), ctx->h2d));
             CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(486 + b), 0));

@@ -1,6 +1,7 @@
 """compute-sanitizer over a small compress / decompress round trip on every kernel family:
-memcheck (out-of-bounds / misaligned device accesses, leaks) and racecheck (shared-memory
-hazards, including the mbarrier-ordered TMA ring of k_pass1_quad)."""
+memcheck (out-of-bounds / misaligned device accesses, leaks), racecheck (shared-memory
+hazards, including the mbarrier-ordered TMA ring of k_pass1_quad) and initcheck (device memory
+read before it is written, including the payload copies of the streamed drop-in paths)."""
 import os
 import shutil
 import subprocess
@@ -19,8 +20,10 @@ sys.path.insert(0, %r)
 import paper_2503_06322_b200 as P
 from paper_2503_06322_b200 import synthetic as S
 # quad pass 1 with TMA (rows of 64 fp32) and with cp.async (odd rows), fused levels, Thomas,
-# Huffman, the streamed decompress, the fixed-rate coder and the per-axis rank-4 path
-for shape, dt in (((34, 36, 64), np.float32), ((21, 19, 23), np.float64), ((9, 10, 11, 6), np.float32)):
+# Huffman, the streamed decompress, the fixed-rate coder, the per-axis rank-4 path and the
+# one-block small end of the hierarchy
+for shape, dt in (((34, 36, 64), np.float32), ((21, 19, 23), np.float64), ((9, 10, 11, 6), np.float32),
+                  ((5,), np.float64)):   # (5,): a payload of a few bits
     a = S.smooth_noise(shape, seed=1, dtype=dt)
     for vr in (None, (-1.0, 2.0)):
         b = P.mgard_compress(a, 1e-3, value_range=vr)
@@ -33,7 +36,7 @@ print("sanitized run ok")
 """
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "initcheck"])
 def test_compute_sanitizer_clean(tool):
     if not os.path.exists(SANITIZER):
         pytest.skip("compute-sanitizer not found")

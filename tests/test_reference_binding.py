@@ -60,7 +60,11 @@ def test_reference_api_through_binding_matches_goldens(ref_hpdr, small_cases, co
             u = TensorData(tuple(a.shape), DType.F32 if a.dtype == np.float32 else DType.F64, a)
             vr = tuple(c["value_range"]) if c["value_range"] else None
             blob = mg.mgard_compress(u, c["eb_rel"], c["dict_size"], value_range=vr)
-            assert blob == c["blob"], c["shape"]
+            if blob != c["blob"]:   # say where (length, first differing byte, both tails)
+                d = next((k for k in range(min(len(blob), len(c["blob"]))) if blob[k] != c["blob"][k]), None)
+                again = mg.mgard_compress(u, c["eb_rel"], c["dict_size"], value_range=vr)
+                pytest.fail(f"{c['shape']}: len {len(blob)} vs {len(c['blob'])}, first diff at {d}, "
+                            f"tail {blob[-16:].hex()} vs {c['blob'][-16:].hex()}, repeat equal: {again == c['blob']}")
             y = mg.mgard_decompress(blob)
             assert isinstance(y, TensorData) and y.dtype == u.dtype and tuple(y.dims) == tuple(a.shape)
             assert np.array_equal(y.values.view(np.uint8), c["out"].view(np.uint8)), c["shape"]
