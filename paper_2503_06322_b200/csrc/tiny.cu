@@ -18,7 +18,8 @@ namespace {
 using namespace lvl;
 
 constexpr int kTinySteps = 10;
-constexpr int kTinyMaxNodes = 6144;   // fine nodes of the first transition run here
+constexpr int kTinyMaxNodes = 1024;   // fine nodes of the first transition run here (9^3, 32^2)
+constexpr int kTinyHist = 4096;       // shared key histogram (dict sizes up to this)
 constexpr int kTinyThreads = 512;
 
 struct TinyStep {
@@ -35,13 +36,26 @@ struct TinyArgs {
     Shape4 shL;              // coarsest level shape
 };
 
+// q = e / n, r = e % n for 0 <= e < 2^23 through a float reciprocal and a one-step fix-up (the
+// integer divisions of a naive index decode dominated these latency-bound phases)
+__device__ __forceinline__ int fdiv(int e, int n, float inv, int &r) {
+    int q = __float2int_rz((float)e * inv);
+    r = e - q * n;
+    if (r < 0) {
+        q--;
+        r += n;
+    } else if (r >= n) {
+        q++;
+        r -= n;
+    }
+    return q;
+}
+
 __device__ __forceinline__ void coords4(int e, const Shape4 &s, int c[4]) {
-    c[3] = e % (int)s.n[3];
-    int t = e / (int)s.n[3];
-    c[2] = t % (int)s.n[2];
-    t /= (int)s.n[2];
-    c[1] = t % (int)s.n[1];
-    c[0] = t / (int)s.n[1];
+    const int n1 = (int)s.n[1], n2 = (int)s.n[2], n3 = (int)s.n[3];
+    int t = fdiv(e, n3, 1.0f / (float)n3, c[3]);
+    t = fdiv(t, n2, 1.0f / (float)n2, c[2]);
+    c[0] = fdiv(t, n1, 1.0f / (float)n1, c[1]);
 }
 
 __device__ __forceinline__ int lin4(const Shape4 &s, const int c[4]) {
@@ -152,7 +166,8 @@ __device__ void t_thomas(double *x0, const Shape4 &sh, int a, const DevAxis &ax)
     for (int d = a + 1; d < 4; d++) inner *= (int)sh.n[d];
     const int n = ax.nc, lines = outer * inner;
     for (int ln = threadIdx.x; ln < lines; ln += blockDim.x) {
-        const int p = ln / inner, q = ln - p * inner;
+        int q;
+        const int p = fdiv(ln, inner, 1.0f / (float)inner, q);
         double *x = x0 + p * n * inner + q;
         double prev = x[0];
         for (int i = 1; i < n; i++) {
@@ -196,6 +211,37 @@ __device__ double *t_correction(const TinyStep &st, const double *mc, double *A,
     return out;
 }
 
+// A step's record (shapes, axis tables, maps) into shared memory: the per-element reads of a
+// dynamically indexed kernel parameter otherwise go to the constant bank with a computed address.
+__device__ __forceinline__ void load_step(TinyStep &dst, const TinyStep &src) {
+    __syncthreads();   // the previous step's readers are done
+    static_assert(sizeof(TinyStep) % 8 == 0, "");
+    for (int i = threadIdx.x; i < (int)(sizeof(TinyStep) / 8); i += blockDim.x)
+        reinterpret_cast<long long *>(&dst)[i] = reinterpret_cast<const long long *>(&src)[i];
+    __syncthreads();
+}
+
+// Every operator table of every step into L1 up front (a few KB, all lines in flight at once), so
+// the per-phase table reads hit L1 instead of paying a cold global-memory latency each.
+__device__ void t_prefetch_tables(const TinyArgs &T) {
+    auto pf = [](const void *p, int bytes) {
+        if (!p) return;
+        for (int o = threadIdx.x * 128; o < bytes; o += blockDim.x * 128)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"((const char *)p + o));
+    };
+    for (int k = 0; k < T.nsteps; k++)
+        for (int d = 0; d < 4; d++) {
+            const DevAxis &a = T.st[k].ax[d];
+            if (a.active) {
+                const int n = a.n * 8, nc = a.nc * 8;
+                pf(a.pa, n / 2), pf(a.pb, n / 2), pf(a.pt, n), pf(a.md, n), pf(a.ml, n), pf(a.mu, n);
+                pf(a.r0, nc / 2), pf(a.rr, nc / 2), pf(a.rl, nc / 2), pf(a.wr, nc), pf(a.wl, nc);
+                pf(a.tw, nc), pf(a.tb, nc), pf(a.tu, nc), pf(a.tr, nc);
+            }
+            pf(T.st[k].map[d], (int)T.st[k].fsh.n[d] * 4);
+        }
+}
+
 __device__ __forceinline__ bool t_is_coarse(const TinyStep &st, const int c[4]) {
     for (int d = 0; d < 4; d++)
         if (st.ax[d].active && __ldg(st.ax[d].pb + c[d]) >= 0) return false;
@@ -210,12 +256,21 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny_decompose(TinyArgs T, con
     extern __shared__ double tsm[];
     const int nmax = (int)T.st[0].fsh.size();
     double *F = tsm, *M = F + nmax, *A = M + nmax, *B = A + nmax, *Cg = B + nmax;
+    // keys concentrate on a few values: count them in shared memory, flush once (one global
+    // atomic per used bin instead of one per node on the same few addresses)
+    uint32_t *sh_hist = reinterpret_cast<uint32_t *>(Cg + nmax / 2 + 1);
+    const bool sh_ok = q.dict <= (uint32_t)kTinyHist;
+    if (sh_ok)
+        for (uint32_t k = threadIdx.x; k < q.dict; k += blockDim.x) sh_hist[k] = 0;
+    t_prefetch_tables(T);
     for (int i = threadIdx.x; i < nmax; i += blockDim.x) F[i] = F0[i];
     __syncthreads();
     const double rbin = 1.0 / qbin(q);
     int fl = 0;
+    __shared__ __align__(16) TinyStep sst;   // the current step's tables, off the parameter bank
     for (int s = 0; s < T.nsteps; s++) {
-        const TinyStep &st = T.st[s];
+        load_step(sst, T.st[s]);
+        const TinyStep &st = sst;
         t_gather_coarse(F, st, Cg);
         __syncthreads();
         t_interpolate<1>(st, Cg, M, F, A, B);   // M = F - pred
@@ -224,7 +279,7 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny_decompose(TinyArgs T, con
         for (int e = threadIdx.x; e < nf; e += blockDim.x) {
             int c[4];
             coords4(e, st.fsh, c);
-            if (!t_is_coarse(st, c)) quant_node(M[e], q, rbin, finest(T.dims, st.map, c), fl, nullptr, false);
+            if (!t_is_coarse(st, c)) quant_node(M[e], q, rbin, finest(T.dims, st.map, c), fl, sh_hist, sh_ok);
         }
         const double *corr = t_correction(st, M, A, B);
         const int nc = (int)st.csh.size();
@@ -244,6 +299,11 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny_decompose(TinyArgs T, con
     }
     if (threadIdx.x == 0 && n_co) atomicAdd(&q.hist[0], (unsigned long long)n_co);
     if (fl) atomicOr(q.flags, fl);
+    if (sh_ok) {
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < q.dict; k += blockDim.x)
+            if (sh_hist[k]) atomicAdd(&q.hist[k], (unsigned long long)sh_hist[k]);
+    }
 }
 
 // Recomposition of transitions (the caller's last) .. st_a from the coefficient set: the coarsest
@@ -254,6 +314,7 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny_recompose(TinyArgs T, con
     extern __shared__ double tsm[];
     const int nmax = (int)T.st[0].fsh.size();
     double *F = tsm, *M = F + nmax, *A = M + nmax, *B = A + nmax, *Cg = B + nmax;
+    t_prefetch_tables(T);
     {
         const int nL = (int)T.shL.size();
         for (int e = threadIdx.x; e < nL; e += blockDim.x) {
@@ -263,8 +324,10 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny_recompose(TinyArgs T, con
         }
     }
     __syncthreads();
+    __shared__ __align__(16) TinyStep sst;
     for (int s = T.nsteps - 1; s >= 0; s--) {
-        const TinyStep &st = T.st[s];
+        load_step(sst, T.st[s]);
+        const TinyStep &st = sst;
         // mc of this level, zero at the next-coarser level's nodes (k_gather_level)
         const int nf = (int)st.fsh.size();
         for (int e = threadIdx.x; e < nf; e += blockDim.x) {
@@ -318,15 +381,15 @@ TinyArgs tiny_args(const DevPlan &p, int st_a) {
     return T;
 }
 
-size_t tiny_smem(const DevPlan &p, int st_a) {
-    const int64_t nf = p.steps[st_a].fsh.size(), nc = p.steps[st_a].csh.size();
-    return (size_t)(4 * nf + nc) * 8;
+size_t tiny_smem(const DevPlan &p, int st_a) {   // F, M, A, B (fine), Cg (<= fine / 2 + 1), histogram
+    const int64_t nf = p.steps[st_a].fsh.size();
+    return (size_t)(4 * nf + nf / 2 + 1) * 8 + kTinyHist * 4;
 }
 
 void tiny_attr() {
     static bool done = false;
     if (done) return;
-    const int mx = (4 * kTinyMaxNodes + kTinyMaxNodes / 2 + 1) * 8;   // coarse <= fine / 2 + 1 (221 KB)
+    const int mx = (4 * kTinyMaxNodes + kTinyMaxNodes / 2 + 1) * 8 + kTinyHist * 4;   // 200 KB
     CUDA_CHECK(cudaFuncSetAttribute(k_tiny_decompose, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     CUDA_CHECK(cudaFuncSetAttribute(k_tiny_recompose, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     done = true;
