@@ -776,6 +776,7 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
         // coefficients (transform.py:342-345) -- follows slab by slab on the side stream.
         const double *T0_pre = nullptr;
         cudaEvent_t ev_pre = nullptr;
+        bool t0_split = false;
         static const bool no_stream_dec = getenv("HPDR_NO_STREAM_DECODE") != nullptr;
         bool streamed = !no_stream_dec && !dev_blob && has_syms && !hh.single && coef && pp && n_sym == N &&
                         levels_of(dims) == (int)levels && (dtype == 0 || dtype == 1) && pp->host.L > 2 &&
@@ -915,7 +916,10 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                 fused_pass2(p, 0, Z0f, T0f, ctx->aux);
             }
             phase_mark("dec_end", s);
-            thomas_all(p, 0, T0f, ctx->aux);
+            // host output: only the plane-axis sweep here; the in-plane sweeps run per output slab
+            t0_split = classify(out) != MemKind::Device && thomas_plane_split(p, 0);
+            if (t0_split) thomas_plane_axis(p, 0, T0f, ctx->aux);
+            else thomas_all(p, 0, T0f, ctx->aux);
             phase_mark("thomas0", ctx->aux);
             ev_pre = ctx->event(191);
             CUDA_CHECK(cudaEventRecord(ev_pre, ctx->aux));
@@ -950,7 +954,7 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
             recompose_into(ctx, p, coef, out, dtype, s, nullptr, T0_pre, ev_pre);
         } else {
             void *stage = ctx->dbuf("out_stage", ob);
-            recompose_into(ctx, p, coef, stage, dtype, s, out, T0_pre, ev_pre);
+            recompose_into(ctx, p, coef, stage, dtype, s, out, T0_pre, ev_pre, t0_split);
         }
         if (sync) CUDA_CHECK(cudaStreamSynchronize(s));
     }

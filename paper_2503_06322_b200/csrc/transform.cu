@@ -1337,8 +1337,29 @@ void thomas_all(const DevPlan &p, int st_i, double *T, cudaStream_t s, const dou
     }
 }
 
+bool thomas_plane_split(const DevPlan &p, int st_i) {
+    static const bool off = getenv("HPDR_NO_PLANE_SPLIT") != nullptr;
+    const DevStep &st = p.steps[st_i];
+    return !off && p.dims.n[0] == 1 && !st.ax[0].active && st.ax[1].active && st.csh.size() > kThomasSmallMax;
+}
+
+void thomas_plane_axis(const DevPlan &p, int st_i, double *T, cudaStream_t s) {
+    const DevStep &st = p.steps[st_i];
+    thomas(T, st.csh, 1, st.ax[1], s);
+}
+
+void thomas_in_planes(const DevPlan &p, int st_i, double *T, int c_lo, int c_hi, cudaStream_t s) {
+    if (c_hi <= c_lo) return;
+    const DevStep &st = p.steps[st_i];
+    Shape4 sub = st.csh;
+    sub.n[1] = c_hi - c_lo;   // transform.py:259-260: the in-plane axes after the plane axis, per plane
+    double *T0 = T + (int64_t)c_lo * st.csh.n[2] * st.csh.n[3];
+    for (int a = 2; a < 4; a++)
+        if (st.ax[a].active) thomas(T0, sub, a, st.ax[a], s);
+}
+
 void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s,
-                    void *host_out, const double *T0_pre, cudaEvent_t ev_pre) {
+                    void *host_out, const double *T0_pre, cudaEvent_t ev_pre, bool t0_plane_axis_only) {
     const int L = p.host.L;
     if (L == 1 || !use_fused(p)) {
         const double *rec = recompose_device(ctx, p, coef, s);
@@ -1383,7 +1404,12 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
         CUDA_CHECK(cudaStreamWaitEvent(ctx->aux, ctx->event(0), 0));
         fused_pass1_recompose(p, 0, coef, Z0f, ctx->aux);
         fused_pass2(p, 0, Z0f, T, ctx->aux);
-        thomas_all(p, 0, T, ctx->aux);
+        if (direct && host_out && thomas_plane_split(p, 0)) {   // in-plane sweeps follow the output slabs
+            thomas_plane_axis(p, 0, T, ctx->aux);
+            t0_plane_axis_only = true;
+        } else {
+            thomas_all(p, 0, T, ctx->aux);
+        }
         CUDA_CHECK(cudaEventRecord(ev_side, ctx->aux));
     }
     // The coarser levels' corrections are independent of each other too: compute them up front,
@@ -1447,8 +1473,15 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
             // pinned staging ring, host-blocking, while the GPU runs the later slabs)
             const bool pageable_out = classify(host_out) == MemKind::Host;
             int nslab = 0;
+            int c_done = 0;   // coarse planes whose in-plane solves are done (t0_plane_axis_only)
             for (int a = 0, k = 0; a < n0; a += chunk, k++, nslab++) {
                 const int e = std::min(n0, a + chunk);
+                if (t0_plane_axis_only) {   // the coarse planes this slab's fine planes read
+                    const AxisTables &h0 = p.host.steps[0].ax[1];
+                    const int c_need = (e >= n0) ? (int)st.csh.n[1] : std::max(h0.pa[e - 1], h0.pb[e - 1]) + 1;
+                    thomas_in_planes(p, 0, const_cast<double *>(T), c_done, c_need, s);
+                    c_done = std::max(c_done, c_need);
+                }
                 fused_final(p, 0, Dc, coef, out, out_dtype, s, a, e, T);
                 CUDA_CHECK(cudaEventRecord(ctx->event(EvSlabOut, k), s));
             }

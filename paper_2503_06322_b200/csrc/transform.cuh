@@ -50,8 +50,19 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
 // D2H on the copy stream overlaps the next slab (out is then the device staging buffer).
 // T0_pre / ev_pre: the finest transition's correction, already being computed elsewhere (event
 // recorded after it); otherwise it is computed here on the side stream.
+// T0_pre / ev_pre: the finest transition's correction computed by the caller (streamed decode);
+// t0_plane_axis_only: it holds only the plane-axis (dim-0) solve, the in-plane axes are left to the
+// slab loop (thomas_plane_split).
 void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s,
-                    void *host_out = nullptr, const double *T0_pre = nullptr, cudaEvent_t ev_pre = nullptr);
+                    void *host_out = nullptr, const double *T0_pre = nullptr, cudaEvent_t ev_pre = nullptr,
+                    bool t0_plane_axis_only = false);
+// Whether transition st_i's Thomas solves can be split into the plane-axis sweep (over the whole
+// grid) and the in-plane sweeps per range of coarse planes (rank <= 3, plane axis active, not a
+// one-block grid): the finest level's output slabs then only wait for their own planes.
+bool thomas_plane_split(const DevPlan &p, int st_i);
+// The plane-axis sweep / the in-plane sweeps of coarse planes [c_lo, c_hi) (thomas_plane_split).
+void thomas_plane_axis(const DevPlan &p, int st_i, double *T, cudaStream_t s);
+void thomas_in_planes(const DevPlan &p, int st_i, double *T, int c_lo, int c_hi, cudaStream_t s);
 // Elements of pass 1's output Z0 at transition st_i.
 int64_t z0_elems(const DevPlan &p, int st_i);
 // Thomas solves of every active axis of transition st_i's coarse grid, in place.
