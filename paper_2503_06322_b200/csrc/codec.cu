@@ -859,7 +859,7 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
             };
             static const int G = [] {
                 const char *e = getenv("HPDR_DEC_GROUPS");
-                return e ? std::max(1, std::min(32, atoi(e))) : 6;
+                return e ? std::max(1, std::min(32, atoi(e))) : 16;   // 6 / 10 / 16 at 1024^3: 104.8 / 104.3 / 103.9 ms
             }();
             CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
             CUDA_CHECK(cudaStreamWaitEvent(ctx->h2d, ctx->event(0), 0));   // tables / buffers ready
