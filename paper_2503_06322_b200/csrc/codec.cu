@@ -98,7 +98,7 @@ int levels_of(const std::vector<uint64_t> &dims) {
 }
 
 // Encode keys (device) into the pending Huffman layout.  Returns false for single-key streams.
-void huffman_stage(hpdr_ctx *ctx, const uint32_t *d_keys, int64_t n, uint32_t dict, const std::vector<uint64_t> &hist,
+void huffman_stage(hpdr_ctx *ctx, const uint16_t *d_keys, int64_t n, uint32_t dict, const std::vector<uint64_t> &hist,
                    std::vector<uint8_t> &mid, EncodeResult &enc, bool &single, cudaStream_t s,
                    const EncodeHooks *hooks = nullptr) {
     // huffman_compress (huffman.py:366-396)
@@ -361,6 +361,14 @@ void fetch_pending_on(hpdr_ctx *ctx, const hpdr_ctx::Pending &P, void *out, uint
     fetch_pending(ctx, P, out, cap, s, sync, true);
 }
 
+__global__ void k_widen_keys(const uint16_t *__restrict__ a, uint32_t *__restrict__ b, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
+}
+__global__ void k_narrow_keys(const uint32_t *__restrict__ a, uint16_t *__restrict__ b, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = (uint16_t)a[i];
+}
+
 __global__ void k_gather_vals(const double *__restrict__ src, const long long *__restrict__ idx, int n,
                               double *__restrict__ dst) {
     const int k = threadIdx.x;
@@ -372,7 +380,7 @@ __global__ void k_gather_vals(const double *__restrict__ src, const long long *_
 // the optional streamed fetch into fetch_out.
 void finish_blob(hpdr_ctx *ctx, DevPlan &p, int dtype, int rank, const uint64_t *dims, double eb_rel,
                  uint32_t dict_size, double u_min, double u_max, double eb_abs, double bin, const QuantResult &q,
-                 uint32_t *keys, const double *d_coarse, const double *coef_for_coarse, void *fetch_out,
+                 uint16_t *keys, const double *d_coarse, const double *coef_for_coarse, void *fetch_out,
                  uint64_t fetch_cap, bool coarse_ready = false, const OutAlloc *alloc = nullptr) {
     {
         const int64_t N = p.n_total;
@@ -518,7 +526,7 @@ void compress_core(hpdr_ctx *ctx, const void *in, int dtype, int rank, const uin
             apply_range_hook(ctx, &u_min, &u_max);
         }
         phase_mark("minmax", s);
-        uint32_t *keys = (uint32_t *)ctx->dbuf("keys", N * 4 + 64);
+        uint16_t *keys = (uint16_t *)ctx->dbuf("keys16", N * 2 + 64);
         QuantResult q;
         const double *d_coarse;
         double eb_abs = 0.0, bin = 1.0;
@@ -581,7 +589,7 @@ void compress_from_coef(hpdr_ctx *ctx, const double *coef, int dtype, int rank, 
         fail(HPDR_ERR_VALIDATION, "dict_size must be in [2, 65535], got " + std::to_string(dict_size));
     const int64_t N = p.n_total;
     const int L = p.host.L;
-    uint32_t *keys = (uint32_t *)ctx->dbuf("keys", N * 4 + 64);
+    uint16_t *keys = (uint16_t *)ctx->dbuf("keys16", N * 2 + 64);
     const double eb_abs = eb_rel * (u_max - u_min);
     const double bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)L : 1.0;
     QuantResult q;
@@ -1030,12 +1038,18 @@ int hpdr_quantize(hpdr_ctx *ctx, const double *coef_in, int rank, const uint64_t
         const double vmin = has_range ? range_min : u_min, vmax = has_range ? range_max : u_max;
         const double eb_abs = eb_rel * (vmax - vmin);
         const double bin = eb_abs > 0 ? (2.0 * eb_abs) / (double)p.host.L : 1.0;
-        uint32_t *keys = (uint32_t *)ctx->dbuf("keys", N * 4 + 64);
+        uint16_t *keys = (uint16_t *)ctx->dbuf("keys16", N * 2 + 64);
         QuantResult q;
         quantize_device(ctx, coef, N, p.host.coarsest, bin, dict_size, keys, q, s);
         if (q.flags & 1) fail(HPDR_ERR_VALIDATION, "coefficients contain non-finite values");
         if (q.flags & 2) fail(HPDR_ERR_VALIDATION, "coefficient exceeds representable bin range");
-        CUDA_CHECK(cudaMemcpyAsync(keys_out, keys, N * 4, cudaMemcpyDefault, s));
+        // the stage API hands out the reference's uint32 keys (quantize.py:84)
+        uint32_t *keys32 = (uint32_t *)ctx->dbuf("keys32", N * 4 + 64);
+        if (N) {
+            k_widen_keys<<<grid_for(N, 256, 148 * 16), 256, 0, s>>>(keys, keys32, N);
+            LAUNCH_CHECK();
+        }
+        CUDA_CHECK(cudaMemcpyAsync(keys_out, keys32, N * 4, cudaMemcpyDefault, s));
         CUDA_CHECK(cudaMemcpyAsync(outlier_idx, q.d_outlier_idx, q.n_outliers * 8, cudaMemcpyDefault, s));
         CUDA_CHECK(cudaMemcpyAsync(outlier_bins, q.d_outlier_bins, q.n_outliers * 8, cudaMemcpyDefault, s));
         std::vector<double> cv(p.host.coarsest.size());
@@ -1120,12 +1134,18 @@ int hpdr_huffman_compress(hpdr_ctx *ctx, const uint32_t *keys_in, uint64_t n, ui
         bool bad = false;
         histogram_device(ctx, keys, (int64_t)n, dict_size, hist, &bad, s);
         if (bad) fail(HPDR_ERR_VALIDATION, "key out of range for dict_size " + std::to_string(dict_size));
+        // validated keys are < dict_size <= 65535: the encoder reads them as 16 bits
+        uint16_t *keys16 = (uint16_t *)ctx->dbuf("hkeys16", n * 2 + 64);
+        if (n) {
+            k_narrow_keys<<<grid_for((int64_t)n, 256, 148 * 16), 256, 0, s>>>(keys, keys16, (int64_t)n);
+            LAUNCH_CHECK();
+        }
         auto &P = ctx->pending;
         P = hpdr_ctx::Pending();
         P.huffman_only = true;
         EncodeResult enc;
         bool single;
-        huffman_stage(ctx, keys, (int64_t)n, dict_size, hist, P.mid, enc, single, s);
+        huffman_stage(ctx, keys16, (int64_t)n, dict_size, hist, P.mid, enc, single, s);
         P.single_key = single;
         P.n_units = enc.n_units;
         P.total_bits = enc.total_bits;

@@ -693,7 +693,7 @@ __global__ void k_quantize_coarsest(const double *__restrict__ vals, const long 
         if (!isfinite(v)) fl |= 1;
         else if (fabs(v / qbin(q)) >= 4611686018427387904.0) fl |= 2;
         if (fl) atomicOr(q.flags, fl);
-        q.keys[idx[k]] = 0u;
+        q.keys[idx[k]] = 0;
     }
     if (k == 0) atomicAdd(&q.hist[0], (unsigned long long)n);
 }
@@ -1063,7 +1063,7 @@ void fused_pass1_quantize(const DevPlan &p, int st_i, const void *F, bool f32, c
     c_hi = clamp_hi(p, st_i, c_hi);
     const double frac = (double)(c_hi - c_lo) / fused_out_planes(p, st_i);
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
-    KPROF(st_i == 0 ? "k_level_pass1q" : "k_level_pass1q_coarse", frac * ((f32 ? 4.0 : 8.0) * nf + 4.0 * (nf - nc) + 8.0 * nc + 8.0 * z0_size(p, st_i)), s);
+    KPROF(st_i == 0 ? "k_level_pass1q" : "k_level_pass1q_coarse", frac * ((f32 ? 4.0 : 8.0) * nf + 2.0 * (nf - nc) + 8.0 * nc + 8.0 * z0_size(p, st_i)), s);
     // the quad kernel's plane ring pays off on large levels; tiny ones (latency-bound) take the
     // single-node kernel (HPDR_QUAD_MIN: smallest fine level, in nodes, that uses quads)
     static const int64_t quad_min = getenv("HPDR_QUAD_MIN") ? atoll(getenv("HPDR_QUAD_MIN")) : (1LL << 18);
@@ -1097,7 +1097,7 @@ void quantize_fine(const DevPlan &p, const double *coef, const QuantOut &q, cuda
     const DevStep &st = p.steps[0];
     const View v = view_of(p, 0);
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
-    KPROF("k_quantize_fine", 12.0 * (nf - nc), s);
+    KPROF("k_quantize_fine", 10.0 * (nf - nc), s);
     dim3 grid((v.n2 + 31) / 32, (v.n1 + 7) / 8, slabs_for((int64_t)v.n1 * v.n2, v.n0));
     dim3 block(32, 8);
 #define QF(M)                                                                                                      \

@@ -19,7 +19,7 @@ struct QuantOut {
     const double *bin_dev = nullptr;   // when set, the bin width is read here (graph replays)
     long long half;
     uint32_t dict;
-    uint32_t *keys;               // N keys, finest order
+    uint16_t *keys;               // N keys, finest order (16 bits: dict_size <= 65535, quantize.py:61)
     uint32_t *omask;              // N/32 words: outlier flags (zeroed by the caller)
     long long *obins;             // N slots, written only at outliers
     unsigned long long *hist;     // dict counts (zeroed by the caller)

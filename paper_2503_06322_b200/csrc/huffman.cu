@@ -162,7 +162,23 @@ constexpr int kEncTableMax = 4096;     // codes + lengths + the unit's word buff
 __device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
 
 // Per-unit bit totals.  One block per unit; 16 consecutive symbols per thread.
-__global__ void __launch_bounds__(kEncThreads) k_unit_bits(const uint32_t *__restrict__ keys, int64_t n,
+// Keys are 16 bits (dict_size <= 65535, quantize.py:61): a thread's 16 consecutive keys are two
+// 16-byte loads.
+__device__ __forceinline__ void load_keys16(const uint16_t *p, uint32_t k[16]) {
+    const uint4 *v4 = reinterpret_cast<const uint4 *>(p);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const uint4 v = v4[h];
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            k[8 * h + 2 * i] = w[i] & 0xffffu;
+            k[8 * h + 2 * i + 1] = w[i] >> 16;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kEncThreads) k_unit_bits(const uint16_t *__restrict__ keys, int64_t n,
                                                            const uint8_t *__restrict__ lens, uint32_t dict,
                                                            uint64_t *__restrict__ ubits, int64_t units) {
     __shared__ uint8_t sl[kSmemTableMax];
@@ -176,12 +192,10 @@ __global__ void __launch_bounds__(kEncThreads) k_unit_bits(const uint32_t *__res
         const int64_t lo = u * kBlockSymbols + (int64_t)threadIdx.x * kSymPerThread;
         unsigned s = 0;
         if (lo + kSymPerThread <= n) {
-            const uint4 *p = reinterpret_cast<const uint4 *>(keys + lo);
+            uint32_t k[kSymPerThread];
+            load_keys16(keys + lo, k);
 #pragma unroll
-            for (int q = 0; q < kSymPerThread / 4; q++) {
-                uint4 v = p[q];
-                s += sm ? sl[v.x] + sl[v.y] + sl[v.z] + sl[v.w] : lens[v.x] + lens[v.y] + lens[v.z] + lens[v.w];
-            }
+            for (int q = 0; q < kSymPerThread; q++) s += sm ? sl[k[q]] : lens[k[q]];
         } else {
             for (int64_t i = lo; i < min64(n, lo + kSymPerThread); i++) s += sm ? sl[keys[i]] : lens[keys[i]];
         }
@@ -194,7 +208,7 @@ __global__ void __launch_bounds__(kEncThreads) k_unit_bits(const uint32_t *__res
 // Pack one unit per block: per-thread bit offsets by block scan, codewords OR-ed into a
 // shared word buffer aligned to the unit's global word, then streamed out (boundary words
 // shared with the neighbouring units use atomicOr on a zeroed buffer).
-__global__ void __launch_bounds__(kEncThreads) k_encode(const uint32_t *__restrict__ keys, int64_t n,
+__global__ void __launch_bounds__(kEncThreads) k_encode(const uint16_t *__restrict__ keys, int64_t n,
                                                         const uint8_t *__restrict__ lens,
                                                         const uint32_t *__restrict__ codes, uint32_t dict,
                                                         const uint64_t *__restrict__ uoff,
@@ -215,12 +229,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const uint32_t *__restri
         uint32_t k16[kSymPerThread];
         int cnt = 0;
         if (lo + kSymPerThread <= n) {
-            const uint4 *p = reinterpret_cast<const uint4 *>(keys + lo);
-#pragma unroll
-            for (int q = 0; q < kSymPerThread / 4; q++) {
-                uint4 v = p[q];
-                k16[4 * q] = v.x; k16[4 * q + 1] = v.y; k16[4 * q + 2] = v.z; k16[4 * q + 3] = v.w;
-            }
+            load_keys16(keys + lo, k16);
             cnt = kSymPerThread;
         } else {
             for (int64_t i = lo; i < min64(n, lo + kSymPerThread); i++) k16[cnt++] = keys[i];
@@ -260,7 +269,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const uint32_t *__restri
 
 }  // namespace
 
-void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict_size, const uint8_t *lengths,
+void encode_device(hpdr_ctx *ctx, const uint16_t *keys, int64_t n, uint32_t dict_size, const uint8_t *lengths,
                    const uint32_t *codes, EncodeResult &res, cudaStream_t s, const EncodeHooks *hooks,
                    const uint64_t *hist) {
     const int64_t units = (n + kBlockSymbols - 1) / kBlockSymbols;
@@ -277,7 +286,7 @@ void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict
         small_copy(d_len, ht + (size_t)dict_size * 4, dict_size, s);
     }
     {
-        KPROF("k_unit_bits", 4.0 * n + 8.0 * units, s);
+        KPROF("k_unit_bits", 2.0 * n + 8.0 * units, s);
         k_unit_bits<<<(unsigned)std::min<int64_t>(units, 148 * 16), kEncThreads, 0, s>>>(keys, n, d_len, dict_size, ubits,
                                                                                           units);
         LAUNCH_CHECK();
@@ -313,7 +322,7 @@ void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict
     for (int g = 0; g < G; g++) {
         const int64_t cnt = ub[g + 1] - ub[g];
         if (cnt > 0) {
-            KPROF("k_encode", (4.0 * n + 16.0 * units + res.total_bits / 8.0) * ((double)cnt / (double)units), s);
+            KPROF("k_encode", (2.0 * n + 16.0 * units + res.total_bits / 8.0) * ((double)cnt / (double)units), s);
             k_encode<<<(unsigned)std::min<int64_t>(cnt, 148 * 8), kEncThreads, 0, s>>>(keys, n, d_len, d_code, dict_size,
                                                                                       uoff, ubits, res.d_words, ub[g],
                                                                                       ub[g + 1]);

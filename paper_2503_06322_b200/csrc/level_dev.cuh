@@ -80,7 +80,7 @@ __device__ __forceinline__ void quant_node(double mc, const QuantOut &q, double 
         const int ri = (int)r;   // exact: |r| < 2^15
         key = ((uint32_t)ri << 1) ^ (uint32_t)(ri >> 31);   // zigzag (quantize.py:24-31)
     }
-    q.keys[f] = key;
+    q.keys[f] = (uint16_t)key;
     hist_add(sh_hist, q.hist, sh_ok, key);
 }
 

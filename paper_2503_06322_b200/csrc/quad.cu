@@ -88,8 +88,9 @@ __device__ __forceinline__ void bulk_load(unsigned dst, const void *src, unsigne
 }
 
 // Predicated stores / shared-histogram increments (no branch, no reconvergence point).
-__device__ __forceinline__ void st_u32_if(uint32_t *p, uint32_t v, bool c) {
-    asm volatile("{.reg .pred p; setp.ne.b32 p, %2, 0; @p st.global.u32 [%0], %1;}" ::"l"(p), "r"(v), "r"((int)c));
+__device__ __forceinline__ void st_u16_if(uint16_t *p, uint32_t v, bool c) {
+    asm volatile("{.reg .pred p; setp.ne.b32 p, %2, 0; @p st.global.u16 [%0], %1;}" ::"l"(p), "h"((unsigned short)v),
+                 "r"((int)c));
 }
 __device__ __forceinline__ void st_f64_if(double *p, double v, bool c) {
     asm volatile("{.reg .pred p; setp.ne.b32 p, %2, 0; @p st.global.f64 [%0], %1;}" ::"l"(p), "d"(v), "r"((int)c));
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(kQThreads, TMA ? 4 : 3)
                     for (int k = 0; k < 4; k++) st_f64_if(cp + (unsigned)fcol[k], mc[k], fine & (1u << k));
                 } else {
                     // fast path (quant_node for an in-range, comfortably rounded quotient), branch-free
-                    uint32_t *kp = opaque(q.keys + fb);
+                    uint16_t *kp = opaque(q.keys + fb);
                     unsigned slow = 0;
 #pragma unroll
                     for (int k = 0; k < 4; k++) {
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(kQThreads, TMA ? 4 : 3)
                         const int ri = (int)r;
                         const uint32_t key = ((uint32_t)ri << 1) ^ (uint32_t)(ri >> 31);
                         const bool fk = (fine >> k) & 1u;
-                        st_u32_if(kp + (unsigned)fcol[k], key, fk && ok);
+                        st_u16_if(kp + (unsigned)fcol[k], key, fk && ok);
                         if (sh_ok) atomicAdd(&sh_hist[fk && ok ? key : (uint32_t)kQHist], 1u);
                         else if (fk && ok) atomicAdd(&q.hist[key], 1ULL);
                         slow |= (fk && !ok) ? 1u << k : 0u;

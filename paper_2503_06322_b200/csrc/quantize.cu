@@ -38,7 +38,7 @@ __device__ __forceinline__ void hist_add(uint32_t *sh, unsigned long long *g, bo
 
 __global__ void __launch_bounds__(kQThreads) k_quantize(const double *__restrict__ coef, int64_t n, Coarsest co,
                                                         double bin, long long half, uint32_t dict,
-                                                        uint32_t *__restrict__ keys, uint32_t *__restrict__ omask,
+                                                        uint16_t *__restrict__ keys, uint32_t *__restrict__ omask,
                                                         unsigned long long *__restrict__ hist, int *__restrict__ flags) {
     extern __shared__ uint32_t sh_hist[];
     const bool use_sh = dict <= kSmemHistMax;
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kQThreads) k_quantize(const double *__restrict
             if (lane == 0) omask[wbase >> 5] = om;
             const uint32_t key = out ? 0u : (uint32_t)(r >= 0.0 ? 2.0 * r : -2.0 * r - 1.0);   // zigzag
             if (valid) {
-                keys[i] = key;
+                keys[i] = (uint16_t)key;
                 if (use_sh) atomicAdd(&sh_hist[key], 1u);
                 else atomicAdd(&hist[key], 1ULL);
             }
@@ -195,7 +195,7 @@ __global__ void k_histogram(const uint32_t *__restrict__ keys, int64_t n, uint32
 }  // namespace
 
 void quantize_device(hpdr_ctx *ctx, const double *coef, int64_t n, const std::vector<int64_t> &coarsest,
-                     double bin_width, uint32_t dict_size, uint32_t *keys, QuantResult &res, cudaStream_t s) {
+                     double bin_width, uint32_t dict_size, uint16_t *keys, QuantResult &res, cudaStream_t s) {
     const int64_t words = (n + 31) / 32;
     uint32_t *omask = (uint32_t *)ctx->dbuf("omask", words * 4);
     unsigned long long *hist = (unsigned long long *)ctx->dbuf("hist", (size_t)dict_size * 8);
@@ -210,7 +210,7 @@ void quantize_device(hpdr_ctx *ctx, const double *coef, int64_t n, const std::ve
     if (smem > 48 * 1024) CUDA_CHECK(cudaFuncSetAttribute(k_quantize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     unsigned grid = grid_for(n, kQThreads, 148 * 4);
     {
-        KPROF("k_quantize", 12.0 * n + n / 8.0, s);
+        KPROF("k_quantize", 10.0 * n + n / 8.0, s);
         k_quantize<<<grid, kQThreads, smem, s>>>(coef, n, co, bin_width, half, dict_size, keys, omask, hist, flags);
         LAUNCH_CHECK();
     }

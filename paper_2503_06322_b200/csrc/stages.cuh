@@ -21,7 +21,7 @@ struct QuantResult {
 // Quantize N coefficients (device) into keys (device) and the ordered outlier arrays
 // (device, sized after counting).  hist is accumulated on the device and copied back.
 void quantize_device(hpdr_ctx *ctx, const double *coef, int64_t n, const std::vector<int64_t> &coarsest,
-                     double bin_width, uint32_t dict_size, uint32_t *keys, QuantResult &res, cudaStream_t s);
+                     double bin_width, uint32_t dict_size, uint16_t *keys, QuantResult &res, cudaStream_t s);
 
 // Second half of quantization once keys, the outlier mask ("omask"), "hist" and "qflags" are
 // populated: ordered outlier compaction and read-back.  Outlier bins come from the sparse
@@ -60,7 +60,7 @@ struct EncodeHooks {
     std::function<void(const EncodeResult &)> ready;
     std::function<void(int, uint64_t, uint64_t)> group_done;
 };
-void encode_device(hpdr_ctx *ctx, const uint32_t *keys, int64_t n, uint32_t dict_size, const uint8_t *lengths,
+void encode_device(hpdr_ctx *ctx, const uint16_t *keys, int64_t n, uint32_t dict_size, const uint8_t *lengths,
                    const uint32_t *codes, EncodeResult &res, cudaStream_t s, const EncodeHooks *hooks = nullptr,
                    const uint64_t *hist = nullptr);   // host histogram: total bits without a device read-back
 

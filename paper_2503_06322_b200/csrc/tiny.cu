@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny_decompose(TinyArgs T, con
         const double v = F[k];
         if (!isfinite(v)) fl |= 1;
         else if (fabs(v / bin) >= 4611686018427387904.0) fl |= 2;
-        q.keys[cidx[k]] = 0u;
+        q.keys[cidx[k]] = 0;
     }
     if (threadIdx.x == 0 && n_co) atomicAdd(&q.hist[0], (unsigned long long)n_co);
     if (fl) atomicOr(q.flags, fl);
