@@ -486,7 +486,8 @@ void launch_pass1_quad(const TIn *F, int n0, int n1, int n2, const DevAxis &a0, 
     const int min_planes = (int64_t)gx * gy * std::max(1, c_count / 8) >= want ? 8 : 2;
     slabs = std::max(1, std::min(slabs, std::max(1, c_count / min_planes)));
     // every block flushes its shared histogram: no more than ~4 blocks per SM on small grids
-    if (slab_env <= 0) slabs = std::max(1, std::min<int>(slabs, (int)std::max<int64_t>(1, 148LL * 4 / ((int64_t)gx * gy))));
+    if (slab_env <= 0 && min_planes == 2)
+        slabs = std::max(1, std::min<int>(slabs, (int)std::max<int64_t>(1, 148LL * 4 / ((int64_t)gx * gy))));
     const dim3 grid(gx, gy, (unsigned)slabs);
     const int z0_vec = ((int64_t)n1 * n2 % 2 == 0 && n2 % 2 == 0) ? 1 : 0;
     CUtensorMap tm;
