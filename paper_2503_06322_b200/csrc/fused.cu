@@ -1136,6 +1136,16 @@ void fused_final(const DevPlan &p, int st_i, const double *cv, const double *coe
     if (j_hi < 0 || j_hi > v.n0) j_hi = v.n0;
     const double frac = (double)(j_hi - j_lo) / v.n0;
     KPROF("k_level_final", frac * ((corr ? 16.0 : 8.0) * nc + 8.0 * (nf - nc) + (out_dtype == 0 ? 4.0 : 8.0) * nf), s);
+    static const bool no_quad_final = getenv("HPDR_NO_QUAD_FINAL") != nullptr;
+    if (v.act == 7 && !no_quad_final && quad_eligible(p, st_i)) {
+        if (out_dtype == 0)
+            launch_final_quad<float>(cv, corr, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, coef, (float *)D,
+                                     j_lo, j_hi - j_lo, s);
+        else
+            launch_final_quad<double>(cv, corr, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, coef, (double *)D,
+                                      j_lo, j_hi - j_lo, s);
+        return;
+    }
     if (out_dtype == 0)
         launch_final<float>(v.act, cv, corr, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, coef, (float *)D, j_lo,
                             j_hi - j_lo, s);

@@ -28,6 +28,11 @@ struct QuantOut {
 
 // quad.cu: pass 1 with one 2 x 2 node quad per thread (regular all-active 3-D transitions).
 bool quad_eligible(const DevPlan &p, int st_i);
+// quad.cu: the recompose output of a regular all-active transition, one 2 x 2 node quad per thread.
+template <typename TOut>
+void launch_final_quad(const double *cv, const double *corr, int n0, int n1, int n2, const DevAxis &a0,
+                       const DevAxis &a1, const DevAxis &a2, const LevelMap &lm, const double *coef, TOut *D, int j_base,
+                       int j_count, cudaStream_t s);
 template <int MODE, typename TIn>
 void launch_pass1_quad(const TIn *F, int n0, int n1, int n2, const DevAxis &a0, const DevAxis &a1, const DevAxis &a2,
                        const LevelMap &lm, double *coef, double *Z0, double *Cg, const QuantOut &q, int c_base,

@@ -460,6 +460,115 @@ bool axis_regular(const AxisTables &t) {
     return true;
 }
 
+// ---------------------------------------------------------------------------------- final (quads)
+// Recompose output of a regular all-active transition, one 2 x 2 node quad per thread:
+// D = P(cv - corr) + mc (transform.py:345-347) with P the nested lerps of transform.py:264-268.
+// The quad's interpolant reads the axis-0 interpolant P0 only at its four coarse corners, so each
+// thread forms those itself from the two coarse planes around the fine plane (cv - corr, cached per
+// corner for the next fine plane) -- no shared footprint and no barrier -- and the coefficients of
+// the next plane are loaded one plane ahead.  Same values and operation order as k_level_final.
+template <typename TOut>
+__global__ void __launch_bounds__(kQThreads) k_final_quad(const double *__restrict__ cv, const double *__restrict__ corr,
+                                                         int n0, int n1, int n2, DevAxis ax0, DevAxis ax1, DevAxis ax2,
+                                                         LevelMap lm, const double *__restrict__ coef,
+                                                         TOut *__restrict__ D, int j_base, int j_count) {
+    const int tid = threadIdx.x;
+    const int qx = tid & (kQX - 1), qy = tid / kQX;
+    const int c0 = blockIdx.x * kTileX + 2 * qx, r0 = blockIdx.y * kTileY + 2 * qy;
+    if (r0 >= n1 || c0 >= n2) return;   // no barriers below
+    int lo, hi;
+    slab_range(j_count, gridDim.z, blockIdx.z, lo, hi);
+    lo += j_base;
+    hi += j_base;
+    const bool rowB = r0 + 1 < n1, colB = c0 + 1 < n2;
+    const bool rowfo = rowB && __ldg(ax1.pb + r0 + 1) >= 0;
+    const bool colfo = colB && __ldg(ax2.pb + c0 + 1) >= 0;
+    const double t1 = rowfo ? __ldg(ax1.pt + r0 + 1) : 0.0;
+    const double t2 = colfo ? __ldg(ax2.pt + c0 + 1) : 0.0;
+    // coarse corners: rows cy0 / cyB, columns cx0 / cxB (the coarse neighbours of r0 + 1 / c0 + 1)
+    const int nc2 = ax2.nc;
+    const int cy0 = __ldg(ax1.pa + r0), cx0 = __ldg(ax2.pa + c0);
+    const int cyB = rowfo ? __ldg(ax1.pb + r0 + 1) : (rowB ? __ldg(ax1.pa + r0 + 1) : cy0);
+    const int cxB = colfo ? __ldg(ax2.pb + c0 + 1) : (colB ? __ldg(ax2.pa + c0 + 1) : cx0);
+    const int64_t cplane = (int64_t)ax1.nc * nc2;
+    const int64_t co[4] = {(int64_t)cy0 * nc2 + cx0, (int64_t)cy0 * nc2 + cxB, (int64_t)cyB * nc2 + cx0,
+                           (int64_t)cyB * nc2 + cxB};
+    // finest offsets of the four nodes within a finest plane; node k: (r0 | r0 + 1) x (c0 | c0 + 1)
+    const int64_t m1a = __ldg(lm.m1 + r0), m2a = __ldg(lm.m2 + c0);
+    const int64_t f00 = m1a * lm.D2 + m2a;
+    const int64_t fd1 = rowB ? (__ldg(lm.m1 + r0 + 1) - m1a) * lm.D2 : 0, fd2 = colB ? __ldg(lm.m2 + c0 + 1) - m2a : 0;
+    const unsigned act = 1u | (colB ? 2u : 0u) | (rowB ? 4u : 0u) | (rowB && colB ? 8u : 0u);
+    const unsigned cfo = (colfo ? 2u : 0u) | (rowfo ? 4u : 0u) | (rowfo || colfo ? 8u : 0u);   // fine-only in-plane
+    const int64_t fplane = lm.D1 * lm.D2;
+    // coarse - corr at the four corners of coarse plane c; the even and the odd plane last read are
+    // kept (a coarse plane serves up to three consecutive fine planes)
+    int ce = -1, cod = -1;
+    double ve[4], vo[4];
+    auto fetch = [&](int c, double *v) {
+        const double *b = cv + (int64_t)c * cplane;
+#pragma unroll
+        for (int k = 0; k < 4; k++) v[k] = __ldg(b + co[k]);
+        if (corr) {   // coarse - corr (the elementwise k_sub folded in)
+            const double *r = corr + (int64_t)c * cplane;
+#pragma unroll
+            for (int k = 0; k < 4; k++) v[k] = dsub(v[k], __ldg(r + co[k]));
+        }
+    };
+    auto corners = [&](int c, double *v) {
+        if (c & 1) {
+            if (cod != c) {
+                cod = c;
+                fetch(c, vo);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; k++) v[k] = vo[k];
+        } else {
+            if (ce != c) {
+                ce = c;
+                fetch(c, ve);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; k++) v[k] = ve[k];
+        }
+    };
+    auto load_mc = [&](int j, double *m) {
+        const unsigned need = act & (__ldg(ax0.pb + j) >= 0 ? 15u : cfo);
+        const double *cp = coef + (int64_t)__ldg(lm.m0 + j) * fplane;
+        m[0] = (need & 1u) ? __ldg(cp + f00) : 0.0;
+        m[1] = (need & 2u) ? __ldg(cp + f00 + fd2) : 0.0;
+        m[2] = (need & 4u) ? __ldg(cp + f00 + fd1) : 0.0;
+        m[3] = (need & 8u) ? __ldg(cp + f00 + fd1 + fd2) : 0.0;
+    };
+    double mcn[4];
+    if (lo < hi) load_mc(lo, mcn);
+    for (int j = lo; j < hi; j++) {
+        double mc[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) mc[k] = mcn[k];
+        if (j + 1 < hi) load_mc(j + 1, mcn);   // one plane ahead
+        const int pb0 = __ldg(ax0.pb + j);
+        const int ca = __ldg(ax0.pa + j);
+        double P[4];
+        corners(ca, P);
+        if (pb0 >= 0) {   // fine-only plane: P0 = lerp(cv[ca], cv[cb], t0) at the corners
+            const double t0 = __ldg(ax0.pt + j);
+            double Q[4];
+            corners(pb0, Q);
+#pragma unroll
+            for (int k = 0; k < 4; k++) P[k] = lerp(P[k], Q[k], t0);
+        }
+        // P[0] = P00, P[1] = P0B, P[2] = PB0, P[3] = PBB
+        const double p1a = rowfo ? lerp(P[0], P[2], t1) : P[2];
+        const double p1b = rowfo ? lerp(P[1], P[3], t1) : P[3];
+        const double pred[4] = {P[0], colfo ? lerp(P[0], P[1], t2) : P[1], p1a, colfo ? lerp(p1a, p1b, t2) : p1b};
+        TOut *dp = D + (int64_t)j * n1 * n2 + (int64_t)r0 * n2 + c0;
+        dp[0] = (TOut)dadd(pred[0], mc[0]);
+        if (act & 2u) dp[1] = (TOut)dadd(pred[1], mc[1]);
+        if (act & 4u) dp[n2] = (TOut)dadd(pred[2], mc[2]);
+        if (act & 8u) dp[n2 + 1] = (TOut)dadd(pred[3], mc[3]);
+    }
+}
+
 }  // namespace
 
 bool quad_eligible(const DevPlan &p, int st_i) {
@@ -471,6 +580,24 @@ bool quad_eligible(const DevPlan &p, int st_i) {
     if (getenv("HPDR_NO_QUAD")) return false;
     return axis_regular(h.ax[1]) && axis_regular(h.ax[2]) && axis_regular(h.ax[3]);
 }
+
+template <typename TOut>
+void launch_final_quad(const double *cv, const double *corr, int n0, int n1, int n2, const DevAxis &a0,
+                       const DevAxis &a1, const DevAxis &a2, const LevelMap &lm, const double *coef, TOut *D, int j_base,
+                       int j_count, cudaStream_t s) {
+    if (j_count <= 0) return;
+    const unsigned gx = (n2 + kTileX - 1) / kTileX, gy = (n1 + kTileY - 1) / kTileY;
+    const int64_t want = 148LL * 12 * 4;   // >= 4 waves of 12 resident blocks per SM
+    const int slabs = (int)std::max<int64_t>(1, std::min<int64_t>(j_count, (want + (int64_t)gx * gy - 1) / ((int64_t)gx * gy)));
+    k_final_quad<TOut><<<dim3(gx, gy, (unsigned)slabs), kQThreads, 0, s>>>(cv, corr, n0, n1, n2, a0, a1, a2, lm, coef, D,
+                                                                          j_base, j_count);
+    LAUNCH_CHECK();
+}
+template void launch_final_quad<float>(const double *, const double *, int, int, int, const DevAxis &, const DevAxis &,
+                                       const DevAxis &, const LevelMap &, const double *, float *, int, int, cudaStream_t);
+template void launch_final_quad<double>(const double *, const double *, int, int, int, const DevAxis &, const DevAxis &,
+                                        const DevAxis &, const LevelMap &, const double *, double *, int, int,
+                                        cudaStream_t);
 
 template <int MODE, typename TIn>
 void launch_pass1_quad(const TIn *F, int n0, int n1, int n2, const DevAxis &a0, const DevAxis &a1, const DevAxis &a2,

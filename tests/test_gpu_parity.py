@@ -219,14 +219,15 @@ print("variant ok")
 @pytest.mark.parametrize("env", [{"HPDR_GENERIC": "1"}, {"HPDR_NO_STREAM": "1"}, {"HPDR_NO_QUAD": "1"},
                                  {"HPDR_NO_TMA": "1"}, {"HPDR_QUAD_SLABS": "3"}, {"HPDR_QUAD_SLABS": "64"}, {"HPDR_QUAD_MIN": "0"},
                                  {"HPDR_NO_TINY": "1"}, {"HPDR_NO_TINY": "1", "HPDR_NO_GRAPH": "1"},
-                                 {"HPDR_NO_PLANE_SPLIT": "1"},
+                                 {"HPDR_NO_PLANE_SPLIT": "1"}, {"HPDR_NO_QUAD_FINAL": "1"},
                                  {"HPDR_THOMAS_TILE": "1"}, {}])
 def test_execution_variants_bit_identical(env):
     """Every execution variant gives the reference's blobs: the per-axis (generic) path, the non-streamed
     fused path, pass 1 without quads, the quad kernel without TMA, forced slab splits (down to two coarse
     planes per slab), the shared-memory tile Thomas solve at every size, and the small end of the
     hierarchy as per-level launches instead of the one-block kernel (tiny.cu), and the finest
-    correction solved whole before the output slabs instead of plane range by plane range."""
+    correction solved whole before the output slabs instead of plane range by plane range, and the
+    final level with one node per thread instead of quads."""
     import subprocess
     import sys
 
