@@ -1089,6 +1089,13 @@ void fused_pass1_recompose(const DevPlan &p, int st_i, const double *coef, doubl
     const int64_t nf = st.fsh.size(), nc = st.csh.size();
     KPROF("k_level_pass1r", frac * (8.0 * (nf - nc) + 8.0 * z0_size(p, st_i)), s);
     const QuantOut q{};
+    // the finest transition (coef is dense in its own layout there): quads over coef planes
+    static const bool no_quad_p1r = getenv("HPDR_NO_QUAD_P1R") != nullptr;
+    if (st_i == 0 && v.act == 7 && !no_quad_p1r && quad_eligible(p, 0)) {
+        launch_pass1_quad<1, double>(coef, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, nullptr, Z0, nullptr, q,
+                                     c_lo, c_hi - c_lo, s);
+        return;
+    }
     launch_pass1<1, double>(v.act, nullptr, v.n0, v.n1, v.n2, st.ax[1], st.ax[2], st.ax[3], v.lm, nullptr, coef, Z0,
                             nullptr, q, c_lo, c_hi - c_lo, s);
 }

@@ -301,10 +301,15 @@ __global__ void __launch_bounds__(kQThreads, TMA ? 4 : 3)
             const int4 hd = *reinterpret_cast<const int4 *>(&pj);   // fa, fb, ca, cb
             const bool pfo = pj.fo != 0;
             const TIn *so = ring + ((unsigned)i % R) * G::slot_elems;
-            double own[4], P00, P0B, PB0, PBB;
+            double own[4], P00 = 0.0, P0B = 0.0, PB0 = 0.0, PBB = 0.0;
             ld2(so + so_r0, own[0], own[1]);
             ld2(so + so_r0 + G::pitch, own[2], own[3]);
-            if (pfo) {   // fine-only plane: P0 = lerp(F[fa], F[fb], t0) at the four corners
+            double mc[4];
+            if constexpr (MODE == 1) {   // recompose: the coefficients of this level's fine-only nodes, 0 elsewhere
+                const unsigned fm = act & (pfo ? 15u : nfo);
+#pragma unroll
+                for (int k = 0; k < 4; k++) mc[k] = ((fm >> k) & 1u) ? own[k] : 0.0;
+            } else if (pfo) {   // fine-only plane: P0 = lerp(F[fa], F[fb], t0) at the four corners
                 const double t0 = pj.t;
                 const TIn *sa = ring + ((unsigned)(hd.x - j_start) % R) * G::slot_elems;
                 const TIn *sb = ring + ((unsigned)(hd.y - j_start) % R) * G::slot_elems;
@@ -318,8 +323,8 @@ __global__ void __launch_bounds__(kQThreads, TMA ? 4 : 3)
                 PB0 = (double)so[so_rB];
                 PBB = (double)so[so_rB + dcB];
             }
-            double mc[4];
-            {
+            (void)P0B;
+            if constexpr (MODE != 1) {
                 const double p1a = rowfo ? lerp(P00, PB0, t1) : PB0;
                 const double p1b = rowfo ? lerp(P0B, PBB, t1) : PBB;
                 mc[0] = dsub(own[0], P00);
@@ -327,7 +332,7 @@ __global__ void __launch_bounds__(kQThreads, TMA ? 4 : 3)
                 mc[2] = dsub(own[2], p1a);
                 mc[3] = dsub(own[3], colfo ? lerp(p1a, p1b, t2) : p1b);
             }
-            if (j >= own_lo && j < own_hi) {   // uniform
+            if (MODE != 1 && j >= own_lo && j < own_hi) {   // uniform
                 const int64_t fb = (int64_t)m0j * fplane;
                 const unsigned fine = act & (pfo ? 15u : nfo), coarse = act & ~fine;
                 if (coarse) {
@@ -335,7 +340,7 @@ __global__ void __launch_bounds__(kQThreads, TMA ? 4 : 3)
 #pragma unroll
                     for (int k = 0; k < 4; k++) st_f64_if(cgp + cgc[k], own[k], coarse & (1u << k));
                 }
-                if (MODE == 0) {
+                if constexpr (MODE == 0) {
                     double *cp = opaque(coef + fb);
 #pragma unroll
                     for (int k = 0; k < 4; k++) st_f64_if(cp + (unsigned)fcol[k], mc[k], fine & (1u << k));
@@ -637,6 +642,9 @@ template void launch_pass1_quad<0, float>(const float *, int, int, int, const De
                                           const DevAxis &, const LevelMap &, double *, double *, double *,
                                           const QuantOut &, int, int, cudaStream_t);
 template void launch_pass1_quad<0, double>(const double *, int, int, int, const DevAxis &, const DevAxis &,
+                                           const DevAxis &, const LevelMap &, double *, double *, double *,
+                                           const QuantOut &, int, int, cudaStream_t);
+template void launch_pass1_quad<1, double>(const double *, int, int, int, const DevAxis &, const DevAxis &,
                                            const DevAxis &, const LevelMap &, double *, double *, double *,
                                            const QuantOut &, int, int, cudaStream_t);
 template void launch_pass1_quad<2, float>(const float *, int, int, int, const DevAxis &, const DevAxis &,

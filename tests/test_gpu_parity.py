@@ -219,7 +219,7 @@ print("variant ok")
 @pytest.mark.parametrize("env", [{"HPDR_GENERIC": "1"}, {"HPDR_NO_STREAM": "1"}, {"HPDR_NO_QUAD": "1"},
                                  {"HPDR_NO_TMA": "1"}, {"HPDR_QUAD_SLABS": "3"}, {"HPDR_QUAD_SLABS": "64"}, {"HPDR_QUAD_MIN": "0"},
                                  {"HPDR_NO_TINY": "1"}, {"HPDR_NO_TINY": "1", "HPDR_NO_GRAPH": "1"},
-                                 {"HPDR_NO_PLANE_SPLIT": "1"}, {"HPDR_NO_QUAD_FINAL": "1"},
+                                 {"HPDR_NO_PLANE_SPLIT": "1"}, {"HPDR_NO_QUAD_FINAL": "1"}, {"HPDR_NO_QUAD_P1R": "1"},
                                  {"HPDR_THOMAS_TILE": "1"}, {}])
 def test_execution_variants_bit_identical(env):
     """Every execution variant gives the reference's blobs: the per-axis (generic) path, the non-streamed

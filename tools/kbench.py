@@ -29,7 +29,7 @@ res = {}
 for name, fn in (("compress", lambda: P.mgard_compress(d, 1e-4)),
                  ("decompress", lambda: P.mgard_decompress(pin, out=out))):
     torch.cuda.synchronize()
-    _lib.prof_enable(True)
+    _lib.prof_enable("serial" if os.environ.get("KB_SERIAL") else True)
     t = time.perf_counter()
     for _ in range(reps):
         fn()
