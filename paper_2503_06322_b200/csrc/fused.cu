@@ -658,8 +658,11 @@ __global__ void __launch_bounds__(256) k_quantize_fine(const double *__restrict_
         int lo, hi;
         slab_range(n0, gridDim.z, blockIdx.z, lo, hi);
         const int64_t plane = (int64_t)n1 * n2, col = (int64_t)j1 * n2 + j2;
-        // 8 planes' coefficients in flight per thread before any is quantized (latency-bound otherwise)
+        // 8 planes' coefficients in flight per thread before any is quantized (latency-bound otherwise);
+        // the histogram is counted in runs of equal keys down the column (smooth data repeats a few
+        // keys, so one shared atomic per run instead of per node)
         constexpr int U = 8;
+        uint32_t run_key = 0, run_n = 0;
         for (int j0 = lo; j0 < hi; j0 += U) {
             double v[U];
             bool use[U];
@@ -671,7 +674,20 @@ __global__ void __launch_bounds__(256) k_quantize_fine(const double *__restrict_
             }
 #pragma unroll
             for (int k = 0; k < U; k++)
-                if (use[k]) quant_node(v[k], q, rbin, (int64_t)(j0 + k) * plane + col, fl, sh_hist, sh_ok);
+                if (use[k]) {
+                    const uint32_t key = quant_key(v[k], q, rbin, (int64_t)(j0 + k) * plane + col, fl);
+                    if (key != run_key && run_n) {
+                        if (sh_ok) atomicAdd(&sh_hist[run_key], run_n);
+                        else atomicAdd(&q.hist[run_key], (unsigned long long)run_n);
+                        run_n = 0;
+                    }
+                    run_key = key;
+                    run_n++;
+                }
+        }
+        if (run_n) {
+            if (sh_ok) atomicAdd(&sh_hist[run_key], run_n);
+            else atomicAdd(&q.hist[run_key], (unsigned long long)run_n);
         }
     }
     if (fl) atomicOr(q.flags, fl);

@@ -52,8 +52,7 @@ __device__ __forceinline__ double qbin(const QuantOut &q) { return q.bin_dev ? *
 // lies within that distance of a half-integer -- then (and for |qa| >= 2^61) the IEEE division
 // decides; |mc / bin| >= 2^62 is the bin overflow.  Outlier iff |r| >= dict/2, key = zigzag(r)
 // (exact: non-outlier |r| < 2^15), histogram.
-__device__ __forceinline__ void quant_node(double mc, const QuantOut &q, double rbin, int64_t f, int &fl,
-                                           uint32_t *sh_hist, bool sh_ok) {
+__device__ __forceinline__ uint32_t quant_key(double mc, const QuantOut &q, double rbin, int64_t f, int &fl) {
     // a non-finite mc makes qa, r and dist NaN / inf, so it always takes the checked path
     const double qa = dmul(mc, rbin);
     double r = rint(qa);
@@ -81,7 +80,13 @@ __device__ __forceinline__ void quant_node(double mc, const QuantOut &q, double 
         key = ((uint32_t)ri << 1) ^ (uint32_t)(ri >> 31);   // zigzag (quantize.py:24-31)
     }
     q.keys[f] = (uint16_t)key;
-    hist_add(sh_hist, q.hist, sh_ok, key);
+    return key;
+}
+
+// quant_key plus the histogram count of the key.
+__device__ __forceinline__ void quant_node(double mc, const QuantOut &q, double rbin, int64_t f, int &fl,
+                                           uint32_t *sh_hist, bool sh_ok) {
+    hist_add(sh_hist, q.hist, sh_ok, quant_key(mc, q, rbin, f, fl));
 }
 
 // Per-thread description of one axis at a fine index j: coarse neighbours (fine indices fa/fb,
