@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kQThreads, TMA ? 4 : 3)
                 PB0 = (double)so[so_rB];
                 PBB = (double)so[so_rB + dcB];
             }
-            (void)P0B;
+            (void)P00, (void)P0B, (void)PB0, (void)PBB;   // MODE 1 interpolates nothing
             if constexpr (MODE != 1) {
                 const double p1a = rowfo ? lerp(P00, PB0, t1) : PB0;
                 const double p1b = rowfo ? lerp(P0B, PBB, t1) : PBB;
