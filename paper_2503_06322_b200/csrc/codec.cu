@@ -903,10 +903,10 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                 const int c_ready = ready(planes_done);
                 if (c_ready > c_done) {
                     CUDA_CHECK(cudaEventRecord(ctx->event(EvDecCorr, g), s));
-                    CUDA_CHECK(cudaStreamWaitEvent(ctx->aux, ctx->event(EvDecCorr, g), 0));
-                    fused_pass1_recompose(p, 0, coef, Z0f, ctx->aux, c_done, c_ready);
-                    fused_pass2(p, 0, Z0f, T0f, ctx->aux, c_done, c_ready);
-                    phase_mark("corr", ctx->aux);
+                    CUDA_CHECK(cudaStreamWaitEvent(ctx->aux_hi, ctx->event(EvDecCorr, g), 0));
+                    fused_pass1_recompose(p, 0, coef, Z0f, ctx->aux_hi, c_done, c_ready);
+                    fused_pass2(p, 0, Z0f, T0f, ctx->aux_hi, c_done, c_ready);
+                    phase_mark("corr", ctx->aux_hi);
                     c_done = c_ready;
                 }
             }
@@ -919,18 +919,18 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                     LAUNCH_CHECK();
                 }
                 CUDA_CHECK(cudaEventRecord(ctx->event(190), s));
-                CUDA_CHECK(cudaStreamWaitEvent(ctx->aux, ctx->event(190), 0));
-                fused_pass1_recompose(p, 0, coef, Z0f, ctx->aux);
-                fused_pass2(p, 0, Z0f, T0f, ctx->aux);
+                CUDA_CHECK(cudaStreamWaitEvent(ctx->aux_hi, ctx->event(190), 0));
+                fused_pass1_recompose(p, 0, coef, Z0f, ctx->aux_hi);
+                fused_pass2(p, 0, Z0f, T0f, ctx->aux_hi);
             }
             phase_mark("dec_end", s);
             // host output: only the plane-axis sweep here; the in-plane sweeps run per output slab
             t0_split = classify(out) != MemKind::Device && thomas_plane_split(p, 0);
-            if (t0_split) thomas_plane_axis(p, 0, T0f, ctx->aux);
-            else thomas_all(p, 0, T0f, ctx->aux);
-            phase_mark("thomas0", ctx->aux);
+            if (t0_split) thomas_plane_axis(p, 0, T0f, ctx->aux_hi);
+            else thomas_all(p, 0, T0f, ctx->aux_hi);
+            phase_mark("thomas0", ctx->aux_hi);
             ev_pre = ctx->event(191);
-            CUDA_CHECK(cudaEventRecord(ev_pre, ctx->aux));
+            CUDA_CHECK(cudaEventRecord(ev_pre, ctx->aux_hi));
             T0_pre = T0f;
         } else if (has_syms) {
             dr = run_decode(ctx, hh, nullptr, coef, bin, dict, s);

@@ -419,7 +419,7 @@ void *hpdr_ctx::hbuf(const std::string &name, size_t bytes) {
 void hpdr_ctx::sync() { CUDA_CHECK(cudaStreamSynchronize(stream)); }
 
 void hpdr_ctx::sync_all() {
-    for (cudaStream_t x : {stream, h2d, d2h, aux}) CUDA_CHECK(cudaStreamSynchronize(x));
+    for (cudaStream_t x : {stream, h2d, d2h, aux, aux_hi}) CUDA_CHECK(cudaStreamSynchronize(x));
     for (cudaStream_t x : side) CUDA_CHECK(cudaStreamSynchronize(x));
 }
 
@@ -633,8 +633,11 @@ int hpdr_ctx_create(int device, hpdr_ctx **out) {
         CUDA_CHECK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi_pri));
         CUDA_CHECK(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
         CUDA_CHECK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
-        static const bool aux_high = getenv("HPDR_AUX_HIGH") != nullptr;
-        CUDA_CHECK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, aux_high ? hi_pri : lo_pri));
+        // aux: the finest quantization of a relative-mode compress (off the level chain), low;
+        // aux_hi: the finest correction of a decompress, the longest chain before the output, high
+        // (1024^3: the first output slab 0.5 ms earlier than at low priority)
+        CUDA_CHECK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, lo_pri));
+        CUDA_CHECK(cudaStreamCreateWithPriority(&c->aux_hi, cudaStreamNonBlocking, hi_pri));
         for (auto &x : c->side) CUDA_CHECK(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, hi_pri));
         *out = c;
         return HPDR_OK;
@@ -667,6 +670,7 @@ void hpdr_ctx_destroy(hpdr_ctx *c) {
     cudaStreamDestroy(c->h2d);
     cudaStreamDestroy(c->d2h);
     cudaStreamDestroy(c->aux);
+    cudaStreamDestroy(c->aux_hi);
     for (auto x : c->side) cudaStreamDestroy(x);
     delete c;
 }

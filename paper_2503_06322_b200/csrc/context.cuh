@@ -95,7 +95,8 @@ struct hpdr_ctx {
     cudaStream_t stream = nullptr;    // compute
     cudaStream_t h2d = nullptr;       // copy engine 0
     cudaStream_t d2h = nullptr;       // copy engine 1
-    cudaStream_t aux = nullptr;       // side compute (work independent of the level chain)
+    cudaStream_t aux = nullptr;       // side compute off the critical path (low priority)
+    cudaStream_t aux_hi = nullptr;    // side compute on the critical path (the finest correction of a decompress)
     cudaStream_t side[4] = {};        // more side streams (independent per-level corrections)
     uint64_t alloc_events = 0;
     hpdr_range_hook range_hook = nullptr;   // job-wide range exchange (hpdr_ctx_set_range_hook)

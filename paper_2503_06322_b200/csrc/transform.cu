@@ -1401,16 +1401,16 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
         double *T = (double *)ctx->dbuf("t0f", st.csh.size() * 8);
         T0f = T;
         CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
-        CUDA_CHECK(cudaStreamWaitEvent(ctx->aux, ctx->event(0), 0));
-        fused_pass1_recompose(p, 0, coef, Z0f, ctx->aux);
-        fused_pass2(p, 0, Z0f, T, ctx->aux);
+        CUDA_CHECK(cudaStreamWaitEvent(ctx->aux_hi, ctx->event(0), 0));
+        fused_pass1_recompose(p, 0, coef, Z0f, ctx->aux_hi);
+        fused_pass2(p, 0, Z0f, T, ctx->aux_hi);
         if (direct && host_out && thomas_plane_split(p, 0)) {   // in-plane sweeps follow the output slabs
-            thomas_plane_axis(p, 0, T, ctx->aux);
+            thomas_plane_axis(p, 0, T, ctx->aux_hi);
             t0_plane_axis_only = true;
         } else {
-            thomas_all(p, 0, T, ctx->aux);
+            thomas_all(p, 0, T, ctx->aux_hi);
         }
-        CUDA_CHECK(cudaEventRecord(ev_side, ctx->aux));
+        CUDA_CHECK(cudaEventRecord(ev_side, ctx->aux_hi));
     }
     // The coarser levels' corrections are independent of each other too: compute them up front,
     // round-robin on the side streams (they are small, latency-bound launches), so the level chain
