@@ -786,10 +786,13 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
         cudaEvent_t ev_pre = nullptr;
         bool t0_split = false;
         static const bool no_stream_dec = getenv("HPDR_NO_STREAM_DECODE") != nullptr;
+        static const uint64_t min_stream_bits = getenv("HPDR_STREAM_DECODE_MIN_BITS")
+                                                    ? strtoull(getenv("HPDR_STREAM_DECODE_MIN_BITS"), nullptr, 10)
+                                                    : (4ull << 20);   // C1 129^3 (4 MB blob): 0.85 -> 0.75 ms
         bool streamed = !no_stream_dec && !dev_blob && has_syms && !hh.single && coef && pp && n_sym == N &&
                         levels_of(dims) == (int)levels && (dtype == 0 || dtype == 1) && pp->host.L > 2 &&
                         use_fused(*pp) && classify(blob_in) != MemKind::Device && hh.n_units >= 64 &&
-                        hh.total_bits >= (uint64_t)(32u << 20) && n_out <= N / 64;
+                        hh.total_bits >= (uint64_t)min_stream_bits && n_out <= N / 64;
         std::vector<uint64_t> uoffs;
         const uint64_t *oidx_h = (const uint64_t *)(blob + oidx_off);   // unaligned-safe reads below
         if (streamed) {
