@@ -86,3 +86,21 @@ def test_bytes_result_size_hint_paths(oracle):
             assert type(b) is bytes and b == want
     finally:
         _lib.BytesSink.MIN_HINT = old
+
+
+def test_bytes_result_allocation_failure_raises():
+    """A failed result allocation (the allocator callback returns NULL) raises AllocationError and
+    leaves the context usable (hpdr_mgard_compress_alloc, include/hpdr_b200.h)."""
+    from paper_2503_06322_b200 import _lib
+    from paper_2503_06322_b200.errors import AllocationError
+
+    a = S.smooth_noise((40, 50, 60), seed=9)
+    ref = P.mgard_compress(a, 1e-3)
+    orig = _lib.BytesSink._alloc
+    _lib.BytesSink._alloc = lambda self, _user, n: None
+    try:
+        with pytest.raises(AllocationError):
+            P.mgard_compress(a, 1e-3)
+    finally:
+        _lib.BytesSink._alloc = orig
+    assert P.mgard_compress(a, 1e-3) == ref
