@@ -782,8 +782,8 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
         // Streamed decompress (host blob): the payload arrives in unit groups, each decoded as its
         // bytes land, and the finest transition's correction -- which depends only on the finest
         // coefficients (transform.py:342-345) -- follows slab by slab on the side stream.
-        const double *T0_pre = nullptr;
-        cudaEvent_t ev_pre = nullptr;
+        const double *T0_pre = nullptr, *T1_pre = nullptr;
+        cudaEvent_t ev_pre = nullptr, ev1_pre = nullptr;
         bool t0_split = false;
         static const bool no_stream_dec = getenv("HPDR_NO_STREAM_DECODE") != nullptr;
         static const uint64_t min_stream_bits = getenv("HPDR_STREAM_DECODE_MIN_BITS")
@@ -854,6 +854,27 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
             };
             double *Z0f = (double *)ctx->dbuf("z0f", z0_elems(p, 0) * 8);
             double *T0f = (double *)ctx->dbuf("t0f", st0.csh.size() * 8);
+            // Transition 1's correction streams too: its coefficients arrive with the finest ones,
+            // so its pass 1 / pass 2 follow the decode like the finest's and only its Thomas solve
+            // is left after the last group (the coarse chain of the recompose waits on it).
+            static const bool no_l1 = getenv("HPDR_NO_STREAM_L1") != nullptr;
+            const bool lvl1 = !no_l1 && p.host.L > 2 && tiny_start(p, 1) != 1;
+            double *Z1f = lvl1 ? (double *)ctx->dbuf("z1f", z0_elems(p, 1) * 8) : nullptr;
+            double *T1f = lvl1 ? (double *)ctx->dbuf("t1f", p.steps[1].csh.size() * 8) : nullptr;
+            const AxisTables &ax01 = p.host.steps[1].ax[1];
+            const std::vector<int32_t> &map01 = p.host.map[1][1];   // level-1 plane -> finest plane
+            const int n01 = (int)p.steps[1].fsh.n[1];
+            const int m1 = lvl1 ? fused_out_planes(p, 1) : 0;
+            auto ready1 = [&](int finest_planes) -> int {   // transition-1 outputs whose stencil has landed
+                if (finest_planes >= n0) return m1;
+                int arrived = 0;
+                while (arrived < n01 && map01[arrived] < finest_planes) arrived++;
+                if (!ax01.active) return arrived;
+                int c = 0;
+                while (c < m1 && ax01.r0[c] + 2 < arrived) c++;
+                return c;
+            };
+            int c1_done = 0;
             auto oidx_at = [&](uint64_t k) {
                 uint64_t i;
                 memcpy(&i, oidx_h + k, 8);
@@ -912,6 +933,16 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                     phase_mark("corr", ctx->aux_hi);
                     c_done = c_ready;
                 }
+                if (lvl1) {
+                    const int c1_ready = ready1(planes_done);
+                    if (c1_ready > c1_done) {
+                        CUDA_CHECK(cudaEventRecord(ctx->event(EvDecCorr, g), s));
+                        CUDA_CHECK(cudaStreamWaitEvent(ctx->side[0], ctx->event(EvDecCorr, g), 0));
+                        fused_pass1_recompose(p, 1, coef, Z1f, ctx->side[0], c1_done, c1_ready);
+                        fused_pass2(p, 1, Z1f, T1f, ctx->side[0], c1_done, c1_ready);
+                        c1_done = c1_ready;
+                    }
+                }
             }
             decode_end(ctx, S, dr, s, true);
             if (dr.bad_bit >= 0)
@@ -925,6 +956,12 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                 CUDA_CHECK(cudaStreamWaitEvent(ctx->aux_hi, ctx->event(190), 0));
                 fused_pass1_recompose(p, 0, coef, Z0f, ctx->aux_hi);
                 fused_pass2(p, 0, Z0f, T0f, ctx->aux_hi);
+                if (lvl1) {
+                    CUDA_CHECK(cudaStreamWaitEvent(ctx->side[0], ctx->event(190), 0));
+                    fused_pass1_recompose(p, 1, coef, Z1f, ctx->side[0]);
+                    fused_pass2(p, 1, Z1f, T1f, ctx->side[0]);
+                    c1_done = m1;
+                }
             }
             phase_mark("dec_end", s);
             // host output: only the plane-axis sweep here; the in-plane sweeps run per output slab
@@ -935,6 +972,18 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
             ev_pre = ctx->event(191);
             CUDA_CHECK(cudaEventRecord(ev_pre, ctx->aux_hi));
             T0_pre = T0f;
+            if (lvl1) {
+                if (c1_done < m1) {   // outputs whose stencil reached the end of the field
+                    CUDA_CHECK(cudaEventRecord(ctx->event(192), s));
+                    CUDA_CHECK(cudaStreamWaitEvent(ctx->side[0], ctx->event(192), 0));
+                    fused_pass1_recompose(p, 1, coef, Z1f, ctx->side[0], c1_done, m1);
+                    fused_pass2(p, 1, Z1f, T1f, ctx->side[0], c1_done, m1);
+                }
+                thomas_all(p, 1, T1f, ctx->side[0]);
+                ev1_pre = ctx->event(193);
+                CUDA_CHECK(cudaEventRecord(ev1_pre, ctx->side[0]));
+                T1_pre = T1f;
+            }
         } else if (has_syms) {
             dr = run_decode(ctx, hh, nullptr, coef, bin, dict, s);
         }
@@ -962,10 +1011,10 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
         const size_t ob = (size_t)N * itemsize(dtype);
         if (out_bytes < ob) fail(HPDR_ERR_BUFFER, "output buffer too small: need " + std::to_string(ob));
         if (classify(out) == MemKind::Device) {
-            recompose_into(ctx, p, coef, out, dtype, s, nullptr, T0_pre, ev_pre);
+            recompose_into(ctx, p, coef, out, dtype, s, nullptr, T0_pre, ev_pre, false, T1_pre, ev1_pre);
         } else {
             void *stage = ctx->dbuf("out_stage", ob);
-            recompose_into(ctx, p, coef, stage, dtype, s, out, T0_pre, ev_pre, t0_split);
+            recompose_into(ctx, p, coef, stage, dtype, s, out, T0_pre, ev_pre, t0_split, T1_pre, ev1_pre);
         }
         if (sync) CUDA_CHECK(cudaStreamSynchronize(s));
     }

@@ -1359,7 +1359,8 @@ void thomas_in_planes(const DevPlan &p, int st_i, double *T, int c_lo, int c_hi,
 }
 
 void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s,
-                    void *host_out, const double *T0_pre, cudaEvent_t ev_pre, bool t0_plane_axis_only) {
+                    void *host_out, const double *T0_pre, cudaEvent_t ev_pre, bool t0_plane_axis_only,
+                    const double *T1_pre, cudaEvent_t ev1_pre) {
     const int L = p.host.L;
     if (L == 1 || !use_fused(p)) {
         const double *rec = recompose_device(ctx, p, coef, s);
@@ -1429,6 +1430,7 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
         CUDA_CHECK(cudaEventRecord(ctx->event(199), s));   // coef ready
         int k = 0;
         for (int st_i = top - 1; st_i >= 1; st_i--, k++) {
+            if (st_i == 1 && T1_pre) continue;   // computed by the caller (streamed decode)
             cudaStream_t x = ctx->side[k % 4];
             if (k < 4) CUDA_CHECK(cudaStreamWaitEvent(x, ctx->event(199), 0));
             double *Zl = zarena, *T = tarena;
@@ -1450,6 +1452,9 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
         if (st_i == 0 && side) {
             T = T0f;
             CUDA_CHECK(cudaStreamWaitEvent(s, ev_side, 0));
+        } else if (st_i == 1 && T1_pre) {
+            T = T1_pre;
+            CUDA_CHECK(cudaStreamWaitEvent(s, ev1_pre, 0));
         } else if (Tl[st_i]) {
             T = Tl[st_i];
             CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(EvLevel, ev_l[st_i]), 0));

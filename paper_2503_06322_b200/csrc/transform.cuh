@@ -53,9 +53,10 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
 // T0_pre / ev_pre: the finest transition's correction computed by the caller (streamed decode);
 // t0_plane_axis_only: it holds only the plane-axis (dim-0) solve, the in-plane axes are left to the
 // slab loop (thomas_plane_split).
+// T1_pre / ev1_pre: the same for transition 1 (complete solve).
 void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s,
                     void *host_out = nullptr, const double *T0_pre = nullptr, cudaEvent_t ev_pre = nullptr,
-                    bool t0_plane_axis_only = false);
+                    bool t0_plane_axis_only = false, const double *T1_pre = nullptr, cudaEvent_t ev1_pre = nullptr);
 // Whether transition st_i's Thomas solves can be split into the plane-axis sweep (over the whole
 // grid) and the in-plane sweeps per range of coarse planes (rank <= 3, plane axis active, not a
 // one-block grid): the finest level's output slabs then only wait for their own planes.
