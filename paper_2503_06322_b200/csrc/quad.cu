@@ -472,14 +472,16 @@ bool axis_regular(const AxisTables &t) {
 // thread forms those itself from the two coarse planes around the fine plane (cv - corr, cached per
 // corner for the next fine plane) -- no shared footprint and no barrier -- and the coefficients of
 // the next plane are loaded one plane ahead.  Same values and operation order as k_level_final.
+// block shape: 64 x 2 quads (128 x 4 nodes): a row of the tile is 1 KB of contiguous coefficients
+constexpr int kFQX = 64, kFQY = 2;
 template <typename TOut>
 __global__ void __launch_bounds__(kQThreads) k_final_quad(const double *__restrict__ cv, const double *__restrict__ corr,
                                                          int n0, int n1, int n2, DevAxis ax0, DevAxis ax1, DevAxis ax2,
                                                          LevelMap lm, const double *__restrict__ coef,
                                                          TOut *__restrict__ D, int j_base, int j_count) {
     const int tid = threadIdx.x;
-    const int qx = tid & (kQX - 1), qy = tid / kQX;
-    const int c0 = blockIdx.x * kTileX + 2 * qx, r0 = blockIdx.y * kTileY + 2 * qy;
+    const int qx = tid & (kFQX - 1), qy = tid / kFQX;
+    const int c0 = blockIdx.x * (2 * kFQX) + 2 * qx, r0 = blockIdx.y * (2 * kFQY) + 2 * qy;
     if (r0 >= n1 || c0 >= n2) return;   // no barriers below
     int lo, hi;
     slab_range(j_count, gridDim.z, blockIdx.z, lo, hi);
@@ -591,7 +593,7 @@ void launch_final_quad(const double *cv, const double *corr, int n0, int n1, int
                        const DevAxis &a1, const DevAxis &a2, const LevelMap &lm, const double *coef, TOut *D, int j_base,
                        int j_count, cudaStream_t s) {
     if (j_count <= 0) return;
-    const unsigned gx = (n2 + kTileX - 1) / kTileX, gy = (n1 + kTileY - 1) / kTileY;
+    const unsigned gx = (n2 + 2 * kFQX - 1) / (2 * kFQX), gy = (n1 + 2 * kFQY - 1) / (2 * kFQY);
     const int64_t want = 148LL * 12 * 4;   // >= 4 waves of 12 resident blocks per SM
     const int slabs = (int)std::max<int64_t>(1, std::min<int64_t>(j_count, (want + (int64_t)gx * gy - 1) / ((int64_t)gx * gy)));
     k_final_quad<TOut><<<dim3(gx, gy, (unsigned)slabs), kQThreads, 0, s>>>(cv, corr, n0, n1, n2, a0, a1, a2, lm, coef, D,
