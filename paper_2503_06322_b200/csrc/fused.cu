@@ -886,6 +886,161 @@ __global__ void __launch_bounds__(kP2Threads) k_level_pass2(const double *__rest
     cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------------- pass 2, 2 columns
+// k_level_pass2<true, true> with two adjacent fine columns per thread (512 per block): the axis-1
+// march control (record reads, emission test, ring wait) and the two barriers of each emitted row
+// are paid once per two columns.  Same operation order.
+constexpr int kP2Out2 = (2 * kP2Threads - 4) / 2;   // coarse outputs along axis 2 per block
+constexpr int kP2Ring2 = 6;                         // rows in flight (shared memory < 48 KB)
+constexpr int kP2MaxRows2 = 136;                    // fine rows per slab (<= 66 coarse outputs + stencil)
+
+struct March2 {
+    double m1[2], m2[2];
+    double ya[2], yb[2], yc[2];
+};
+
+__global__ void __launch_bounds__(kP2Threads) k_level_pass2_x2(const double *__restrict__ Z0, int m0, int n1, int n2,
+                                                               DevAxis ax1, DevAxis ax2, double *__restrict__ B,
+                                                               int slabs1, int p_base) {
+    constexpr int W = 2 * kP2Threads;
+    __shared__ double sw[W];
+    __shared__ double sy[W];
+    __shared__ __align__(16) double ring[kP2Ring2][W];
+    __shared__ __align__(16) PlaneInfo ptab[kP2MaxRows2];
+    const int t = threadIdx.x;
+    const int p = p_base + blockIdx.y;
+    const int nc1 = ax1.nc, nc2 = ax2.nc;
+    const int c2_lo = blockIdx.x * kP2Out2;
+    const int c2_cnt = min(kP2Out2, nc2 - c2_lo);
+    const int base = __ldg(ax2.r0 + c2_lo) - 2;
+    const int jA = base + 2 * t, jB = jA + 1;   // this thread's fine columns
+    const bool inA = jA >= 0 && jA < n2, inB = jB >= 0 && jB < n2;
+    int c_lo, c_hi;
+    slab_range(nc1, slabs1, blockIdx.z, c_lo, c_hi);
+    if (c_lo >= c_hi) return;   // uniform across the block
+    const double *zp = Z0 + (int64_t)p * n1 * n2;
+    double *bp = B + (int64_t)p * nc1 * nc2;
+    // axis-2 stencil constants: mass bands at the two columns, restriction of output t
+    double md2[2] = {0, 0}, ml2[2] = {0, 0}, mu2[2] = {0, 0};
+    if (inA) { md2[0] = __ldg(ax2.md + jA); ml2[0] = __ldg(ax2.ml + jA); mu2[0] = __ldg(ax2.mu + jA); }
+    if (inB) { md2[1] = __ldg(ax2.md + jB); ml2[1] = __ldg(ax2.ml + jB); mu2[1] = __ldg(ax2.mu + jB); }
+    double wr2 = 0, wl2 = 0;
+    int r02 = 0, rr2 = -1, rl2 = -1;
+    if (t < c2_cnt) {
+        const int c2 = c2_lo + t;
+        r02 = __ldg(ax2.r0 + c2) - base;
+        rr2 = __ldg(ax2.rr + c2);
+        rl2 = __ldg(ax2.rl + c2);
+        wr2 = __ldg(ax2.wr + c2);
+        wl2 = __ldg(ax2.wl + c2);
+    }
+    auto out_row = [&](int c1, double w0, double w1) {
+        sw[2 * t] = w0;
+        sw[2 * t + 1] = w1;
+        __syncthreads();
+        double y0 = 0.0, y1 = 0.0;
+        const int l0 = 2 * t, l1 = 2 * t + 1;
+        if (inA) {
+            y0 = dmul(md2[0], sw[l0]);
+            if (jA >= 1 && l0 >= 1) y0 = dadd(y0, dmul(ml2[0], sw[l0 - 1]));
+            if (jA + 1 < n2) y0 = dadd(y0, dmul(mu2[0], sw[l0 + 1]));
+        }
+        if (inB) {
+            y1 = dmul(md2[1], sw[l1]);
+            if (jB >= 1) y1 = dadd(y1, dmul(ml2[1], sw[l1 - 1]));
+            if (jB + 1 < n2 && l1 + 1 < W) y1 = dadd(y1, dmul(mu2[1], sw[l1 + 1]));
+        }
+        sy[l0] = y0;
+        sy[l1] = y1;
+        __syncthreads();
+        if (t < c2_cnt) {
+            double z = sy[r02];
+            if (rr2 >= 0) z = dadd(z, dmul(wr2, sy[rr2 - base]));
+            if (rl2 >= 0) z = dadd(z, dmul(wl2, sy[rl2 - base]));
+            bp[(int64_t)c1 * nc2 + c2_lo + t] = z;
+        }
+    };
+    const int j_start = max(0, __ldg(ax1.r0 + c_lo) - 2);
+    const int j_end = min(n1 - 1, __ldg(ax1.r0 + c_hi - 1) + 2);
+    {   // the slab's axis-1 records (the launcher bounds the rows per slab)
+        const int nrec = j_end - j_start + 1;
+        const int4 *src = reinterpret_cast<const int4 *>(ax1.pi + j_start);
+        int4 *dst = reinterpret_cast<int4 *>(ptab);
+        for (int i = t; i < nrec * 5; i += kP2Threads) dst[i] = __ldg(src + i);
+        __syncthreads();
+    }
+    const PlaneInfo *P1 = ptab - j_start;   // record k at P1 + k
+    const bool vec = ((((int64_t)n2 | base) & 1) == 0);   // 16-byte aligned column pairs
+    auto issue = [&](int r) {
+        if (r <= j_end) {
+            const double *g = zp + (int64_t)r * n2 + jA;
+            double *d = &ring[r % kP2Ring2][2 * t];
+            if (vec && inA && inB) cp_async<16>(d, g);
+            else {
+                if (inA) cp_async<8>(d, g);
+                if (inB) cp_async<8>(d + 1, g + 1);
+            }
+        }
+        cp_async_commit();
+    };
+    for (int k = 0; k < kP2Ring2 - 1; k++) issue(j_start + k);
+    March2 M;
+#pragma unroll
+    for (int k = 0; k < 2; k++) M.m1[k] = M.m2[k] = M.ya[k] = M.yb[k] = M.yc[k] = 0.0;
+    // y(kk) for both columns and its emission (march_emit_y of fused.cu, two columns)
+    auto emit_y = [&](int kk, const double *xk, const double *xkm1, const double *xkp1, bool has_up) {
+        const PlaneInfo *pr = P1 + kk;
+        double v[2];
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            v[k] = dmul(pr->md, xk[k]);
+            if (kk >= 1) v[k] = dadd(v[k], dmul(pr->ml, xkm1[k]));
+            if (has_up) v[k] = dadd(v[k], dmul(pr->mu, xkp1[k]));
+        }
+        const int4 e = *reinterpret_cast<const int4 *>(&pr->fo);   // fo, emit, e_rr, e_rl
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            M.ya[k] = M.yb[k];
+            M.yb[k] = M.yc[k];
+            M.yc[k] = v[k];
+        }
+        if (e.y >= c_lo && e.y < c_hi) {
+            const double wr = pr->ewr, wl = pr->ewl;
+            double z[2];
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                if (e.z) {
+                    z[k] = dadd(M.yb[k], dmul(wr, M.yc[k]));
+                    if (e.w) z[k] = dadd(z[k], dmul(wl, M.ya[k]));
+                } else {
+                    z[k] = M.yc[k];
+                    if (e.w) z[k] = dadd(z[k], dmul(wl, M.yb[k]));
+                }
+            }
+            out_row(e.y, z[0], z[1]);
+        }
+    };
+    for (int j = j_start; j <= j_end; j++) {
+        cp_async_wait<kP2Ring2 - 2>();   // row j has landed (own copies)
+        double x[2];
+        x[0] = inA ? ring[j % kP2Ring2][2 * t] : 0.0;
+        x[1] = inB ? ring[j % kP2Ring2][2 * t + 1] : 0.0;
+        issue(j + kP2Ring2 - 1);          // into the slot of row j - 1
+        // march_push: y(j - 1) once x(j) is known, y(j) at the last row
+        if (j >= (j_start == 0 ? 1 : j_start + 2)) emit_y(j - 1, M.m1, M.m2, x, true);
+        if (j == n1 - 1 && (j > j_start || j == 0)) {
+            const double zero[2] = {0.0, 0.0};
+            emit_y(j, x, M.m1, zero, false);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            M.m2[k] = M.m1[k];
+            M.m1[k] = x[k];
+        }
+    }
+    cp_async_wait<0>();
+}
+
 // ---------------------------------------------------------------------------------- final
 // Recompose output of one transition: D(j) = P(cv)(j) + mc(j) (transform.py:346-347), P the
 // nested lerps over the corrected coarse values cv (nc0, nc1, nc2), mc from the coefficients.
@@ -1047,6 +1202,15 @@ void launch_pass2(int act, const double *Z0, int m0, int n1, int n2, const DevAx
     const int64_t cols = (int64_t)m0 * gx * kP2Threads;
     // enough slabs that a slab's rows fit the shared record table (<= 130 coarse rows each)
     const int slabs = std::max(slabs_for(cols, nc1), A1 ? (nc1 + 129) / 130 : 1);
+    static const bool one_col = getenv("HPDR_P2_ONE_COL") != nullptr;
+    if (A1 && A2 && !one_col) {   // two columns per thread
+        const unsigned gx2 = (unsigned)((nc2 + kP2Out2 - 1) / kP2Out2);
+        const int slabs2 = std::max(slabs_for((int64_t)m0 * gx2 * kP2Threads, nc1), (nc1 + 65) / 66);
+        k_level_pass2_x2<<<dim3(gx2, (unsigned)p_count, (unsigned)slabs2), kP2Threads, 0, s>>>(Z0, m0, n1, n2, a1, a2, B,
+                                                                                             slabs2, p_base);
+        LAUNCH_CHECK();
+        return;
+    }
     dim3 grid(gx, (unsigned)p_count, (unsigned)slabs);
     if (A1 && A2) k_level_pass2<true, true><<<grid, kP2Threads, 0, s>>>(Z0, m0, n1, n2, a1, a2, B, slabs, p_base);
     else if (A1) k_level_pass2<true, false><<<grid, kP2Threads, 0, s>>>(Z0, m0, n1, n2, a1, a2, B, slabs, p_base);

@@ -221,7 +221,7 @@ print("variant ok")
                                  {"HPDR_NO_TINY": "1"}, {"HPDR_NO_TINY": "1", "HPDR_NO_GRAPH": "1"},
                                  {"HPDR_NO_PLANE_SPLIT": "1"}, {"HPDR_NO_QUAD_FINAL": "1"}, {"HPDR_NO_QUAD_P1R": "1"},
                                  {"HPDR_NO_STREAM_L1": "1", "HPDR_STREAM_DECODE_MIN_BITS": "0"},
-                                 {"HPDR_STREAM_DECODE_MIN_BITS": "0"}, {"HPDR_QF_COLUMNS": "1"},
+                                 {"HPDR_STREAM_DECODE_MIN_BITS": "0"}, {"HPDR_QF_COLUMNS": "1"}, {"HPDR_P2_ONE_COL": "1"},
                                  {"HPDR_THOMAS_TILE": "1"}, {}])
 def test_execution_variants_bit_identical(env):
     """Every execution variant gives the reference's blobs: the per-axis (generic) path, the non-streamed
