@@ -793,6 +793,32 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                         levels_of(dims) == (int)levels && (dtype == 0 || dtype == 1) && pp->host.L > 2 &&
                         use_fused(*pp) && classify(blob_in) != MemKind::Device && hh.n_units >= 64 &&
                         hh.total_bits >= (uint64_t)min_stream_bits && n_out <= N / 64;
+        static const int G = [] {
+            const char *e = getenv("HPDR_DEC_GROUPS");
+            return e ? std::max(1, std::min(32, atoi(e))) : 16;   // 6 / 10 / 16 at 1024^3: 104.8 / 104.3 / 103.9 ms
+        }();
+        // Pinned blob: the first payload group goes out before the host-side checks below (~1 ms at
+        // 1024^3), into the buffer decode_begin will hand out (same name and size); it stops short
+        // of the zero-padded tail decode_begin clears on the compute stream.
+        size_t early = 0;
+        if (streamed && classify(hh.packed) == MemKind::Pinned) {
+            const uint64_t units0 = (hh.n_sym + kBlockSymbols - 1) / kBlockSymbols;
+            const uint64_t ub0 = units0 / G;
+            const size_t pbytes = (size_t)((hh.total_bits + 7) / 8);
+            if (ub0 > 0 && ub0 < units0 && ub0 < hh.n_units) {
+                uint64_t off;
+                memcpy(&off, hh.offsets + 8 * ub0, 8);   // (byte pointer into the blob)
+                const size_t want = std::min<size_t>(pbytes, ((size_t)(off / 8) + 64) & ~size_t(3));
+                if (off <= hh.total_bits && want <= (pbytes & ~size_t(3))) {
+                    const size_t pwords = ((pbytes / 4 + 12) & ~size_t(3));
+                    void *dw = ctx->dbuf("dec_words", pwords * 4);
+                    CUDA_CHECK(cudaEventRecord(ctx->event(194), s));
+                    CUDA_CHECK(cudaStreamWaitEvent(ctx->h2d, ctx->event(194), 0));
+                    CUDA_CHECK(cudaMemcpyAsync(dw, hh.packed, want, cudaMemcpyHostToDevice, ctx->h2d));
+                    early = want;
+                }
+            }
+        }
         std::vector<uint64_t> uoffs;
         const uint64_t *oidx_h = (const uint64_t *)(blob + oidx_off);   // unaligned-safe reads below
         if (streamed) {
@@ -810,6 +836,10 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                 if (i >= N || (k && i <= prev)) streamed = false;
                 prev = i;
             }
+        }
+        if (early && !streamed) {   // the one-shot path rewrites the payload buffer on the compute stream
+            CUDA_CHECK(cudaEventRecord(ctx->event(195), ctx->h2d));
+            CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(195), 0));
         }
         if (streamed) {
             DevPlan &p = *pp;
@@ -830,16 +860,9 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
             uint64_t *di = (uint64_t *)ctx->dbuf("dq_oidx", n_out * 8);
             int64_t *db = (int64_t *)ctx->dbuf("dq_obins", n_out * 8);
             int *fl = (int *)ctx->dbuf("dq_flags", 16);
-            if (n_out) {
-                if (classify(blob) == MemKind::Host && n_out * 8 >= (1u << 20)) {
-                    stage_h2d(ctx, di, blob + oidx_off, n_out * 8, s);
-                    stage_h2d(ctx, db, blob + obins_off, n_out * 8, s);
-                } else {
-                    CUDA_CHECK(cudaMemcpyAsync(di, blob + oidx_off, n_out * 8, cudaMemcpyDefault, s));
-                    CUDA_CHECK(cudaMemcpyAsync(db, blob + obins_off, n_out * 8, cudaMemcpyDefault, s));
-                }
-            }
+            // (the outlier lists follow the payload group by group on the copy stream, below)
             zero_async(fl, 16, s);
+            phase_mark("dec_begin", s);
             const int64_t units = S.units;
             const int64_t plane = st0.fsh.n[2] * st0.fsh.n[3];
             const int n0 = (int)st0.fsh.n[1];
@@ -889,15 +912,13 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                 }
                 return lo;
             };
-            static const int G = [] {
-                const char *e = getenv("HPDR_DEC_GROUPS");
-                return e ? std::max(1, std::min(32, atoi(e))) : 16;   // 6 / 10 / 16 at 1024^3: 104.8 / 104.3 / 103.9 ms
-            }();
             CUDA_CHECK(cudaEventRecord(ctx->event(0), s));
             CUDA_CHECK(cudaStreamWaitEvent(ctx->h2d, ctx->event(0), 0));   // tables / buffers ready
             const bool pageable_blob = classify(hh.packed) == MemKind::Host;
-            size_t copied = 0;
+            size_t copied = early;
             int c_done = 0;
+            const bool fwd0 = thomas_fwd_stream(p, 0);
+            int f0 = 0;   // coarse planes of T0f whose forward elimination is done
             for (int g = 0; g < G; g++) {
                 const int64_t ua = units * g / G, ub = units * (g + 1) / G;
                 if (ub <= ua) continue;
@@ -911,13 +932,24 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                                                    cudaMemcpyHostToDevice, ctx->h2d));
                     copied = want;
                 }
+                const uint64_t o_lo = lower((uint64_t)ua * kBlockSymbols);
+                const uint64_t o_hi = ub == units ? n_out : lower((uint64_t)ub * kBlockSymbols);
+                if (o_hi > o_lo) {   // this group's outliers (ascending indices: one contiguous range)
+                    const size_t ob = 8 * (o_hi - o_lo);
+                    const uint8_t *si = blob + oidx_off + 8 * o_lo, *sb = blob + obins_off + 8 * o_lo;
+                    if (pageable_blob && ob >= (1u << 20)) {
+                        stage_h2d(ctx, di + o_lo, si, ob, ctx->h2d);
+                        stage_h2d(ctx, db + o_lo, sb, ob, ctx->h2d);
+                    } else {
+                        CUDA_CHECK(cudaMemcpyAsync(di + o_lo, si, ob, cudaMemcpyDefault, ctx->h2d));
+                        CUDA_CHECK(cudaMemcpyAsync(db + o_lo, sb, ob, cudaMemcpyDefault, ctx->h2d));
+                    }
+                }
                 CUDA_CHECK(cudaEventRecord(ctx->event(EvDecIn, g), ctx->h2d));
                 phase_mark("h2d", ctx->h2d);
                 CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(EvDecIn, g), 0));
                 decode_units(S, ua, ub, true, s);
                 phase_mark("dec", s);
-                const uint64_t o_lo = lower((uint64_t)ua * kBlockSymbols);
-                const uint64_t o_hi = ub == units ? n_out : lower((uint64_t)ub * kBlockSymbols);
                 if (o_hi > o_lo) {
                     k_outliers<<<grid_for(o_hi - o_lo, 256, 148 * 8), 256, 0, s>>>(coef, (int64_t)N, di + o_lo, db + o_lo,
                                                                                  o_hi - o_lo, bin, fl);
@@ -930,6 +962,10 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                     CUDA_CHECK(cudaStreamWaitEvent(ctx->aux_hi, ctx->event(EvDecCorr, g), 0));
                     fused_pass1_recompose(p, 0, coef, Z0f, ctx->aux_hi, c_done, c_ready);
                     fused_pass2(p, 0, Z0f, T0f, ctx->aux_hi, c_done, c_ready);
+                    if (fwd0) {   // the plane-axis solve follows its right-hand side
+                        thomas_plane_fwd(p, 0, T0f, c_done, c_ready, ctx->aux_hi);
+                        f0 = c_ready;
+                    }
                     phase_mark("corr", ctx->aux_hi);
                     c_done = c_ready;
                 }
@@ -956,6 +992,7 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                 CUDA_CHECK(cudaStreamWaitEvent(ctx->aux_hi, ctx->event(190), 0));
                 fused_pass1_recompose(p, 0, coef, Z0f, ctx->aux_hi);
                 fused_pass2(p, 0, Z0f, T0f, ctx->aux_hi);
+                f0 = 0;
                 if (lvl1) {
                     CUDA_CHECK(cudaStreamWaitEvent(ctx->side[0], ctx->event(190), 0));
                     fused_pass1_recompose(p, 1, coef, Z1f, ctx->side[0]);
@@ -966,7 +1003,8 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
             phase_mark("dec_end", s);
             // host output: only the plane-axis sweep here; the in-plane sweeps run per output slab
             t0_split = classify(out) != MemKind::Device && thomas_plane_split(p, 0);
-            if (t0_split) thomas_plane_axis(p, 0, T0f, ctx->aux_hi);
+            if (fwd0) thomas_finish_fwd(p, 0, T0f, f0, !t0_split, ctx->aux_hi);
+            else if (t0_split) thomas_plane_axis(p, 0, T0f, ctx->aux_hi);
             else thomas_all(p, 0, T0f, ctx->aux_hi);
             phase_mark("thomas0", ctx->aux_hi);
             ev_pre = ctx->event(191);

@@ -389,47 +389,58 @@ __global__ void __launch_bounds__(kThomasWarps * 32) k_thomas_contig(double *__r
 // Register-blocked sweeps: one thread per line, U values of the line loaded ahead of the
 // recurrence (double-buffered), so the sequential dependency never waits on DRAM.  Works for
 // strided (inner > 1, coalesced across threads) and contiguous (inner == 1) lines alike.
-template <int U, bool EPI>
+template <int U, bool EPI, int PH = 0>
 __global__ void __launch_bounds__(128) k_thomas_reg(double *__restrict__ arr, int64_t outer, int32_t n, int64_t inner,
                                                     const double *__restrict__ tw, const double *__restrict__ tb,
                                                     const double *__restrict__ tu, const double *__restrict__ tr,
-                                                    Epi epi) {
+                                                    Epi epi, int32_t f_lo = 1, int32_t f_hi = 0) {
+    // PH 0: the whole solve.  PH 1: forward elimination of positions [f_lo, f_hi) only (f_lo >= 1; the
+    // planes below are already eliminated -- a solve that follows its right-hand side as it is
+    // produced).  PH 2: back substitution only.  The split solve does the same operations in the
+    // same order as PH 0.
     const int64_t lines = outer * inner;
+    if (PH == 0) f_hi = n;
     for (int64_t ln = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ln < lines; ln += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = ln / inner, q = ln - p * inner;
         double *x = arr + p * (int64_t)n * inner + q;
         const int64_t o = p * (int64_t)n * inner + q;
         double cur[U], nxt[U];
-        auto load = [&](double *buf, int i0) {
+        auto load = [&](double *buf, int i0, int lim) {
 #pragma unroll
             for (int k = 0; k < U; k++) {
                 const int i = i0 + k;
-                if (i >= 0 && i < n) buf[k] = x[(int64_t)i * inner];
+                if (i >= 0 && i < lim) buf[k] = x[(int64_t)i * inner];
             }
         };
-        // forward elimination: x_i -= w_i x_{i-1}
-        double prev = x[0];
-        load(cur, 1);
-        for (int i0 = 1; i0 < n; i0 += U) {
-            if (i0 + U < n) load(nxt, i0 + U);
+        double prev;
+        if (PH != 2) {
+            // forward elimination: x_i -= w_i x_{i-1}
+            prev = x[(int64_t)(f_lo - 1) * inner];
+            load(cur, f_lo, f_hi);
+            for (int i0 = f_lo; i0 < f_hi; i0 += U) {
+                if (i0 + U < f_hi) load(nxt, i0 + U, f_hi);
 #pragma unroll
-            for (int k = 0; k < U; k++) {
-                const int i = i0 + k;
-                if (i < n) {
-                    const double v = dsub(cur[k], dmul(__ldg(tw + i), prev));
-                    x[(int64_t)i * inner] = v;
-                    prev = v;
+                for (int k = 0; k < U; k++) {
+                    const int i = i0 + k;
+                    if (i < f_hi) {
+                        const double v = dsub(cur[k], dmul(__ldg(tw + i), prev));
+                        x[(int64_t)i * inner] = v;
+                        prev = v;
+                    }
                 }
-            }
 #pragma unroll
-            for (int k = 0; k < U; k++) cur[k] = nxt[k];
+                for (int k = 0; k < U; k++) cur[k] = nxt[k];
+            }
+        } else {
+            prev = x[(int64_t)(n - 1) * inner];
         }
+        if (PH == 1) continue;
         double last = ddiv(prev, __ldg(tb + n - 1));   // (__ddiv_rn beat a checked fast division here)
         epi_store<EPI>(arr, o + (int64_t)(n - 1) * inner, last, epi);
         // back substitution: x_i = (x_i - u_i x_{i+1}) / b'_i, i = n-2 .. 0
-        load(cur, n - 1 - U);
+        load(cur, n - 1 - U, n);
         for (int i1 = n - 2; i1 >= 0; i1 -= U) {
-            if (i1 - U >= 0) load(nxt, i1 - 2 * U + 1);
+            if (i1 - U >= 0) load(nxt, i1 - 2 * U + 1, n);
 #pragma unroll
             for (int k = U - 1; k >= 0; k--) {
                 const int i = i1 - (U - 1 - k);
@@ -1133,6 +1144,7 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
     };
     issue(0);
     int c_done = 0;
+    const bool fwd = thomas_fwd_stream(p, 0);
     for (int k = 0; k < K; k++) {
         CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(EvChunkIn, k), 0));
         const int64_t a = (int64_t)k * chunk, e = std::min<int64_t>(n0, a + chunk);
@@ -1147,6 +1159,7 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
             if (has_range) fused_pass1_quantize(p, 0, d_in, dtype == 0, q, Z0, b.cg, s, c_done, c_ready);
             else fused_pass1_decompose(p, 0, d_in, dtype == 0, coef, Z0, b.cg, s, c_done, c_ready);
             fused_pass2(p, 0, Z0, b.t0, s, c_done, c_ready);
+            if (fwd) thomas_plane_fwd(p, 0, b.t0, c_done, c_ready, s);   // the solve follows its right-hand side
             c_done = c_ready;
         }
         if (k + 1 < K) issue(k + 1);
@@ -1182,8 +1195,10 @@ const double *decompose_quantize_streamed(hpdr_ctx *ctx, DevPlan &p, const void 
     phase_mark("fine_quantized", s);
     // the rest of transition 0 (IPK + coarse update) and the coarser levels
     {
-        thomas_all(p, 0, b.t0, s, b.cg, level_ptr(b, p, 1));
+        if (fwd) thomas_finish_fwd(p, 0, b.t0, c_done, true, s, b.cg, level_ptr(b, p, 1));
+        else thomas_all(p, 0, b.t0, s, b.cg, level_ptr(b, p, 1));
     }
+    phase_mark("thomas_l0", s);
     const double *DL = coarse_levels_quantize(ctx, p, q, s);
     phase_mark("levels_done", s);
     if (side) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(1), 0));
@@ -1358,6 +1373,55 @@ void thomas_in_planes(const DevPlan &p, int st_i, double *T, int c_lo, int c_hi,
         if (st.ax[a].active) thomas(T0, sub, a, st.ax[a], s);
 }
 
+bool thomas_fwd_stream(const DevPlan &p, int st_i) {
+    static const bool off = getenv("HPDR_NO_FWD_STREAM") != nullptr;
+    const DevStep &st = p.steps[st_i];
+    return !off && p.dims.n[0] == 1 && !st.ax[0].active && st.ax[1].active && st.csh.size() > kThomasSmallMax;
+}
+
+void thomas_plane_fwd(const DevPlan &p, int st_i, double *T, int c_lo, int c_hi, cudaStream_t s) {
+    const DevStep &st = p.steps[st_i];
+    const DevAxis &ax = st.ax[1];
+    const int lo = std::max(c_lo, 1);
+    c_hi = std::min(c_hi, (int)ax.nc);
+    if (c_hi <= lo) return;
+    int64_t outer, inner;
+    view(st.csh, 1, outer, inner);
+    const int64_t lines = outer * inner;
+    KPROF("k_thomas_fwd", 8.0 * lines * (c_hi - lo), s);
+    k_thomas_reg<8, false, 1><<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(T, outer, ax.nc, inner, ax.tw, ax.tb, ax.tu,
+                                                                             ax.tr, Epi{}, lo, c_hi);
+    LAUNCH_CHECK();
+}
+
+void thomas_finish_fwd(const DevPlan &p, int st_i, double *T, int f_done, bool in_planes, cudaStream_t s,
+                       const double *add_base, double *add_dst) {
+    const DevStep &st = p.steps[st_i];
+    const DevAxis &ax = st.ax[1];
+    thomas_plane_fwd(p, st_i, T, f_done, ax.nc, s);
+    int last = 1;
+    if (in_planes)
+        for (int a = 2; a < 4; a++)
+            if (st.ax[a].active) last = a;
+    Epi epi;
+    epi.base = add_base;
+    epi.dst = add_dst;
+    int64_t outer, inner;
+    view(st.csh, 1, outer, inner);
+    const int64_t lines = outer * inner;
+    KPROF("k_thomas_bwd", (last == 1 && add_dst ? 16.0 : 8.0) * lines * ax.nc, s);
+    if (last == 1 && add_dst)
+        k_thomas_reg<8, true, 2><<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(T, outer, ax.nc, inner, ax.tw, ax.tb,
+                                                                                ax.tu, ax.tr, epi);
+    else
+        k_thomas_reg<8, false, 2><<<grid_for(lines, 128, 148 * 64), 128, 0, s>>>(T, outer, ax.nc, inner, ax.tw, ax.tb,
+                                                                                 ax.tu, ax.tr, Epi{});
+    LAUNCH_CHECK();
+    if (in_planes)
+        for (int a = 2; a < 4; a++)
+            if (st.ax[a].active) thomas(T, st.csh, a, st.ax[a], s, a == last ? epi : Epi{});
+}
+
 void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, int out_dtype, cudaStream_t s,
                     void *host_out, const double *T0_pre, cudaEvent_t ev_pre, bool t0_plane_axis_only,
                     const double *T1_pre, cudaEvent_t ev1_pre) {
@@ -1428,11 +1492,14 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
         double *tarena = (double *)ctx->dbuf("t0c", std::max<int64_t>(tc, 1) * 8);
         // event ids: 199 / 200 + level (distinct from the streamed decode's and the slab loop's)
         CUDA_CHECK(cudaEventRecord(ctx->event(199), s));   // coef ready
+        // side[0] still carries the streamed decode's level-1 solve when T1_pre is set: the coarser
+        // levels (the head of the chain) go round-robin on the other three side streams
+        const int k0 = T1_pre ? 1 : 0, nk = 4 - k0;
         int k = 0;
         for (int st_i = top - 1; st_i >= 1; st_i--, k++) {
             if (st_i == 1 && T1_pre) continue;   // computed by the caller (streamed decode)
-            cudaStream_t x = ctx->side[k % 4];
-            if (k < 4) CUDA_CHECK(cudaStreamWaitEvent(x, ctx->event(199), 0));
+            cudaStream_t x = ctx->side[k0 + k % nk];
+            if (k < nk) CUDA_CHECK(cudaStreamWaitEvent(x, ctx->event(199), 0));
             double *Zl = zarena, *T = tarena;
             zarena += (z0_elems(p, st_i) + 31) & ~int64_t(31);
             tarena += (p.steps[st_i].csh.size() + 31) & ~int64_t(31);
@@ -1445,6 +1512,15 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
         }
     }
     if (tiny >= 1) tiny_recompose(p, tiny, coef, level_ptr(b, p, tiny), s);
+    phase_mark("tiny", s);
+    static const char *kLvlMark[8] = {"final0", "final1", "final2", "final3", "final4", "final5", "final6", "final7"};
+    // Host output in slabs: transition 1's final pass (the level-1 grid the finest slabs interpolate
+    // from) is cut into plane ranges too, each launched just ahead of the first slab that reads it,
+    // so the first D2H does not wait for the whole level-1 grid.
+    static const bool no_defer1 = getenv("HPDR_NO_DEFER_L1") != nullptr;
+    const bool defer1 = !no_defer1 && direct && host_out && top >= 2 && p.dims.n[0] == 1 &&
+                        p.host.steps[0].ax[1].active;
+    const double *Dc1 = nullptr, *T1s = nullptr;
     for (int st_i = top - 1; st_i >= 0; st_i--) {
         const DevStep &st = p.steps[st_i];
         double *Dc = level_ptr(b, p, st_i + 1);
@@ -1455,6 +1531,7 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
         } else if (st_i == 1 && T1_pre) {
             T = T1_pre;
             CUDA_CHECK(cudaStreamWaitEvent(s, ev1_pre, 0));
+            phase_mark("t1_ready", s);
         } else if (Tl[st_i]) {
             T = Tl[st_i];
             CUDA_CHECK(cudaStreamWaitEvent(s, ctx->event(EvLevel, ev_l[st_i]), 0));
@@ -1464,6 +1541,11 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
             thomas_all(p, st_i, b.t0, s);
         }
         // coarse - corr is formed inside the final level kernel as it reads the coarse values
+        if (st_i == 1 && defer1) {   // transition 1's output follows the finest slabs (slab loop below)
+            Dc1 = Dc;
+            T1s = T;
+            continue;
+        }
         if (st_i == 0) phase_mark("coarse_levels_done", s);
         if (st_i == 0 && direct && host_out) {
             // finest level in dim-0 slabs; each slab's D2H (copy stream) overlaps the next slab
@@ -1479,11 +1561,20 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
             const bool pageable_out = classify(host_out) == MemKind::Host;
             int nslab = 0;
             int c_done = 0;   // coarse planes whose in-plane solves are done (t0_plane_axis_only)
+            int c1_done = 0;  // level-1 planes written (defer1)
+            const int nc0 = (int)st.csh.n[1];
             for (int a = 0, k = 0; a < n0; a += chunk, k++, nslab++) {
                 const int e = std::min(n0, a + chunk);
-                if (t0_plane_axis_only) {   // the coarse planes this slab's fine planes read
-                    const AxisTables &h0 = p.host.steps[0].ax[1];
-                    const int c_need = (e >= n0) ? (int)st.csh.n[1] : std::max(h0.pa[e - 1], h0.pb[e - 1]) + 1;
+                const AxisTables &h0 = p.host.steps[0].ax[1];
+                // the coarse planes this slab's fine planes read
+                const int c_need = (e >= n0 || !h0.active) ? nc0 : std::max(h0.pa[e - 1], h0.pb[e - 1]) + 1;
+                if (defer1 && c_need > c1_done) {
+                    const int c1 = std::min(nc0, (c_need + 1) & ~1);
+                    fused_final(p, 1, Dc1, coef, Dc, 1, s, c1_done, c1, T1s);
+                    c1_done = c1;
+                    if (k == 0) phase_mark("final1_first", s);
+                }
+                if (t0_plane_axis_only) {
                     thomas_in_planes(p, 0, const_cast<double *>(T), c_done, c_need, s);
                     c_done = std::max(c_done, c_need);
                 }
@@ -1509,6 +1600,7 @@ void recompose_into(hpdr_ctx *ctx, DevPlan &p, const double *coef, void *out, in
             fused_final(p, st_i, Dc, coef, out, out_dtype, s, 0, -1, T);
         } else {
             fused_final(p, st_i, Dc, coef, level_ptr(b, p, st_i), 1, s, 0, -1, T);
+            if (st_i < 8) phase_mark(kLvlMark[st_i], s);
         }
     }
     if (!direct) cast_output(b.lvl0, out, out_dtype, p.n_total, s);

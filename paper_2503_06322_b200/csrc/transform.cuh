@@ -64,6 +64,15 @@ bool thomas_plane_split(const DevPlan &p, int st_i);
 // The plane-axis sweep / the in-plane sweeps of coarse planes [c_lo, c_hi) (thomas_plane_split).
 void thomas_plane_axis(const DevPlan &p, int st_i, double *T, cudaStream_t s);
 void thomas_in_planes(const DevPlan &p, int st_i, double *T, int c_lo, int c_hi, cudaStream_t s);
+// Plane-axis forward elimination that follows the right-hand side as its coarse planes are
+// produced (same rank / axis conditions as thomas_plane_split; env HPDR_NO_FWD_STREAM disables):
+// thomas_plane_fwd eliminates coarse planes [c_lo, c_hi) given the planes below are done, and
+// thomas_finish_fwd completes the solve -- the planes from f_done on, back substitution, then (when
+// in_planes) the in-plane axes, `add_base` + x into `add_dst` on the last sweep as thomas_all does.
+bool thomas_fwd_stream(const DevPlan &p, int st_i);
+void thomas_plane_fwd(const DevPlan &p, int st_i, double *T, int c_lo, int c_hi, cudaStream_t s);
+void thomas_finish_fwd(const DevPlan &p, int st_i, double *T, int f_done, bool in_planes, cudaStream_t s,
+                       const double *add_base = nullptr, double *add_dst = nullptr);
 // Elements of pass 1's output Z0 at transition st_i.
 int64_t z0_elems(const DevPlan &p, int st_i);
 // Thomas solves of every active axis of transition st_i's coarse grid, in place.

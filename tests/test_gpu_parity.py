@@ -202,7 +202,8 @@ from oracle import oracle as O
 from paper_2503_06322_b200 import synthetic as S
 import torch
 cases = [((33, 34, 35), np.float32), ((16, 5, 7), np.float32), ((65, 40), np.float32), ((1000,), np.float32),
-         ((12, 10, 9), np.float32), ((40, 36, 64), np.float32), ((67, 20, 34), np.float64), ((9, 48, 16), np.float64)]
+         ((12, 10, 9), np.float32), ((40, 36, 64), np.float32), ((67, 20, 34), np.float64), ((9, 48, 16), np.float64),
+         ((70, 66, 90), np.float32)]   # (last: coarse grid above the one-block solve; streamed plane-axis solve)
 for shape, dt in cases:
     a = S.smooth_noise(shape, seed=3, dtype=dt)
     for vr in (None, (-1.0, 2.0)):
@@ -222,14 +223,16 @@ print("variant ok")
                                  {"HPDR_NO_PLANE_SPLIT": "1"}, {"HPDR_NO_QUAD_FINAL": "1"}, {"HPDR_NO_QUAD_P1R": "1"},
                                  {"HPDR_NO_STREAM_L1": "1", "HPDR_STREAM_DECODE_MIN_BITS": "0"},
                                  {"HPDR_STREAM_DECODE_MIN_BITS": "0"}, {"HPDR_QF_COLUMNS": "1"}, {"HPDR_P2_ONE_COL": "1"},
-                                 {"HPDR_THOMAS_TILE": "1"}, {}])
+                                 {"HPDR_THOMAS_TILE": "1"}, {"HPDR_NO_FWD_STREAM": "1"}, {"HPDR_NO_DEFER_L1": "1"},
+                                 {"HPDR_STREAM_DECODE_MIN_BITS": "0", "HPDR_DEC_GROUPS": "32"}, {}])
 def test_execution_variants_bit_identical(env):
     """Every execution variant gives the reference's blobs: the per-axis (generic) path, the non-streamed
     fused path, pass 1 without quads, the quad kernel without TMA, forced slab splits (down to two coarse
     planes per slab), the shared-memory tile Thomas solve at every size, and the small end of the
     hierarchy as per-level launches instead of the one-block kernel (tiny.cu), and the finest
     correction solved whole before the output slabs instead of plane range by plane range, and the
-    final level with one node per thread instead of quads."""
+    final level with one node per thread instead of quads, and the finest plane-axis solve run whole
+    after the last chunk instead of following its right-hand side."""
     import subprocess
     import sys
 
