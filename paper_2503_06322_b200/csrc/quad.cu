@@ -352,7 +352,9 @@ __global__ void __launch_bounds__(kQThreads, TMA ? 4 : 3)
                     for (int k = 0; k < 4; k++) {
                         const double qa = dmul(mc[k], rbin);
                         const double r = rint(qa);
-                        const bool ok = (0.5 - fabs(dsub(qa, r))) > fabs(qa) * 0x1p-49 && fabs(r) < (double)q.half;
+                        // |r| < half bounds |qa| < 2^15: the fixed 2^-33 margin is stricter than quant_key's
+                        // |qa| * 2^-49 (one multiply fewer; near-half quotients take the exact path)
+                        const bool ok = (0.5 - fabs(dsub(qa, r))) > 0x1p-33 && fabs(r) < (double)q.half;
                         const int ri = (int)r;
                         const uint32_t key = ((uint32_t)ri << 1) ^ (uint32_t)(ri >> 31);
                         const bool fk = (fine >> k) & 1u;
