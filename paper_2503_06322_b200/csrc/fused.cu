@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(256) k_quantize_fine_rows(const double *__rest
                 const uint32_t key = ((uint32_t)ri << 1) ^ (uint32_t)(ri >> 31);
                 // |r| < half <= 32767.5 bounds |qa| < 2^15, so a fixed 2^-33 margin is stricter than
                 // quant_key's |qa| * 2^-49 (one multiply fewer; the rare miss takes the exact path)
-                const bool ok = (0.5 - fabs(dsub(qa, r))) > 0x1p-33 && fabs(r) < half;
+                const bool ok = fabs(dsub(qa, r)) < 0.5 - 0x1p-33 && fabs(r) < half;   // (qa - r is exact)
                 if (use[k] && ok) {
                     kr[c0 + 32 * k] = (uint16_t)key;
                     if (sh_ok) atomicAdd(&sh_hist[key], 1u);

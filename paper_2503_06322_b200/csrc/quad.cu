@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kQThreads, TMA ? 4 : 3)
                         const double r = rint(qa);
                         // |r| < half bounds |qa| < 2^15: the fixed 2^-33 margin is stricter than quant_key's
                         // |qa| * 2^-49 (one multiply fewer; near-half quotients take the exact path)
-                        const bool ok = (0.5 - fabs(dsub(qa, r))) > 0x1p-33 && fabs(r) < (double)q.half;
+                        const bool ok = fabs(dsub(qa, r)) < 0.5 - 0x1p-33 && fabs(r) < (double)q.half;   // (qa - r is exact)
                         const int ri = (int)r;
                         const uint32_t key = ((uint32_t)ri << 1) ^ (uint32_t)(ri >> 31);
                         const bool fk = (fine >> k) & 1u;
