@@ -793,10 +793,11 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                         levels_of(dims) == (int)levels && (dtype == 0 || dtype == 1) && pp->host.L > 2 &&
                         use_fused(*pp) && classify(blob_in) != MemKind::Device && hh.n_units >= 64 &&
                         hh.total_bits >= (uint64_t)min_stream_bits && n_out <= N / 64;
-        static const int G = [] {
-            const char *e = getenv("HPDR_DEC_GROUPS");
-            return e ? std::max(1, std::min(32, atoi(e))) : 16;   // 6 / 10 / 16 at 1024^3: 104.8 / 104.3 / 103.9 ms
-        }();
+        // payload groups of >= 12 MB, 4..16 (decode launches of fewer units lose more than the
+        // earlier start gains): 513^3 (106 MB) 8 groups 12.57 vs 12.97 ms with 16; 1024^3 16
+        static const int G_env = getenv("HPDR_DEC_GROUPS") ? std::max(1, std::min(32, atoi(getenv("HPDR_DEC_GROUPS")))) : 0;
+        const int G = G_env ? G_env
+                            : (int)std::max<uint64_t>(4, std::min<uint64_t>(16, ((hh.total_bits + 7) / 8) / (12ull << 20)));
         // Pinned blob: the first payload group goes out before the host-side checks below (~1 ms at
         // 1024^3), into the buffer decode_begin will hand out (same name and size); it stops short
         // of the zero-padded tail decode_begin clears on the compute stream.
