@@ -899,6 +899,8 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                 return c;
             };
             int c1_done = 0;
+            const bool fwd1 = lvl1 && thomas_fwd_stream(p, 1);
+            int f1 = 0;   // coarse planes of T1f whose forward elimination is done
             auto oidx_at = [&](uint64_t k) {
                 uint64_t i;
                 memcpy(&i, oidx_h + k, 8);
@@ -977,6 +979,10 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                         CUDA_CHECK(cudaStreamWaitEvent(ctx->side[0], ctx->event(EvDecCorr, g), 0));
                         fused_pass1_recompose(p, 1, coef, Z1f, ctx->side[0], c1_done, c1_ready);
                         fused_pass2(p, 1, Z1f, T1f, ctx->side[0], c1_done, c1_ready);
+                        if (fwd1) {   // transition 1's plane-axis solve follows too
+                            thomas_plane_fwd(p, 1, T1f, c1_done, c1_ready, ctx->side[0]);
+                            f1 = c1_ready;
+                        }
                         c1_done = c1_ready;
                     }
                 }
@@ -999,6 +1005,7 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                     fused_pass1_recompose(p, 1, coef, Z1f, ctx->side[0]);
                     fused_pass2(p, 1, Z1f, T1f, ctx->side[0]);
                     c1_done = m1;
+                    f1 = 0;
                 }
             }
             phase_mark("dec_end", s);
@@ -1018,7 +1025,8 @@ void decompress_core(hpdr_ctx *ctx, const void *blob_in, uint64_t len, const uin
                     fused_pass1_recompose(p, 1, coef, Z1f, ctx->side[0], c1_done, m1);
                     fused_pass2(p, 1, Z1f, T1f, ctx->side[0], c1_done, m1);
                 }
-                thomas_all(p, 1, T1f, ctx->side[0]);
+                if (fwd1) thomas_finish_fwd(p, 1, T1f, f1, true, ctx->side[0]);
+                else thomas_all(p, 1, T1f, ctx->side[0]);
                 ev1_pre = ctx->event(193);
                 CUDA_CHECK(cudaEventRecord(ev1_pre, ctx->side[0]));
                 T1_pre = T1f;
