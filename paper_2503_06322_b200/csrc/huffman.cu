@@ -267,6 +267,20 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const uint16_t *__restri
     }
 }
 
+// The words k_encode merges with atomicOr -- each unit's first and last word -- are cleared; every
+// other word of the stream is written whole by exactly one unit (no full-buffer memset).
+__global__ void k_zero_unit_bounds(const uint64_t *__restrict__ uoff, const uint64_t *__restrict__ ubits,
+                                   uint32_t *__restrict__ out, int64_t units) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < units; u += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = ubits[u];
+        if (b) {
+            const uint64_t g = uoff[u];
+            out[g >> 5] = 0;
+            out[(g + b - 1) >> 5] = 0;
+        }
+    }
+}
+
 }  // namespace
 
 void encode_device(hpdr_ctx *ctx, const uint16_t *keys, int64_t n, uint32_t dict_size, const uint8_t *lengths,
@@ -316,7 +330,16 @@ void encode_device(hpdr_ctx *ctx, const uint16_t *keys, int64_t n, uint32_t dict
     const size_t words = (size_t)((res.total_bits + 31) / 32) + 2;
     res.d_words = (uint32_t *)ctx->dbuf(ctx->oname("enc_words"), words * 4);
     res.d_offsets = uoff;
-    zero_async(res.d_words, words * 4, s);
+    {
+        static const bool full_zero = getenv("HPDR_ENC_FULL_ZERO") != nullptr;
+        if (full_zero) {
+            zero_async(res.d_words, words * 4, s);
+        } else {
+            KPROF("k_zero_unit_bounds", 24.0 * units, s);
+            k_zero_unit_bounds<<<grid_for(units, 256, 148 * 4), 256, 0, s>>>(uoff, ubits, res.d_words, units);
+            LAUNCH_CHECK();
+        }
+    }
     if (hooks && hooks->ready) hooks->ready(res);
     const uint64_t pbytes = (res.total_bits + 7) / 8;
     for (int g = 0; g < G; g++) {
